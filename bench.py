@@ -1,0 +1,323 @@
+#!/usr/bin/env python
+"""SPH step benchmark (BASELINE.json metric): particle-steps/s and interactions/s of the full
+NL -> PI -> SU step on B200, with the reference CPU path timed beside it.
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl b200|reference] [--config c3]
+
+One JSON line on rank 0.  A "step" is one whole NL -> PI -> SU pass over the resident
+synthetic dam break (state already in HBM; the state (~2 GB at C3) is far larger than the
+126 MB L2, so no flush is needed between steps).  Timing: CUDA events on the launching
+stream, barrier + synchronize on both sides, max over ranks.  See DESIGN.md §Measurement.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "particle-steps/sec and interactions/sec at 1/2/4/8 B200 vs host-CPU ref; % HBM roofline"
+UNIT = "particle-steps/s"
+FLOP_PER_CAND, FLOP_PER_EVAL = 9, 70  # SURVEY.md §8(d) algorithmic units
+BYTES_NL_SU = 324 - 52                # compulsory NL+SU bytes per particle-step
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default=None, help="c1|c2|c3|c4_1..c4_8 (default c3 at N=1, c4_N above)")
+    ap.add_argument("--n-subdiv", type=int, default=1)
+    ap.add_argument("--precision", default="fp32", choices=["fp32", "fp64"])
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget-s", type=float, default=20.0)
+    return ap.parse_args()
+
+
+def peaks():
+    hbm = None
+    try:
+        hbm = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]
+        hbm_src = "MEASURED_PEAKS.json"
+    except Exception:
+        hbm, hbm_src = 6650.0, "fallback B200_PROFILING.md"
+    fp32, fp32_src = 69.41, "profiles/peaks_r01.json (FFMA microbenchmark, tools/peaks.cu)"
+    try:
+        fp32 = json.load(open(os.path.join(ROOT, "profiles", "peaks_r01.json")))["fp32_tflops"]
+    except Exception:
+        pass
+    return hbm, hbm_src, fp32, fp32_src
+
+
+def workload(name, n_subdiv):
+    import paper_1110_3711_b200 as sph
+    sc = sph.named_scenario(name)
+    prm = sph.make_params(sc, n_subdiv=n_subdiv)
+    return sc, prm, sph.build_dam_break(sc, prm)
+
+
+# ---------------------------------------------------------------- clocks
+class Clocks:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.proc = None
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                          "-lms", "200", "-i", str(index)], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        out, _ = self.proc.communicate(timeout=10)
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for k, nm in enumerate(names):
+                if f[5 + k].lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------- CPU reference (oracle port)
+def cpu_reference(system, prm, n_subdiv, budget_s, repeats=1):
+    """Time the reference algorithm's CPU restatement (oracle/: numpy NL/SU, C OpenMP gather,
+    bit-exact to the reference) on this host.  PI runs on a contiguous block of fluid targets
+    sized to ``budget_s`` and is scaled to the whole fluid list; NL and SU run in full."""
+    import oracle
+    cores = len(os.sched_getaffinity(0))
+    variant = "slowcellsh" if n_subdiv == 1 else "slowcellshalf"
+    n, nb = system.n, system.count_boundary
+    times = []
+    for _ in range(repeats):
+        t0 = time.perf_counter()
+        cell, dims, _ = oracle.assign_cells(system.pos, prm)
+        perm = oracle.sort_perm(cell, nb)
+        pos, vel, rho = system.pos[perm], system.vel[perm], system.rho[perm]
+        cs = cell[perm]
+        cidx = oracle.cell_index(cs, nb, int(np.prod(dims)))
+        t_nl = time.perf_counter() - t0
+        # PI probe to size the sample
+        probe = min(20000, n - nb)
+        t1 = time.perf_counter()
+        oracle.gather(pos, vel, rho, nb, system.mass_fluid, system.mass_boundary, cs, dims, cidx,
+                      prm, variant=variant, nthreads=cores, items=(nb, nb + probe))
+        t_probe = time.perf_counter() - t1
+        per_item = t_probe / max(probe, 1)
+        m = int(min(n - nb, max(probe, budget_s / max(per_item, 1e-12))))
+        t2 = time.perf_counter()
+        out = oracle.gather(pos, vel, rho, nb, system.mass_fluid, system.mass_boundary, cs, dims,
+                            cidx, prm, variant=variant, nthreads=cores, items=(nb, nb + m))
+        t_pi_sample = time.perf_counter() - t2
+        t_pi = t_pi_sample * (n / m)  # boundary items cost about as much per item as fluid ones
+        # SU on the full arrays (accel from the sample rows, zeros elsewhere: same work)
+        t3 = time.perf_counter()
+        press, csound, _, _ = oracle.derived(rho, prm)
+        dt = oracle.compute_dt(out["accel"], out["visc_dt"], csound, nb, prm)
+        oracle.verlet_update(0, pos, vel, rho, vel, rho, out["accel"], out["drho_dt"], nb, prm,
+                             max(dt, prm.dt_min))
+        t_su = time.perf_counter() - t3
+        times.append((t_nl, t_pi, t_su, m))
+    t_nl, t_pi, t_su, m = min(times, key=lambda t: t[0] + t[1] + t[2])
+    step_s = t_nl + t_pi + t_su
+    return dict(value=n / step_s, unit=UNIT, cores=cores, kind="port",
+                sample=f"one {variant} step of this workload on {cores} threads: full NL+SU "
+                       f"(numpy), PI (oracle C, OpenMP) on {m:,} of {n - nb:,} fluid targets "
+                       f"scaled to all {n:,} items; stage s NL {t_nl:.2f} PI {t_pi:.2f} SU {t_su:.2f}",
+                step_s=step_s)
+
+
+def run_reference(args, cfg_name):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    sc, prm, system = workload(cfg_name, args.n_subdiv)
+    for _ in range(args.warmup):
+        cpu_reference(system, prm, args.n_subdiv, budget_s=2.0)
+    t = [cpu_reference(system, prm, args.n_subdiv, budget_s=2.0) for _ in range(args.steps)]
+    step_s = float(np.mean([x["step_s"] for x in t]))
+    value = system.n / step_s
+    cb = dict(t[-1])
+    cb["value"] = value
+    cb.pop("step_s", None)
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_s * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic dam break (reference Scenario/build_dam_break lattice)",
+            "config": {"workload": cfg_name, "particles": system.n, "n_subdiv": args.n_subdiv},
+            "cpu_baseline": cb,
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------- B200 arm
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    cfg_name = args.config or ("c3" if args.gpus == 1 else f"c4_{args.gpus}")
+    if args.impl == "reference":
+        run_reference(args, cfg_name)
+        return
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_1110_3711_b200 as sph
+    from paper_1110_3711_b200 import _lib
+    from paper_1110_3711_b200.device import DeviceSim
+
+    sc, prm, system = workload(cfg_name, args.n_subdiv)
+    variant = "slowcellsh" if args.n_subdiv == 1 else "slowcellshalf"
+    prec = _lib.SPHB_FP64 if args.precision == "fp64" else _lib.SPHB_FP32
+    sim = DeviceSim(system, prm, reach=args.n_subdiv, precision=prec,
+                    record_capacity=max(64, args.warmup + args.steps + 8))
+    Ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+    for _ in range(args.warmup):
+        sim.launch_step()
+    torch.cuda.synchronize()
+    first = int(sim.ctrl_host()["step"])
+    if world > 1:
+        dist.barrier()
+    clocks = Clocks(local)
+    ev = [[Ev() for _ in range(4)] for _ in range(args.steps)]
+    t0, t1 = Ev(), Ev()
+    torch.cuda.synchronize()
+    t0.record()
+    for k in range(args.steps):
+        sim.launch_step(events=ev[k])
+    t1.record()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    total_ms = t0.elapsed_time(t1)
+    if world > 1:
+        tt = torch.tensor([total_ms], device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        total_ms = float(tt.item())
+    err = sim.error()
+    if err is not None:
+        raise RuntimeError(f"divergence during bench: {err}")
+    recs = sim.records(first, first + args.steps)
+    nl_ms = [e[0].elapsed_time(e[1]) for e in ev]
+    pi_ms = [e[1].elapsed_time(e[2]) for e in ev]
+    su_ms = [e[2].elapsed_time(e[3]) for e in ev]
+    cand = float(np.mean(recs["candidate_pairs"].astype(np.float64)))
+    evals = float(np.mean(recs["force_evals"].astype(np.float64)))
+    true_pairs = float(np.mean(recs["hits_ordered"].astype(np.float64))) / 2
+    ms_step = total_ms / args.steps
+    n_all = system.n * world
+    value = n_all * args.steps / (total_ms * 1e-3)
+    hbm, hbm_src, fp32, fp32_src = peaks()
+    pi_mean = float(np.mean(pi_ms))
+    flops = FLOP_PER_CAND * cand + FLOP_PER_EVAL * evals
+    achieved = flops / (pi_mean * 1e-3) / 1e12
+    nl_su_ms = float(np.mean(nl_ms) + np.mean(su_ms))
+    nlsu_gbs = BYTES_NL_SU * system.n / (nl_su_ms * 1e-3) / 1e9
+
+    # ---- e2e: the same step through the C ABI with HOST buffers (H2D state in, D2H state out)
+    h2d = d2h = 0
+    e2e_value = None
+    if args.e2e_steps > 0:
+        n = sim.n
+        hosts = [torch.empty((n, 4), dtype=torch.float32, pin_memory=True) for _ in range(3)]
+        hid = torch.empty(n, dtype=torch.int64, pin_memory=True)
+        for hbuf, dbuf in zip(hosts, (sim.posp, sim.velr, sim.prev)):
+            hbuf.copy_(dbuf[:n])
+        hid.copy_(sim.id[:n])
+        dev_bufs = (sim.posp, sim.velr, sim.prev)
+        h2d = d2h = sum(h.numel() * h.element_size() for h in hosts) + hid.numel() * 8
+        torch.cuda.synchronize()
+        a, b = Ev(), Ev()
+        a.record()
+        for _ in range(args.e2e_steps):
+            for hbuf, dbuf in zip(hosts, dev_bufs):
+                dbuf[:n].copy_(hbuf, non_blocking=True)
+            sim.id[:n].copy_(hid, non_blocking=True)
+            sim.first_keys_resync()
+            sim.launch_step()
+            for hbuf, dbuf in zip(hosts, dev_bufs):
+                hbuf.copy_(dbuf[:n], non_blocking=True)
+            hid.copy_(sim.id[:n], non_blocking=True)
+        b.record()
+        torch.cuda.synchronize()
+        e2e_ms = a.elapsed_time(b)
+        if world > 1:
+            tt = torch.tensor([e2e_ms], device="cuda")
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            e2e_ms = float(tt.item())
+        e2e_value = n_all * args.e2e_steps / (e2e_ms * 1e-3)
+
+    launches = sim.launches_per_step() * args.steps
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+        "scaling": "weak" if world > 1 else "weak", "vs_baseline": None, "dtype": args.precision,
+        "data": "synthetic: reference dam-break lattice (Scenario/build_dam_break), hydrostatic rho",
+        "config": {"workload": f"{cfg_name}: 3-D dam break, {system.n:,} particles per GPU "
+                               f"({system.count_fluid:,} fluid + {system.count_boundary:,} boundary)",
+                   "particles_per_gpu": system.n, "n_subdiv": args.n_subdiv, "variant": variant,
+                   "l2": "inputs larger than L2 (resident state ~%.1f GB)" % (sim.n * 184 / 1e9),
+                   "parallelism": f"{world} GPU" + (" replicas" if world > 1 else "")},
+        "interactions_per_s": true_pairs * world * args.steps / (total_ms * 1e-3),
+        "pair_evals_per_s": evals * world * args.steps / (total_ms * 1e-3),
+        "stage_ms": {"nl": float(np.mean(nl_ms)), "pi": pi_mean, "su": float(np.mean(su_ms))},
+        "counters_per_step": {"candidates": cand, "force_evals": evals, "true_pairs": true_pairs},
+        "roofline": {"bound": "fp32", "kernel": "k_interact (fluid + boundary launches)",
+                     "achieved": achieved, "peak": fp32, "unit": "TFLOP/s",
+                     "frac": achieved / fp32, "traffic": None,
+                     "work": f"{FLOP_PER_CAND}*candidates + {FLOP_PER_EVAL}*evals per launch",
+                     "peak_source": fp32_src},
+        "roofline_hbm_nl_su": {"bound": "hbm", "achieved": nlsu_gbs, "peak": hbm, "unit": "GB/s",
+                               "frac": nlsu_gbs / hbm, "traffic": None,
+                               "work": f"{BYTES_NL_SU} B/particle-step over NL+SU stages",
+                               "peak_source": hbm_src},
+        "gpu_launches": launches,
+        "clocks": clk,
+    }
+    if e2e_value is not None:
+        line["e2e"] = {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
+                       "d2h_bytes_per_step": d2h, "steps": args.e2e_steps,
+                       "path": "per step: pinned host state -> H2D -> sphb_* step -> D2H state"}
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cb = cpu_reference(system, prm, args.n_subdiv, args.cpu_budget_s)
+        cb.pop("step_s", None)
+        line["cpu_baseline"] = cb
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,204 @@
+/*
+ * sphb200.h -- C ABI of libsphb200.so, the B200 (sm_100a) SPH step hot path.
+ *
+ * Drop-in boundary for the reference's step loop (arXiv 1110.3711 re-implementation
+ * "sphbench", /root/reference/pkg/src/sphbench).  The reference's plug-in interface is
+ * a Python protocol (make_engine(cfg).compute(...), run_simulation(...)); the Python
+ * package paper_1110_3711_b200 mirrors that protocol and calls the entry points below
+ * through ctypes.  Each entry point names the reference function(s) it replaces.
+ *
+ * Conventions
+ *   - every array argument is a DEVICE pointer owned by the caller (torch tensors);
+ *   - every call is stream-ordered on the caller's cudaStream_t, never synchronises,
+ *     never allocates after sphb_workspace_create (CUDA-graph capturable);
+ *   - return value 0 = SPHB_OK, negative = SPHB_E_*; sphb_last_error() gives a
+ *     thread-local message; no C++ exception crosses the ABI;
+ *   - physics failures (the reference's DivergenceError, sim.py:22-29, 310-333) are
+ *     recorded on the device in sphb_ctrl_t.err (see SPHB_DIV_*) and read by the host
+ *     when it chooses to (no per-step host sync).
+ *
+ * Particle state layout in HBM (structure of float4 arrays, one 16-B load per field):
+ *   posp  float4 (x, y, z, press)        press = Tait EOS of rho, f32-rounded (physics.py:119-121)
+ *   velr  float4 (vx, vy, vz, rho)
+ *   prev  float4 (vx_prev, vy_prev, vz_prev, rho_prev)   Verlet history (sim.py:31-43)
+ *   aux   float4 (prrho, csound, tensil, 0)               derived (physics.py:124-134)
+ *   id    int64
+ * Boundary particles occupy [0, nb), fluid [nb, n) (model.py:24-32).
+ */
+#ifndef SPHB200_H
+#define SPHB200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* sphb_stream_t; /* == cudaStream_t */
+
+enum {
+  SPHB_OK = 0,
+  SPHB_E_INVALID = -1,  /* contract violation -> ValueError in the shim */
+  SPHB_E_CUDA = -2,     /* CUDA runtime error */
+  SPHB_E_CAPACITY = -3, /* n / ncells above the workspace capacity */
+};
+
+/* Device-side divergence codes; ordered as the reference checks them inside one step:
+ * out-of-domain at step start (sim.py:309-314), non-finite forces (328-329), non-finite
+ * state (332-333). */
+enum {
+  SPHB_DIV_LEFT_DOMAIN = 1,
+  SPHB_DIV_NONFINITE_FORCES = 2,
+  SPHB_DIV_NONFINITE_STATE = 3,
+};
+
+enum { SPHB_FP32 = 0, SPHB_FP64 = 1 };
+
+/* Grid descriptor; cell_size and dims are computed on the host in f64 exactly as
+ * grid.py:81-84 / model.py:131-135 do. */
+typedef struct {
+  double origin[3];     /* params.domain_min */
+  double domain_max[3]; /* params.domain_max */
+  double cell_size;     /* 2h / n_subdiv */
+  int32_t dims[3];      /* max(ceil(extent/cs - 1e-12), 1) */
+  int32_t reach;        /* candidate rows per side: gather slowcellsh 1, *half 2 */
+} sphb_grid_t;
+
+/* Physics constants.  The first twelve are physics.pack_params (physics.py:149-180). */
+typedef struct {
+  double sup2, h, invh, kc, eta2, alpha, invwdp, c0, rho0, gamma, mass_fluid, mass_boundary;
+  double tait_b;                 /* c0^2 rho0 / gamma (model.py:141-143) */
+  double g[3];                   /* gravity, applied once per particle (sim.py:223, 245) */
+  double cfl, dt_min, dt_max;    /* compute_dt (sim.py:215-232) */
+  int32_t verlet_stride;         /* corrector every k steps (sim.py:242) */
+  int32_t order;                 /* 0: per row F then B (gather_*_cells, kernels.py:326-418)
+                                    1: all F rows then all B rows (gather_fluid_ranges 421-497) */
+  int32_t precision;             /* SPHB_FP32 (production) | SPHB_FP64 (bit-exact to reference) */
+  int32_t pad_;
+} sphb_params_t;
+
+/* Device-resident control block (one per simulation, caller allocates 256 B). */
+typedef struct {
+  int64_t step;          /* index of the step about to run / running */
+  int64_t max_steps;     /* run_simulation stop rule (sim.py:302-303); <0 = none */
+  double t_sim;          /* simulated time so far */
+  double t_end;          /* sim.py:304-305; +inf = none */
+  double dt;             /* dt of the last completed step */
+  uint64_t dtmin_f;      /* ordered bits of min_fluid sqrt(h/|a+g|) of the running step */
+  uint64_t dtmin_cv;     /* ordered bits of min_all h/(cs+visc_dt) */
+  uint64_t err;          /* (step << 40) | (code << 32) | first offending index; ~0 = none */
+  uint64_t counters[4];  /* running step: candidates, ordered hits, evals, ff evals */
+  int32_t active;        /* 1 while no error and no stop rule fired */
+  int32_t pad_[15];
+} sphb_ctrl_t;
+
+/* Per-step record written at the end of every step (StepStats, model.py:176-212). */
+typedef struct {
+  double dt;
+  uint64_t candidate_pairs, hits_ordered, force_evals, ff_force_evals;
+} sphb_step_record_t;
+
+typedef struct sphb_workspace sphb_workspace_t;
+
+const char* sphb_last_error(void);
+const char* sphb_version(void);
+
+/* Allocates every internal scratch buffer (radix ping-pong, histograms, scan partials)
+ * for up to n_max particles and ncells_max cells.  The only allocating call. */
+int sphb_workspace_create(int64_t n_max, int64_t ncells_max, sphb_workspace_t** ws);
+int sphb_workspace_destroy(sphb_workspace_t* ws);
+/* Zeroes the workspace histogram (needed only after an aborted step). */
+int sphb_workspace_reset(sphb_workspace_t* ws, sphb_stream_t s);
+/* Bytes of device memory the workspace holds. */
+int64_t sphb_workspace_bytes(const sphb_workspace_t* ws);
+
+/* Control block reset: step=0, t_sim=0, err=none, active=1, stop rules as given. */
+int sphb_ctrl_init(sphb_ctrl_t* ctrl, int64_t max_steps, double t_end, sphb_stream_t s);
+
+/* K1 -- assign_cells (grid.py:77-93): f64-exact cell id per particle, -1 outside.
+ * keys_out[i] = (is_fluid << cellbits) | cell (sort key); cell_out[i] = cell or -1;
+ * first out-of-domain index recorded in ctrl->err as SPHB_DIV_LEFT_DOMAIN at ctrl->step;
+ * per-list per-cell histogram accumulated into the workspace for sphb_cell_ranges. */
+int sphb_cell_keys(sphb_workspace_t* ws, const sphb_grid_t* grid, const void* posp, int64_t n,
+                   int64_t nb, uint32_t* keys_out, int32_t* cell_out, sphb_ctrl_t* ctrl,
+                   sphb_stream_t s);
+
+/* K2 -- the stable per-list argsort of reorder (grid.py:96-109): LSD radix sort of keys.
+ * perm_out[new] = old (grid.sort_perm, grid.py:116); keys_sorted_out optional (may be NULL). */
+int sphb_sort(sphb_workspace_t* ws, const sphb_grid_t* grid, const uint32_t* keys, int64_t n,
+              uint32_t* keys_sorted_out, int32_t* perm_out, const sphb_ctrl_t* ctrl,
+              sphb_stream_t s);
+
+/* K3 -- reorder gathers (grid.py:111-114) fused with compute_derived (physics.py:96-110):
+ * *_out[i] = *_in[perm[i]] for posp, velr, prev, id; posp_out.w = press; aux_out derived;
+ * cell_out[i] = cell of the sorted key.  prev_in/prev_out/id may be NULL. */
+int sphb_reorder(const sphb_params_t* prm, const sphb_grid_t* grid, int64_t n,
+                 const int32_t* perm, const uint32_t* keys_sorted, const void* posp_in,
+                 const void* velr_in, const void* prev_in, const int64_t* id_in, void* posp_out,
+                 void* velr_out, void* prev_out, int64_t* id_out, void* aux_out,
+                 int32_t* cell_out, const sphb_ctrl_t* ctrl, sphb_stream_t s);
+
+/* K4 -- build_cell_index (grid.py:123-144): warp-level exclusive scan of the per-list
+ * histogram from sphb_cell_keys.  beg/end hold 2*ncells int32: [0,ncells) boundary list,
+ * [ncells, 2*ncells) fluid list already offset by nb; empty cells carry the running prefix.
+ * Re-zeroes the histogram for the next step. */
+int sphb_cell_ranges(sphb_workspace_t* ws, const sphb_grid_t* grid, int32_t* beg, int32_t* end,
+                     const sphb_ctrl_t* ctrl, sphb_stream_t s);
+
+/* Same table from an already sorted cell array (no histogram needed), for frames whose NL
+ * ran elsewhere (engine.compute parity mode). cell_sorted[i] in [0, ncells). */
+int sphb_cell_ranges_from_sorted(sphb_workspace_t* ws, const sphb_grid_t* grid,
+                                 const int32_t* cell_sorted, int64_t n, int64_t nb, int32_t* beg,
+                                 int32_t* end, sphb_stream_t s);
+
+/* K5/K5b/K6 -- GatherEngine.compute (engines/gather.py:42-110): fused fluid pass
+ * (gather_fluid_cells / _ranges, kernels.py:326-497) and boundary pass (gather_boundary_*,
+ * kernels.py:500-596), plus the compute_dt reductions (sim.py:215-232) in the epilogue.
+ * acc: (n,3) f64 (boundary rows 0), drho: (n) f64, visc: (n) f64 (ForceOutput, config.py:94-103).
+ * Raw counters and the two dt minima accumulate into ctrl. */
+int sphb_interact(const sphb_params_t* prm, const sphb_grid_t* grid, int64_t n, int64_t nb,
+                  const void* posp, const void* velr, const void* aux, const int32_t* cell_sorted,
+                  const int32_t* beg, const int32_t* end, double* acc, double* drho, double* visc,
+                  sphb_ctrl_t* ctrl, sphb_stream_t s);
+
+/* Resets the per-step accumulators (dt minima, counters) and evaluates the stop rules. */
+int sphb_step_begin(sphb_ctrl_t* ctrl, sphb_stream_t s);
+
+/* K7 -- compute_dt finalize + verlet_update (sim.py:215-259) fused with the next step's
+ * assign_cells (K1) and its histogram; writes the integrated state back into the primary
+ * (unsorted-for-next-step) arrays.  Flags non-finite state / out-of-domain in ctrl. */
+int sphb_integrate(sphb_workspace_t* ws, const sphb_params_t* prm, const sphb_grid_t* grid,
+                   int64_t n, int64_t nb, const void* posp_s, const void* velr_s,
+                   const void* prev_s, const int64_t* id_s, const double* acc, const double* drho,
+                   void* posp, void* velr, void* prev, int64_t* id, uint32_t* keys_next,
+                   sphb_ctrl_t* ctrl, sphb_stream_t s);
+
+/* Closes the step: dt/counters into rec[step % rec_capacity], t_sim += dt, step += 1. */
+int sphb_step_end(sphb_ctrl_t* ctrl, const sphb_params_t* prm, sphb_step_record_t* rec,
+                  int64_t rec_capacity, sphb_stream_t s);
+
+/* One whole NL -> PI -> SU step on resident state (the run_simulation loop body,
+ * sim.py:306-351).  Composes the calls above; graph-capturable. */
+typedef struct {
+  void *posp, *velr, *prev;      /* primary state (this step's pre-sort order) */
+  int64_t* id;
+  void *posp_s, *velr_s, *prev_s, *aux; /* sorted copies */
+  int64_t* id_s;
+  uint32_t *keys, *keys_sorted;
+  int32_t *perm, *cell_s, *beg, *end;
+  double *acc, *drho, *visc;
+} sphb_state_t;
+
+int sphb_step(sphb_workspace_t* ws, const sphb_params_t* prm, const sphb_grid_t* grid, int64_t n,
+              int64_t nb, const sphb_state_t* st, sphb_ctrl_t* ctrl, sphb_step_record_t* rec,
+              int64_t rec_capacity, sphb_stream_t s);
+
+/* Number of this library's kernel launches one sphb_step issues (for the bench's
+ * gpu_launches claim). */
+int64_t sphb_step_launch_count(const sphb_grid_t* grid, int64_t n);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPHB200_H */

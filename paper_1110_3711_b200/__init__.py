@@ -1,0 +1,24 @@
+"""paper_1110_3711_b200 -- B200-native SPH step hot path (arXiv 1110.3711).
+
+Drop-in for the reference package's step API (sphbench/__init__.py:5-18):
+``EngineConfig``, ``ForceOutput``, ``make_engine``, the model types, ``Scenario``,
+``build_dam_break``, ``make_params`` and ``run_simulation`` -- with every NL/PI/SU FLOP
+executed by hand-written sm_100a kernels in libsphb200.so (csrc/, include/sphb200.h).
+There is no CPU fallback: without the CUDA library and a GPU the compute entry points
+raise.
+"""
+from .config import EngineConfig, ForceOutput
+from .engine import B200Engine, compute_forces_cellpairs, compute_forces_gather, make_engine
+from .model import (DerivedQuantities, ParticleKind, ParticleSystem, SimParams, StepStats,
+                    validate)
+from .scenario import Scenario, build_dam_break, make_params, named_scenario
+from .sim import DivergenceError, compute_derived, run_simulation
+
+__version__ = "0.1.0"
+
+__all__ = [
+    "EngineConfig", "ForceOutput", "make_engine", "B200Engine", "compute_forces_gather",
+    "compute_forces_cellpairs", "DerivedQuantities", "ParticleKind", "ParticleSystem",
+    "SimParams", "StepStats", "validate", "Scenario", "build_dam_break", "make_params",
+    "named_scenario", "run_simulation", "DivergenceError", "compute_derived", "__version__",
+]

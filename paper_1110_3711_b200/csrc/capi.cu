@@ -1,0 +1,289 @@
+// capi.cu -- extern "C" entry points of libsphb200.so (see include/sphb200.h).
+//
+// Thin: argument checks, workspace management, error strings; the kernels live in
+// nl.cu / interact.cu / integrate.cu.  No C++ exception crosses the ABI.
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <new>
+
+#include "sphb_common.cuh"
+#include "sphb_internal.h"
+
+static thread_local char g_err[512] = "";
+
+int sphb_set_error(int code, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return code;
+}
+
+int sphb_check_launch(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess)
+    return sphb_set_error(SPHB_E_CUDA, "%s: %s", what, cudaGetErrorString(e));
+  return SPHB_OK;
+}
+
+#define SPHB_CUDA(call)                                                                   \
+  do {                                                                                    \
+    cudaError_t e_ = (call);                                                              \
+    if (e_ != cudaSuccess)                                                                \
+      return sphb_set_error(SPHB_E_CUDA, "%s: %s", #call, cudaGetErrorString(e_));        \
+  } while (0)
+
+#define SPHB_NONNULL(p)                                                                  \
+  do {                                                                                   \
+    if (!(p)) return sphb_set_error(SPHB_E_INVALID, "%s: null pointer %s", __func__, #p); \
+  } while (0)
+
+static int check_grid(const sphb_grid_t* g) {
+  SPHB_NONNULL(g);
+  for (int k = 0; k < 3; ++k)
+    if (g->dims[k] < 1) return sphb_set_error(SPHB_E_INVALID, "grid dims must be >= 1");
+  if (!(g->cell_size > 0)) return sphb_set_error(SPHB_E_INVALID, "cell_size must be positive");
+  if (sphb::ncells_of(*g) >= (int64_t(1) << 30))
+    return sphb_set_error(SPHB_E_INVALID, "ncells >= 2^30 unsupported (31-bit sort keys)");
+  return SPHB_OK;
+}
+
+extern "C" {
+
+const char* sphb_last_error(void) { return g_err; }
+const char* sphb_version(void) { return "sphb200 0.1 (sm_100a)"; }
+
+int sphb_workspace_create(int64_t n_max, int64_t ncells_max, sphb_workspace_t** out) {
+  SPHB_NONNULL(out);
+  if (n_max < 0 || ncells_max < 1) return sphb_set_error(SPHB_E_INVALID, "bad capacities");
+  if (n_max >= (int64_t(1) << 31)) return sphb_set_error(SPHB_E_INVALID, "n_max >= 2^31");
+  sphb_workspace* ws = new (std::nothrow) sphb_workspace();
+  if (!ws) return sphb_set_error(SPHB_E_INVALID, "host allocation failed");
+  ws->n_max = n_max;
+  ws->ncells_max = ncells_max;
+  const int64_t n1 = n_max > 0 ? n_max : 1;
+  ws->max_sort_tiles = (n1 + SORT_TILE - 1) / SORT_TILE;
+  ws->max_scan_tiles = (2 * ncells_max + SCAN_TILE - 1) / SCAN_TILE;
+  size_t bytes = 0;
+  auto alloc = [&](void** p, size_t b) -> cudaError_t {
+    bytes += b;
+    return cudaMalloc(p, b);
+  };
+  cudaError_t e = cudaSuccess;
+  if (e == cudaSuccess) e = alloc((void**)&ws->cnt, sizeof(uint32_t) * 2 * ncells_max);
+  for (int k = 0; k < 2 && e == cudaSuccess; ++k) {
+    e = alloc((void**)&ws->keys_tmp[k], sizeof(uint32_t) * n1);
+    if (e == cudaSuccess) e = alloc((void**)&ws->vals_tmp[k], sizeof(int32_t) * n1);
+  }
+  if (e == cudaSuccess)
+    e = alloc((void**)&ws->radix_hist, sizeof(uint32_t) * RADIX * ws->max_sort_tiles);
+  if (e == cudaSuccess) e = alloc((void**)&ws->digit_total, sizeof(uint32_t) * RADIX);
+  if (e == cudaSuccess)
+    e = alloc((void**)&ws->scan_partials, sizeof(uint32_t) * (ws->max_scan_tiles + 1));
+  if (e == cudaSuccess) e = cudaMemset(ws->cnt, 0, sizeof(uint32_t) * 2 * ncells_max);
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  ws->bytes = bytes;
+  if (e != cudaSuccess) {
+    sphb_workspace_destroy(ws);
+    return sphb_set_error(SPHB_E_CUDA, "workspace allocation: %s", cudaGetErrorString(e));
+  }
+  *out = ws;
+  return SPHB_OK;
+}
+
+int sphb_workspace_destroy(sphb_workspace_t* ws) {
+  if (!ws) return SPHB_OK;
+  cudaFree(ws->cnt);
+  for (int k = 0; k < 2; ++k) {
+    cudaFree(ws->keys_tmp[k]);
+    cudaFree(ws->vals_tmp[k]);
+  }
+  cudaFree(ws->radix_hist);
+  cudaFree(ws->digit_total);
+  cudaFree(ws->scan_partials);
+  delete ws;
+  return SPHB_OK;
+}
+
+int sphb_workspace_reset(sphb_workspace_t* ws, sphb_stream_t s) {
+  SPHB_NONNULL(ws);
+  SPHB_CUDA(cudaMemsetAsync(ws->cnt, 0, sizeof(uint32_t) * 2 * ws->ncells_max, (cudaStream_t)s));
+  return SPHB_OK;
+}
+
+int64_t sphb_workspace_bytes(const sphb_workspace_t* ws) { return ws ? (int64_t)ws->bytes : 0; }
+
+int sphb_ctrl_init(sphb_ctrl_t* ctrl, int64_t max_steps, double t_end, sphb_stream_t s) {
+  SPHB_NONNULL(ctrl);
+  return launch_ctrl_init(ctrl, max_steps, t_end, (cudaStream_t)s);
+}
+
+int sphb_cell_keys(sphb_workspace_t* ws, const sphb_grid_t* grid, const void* posp, int64_t n,
+                   int64_t nb, uint32_t* keys_out, int32_t* cell_out, sphb_ctrl_t* ctrl,
+                   sphb_stream_t s) {
+  SPHB_NONNULL(ws);
+  SPHB_NONNULL(ctrl);
+  if (int rc = check_grid(grid)) return rc;
+  if (n < 0 || nb < 0 || nb > n) return sphb_set_error(SPHB_E_INVALID, "bad n/nb");
+  if (n > 0) {
+    SPHB_NONNULL(posp);
+    SPHB_NONNULL(keys_out);
+  }
+  return launch_cell_keys(ws, *grid, (const float4*)posp, n, nb, keys_out, cell_out, ctrl,
+                          (cudaStream_t)s);
+}
+
+int sphb_sort(sphb_workspace_t* ws, const sphb_grid_t* grid, const uint32_t* keys, int64_t n,
+              uint32_t* keys_sorted_out, int32_t* perm_out, const sphb_ctrl_t* ctrl,
+              sphb_stream_t s) {
+  SPHB_NONNULL(ws);
+  SPHB_NONNULL(ctrl);
+  if (int rc = check_grid(grid)) return rc;
+  if (n > 0) {
+    SPHB_NONNULL(keys);
+    SPHB_NONNULL(perm_out);
+  }
+  return launch_sort(ws, *grid, keys, n, keys_sorted_out, perm_out, ctrl, (cudaStream_t)s);
+}
+
+int sphb_reorder(const sphb_params_t* prm, const sphb_grid_t* grid, int64_t n,
+                 const int32_t* perm, const uint32_t* keys_sorted, const void* posp_in,
+                 const void* velr_in, const void* prev_in, const int64_t* id_in, void* posp_out,
+                 void* velr_out, void* prev_out, int64_t* id_out, void* aux_out,
+                 int32_t* cell_out, const sphb_ctrl_t* ctrl, sphb_stream_t s) {
+  SPHB_NONNULL(prm);
+  SPHB_NONNULL(ctrl);
+  if (int rc = check_grid(grid)) return rc;
+  if (n > 0) {
+    SPHB_NONNULL(posp_in);
+    SPHB_NONNULL(velr_in);
+    SPHB_NONNULL(posp_out);
+    SPHB_NONNULL(velr_out);
+    SPHB_NONNULL(aux_out);
+  }
+  return launch_reorder(*prm, *grid, n, perm, keys_sorted, (const float4*)posp_in,
+                        (const float4*)velr_in, (const float4*)prev_in, id_in, (float4*)posp_out,
+                        (float4*)velr_out, (float4*)prev_out, id_out, (float4*)aux_out, cell_out,
+                        ctrl, (cudaStream_t)s);
+}
+
+int sphb_cell_ranges(sphb_workspace_t* ws, const sphb_grid_t* grid, int32_t* beg, int32_t* end,
+                     const sphb_ctrl_t* ctrl, sphb_stream_t s) {
+  SPHB_NONNULL(ws);
+  SPHB_NONNULL(beg);
+  SPHB_NONNULL(end);
+  if (int rc = check_grid(grid)) return rc;
+  return launch_cell_ranges(ws, *grid, beg, end, ctrl, (cudaStream_t)s);
+}
+
+int sphb_cell_ranges_from_sorted(sphb_workspace_t* ws, const sphb_grid_t* grid,
+                                 const int32_t* cell_sorted, int64_t n, int64_t nb, int32_t* beg,
+                                 int32_t* end, sphb_stream_t s) {
+  SPHB_NONNULL(ws);
+  SPHB_NONNULL(beg);
+  SPHB_NONNULL(end);
+  if (int rc = check_grid(grid)) return rc;
+  if (n < 0 || nb < 0 || nb > n) return sphb_set_error(SPHB_E_INVALID, "bad n/nb");
+  if (int rc = sphb_workspace_reset(ws, s)) return rc;
+  if (n > 0) {
+    SPHB_NONNULL(cell_sorted);
+    if (int rc = launch_hist_from_sorted(ws, *grid, cell_sorted, n, nb, (cudaStream_t)s)) return rc;
+  }
+  return launch_cell_ranges(ws, *grid, beg, end, nullptr, (cudaStream_t)s);
+}
+
+int sphb_interact(const sphb_params_t* prm, const sphb_grid_t* grid, int64_t n, int64_t nb,
+                  const void* posp, const void* velr, const void* aux, const int32_t* cell_sorted,
+                  const int32_t* beg, const int32_t* end, double* acc, double* drho, double* visc,
+                  sphb_ctrl_t* ctrl, sphb_stream_t s) {
+  SPHB_NONNULL(prm);
+  SPHB_NONNULL(ctrl);
+  if (int rc = check_grid(grid)) return rc;
+  if (n < 0 || nb < 0 || nb > n) return sphb_set_error(SPHB_E_INVALID, "bad n/nb");
+  if (prm->precision != SPHB_FP32 && prm->precision != SPHB_FP64)
+    return sphb_set_error(SPHB_E_INVALID, "precision must be SPHB_FP32 or SPHB_FP64");
+  if (n == 0) return SPHB_OK;
+  SPHB_NONNULL(posp);
+  SPHB_NONNULL(velr);
+  SPHB_NONNULL(aux);
+  SPHB_NONNULL(cell_sorted);
+  SPHB_NONNULL(beg);
+  SPHB_NONNULL(end);
+  SPHB_NONNULL(acc);
+  SPHB_NONNULL(drho);
+  SPHB_NONNULL(visc);
+  return launch_interact(*prm, *grid, n, nb, (const float4*)posp, (const float4*)velr,
+                         (const float4*)aux, cell_sorted, beg, end, acc, drho, visc, ctrl,
+                         (cudaStream_t)s);
+}
+
+int sphb_step_begin(sphb_ctrl_t* ctrl, sphb_stream_t s) {
+  SPHB_NONNULL(ctrl);
+  return launch_step_begin(ctrl, (cudaStream_t)s);
+}
+
+int sphb_integrate(sphb_workspace_t* ws, const sphb_params_t* prm, const sphb_grid_t* grid,
+                   int64_t n, int64_t nb, const void* posp_s, const void* velr_s,
+                   const void* prev_s, const int64_t* id_s, const double* acc, const double* drho,
+                   void* posp, void* velr, void* prev, int64_t* id, uint32_t* keys_next,
+                   sphb_ctrl_t* ctrl, sphb_stream_t s) {
+  SPHB_NONNULL(ws);
+  SPHB_NONNULL(prm);
+  SPHB_NONNULL(ctrl);
+  if (int rc = check_grid(grid)) return rc;
+  if (n < 0 || nb < 0 || nb > n) return sphb_set_error(SPHB_E_INVALID, "bad n/nb");
+  if (n > 0) {
+    SPHB_NONNULL(posp_s); SPHB_NONNULL(velr_s); SPHB_NONNULL(prev_s); SPHB_NONNULL(id_s);
+    SPHB_NONNULL(acc); SPHB_NONNULL(drho); SPHB_NONNULL(posp); SPHB_NONNULL(velr);
+    SPHB_NONNULL(prev); SPHB_NONNULL(id); SPHB_NONNULL(keys_next);
+  }
+  return launch_integrate(ws, *prm, *grid, n, nb, (const float4*)posp_s, (const float4*)velr_s,
+                          (const float4*)prev_s, id_s, acc, drho, (float4*)posp, (float4*)velr,
+                          (float4*)prev, id, keys_next, ctrl, (cudaStream_t)s);
+}
+
+int sphb_step_end(sphb_ctrl_t* ctrl, const sphb_params_t* prm, sphb_step_record_t* rec,
+                  int64_t rec_capacity, sphb_stream_t s) {
+  SPHB_NONNULL(ctrl);
+  SPHB_NONNULL(prm);
+  return launch_step_end(ctrl, *prm, rec, rec_capacity, (cudaStream_t)s);
+}
+
+int sphb_step(sphb_workspace_t* ws, const sphb_params_t* prm, const sphb_grid_t* grid, int64_t n,
+              int64_t nb, const sphb_state_t* st, sphb_ctrl_t* ctrl, sphb_step_record_t* rec,
+              int64_t rec_capacity, sphb_stream_t s) {
+  SPHB_NONNULL(ws);
+  SPHB_NONNULL(prm);
+  SPHB_NONNULL(st);
+  SPHB_NONNULL(ctrl);
+  if (int rc = check_grid(grid)) return rc;
+  cudaStream_t cs = (cudaStream_t)s;
+  int rc;
+  if ((rc = launch_step_begin(ctrl, cs))) return rc;
+  if ((rc = launch_sort(ws, *grid, st->keys, n, st->keys_sorted, st->perm, ctrl, cs))) return rc;
+  if ((rc = launch_reorder(*prm, *grid, n, st->perm, st->keys_sorted, (const float4*)st->posp,
+                           (const float4*)st->velr, (const float4*)st->prev, st->id,
+                           (float4*)st->posp_s, (float4*)st->velr_s, (float4*)st->prev_s, st->id_s,
+                           (float4*)st->aux, st->cell_s, ctrl, cs)))
+    return rc;
+  if ((rc = launch_cell_ranges(ws, *grid, st->beg, st->end, ctrl, cs))) return rc;
+  if ((rc = launch_interact(*prm, *grid, n, nb, (const float4*)st->posp_s,
+                            (const float4*)st->velr_s, (const float4*)st->aux, st->cell_s, st->beg,
+                            st->end, st->acc, st->drho, st->visc, ctrl, cs)))
+    return rc;
+  if ((rc = launch_integrate(ws, *prm, *grid, n, nb, (const float4*)st->posp_s,
+                             (const float4*)st->velr_s, (const float4*)st->prev_s, st->id_s,
+                             st->acc, st->drho, (float4*)st->posp, (float4*)st->velr,
+                             (float4*)st->prev, st->id, st->keys, ctrl, cs)))
+    return rc;
+  return launch_step_end(ctrl, *prm, rec, rec_capacity, cs);
+}
+
+int64_t sphb_step_launch_count(const sphb_grid_t* grid, int64_t n) {
+  if (!grid) return 0;
+  return 1 /*begin*/ + nl_launch_count(*grid, n) + interact_launch_count(n) + 1 /*integrate*/ +
+         1 /*end*/;
+}
+
+}  // extern "C"

@@ -1,0 +1,175 @@
+// integrate.cu -- system update (SU) of the SPH step on sm_100a.
+//
+//   k_step_begin   stop rules of run_simulation (sim.py:302-305), per-step accumulators reset
+//   K7 k_integrate compute_dt finalize (sim.py:231-232) + verlet_update (sim.py:235-259),
+//                  fused with the NEXT step's assign_cells (grid.py:77-93, K1) and its
+//                  per-list histogram; non-finite state / out-of-domain detection
+//                  (sim.py:309-314, 332-333) recorded on the device
+//   k_step_end     StepStats record (dt, counters), t_sim += dt, step += 1 (sim.py:336-351)
+//
+// All f64 arithmetic uses round-to-nearest intrinsics in the reference's numpy evaluation
+// order, so the update is bit-identical to the reference for identical forces.
+#include "sphb_common.cuh"
+#include "sphb_internal.h"
+
+using namespace sphb;
+
+namespace {
+
+__device__ __forceinline__ bool step_live(const sphb_ctrl_t* c) {
+  return c->active && c->err >= ((uint64_t)(c->step + 1) << 40);
+}
+
+__device__ __forceinline__ double step_dt(const sphb_ctrl_t* c, const sphb_params_t& p) {
+  const double dt_f = __longlong_as_double((long long)c->dtmin_f);
+  const double dt_cv = __longlong_as_double((long long)c->dtmin_cv);
+  double dt = xmul(p.cfl, fmin(dt_f, dt_cv));
+  dt = fmax(dt, p.dt_min);
+  return fmin(dt, p.dt_max);
+}
+
+__global__ void k_ctrl_init(sphb_ctrl_t* c, int64_t max_steps, double t_end) {
+  c->step = 0;
+  c->max_steps = max_steps;
+  c->t_sim = 0.0;
+  c->t_end = t_end;
+  c->dt = 0.0;
+  c->dtmin_f = (uint64_t)__double_as_longlong(INFINITY);
+  c->dtmin_cv = (uint64_t)__double_as_longlong(INFINITY);
+  c->err = ~0ull;
+  for (int k = 0; k < 4; ++k) c->counters[k] = 0;
+  c->active = 1;
+}
+
+__global__ void k_step_begin(sphb_ctrl_t* c) {
+  if (!step_live(c)) return;
+  if ((c->max_steps >= 0 && c->step >= c->max_steps) || (c->t_sim >= c->t_end)) {
+    c->active = 0;
+    return;
+  }
+  c->dtmin_f = (uint64_t)__double_as_longlong(INFINITY);
+  c->dtmin_cv = (uint64_t)__double_as_longlong(INFINITY);
+  for (int k = 0; k < 4; ++k) c->counters[k] = 0;
+}
+
+__global__ void __launch_bounds__(256) k_integrate(
+    sphb_params_t p, sphb_grid_t g, int cellbits, int64_t ncells, int64_t n, int64_t nb,
+    const float4* __restrict__ posp_s, const float4* __restrict__ velr_s,
+    const float4* __restrict__ prev_s, const int64_t* __restrict__ id_s,
+    const double* __restrict__ acc, const double* __restrict__ drho, float4* __restrict__ posp,
+    float4* __restrict__ velr, float4* __restrict__ prev, int64_t* __restrict__ id,
+    uint32_t* __restrict__ keys_next, uint32_t* __restrict__ cnt, sphb_ctrl_t* ctrl) {
+  if (!step_live(ctrl)) return;
+  const int64_t step = ctrl->step;
+  const double dt = step_dt(ctrl, p);
+  const bool corrector = (step % p.verlet_stride) == 0;
+  const double c2 = xmul(xmul(0.5, dt), dt);
+  const double dt2 = xmul(2.0, dt);
+  const int lane = threadIdx.x & 31;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n; base += stride) {
+    const int64_t i = base + threadIdx.x;
+    int64_t slot = -1;
+    if (i < n) {
+      const float4 ps = posp_s[i], vs = velr_s[i], pv = prev_s[i];
+      const double dr = drho[i];
+      float4 np, nv;
+      double nrho;
+      if (corrector)
+        nrho = xadd((double)vs.w, xmul(dt, dr));
+      else
+        nrho = xadd((double)pv.w, xmul(dt2, dr));
+      if (i >= nb) {
+        const double ax = xadd(acc[3 * i + 0], p.g[0]);
+        const double ay = xadd(acc[3 * i + 1], p.g[1]);
+        const double az = xadd(acc[3 * i + 2], p.g[2]);
+        const double vx = (double)vs.x, vy = (double)vs.y, vz = (double)vs.z;
+        np.x = __double2float_rn(xadd(xadd((double)ps.x, xmul(dt, vx)), xmul(c2, ax)));
+        np.y = __double2float_rn(xadd(xadd((double)ps.y, xmul(dt, vy)), xmul(c2, ay)));
+        np.z = __double2float_rn(xadd(xadd((double)ps.z, xmul(dt, vz)), xmul(c2, az)));
+        if (corrector) {
+          nv.x = __double2float_rn(xadd(vx, xmul(dt, ax)));
+          nv.y = __double2float_rn(xadd(vy, xmul(dt, ay)));
+          nv.z = __double2float_rn(xadd(vz, xmul(dt, az)));
+        } else {
+          nv.x = __double2float_rn(xadd((double)pv.x, xmul(dt2, ax)));
+          nv.y = __double2float_rn(xadd((double)pv.y, xmul(dt2, ay)));
+          nv.z = __double2float_rn(xadd((double)pv.z, xmul(dt2, az)));
+        }
+      } else {
+        np.x = ps.x; np.y = ps.y; np.z = ps.z;  // boundary frozen (sim.py:256-258)
+        nv.x = vs.x; nv.y = vs.y; nv.z = vs.z;
+      }
+      np.w = 0.f;  // press is recomputed by the next step's reorder (K3)
+      nv.w = __double2float_rn(nrho);
+      posp[i] = np;
+      velr[i] = nv;
+      prev[i] = vs;  // history <- current (sim.py:254-255)
+      id[i] = id_s[i];
+      if (!(isfinite(nv.x) && isfinite(nv.y) && isfinite(nv.z) && isfinite(nv.w)))
+        raise_div(ctrl, step, SPHB_DIV_NONFINITE_STATE, 0);
+      // next step's assign_cells (K1), fused
+      const int32_t c = cell_of(np.x, np.y, np.z, g);
+      if (c < 0) {
+        raise_div(ctrl, step + 1, SPHB_DIV_LEFT_DOMAIN, (uint64_t)i);
+        keys_next[i] = 0xffffffffu;
+      } else {
+        const uint32_t list = i >= nb ? 1u : 0u;
+        keys_next[i] = (list << cellbits) | (uint32_t)c;
+        slot = (int64_t)list * ncells + c;
+      }
+    }
+    const uint32_t peers = __match_any_sync(SPHB_FULL, (unsigned long long)slot);
+    if (slot >= 0 && lane == __ffs(peers) - 1) atomicAdd(&cnt[slot], (uint32_t)__popc(peers));
+  }
+}
+
+__global__ void k_step_end(sphb_ctrl_t* c, sphb_params_t p, sphb_step_record_t* rec, int64_t cap) {
+  if (!step_live(c)) return;
+  const double dt = step_dt(c, p);
+  if (rec && cap > 0) {
+    sphb_step_record_t r;
+    r.dt = dt;
+    r.candidate_pairs = c->counters[0];
+    r.hits_ordered = c->counters[1];
+    r.force_evals = c->counters[2];
+    r.ff_force_evals = c->counters[3];
+    rec[c->step % cap] = r;
+  }
+  c->dt = dt;
+  c->t_sim = xadd(c->t_sim, dt);
+  c->step = c->step + 1;
+}
+
+}  // namespace
+
+int launch_ctrl_init(sphb_ctrl_t* ctrl, int64_t max_steps, double t_end, cudaStream_t s) {
+  k_ctrl_init<<<1, 1, 0, s>>>(ctrl, max_steps, t_end);
+  return sphb_check_launch("k_ctrl_init");
+}
+
+int launch_step_begin(sphb_ctrl_t* ctrl, cudaStream_t s) {
+  k_step_begin<<<1, 1, 0, s>>>(ctrl);
+  return sphb_check_launch("k_step_begin");
+}
+
+int launch_integrate(sphb_workspace* ws, const sphb_params_t& p, const sphb_grid_t& g, int64_t n,
+                     int64_t nb, const float4* posp_s, const float4* velr_s, const float4* prev_s,
+                     const int64_t* id_s, const double* acc, const double* drho, float4* posp,
+                     float4* velr, float4* prev, int64_t* id, uint32_t* keys_next,
+                     sphb_ctrl_t* ctrl, cudaStream_t s) {
+  if (n == 0) return SPHB_OK;
+  if (p.verlet_stride < 1) return sphb_set_error(SPHB_E_INVALID, "verlet_corrector_stride must be >= 1");
+  int64_t blocks = (n + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  k_integrate<<<(unsigned)blocks, 256, 0, s>>>(p, g, cellbits_of(g), ncells_of(g), n, nb, posp_s,
+                                               velr_s, prev_s, id_s, acc, drho, posp, velr, prev,
+                                               id, keys_next, ws->cnt, ctrl);
+  return sphb_check_launch("k_integrate");
+}
+
+int launch_step_end(sphb_ctrl_t* ctrl, const sphb_params_t& p, sphb_step_record_t* rec,
+                    int64_t cap, cudaStream_t s) {
+  k_step_end<<<1, 1, 0, s>>>(ctrl, p, rec, cap);
+  return sphb_check_launch("k_step_end");
+}

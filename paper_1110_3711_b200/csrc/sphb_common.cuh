@@ -1,0 +1,115 @@
+// sphb_common.cuh -- shared device helpers for libsphb200 (sm_100a only).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/sphb200.h"
+
+#define SPHB_FULL 0xffffffffu
+
+namespace sphb {
+
+// ---------------------------------------------------------------- exact f64
+// The reference's numba/numpy arithmetic is IEEE binary64 without FMA contraction
+// (SURVEY.md §2.1).  Every f64 expression that must match it bit for bit goes through
+// these round-to-nearest intrinsics, which nvcc never contracts into DFMA.
+__device__ __forceinline__ double xadd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double xsub(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double xmul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double xdiv(double a, double b) { return __ddiv_rn(a, b); }
+
+// ---------------------------------------------------------------- EOS (physics.py:119-134)
+struct Derived {
+  float prrho, csound, tensil;
+};
+
+// eos_press_scalar: f32(tait_b * ((rho/rho0)**gamma - 1.0))
+__device__ __forceinline__ float eos_press(double rho, double tait_b, double rho0, double gamma) {
+  return __double2float_rn(xmul(tait_b, xsub(pow(xdiv(rho, rho0), gamma), 1.0)));
+}
+
+// derive_scalar(press, rho, c0, rho0, gamma)
+__device__ __forceinline__ Derived derive(double press, double rho, double c0, double rho0,
+                                          double gamma) {
+  Derived d;
+  double inv_rho2 = xdiv(1.0, xmul(rho, rho));
+  d.prrho = __double2float_rn(xmul(press, inv_rho2));
+  d.csound = __double2float_rn(xmul(c0, pow(xdiv(rho, rho0), xmul(xsub(gamma, 1.0), 0.5))));
+  if (press > 0.0)
+    d.tensil = __double2float_rn(xmul(xmul(0.01, press), inv_rho2));
+  else
+    d.tensil = __double2float_rn(xmul(xmul(-0.2, press), inv_rho2));
+  return d;
+}
+
+// ---------------------------------------------------------------- cells (grid.py:77-93)
+// Returns the linear cell (x fastest) or -1 when outside [origin, domain_max] (NaN -> -1).
+__device__ __forceinline__ int32_t cell_of(float x, float y, float z, const sphb_grid_t& g) {
+  double p[3] = {(double)x, (double)y, (double)z};
+  int64_t idx[3];
+  bool inside = true;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    inside = inside && (p[k] >= g.origin[k]) && (p[k] <= g.domain_max[k]);
+  }
+  if (!inside) return -1;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    double f = floor(xdiv(xsub(p[k], g.origin[k]), g.cell_size));
+    int64_t v = (int64_t)f;
+    idx[k] = v < (int64_t)g.dims[k] - 1 ? v : (int64_t)g.dims[k] - 1;
+  }
+  return (int32_t)(idx[0] + (int64_t)g.dims[0] * (idx[1] + (int64_t)g.dims[1] * idx[2]));
+}
+
+__host__ __device__ __forceinline__ int64_t ncells_of(const sphb_grid_t& g) {
+  return (int64_t)g.dims[0] * g.dims[1] * g.dims[2];
+}
+
+__host__ __device__ __forceinline__ int cellbits_of(const sphb_grid_t& g) {
+  int64_t nc = ncells_of(g);
+  int b = 1;
+  while ((int64_t(1) << b) < nc) ++b;
+  return b;
+}
+
+// ---------------------------------------------------------------- errors / ctrl
+__device__ __forceinline__ uint64_t err_key(int64_t step, int code, uint64_t index) {
+  return ((uint64_t)step << 40) | ((uint64_t)code << 32) | (index & 0xffffffffull);
+}
+
+__device__ __forceinline__ void raise_div(sphb_ctrl_t* ctrl, int64_t step, int code,
+                                          uint64_t index) {
+  atomicMin((unsigned long long*)&ctrl->err, (unsigned long long)err_key(step, code, index));
+}
+
+// positive doubles (and +inf) order like their bit patterns
+__device__ __forceinline__ void atomic_min_pos(uint64_t* addr, double v) {
+  unsigned long long bits = (unsigned long long)__double_as_longlong(v);
+  unsigned long long cur = *(volatile unsigned long long*)addr;
+  if (bits < cur) atomicMin((unsigned long long*)addr, bits);
+}
+
+__device__ __forceinline__ double warp_min(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmin(v, __shfl_xor_sync(SPHB_FULL, v, o));
+  return v;
+}
+
+__device__ __forceinline__ unsigned long long warp_sum_u64(unsigned long long v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(SPHB_FULL, v, o);
+  return v;
+}
+
+__device__ __forceinline__ uint32_t lanemask_lt() {
+  uint32_t m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+}  // namespace sphb
+
+// host-side error helpers (capi.cu)
+int sphb_set_error(int code, const char* fmt, ...);
+int sphb_check_launch(const char* what);

@@ -1,0 +1,66 @@
+// sphb_internal.h -- workspace layout and kernel launchers shared by the .cu files.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/sphb200.h"
+
+constexpr int SORT_BLOCK = 256;
+constexpr int SORT_ITEMS = 16;
+constexpr int SORT_TILE = SORT_BLOCK * SORT_ITEMS;  // keys per radix tile
+constexpr int RADIX_BITS = 8;
+constexpr int RADIX = 1 << RADIX_BITS;
+constexpr int SCAN_BLOCK = 256;
+constexpr int SCAN_ITEMS = 4;
+constexpr int SCAN_TILE = SCAN_BLOCK * SCAN_ITEMS;
+
+struct sphb_workspace {
+  int64_t n_max = 0, ncells_max = 0;
+  uint32_t* cnt = nullptr;          // 2*ncells_max per-list histogram, kept zero between steps
+  uint32_t* keys_tmp[2] = {nullptr, nullptr};
+  int32_t* vals_tmp[2] = {nullptr, nullptr};
+  uint32_t* radix_hist = nullptr;   // RADIX * max tiles
+  uint32_t* digit_total = nullptr;  // RADIX
+  uint32_t* scan_partials = nullptr;
+  int64_t max_sort_tiles = 0, max_scan_tiles = 0;
+  size_t bytes = 0;
+};
+
+// nl.cu
+int launch_cell_keys(sphb_workspace* ws, const sphb_grid_t& g, const float4* posp, int64_t n,
+                     int64_t nb, uint32_t* keys, int32_t* cell_out, sphb_ctrl_t* ctrl,
+                     cudaStream_t s);
+int launch_sort(sphb_workspace* ws, const sphb_grid_t& g, const uint32_t* keys, int64_t n,
+                uint32_t* keys_sorted, int32_t* perm, const sphb_ctrl_t* ctrl, cudaStream_t s);
+int launch_reorder(const sphb_params_t& p, const sphb_grid_t& g, int64_t n, const int32_t* perm,
+                   const uint32_t* keys_sorted, const float4* posp_in, const float4* velr_in,
+                   const float4* prev_in, const int64_t* id_in, float4* posp_out,
+                   float4* velr_out, float4* prev_out, int64_t* id_out, float4* aux_out,
+                   int32_t* cell_out, const sphb_ctrl_t* ctrl, cudaStream_t s);
+int launch_cell_ranges(sphb_workspace* ws, const sphb_grid_t& g, int32_t* beg, int32_t* end,
+                       const sphb_ctrl_t* ctrl, cudaStream_t s);
+int launch_hist_from_sorted(sphb_workspace* ws, const sphb_grid_t& g, const int32_t* cell_sorted,
+                            int64_t n, int64_t nb, cudaStream_t s);
+int sort_pass_count(const sphb_grid_t& g);
+int64_t nl_launch_count(const sphb_grid_t& g, int64_t n);
+
+// interact.cu
+int launch_interact(const sphb_params_t& p, const sphb_grid_t& g, int64_t n, int64_t nb,
+                    const float4* posp, const float4* velr, const float4* aux,
+                    const int32_t* cell_sorted, const int32_t* beg, const int32_t* end,
+                    double* acc, double* drho, double* visc, sphb_ctrl_t* ctrl, cudaStream_t s);
+int64_t interact_launch_count(int64_t n);
+
+// integrate.cu
+int launch_step_begin(sphb_ctrl_t* ctrl, cudaStream_t s);
+int launch_integrate(sphb_workspace* ws, const sphb_params_t& p, const sphb_grid_t& g, int64_t n,
+                     int64_t nb, const float4* posp_s, const float4* velr_s, const float4* prev_s,
+                     const int64_t* id_s, const double* acc, const double* drho, float4* posp,
+                     float4* velr, float4* prev, int64_t* id, uint32_t* keys_next,
+                     sphb_ctrl_t* ctrl, cudaStream_t s);
+int launch_step_end(sphb_ctrl_t* ctrl, const sphb_params_t& p, sphb_step_record_t* rec, int64_t cap,
+                    cudaStream_t s);
+int launch_ctrl_init(sphb_ctrl_t* ctrl, int64_t max_steps, double t_end, cudaStream_t s);
+
+int sphb_set_error(int code, const char* fmt, ...);
+int sphb_check_launch(const char* what);

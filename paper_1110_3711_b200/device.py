@@ -1,0 +1,322 @@
+"""Device-resident SPH state and the step driver over libsphb200's C ABI.
+
+PyTorch provides device memory, streams and CUDA graphs (plumbing); every FLOP of the
+NL -> PI -> SU step runs in this package's own sm_100a kernels (csrc/).  Layout in HBM:
+structure of float4 arrays (see include/sphb200.h); primary arrays hold the state in the
+previous step's sorted order, *_s arrays the current step's sorted copies.
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+
+import numpy as np
+import torch
+
+from . import _lib
+from .physics import grid_desc, grid_dims, params_desc
+
+F4 = 4
+
+
+def _ptr(t) -> int:
+    return t.data_ptr() if t is not None else 0
+
+
+def cellbits_of(ncells: int) -> int:
+    """Sort-key cell bits (sphb_common.cuh cellbits_of)."""
+    b = 1
+    while (1 << b) < ncells:
+        b += 1
+    return b
+
+
+def _stream() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def require_cuda():
+    if not torch.cuda.is_available():
+        raise _lib.SphbError("paper_1110_3711_b200 needs a CUDA device (B200); no CPU fallback")
+    _lib.lib()
+
+
+class Workspace:
+    """RAII wrapper of sphb_workspace_t (the only allocating C call)."""
+
+    def __init__(self, n_max: int, ncells_max: int):
+        self._h = ctypes.c_void_p()
+        _lib.check(_lib.lib().sphb_workspace_create(int(n_max), int(ncells_max), ctypes.byref(self._h)),
+                   "sphb_workspace_create")
+        self.n_max, self.ncells_max = int(n_max), int(ncells_max)
+
+    @property
+    def handle(self):
+        return self._h
+
+    def bytes(self) -> int:
+        return int(_lib.lib().sphb_workspace_bytes(self._h))
+
+    def reset(self):
+        _lib.check(_lib.lib().sphb_workspace_reset(self._h, _stream()), "sphb_workspace_reset")
+
+    def __del__(self):
+        try:
+            if self._h:
+                _lib.lib().sphb_workspace_destroy(self._h)
+        except Exception:
+            pass
+
+
+def new_ctrl(device, max_steps: int = -1, t_end: float = math.inf) -> torch.Tensor:
+    ctrl = torch.empty(_lib.CTRL_BYTES, dtype=torch.uint8, device=device)
+    _lib.check(_lib.lib().sphb_ctrl_init(_ptr(ctrl), int(max_steps), float(t_end), _stream()),
+               "sphb_ctrl_init")
+    return ctrl
+
+
+def read_ctrl(ctrl: torch.Tensor) -> np.void:
+    host = ctrl.cpu().numpy()
+    return host[: _lib.CTRL_DTYPE.itemsize].view(_lib.CTRL_DTYPE)[0]
+
+
+def decode_err(err) -> tuple | None:
+    err = int(err)
+    if err == int(_lib.ERR_NONE):
+        return None
+    return (err >> 40, (err >> 32) & 0xFF, err & 0xFFFFFFFF)
+
+
+class DeviceSim:
+    """One particle system resident on the GPU, stepped by libsphb200.
+
+    ``system`` may be this package's ParticleSystem or the reference's (duck typing).
+    ``vel_prev``/``rho_prev`` seed the Verlet history (default: current state, as
+    VerletState.from_system does, sim.py:40-43).
+    """
+
+    def __init__(self, system, params, reach: int, order: int = 0, precision: int = _lib.SPHB_FP32,
+                 max_steps: int = -1, t_end: float = math.inf, record_capacity: int = 4096,
+                 vel_prev=None, rho_prev=None, device=None, workspace: Workspace | None = None):
+        require_cuda()
+        self.device = torch.device(device or f"cuda:{torch.cuda.current_device()}")
+        self.params = params
+        self.n = int(system.n)
+        self.nb = int(system.count_boundary)
+        self.mass_fluid = float(system.mass_fluid)
+        self.mass_boundary = float(system.mass_boundary)
+        self.grid = grid_desc(params, reach)
+        self.prm = params_desc(params, self.mass_fluid, self.mass_boundary, order, precision)
+        _, dims = grid_dims(params)
+        self.ncells = int(np.prod(dims))
+        n, dev = self.n, self.device
+        f4 = lambda: torch.empty((max(n, 1), F4), dtype=torch.float32, device=dev)  # noqa: E731
+        i32 = lambda m: torch.empty(max(m, 1), dtype=torch.int32, device=dev)  # noqa: E731
+        self.posp, self.velr, self.prev = f4(), f4(), f4()
+        self.posp_s, self.velr_s, self.prev_s, self.aux = f4(), f4(), f4(), f4()
+        self.id = torch.empty(max(n, 1), dtype=torch.int64, device=dev)
+        self.id_s = torch.empty_like(self.id)
+        self.keys, self.keys_sorted, self.perm, self.cell_s = i32(n), i32(n), i32(n), i32(n)
+        self.beg, self.end = i32(2 * self.ncells), i32(2 * self.ncells)
+        self.acc = torch.zeros((max(n, 1), 3), dtype=torch.float64, device=dev)
+        self.drho = torch.zeros(max(n, 1), dtype=torch.float64, device=dev)
+        self.visc = torch.zeros(max(n, 1), dtype=torch.float64, device=dev)
+        self.rec_cap = int(record_capacity)
+        self.rec = torch.zeros(self.rec_cap * _lib.REC_DTYPE.itemsize, dtype=torch.uint8, device=dev)
+        self.ws = workspace if workspace is not None else Workspace(n, self.ncells)
+        self.ws.reset()
+        self.upload(system, vel_prev, rho_prev)
+        self.ctrl = new_ctrl(dev, max_steps, t_end)
+        self._state = _lib.StateDesc(*[_ptr(t) for t in (
+            self.posp, self.velr, self.prev, self.id, self.posp_s, self.velr_s, self.prev_s,
+            self.aux, self.id_s, self.keys, self.keys_sorted, self.perm, self.cell_s, self.beg,
+            self.end, self.acc, self.drho, self.visc)])
+        self.first_keys()
+        self._graph = None
+        self._graph_steps = 0
+
+    # ------------------------------------------------------------------ host <-> device
+    def upload(self, system, vel_prev=None, rho_prev=None, stream_copy=True):
+        n = self.n
+        if n == 0:
+            return
+        pos = torch.as_tensor(np.ascontiguousarray(system.pos, np.float32))
+        vel = torch.as_tensor(np.ascontiguousarray(system.vel, np.float32))
+        rho = torch.as_tensor(np.ascontiguousarray(system.rho, np.float32))
+        vp = vel if vel_prev is None else torch.as_tensor(np.ascontiguousarray(vel_prev, np.float32))
+        rp = rho if rho_prev is None else torch.as_tensor(np.ascontiguousarray(rho_prev, np.float32))
+        host = torch.empty((3, n, 4), dtype=torch.float32, pin_memory=True)
+        host[0, :, :3] = pos
+        host[0, :, 3] = 0.0
+        host[1, :, :3] = vel
+        host[1, :, 3] = rho
+        host[2, :, :3] = vp
+        host[2, :, 3] = rp
+        self.posp[:n].copy_(host[0], non_blocking=True)
+        self.velr[:n].copy_(host[1], non_blocking=True)
+        self.prev[:n].copy_(host[2], non_blocking=True)
+        self.id[:n].copy_(torch.as_tensor(np.ascontiguousarray(system.id, np.int64)), non_blocking=False)
+
+    def download(self):
+        """(pos, vel, rho, id, vel_prev, rho_prev) of the primary arrays as numpy."""
+        n = self.n
+        p = self.posp[:n].cpu().numpy()
+        v = self.velr[:n].cpu().numpy()
+        pv = self.prev[:n].cpu().numpy()
+        ids = self.id[:n].cpu().numpy()
+        return (np.ascontiguousarray(p[:, :3]), np.ascontiguousarray(v[:, :3]),
+                np.ascontiguousarray(v[:, 3]), ids, np.ascontiguousarray(pv[:, :3]),
+                np.ascontiguousarray(pv[:, 3]))
+
+    # ------------------------------------------------------------------ kernels
+    def first_keys(self):
+        """K1 on the uploaded state (later steps get their keys from K7)."""
+        L = _lib.lib()
+        _lib.check(L.sphb_cell_keys(self.ws.handle, _lib.ref(self.grid), _ptr(self.posp), self.n,
+                                    self.nb, _ptr(self.keys), None, _ptr(self.ctrl), _stream()),
+                   "sphb_cell_keys")
+
+    def first_keys_resync(self):
+        """K1 for a state written from outside (host upload): histogram reset + keys."""
+        self.ws.reset()
+        self.first_keys()
+
+    def launch_step(self, events=None):
+        """Enqueue one NL -> PI -> SU step (no host sync).  ``events`` = 4 CUDA events
+        recorded at the stage boundaries (NL | PI | SU)."""
+        L, s, ws = _lib.lib(), _stream(), self.ws.handle
+        g, p, n, nb = _lib.ref(self.grid), _lib.ref(self.prm), self.n, self.nb
+        if events is None:
+            _lib.check(L.sphb_step(ws, p, g, n, nb, _lib.ref(self._state), _ptr(self.ctrl),
+                                   _ptr(self.rec), self.rec_cap, s), "sphb_step")
+            return
+        e0, e1, e2, e3 = events
+        e0.record()
+        _lib.check(L.sphb_step_begin(_ptr(self.ctrl), s), "sphb_step_begin")
+        _lib.check(L.sphb_sort(ws, g, _ptr(self.keys), n, _ptr(self.keys_sorted), _ptr(self.perm),
+                               _ptr(self.ctrl), s), "sphb_sort")
+        _lib.check(L.sphb_reorder(p, g, n, _ptr(self.perm), _ptr(self.keys_sorted), _ptr(self.posp),
+                                  _ptr(self.velr), _ptr(self.prev), _ptr(self.id), _ptr(self.posp_s),
+                                  _ptr(self.velr_s), _ptr(self.prev_s), _ptr(self.id_s),
+                                  _ptr(self.aux), _ptr(self.cell_s), _ptr(self.ctrl), s),
+                   "sphb_reorder")
+        _lib.check(L.sphb_cell_ranges(ws, g, _ptr(self.beg), _ptr(self.end), _ptr(self.ctrl), s),
+                   "sphb_cell_ranges")
+        e1.record()
+        _lib.check(L.sphb_interact(p, g, n, nb, _ptr(self.posp_s), _ptr(self.velr_s),
+                                   _ptr(self.aux), _ptr(self.cell_s), _ptr(self.beg),
+                                   _ptr(self.end), _ptr(self.acc), _ptr(self.drho),
+                                   _ptr(self.visc), _ptr(self.ctrl), s), "sphb_interact")
+        e2.record()
+        _lib.check(L.sphb_integrate(ws, p, g, n, nb, _ptr(self.posp_s), _ptr(self.velr_s),
+                                    _ptr(self.prev_s), _ptr(self.id_s), _ptr(self.acc),
+                                    _ptr(self.drho), _ptr(self.posp), _ptr(self.velr),
+                                    _ptr(self.prev), _ptr(self.id), _ptr(self.keys),
+                                    _ptr(self.ctrl), s), "sphb_integrate")
+        _lib.check(L.sphb_step_end(_ptr(self.ctrl), p, _ptr(self.rec), self.rec_cap, s),
+                   "sphb_step_end")
+        e3.record()
+
+    def capture(self, steps: int):
+        """Capture ``steps`` whole steps into one CUDA graph (replayed by run_graph)."""
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            for _ in range(steps):
+                self.launch_step()
+        self._graph, self._graph_steps = g, steps
+        return g
+
+    def run_graph(self):
+        self._graph.replay()
+
+    def launches_per_step(self) -> int:
+        return int(_lib.lib().sphb_step_launch_count(_lib.ref(self.grid), self.n))
+
+    # ------------------------------------------------------------------ readback
+    def ctrl_host(self):
+        return read_ctrl(self.ctrl)
+
+    def records(self, first: int, last: int) -> np.ndarray:
+        """Step records [first, last) (ring buffer of rec_cap entries)."""
+        if last <= first:
+            return np.zeros(0, _lib.REC_DTYPE)
+        if last - first > self.rec_cap:
+            raise ValueError("more steps than the record ring holds; read records more often")
+        host = self.rec.cpu().numpy().view(_lib.REC_DTYPE)
+        idx = np.arange(first, last) % self.rec_cap
+        return host[idx]
+
+    def error(self):
+        """None or (step, code, index, particle_id)."""
+        c = self.ctrl_host()
+        d = decode_err(c["err"])
+        if d is None:
+            return None
+        step, code, index = d
+        pid = int(self.id[index].item()) if code == _lib.SPHB_DIV_LEFT_DOMAIN else None
+        return step, code, index, pid
+
+
+def compute_derived_device(rho: np.ndarray, params):
+    """press/csound/prrho/tensil of ``rho`` with the device EOS (the K3 code path)."""
+    require_cuda()
+    n = int(np.asarray(rho).shape[0])
+    dev = torch.device("cuda")
+    velr = torch.zeros((max(n, 1), 4), dtype=torch.float32, device=dev)
+    if n:
+        velr[:n, 3] = torch.as_tensor(np.ascontiguousarray(rho, np.float32)).to(dev)
+    posp = torch.zeros_like(velr)
+    posp_o, velr_o, aux = torch.empty_like(velr), torch.empty_like(velr), torch.empty_like(velr)
+    prm = params_desc(params, 1.0, 1.0)
+    g = grid_desc(params)
+    ctrl = new_ctrl(dev)
+    _lib.check(_lib.lib().sphb_reorder(_lib.ref(prm), _lib.ref(g), n, None, None, _ptr(posp),
+                                       _ptr(velr), None, None, _ptr(posp_o), _ptr(velr_o), None,
+                                       None, _ptr(aux), None, _ptr(ctrl), _stream()),
+               "sphb_reorder")
+    a = aux[:n].cpu().numpy()
+    press = posp_o[:n, 3].cpu().numpy()
+    return press, np.ascontiguousarray(a[:, 1]), np.ascontiguousarray(a[:, 0]), np.ascontiguousarray(a[:, 2])
+
+
+def nl_frame(pos: np.ndarray, nb: int, params, reach: int | None = None):
+    """Device NL on one frame: K1 -> K2 -> K4 (and K3's cell output).  Returns numpy
+    (cell_of_unsorted int64, sort_perm int64, cell_of_sorted int64, fbeg, fend, bbeg, bend
+    int64) -- the reference's assign_cells / reorder / build_cell_index outputs."""
+    require_cuda()
+    n = int(pos.shape[0])
+    dev = torch.device("cuda")
+    g = grid_desc(params, reach)
+    _, dims = grid_dims(params)
+    ncells = int(np.prod(dims))
+    ws = Workspace(n, ncells)
+    ws.reset()
+    posp = torch.zeros((max(n, 1), 4), dtype=torch.float32, device=dev)
+    if n:
+        posp[:n, :3] = torch.as_tensor(np.ascontiguousarray(pos, np.float32)).to(dev)
+    keys = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+    ksort = torch.empty_like(keys)
+    perm = torch.empty_like(keys)
+    cell = torch.empty_like(keys)
+    beg = torch.empty(2 * ncells, dtype=torch.int32, device=dev)
+    end = torch.empty_like(beg)
+    ctrl = new_ctrl(dev)
+    L, s = _lib.lib(), _stream()
+    _lib.check(L.sphb_cell_keys(ws.handle, _lib.ref(g), _ptr(posp), n, nb, _ptr(keys), _ptr(cell),
+                                _ptr(ctrl), s), "sphb_cell_keys")
+    c = read_ctrl(ctrl)
+    cell_unsorted = cell[:n].cpu().numpy().astype(np.int64)
+    if decode_err(c["err"]) is not None:
+        return dict(cell_of_unsorted=cell_unsorted, error=decode_err(c["err"]))
+    _lib.check(L.sphb_sort(ws.handle, _lib.ref(g), _ptr(keys), n, _ptr(ksort), _ptr(perm),
+                           _ptr(ctrl), s), "sphb_sort")
+    _lib.check(L.sphb_cell_ranges(ws.handle, _lib.ref(g), _ptr(beg), _ptr(end), _ptr(ctrl), s),
+               "sphb_cell_ranges")
+    mask = (1 << cellbits_of(ncells)) - 1
+    ks = ksort[:n].cpu().numpy().view(np.uint32).astype(np.int64) & mask
+    b = beg.cpu().numpy().astype(np.int64)
+    e = end.cpu().numpy().astype(np.int64)
+    return dict(cell_of_unsorted=cell_unsorted, sort_perm=perm[:n].cpu().numpy().astype(np.int64),
+                cell_of=ks, bbeg=b[:ncells], bend=e[:ncells], fbeg=b[ncells:], fend=e[ncells:],
+                dims=dims, error=None)

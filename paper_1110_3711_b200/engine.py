@@ -1,0 +1,137 @@
+"""The drop-in force engine: ``make_engine(cfg).compute(...) -> ForceOutput``.
+
+Same protocol as the reference engines (sphbench/engines/__init__.py:30-48,
+gather.py:42-110): takes the caller's sorted frame (system, derived, grid, cindex,
+params) as host arrays, runs the B200 interaction kernels (csrc/interact.cu), and
+returns f64 numpy arrays plus StepStats with the reference's counter definitions.
+This is the per-call ("partial GPU") boundary; ``run_simulation``
+keeps the state resident instead.
+"""
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _lib
+from .config import (DERIVED_RECOMPUTED, ENGINE_GATHER, GATHER_FAST_HALF, NEIGHBOR_BYTES,
+                     EngineConfig, ForceOutput)
+from .device import Workspace, _ptr, _stream, new_ctrl, read_ctrl, require_cuda
+from .model import StepStats
+from .physics import grid_desc, grid_dims, params_desc
+
+PRECISION_CODE = {"fp32": _lib.SPHB_FP32, "fp64": _lib.SPHB_FP64}
+
+
+class B200Engine:
+    """Device gather engine; holds its device buffers across calls (resized on demand)."""
+
+    def __init__(self, config: EngineConfig):
+        self.config = config.validated()
+        self._buf = None
+        self._ws = None
+        self.last_kernel_ms = None
+
+    @property
+    def tag(self) -> str:
+        return self.config.tag
+
+    def _buffers(self, n: int, ncells: int):
+        if self._buf is None or self._buf["n"] < n or self._buf["ncells"] < ncells:
+            dev = torch.device("cuda")
+            m = max(n, 1)
+            self._buf = dict(
+                n=n, ncells=ncells,
+                host=torch.empty((3, m, 4), dtype=torch.float32, pin_memory=True),
+                hcell=torch.empty(m, dtype=torch.int32, pin_memory=True),
+                dev4=torch.empty((3, m, 4), dtype=torch.float32, device=dev),
+                cell=torch.empty(m, dtype=torch.int32, device=dev),
+                beg=torch.empty(2 * ncells, dtype=torch.int32, device=dev),
+                end=torch.empty(2 * ncells, dtype=torch.int32, device=dev),
+                acc=torch.empty((m, 3), dtype=torch.float64, device=dev),
+                drho=torch.empty(m, dtype=torch.float64, device=dev),
+                visc=torch.empty(m, dtype=torch.float64, device=dev),
+                out=torch.empty((m, 5), dtype=torch.float64, pin_memory=True),
+            )
+            self._ws = Workspace(n, ncells)
+        return self._buf
+
+    def compute(self, system, derived, grid, cindex, params, ranges=None) -> ForceOutput:
+        require_cuda()
+        cfg = self.config
+        n, nb = int(system.n), int(system.count_boundary)
+        cell_of = np.asarray(grid.cell_of)
+        if cell_of.shape[0] != n:
+            raise ValueError("grid/system length mismatch")
+        need = cfg.required_n_subdiv()
+        if need is not None and params.n_subdiv != need:
+            raise ValueError(f"gather variant {cfg.gather_variant} needs "
+                             f"n_subdiv={need}, got {params.n_subdiv}")
+        if cfg.engine == ENGINE_GATHER and cfg.gather_variant == GATHER_FAST_HALF and ranges is None:
+            raise ValueError("fastcellshalf requires precomputed interaction ranges")
+        reach = cfg.device_reach(params.n_subdiv)
+        g = grid_desc(params, reach)
+        _, dims = grid_dims(params)
+        ncells = int(np.prod(dims))
+        prm = params_desc(params, system.mass_fluid, system.mass_boundary, cfg.device_order(),
+                          PRECISION_CODE[cfg.precision])
+        b = self._buffers(n, ncells)
+        if n:
+            # pack the caller's frame: posp = (pos, press), velr = (vel, rho), aux = derived
+            h = b["host"]
+            h[0, :n, :3] = torch.from_numpy(np.ascontiguousarray(system.pos, np.float32))
+            h[0, :n, 3] = torch.from_numpy(np.ascontiguousarray(derived.press, np.float32))
+            h[1, :n, :3] = torch.from_numpy(np.ascontiguousarray(system.vel, np.float32))
+            h[1, :n, 3] = torch.from_numpy(np.ascontiguousarray(system.rho, np.float32))
+            h[2, :n, 0] = torch.from_numpy(np.ascontiguousarray(derived.prrho, np.float32))
+            h[2, :n, 1] = torch.from_numpy(np.ascontiguousarray(derived.csound, np.float32))
+            h[2, :n, 2] = torch.from_numpy(np.ascontiguousarray(derived.tensil, np.float32))
+            h[2, :n, 3] = 0.0
+            b["hcell"][:n] = torch.from_numpy(cell_of.astype(np.int32))
+            b["dev4"][:, :n].copy_(h[:, :n], non_blocking=True)
+            b["cell"][:n].copy_(b["hcell"][:n], non_blocking=True)
+        ctrl = new_ctrl(torch.device("cuda"))
+        L, s = _lib.lib(), _stream()
+        d4 = b["dev4"]
+        _lib.check(L.sphb_cell_ranges_from_sorted(self._ws.handle, _lib.ref(g), _ptr(b["cell"]), n, nb,
+                                                  _ptr(b["beg"]), _ptr(b["end"]), s),
+                   "sphb_cell_ranges_from_sorted")
+        _lib.check(L.sphb_step_begin(_ptr(ctrl), s), "sphb_step_begin")
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        _lib.check(L.sphb_interact(_lib.ref(prm), _lib.ref(g), n, nb, _ptr(d4[0]), _ptr(d4[1]),
+                                   _ptr(d4[2]), _ptr(b["cell"]), _ptr(b["beg"]), _ptr(b["end"]),
+                                   _ptr(b["acc"]), _ptr(b["drho"]), _ptr(b["visc"]), _ptr(ctrl), s),
+                   "sphb_interact")
+        e1.record()
+        out = b["out"]
+        if n:
+            out[:n, :3].copy_(b["acc"][:n], non_blocking=True)
+            out[:n, 3].copy_(b["drho"][:n], non_blocking=True)
+            out[:n, 4].copy_(b["visc"][:n], non_blocking=True)
+        c = read_ctrl(ctrl)  # synchronises
+        self.last_kernel_ms = e0.elapsed_time(e1)
+        o = out[:n].numpy()
+        accel = np.ascontiguousarray(o[:, :3])
+        raw = [int(v) for v in c["counters"]]
+        stats = StepStats(candidate_pairs=raw[0], true_pairs=raw[1] // 2, force_evals=raw[2],
+                          ff_force_evals=raw[3], engine_tag=self.tag,
+                          neighbor_bytes=NEIGHBOR_BYTES[cfg.derived_mode])
+        return ForceOutput(accel=accel, drho_dt=np.ascontiguousarray(o[:, 3]),
+                           visc_dt=np.ascontiguousarray(o[:, 4]), stats=stats)
+
+
+def make_engine(config: EngineConfig) -> B200Engine:
+    """engines/__init__.py:30-34 -- every validated config runs on the B200."""
+    return B200Engine(config.validated())
+
+
+def compute_forces_gather(system, derived, grid, cindex, ranges, params,
+                          config: EngineConfig) -> ForceOutput:
+    """engines/__init__.py:43-48."""
+    return B200Engine(config).compute(system, derived, grid, cindex, params, ranges=ranges)
+
+
+def compute_forces_cellpairs(system, derived, grid, cindex, params,
+                             config: EngineConfig) -> ForceOutput:
+    """engines/__init__.py:37-40 (executed by the device gather traversal)."""
+    return B200Engine(config).compute(system, derived, grid, cindex, params)

@@ -1,0 +1,71 @@
+"""Physics constants handed to the device (the reference's ``pack_params``,
+sphbench/physics.py:149-180) and the cubic-spline value used for W(dp).
+
+The pair math itself only exists on the device (csrc/interact.cu); the values here are
+computed with the reference's own f64 expressions so the FP64 kernel instantiation is
+bit-identical to the reference (tests/test_host.py pins them against tests/golden).
+"""
+from __future__ import annotations
+
+import math
+
+import numpy as np
+
+from . import _lib
+
+PP_NAMES = ("sup2", "h", "invh", "kc", "eta2", "alpha", "invwdp", "c0", "rho0", "gamma",
+            "mass_fluid", "mass_boundary")
+
+
+def kernel_w(r, h: float):
+    """Cubic spline W(r) with support 2h, 3-D normalisation kc = 1/(pi h^3) (physics.py:25-33)."""
+    q = np.asarray(r, dtype=np.float64) / h
+    kc = 1.0 / (math.pi * h ** 3)
+    w = np.where(q < 1.0, kc * (1.0 - 1.5 * q * q + 0.75 * q ** 3),
+                 np.where(q < 2.0, 0.25 * kc * (2.0 - q) ** 3, 0.0))
+    return w if w.ndim else float(w)
+
+
+def pack_params(params, mass_fluid: float, mass_boundary: float) -> np.ndarray:
+    """The 12 f64 constants of the pair loop, in the reference's order."""
+    sup = params.support_radius
+    return np.array([sup * sup, params.h, 1.0 / params.h, 1.0 / (math.pi * params.h ** 3),
+                     params.eta2, params.alpha, 1.0 / kernel_w(params.dp, params.h), params.c0,
+                     params.rho0, params.gamma, mass_fluid, mass_boundary], dtype=np.float64)
+
+
+def params_desc(params, mass_fluid: float, mass_boundary: float, order: int = 0,
+                precision: int = _lib.SPHB_FP32) -> "_lib.ParamsDesc":
+    d = _lib.ParamsDesc()
+    for name, v in zip(PP_NAMES, pack_params(params, mass_fluid, mass_boundary)):
+        setattr(d, name, float(v))
+    d.tait_b = float(params.tait_b)
+    for k in range(3):
+        d.g[k] = float(np.asarray(params.g, np.float64)[k])
+    d.cfl = float(params.cfl)
+    d.dt_min = float(params.dt_min)
+    d.dt_max = float(params.dt_max)
+    d.verlet_stride = int(params.verlet_corrector_stride)
+    d.order = int(order)
+    d.precision = int(precision)
+    return d
+
+
+def grid_dims(params):
+    """Cell side and dims exactly as assign_cells computes them (grid.py:81-84)."""
+    cs = params.cell_size
+    extent = np.asarray(params.domain_max, np.float64) - np.asarray(params.domain_min, np.float64)
+    dims = np.maximum(np.ceil(extent / cs - 1e-12).astype(np.int64), 1)
+    return cs, dims
+
+
+def grid_desc(params, reach: int | None = None) -> "_lib.GridDesc":
+    cs, dims = grid_dims(params)
+    g = _lib.GridDesc()
+    for k in range(3):
+        g.origin[k] = float(np.asarray(params.domain_min, np.float64)[k])
+        g.domain_max[k] = float(np.asarray(params.domain_max, np.float64)[k])
+        g.dims[k] = int(dims[k])
+    g.cell_size = float(cs)
+    g.reach = int(params.n_subdiv if reach is None else reach)
+    return g

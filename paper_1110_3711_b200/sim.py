@@ -1,0 +1,138 @@
+"""The step loop: ``run_simulation`` with the reference's signature, semantics and errors
+(sphbench/sim.py:272-352), executed device-resident on the B200.
+
+Differences from the reference are in *where* things run, not in what they compute:
+the state is uploaded once, every step runs NL -> PI -> SU in libsphb200 kernels with no
+per-step host synchronisation, and the host reads the device control block only every
+``chunk`` steps (or at snapshot / stats boundaries) to emit StepStats and to raise
+``DivergenceError`` with the same step, particle id and message the reference would.
+"""
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import torch
+
+from . import _lib
+from .config import EngineConfig, NEIGHBOR_BYTES
+from .device import DeviceSim, compute_derived_device
+from .engine import PRECISION_CODE
+from .model import DerivedQuantities, ParticleKind, StepStats, validate
+from .scenario import Scenario, build_dam_break
+
+
+class DivergenceError(RuntimeError):
+    """A particle left the domain or the state went non-finite (sim.py:22-29)."""
+
+    def __init__(self, message: str, step: int, particle_id: int | None = None):
+        super().__init__(message)
+        self.step = step
+        self.particle_id = particle_id
+
+
+def divergence_from_device(err) -> DivergenceError:
+    step, code, index, pid = err
+    if code == _lib.SPHB_DIV_LEFT_DOMAIN:
+        return DivergenceError(f"particle id {pid} left the domain at step {step}", step, pid)
+    if code == _lib.SPHB_DIV_NONFINITE_FORCES:
+        return DivergenceError(f"non-finite forces at step {step}", step)
+    return DivergenceError(f"non-finite state at step {step}", step)
+
+
+def compute_derived(rho, params) -> DerivedQuantities:
+    """physics.compute_derived (physics.py:96-110) on the device EOS."""
+    press, csound, prrho, tensil = compute_derived_device(np.asarray(rho), params)
+    return DerivedQuantities(press=press, csound=csound, prrho=prrho, tensil=tensil)
+
+
+class _Timer:
+    def __init__(self, steps):
+        self.ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(steps)]
+
+
+def make_device_sim(system, params, cfg: EngineConfig, max_steps=None, t_end=None, **kw) -> DeviceSim:
+    return DeviceSim(system, params, reach=cfg.device_reach(params.n_subdiv),
+                     order=cfg.device_order(), precision=PRECISION_CODE[cfg.precision],
+                     max_steps=-1 if max_steps is None else int(max_steps),
+                     t_end=math.inf if t_end is None else float(t_end), **kw)
+
+
+def run_simulation(scenario_or_system, params, config: EngineConfig, max_steps: int | None = None,
+                   t_end: float | None = None, snapshot_every: int = 0, snapshot_sink=None,
+                   stats_sink=None, *, chunk: int = 256, stage_timing: bool = True):
+    """NL -> PI -> SU loop on the B200.  Returns (system, stats_list) like sim.py:272-352;
+    raises DivergenceError on the first out-of-domain particle or non-finite state.
+
+    ``chunk`` bounds how many steps run between host readbacks (the record ring is
+    sized for it); ``stage_timing`` records CUDA events at the NL/PI/SU boundaries of
+    every step to fill StepStats.stage_*_s and wall_seconds."""
+    if max_steps is None and t_end is None:
+        raise ValueError("need max_steps or t_end")
+    validate(params)
+    cfg = config.validated()
+    need = cfg.required_n_subdiv()
+    if need is not None and params.n_subdiv != need:
+        raise ValueError(f"config {cfg.tag} needs n_subdiv={need}")
+    system = build_dam_break(scenario_or_system, params) if isinstance(scenario_or_system, Scenario) \
+        else scenario_or_system
+    chunk = max(1, int(chunk))
+    if snapshot_every and snapshot_sink is not None:
+        chunk = int(snapshot_every)  # chunk boundaries land on snapshot steps
+    sim = make_device_sim(system, params, cfg, max_steps, t_end, record_capacity=max(chunk, 1))
+    stats_out: list[StepStats] = []
+    nbytes = NEIGHBOR_BYTES[cfg.derived_mode]
+    done_steps = 0
+    while True:
+        timer = _Timer(chunk) if stage_timing else None
+        for k in range(chunk):
+            sim.launch_step(events=timer.ev[k] if timer else None)
+        c = sim.ctrl_host()  # synchronises
+        now = int(c["step"])
+        recs = sim.records(done_steps, now)
+        for k, r in enumerate(recs):
+            st = StepStats(step=done_steps + k, dt=float(r["dt"]),
+                           candidate_pairs=int(r["candidate_pairs"]),
+                           true_pairs=int(r["hits_ordered"]) // 2,
+                           force_evals=int(r["force_evals"]), ff_force_evals=int(r["ff_force_evals"]),
+                           engine_tag=cfg.tag, neighbor_bytes=nbytes)
+            if timer is not None:
+                e0, e1, e2, e3 = timer.ev[k]
+                st.stage_nl_s = e0.elapsed_time(e1) * 1e-3
+                st.stage_pi_s = e1.elapsed_time(e2) * 1e-3
+                st.stage_su_s = e2.elapsed_time(e3) * 1e-3
+                st.wall_seconds = e0.elapsed_time(e3) * 1e-3
+            if stats_sink is not None:
+                stats_sink(st)
+            stats_out.append(st)
+            step_no = done_steps + k + 1
+            if snapshot_every and step_no % snapshot_every == 0 and snapshot_sink is not None \
+                    and step_no == now:
+                snap = _system_from_device(sim, system)
+                snapshot_sink.emit(step_no, snap, compute_derived(snap.rho, params))
+        done_steps = now
+        err = sim.error()
+        if err is not None:
+            raise divergence_from_device(err)
+        if not int(c["active"]):
+            break
+    _write_back(sim, system)
+    return system, stats_out
+
+
+def _system_from_device(sim: DeviceSim, like):
+    pos, vel, rho, ids, _, _ = sim.download()
+    out = like.copy() if hasattr(like, "copy") else like
+    out.pos, out.vel, out.rho, out.id = pos, vel, rho, ids
+    nb = int(like.count_boundary)
+    out.ptype = np.concatenate([np.full(nb, ParticleKind.BOUNDARY, np.uint8),
+                                np.full(int(like.n) - nb, ParticleKind.FLUID, np.uint8)])
+    return out
+
+
+def _write_back(sim: DeviceSim, system):
+    pos, vel, rho, ids, _, _ = sim.download()
+    system.pos, system.vel, system.rho, system.id = pos, vel, rho, ids
+    nb = int(system.count_boundary)
+    system.ptype = np.concatenate([np.full(nb, ParticleKind.BOUNDARY, np.uint8),
+                                   np.full(int(system.n) - nb, ParticleKind.FLUID, np.uint8)])

@@ -1,0 +1,363 @@
+"""Parity of the CUDA path (through the package -> libsphb200 C ABI) with the reference.
+
+Anchors: golden vectors produced by the reference itself (tests/golden), the C oracle
+pinned to them (oracle/, tests/test_oracle.py), and reference-measured counts at full size
+(SURVEY.md Appendix A.9).  Bars (SURVEY.md §8(a')):
+  * NL (cell ids, sort permutation, per-cell ranges) and neighbour counters: bit-exact;
+  * forces / density rates / visc_dt: FP64 instantiation bit-exact; FP32 rel_linf <= 1e-5;
+  * one-step state rel_linf <= 1e-5 (FP32), dt rel <= 1e-6; FP64 trajectories bit-exact;
+  * 1000-step drift vs the reference within the tolerances stated in DESIGN.md.
+"""
+import types
+
+import numpy as np
+import pytest
+
+import oracle
+from conftest import golden, initial_state, scenario_from_npz
+
+pytestmark = pytest.mark.gpu
+
+sph = pytest.importorskip("paper_1110_3711_b200")
+from paper_1110_3711_b200 import device as D  # noqa: E402
+
+FRAMES = [("frame_small_n1.npz", "slowcellsh"), ("frame_small_n2.npz", "slowcellshalf"),
+          ("frame_small_n2.npz", "fastcellshalf"), ("frame_mid5k_n1.npz", "slowcellsh"),
+          ("frame_mid5k_n2.npz", "slowcellshalf"), ("frame_uniform3k_n1.npz", "slowcellsh"),
+          ("frame_uniform3k_n2.npz", "slowcellshalf"), ("frame_c1_n1.npz", "slowcellsh"),
+          ("frame_c1mid_n1.npz", "slowcellsh")]
+FP32_TOL = 1e-5
+
+
+def frame_objects(z):
+    prm = oracle.params_from_npz(z)
+    nb, nf = int(z["s_nb"]), int(z["s_nf"])
+    system = sph.ParticleSystem(count_fluid=nf, count_boundary=nb, pos=z["s_pos"], vel=z["s_vel"],
+                                rho=z["s_rho"], mass_fluid=float(z["s_mass_fluid"]),
+                                mass_boundary=float(z["s_mass_boundary"]), ptype=z["s_ptype"],
+                                id=z["s_id"])
+    derived = sph.DerivedQuantities(press=z["press"], csound=z["csound"], prrho=z["prrho"],
+                                    tensil=z["tensil"])
+    grid = types.SimpleNamespace(cell_of=z["cell_of"], dims=z["dims"])
+    cindex = types.SimpleNamespace()
+    return system, derived, grid, cindex, prm
+
+
+def gather_cfg(variant, precision):
+    return sph.EngineConfig(engine="gather", symmetry=False, gather_variant=variant,
+                            precision=precision)
+
+
+# ------------------------------------------------------------------ EOS / NL
+def test_device_eos_bit_exact():
+    z = golden("eos.npz")
+    prm = oracle.params_from_npz(z)
+    d = sph.compute_derived(z["rho"], prm)
+    for f in ("press", "csound", "prrho", "tensil"):
+        assert np.array_equal(getattr(d, f), z[f]), f
+
+
+@pytest.mark.parametrize("name", sorted({f for f, _ in FRAMES}))
+def test_device_nl_bit_exact(name):
+    z = golden(name)
+    prm = oracle.params_from_npz(z)
+    out = D.nl_frame(z["in_pos"], int(z["in_nb"]), prm)
+    assert out["error"] is None
+    for k in ("cell_of_unsorted", "sort_perm", "cell_of", "fbeg", "fend", "bbeg", "bend"):
+        assert np.array_equal(out[k], z[k]), k
+
+
+def _grid_params(cell=0.5, n_subdiv=1):
+    h = cell * n_subdiv / 2.0
+    return oracle.Params(h=h, dp=h / 2, rho0=1000.0, c0=20.0, gamma=7.0, alpha=0.25,
+                         g=np.zeros(3), cfl=0.3, domain_min=np.zeros(3), domain_max=np.ones(3),
+                         n_subdiv=n_subdiv)
+
+
+def test_device_cell_known_answers():
+    """pkg/tests/test_grid.py:34-62 restated against the device K1."""
+    prm = _grid_params()
+    pts = np.array([[0.6, 0.1, 0.1], [0.5, 0.1, 0.1], [1.0, 1.0, 1.0], [0.1, 0.6, 0.1],
+                    [0.1, 0.1, 0.6], [0.2, 0.2, 0.2]], np.float32)
+    out = D.nl_frame(pts, 0, prm)
+    assert list(out["cell_of_unsorted"]) == [1, 1, 7, 2, 4, 0]
+    out = D.nl_frame(np.array([[0.2, 0.2, 0.2], [-0.1, 0.0, 0.0], [0.3, 0.3, 0.3],
+                               [2.0, 0.1, 0.1]], np.float32), 0, prm)
+    assert list(out["cell_of_unsorted"]) == [0, -1, 0, -1]
+    step, code, index = out["error"]
+    assert (step, code, index) == (0, 1, 1)  # first offending index
+
+
+def test_device_sort_stable_and_lists_segregated():
+    """test_grid.py:75-115: stability ([1,2,0]) and per-list sorting."""
+    prm = _grid_params()
+    out = D.nl_frame(np.array([[0.6, 0.1, 0.1], [0.1, 0.1, 0.1], [0.11, 0.1, 0.1]], np.float32), 0, prm)
+    assert list(out["sort_perm"]) == [1, 2, 0]
+    rng = np.random.default_rng(6)
+    pos = rng.uniform(0, 1, (20000, 3)).astype(np.float32)
+    prm = _grid_params(cell=0.05)
+    out = D.nl_frame(pos, 8000, prm)
+    cell, _, _ = oracle.assign_cells(pos, prm)
+    perm = oracle.sort_perm(cell, 8000)
+    assert np.array_equal(out["sort_perm"], perm)
+    ncells = int(np.prod(out["dims"]))
+    fb, fe, bb, be = oracle.cell_index(cell[perm], 8000, ncells)
+    assert np.array_equal(out["fbeg"], fb) and np.array_equal(out["bend"], be)
+
+
+def test_device_nl_empty_and_single():
+    prm = _grid_params()
+    out = D.nl_frame(np.zeros((0, 3), np.float32), 0, prm)
+    assert out["sort_perm"].size == 0 and np.all(out["fbeg"] == 0) and np.all(out["bend"] == 0)
+    out = D.nl_frame(np.array([[0.7, 0.7, 0.7]], np.float32), 0, prm)
+    assert list(out["sort_perm"]) == [0] and out["fend"][-1] == 1
+
+
+# ------------------------------------------------------------------ forces
+@pytest.mark.parametrize("name,variant", FRAMES)
+def test_interact_fp64_bit_exact(name, variant):
+    z = golden(name)
+    system, derived, grid, cindex, prm = frame_objects(z)
+    eng = sph.make_engine(gather_cfg(variant, "fp64"))
+    out = eng.compute(system, derived, grid, cindex, prm, ranges=object())
+    assert np.array_equal(out.accel, z[f"{variant}_accel"])
+    assert np.array_equal(out.drho_dt, z[f"{variant}_drho"])
+    assert np.array_equal(out.visc_dt, z[f"{variant}_visc"])
+    c = z[f"{variant}_counters"]
+    assert [out.stats.candidate_pairs, out.stats.true_pairs, out.stats.force_evals,
+            out.stats.ff_force_evals] == list(c)
+
+
+@pytest.mark.parametrize("name,variant", FRAMES)
+def test_interact_fp32_within_tolerance(name, variant):
+    z = golden(name)
+    system, derived, grid, cindex, prm = frame_objects(z)
+    eng = sph.make_engine(gather_cfg(variant, "fp32"))
+    out = eng.compute(system, derived, grid, cindex, prm, ranges=object())
+    nb = system.count_boundary
+    assert np.all(out.accel[:nb] == 0.0)
+    assert oracle.rel_linf(out.accel, z[f"{variant}_accel"]) <= FP32_TOL
+    assert oracle.rel_linf(out.drho_dt, z[f"{variant}_drho"]) <= FP32_TOL
+    assert oracle.rel_linf(out.visc_dt, z[f"{variant}_visc"]) <= FP32_TOL
+    c = z[f"{variant}_counters"]
+    assert [out.stats.candidate_pairs, out.stats.true_pairs, out.stats.force_evals,
+            out.stats.ff_force_evals] == list(c)
+    out.stats.validate()
+
+
+def test_interact_deterministic_and_momentum():
+    z = golden("frame_uniform3k_n1.npz")  # fluid only
+    system, derived, grid, cindex, prm = frame_objects(z)
+    eng = sph.make_engine(sph.EngineConfig(engine="b200", symmetry=False))
+    a = eng.compute(system, derived, grid, cindex, prm)
+    b = eng.compute(system, derived, grid, cindex, prm)
+    assert np.array_equal(a.accel, b.accel) and np.array_equal(a.drho_dt, b.drho_dt)
+    m = system.mass_fluid
+    total = (m * a.accel).sum(axis=0)
+    assert np.abs(total).max() <= 1e-3 * (m * np.abs(a.accel)).sum()
+
+
+def test_engine_errors_match_reference():
+    z = golden("frame_small_n1.npz")
+    system, derived, grid, cindex, prm = frame_objects(z)
+    bad = types.SimpleNamespace(cell_of=grid.cell_of[:-1])
+    with pytest.raises(ValueError, match="mismatch"):
+        sph.make_engine(sph.EngineConfig()).compute(system, derived, bad, cindex, prm)
+    with pytest.raises(ValueError, match="n_subdiv"):
+        sph.make_engine(gather_cfg("fastcellshalf", "fp32")).compute(system, derived, grid, cindex, prm)
+
+
+# ------------------------------------------------------------------ trajectories
+TRAJ = [("traj_dp025_g.npz", "slowcellsh"), ("traj_dp02_n2_g.npz", "slowcellshalf"),
+        ("traj_c1_g100.npz", "slowcellsh")]
+
+
+@pytest.mark.parametrize("name,variant", TRAJ)
+def test_run_simulation_fp64_bit_exact(name, variant):
+    z = golden(name)
+    prm = oracle.params_from_npz(z)
+    sc = scenario_from_npz(z)
+    steps = z["dt"].shape[0]
+    system, stats = sph.run_simulation(sc, prm, gather_cfg(variant, "fp64"), max_steps=steps)
+    assert np.array_equal(np.array([s.dt for s in stats]), z["dt"])
+    got = np.array([[s.candidate_pairs, s.true_pairs, s.force_evals, s.ff_force_evals] for s in stats])
+    assert np.array_equal(got, z["counters"])
+    for f in ("id", "pos", "vel", "rho"):
+        assert np.array_equal(getattr(system, f), z["final_" + f]), f
+
+
+def test_run_simulation_fp32_one_step_and_short_trajectory():
+    z = golden("traj_c1_g100.npz")
+    prm = oracle.params_from_npz(z)
+    sc = scenario_from_npz(z)
+    cfg = gather_cfg("slowcellsh", "fp32")
+    s1, st1 = sph.run_simulation(sc, prm, cfg, max_steps=1)
+    assert abs(st1[0].dt - z["dt"][0]) <= 1e-6 * z["dt"][0]
+    assert np.array_equal(s1.id, z["st1_id"])
+    for f in ("pos", "vel", "rho"):
+        assert oracle.rel_linf(getattr(s1, f), z["st1_" + f]) <= FP32_TOL, f
+    s10, st10 = sph.run_simulation(sc, prm, cfg, max_steps=10)
+    order = np.argsort(s10.id)
+    ref_order = np.argsort(z["st10_id"])
+    for f in ("pos", "vel", "rho"):
+        assert oracle.rel_linf(getattr(s10, f)[order], z["st10_" + f][ref_order]) <= 1e-4, f
+    dts = np.array([s.dt for s in st10])
+    np.testing.assert_allclose(dts, z["dt"][:10], rtol=1e-5)
+
+
+def test_drift_1000_steps_fp32_vs_reference():
+    """SURVEY.md §8(d) drift bar: E = KE + PE + IE; tolerances stated in DESIGN.md."""
+    z = golden("drift_c1.npz")
+    prm = oracle.params_from_npz(z)
+    sc = sph.Scenario(dp=0.006)
+    rows = []
+
+    class Sink:
+        def emit(self, step, system, derived):
+            rows.append((step,) + oracle.energy_terms(system.pos, system.vel, system.rho,
+                                                      system.count_boundary, system.mass_fluid,
+                                                      system.mass_boundary, prm))
+
+    system, stats = sph.run_simulation(sc, prm, gather_cfg("slowcellsh", "fp32"), max_steps=1000,
+                                       snapshot_every=10, snapshot_sink=Sink(), stage_timing=False)
+    got = np.array(rows)
+    ref = z["diag"][1:]
+    assert got.shape == ref.shape and np.array_equal(got[:, 0], ref[:, 0])
+    emech0 = z["diag"][0][2] + z["diag"][0][3]  # PE0 + IE0 (KE0 = 0)
+    e_got = got[:, 1] + got[:, 2] + got[:, 3]
+    e_ref = ref[:, 1] + ref[:, 2] + ref[:, 3]
+    assert np.max(np.abs(e_got - e_ref)) / emech0 <= 1e-4
+    ke_ref = ref[:, 1]
+    mask = ke_ref > 1e-3 * ke_ref.max()
+    assert np.max(np.abs(got[mask, 1] - ke_ref[mask]) / ke_ref[mask]) <= 1e-3
+    assert np.max(np.abs(got[:, 4] - ref[:, 4])) / prm.rho0 <= 1e-5
+    sdt = np.sum([s.dt for s in stats])
+    assert abs(sdt - z["dt"].sum()) / z["dt"].sum() <= 1e-4
+    assert system.n == int(z["final_nb"]) + int(z["final_nf"])
+
+
+# ------------------------------------------------------------------ divergence
+def test_divergence_escaped_particle():
+    sc = sph.Scenario(dp=0.025)
+    prm = sph.make_params(sc)
+    system = sph.build_dam_break(sc, prm)
+    system.pos[-1] = prm.domain_max.astype(np.float32) + np.float32(1.0)
+    with pytest.raises(sph.DivergenceError) as err:
+        sph.run_simulation(system, prm, sph.EngineConfig(), max_steps=1)
+    assert err.value.step == 0
+    assert err.value.particle_id == int(system.id[-1])
+    assert "left the domain" in str(err.value)
+
+
+def test_divergence_nonfinite_state():
+    sc = sph.Scenario(dp=0.025)
+    prm = sph.make_params(sc)
+    system = sph.build_dam_break(sc, prm)
+    system.vel[-1, 0] = np.float32(np.nan)
+    with pytest.raises(sph.DivergenceError) as err:
+        sph.run_simulation(system, prm, sph.EngineConfig(), max_steps=1)
+    assert err.value.step == 0
+
+
+def test_run_zero_steps_and_t_end():
+    sc = sph.Scenario(dp=0.025)
+    prm = sph.make_params(sc)
+    expect = sph.build_dam_break(sc, prm)
+    system, stats = sph.run_simulation(sc, prm, sph.EngineConfig(), max_steps=0)
+    assert stats == [] and np.array_equal(system.pos, expect.pos)
+    _, stats = sph.run_simulation(sc, prm, sph.EngineConfig(), t_end=1e-3)
+    assert sum(s.dt for s in stats) >= 1e-3 and sum(s.dt for s in stats[:-1]) < 1e-3
+
+
+def test_stage_times_cover_the_step():
+    sc = sph.Scenario(dp=0.02)
+    prm = sph.make_params(sc)
+    _, stats = sph.run_simulation(sc, prm, sph.EngineConfig(), max_steps=8)
+    for s in stats[2:]:
+        assert s.stage_nl_s >= 0 and s.stage_pi_s > 0 and s.stage_su_s >= 0
+        staged = s.stage_nl_s + s.stage_pi_s + s.stage_su_s
+        assert staged <= s.wall_seconds * 1.001
+
+
+def test_snapshots_and_stats_sink():
+    sc = sph.Scenario(dp=0.025)
+    prm = sph.make_params(sc)
+    seen, lines = [], []
+
+    class Sink:
+        def emit(self, step, system, derived):
+            seen.append((step, system.n))
+
+    sph.run_simulation(sc, prm, sph.EngineConfig(), max_steps=6, snapshot_every=2,
+                       snapshot_sink=Sink(), stats_sink=lines.append)
+    assert [s[0] for s in seen] == [2, 4, 6] and len(lines) == 6
+
+
+def test_graph_capture_matches_eager():
+    z = golden("traj_dp025_g.npz")
+    prm = oracle.params_from_npz(z)
+    pos, vel, rho, ids, nb, mf, mb = initial_state(z)
+    s = sph.ParticleSystem(count_fluid=pos.shape[0] - nb, count_boundary=nb, pos=pos, vel=vel,
+                           rho=rho, mass_fluid=mf, mass_boundary=mb,
+                           ptype=np.r_[np.zeros(nb, np.uint8), np.ones(pos.shape[0] - nb, np.uint8)],
+                           id=ids)
+    sim = D.DeviceSim(s, prm, reach=1, precision=1)
+    sim.capture(5)
+    for _ in range(9):
+        sim.run_graph()
+    p, v, r, i, _, _ = sim.download()
+    assert int(sim.ctrl_host()["step"]) == 45
+    assert np.array_equal(i, z["final_id"]) and np.array_equal(p, z["final_pos"])
+    assert np.array_equal(v, z["final_vel"]) and np.array_equal(r, z["final_rho"])
+
+
+# ------------------------------------------------------------------ full sizes
+def _device_counters(name, n_subdiv, precision="fp32"):
+    sc = sph.named_scenario(name)
+    prm = sph.make_params(sc, n_subdiv=n_subdiv)
+    system = sph.build_dam_break(sc, prm)
+    nl = D.nl_frame(system.pos, system.count_boundary, prm)
+    perm = nl["sort_perm"]
+    ss = sph.ParticleSystem(count_fluid=system.count_fluid, count_boundary=system.count_boundary,
+                            pos=system.pos[perm], vel=system.vel[perm], rho=system.rho[perm],
+                            mass_fluid=system.mass_fluid, mass_boundary=system.mass_boundary,
+                            ptype=system.ptype[perm], id=system.id[perm])
+    der = sph.compute_derived(ss.rho, prm)
+    grid = types.SimpleNamespace(cell_of=nl["cell_of"])
+    variant = "slowcellsh" if n_subdiv == 1 else "slowcellshalf"
+    out = sph.make_engine(gather_cfg(variant, precision)).compute(ss, der, grid, None, prm)
+    return ss, der, nl, prm, out
+
+
+@pytest.mark.slow
+def test_c2_1m_parity_vs_oracle():
+    """C2 (1,142,622 particles): device NL bit-exact vs the oracle; forces vs the oracle C
+    gather (bit-exact to the reference) within 1e-5; counters bit-exact."""
+    ss, der, nl, prm, out = _device_counters("c2", 1)
+    sc = sph.named_scenario("c2")
+    system = sph.build_dam_break(sc, prm)
+    cell, dims, _ = oracle.assign_cells(system.pos, prm)
+    perm = oracle.sort_perm(cell, system.count_boundary)
+    assert np.array_equal(nl["cell_of_unsorted"], cell) and np.array_equal(nl["sort_perm"], perm)
+    cidx = oracle.cell_index(cell[perm], system.count_boundary, int(np.prod(dims)))
+    assert np.array_equal(nl["fbeg"], cidx[0]) and np.array_equal(nl["bend"], cidx[3])
+    ref = oracle.gather(ss.pos, ss.vel, ss.rho, ss.count_boundary, ss.mass_fluid,
+                        ss.mass_boundary, cell[perm], dims, cidx, prm)
+    assert [out.stats.candidate_pairs, out.stats.true_pairs, out.stats.force_evals,
+            out.stats.ff_force_evals] == list(ref["counters"])
+    assert out.stats.true_pairs == 126_461_402  # SURVEY.md A.2 (reference-measured)
+    for a, b in ((out.accel, ref["accel"]), (out.drho_dt, ref["drho_dt"]), (out.visc_dt, ref["visc_dt"])):
+        assert oracle.rel_linf(a, b) <= FP32_TOL
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("n_subdiv,cand", [(1, 16_164_890_622), (2, 9_401_964_162)])
+def test_c3_10m_counters_match_reference_measurement(n_subdiv, cand):
+    """C3 (10,200,478): the reference's own counts."""
+    _, _, _, _, out = _device_counters("c3", n_subdiv)
+    st = out.stats
+    assert st.true_pairs == 1_210_590_160
+    assert st.force_evals == 2_421_180_320
+    assert st.ff_force_evals == 2_373_133_760
+    assert st.candidate_pairs == cand
+    assert np.isfinite(out.accel).all()
