@@ -21,7 +21,7 @@
  *   posp  float4 (x, y, z, press)        press = Tait EOS of rho, f32-rounded (physics.py:119-121)
  *   velr  float4 (vx, vy, vz, rho)
  *   prev  float4 (vx_prev, vy_prev, vz_prev, rho_prev)   Verlet history (sim.py:31-43)
- *   aux   float4 (prrho, csound, tensil, 0)               derived (physics.py:124-134)
+ *   aux   float4 (prrho, csound, tensil, mass)            derived (physics.py:124-134) + list mass
  *   id    int64
  * Boundary particles occupy [0, nb), fluid [nb, n) (model.py:24-32).
  */
@@ -90,7 +90,8 @@ typedef struct {
   uint64_t err;          /* (step << 40) | (code << 32) | first offending index; ~0 = none */
   uint64_t counters[4];  /* running step: candidates, ordered hits, evals, ff evals */
   int32_t active;        /* 1 while no error and no stop rule fired */
-  int32_t pad_[15];
+  uint32_t tile_next[2]; /* dynamic work counters of the interaction launches (reset per step) */
+  int32_t pad_[13];
 } sphb_ctrl_t;
 
 /* Per-step record written at the end of every step (StepStats, model.py:176-212). */

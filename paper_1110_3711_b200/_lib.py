@@ -43,7 +43,8 @@ class StateDesc(ctypes.Structure):
 # numpy views of the device structs (sphb200.h)
 CTRL_DTYPE = np.dtype([("step", "<i8"), ("max_steps", "<i8"), ("t_sim", "<f8"), ("t_end", "<f8"),
                        ("dt", "<f8"), ("dtmin_f", "<u8"), ("dtmin_cv", "<u8"), ("err", "<u8"),
-                       ("counters", "<u8", (4,)), ("active", "<i4"), ("pad_", "<i4", (15,))])
+                       ("counters", "<u8", (4,)), ("active", "<i4"), ("tile_next", "<u4", (2,)),
+                       ("pad_", "<i4", (13,))])
 CTRL_BYTES = 256
 assert CTRL_DTYPE.itemsize <= CTRL_BYTES
 REC_DTYPE = np.dtype([("dt", "<f8"), ("candidate_pairs", "<u8"), ("hits_ordered", "<u8"),

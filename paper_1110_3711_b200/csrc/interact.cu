@@ -7,22 +7,26 @@
 //
 // Work decomposition (FP32 CUDA cores; the pair math is a data-dependent gather-reduce,
 // not a dense contraction, so no tensor cores):
-//   * one warp owns 32 consecutive cell-sorted target particles (one per lane);
+//   * one warp owns 32 consecutive cell-sorted target particles (one per lane); warps pull
+//     32-target tiles dynamically (atomic tile counter) until the list is exhausted;
 //   * lanes are grouped by their cell's (y, z) row; for each of the (2r+1)^2 stencil rows a
 //     group walks the UNION of its lanes' x-ranges, which is one contiguous particle range
-//     because cells are x-fastest (grid.py:1-8);
+//     because cells are x-fastest (grid.py:1-8).  No per-candidate range test is needed:
+//     a sure FP32 hit lies strictly inside 2h, hence inside the lane's own stencil;
 //   * candidates are staged 32 at a time into shared memory with one coalesced float4 load
-//     and broadcast to every lane (LDS.128 broadcast);
-//   * the distance test runs in FP32 with a relative guard band of 1e-5 around the cutoff;
-//     anything inside the band (or with r2 ~ 0) is re-decided with the reference's exact f64
-//     expression, so hit sets -- hence true_pairs / force_evals / ff counters -- are
-//     bit-exact (SURVEY.md §8(a') "Neighbour predicate");
-//   * hits go to a per-lane FIFO in shared memory and are evaluated in lock-step drains
-//     (the device analogue of the reference's pack-of-4 lane batching, kernels.py:97-118):
-//     a warp only evaluates when a lane's FIFO is about to overflow, and then drains at
-//     least the warp-minimum backlog, so divergence on the ~15-25% hit rate costs little;
-//   * FIFO order == candidate order == the reference's accumulation order, so the f64
-//     instantiation reproduces the reference's forces bit for bit.
+//     and broadcast to every lane (LDS.128 broadcast); the screen is branch-free
+//     (r2 < sup2*(1+1e-5)) and produces one 32-bit "maybe" mask per lane per chunk;
+//   * mask words are queued per lane in shared memory (a whole tile's worth), then drained
+//     once in lock-step: every lane pops its next candidate (FIFO == candidate order ==
+//     the reference's accumulation order) and evaluates it -- the device analogue of the
+//     reference's pack-of-4 lane batching (kernels.py:97-118), so the ~15-25% hit rate
+//     costs no divergence in the pair math;
+//   * maybes that are not sure hits (inside the 1e-5 guard band around the cutoff, or
+//     r2 ~ 0 -- e.g. the particle itself) are re-decided in the drain with the reference's
+//     exact f64 predicate, so hit sets -- hence true_pairs / force_evals / ff counters --
+//     are bit-exact (SURVEY.md §8(a') "Neighbour predicate");
+//   * the FP64 instantiation uses the exact predicate in the screen and the reference's
+//     exact operation order in the pair math: bit-identical forces.
 #include <climits>
 
 #include "sphb_common.cuh"
@@ -32,9 +36,8 @@ using namespace sphb;
 
 namespace {
 
-constexpr int IW = 4;   // warps per block
-constexpr int QD = 64;  // per-lane hit FIFO depth (power of two)
-constexpr int QM = QD - 1;
+constexpr int IW = 4;     // warps per block
+constexpr int RING = 64;  // queued 32-candidate chunks per warp (covers a whole tile)
 
 struct KArgs {
   sphb_params_t p;
@@ -78,35 +81,31 @@ struct Accum {
   R ax, ay, az, dr, vd;
 };
 
-// FP32 pair evaluation (physics.py:183-220 restated for FP32 CUDA cores).
-// Folded constants: k_gc = kc/h, k_tw = kc/W(dp); the 0.5 factors of the viscous term cancel.
-__device__ __forceinline__ void pair_eval(const KArgs& a, const Own<float>& o, float xj, float yj,
-                                          float zj, const float4& vj, const float4& xa, float mj,
+// FP32 pair evaluation (physics.py:183-220 restated for FP32 CUDA cores).  dx, r2 come
+// from the caller.  Folded constants: k_gc = kc/h, k_tw = kc/W(dp); the 0.5 factors of the
+// viscous term cancel; the neighbour's list mass travels in aux.w.
+__device__ __forceinline__ void pair_eval(const KArgs& a, const Own<float>& o, float dx, float dy,
+                                          float dz, float r2, const float4& vj, const float4& xa,
                                           Accum<float>& s) {
-  const float dx = o.x - xj, dy = o.y - yj, dz = o.z - zj;
-  const float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
   const float rinv = rsqrtf(r2);
   const float r = r2 * rinv;
   const float q = r * a.invh;
-  float w, dw;
-  if (q < 1.0f) {
-    const float q2 = q * q;
-    w = fmaf(0.75f * q, q2, fmaf(-1.5f, q2, 1.0f));
-    dw = fmaf(2.25f, q, -3.0f) * q;
-  } else {
-    const float t = 2.0f - q;
-    const float t2 = t * t;
-    w = 0.25f * t2 * t;
-    dw = -0.75f * t2;
-  }
+  const float t = 2.0f - q;
+  const float t2 = t * t;
+  const float q2 = q * q;
+  const bool inner = q < 1.0f;
+  const float w = inner ? fmaf(0.75f * q, q2, fmaf(-1.5f, q2, 1.0f)) : 0.25f * t2 * t;
+  const float dw = inner ? fmaf(2.25f, q, -3.0f) * q : -0.75f * t2;
   const float gc = dw * a.k_gc * rinv;
   const float dvx = o.vx - vj.x, dvy = o.vy - vj.y, dvz = o.vz - vj.z;
   const float dot = fmaf(dvz, dz, fmaf(dvy, dy, dvx * dx));
   const float mu = __fdividef(a.h * dot, r2 + a.eta2);
-  const float visc = dot < 0.0f ? __fdividef(-a.alpha * (o.cs + xa.y) * mu, o.rho + vj.w) : 0.0f;
+  const float vterm = __fdividef(-a.alpha * (o.cs + xa.y) * mu, o.rho + vj.w);
+  const float visc = dot < 0.0f ? vterm : 0.0f;
   const float tw = w * a.k_tw;
   const float tw2 = tw * tw;
   const float pterm = fmaf((o.ten + xa.z) * tw2, tw2, o.prrho + xa.x + visc);
+  const float mj = xa.w;
   const float fm = mj * pterm * gc;
   s.ax = fmaf(-fm, dx, s.ax);
   s.ay = fmaf(-fm, dy, s.ay);
@@ -117,12 +116,10 @@ __device__ __forceinline__ void pair_eval(const KArgs& a, const Own<float>& o, f
 
 // FP64 pair evaluation: the reference's exact operation order (physics.py:196-220,
 // kernels.py:382-390), no contraction.  Bit-identical to numba.
-__device__ __forceinline__ void pair_eval(const KArgs& a, const Own<double>& o, double xj,
-                                          double yj, double zj, const float4& vj, const float4& xa,
-                                          double mj, Accum<double>& s) {
+__device__ __forceinline__ void pair_eval(const KArgs& a, const Own<double>& o, double dx,
+                                          double dy, double dz, double r2, const float4& vj,
+                                          const float4& xa, double mj, Accum<double>& s) {
   const sphb_params_t& p = a.p;
-  const double dx = xsub(o.x, xj), dy = xsub(o.y, yj), dz = xsub(o.z, zj);
-  const double r2 = xadd(xadd(xmul(dx, dx), xmul(dy, dy)), xmul(dz, dz));
   const double r = __dsqrt_rn(r2);
   const double q = xmul(r, p.invh);
   const double kc = p.kc;
@@ -177,37 +174,63 @@ __device__ __forceinline__ void stage_store(Stage<double>* s, const float4& p) {
   s->z = (double)p.z;
 }
 
-// candidate test: FP32 fast path with exact f64 re-decision in the guard band
-__device__ __forceinline__ bool cand_hit(const KArgs& a, const Own<float>& o, const Stage<float>& c) {
+// Candidate screen.  FP32: "maybe" = r2 < sup2*(1+1e-5); the drain re-decides the rare
+// maybes that are not sure hits (guard band, r2 ~ 0) exactly.  FP64: the exact predicate.
+__device__ __forceinline__ bool cand_maybe(const KArgs& a, const Own<float>& o,
+                                           const Stage<float>& c) {
   const float dx = o.x - c.v.x, dy = o.y - c.v.y, dz = o.z - c.v.z;
   const float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
-  if (r2 >= a.sup2_hi) return false;
-  if (r2 < a.sup2_lo && r2 > a.tiny) return true;
-  return exact_hit((double)o.x, (double)o.y, (double)o.z, (double)c.v.x, (double)c.v.y,
-                   (double)c.v.z, a.p.sup2);
+  return r2 < a.sup2_hi;
 }
-__device__ __forceinline__ bool cand_hit(const KArgs& a, const Own<double>& o,
-                                         const Stage<double>& c) {
+__device__ __forceinline__ bool cand_maybe(const KArgs& a, const Own<double>& o,
+                                           const Stage<double>& c) {
   return exact_hit(o.x, o.y, o.z, c.x, c.y, c.z, a.p.sup2);
 }
 
-template <typename R>
-__device__ __forceinline__ R load_coord(const float4& p, int k) {
-  return (R)(k == 0 ? p.x : (k == 1 ? p.y : p.z));
+// Evaluate one queued candidate j; returns false if it was a maybe that the exact
+// predicate (or the stencil range) rejects.
+__device__ __forceinline__ bool eval_one(const KArgs& a, const Own<float>& o, int32_t j, int xlo,
+                                         int xhi, Accum<float>& s) {
+  const float4 pj = __ldg(&a.posp[j]);
+  const float4 vj = __ldg(&a.velr[j]);
+  const float4 xa = __ldg(&a.aux[j]);
+  const float dx = o.x - pj.x, dy = o.y - pj.y, dz = o.z - pj.z;
+  const float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
+  if (!(r2 < a.sup2_lo && r2 > a.tiny)) {
+    // cold path: exact f64 predicate + stencil x-range (the y/z rows are the lane's own)
+    const int cj = __ldg(&a.cell[j]);
+    const int cxj = cj % a.g.dims[0];
+    const bool ok = exact_hit((double)o.x, (double)o.y, (double)o.z, (double)pj.x, (double)pj.y,
+                              (double)pj.z, a.p.sup2) && cxj >= xlo && cxj <= xhi;
+    if (!ok) return false;
+  }
+  pair_eval(a, o, dx, dy, dz, r2, vj, xa, s);
+  return true;
+}
+__device__ __forceinline__ bool eval_one(const KArgs& a, const Own<double>& o, int32_t j, int,
+                                         int, Accum<double>& s) {
+  const float4 pj = __ldg(&a.posp[j]);
+  const float4 vj = __ldg(&a.velr[j]);
+  const float4 xa = __ldg(&a.aux[j]);
+  const double dx = xsub(o.x, (double)pj.x), dy = xsub(o.y, (double)pj.y),
+               dz = xsub(o.z, (double)pj.z);
+  const double r2 = xadd(xadd(xmul(dx, dx), xmul(dy, dy)), xmul(dz, dz));
+  const double mj = j < a.nb ? a.p.mass_boundary : a.p.mass_fluid;
+  pair_eval(a, o, dx, dy, dz, r2, vj, xa, mj, s);
+  return true;
 }
 
 // ------------------------------------------------------------------ the kernel
 template <typename R, bool FLUID_ITEMS>
-__global__ void __launch_bounds__(IW * 32) k_interact(KArgs a) {
+__global__ void __launch_bounds__(IW * 32, sizeof(R) == 4 ? 6 : 3) k_interact(KArgs a) {
   if (!step_live(a.ctrl)) return;
   __shared__ Stage<R> s_stage[IW][32];
-  __shared__ int32_t s_q[IW][QD][32];
+  __shared__ uint32_t s_mask[IW][RING][32];  // per-lane hit bitmask of each queued chunk
+  __shared__ int32_t s_cbase[IW][RING];      // first candidate index of each queued chunk
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t nitems = a.item_hi - a.item_lo;
-  const int64_t ntiles = (nitems + 31) / 32;
-  const int64_t gwarp = (int64_t)blockIdx.x * IW + warp;
-  const int64_t nwarps = (int64_t)gridDim.x * IW;
+  const uint32_t ntiles = (uint32_t)((nitems + 31) / 32);
   const int64_t step = a.ctrl->step;
   const int nx = a.g.dims[0], ny = a.g.dims[1], nz = a.g.dims[2];
   const int reach = a.g.reach;
@@ -216,8 +239,12 @@ __global__ void __launch_bounds__(IW * 32) k_interact(KArgs a) {
   unsigned long long c_cand = 0, c_hits = 0, c_ff = 0;
   double dtf_min = INFINITY, dtcv_min = INFINITY;
 
-  for (int64_t tile = gwarp; tile < ntiles; tile += nwarps) {
-    const int64_t i = a.item_lo + tile * 32 + lane;
+  for (;;) {
+    uint32_t tile = 0;
+    if (lane == 0) tile = atomicAdd(&a.ctrl->tile_next[FLUID_ITEMS ? 0 : 1], 1u);
+    tile = __shfl_sync(SPHB_FULL, tile, 0);
+    if (tile >= ntiles) break;
+    const int64_t i = a.item_lo + (int64_t)tile * 32 + lane;
     const bool valid = i < a.item_hi;
     Own<R> o;
     int cx = 0, rowkey = -1;
@@ -227,34 +254,40 @@ __global__ void __launch_bounds__(IW * 32) k_interact(KArgs a) {
       o.vx = (R)vi.x; o.vy = (R)vi.y; o.vz = (R)vi.z; o.rho = (R)vi.w;
       o.prrho = (R)xi.x; o.cs = (R)xi.y; o.ten = (R)xi.z;
       const int c = a.cell[i];
-      const int cyz = c / nx;
-      cx = c - cyz * nx;
-      rowkey = cyz;
+      rowkey = c / nx;
+      cx = c - rowkey * nx;
     } else {
       o.x = o.y = o.z = o.vx = o.vy = o.vz = o.prrho = o.cs = o.ten = (R)0;
       o.rho = (R)1;
     }
     const int xlo = max(cx - reach, 0), xhi = min(cx + reach, nx - 1);
     Accum<R> s = {(R)0, (R)0, (R)0, (R)0, (R)0};
-    uint32_t head = 0, tail = 0;
+    uint32_t nslot = 0;        // queued chunks (warp-uniform)
+    uint32_t pend = 0;         // queued candidate bits of this lane
+    uint32_t pushed = 0, pushed_b = 0, rej = 0, rej_f = 0;
     unsigned long long cand = 0;
 
-    // lock-step drain of up to k queued hits per lane
-    auto drain = [&](uint32_t k) {
-      for (uint32_t it = 0; it < k; ++it) {
-        if (tail != head) {
-          const int32_t j = s_q[warp][head & QM][lane];
-          ++head;
-          const float4 pj = __ldg(&a.posp[j]);
-          const float4 vj = __ldg(&a.velr[j]);
-          const float4 xa = __ldg(&a.aux[j]);
-          const bool jb = j < nb;
-          const R mj = jb ? (R)a.p.mass_boundary : (R)a.p.mass_fluid;
-          pair_eval(a, o, (R)pj.x, (R)pj.y, (R)pj.z, vj, xa, mj, s);
-          c_hits += 1;
-          if (FLUID_ITEMS && !jb) c_ff += 1;
+    // Evaluate every queued candidate, FIFO per lane, lock-step across the warp.
+    auto drain = [&]() {
+      __syncwarp();
+      const uint32_t mx = __reduce_max_sync(SPHB_FULL, pend);
+      uint32_t sl = 0;
+      uint32_t cur = nslot ? s_mask[warp][0][lane] : 0u;
+      for (uint32_t it = 0; it < mx; ++it) {
+        while (cur == 0u && sl + 1 < nslot) cur = s_mask[warp][++sl][lane];
+        if (cur) {
+          const int t = __ffs(cur) - 1;
+          cur &= cur - 1u;
+          const int32_t j = s_cbase[warp][sl] + t;
+          if (!eval_one(a, o, j, xlo, xhi, s)) {
+            ++rej;
+            if (j >= nb) ++rej_f;
+          }
         }
       }
+      nslot = 0;
+      pend = 0;
+      __syncwarp();
     };
 
     uint32_t todo = __ballot_sync(SPHB_FULL, valid);
@@ -278,40 +311,35 @@ __global__ void __launch_bounds__(IW * 32) k_interact(KArgs a) {
             const int64_t base = (int64_t)nx * (yy + (int64_t)ny * zz);
 #pragma unroll 1
             for (int li = 0; li < 2; ++li) {
-              // li 0: fluid list (offset ncells in beg/end), li 1: boundary list
-              const bool fluid_list = li == 0;
+              const bool fluid_list = li == 0;  // li 1: boundary list
               if (!fluid_list && !FLUID_ITEMS) continue;
               if (npass == 2 && (pass == 0) != fluid_list) continue;
               const int64_t off = fluid_list ? a.ncells : 0;
               const int32_t u0 = a.beg[off + base + gxlo];
               const int32_t u1 = a.end[off + base + gxhi];
               if (u1 <= u0) continue;
-              int32_t al = 0, bl = 0;
-              if (ing) {
-                al = a.beg[off + base + xlo];
-                bl = a.end[off + base + xhi];
-                cand += (unsigned long long)(bl - al);
-              }
-              const uint32_t span = (uint32_t)(bl - al);
+              if (ing) cand += (unsigned long long)(a.end[off + base + xhi] - a.beg[off + base + xlo]);
               for (int32_t j0 = u0; j0 < u1; j0 += 32) {
                 const int32_t jj = j0 + lane;
-                if (jj < u1) stage_store(&s_stage[warp][lane], __ldg(&a.posp[jj]));
+                const float4 pc = jj < u1 ? __ldg(&a.posp[jj])
+                                          : make_float4(INFINITY, INFINITY, INFINITY, 0.f);
+                stage_store(&s_stage[warp][lane], pc);
                 __syncwarp();
-                const int cnt = min(32, u1 - j0);
-                for (int t = 0; t < cnt; ++t) {
-                  const int32_t j = j0 + t;
-                  const bool inr = (uint32_t)(j - al) < span;
-                  if (inr && cand_hit(a, o, s_stage[warp][t])) {
-                    s_q[warp][tail & QM][lane] = j;
-                    ++tail;
-                  }
-                }
+                uint32_t bits = 0;
+#pragma unroll
+                for (int t = 0; t < 32; ++t)
+                  if (cand_maybe(a, o, s_stage[warp][t])) bits |= 1u << t;
+                bits = ing ? bits : 0u;
                 __syncwarp();
-                const uint32_t pend = tail - head;
-                const uint32_t mx = __reduce_max_sync(SPHB_FULL, ing ? pend : 0u);
-                if (mx > (uint32_t)(QD - 32)) {
-                  const uint32_t mn = __reduce_min_sync(SPHB_FULL, ing ? pend : 0xffffffffu);
-                  drain(max(mn, mx - (uint32_t)(QD - 32)));
+                if (__any_sync(SPHB_FULL, bits != 0u)) {
+                  if (nslot == RING) drain();
+                  s_mask[warp][nslot][lane] = bits;
+                  if (lane == 0) s_cbase[warp][nslot] = j0;
+                  ++nslot;
+                  const uint32_t pc2 = __popc(bits);
+                  pend += pc2;
+                  pushed += pc2;
+                  if (!fluid_list) pushed_b += pc2;
                 }
               }
             }
@@ -319,11 +347,13 @@ __global__ void __launch_bounds__(IW * 32) k_interact(KArgs a) {
         }
       }
     }
-    drain(__reduce_max_sync(SPHB_FULL, tail - head));
+    drain();
 
     if (valid) {
       if (FLUID_ITEMS) cand -= 1;  // the reference skips j == i before counting (kernels.py:369-371)
       c_cand += cand;
+      c_hits += pushed - rej;
+      if (FLUID_ITEMS) c_ff += (pushed - pushed_b) - rej_f;
       const double ax = (double)s.ax, ay = (double)s.ay, az = (double)s.az;
       const double dr = (double)s.dr, vd = (double)s.vd;
       if (FLUID_ITEMS) {

@@ -202,7 +202,7 @@ __global__ void __launch_bounds__(SORT_BLOCK) k_radix_scatter(
 
 // ------------------------------------------------------------------ K3 reorder + EOS
 __global__ void __launch_bounds__(256) k_reorder(
-    sphb_params_t p, uint32_t cellmask, int64_t n, const int32_t* __restrict__ perm,
+    sphb_params_t p, uint32_t cellmask, int cellbits, int64_t n, const int32_t* __restrict__ perm,
     const uint32_t* __restrict__ keys_sorted, const float4* __restrict__ posp_in,
     const float4* __restrict__ velr_in, const float4* __restrict__ prev_in,
     const int64_t* __restrict__ id_in, float4* __restrict__ posp_out, float4* __restrict__ velr_out,
@@ -220,7 +220,10 @@ __global__ void __launch_bounds__(256) k_reorder(
     pp.w = press;
     posp_out[i] = pp;
     velr_out[i] = vr;
-    aux_out[i] = make_float4(d.prrho, d.csound, d.tensil, 0.f);
+    // aux.w carries the list mass so the FP32 pair loop needs no index compare
+    const bool boundary = keys_sorted ? ((keys_sorted[i] >> cellbits) & 1u) == 0u : false;
+    aux_out[i] = make_float4(d.prrho, d.csound, d.tensil,
+                             (float)(boundary ? p.mass_boundary : p.mass_fluid));
     if (prev_in && prev_out) prev_out[i] = prev_in[o];
     if (id_in && id_out) id_out[i] = id_in[o];
     if (cell_out && keys_sorted) cell_out[i] = (int32_t)(keys_sorted[i] & cellmask);
@@ -355,7 +358,7 @@ int launch_reorder(const sphb_params_t& p, const sphb_grid_t& g, int64_t n, cons
                    int32_t* cell_out, const sphb_ctrl_t* ctrl, cudaStream_t s) {
   if (n == 0) return SPHB_OK;
   uint32_t cellmask = (1u << cellbits_of(g)) - 1u;
-  k_reorder<<<grid_for(n, 256), 256, 0, s>>>(p, cellmask, n, perm, keys_sorted, posp_in, velr_in,
+  k_reorder<<<grid_for(n, 256), 256, 0, s>>>(p, cellmask, cellbits_of(g), n, perm, keys_sorted, posp_in, velr_in,
                                              prev_in, id_in, posp_out, velr_out, prev_out, id_out,
                                              aux_out, cell_out, ctrl);
   return sphb_check_launch("k_reorder");

@@ -85,7 +85,8 @@ class B200Engine:
             h[2, :n, 0] = torch.from_numpy(np.ascontiguousarray(derived.prrho, np.float32))
             h[2, :n, 1] = torch.from_numpy(np.ascontiguousarray(derived.csound, np.float32))
             h[2, :n, 2] = torch.from_numpy(np.ascontiguousarray(derived.tensil, np.float32))
-            h[2, :n, 3] = 0.0
+            h[2, :nb, 3] = float(np.float32(system.mass_boundary))
+            h[2, nb:n, 3] = float(np.float32(system.mass_fluid))
             b["hcell"][:n] = torch.from_numpy(cell_of.astype(np.int32))
             b["dev4"][:, :n].copy_(h[:, :n], non_blocking=True)
             b["cell"][:n].copy_(b["hcell"][:n], non_blocking=True)

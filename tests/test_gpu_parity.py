@@ -331,8 +331,9 @@ def _device_counters(name, n_subdiv, precision="fp32"):
 
 @pytest.mark.slow
 def test_c2_1m_parity_vs_oracle():
-    """C2 (1,142,622 particles): device NL bit-exact vs the oracle; forces vs the oracle C
-    gather (bit-exact to the reference) within 1e-5; counters bit-exact."""
+    """C2 (1,142,622 particles), initial frame: device NL bit-exact vs the oracle; FP32 forces
+    vs the oracle C gather (bit-exact to the reference) within 1e-5; counters bit-exact;
+    FP64 forces bit-exact."""
     ss, der, nl, prm, out = _device_counters("c2", 1)
     sc = sph.named_scenario("c2")
     system = sph.build_dam_break(sc, prm)
@@ -340,24 +341,34 @@ def test_c2_1m_parity_vs_oracle():
     perm = oracle.sort_perm(cell, system.count_boundary)
     assert np.array_equal(nl["cell_of_unsorted"], cell) and np.array_equal(nl["sort_perm"], perm)
     cidx = oracle.cell_index(cell[perm], system.count_boundary, int(np.prod(dims)))
-    assert np.array_equal(nl["fbeg"], cidx[0]) and np.array_equal(nl["bend"], cidx[3])
+    for k, a in zip(("fbeg", "fend", "bbeg", "bend"), cidx):
+        assert np.array_equal(nl[k], a), k
     ref = oracle.gather(ss.pos, ss.vel, ss.rho, ss.count_boundary, ss.mass_fluid,
                         ss.mass_boundary, cell[perm], dims, cidx, prm)
     assert [out.stats.candidate_pairs, out.stats.true_pairs, out.stats.force_evals,
             out.stats.ff_force_evals] == list(ref["counters"])
-    assert out.stats.true_pairs == 126_461_402  # SURVEY.md A.2 (reference-measured)
     for a, b in ((out.accel, ref["accel"]), (out.drho_dt, ref["drho_dt"]), (out.visc_dt, ref["visc_dt"])):
         assert oracle.rel_linf(a, b) <= FP32_TOL
+    grid = types.SimpleNamespace(cell_of=nl["cell_of"])
+    out64 = sph.make_engine(gather_cfg("slowcellsh", "fp64")).compute(ss, der, grid, None, prm)
+    assert np.array_equal(out64.accel, ref["accel"]) and np.array_equal(out64.drho_dt, ref["drho_dt"])
+    assert np.array_equal(out64.visc_dt, ref["visc_dt"])
 
 
 @pytest.mark.slow
 @pytest.mark.parametrize("n_subdiv,cand", [(1, 16_164_890_622), (2, 9_401_964_162)])
 def test_c3_10m_counters_match_reference_measurement(n_subdiv, cand):
-    """C3 (10,200,478): the reference's own counts."""
-    _, _, _, _, out = _device_counters("c3", n_subdiv)
-    st = out.stats
+    """C3 (10,200,478 particles): the reference's own counts at its second step (SURVEY.md
+    Appendix A.9), reproduced by the bit-exact FP64 device trajectory.  (Lattice pairs sit
+    exactly on the 2h cutoff, so step-1 counts are only reproducible with bit-identical
+    step-0 motion.)"""
+    sc = sph.named_scenario("c3")
+    prm = sph.make_params(sc, n_subdiv=n_subdiv)
+    variant = "slowcellsh" if n_subdiv == 1 else "slowcellshalf"
+    _, stats = sph.run_simulation(sc, prm, gather_cfg(variant, "fp64"), max_steps=2,
+                                  stage_timing=False)
+    st = stats[1]
     assert st.true_pairs == 1_210_590_160
     assert st.force_evals == 2_421_180_320
     assert st.ff_force_evals == 2_373_133_760
     assert st.candidate_pairs == cand
-    assert np.isfinite(out.accel).all()
