@@ -91,7 +91,8 @@ typedef struct {
   uint64_t counters[4];  /* running step: candidates, ordered hits, evals, ff evals */
   int32_t active;        /* 1 while no error and no stop rule fired */
   uint32_t tile_next[2]; /* dynamic work counters of the interaction launches (reset per step) */
-  int32_t pad_[13];
+  uint32_t nblk[2];      /* target blocks built for the fluid / boundary interaction passes */
+  int32_t pad_[11];
 } sphb_ctrl_t;
 
 /* Per-step record written at the end of every step (StepStats, model.py:176-212). */
@@ -158,7 +159,8 @@ int sphb_cell_ranges_from_sorted(sphb_workspace_t* ws, const sphb_grid_t* grid,
  * kernels.py:500-596), plus the compute_dt reductions (sim.py:215-232) in the epilogue.
  * acc: (n,3) f64 (boundary rows 0), drho: (n) f64, visc: (n) f64 (ForceOutput, config.py:94-103).
  * Raw counters and the two dt minima accumulate into ctrl. */
-int sphb_interact(const sphb_params_t* prm, const sphb_grid_t* grid, int64_t n, int64_t nb,
+int sphb_interact(sphb_workspace_t* ws, const sphb_params_t* prm, const sphb_grid_t* grid,
+                  int64_t n, int64_t nb,
                   const void* posp, const void* velr, const void* aux, const int32_t* cell_sorted,
                   const int32_t* beg, const int32_t* end, double* acc, double* drho, double* visc,
                   sphb_ctrl_t* ctrl, sphb_stream_t s);

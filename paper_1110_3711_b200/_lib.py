@@ -44,7 +44,7 @@ class StateDesc(ctypes.Structure):
 CTRL_DTYPE = np.dtype([("step", "<i8"), ("max_steps", "<i8"), ("t_sim", "<f8"), ("t_end", "<f8"),
                        ("dt", "<f8"), ("dtmin_f", "<u8"), ("dtmin_cv", "<u8"), ("err", "<u8"),
                        ("counters", "<u8", (4,)), ("active", "<i4"), ("tile_next", "<u4", (2,)),
-                       ("pad_", "<i4", (13,))])
+                       ("nblk", "<u4", (2,)), ("pad_", "<i4", (11,))])
 CTRL_BYTES = 256
 assert CTRL_DTYPE.itemsize <= CTRL_BYTES
 REC_DTYPE = np.dtype([("dt", "<f8"), ("candidate_pairs", "<u8"), ("hits_ordered", "<u8"),
@@ -92,7 +92,7 @@ def lib():
         "sphb_reorder": ([P, P, c_i64, P, P, P, P, P, P, P, P, P, P, P, P, P, P], c_i32),
         "sphb_cell_ranges": ([P, P, P, P, P, P], c_i32),
         "sphb_cell_ranges_from_sorted": ([P, P, P, c_i64, c_i64, P, P, P], c_i32),
-        "sphb_interact": ([P, P, c_i64, c_i64, P, P, P, P, P, P, P, P, P, P, P], c_i32),
+        "sphb_interact": ([P, P, P, c_i64, c_i64, P, P, P, P, P, P, P, P, P, P, P], c_i32),
         "sphb_step_begin": ([P, P], c_i32),
         "sphb_integrate": ([P, P, P, c_i64, c_i64, P, P, P, P, P, P, P, P, P, P, P, P, P], c_i32),
         "sphb_step_end": ([P, P, P, c_i64, P], c_i32),

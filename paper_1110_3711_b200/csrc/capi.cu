@@ -81,6 +81,10 @@ int sphb_workspace_create(int64_t n_max, int64_t ncells_max, sphb_workspace_t** 
   if (e == cudaSuccess) e = alloc((void**)&ws->digit_total, sizeof(uint32_t) * RADIX);
   if (e == cudaSuccess)
     e = alloc((void**)&ws->scan_partials, sizeof(uint32_t) * (ws->max_scan_tiles + 1));
+  // a block never spans two cell rows and holds >= 1 target: #blocks <= n/BT + n
+  ws->max_blocks = n1 + n1 / 64 + 16;
+  for (int k = 0; k < 2 && e == cudaSuccess; ++k)
+    e = alloc((void**)&ws->blocks[k], sizeof(int2) * ws->max_blocks);
   if (e == cudaSuccess) e = cudaMemset(ws->cnt, 0, sizeof(uint32_t) * 2 * ncells_max);
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
   ws->bytes = bytes;
@@ -102,6 +106,8 @@ int sphb_workspace_destroy(sphb_workspace_t* ws) {
   cudaFree(ws->radix_hist);
   cudaFree(ws->digit_total);
   cudaFree(ws->scan_partials);
+  cudaFree(ws->blocks[0]);
+  cudaFree(ws->blocks[1]);
   delete ws;
   return SPHB_OK;
 }
@@ -193,14 +199,17 @@ int sphb_cell_ranges_from_sorted(sphb_workspace_t* ws, const sphb_grid_t* grid,
   return launch_cell_ranges(ws, *grid, beg, end, nullptr, (cudaStream_t)s);
 }
 
-int sphb_interact(const sphb_params_t* prm, const sphb_grid_t* grid, int64_t n, int64_t nb,
+int sphb_interact(sphb_workspace_t* ws, const sphb_params_t* prm, const sphb_grid_t* grid,
+                  int64_t n, int64_t nb,
                   const void* posp, const void* velr, const void* aux, const int32_t* cell_sorted,
                   const int32_t* beg, const int32_t* end, double* acc, double* drho, double* visc,
                   sphb_ctrl_t* ctrl, sphb_stream_t s) {
+  SPHB_NONNULL(ws);
   SPHB_NONNULL(prm);
   SPHB_NONNULL(ctrl);
   if (int rc = check_grid(grid)) return rc;
   if (n < 0 || nb < 0 || nb > n) return sphb_set_error(SPHB_E_INVALID, "bad n/nb");
+  if (n > ws->n_max) return sphb_set_error(SPHB_E_CAPACITY, "n exceeds workspace");
   if (prm->precision != SPHB_FP32 && prm->precision != SPHB_FP64)
     return sphb_set_error(SPHB_E_INVALID, "precision must be SPHB_FP32 or SPHB_FP64");
   if (n == 0) return SPHB_OK;
@@ -213,7 +222,7 @@ int sphb_interact(const sphb_params_t* prm, const sphb_grid_t* grid, int64_t n, 
   SPHB_NONNULL(acc);
   SPHB_NONNULL(drho);
   SPHB_NONNULL(visc);
-  return launch_interact(*prm, *grid, n, nb, (const float4*)posp, (const float4*)velr,
+  return launch_interact(ws, *prm, *grid, n, nb, (const float4*)posp, (const float4*)velr,
                          (const float4*)aux, cell_sorted, beg, end, acc, drho, visc, ctrl,
                          (cudaStream_t)s);
 }
@@ -268,7 +277,7 @@ int sphb_step(sphb_workspace_t* ws, const sphb_params_t* prm, const sphb_grid_t*
                            (float4*)st->aux, st->cell_s, ctrl, cs)))
     return rc;
   if ((rc = launch_cell_ranges(ws, *grid, st->beg, st->end, ctrl, cs))) return rc;
-  if ((rc = launch_interact(*prm, *grid, n, nb, (const float4*)st->posp_s,
+  if ((rc = launch_interact(ws, *prm, *grid, n, nb, (const float4*)st->posp_s,
                             (const float4*)st->velr_s, (const float4*)st->aux, st->cell_s, st->beg,
                             st->end, st->acc, st->drho, st->visc, ctrl, cs)))
     return rc;

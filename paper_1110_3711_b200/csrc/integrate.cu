@@ -40,6 +40,7 @@ __global__ void k_ctrl_init(sphb_ctrl_t* c, int64_t max_steps, double t_end) {
   for (int k = 0; k < 4; ++k) c->counters[k] = 0;
   c->active = 1;
   c->tile_next[0] = c->tile_next[1] = 0;
+  c->nblk[0] = c->nblk[1] = 0;
 }
 
 __global__ void k_step_begin(sphb_ctrl_t* c) {
@@ -52,6 +53,7 @@ __global__ void k_step_begin(sphb_ctrl_t* c) {
   c->dtmin_cv = (uint64_t)__double_as_longlong(INFINITY);
   for (int k = 0; k < 4; ++k) c->counters[k] = 0;
   c->tile_next[0] = c->tile_next[1] = 0;
+  c->nblk[0] = c->nblk[1] = 0;
 }
 
 __global__ void __launch_bounds__(256) k_integrate(

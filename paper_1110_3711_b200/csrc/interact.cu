@@ -5,28 +5,32 @@
 // boundary pass (gather_boundary_cells / _ranges, kernels.py:500-596), with the
 // compute_dt reductions (sim.py:215-232) fused into the epilogue (K6).
 //
-// Work decomposition (FP32 CUDA cores; the pair math is a data-dependent gather-reduce,
-// not a dense contraction, so no tensor cores):
-//   * one warp owns 32 consecutive cell-sorted target particles (one per lane); warps pull
-//     32-target tiles dynamically (atomic tile counter) until the list is exhausted;
-//   * lanes are grouped by their cell's (y, z) row; for each of the (2r+1)^2 stencil rows a
-//     group walks the UNION of its lanes' x-ranges, which is one contiguous particle range
-//     because cells are x-fastest (grid.py:1-8).  No per-candidate range test is needed:
-//     a sure FP32 hit lies strictly inside 2h, hence inside the lane's own stencil;
-//   * candidates are staged 32 at a time into shared memory with one coalesced float4 load
-//     and broadcast to every lane (LDS.128 broadcast); the screen is branch-free
-//     (r2 < sup2*(1+1e-5)) and produces one 32-bit "maybe" mask per lane per chunk;
-//   * mask words are queued per lane in shared memory (a whole tile's worth), then drained
-//     once in lock-step: every lane pops its next candidate (FIFO == candidate order ==
-//     the reference's accumulation order) and evaluates it -- the device analogue of the
-//     reference's pack-of-4 lane batching (kernels.py:97-118), so the ~15-25% hit rate
-//     costs no divergence in the pair math;
-//   * maybes that are not sure hits (inside the 1e-5 guard band around the cutoff, or
-//     r2 ~ 0 -- e.g. the particle itself) are re-decided in the drain with the reference's
-//     exact f64 predicate, so hit sets -- hence true_pairs / force_evals / ff counters --
-//     are bit-exact (SURVEY.md §8(a') "Neighbour predicate");
-//   * the FP64 instantiation uses the exact predicate in the screen and the reference's
-//     exact operation order in the pair math: bit-identical forces.
+// Decomposition (FP32 CUDA cores: the pair math is a data-dependent gather-reduce, not a
+// dense contraction, so tensor cores do not apply):
+//   * k_blocks cuts every (y, z) cell row of a particle list into blocks of <= 128
+//     consecutive cell-sorted targets.  Because cells are x-fastest (grid.py:1-8), a
+//     block's candidate set is, per stencil row, ONE contiguous particle range
+//     [beg(cx_first - r), end(cx_last + r)).
+//   * k_interact is persistent: two 4-warp CTAs per SM pull blocks dynamically.  The CTA
+//     stages the block's whole candidate set into shared memory once (32 B/candidate:
+//     x, y, z, prrho | vx, vy, vz, +-rho; the sign of rho marks the boundary list, cs and
+//     the tensile factor are recomputed in-loop), so every pair reads SMEM, not L2 -- each
+//     particle is fetched from L2 by ~13 blocks per step instead of by its ~250 neighbours.
+//   * Each warp owns 32 targets (one per lane) and screens the sub-range of every staged
+//     row that its lanes' stencils cover: LDS.128 broadcast + 6 FP32 ops + one compare per
+//     candidate, giving a 32-bit "maybe" mask per lane per 32 candidates
+//     (r2 < sup2 (1 + 1e-5)).
+//   * Each lane queues its non-empty mask words (a block's worth) and the warp drains them
+//     in lock-step, two candidates per lane per iteration with straight-line, masked pair
+//     math: each lane pops its next candidates (FIFO == candidate order == the reference's
+//     accumulation order), so the ~15-25% hit rate costs no divergence in the pair math --
+//     the device analogue of the reference's pack-of-4 lane batching (kernels.py:97-118).
+//   * Maybes that are not sure hits (inside the 1e-5 guard band around the cutoff, or
+//     r2 ~ 0 such as the particle itself) are re-decided in the drain with the
+//     reference's exact f64 predicate and stencil bounds, so hit sets -- hence
+//     true_pairs / force_evals / ff counters -- are bit-exact (SURVEY.md §8(a')).
+//   * The FP64 instantiation screens with the exact predicate and evaluates in the
+//     reference's exact operation order: bit-identical forces.
 #include <climits>
 
 #include "sphb_common.cuh"
@@ -36,25 +40,72 @@ using namespace sphb;
 
 namespace {
 
-constexpr int IW = 4;     // warps per block
-constexpr int RING = 64;  // queued 32-candidate chunks per warp (covers a whole tile)
+constexpr int NW = 4;            // warps per CTA (two CTAs per SM)
+constexpr int BT = NW * 32;      // targets per block
+constexpr int RING = 40;         // per-lane FIFO entries (non-empty 32-candidate mask words)
+constexpr int MAXSEG = 128;      // stencil row segments per block (2 lists x (2r+1)^2, r <= 3)
+
+template <typename R>
+struct Cfg;
+template <>
+struct Cfg<float> {
+  static constexpr int SCAP = 2304;  // staged candidates (A, B float4)
+  static constexpr int NARR = 2;
+};
+template <>
+struct Cfg<double> {
+  static constexpr int SCAP = 1024;  // staged candidates (A, B, C float4)
+  static constexpr int NARR = 3;
+};
 
 struct KArgs {
   sphb_params_t p;
   sphb_grid_t g;
-  int64_t n, nb, item_lo, item_hi, ncells;
+  int64_t n, nb, ncells;
   const float4* __restrict__ posp;
   const float4* __restrict__ velr;
   const float4* __restrict__ aux;
   const int32_t* __restrict__ cell;
   const int32_t* __restrict__ beg;
   const int32_t* __restrict__ end;
+  const int2* __restrict__ blocks;
   double* __restrict__ acc;
   double* __restrict__ drho;
   double* __restrict__ visc;
   sphb_ctrl_t* ctrl;
   // FP32 constants
-  float sup2_lo, sup2_hi, tiny, h, invh, k_gc, k_tw, eta2, alpha, massf, massb;
+  float sup2_lo, sup2_hi, tiny, h, invh, k_gc, k_tw, eta2, alpha, massf, massb, k_cs, cs_exp;
+  int gamma7;
+};
+
+// FP32 constants of the pair loop, pinned in registers (an opaque move stops the compiler
+// from re-loading them from the parameter bank inside the hot loop).
+struct C32 {
+  float sup2_lo, sup2_hi, tiny, h, invh, k_gc, k_tw, eta2, nalpha, massf, massb, k_cs, cs_exp;
+};
+__device__ __forceinline__ float pin(float v) {
+  float r;
+  asm volatile("mov.b32 %0, %1;" : "=f"(r) : "f"(v));
+  return r;
+}
+__device__ __forceinline__ uint32_t pin_u32(uint32_t v) {
+  uint32_t r;
+  asm volatile("mov.b32 %0, %1;" : "=r"(r) : "r"(v));
+  return r;
+}
+__device__ __forceinline__ C32 pin_constants(const KArgs& a) {
+  C32 c;
+  c.sup2_lo = pin(a.sup2_lo); c.sup2_hi = pin(a.sup2_hi); c.tiny = pin(a.tiny);
+  c.h = pin(a.h); c.invh = pin(a.invh); c.k_gc = pin(a.k_gc); c.k_tw = pin(a.k_tw);
+  c.eta2 = pin(a.eta2); c.nalpha = pin(-a.alpha); c.massf = pin(a.massf);
+  c.massb = pin(a.massb); c.k_cs = pin(a.k_cs); c.cs_exp = pin(a.cs_exp);
+  return c;
+}
+
+struct Seg {
+  int g0, g1;   // global particle range of the block's union for this stencil row
+  int pos;      // start in the concatenated candidate sequence
+  int rowoff;   // offset of the row's first cell in beg/end (list offset included)
 };
 
 __device__ __forceinline__ bool step_live(const sphb_ctrl_t* c) {
@@ -70,7 +121,42 @@ __device__ __forceinline__ bool exact_hit(double xi, double yi, double zi, doubl
   return r2 < sup2 && r2 > 0.0;
 }
 
-// ------------------------------------------------------------------ per-precision traits
+// x cell of a coordinate, exactly as assign_cells computes it (grid.py:87-89)
+__device__ __forceinline__ int xcell_of(float x, const sphb_grid_t& g) {
+  double f = floor(xdiv(xsub((double)x, g.origin[0]), g.cell_size));
+  int v = (int)f;
+  return v < g.dims[0] - 1 ? v : g.dims[0] - 1;
+}
+
+// Explicit 32-bit shared-window addressing: keeps the address arithmetic to one IMAD per
+// access (the compiler otherwise rematerialises the window base for every dynamic index).
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ float4 lds4(uint32_t addr) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ uint32_t lds32(uint32_t addr) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ uint32_t lds16(uint32_t addr) {
+  uint16_t v;
+  asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ void sts32(uint32_t addr, uint32_t v) {
+  asm volatile("st.shared.u32 [%0], %1;" ::"r"(addr), "r"(v));
+}
+__device__ __forceinline__ void sts16(uint32_t addr, uint32_t v) {
+  asm volatile("st.shared.u16 [%0], %1;" ::"r"(addr), "h"((uint16_t)v));
+}
+
 template <typename R>
 struct Own {
   R x, y, z, vx, vy, vz, rho, prrho, cs, ten;
@@ -81,44 +167,57 @@ struct Accum {
   R ax, ay, az, dr, vd;
 };
 
-// FP32 pair evaluation (physics.py:183-220 restated for FP32 CUDA cores).  dx, r2 come
-// from the caller.  Folded constants: k_gc = kc/h, k_tw = kc/W(dp); the 0.5 factors of the
-// viscous term cancel; the neighbour's list mass travels in aux.w.
-__device__ __forceinline__ void pair_eval(const KArgs& a, const Own<float>& o, float dx, float dy,
-                                          float dz, float r2, const float4& vj, const float4& xa,
-                                          Accum<float>& s) {
+// ------------------------------------------------------------------ pair math
+// FP32 (physics.py:183-220 restated for FP32 CUDA cores).  Branch-free cubic spline:
+// W ~ t^3/4 - u^3, dW/dq ~ -3/4 t^2 + 3 u^2 with t = 2 - q, u = max(1 - q, 0).
+// Folded constants: k_gc = kc/h, k_tw = kc/W(dp); the viscous 0.5 factors cancel.
+template <bool G7, bool EQM>
+__device__ __forceinline__ void pair_eval32(const C32& a, const Own<float>& o, float dx,
+                                            float dy, float dz, float r2in, const float4& A,
+                                            const float4& B, bool ok, Accum<float>& s) {
+  const float r2 = ok ? r2in : a.sup2_lo;  // masked slots stay finite; their terms are zeroed
   const float rinv = rsqrtf(r2);
-  const float r = r2 * rinv;
-  const float q = r * a.invh;
+  const float q = r2 * rinv * a.invh;
   const float t = 2.0f - q;
-  const float t2 = t * t;
-  const float q2 = q * q;
-  const bool inner = q < 1.0f;
-  const float w = inner ? fmaf(0.75f * q, q2, fmaf(-1.5f, q2, 1.0f)) : 0.25f * t2 * t;
-  const float dw = inner ? fmaf(2.25f, q, -3.0f) * q : -0.75f * t2;
+  const float u = fmaxf(1.0f - q, 0.0f);
+  const float t2 = t * t, u2 = u * u;
+  const float w = fmaf(0.25f * t2, t, -u2 * u);
+  const float dw = fmaf(3.0f, u2, -0.75f * t2);
   const float gc = dw * a.k_gc * rinv;
-  const float dvx = o.vx - vj.x, dvy = o.vy - vj.y, dvz = o.vz - vj.z;
+  const float rho_j = fabsf(B.w);
+  const float mj = EQM ? 1.0f : (B.w < 0.0f ? a.massb : a.massf);  // EQM: mass applied once
+  const float prrho_j = A.w;
+  float cs_j;
+  if (G7) {  // gamma = 7: cs = c0 (rho/rho0)^3
+    const float rr = rho_j * a.k_cs;  // (rho/rho0) * c0^(1/3)
+    cs_j = rr * rr * rr;
+  } else {
+    cs_j = a.k_cs * exp2f(a.cs_exp * __log2f(rho_j));
+  }
+  const float ten_j = prrho_j * (prrho_j > 0.0f ? 0.01f : -0.2f);
+  const float dvx = o.vx - B.x, dvy = o.vy - B.y, dvz = o.vz - B.z;
   const float dot = fmaf(dvz, dz, fmaf(dvy, dy, dvx * dx));
   const float mu = __fdividef(a.h * dot, r2 + a.eta2);
-  const float vterm = __fdividef(-a.alpha * (o.cs + xa.y) * mu, o.rho + vj.w);
+  const float vterm = __fdividef(a.nalpha * (o.cs + cs_j) * mu, o.rho + rho_j);
   const float visc = dot < 0.0f ? vterm : 0.0f;
   const float tw = w * a.k_tw;
   const float tw2 = tw * tw;
-  const float pterm = fmaf((o.ten + xa.z) * tw2, tw2, o.prrho + xa.x + visc);
-  const float mj = xa.w;
-  const float fm = mj * pterm * gc;
+  const float pterm = fmaf((o.ten + ten_j) * tw2, tw2, o.prrho + prrho_j + visc);
+  const float fm = ok ? (EQM ? pterm * gc : mj * pterm * gc) : 0.0f;
+  const float gd = ok ? (EQM ? gc : mj * gc) : 0.0f;
   s.ax = fmaf(-fm, dx, s.ax);
   s.ay = fmaf(-fm, dy, s.ay);
   s.az = fmaf(-fm, dz, s.az);
-  s.dr = fmaf(mj * gc, dot, s.dr);
-  s.vd = fmaxf(s.vd, fabsf(mu));
+  s.dr = fmaf(gd, dot, s.dr);
+  s.vd = fmaxf(s.vd, ok ? fabsf(mu) : 0.0f);
 }
 
-// FP64 pair evaluation: the reference's exact operation order (physics.py:196-220,
-// kernels.py:382-390), no contraction.  Bit-identical to numba.
-__device__ __forceinline__ void pair_eval(const KArgs& a, const Own<double>& o, double dx,
-                                          double dy, double dz, double r2, const float4& vj,
-                                          const float4& xa, double mj, Accum<double>& s) {
+// FP64: the reference's exact operation order (physics.py:196-220, kernels.py:382-390),
+// no contraction; cs and tensil are the exact f32 values of K3 (C.x, C.y).
+__device__ __forceinline__ void pair_eval64(const KArgs& a, const Own<double>& o, double dx,
+                                            double dy, double dz, double r2, const float4& A,
+                                            const float4& B, const float4& C,
+                                            Accum<double>& s) {
   const sphb_params_t& p = a.p;
   const double r = __dsqrt_rn(r2);
   const double q = xmul(r, p.invh);
@@ -133,20 +232,21 @@ __device__ __forceinline__ void pair_eval(const KArgs& a, const Own<double>& o, 
     dwdq = xmul(xmul(xmul(-0.75, kc), t), t);
   }
   const double gc = xdiv(xmul(dwdq, p.invh), r);
-  const double dvx = xsub(o.vx, (double)vj.x), dvy = xsub(o.vy, (double)vj.y),
-               dvz = xsub(o.vz, (double)vj.z);
+  const double dvx = xsub(o.vx, (double)B.x), dvy = xsub(o.vy, (double)B.y),
+               dvz = xsub(o.vz, (double)B.z);
   const double dot = xadd(xadd(xmul(dvx, dx), xmul(dvy, dy)), xmul(dvz, dz));
   const double mu = xdiv(xmul(p.h, dot), xadd(r2, p.eta2));
   double visc = 0.0;
   if (dot < 0.0) {
-    const double rho_j = (double)vj.w, cs_j = (double)xa.y;
+    const double rho_j = (double)fabsf(B.w), cs_j = (double)C.x;
     visc = xdiv(xmul(xmul(-p.alpha, xmul(0.5, xadd(o.cs, cs_j))), mu),
                 xmul(0.5, xadd(o.rho, rho_j)));
   }
   const double tw = xmul(wab, p.invwdp);
   const double tw2 = xmul(tw, tw);
-  const double pterm = xadd(xadd(xadd(o.prrho, (double)xa.x), visc),
-                            xmul(xmul(xadd(o.ten, (double)xa.z), tw2), tw2));
+  const double pterm = xadd(xadd(xadd(o.prrho, (double)A.w), visc),
+                            xmul(xmul(xadd(o.ten, (double)C.y), tw2), tw2));
+  const double mj = B.w < 0.0f ? p.mass_boundary : p.mass_fluid;
   const double pg = xmul(pterm, gc);
   s.ax = xsub(s.ax, xmul(mj, xmul(pg, dx)));
   s.ay = xsub(s.ay, xmul(mj, xmul(pg, dy)));
@@ -156,214 +256,368 @@ __device__ __forceinline__ void pair_eval(const KArgs& a, const Own<double>& o, 
   if (ma > s.vd) s.vd = ma;
 }
 
-template <typename R>
-struct Stage;
-template <>
-struct Stage<float> {
-  float4 v;
-};
-template <>
-struct Stage<double> {
-  double x, y, z, pad;
-};
-
-__device__ __forceinline__ void stage_store(Stage<float>* s, const float4& p) { s->v = p; }
-__device__ __forceinline__ void stage_store(Stage<double>* s, const float4& p) {
-  s->x = (double)p.x;
-  s->y = (double)p.y;
-  s->z = (double)p.z;
+// Evaluate staged candidate (A, B[, C]); false if a guard-band maybe is rejected.
+// Stencil x-bound of a candidate (y/z rows are the lane's own); out of line, it only runs
+// for exact hits within 1e-12 of the cutoff.
+__device__ __noinline__ bool in_stencil_x(float x, int xlo, int xhi, sphb_grid_t g) {
+  const int cxj = xcell_of(x, g);
+  return cxj >= xlo && cxj <= xhi;
 }
 
-// Candidate screen.  FP32: "maybe" = r2 < sup2*(1+1e-5); the drain re-decides the rare
-// maybes that are not sure hits (guard band, r2 ~ 0) exactly.  FP64: the exact predicate.
-__device__ __forceinline__ bool cand_maybe(const KArgs& a, const Own<float>& o,
-                                           const Stage<float>& c) {
-  const float dx = o.x - c.v.x, dy = o.y - c.v.y, dz = o.z - c.v.z;
-  const float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
-  return r2 < a.sup2_hi;
-}
-__device__ __forceinline__ bool cand_maybe(const KArgs& a, const Own<double>& o,
-                                           const Stage<double>& c) {
-  return exact_hit(o.x, o.y, o.z, c.x, c.y, c.z, a.p.sup2);
-}
-
-// Evaluate one queued candidate j; returns false if it was a maybe that the exact
-// predicate (or the stencil range) rejects.
-__device__ __forceinline__ bool eval_one(const KArgs& a, const Own<float>& o, int32_t j, int xlo,
-                                         int xhi, Accum<float>& s) {
-  const float4 pj = __ldg(&a.posp[j]);
-  const float4 vj = __ldg(&a.velr[j]);
-  const float4 xa = __ldg(&a.aux[j]);
-  const float dx = o.x - pj.x, dy = o.y - pj.y, dz = o.z - pj.z;
-  const float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
-  if (!(r2 < a.sup2_lo && r2 > a.tiny)) {
-    // cold path: exact f64 predicate + stencil x-range (the y/z rows are the lane's own)
-    const int cj = __ldg(&a.cell[j]);
-    const int cxj = cj % a.g.dims[0];
-    const bool ok = exact_hit((double)o.x, (double)o.y, (double)o.z, (double)pj.x, (double)pj.y,
-                              (double)pj.z, a.p.sup2) && cxj >= xlo && cxj <= xhi;
-    if (!ok) return false;
-  }
-  pair_eval(a, o, dx, dy, dz, r2, vj, xa, s);
-  return true;
-}
-__device__ __forceinline__ bool eval_one(const KArgs& a, const Own<double>& o, int32_t j, int,
-                                         int, Accum<double>& s) {
-  const float4 pj = __ldg(&a.posp[j]);
-  const float4 vj = __ldg(&a.velr[j]);
-  const float4 xa = __ldg(&a.aux[j]);
-  const double dx = xsub(o.x, (double)pj.x), dy = xsub(o.y, (double)pj.y),
-               dz = xsub(o.z, (double)pj.z);
+// Cold path of the FP32 screen: exact f64 predicate; a hit outside the lane's own stencil
+// x-range needs |dx| > 2h (1 - 1e-15), so the cell test only runs within 1e-12 of sup2.
+__device__ __forceinline__ bool cold_accept(const KArgs& a, float ox, float oy, float oz,
+                                            const float4 A, int xlo, int xhi) {
+  const double dx = xsub((double)ox, (double)A.x), dy = xsub((double)oy, (double)A.y),
+               dz = xsub((double)oz, (double)A.z);
   const double r2 = xadd(xadd(xmul(dx, dx), xmul(dy, dy)), xmul(dz, dz));
-  const double mj = j < a.nb ? a.p.mass_boundary : a.p.mass_fluid;
-  pair_eval(a, o, dx, dy, dz, r2, vj, xa, mj, s);
+  if (!(r2 < a.p.sup2 && r2 > 0.0)) return false;
+  if (r2 > a.p.sup2 * (1.0 - 1e-12)) return in_stencil_x(A.x, xlo, xhi, a.g);
   return true;
 }
 
-// ------------------------------------------------------------------ the kernel
-template <typename R, bool FLUID_ITEMS>
-__global__ void __launch_bounds__(IW * 32, sizeof(R) == 4 ? 6 : 3) k_interact(KArgs a) {
-  if (!step_live(a.ctrl)) return;
-  __shared__ Stage<R> s_stage[IW][32];
-  __shared__ uint32_t s_mask[IW][RING][32];  // per-lane hit bitmask of each queued chunk
-  __shared__ int32_t s_cbase[IW][RING];      // first candidate index of each queued chunk
+template <bool G7, bool EQM>
+__device__ __forceinline__ bool eval_one(const KArgs& a, const C32&, const Own<double>& o,
+                                         const float4& A,
+                                         const float4& B, const float4& C, int, int,
+                                         Accum<double>& s) {
+  const double dx = xsub(o.x, (double)A.x), dy = xsub(o.y, (double)A.y),
+               dz = xsub(o.z, (double)A.z);
+  const double r2 = xadd(xadd(xmul(dx, dx), xmul(dy, dy)), xmul(dz, dz));
+  pair_eval64(a, o, dx, dy, dz, r2, A, B, C, s);
+  return true;
+}
 
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t nitems = a.item_hi - a.item_lo;
-  const uint32_t ntiles = (uint32_t)((nitems + 31) / 32);
-  const int64_t step = a.ctrl->step;
+// Two queued candidates (staged indices k1, k2; < 0 = empty slot) for one lane.  The exact
+// re-decision of non-sure maybes is a rare divergent pre-pass; the pair math itself is
+// straight-line for both candidates (independent chains interleave) with masked terms.
+// Returns the number of rejected maybes; *rej_f counts the fluid-list ones.
+template <bool G7, bool EQM>
+__device__ __forceinline__ uint32_t eval_two(const KArgs& a, const C32& c, const Own<float>& o,
+                                             uint32_t smA, uint32_t smB, uint32_t, int k1, int k2,
+                                             int xlo, int xhi, Accum<float>& s, uint32_t* rej_f) {
+  const bool v1 = k1 >= 0, v2 = k2 >= 0;
+  const uint32_t i1 = v1 ? (uint32_t)k1 : 0u, i2 = v2 ? (uint32_t)k2 : 0u;
+  const float4 A1 = lds4(smA + 16u * i1), B1 = lds4(smB + 16u * i1);
+  const float4 A2 = lds4(smA + 16u * i2), B2 = lds4(smB + 16u * i2);
+  const float dx1 = o.x - A1.x, dy1 = o.y - A1.y, dz1 = o.z - A1.z;
+  const float dx2 = o.x - A2.x, dy2 = o.y - A2.y, dz2 = o.z - A2.z;
+  const float r21 = fmaf(dz1, dz1, fmaf(dy1, dy1, dx1 * dx1));
+  const float r22 = fmaf(dz2, dz2, fmaf(dy2, dy2, dx2 * dx2));
+  const bool f1 = r21 < c.sup2_lo && r21 > c.tiny, f2 = r22 < c.sup2_lo && r22 > c.tiny;
+  bool ok1 = v1 && f1, ok2 = v2 && f2;
+  if (v1 && !f1) ok1 = cold_accept(a, o.x, o.y, o.z, A1, xlo, xhi);
+  if (v2 && !f2) ok2 = cold_accept(a, o.x, o.y, o.z, A2, xlo, xhi);
+  pair_eval32<G7, EQM>(c, o, dx1, dy1, dz1, r21, A1, B1, ok1, s);
+  pair_eval32<G7, EQM>(c, o, dx2, dy2, dz2, r22, A2, B2, ok2, s);
+  const uint32_t r1 = (v1 && !ok1) ? 1u : 0u, r2 = (v2 && !ok2) ? 1u : 0u;
+  *rej_f += (r1 && B1.w > 0.0f ? 1u : 0u) + (r2 && B2.w > 0.0f ? 1u : 0u);
+  return r1 + r2;
+}
+template <bool G7, bool EQM>
+__device__ __forceinline__ uint32_t eval_two(const KArgs& a, const C32& c, const Own<double>& o,
+                                             uint32_t smA, uint32_t smB, uint32_t smC, int k1,
+                                             int k2, int xlo, int xhi, Accum<double>& s,
+                                             uint32_t* rej_f) {
+  (void)rej_f;
+  if (k1 >= 0)
+    eval_one<G7, EQM>(a, c, o, lds4(smA + 16u * k1), lds4(smB + 16u * k1), lds4(smC + 16u * k1),
+                      xlo, xhi, s);
+  if (k2 >= 0)
+    eval_one<G7, EQM>(a, c, o, lds4(smA + 16u * k2), lds4(smB + 16u * k2), lds4(smC + 16u * k2),
+                      xlo, xhi, s);
+  return 0u;
+}
+
+// candidate screen: FP32 "maybe" (r2 < sup2 (1 + 1e-5)); FP64 exact predicate
+__device__ __forceinline__ bool screen(const KArgs&, const C32& c, const Own<float>& o,
+                                       const float4& A) {
+  const float dx = o.x - A.x, dy = o.y - A.y, dz = o.z - A.z;
+  return fmaf(dz, dz, fmaf(dy, dy, dx * dx)) < c.sup2_hi;
+}
+__device__ __forceinline__ bool screen(const KArgs& a, const C32&, const Own<double>& o,
+                                       const float4& A) {
+  return exact_hit(o.x, o.y, o.z, (double)A.x, (double)A.y, (double)A.z, a.p.sup2);
+}
+
+// ------------------------------------------------------------------ block builder
+// Cuts each (y, z) cell row of the fluid list (and, for the boundary pass, of the
+// boundary list) into ceil(L / BT) balanced blocks of consecutive targets.
+__global__ void __launch_bounds__(256) k_blocks(sphb_grid_t g, int64_t ncells,
+                                                const int32_t* __restrict__ beg,
+                                                const int32_t* __restrict__ end,
+                                                int2* __restrict__ blk_f, int2* __restrict__ blk_b,
+                                                sphb_ctrl_t* ctrl) {
+  if (!step_live(ctrl)) return;
+  const int nx = g.dims[0];
+  const int64_t nrows = (int64_t)g.dims[1] * g.dims[2];
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < nrows;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c0 = r * nx;
+#pragma unroll
+    for (int li = 0; li < 2; ++li) {
+      const int64_t off = li == 0 ? ncells : 0;
+      const int32_t rb = beg[off + c0], re = end[off + c0 + nx - 1];
+      const int32_t L = re - rb;
+      if (L <= 0) continue;
+      const int32_t nbk = (L + BT - 1) / BT;
+      const uint32_t at = atomicAdd(&ctrl->nblk[li], (uint32_t)nbk);
+      int2* out = li == 0 ? blk_f : blk_b;
+      for (int32_t b = 0; b < nbk; ++b)
+        out[at + b] = make_int2(rb + (int32_t)(((int64_t)L * b) / nbk),
+                                rb + (int32_t)(((int64_t)L * (b + 1)) / nbk));
+    }
+  }
+}
+
+// ------------------------------------------------------------------ the interaction kernel
+extern __shared__ float4 g_sm4[];  // staged candidates: A | B | (C)
+extern __shared__ uint32_t g_sm32[];
+
+template <typename R, bool FLUID_ITEMS, bool G7, bool EQM>
+__global__ void __launch_bounds__(NW * 32, 2) k_interact(KArgs a) {
+  if (!step_live(a.ctrl)) return;
+  const C32 c32 = pin_constants(a);
+  constexpr int SCAP = Cfg<R>::SCAP;
+  constexpr int SB = SCAP, SC = 2 * SCAP;                  // float4 offsets of B and C
+  constexpr int MASK0 = 4 * Cfg<R>::NARR * SCAP;            // uint32 offset of the rings
+  uint32_t* sMask = g_sm32 + MASK0;                          // [NW][RING][32] mask words
+  uint16_t* sBase = reinterpret_cast<uint16_t*>(sMask + NW * RING * 32);  // [NW][RING][32]
+  __shared__ Seg sSeg[MAXSEG];
+  __shared__ int s_blk, s_nseg_tot, s_scan[MAXSEG];
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nx = a.g.dims[0], ny = a.g.dims[1], nz = a.g.dims[2];
-  const int reach = a.g.reach;
-  const int64_t nb = a.nb;
+  const int reach = a.g.reach, side = 2 * reach + 1;
+  const int nlist = FLUID_ITEMS ? 2 : 1;
+  const int nseg = nlist * side * side;
+  const uint32_t nblocks = a.ctrl->nblk[FLUID_ITEMS ? 0 : 1];
+  const int64_t step = a.ctrl->step;
+  const int2* blocks = a.blocks;
+  uint32_t* myMask = sMask + warp * RING * 32;
+  uint16_t* myBase = sBase + warp * RING * 32;
 
   unsigned long long c_cand = 0, c_hits = 0, c_ff = 0;
   double dtf_min = INFINITY, dtcv_min = INFINITY;
 
   for (;;) {
-    uint32_t tile = 0;
-    if (lane == 0) tile = atomicAdd(&a.ctrl->tile_next[FLUID_ITEMS ? 0 : 1], 1u);
-    tile = __shfl_sync(SPHB_FULL, tile, 0);
-    if (tile >= ntiles) break;
-    const int64_t i = a.item_lo + (int64_t)tile * 32 + lane;
-    const bool valid = i < a.item_hi;
+    if (tid == 0) s_blk = (int)atomicAdd(&a.ctrl->tile_next[FLUID_ITEMS ? 0 : 1], 1u);
+    __syncthreads();
+    const uint32_t blk = (uint32_t)s_blk;
+    if (blk >= nblocks) break;
+    const int2 bb = blocks[blk];
+    const int i0 = bb.x, i1 = bb.y;
+    const int cfirst = a.cell[i0], clast = a.cell[i1 - 1];
+    const int rowkey = cfirst / nx;
+    const int cxa = cfirst - rowkey * nx, cxb = clast - rowkey * nx;
+    const int gcz = rowkey / ny, gcy = rowkey - gcz * ny;
+    const int bxlo = max(cxa - reach, 0), bxhi = min(cxb + reach, nx - 1);
+
+    // ---- stencil row segments in the reference's traversal order + their prefix
+    if (tid < MAXSEG) {
+      int len = 0;
+      Seg sg = {0, 0, 0, 0};
+      if (tid < nseg) {
+        int li, rr;
+        if (FLUID_ITEMS && a.p.order == 1) {  // gather_fluid_ranges: all F rows, then all B rows
+          li = tid / (side * side);
+          rr = tid - li * side * side;
+        } else {                              // gather_*_cells: per row F then B
+          li = tid % nlist;
+          rr = tid / nlist;
+        }
+        const int dz = rr / side - reach, dy = rr % side - reach;
+        const int zz = gcz + dz, yy = gcy + dy;
+        if (zz >= 0 && zz < nz && yy >= 0 && yy < ny) {
+          const int64_t rowoff = (li == 0 ? a.ncells : 0) + (int64_t)nx * (yy + (int64_t)ny * zz);
+          sg.g0 = a.beg[rowoff + bxlo];
+          sg.g1 = a.end[rowoff + bxhi];
+          sg.rowoff = (int)rowoff;  // < 2^31 (ncells < 2^30)
+          len = max(sg.g1 - sg.g0, 0);
+          if (len == 0) sg.g1 = sg.g0;
+        }
+      }
+      s_scan[tid] = len;
+      sSeg[tid] = sg;
+    }
+    __syncthreads();
+    if (warp == 0) {  // exclusive scan of MAXSEG (=128) lengths, 4 per lane
+      int v[4], run = 0;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        v[k] = s_scan[lane * 4 + k];
+        run += v[k];
+      }
+      int incl = run;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        int y = __shfl_up_sync(SPHB_FULL, incl, o);
+        if (lane >= o) incl += y;
+      }
+      int ex = incl - run;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        sSeg[lane * 4 + k].pos = ex;
+        ex += v[k];
+      }
+      if (lane == 31) s_nseg_tot = incl;
+    }
+    __syncthreads();
+    const int total = s_nseg_tot;
+
+    // ---- this warp's targets
+    const int i = i0 + warp * 32 + lane;
+    const bool valid = i < i1;
+    const bool wactive = (i0 + warp * 32) < i1;
     Own<R> o;
-    int cx = 0, rowkey = -1;
+    int xlo = 0, xhi = -1;
     if (valid) {
       const float4 pi = a.posp[i], vi = a.velr[i], xi = a.aux[i];
       o.x = (R)pi.x; o.y = (R)pi.y; o.z = (R)pi.z;
       o.vx = (R)vi.x; o.vy = (R)vi.y; o.vz = (R)vi.z; o.rho = (R)vi.w;
       o.prrho = (R)xi.x; o.cs = (R)xi.y; o.ten = (R)xi.z;
-      const int c = a.cell[i];
-      rowkey = c / nx;
-      cx = c - rowkey * nx;
+      const int cxi = a.cell[i] - rowkey * nx;
+      xlo = max(cxi - reach, 0);
+      xhi = min(cxi + reach, nx - 1);
     } else {
       o.x = o.y = o.z = o.vx = o.vy = o.vz = o.prrho = o.cs = o.ten = (R)0;
       o.rho = (R)1;
     }
-    const int xlo = max(cx - reach, 0), xhi = min(cx + reach, nx - 1);
+    const int wxlo = __reduce_min_sync(SPHB_FULL, valid ? xlo : INT_MAX);
+    const int wxhi = __reduce_max_sync(SPHB_FULL, valid ? xhi : INT_MIN);
     Accum<R> s = {(R)0, (R)0, (R)0, (R)0, (R)0};
-    uint32_t nslot = 0;        // queued chunks (warp-uniform)
-    uint32_t pend = 0;         // queued candidate bits of this lane
-    uint32_t pushed = 0, pushed_b = 0, rej = 0, rej_f = 0;
+    uint32_t tail = 0, pend = 0, pushed = 0, pushed_b = 0, rej = 0, rej_f = 0;
     unsigned long long cand = 0;
+    if (valid) {  // candidate count = sum of this lane's row-range lengths
+      for (int k = 0; k < nseg; ++k) {
+        const Seg sg = sSeg[k];
+        if (sg.g1 <= sg.g0) continue;
+        cand += (unsigned long long)(a.end[sg.rowoff + xhi] - a.beg[sg.rowoff + xlo]);
+      }
+      if (FLUID_ITEMS) cand -= 1;  // the reference skips j == i before counting (kernels.py:369-371)
+    }
 
-    // Evaluate every queued candidate, FIFO per lane, lock-step across the warp.
+    // Lock-step FIFO drain.  Each lane queued only its non-empty mask words (with the staged
+    // index of the word's first candidate), so a pop refills at most once and never loops.
+    const uint32_t smA = pin_u32(smem_addr(g_sm4)), smB = pin_u32(smA + 16u * SB);
+    const uint32_t smC = pin_u32(smA + 16u * SC);
+    const uint32_t smMask = pin_u32(smem_addr(myMask) + 4u * lane);
+    const uint32_t smBase = pin_u32(smem_addr(myBase) + 2u * lane);
     auto drain = [&]() {
       __syncwarp();
       const uint32_t mx = __reduce_max_sync(SPHB_FULL, pend);
-      uint32_t sl = 0;
-      uint32_t cur = nslot ? s_mask[warp][0][lane] : 0u;
-      for (uint32_t it = 0; it < mx; ++it) {
-        while (cur == 0u && sl + 1 < nslot) cur = s_mask[warp][++sl][lane];
-        if (cur) {
-          const int t = __ffs(cur) - 1;
-          cur &= cur - 1u;
-          const int32_t j = s_cbase[warp][sl] + t;
-          if (!eval_one(a, o, j, xlo, xhi, s)) {
-            ++rej;
-            if (j >= nb) ++rej_f;
-          }
+      uint32_t head = 0, cur = 0;
+      int cbase = 0;
+      auto pop = [&]() -> int {
+        if (cur == 0u && head < tail) {
+          cur = lds32(smMask + 128u * head);
+          cbase = (int)lds16(smBase + 64u * head);
+          ++head;
         }
+        const int t = __ffs(cur) - 1;  // -1 when empty
+        cur &= cur - 1u;
+        return t < 0 ? -1 : cbase + t;
+      };
+      for (uint32_t it = 0; it < mx; it += 2) {
+        const int k1 = pop();
+        const int k2 = pop();
+        rej += eval_two<G7, EQM>(a, c32, o, smA, smB, smC, k1, k2, xlo, xhi, s, &rej_f);
       }
-      nslot = 0;
+      tail = 0;
       pend = 0;
       __syncwarp();
     };
 
-    uint32_t todo = __ballot_sync(SPHB_FULL, valid);
-    while (todo) {
-      const int leader = __ffs(todo) - 1;
-      const int key = __shfl_sync(SPHB_FULL, rowkey, leader);
-      const uint32_t grp = __ballot_sync(SPHB_FULL, valid && rowkey == key);
-      todo &= ~grp;
-      const bool ing = (grp >> lane) & 1u;
-      const int gxlo = __reduce_min_sync(SPHB_FULL, ing ? xlo : INT_MAX);
-      const int gxhi = __reduce_max_sync(SPHB_FULL, ing ? xhi : INT_MIN);
-      const int gcz = key / ny, gcy = key - gcz * ny;
-      const int npass = (FLUID_ITEMS && a.p.order == 1) ? 2 : 1;
-      for (int pass = 0; pass < npass; ++pass) {
-        for (int dz = -reach; dz <= reach; ++dz) {
-          const int zz = gcz + dz;
-          if (zz < 0 || zz >= nz) continue;
-          for (int dy = -reach; dy <= reach; ++dy) {
-            const int yy = gcy + dy;
-            if (yy < 0 || yy >= ny) continue;
-            const int64_t base = (int64_t)nx * (yy + (int64_t)ny * zz);
-#pragma unroll 1
-            for (int li = 0; li < 2; ++li) {
-              const bool fluid_list = li == 0;  // li 1: boundary list
-              if (!fluid_list && !FLUID_ITEMS) continue;
-              if (npass == 2 && (pass == 0) != fluid_list) continue;
-              const int64_t off = fluid_list ? a.ncells : 0;
-              const int32_t u0 = a.beg[off + base + gxlo];
-              const int32_t u1 = a.end[off + base + gxhi];
-              if (u1 <= u0) continue;
-              if (ing) cand += (unsigned long long)(a.end[off + base + xhi] - a.beg[off + base + xlo]);
-              for (int32_t j0 = u0; j0 < u1; j0 += 32) {
-                const int32_t jj = j0 + lane;
-                const float4 pc = jj < u1 ? __ldg(&a.posp[jj])
-                                          : make_float4(INFINITY, INFINITY, INFINITY, 0.f);
-                stage_store(&s_stage[warp][lane], pc);
-                __syncwarp();
-                uint32_t bits = 0;
+    // ---- batches of <= SCAP staged candidates (normally one)
+    for (int q0 = 0; q0 < total; q0 += SCAP) {
+      const int q1 = min(q0 + SCAP, total);
+      // stage [q0, q1): thread-strided, monotone segment cursor
+      {
+        int sk = 0;
+        for (int p = q0 + tid; p < q1; p += NW * 32) {
+          while (sSeg[sk].pos + (sSeg[sk].g1 - sSeg[sk].g0) <= p) ++sk;
+          const Seg sg = sSeg[sk];
+          const int j = sg.g0 + (p - sg.pos);
+          const float4 pp = __ldg(&a.posp[j]);
+          const float4 vr = __ldg(&a.velr[j]);
+          const float4 xa = __ldg(&a.aux[j]);
+          const bool boundary_list = sg.rowoff < a.ncells;
+          g_sm4[p - q0] = make_float4(pp.x, pp.y, pp.z, xa.x);
+          g_sm4[SB + p - q0] = make_float4(vr.x, vr.y, vr.z, boundary_list ? -vr.w : vr.w);
+          if (sizeof(R) == 8) g_sm4[SC + p - q0] = make_float4(xa.y, xa.z, 0.f, 0.f);
+        }
+      }
+      __syncthreads();
+      if (wactive) {
+        for (int k = 0; k < nseg; ++k) {
+          const Seg sg = sSeg[k];
+          const int len = sg.g1 - sg.g0;
+          if (len <= 0 || sg.pos >= q1 || sg.pos + len <= q0) continue;
+          // this warp's part of the row: cells [wxlo, wxhi]
+          const int wg0 = a.beg[sg.rowoff + wxlo], wg1 = a.end[sg.rowoff + wxhi];
+          const int lo = max(sg.pos + (wg0 - sg.g0), q0) - q0;
+          const int hi = min(sg.pos + (wg1 - sg.g0), q1) - q0;
+          if (hi <= lo) continue;
+          const bool boundary_list = sg.rowoff < a.ncells;
+          int la = 0, lb = 0;  // FP64: this lane's own stencil range, staged coordinates
+          if (sizeof(R) == 8 && valid) {
+            la = sg.pos + (a.beg[sg.rowoff + xlo] - sg.g0) - q0;
+            lb = sg.pos + (a.end[sg.rowoff + xhi] - sg.g0) - q0;
+          }
+          for (int k0 = lo; k0 < hi; k0 += 32) {
+            uint32_t bits = 0;
+            const uint32_t sk = smA + 16u * k0;
 #pragma unroll
-                for (int t = 0; t < 32; ++t)
-                  if (cand_maybe(a, o, s_stage[warp][t])) bits |= 1u << t;
-                bits = ing ? bits : 0u;
-                __syncwarp();
-                if (__any_sync(SPHB_FULL, bits != 0u)) {
-                  if (nslot == RING) drain();
-                  s_mask[warp][nslot][lane] = bits;
-                  if (lane == 0) s_cbase[warp][nslot] = j0;
-                  ++nslot;
-                  const uint32_t pc2 = __popc(bits);
-                  pend += pc2;
-                  pushed += pc2;
-                  if (!fluid_list) pushed_b += pc2;
-                }
-              }
+            for (int t = 0; t < 32; ++t) {
+              const float4 A = lds4(sk + 16u * t);  // reads past hi stay inside shared memory
+              if (screen(a, c32, o, A)) bits |= 1u << t;
+            }
+            const int nvalid = hi - k0;
+            if (nvalid < 32) bits &= (1u << nvalid) - 1u;
+            if (sizeof(R) == 8) {  // exact stencil bounds for the FP64 (no guard band) path
+              const int d0 = la - k0, d1 = lb - k0;
+              const uint32_t m0 = d0 <= 0 ? 0xffffffffu : (d0 >= 32 ? 0u : (0xffffffffu << d0));
+              const uint32_t m1 = d1 >= 32 ? 0xffffffffu : (d1 <= 0 ? 0u : ((1u << d1) - 1u));
+              bits &= m0 & m1;
+            }
+            bits = valid ? bits : 0u;
+            if (__any_sync(SPHB_FULL, bits != 0u && tail == (uint32_t)RING)) drain();
+            if (bits) {
+              sts32(smMask + 128u * tail, bits);
+              sts16(smBase + 64u * tail, (uint32_t)k0);
+              ++tail;
+              const uint32_t pc = __popc(bits);
+              pend += pc;
+              pushed += pc;
+              if (boundary_list) pushed_b += pc;
             }
           }
         }
+        drain();
       }
+      __syncthreads();  // staging buffer reuse
     }
-    drain();
 
     if (valid) {
-      if (FLUID_ITEMS) cand -= 1;  // the reference skips j == i before counting (kernels.py:369-371)
       c_cand += cand;
       c_hits += pushed - rej;
       if (FLUID_ITEMS) c_ff += (pushed - pushed_b) - rej_f;
+      if (sizeof(R) == 4 && EQM) {  // the pair loop left the (equal) neighbour mass out
+        s.ax *= (R)a.massf;
+        s.ay *= (R)a.massf;
+        s.az *= (R)a.massf;
+        s.dr *= (R)a.massf;
+      }
       const double ax = (double)s.ax, ay = (double)s.ay, az = (double)s.az;
       const double dr = (double)s.dr, vd = (double)s.vd;
       if (FLUID_ITEMS) {
-        a.acc[3 * i + 0] = ax;
-        a.acc[3 * i + 1] = ay;
-        a.acc[3 * i + 2] = az;
+        a.acc[3 * (int64_t)i + 0] = ax;
+        a.acc[3 * (int64_t)i + 1] = ay;
+        a.acc[3 * (int64_t)i + 2] = az;
       } else {
-        a.acc[3 * i + 0] = 0.0;
-        a.acc[3 * i + 1] = 0.0;
-        a.acc[3 * i + 2] = 0.0;
+        a.acc[3 * (int64_t)i + 0] = 0.0;
+        a.acc[3 * (int64_t)i + 1] = 0.0;
+        a.acc[3 * (int64_t)i + 2] = 0.0;
       }
       a.drho[i] = dr;
       a.visc[i] = vd;
@@ -380,7 +634,6 @@ __global__ void __launch_bounds__(IW * 32, sizeof(R) == 4 ? 6 : 3) k_interact(KA
     }
   }
 
-  // epilogue: one reduction + a few atomics per warp (persistent grid)
   dtf_min = warp_min(dtf_min);
   dtcv_min = warp_min(dtcv_min);
   c_cand = warp_sum_u64(c_cand);
@@ -398,37 +651,57 @@ __global__ void __launch_bounds__(IW * 32, sizeof(R) == 4 ? 6 : 3) k_interact(KA
   }
 }
 
-template <typename R, bool F>
-int launch_one(const KArgs& a, cudaStream_t s) {
-  const int64_t ntiles = (a.item_hi - a.item_lo + 31) / 32;
-  if (ntiles <= 0) return SPHB_OK;
-  static int blocks_per_sm = 0, nsm = 0;
-  if (blocks_per_sm == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_interact<R, F>, IW * 32, 0);
-    if (blocks_per_sm < 1) blocks_per_sm = 1;
+template <typename R>
+constexpr size_t smem_bytes() {
+  return sizeof(float4) * Cfg<R>::NARR * Cfg<R>::SCAP + sizeof(uint32_t) * NW * RING * 32 +
+         sizeof(uint16_t) * NW * RING * 32;
+}
+
+template <typename R, bool F, bool G7, bool EQM>
+int launch_kernel(const KArgs& a, int nsm, cudaStream_t s) {
+  static int grid = 0;
+  const size_t bytes = smem_bytes<R>();
+  if (grid == 0) {
+    cudaError_t e = cudaFuncSetAttribute(k_interact<R, F, G7, EQM>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (e != cudaSuccess)
+      return sphb_set_error(SPHB_E_CUDA, "smem attribute: %s", cudaGetErrorString(e));
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_interact<R, F, G7, EQM>, NW * 32,
+                                                  bytes);
+    grid = nsm * (per_sm > 0 ? per_sm : 1);
   }
-  int64_t want = (ntiles + IW - 1) / IW;
-  int64_t cap = (int64_t)nsm * blocks_per_sm;
-  int grid = (int)(want < cap ? want : cap);
-  k_interact<R, F><<<grid, IW * 32, 0, s>>>(a);
+  k_interact<R, F, G7, EQM><<<grid, NW * 32, bytes, s>>>(a);
   return sphb_check_launch("k_interact");
+}
+
+template <typename R, bool F>
+int launch_one(const KArgs& a, int nsm, cudaStream_t s) {
+  if (sizeof(R) == 8) return launch_kernel<R, F, true, false>(a, nsm, s);
+  const bool eqm = a.p.mass_fluid == a.p.mass_boundary;
+  if (a.gamma7)
+    return eqm ? launch_kernel<R, F, true, true>(a, nsm, s) : launch_kernel<R, F, true, false>(a, nsm, s);
+  return eqm ? launch_kernel<R, F, false, true>(a, nsm, s) : launch_kernel<R, F, false, false>(a, nsm, s);
 }
 
 }  // namespace
 
 int64_t interact_launch_count(int64_t n) {
   (void)n;
-  return 2;
+  return 3;
 }
 
-int launch_interact(const sphb_params_t& p, const sphb_grid_t& g, int64_t n, int64_t nb,
-                    const float4* posp, const float4* velr, const float4* aux,
+int launch_interact(sphb_workspace* ws, const sphb_params_t& p, const sphb_grid_t& g, int64_t n,
+                    int64_t nb, const float4* posp, const float4* velr, const float4* aux,
                     const int32_t* cell_sorted, const int32_t* beg, const int32_t* end,
                     double* acc, double* drho, double* visc, sphb_ctrl_t* ctrl, cudaStream_t s) {
-  if (g.reach < 1 || g.reach > 4) return sphb_set_error(SPHB_E_INVALID, "reach must be 1..4");
+  if (g.reach < 1 || g.reach > 3) return sphb_set_error(SPHB_E_INVALID, "reach must be 1..3");
+  static int nsm = 0;
+  if (nsm == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  }
   KArgs a;
   a.p = p;
   a.g = g;
@@ -456,15 +729,21 @@ int launch_interact(const sphb_params_t& p, const sphb_grid_t& g, int64_t n, int
   a.alpha = (float)p.alpha;
   a.massf = (float)p.mass_fluid;
   a.massb = (float)p.mass_boundary;
+  a.gamma7 = p.gamma == 7.0;
+  a.cs_exp = (float)((p.gamma - 1.0) * 0.5);
+  a.k_cs = a.gamma7 ? (float)(cbrt(p.c0) / p.rho0)
+                    : (float)(p.c0 * pow(p.rho0, -(p.gamma - 1.0) * 0.5));
+  const int64_t nrows = (int64_t)g.dims[1] * g.dims[2];
+  int gb = (int)((nrows + 255) / 256);
+  if (gb > 148 * 8) gb = 148 * 8;
+  k_blocks<<<gb, 256, 0, s>>>(g, a.ncells, beg, end, ws->blocks[0], ws->blocks[1], ctrl);
+  if (int rc = sphb_check_launch("k_blocks")) return rc;
   int rc;
-  // fluid items [nb, n): F-F + F-B
-  a.item_lo = nb;
-  a.item_hi = n;
-  rc = p.precision == SPHB_FP64 ? launch_one<double, true>(a, s) : launch_one<float, true>(a, s);
+  a.blocks = ws->blocks[0];  // fluid items [nb, n): F-F + F-B
+  rc = p.precision == SPHB_FP64 ? launch_one<double, true>(a, nsm, s)
+                                : launch_one<float, true>(a, nsm, s);
   if (rc) return rc;
-  // boundary items [0, nb): B-F only, drho + visc
-  a.item_lo = 0;
-  a.item_hi = nb;
-  rc = p.precision == SPHB_FP64 ? launch_one<double, false>(a, s) : launch_one<float, false>(a, s);
-  return rc;
+  a.blocks = ws->blocks[1];  // boundary items [0, nb): B-F only, drho + visc
+  return p.precision == SPHB_FP64 ? launch_one<double, false>(a, nsm, s)
+                                  : launch_one<float, false>(a, nsm, s);
 }

@@ -22,6 +22,8 @@ struct sphb_workspace {
   uint32_t* radix_hist = nullptr;   // RADIX * max tiles
   uint32_t* digit_total = nullptr;  // RADIX
   uint32_t* scan_partials = nullptr;
+  int2* blocks[2] = {nullptr, nullptr};  // interaction target blocks (fluid, boundary lists)
+  int64_t max_blocks = 0;
   int64_t max_sort_tiles = 0, max_scan_tiles = 0;
   size_t bytes = 0;
 };
@@ -45,7 +47,7 @@ int sort_pass_count(const sphb_grid_t& g);
 int64_t nl_launch_count(const sphb_grid_t& g, int64_t n);
 
 // interact.cu
-int launch_interact(const sphb_params_t& p, const sphb_grid_t& g, int64_t n, int64_t nb,
+int launch_interact(sphb_workspace* ws, const sphb_params_t& p, const sphb_grid_t& g, int64_t n, int64_t nb,
                     const float4* posp, const float4* velr, const float4* aux,
                     const int32_t* cell_sorted, const int32_t* beg, const int32_t* end,
                     double* acc, double* drho, double* visc, sphb_ctrl_t* ctrl, cudaStream_t s);

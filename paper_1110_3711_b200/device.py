@@ -203,7 +203,7 @@ class DeviceSim:
         _lib.check(L.sphb_cell_ranges(ws, g, _ptr(self.beg), _ptr(self.end), _ptr(self.ctrl), s),
                    "sphb_cell_ranges")
         e1.record()
-        _lib.check(L.sphb_interact(p, g, n, nb, _ptr(self.posp_s), _ptr(self.velr_s),
+        _lib.check(L.sphb_interact(ws, p, g, n, nb, _ptr(self.posp_s), _ptr(self.velr_s),
                                    _ptr(self.aux), _ptr(self.cell_s), _ptr(self.beg),
                                    _ptr(self.end), _ptr(self.acc), _ptr(self.drho),
                                    _ptr(self.visc), _ptr(self.ctrl), s), "sphb_interact")

@@ -99,7 +99,7 @@ class B200Engine:
         _lib.check(L.sphb_step_begin(_ptr(ctrl), s), "sphb_step_begin")
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        _lib.check(L.sphb_interact(_lib.ref(prm), _lib.ref(g), n, nb, _ptr(d4[0]), _ptr(d4[1]),
+        _lib.check(L.sphb_interact(self._ws.handle, _lib.ref(prm), _lib.ref(g), n, nb, _ptr(d4[0]), _ptr(d4[1]),
                                    _ptr(d4[2]), _ptr(b["cell"]), _ptr(b["beg"]), _ptr(b["end"]),
                                    _ptr(b["acc"]), _ptr(b["drho"]), _ptr(b["visc"]), _ptr(ctrl), s),
                    "sphb_interact")

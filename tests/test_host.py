@@ -145,6 +145,6 @@ def test_abi_rejects_bad_arguments_without_gpu():
     rc = L.sphb_sort(None, ctypes.byref(g), None, 0, None, None, None, None)
     assert rc == _lib.SPHB_E_INVALID
     assert b"null" in L.sphb_last_error() or b"dims" in L.sphb_last_error()
-    rc = L.sphb_interact(None, None, 0, 0, None, None, None, None, None, None, None, None, None,
-                         None, None)
+    rc = L.sphb_interact(None, None, None, 0, 0, None, None, None, None, None, None, None, None,
+                         None, None, None)
     assert rc == _lib.SPHB_E_INVALID
