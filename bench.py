@@ -61,6 +61,15 @@ def peaks():
     return hbm, hbm_src, fp32, fp32_src
 
 
+def traffic_for(cfg_name):
+    """DRAM bytes per launch of the fluid k_interact from the committed ncu capture."""
+    try:
+        t = json.load(open(os.path.join(ROOT, "profiles", "r01_ncu_traffic.json")))[cfg_name]
+        return float(t["dram_bytes_read"] + t["dram_bytes_write"]), t["source"]
+    except Exception:
+        return None, None
+
+
 def workload(name, n_subdiv):
     import paper_1110_3711_b200 as sph
     sc = sph.named_scenario(name)
@@ -183,7 +192,8 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    cfg_name = args.config or ("c3" if args.gpus == 1 else f"c4_{args.gpus}")
+    # replicas of the same per-GPU workload until the X-slab decomposition lands
+    cfg_name = args.config or "c3"
     if args.impl == "reference":
         run_reference(args, cfg_name)
         return
@@ -243,6 +253,7 @@ def main():
     flops = FLOP_PER_CAND * cand + FLOP_PER_EVAL * evals
     achieved = flops / (pi_mean * 1e-3) / 1e12
     nl_su_ms = float(np.mean(nl_ms) + np.mean(su_ms))
+    traffic, traffic_src = traffic_for(cfg_name)
     nlsu_gbs = BYTES_NL_SU * system.n / (nl_su_ms * 1e-3) / 1e9
 
     # ---- e2e: the same step through the C ABI with HOST buffers (H2D state in, D2H state out)
@@ -295,7 +306,10 @@ def main():
         "counters_per_step": {"candidates": cand, "force_evals": evals, "true_pairs": true_pairs},
         "roofline": {"bound": "fp32", "kernel": "k_interact (fluid + boundary launches)",
                      "achieved": achieved, "peak": fp32, "unit": "TFLOP/s",
-                     "frac": achieved / fp32, "traffic": None,
+                     "frac": achieved / fp32, "traffic": traffic,
+                     "traffic_note": ("dram read+write bytes of the fluid launch, " + traffic_src)
+                     if traffic else None,
+                     "algorithmic_bytes": 52 * system.n,
                      "work": f"{FLOP_PER_CAND}*candidates + {FLOP_PER_EVAL}*evals per launch",
                      "peak_source": fp32_src},
         "roofline_hbm_nl_su": {"bound": "hbm", "achieved": nlsu_gbs, "peak": hbm, "unit": "GB/s",
