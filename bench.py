@@ -186,14 +186,98 @@ def run_reference(args, cfg_name):
     print(json.dumps(line), flush=True)
 
 
+# ---------------------------------------------------------------- multi-GPU (X slabs)
+def run_slabs(args, cfg_name, system, prm, prec, world, rank, local):
+    """One slab per GPU: migration + halo exchange over NCCL (torch.distributed send/recv),
+    owned-target interaction, dt allreduce(min) on the device control words."""
+    import torch
+    import torch.distributed as dist
+    from paper_1110_3711_b200 import slab
+
+    sim = slab.device_slab_simulation(system, prm, world, comm=slab.DistComm(), precision=prec)
+    me = sim.ranks[0]
+    Ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+    for _ in range(args.warmup):
+        sim.step()
+    torch.cuda.synchronize()
+    dist.barrier()
+    clocks = Clocks(local)
+    t0, t1 = Ev(), Ev()
+    t0.record()
+    for _ in range(args.steps):
+        sim.step()
+    t1.record()
+    torch.cuda.synchronize()
+    dist.barrier()
+    clk = clocks.stop()
+    tt = torch.tensor([t0.elapsed_time(t1)], device="cuda")
+    dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    total_ms = float(tt.item())
+    # e2e: the same decomposed step with each rank's owned state round-tripped through pinned
+    # host buffers every step (the per-step host boundary of the engine API)
+    h2d = d2h = 0
+    e2e_value = None
+    if args.e2e_steps > 0:
+        torch.cuda.synchronize()
+        a, b = Ev(), Ev()
+        a.record()
+        for _ in range(args.e2e_steps):
+            nbytes = 0
+            for li in (0, 1):
+                hs = me.st[li].to("cpu", non_blocking=False).pin_memory()
+                hi = me.ids[li].to("cpu").pin_memory()
+                nbytes += hs.numel() * 4 + hi.numel() * 8
+                me.st[li] = hs.to(me.st[li].device, non_blocking=True)
+                me.ids[li] = hi.to(me.ids[li].device, non_blocking=True)
+            h2d = d2h = nbytes
+            sim.step()
+        b.record()
+        torch.cuda.synchronize()
+        te = torch.tensor([a.elapsed_time(b)], device="cuda")
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e_value = system.n * args.e2e_steps / (float(te.item()) * 1e-3)
+    recs = me.stats[args.warmup:args.warmup + args.steps]
+    true_pairs = float(np.mean([r["true_pairs"] for r in recs]))
+    evals = float(np.mean([r["force_evals"] for r in recs]))
+    value = system.n * args.steps / (total_ms * 1e-3)
+    owned = torch.tensor([me.n_owned], device="cuda", dtype=torch.int64)
+    dist.all_reduce(owned, op=dist.ReduceOp.MAX)
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": args.precision,
+        "data": "synthetic: reference dam-break lattice (Scenario/build_dam_break), hydrostatic rho",
+        "config": {"workload": f"{cfg_name}: 3-D dam break, {system.n:,} particles over {world} "
+                               f"GPUs (~{system.n // world:,} per GPU)",
+                   "particles": system.n, "n_subdiv": args.n_subdiv,
+                   "l2": "inputs larger than L2",
+                   "parallelism": f"{world} X-slabs (NCCL send/recv halos + migration, "
+                                  "allreduce-min dt)",
+                   "slab_bounds": [int(v) for v in sim.bounds],
+                   "max_owned_per_gpu": int(owned.item())},
+        "interactions_per_s": true_pairs * args.steps / (total_ms * 1e-3),
+        "pair_evals_per_s": evals * args.steps / (total_ms * 1e-3),
+        "gpu_launches": args.steps * 14,
+        "clocks": clk,
+    }
+    if e2e_value is not None:
+        line["e2e"] = {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
+                       "d2h_bytes_per_step": d2h, "steps": args.e2e_steps,
+                       "path": "per step: each rank's owned state via pinned host buffers, then the decomposed step"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    dist.destroy_process_group()
+
+
 # ---------------------------------------------------------------- B200 arm
 def main():
     args = parse()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    # replicas of the same per-GPU workload until the X-slab decomposition lands
-    cfg_name = args.config or "c3"
+    # N=1: C3 (10.2M, the single-GPU roofline configuration); N>1: the weak-scaling family in
+    # C3's tank (~10M particles per GPU), X-slab decomposed with NCCL halo/migration exchange
+    cfg_name = args.config or ("c3" if args.gpus == 1 else f"c3w_{args.gpus}")
     if args.impl == "reference":
         run_reference(args, cfg_name)
         return
@@ -209,6 +293,9 @@ def main():
     sc, prm, system = workload(cfg_name, args.n_subdiv)
     variant = "slowcellsh" if args.n_subdiv == 1 else "slowcellshalf"
     prec = _lib.SPHB_FP64 if args.precision == "fp64" else _lib.SPHB_FP32
+    if world > 1:
+        run_slabs(args, cfg_name, system, prm, prec, world, rank, local)
+        return
     sim = DeviceSim(system, prm, reach=args.n_subdiv, precision=prec,
                     record_capacity=max(64, args.warmup + args.steps + 8))
     Ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731

@@ -63,6 +63,8 @@ typedef struct {
   double cell_size;     /* 2h / n_subdiv */
   int32_t dims[3];      /* max(ceil(extent/cs - 1e-12), 1) */
   int32_t reach;        /* candidate rows per side: gather slowcellsh 1, *half 2 */
+  int32_t tx0, tx1;     /* interaction targets restricted to cell columns [tx0, tx1) (X-slab
+                           decomposition; the whole grid is [0, dims[0])) */
 } sphb_grid_t;
 
 /* Physics constants.  The first twelve are physics.pack_params (physics.py:149-180). */

@@ -168,7 +168,8 @@ static inline void scan_range(const state_t* s, const side_t* si, int64_t i, int
  * (F-F then F-B per row), boundary items otherwise (fluid rows only, drho and
  * visc only).  order: 0 = per-row interleaving (gather_*_cells),
  * 1 = all fluid rows then all boundary rows (gather_fluid_ranges).
- * counters_out[4] = raw (cand, true, evals, ff) summed over items.
+ * counters_out[4] = raw (cand, true, evals, ff) summed over items.  target_mask (may be
+ * NULL) restricts the items (X-slab decomposition tests: owned targets only).
  */
 void oracle_gather_pass(int fluid_items, int order, int64_t i_lo, int64_t i_hi, int reach,
                         const int64_t* cell_of, int64_t nx, int64_t ny, int64_t nz,
@@ -176,7 +177,8 @@ void oracle_gather_pass(int fluid_items, int order, int64_t i_lo, int64_t i_hi, 
                         const int64_t* bend, int dmode, const float* pos, const float* vel,
                         const float* rho, const float* press, const float* prrho,
                         const float* csound, const float* tensil, const double* pp, double* acc,
-                        double* drho, double* viscdt, int64_t* counters_out, int nthreads) {
+                        double* drho, double* viscdt, int64_t* counters_out, int nthreads,
+                        const uint8_t* target_mask) {
   state_t s = {pos, vel, rho, press, prrho, csound, tensil, pp, dmode};
   const double sup2 = pp[PP_SUP2], massf = pp[PP_MASSF], massb = pp[PP_MASSB];
   const int64_t nxy = nx * ny;
@@ -186,6 +188,7 @@ void oracle_gather_pass(int fluid_items, int order, int64_t i_lo, int64_t i_hi, 
 #pragma omp parallel for schedule(dynamic, 256) reduction(+ : c_cand, c_true, c_eval, c_ff)
 #endif
   for (int64_t i = i_lo; i < i_hi; ++i) {
+    if (target_mask && !target_mask[i]) continue; /* not a target of this slab */
     side_t si;
     load_side(&s, i, &si);
     acc_t a = {0.0, 0.0, 0.0, 0.0, 0.0, 0, 0, 0, 0};

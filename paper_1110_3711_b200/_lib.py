@@ -24,7 +24,7 @@ c_i32, c_i64, c_f64, c_p = ctypes.c_int32, ctypes.c_int64, ctypes.c_double, ctyp
 
 class GridDesc(ctypes.Structure):
     _fields_ = [("origin", c_f64 * 3), ("domain_max", c_f64 * 3), ("cell_size", c_f64),
-                ("dims", c_i32 * 3), ("reach", c_i32)]
+                ("dims", c_i32 * 3), ("reach", c_i32), ("tx0", c_i32), ("tx1", c_i32)]
 
 
 class ParamsDesc(ctypes.Structure):

@@ -44,6 +44,8 @@ static int check_grid(const sphb_grid_t* g) {
   for (int k = 0; k < 3; ++k)
     if (g->dims[k] < 1) return sphb_set_error(SPHB_E_INVALID, "grid dims must be >= 1");
   if (!(g->cell_size > 0)) return sphb_set_error(SPHB_E_INVALID, "cell_size must be positive");
+  if (g->tx0 < 0 || g->tx1 > g->dims[0] || g->tx0 > g->tx1)
+    return sphb_set_error(SPHB_E_INVALID, "target columns [tx0, tx1) must lie in [0, dims[0]]");
   if (sphb::ncells_of(*g) >= (int64_t(1) << 30))
     return sphb_set_error(SPHB_E_INVALID, "ncells >= 2^30 unsupported (31-bit sort keys)");
   return SPHB_OK;

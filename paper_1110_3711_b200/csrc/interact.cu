@@ -342,7 +342,9 @@ __device__ __forceinline__ bool screen(const KArgs& a, const C32&, const Own<dou
 
 // ------------------------------------------------------------------ block builder
 // Cuts each (y, z) cell row of the fluid list (and, for the boundary pass, of the
-// boundary list) into ceil(L / BT) balanced blocks of consecutive targets.
+// boundary list) into ceil(L / BT) balanced blocks of consecutive targets.  Only cell
+// columns [tx0, tx1) hold targets (the owned slab of an X-slab decomposition; halo columns
+// outside it are candidates only).
 __global__ void __launch_bounds__(256) k_blocks(sphb_grid_t g, int64_t ncells,
                                                 const int32_t* __restrict__ beg,
                                                 const int32_t* __restrict__ end,
@@ -351,13 +353,14 @@ __global__ void __launch_bounds__(256) k_blocks(sphb_grid_t g, int64_t ncells,
   if (!step_live(ctrl)) return;
   const int nx = g.dims[0];
   const int64_t nrows = (int64_t)g.dims[1] * g.dims[2];
+  if (g.tx1 <= g.tx0) return;
   for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < nrows;
        r += (int64_t)gridDim.x * blockDim.x) {
     const int64_t c0 = r * nx;
 #pragma unroll
     for (int li = 0; li < 2; ++li) {
       const int64_t off = li == 0 ? ncells : 0;
-      const int32_t rb = beg[off + c0], re = end[off + c0 + nx - 1];
+      const int32_t rb = beg[off + c0 + g.tx0], re = end[off + c0 + g.tx1 - 1];
       const int32_t L = re - rb;
       if (L <= 0) continue;
       const int32_t nbk = (L + BT - 1) / BT;

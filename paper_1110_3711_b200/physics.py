@@ -59,7 +59,7 @@ def grid_dims(params):
     return cs, dims
 
 
-def grid_desc(params, reach: int | None = None) -> "_lib.GridDesc":
+def grid_desc(params, reach: int | None = None, target_cols=None) -> "_lib.GridDesc":
     cs, dims = grid_dims(params)
     g = _lib.GridDesc()
     for k in range(3):
@@ -68,4 +68,5 @@ def grid_desc(params, reach: int | None = None) -> "_lib.GridDesc":
         g.dims[k] = int(dims[k])
     g.cell_size = float(cs)
     g.reach = int(params.n_subdiv if reach is None else reach)
+    g.tx0, g.tx1 = (0, int(dims[0])) if target_cols is None else (int(target_cols[0]), int(target_cols[1]))
     return g

@@ -154,6 +154,10 @@ CONFIGS = {
     "c4_2": dict(dp=0.00159, **FULL_TANK),    # 21.55M
     "c4_4": dict(dp=0.001262, **FULL_TANK),   # 42.45M
     "c4_8": dict(dp=0.001, **FULL_TANK),      # 84.20M
+    # weak-scaling family in C3's own tank (SURVEY.md §8 table note): ~10M particles per GPU
+    "c3w_2": dict(dp=0.00054),       # 20.06M
+    "c3w_4": dict(dp=0.00043),       # 39.44M
+    "c3w_8": dict(dp=0.00034),       # 78.83M
 }
 
 

@@ -372,3 +372,32 @@ def test_c3_10m_counters_match_reference_measurement(n_subdiv, cand):
     assert st.force_evals == 2_421_180_320
     assert st.ff_force_evals == 2_373_133_760
     assert st.candidate_pairs == cand
+
+
+# ------------------------------------------------------------------ X-slab decomposition
+@pytest.mark.parametrize("nslabs,precision", [(2, 1), (3, 1), (3, 0)])
+def test_device_virtual_slabs_match_single_domain(nslabs, precision):
+    """k virtual slabs on one GPU (LoopbackComm; the same exchange code as the NCCL path)
+    against the single-domain device run: step 0 identical, 20 steps close (id-aligned)."""
+    from paper_1110_3711_b200 import slab
+    sc = sph.Scenario(dp=0.006)
+    prm = sph.make_params(sc)
+    system = sph.build_dam_break(sc, prm)
+    steps = 20
+    sim = slab.device_slab_simulation(system, prm, nslabs, precision=precision)
+    sim.run(steps)
+    cfg = gather_cfg("slowcellsh", "fp64" if precision == 1 else "fp32")
+    ref, stats = sph.run_simulation(sph.build_dam_break(sc, prm), prm, cfg, max_steps=steps,
+                                    stage_timing=False)
+    st0 = sim.ranks[0].stats[0]
+    assert st0["dt"] == stats[0].dt
+    assert [st0["candidate_pairs"], st0["true_pairs"], st0["force_evals"], st0["ff_force_evals"]] \
+        == [stats[0].candidate_pairs, stats[0].true_pairs, stats[0].force_evals,
+            stats[0].ff_force_evals]
+    pos, vel, rho, ids, _ = sim.gather_host()
+    assert np.array_equal(np.sort(ids), np.sort(ref.id))
+    a, b = np.argsort(ids), np.argsort(ref.id)
+    tol = 1e-9 if precision == 1 else 1e-5
+    assert oracle.rel_linf(pos[a], ref.pos[b]) <= tol
+    assert oracle.rel_linf(vel[a], ref.vel[b]) <= max(tol, 1e-4 if precision == 0 else tol)
+    assert oracle.rel_linf(rho[a], ref.rho[b]) <= tol
