@@ -118,8 +118,9 @@ class Clocks:
 # ---------------------------------------------------------------- CPU reference (oracle port)
 def cpu_reference(system, prm, n_subdiv, budget_s, repeats=1):
     """Time the reference algorithm's CPU restatement (oracle/: numpy NL/SU, C OpenMP gather,
-    bit-exact to the reference) on this host.  PI runs on a contiguous block of fluid targets
-    sized to ``budget_s`` and is scaled to the whole fluid list; NL and SU run in full."""
+    bit-exact to the reference) on this host.  NL and SU run in full; PI runs on every
+    ``stride``-th target of both passes (a spatially uniform sample, sized so PI takes about
+    ``budget_s``) and is scaled by the stride (stride 1 = the full pass)."""
     import oracle
     cores = len(os.sched_getaffinity(0))
     variant = "slowcellsh" if n_subdiv == 1 else "slowcellshalf"
@@ -133,33 +134,35 @@ def cpu_reference(system, prm, n_subdiv, budget_s, repeats=1):
         cs = cell[perm]
         cidx = oracle.cell_index(cs, nb, int(np.prod(dims)))
         t_nl = time.perf_counter() - t0
-        # PI probe to size the sample
-        probe = min(20000, n - nb)
+        args = (pos, vel, rho, nb, system.mass_fluid, system.mass_boundary, cs, dims, cidx, prm)
+        idx = np.arange(n)
+        # fixed cost of a pass (EOS of all particles, thread start-up) vs per-item cost
         t1 = time.perf_counter()
-        oracle.gather(pos, vel, rho, nb, system.mass_fluid, system.mass_boundary, cs, dims, cidx,
-                      prm, variant=variant, nthreads=cores, items=(nb, nb + probe))
-        t_probe = time.perf_counter() - t1
-        per_item = t_probe / max(probe, 1)
-        m = int(min(n - nb, max(probe, budget_s / max(per_item, 1e-12))))
+        oracle.gather(*args, variant=variant, nthreads=cores, target_mask=np.zeros(n, bool))
+        t_fixed = time.perf_counter() - t1
+        probe = 256
+        t1 = time.perf_counter()
+        oracle.gather(*args, variant=variant, nthreads=cores, target_mask=(idx % probe) == 0)
+        est_full = t_fixed + max(time.perf_counter() - t1 - t_fixed, 0.0) * probe
+        stride = max(1, int(math.ceil(est_full / budget_s)))
         t2 = time.perf_counter()
-        out = oracle.gather(pos, vel, rho, nb, system.mass_fluid, system.mass_boundary, cs, dims,
-                            cidx, prm, variant=variant, nthreads=cores, items=(nb, nb + m))
-        t_pi_sample = time.perf_counter() - t2
-        t_pi = t_pi_sample * (n / m)  # boundary items cost about as much per item as fluid ones
-        # SU on the full arrays (accel from the sample rows, zeros elsewhere: same work)
+        out = oracle.gather(*args, variant=variant, nthreads=cores,
+                            target_mask=(idx % stride) == 0 if stride > 1 else None)
+        t_pi = t_fixed + max(time.perf_counter() - t2 - t_fixed, 0.0) * stride
         t3 = time.perf_counter()
         press, csound, _, _ = oracle.derived(rho, prm)
         dt = oracle.compute_dt(out["accel"], out["visc_dt"], csound, nb, prm)
         oracle.verlet_update(0, pos, vel, rho, vel, rho, out["accel"], out["drho_dt"], nb, prm,
                              max(dt, prm.dt_min))
         t_su = time.perf_counter() - t3
-        times.append((t_nl, t_pi, t_su, m))
-    t_nl, t_pi, t_su, m = min(times, key=lambda t: t[0] + t[1] + t[2])
+        times.append((t_nl, t_pi, t_su, stride))
+    t_nl, t_pi, t_su, stride = min(times, key=lambda t: t[0] + t[1] + t[2])
     step_s = t_nl + t_pi + t_su
+    what = "every item" if stride == 1 else f"every {stride}th item (uniform sample, scaled x{stride})"
     return dict(value=n / step_s, unit=UNIT, cores=cores, kind="port",
                 sample=f"one {variant} step of this workload on {cores} threads: full NL+SU "
-                       f"(numpy), PI (oracle C, OpenMP) on {m:,} of {n - nb:,} fluid targets "
-                       f"scaled to all {n:,} items; stage s NL {t_nl:.2f} PI {t_pi:.2f} SU {t_su:.2f}",
+                       f"(numpy, as the reference), PI (oracle C, OpenMP) on {what}; "
+                       f"stage s NL {t_nl:.2f} PI {t_pi:.2f} SU {t_su:.2f}",
                 step_s=step_s)
 
 
@@ -169,8 +172,8 @@ def run_reference(args, cfg_name):
         return
     sc, prm, system = workload(cfg_name, args.n_subdiv)
     for _ in range(args.warmup):
-        cpu_reference(system, prm, args.n_subdiv, budget_s=2.0)
-    t = [cpu_reference(system, prm, args.n_subdiv, budget_s=2.0) for _ in range(args.steps)]
+        cpu_reference(system, prm, args.n_subdiv, budget_s=1.5)
+    t = [cpu_reference(system, prm, args.n_subdiv, budget_s=1.5) for _ in range(args.steps)]
     step_s = float(np.mean([x["step_s"] for x in t]))
     value = system.n / step_s
     cb = dict(t[-1])
