@@ -7,8 +7,8 @@
 //
 // Decomposition (FP32 CUDA cores: the pair math is a data-dependent gather-reduce, not a
 // dense contraction, so tensor cores do not apply):
-//   * k_blocks cuts every (y, z) cell row of a particle list into blocks of <= 128
-//     consecutive cell-sorted targets.  Because cells are x-fastest (grid.py:1-8), a
+//   * k_blocks cuts every (y, z) cell row of a particle list into blocks of whole cells
+//     holding <= 128 consecutive cell-sorted targets.  Because cells are x-fastest (grid.py:1-8), a
 //     block's candidate set is, per stencil row, ONE contiguous particle range
 //     [beg(cx_first - r), end(cx_last + r)).
 //   * k_interact is persistent: two 4-warp CTAs per SM pull blocks dynamically.  The CTA
@@ -31,6 +31,8 @@
 //     true_pairs / force_evals / ff counters -- are bit-exact (SURVEY.md §8(a')).
 //   * The FP64 instantiation screens with the exact predicate and evaluates in the
 //     reference's exact operation order: bit-identical forces.
+#include <cuda_fp16.h>
+
 #include <climits>
 
 #include "sphb_common.cuh"
@@ -42,21 +44,31 @@ namespace {
 
 constexpr int NW = 4;            // warps per CTA (two CTAs per SM)
 constexpr int BT = NW * 32;      // targets per block
-constexpr int RING = 40;         // per-lane FIFO entries (non-empty 32-candidate mask words)
+#ifndef SPHB_H16
+#define SPHB_H16 1
+#endif
+constexpr int RING = SPHB_H16 ? 32 : 48;  // per-lane FIFO entries (non-empty 32-candidate words)
 constexpr int MAXSEG = 128;      // stencil row segments per block (2 lists x (2r+1)^2, r <= 3)
 
 template <typename R>
 struct Cfg;
 template <>
 struct Cfg<float> {
-  static constexpr int SCAP = 2304;  // staged candidates (A, B float4)
+  static constexpr int SCAP = 2304;  // staged candidates (A, B float4 [+ x/y/z FP16 copies])
   static constexpr int NARR = 2;
+  static constexpr int H16 = SPHB_H16;
 };
 template <>
 struct Cfg<double> {
   static constexpr int SCAP = 1024;  // staged candidates (A, B, C float4)
   static constexpr int NARR = 3;
+  static constexpr int H16 = 0;
 };
+// FP16 screen: block-centred coordinates in units of the support radius 2h; maybe = r^2 <
+// 1.025.  Valid while |x| <= 4 (the block's x extent <= 8 support radii): coordinate
+// quantisation <= 2^-9, |d(r^2)| <= 1.6e-2 at the cutoff, so no true hit is screened out.
+constexpr float H16_THR = 1.025f;
+constexpr float H16_MAXABS = 4.0f;
 
 struct KArgs {
   sphb_params_t p;
@@ -139,6 +151,18 @@ __device__ __forceinline__ float4 lds4(uint32_t addr) {
                : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
                : "r"(addr));
   return v;
+}
+__device__ __forceinline__ uint4 lds128u(uint32_t addr) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ __half2 u32_as_h2(uint32_t u) {
+  __half2 h;
+  memcpy(&h, &u, 4);
+  return h;
 }
 __device__ __forceinline__ uint32_t lds32(uint32_t addr) {
   uint32_t v;
@@ -306,8 +330,10 @@ __device__ __forceinline__ uint32_t eval_two(const KArgs& a, const C32& c, const
   const float r22 = fmaf(dz2, dz2, fmaf(dy2, dy2, dx2 * dx2));
   const bool f1 = r21 < c.sup2_lo && r21 > c.tiny, f2 = r22 < c.sup2_lo && r22 > c.tiny;
   bool ok1 = v1 && f1, ok2 = v2 && f2;
-  if (v1 && !f1) ok1 = cold_accept(a, o.x, o.y, o.z, A1, xlo, xhi);
-  if (v2 && !f2) ok2 = cold_accept(a, o.x, o.y, o.z, A2, xlo, xhi);
+  // FP32 r2 >= sup2 (1 + 1e-5) is a certain miss (the FP16 screen's shell); only the guard
+  // band and r2 ~ 0 need the exact f64 decision
+  if (v1 && !f1 && r21 < c.sup2_hi) ok1 = cold_accept(a, o.x, o.y, o.z, A1, xlo, xhi);
+  if (v2 && !f2 && r22 < c.sup2_hi) ok2 = cold_accept(a, o.x, o.y, o.z, A2, xlo, xhi);
   pair_eval32<G7, EQM>(c, o, dx1, dy1, dz1, r21, A1, B1, ok1, s);
   pair_eval32<G7, EQM>(c, o, dx2, dy2, dz2, r22, A2, B2, ok2, s);
   const uint32_t r1 = (v1 && !ok1) ? 1u : 0u, r2 = (v2 && !ok2) ? 1u : 0u;
@@ -342,9 +368,9 @@ __device__ __forceinline__ bool screen(const KArgs& a, const C32&, const Own<dou
 
 // ------------------------------------------------------------------ block builder
 // Cuts each (y, z) cell row of the fluid list (and, for the boundary pass, of the
-// boundary list) into ceil(L / BT) balanced blocks of consecutive targets.  Only cell
-// columns [tx0, tx1) hold targets (the owned slab of an X-slab decomposition; halo columns
-// outside it are candidates only).
+// boundary list) into blocks of whole cells holding <= BT targets.  Only cell columns
+// [tx0, tx1) hold targets (the owned slab of an X-slab decomposition; halo columns outside
+// it are candidates only).
 __global__ void __launch_bounds__(256) k_blocks(sphb_grid_t g, int64_t ncells,
                                                 const int32_t* __restrict__ beg,
                                                 const int32_t* __restrict__ end,
@@ -357,18 +383,38 @@ __global__ void __launch_bounds__(256) k_blocks(sphb_grid_t g, int64_t ncells,
   for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < nrows;
        r += (int64_t)gridDim.x * blockDim.x) {
     const int64_t c0 = r * nx;
-#pragma unroll
+#pragma unroll 1
     for (int li = 0; li < 2; ++li) {
-      const int64_t off = li == 0 ? ncells : 0;
-      const int32_t rb = beg[off + c0 + g.tx0], re = end[off + c0 + g.tx1 - 1];
-      const int32_t L = re - rb;
-      if (L <= 0) continue;
-      const int32_t nbk = (L + BT - 1) / BT;
-      const uint32_t at = atomicAdd(&ctrl->nblk[li], (uint32_t)nbk);
+      const int64_t off = (li == 0 ? ncells : 0) + c0;
+      const int32_t rb = beg[off + g.tx0], re = end[off + g.tx1 - 1];
+      if (re <= rb) continue;
       int2* out = li == 0 ? blk_f : blk_b;
-      for (int32_t b = 0; b < nbk; ++b)
-        out[at + b] = make_int2(rb + (int32_t)(((int64_t)L * b) / nbk),
-                                rb + (int32_t)(((int64_t)L * (b + 1)) / nbk));
+      // Greedy whole-cell blocks: a block never starts or ends inside a cell unless that
+      // cell alone holds more than BT targets (then it is split evenly), so its candidate
+      // rows span (cells + 2 reach) columns, not one more.
+      int32_t b0 = rb, cur = rb;
+      for (int x = g.tx0; x < g.tx1; ++x) {
+        const int32_t ce = end[off + x];
+        if (ce == cur) continue;
+        if (ce - b0 > BT && cur > b0) {  // close the block before this cell
+          const uint32_t at = atomicAdd(&ctrl->nblk[li], 1u);
+          out[at] = make_int2(b0, cur);
+          b0 = cur;
+        }
+        if (ce - b0 > BT) {  // one oversized cell: even split into ceil(len / BT) blocks
+          const int32_t L = ce - b0, nbk = (L + BT - 1) / BT;
+          const uint32_t at = atomicAdd(&ctrl->nblk[li], (uint32_t)nbk);
+          for (int32_t b = 0; b < nbk; ++b)
+            out[at + b] = make_int2(b0 + (int32_t)(((int64_t)L * b) / nbk),
+                                    b0 + (int32_t)(((int64_t)L * (b + 1)) / nbk));
+          b0 = ce;
+        }
+        cur = ce;
+      }
+      if (cur > b0) {
+        const uint32_t at = atomicAdd(&ctrl->nblk[li], 1u);
+        out[at] = make_int2(b0, cur);
+      }
     }
   }
 }
@@ -383,7 +429,8 @@ __global__ void __launch_bounds__(NW * 32, 2) k_interact(KArgs a) {
   const C32 c32 = pin_constants(a);
   constexpr int SCAP = Cfg<R>::SCAP;
   constexpr int SB = SCAP, SC = 2 * SCAP;                  // float4 offsets of B and C
-  constexpr int MASK0 = 4 * Cfg<R>::NARR * SCAP;            // uint32 offset of the rings
+  constexpr int HBYTES = Cfg<R>::H16 ? 6 * SCAP : 0;        // FP16 x | y | z screen copies
+  constexpr int MASK0 = (16 * Cfg<R>::NARR * SCAP + HBYTES) / 4;  // uint32 offset of the rings
   uint32_t* sMask = g_sm32 + MASK0;                          // [NW][RING][32] mask words
   uint16_t* sBase = reinterpret_cast<uint16_t*>(sMask + NW * RING * 32);  // [NW][RING][32]
   __shared__ Seg sSeg[MAXSEG];
@@ -415,6 +462,14 @@ __global__ void __launch_bounds__(NW * 32, 2) k_interact(KArgs a) {
     const int cxa = cfirst - rowkey * nx, cxb = clast - rowkey * nx;
     const int gcz = rowkey / ny, gcy = rowkey - gcz * ny;
     const int bxlo = max(cxa - reach, 0), bxhi = min(cxb + reach, nx - 1);
+    // FP16 screen frame: block centre, unit = 2h (Cfg<float> only)
+    const double cs = a.g.cell_size;
+    const float h16_s = (float)(0.5 * a.p.invh);
+    const float h16_xc = (float)(a.g.origin[0] + 0.5 * (bxlo + bxhi + 1) * cs);
+    const float h16_yc = (float)(a.g.origin[1] + (gcy + 0.5) * cs);
+    const float h16_zc = (float)(a.g.origin[2] + (gcz + 0.5) * cs);
+    const bool use16 = Cfg<R>::H16 && (0.5 * (bxhi - bxlo + 1) * cs * (0.5 * a.p.invh) <= H16_MAXABS) &&
+                       ((reach + 0.5) * cs * (0.5 * a.p.invh) <= H16_MAXABS);
 
     // ---- stencil row segments in the reference's traversal order + their prefix
     if (tid < MAXSEG) {
@@ -506,6 +561,11 @@ __global__ void __launch_bounds__(NW * 32, 2) k_interact(KArgs a) {
     const uint32_t smC = pin_u32(smA + 16u * SC);
     const uint32_t smMask = pin_u32(smem_addr(myMask) + 4u * lane);
     const uint32_t smBase = pin_u32(smem_addr(myBase) + 2u * lane);
+    const uint32_t smH = pin_u32(smA + 16u * Cfg<R>::NARR * SCAP);
+    const __half2 thr16 = __float2half2_rn(H16_THR);
+    const __half2 ohx = __float2half2_rn(((float)o.x - h16_xc) * h16_s);
+    const __half2 ohy = __float2half2_rn(((float)o.y - h16_yc) * h16_s);
+    const __half2 ohz = __float2half2_rn(((float)o.z - h16_zc) * h16_s);
     auto drain = [&]() {
       __syncwarp();
       const uint32_t mx = __reduce_max_sync(SPHB_FULL, pend);
@@ -548,6 +608,12 @@ __global__ void __launch_bounds__(NW * 32, 2) k_interact(KArgs a) {
           g_sm4[p - q0] = make_float4(pp.x, pp.y, pp.z, xa.x);
           g_sm4[SB + p - q0] = make_float4(vr.x, vr.y, vr.z, boundary_list ? -vr.w : vr.w);
           if (sizeof(R) == 8) g_sm4[SC + p - q0] = make_float4(xa.y, xa.z, 0.f, 0.f);
+          if (Cfg<R>::H16) {
+            __half* h = reinterpret_cast<__half*>(g_sm4 + Cfg<R>::NARR * SCAP);
+            h[p - q0] = __float2half_rn((pp.x - h16_xc) * h16_s);
+            h[SCAP + p - q0] = __float2half_rn((pp.y - h16_yc) * h16_s);
+            h[2 * SCAP + p - q0] = __float2half_rn((pp.z - h16_zc) * h16_s);
+          }
         }
       }
       __syncthreads();
@@ -567,13 +633,36 @@ __global__ void __launch_bounds__(NW * 32, 2) k_interact(KArgs a) {
             la = sg.pos + (a.beg[sg.rowoff + xlo] - sg.g0) - q0;
             lb = sg.pos + (a.end[sg.rowoff + xhi] - sg.g0) - q0;
           }
-          for (int k0 = lo; k0 < hi; k0 += 32) {
+          const int lo8 = use16 ? (lo & ~7) : lo;  // FP16 loads are 8-candidate aligned
+          for (int k0 = lo8; k0 < hi; k0 += 32) {
             uint32_t bits = 0;
-            const uint32_t sk = smA + 16u * k0;
+            if (use16) {
+              const uint32_t hx = smH + 2u * k0, hy = hx + 2u * SCAP, hz = hy + 2u * SCAP;
 #pragma unroll
-            for (int t = 0; t < 32; ++t) {
-              const float4 A = lds4(sk + 16u * t);  // reads past hi stay inside shared memory
-              if (screen(a, c32, o, A)) bits |= 1u << t;
+              for (int q = 0; q < 4; ++q) {
+                const uint4 vx = lds128u(hx + 16u * q), vy = lds128u(hy + 16u * q),
+                            vz = lds128u(hz + 16u * q);
+                const uint32_t ux[4] = {vx.x, vx.y, vx.z, vx.w}, uy[4] = {vy.x, vy.y, vy.z, vy.w},
+                               uz[4] = {vz.x, vz.y, vz.z, vz.w};
+#pragma unroll
+                for (int w = 0; w < 4; ++w) {
+                  const __half2 dx = __hsub2(ohx, u32_as_h2(ux[w]));
+                  const __half2 dy = __hsub2(ohy, u32_as_h2(uy[w]));
+                  const __half2 dz = __hsub2(ohz, u32_as_h2(uz[w]));
+                  const __half2 r2 = __hfma2(dz, dz, __hfma2(dy, dy, __hmul2(dx, dx)));
+                  const uint32_t m = __hlt2_mask(r2, thr16);
+                  const int t = q * 8 + w * 2;
+                  bits |= ((m & 1u) << t) | (((m >> 16) & 1u) << (t + 1));
+                }
+              }
+              if (k0 < lo) bits &= 0xffffffffu << (lo - k0);
+            } else {
+              const uint32_t sk = smA + 16u * k0;
+#pragma unroll
+              for (int t = 0; t < 32; ++t) {
+                const float4 A = lds4(sk + 16u * t);  // reads past hi stay inside shared memory
+                if (screen(a, c32, o, A)) bits |= 1u << t;
+              }
             }
             const int nvalid = hi - k0;
             if (nvalid < 32) bits &= (1u << nvalid) - 1u;
@@ -656,8 +745,8 @@ __global__ void __launch_bounds__(NW * 32, 2) k_interact(KArgs a) {
 
 template <typename R>
 constexpr size_t smem_bytes() {
-  return sizeof(float4) * Cfg<R>::NARR * Cfg<R>::SCAP + sizeof(uint32_t) * NW * RING * 32 +
-         sizeof(uint16_t) * NW * RING * 32;
+  return sizeof(float4) * Cfg<R>::NARR * Cfg<R>::SCAP + (Cfg<R>::H16 ? 6 * Cfg<R>::SCAP : 0) +
+         sizeof(uint32_t) * NW * RING * 32 + sizeof(uint16_t) * NW * RING * 32;
 }
 
 template <typename R, bool F, bool G7, bool EQM>
