@@ -80,7 +80,7 @@ struct KArgs {
   const int32_t* __restrict__ cell;
   const int32_t* __restrict__ beg;
   const int32_t* __restrict__ end;
-  const int2* __restrict__ blocks;
+  const int4* __restrict__ blocks;  // (fluid i0, i1, boundary i0, i1) per block
   double* __restrict__ acc;
   double* __restrict__ drho;
   double* __restrict__ visc;
@@ -367,55 +367,47 @@ __device__ __forceinline__ bool screen(const KArgs& a, const C32&, const Own<dou
 }
 
 // ------------------------------------------------------------------ block builder
-// Cuts each (y, z) cell row of the fluid list (and, for the boundary pass, of the
-// boundary list) into blocks of whole cells holding <= BT targets.  Only cell columns
-// [tx0, tx1) hold targets (the owned slab of an X-slab decomposition; halo columns outside
-// it are candidates only).
+// Cuts each (y, z) cell row into blocks of whole cells holding <= BT targets of BOTH lists
+// (fluid targets and boundary targets of the same cells share one staged candidate set).
+// Only cell columns [tx0, tx1) hold targets (the owned slab of an X-slab decomposition;
+// halo columns outside it are candidates only).  A cell with more than BT targets is split
+// into single-list blocks.
+__device__ __forceinline__ void emit_block(sphb_ctrl_t* ctrl, int4* out, int4 b) {
+  out[atomicAdd(&ctrl->nblk[0], 1u)] = b;
+}
+
 __global__ void __launch_bounds__(256) k_blocks(sphb_grid_t g, int64_t ncells,
                                                 const int32_t* __restrict__ beg,
                                                 const int32_t* __restrict__ end,
-                                                int2* __restrict__ blk_f, int2* __restrict__ blk_b,
-                                                sphb_ctrl_t* ctrl) {
+                                                int4* __restrict__ blk, sphb_ctrl_t* ctrl) {
   if (!step_live(ctrl)) return;
   const int nx = g.dims[0];
   const int64_t nrows = (int64_t)g.dims[1] * g.dims[2];
   if (g.tx1 <= g.tx0) return;
   for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < nrows;
        r += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t c0 = r * nx;
-#pragma unroll 1
-    for (int li = 0; li < 2; ++li) {
-      const int64_t off = (li == 0 ? ncells : 0) + c0;
-      const int32_t rb = beg[off + g.tx0], re = end[off + g.tx1 - 1];
-      if (re <= rb) continue;
-      int2* out = li == 0 ? blk_f : blk_b;
-      // Greedy whole-cell blocks: a block never starts or ends inside a cell unless that
-      // cell alone holds more than BT targets (then it is split evenly), so its candidate
-      // rows span (cells + 2 reach) columns, not one more.
-      int32_t b0 = rb, cur = rb;
-      for (int x = g.tx0; x < g.tx1; ++x) {
-        const int32_t ce = end[off + x];
-        if (ce == cur) continue;
-        if (ce - b0 > BT && cur > b0) {  // close the block before this cell
-          const uint32_t at = atomicAdd(&ctrl->nblk[li], 1u);
-          out[at] = make_int2(b0, cur);
-          b0 = cur;
-        }
-        if (ce - b0 > BT) {  // one oversized cell: even split into ceil(len / BT) blocks
-          const int32_t L = ce - b0, nbk = (L + BT - 1) / BT;
-          const uint32_t at = atomicAdd(&ctrl->nblk[li], (uint32_t)nbk);
-          for (int32_t b = 0; b < nbk; ++b)
-            out[at + b] = make_int2(b0 + (int32_t)(((int64_t)L * b) / nbk),
-                                    b0 + (int32_t)(((int64_t)L * (b + 1)) / nbk));
-          b0 = ce;
-        }
-        cur = ce;
+    const int64_t cb = r * nx, cf = ncells + r * nx;  // row offsets in the B / F tables
+    if (end[cf + g.tx1 - 1] <= beg[cf + g.tx0] && end[cb + g.tx1 - 1] <= beg[cb + g.tx0]) continue;
+    int32_t f0 = beg[cf + g.tx0], b0 = beg[cb + g.tx0];  // open block
+    int32_t fcur = f0, bcur = b0;
+    for (int x = g.tx0; x < g.tx1; ++x) {
+      const int32_t fe = end[cf + x], be = end[cb + x];
+      if (fe == fcur && be == bcur) continue;  // empty cell
+      if ((fe - f0) + (be - b0) > BT && (fcur > f0 || bcur > b0)) {  // close before this cell
+        emit_block(ctrl, blk, make_int4(f0, fcur, b0, bcur));
+        f0 = fcur;
+        b0 = bcur;
       }
-      if (cur > b0) {
-        const uint32_t at = atomicAdd(&ctrl->nblk[li], 1u);
-        out[at] = make_int2(b0, cur);
+      if ((fe - f0) + (be - b0) > BT) {  // one oversized cell: single-list chunks of <= BT
+        for (int32_t p = f0; p < fe; p += BT) emit_block(ctrl, blk, make_int4(p, min(p + BT, fe), be, be));
+        for (int32_t p = b0; p < be; p += BT) emit_block(ctrl, blk, make_int4(fe, fe, p, min(p + BT, be)));
+        f0 = fe;
+        b0 = be;
       }
+      fcur = fe;
+      bcur = be;
     }
+    if (fcur > f0 || bcur > b0) emit_block(ctrl, blk, make_int4(f0, fcur, b0, bcur));
   }
 }
 
@@ -423,7 +415,7 @@ __global__ void __launch_bounds__(256) k_blocks(sphb_grid_t g, int64_t ncells,
 extern __shared__ float4 g_sm4[];  // staged candidates: A | B | (C)
 extern __shared__ uint32_t g_sm32[];
 
-template <typename R, bool FLUID_ITEMS, bool G7, bool EQM>
+template <typename R, bool G7, bool EQM>
 __global__ void __launch_bounds__(NW * 32, 2) k_interact(KArgs a) {
   if (!step_live(a.ctrl)) return;
   const C32 c32 = pin_constants(a);
@@ -439,11 +431,9 @@ __global__ void __launch_bounds__(NW * 32, 2) k_interact(KArgs a) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nx = a.g.dims[0], ny = a.g.dims[1], nz = a.g.dims[2];
   const int reach = a.g.reach, side = 2 * reach + 1;
-  const int nlist = FLUID_ITEMS ? 2 : 1;
-  const int nseg = nlist * side * side;
-  const uint32_t nblocks = a.ctrl->nblk[FLUID_ITEMS ? 0 : 1];
+  const uint32_t nblocks = a.ctrl->nblk[0];
   const int64_t step = a.ctrl->step;
-  const int2* blocks = a.blocks;
+  const int4* blocks = a.blocks;
   uint32_t* myMask = sMask + warp * RING * 32;
   uint16_t* myBase = sBase + warp * RING * 32;
 
@@ -451,15 +441,20 @@ __global__ void __launch_bounds__(NW * 32, 2) k_interact(KArgs a) {
   double dtf_min = INFINITY, dtcv_min = INFINITY;
 
   for (;;) {
-    if (tid == 0) s_blk = (int)atomicAdd(&a.ctrl->tile_next[FLUID_ITEMS ? 0 : 1], 1u);
+    if (tid == 0) s_blk = (int)atomicAdd(&a.ctrl->tile_next[0], 1u);
     __syncthreads();
     const uint32_t blk = (uint32_t)s_blk;
     if (blk >= nblocks) break;
-    const int2 bb = blocks[blk];
-    const int i0 = bb.x, i1 = bb.y;
-    const int cfirst = a.cell[i0], clast = a.cell[i1 - 1];
+    const int4 bb = blocks[blk];
+    const int f0 = bb.x, nf = bb.y - bb.x, b0 = bb.z, nbt = bb.w - bb.z;
+    // the block's cells: one row, columns [cxa, cxb] (sorted lists: first/last targets)
+    const int cfirst = min(nf ? a.cell[f0] : INT_MAX, nbt ? a.cell[b0] : INT_MAX);
+    const int clast = max(nf ? a.cell[f0 + nf - 1] : -1, nbt ? a.cell[b0 + nbt - 1] : -1);
     const int rowkey = cfirst / nx;
     const int cxa = cfirst - rowkey * nx, cxb = clast - rowkey * nx;
+    // fluid targets need both lists' rows; a pure-boundary block only the fluid rows
+    const int nlist = nf ? 2 : 1;
+    const int nseg = nlist * side * side;
     const int gcz = rowkey / ny, gcy = rowkey - gcz * ny;
     const int bxlo = max(cxa - reach, 0), bxhi = min(cxb + reach, nx - 1);
     // FP16 screen frame: block centre, unit = 2h (Cfg<float> only)
@@ -477,7 +472,7 @@ __global__ void __launch_bounds__(NW * 32, 2) k_interact(KArgs a) {
       Seg sg = {0, 0, 0, 0};
       if (tid < nseg) {
         int li, rr;
-        if (FLUID_ITEMS && a.p.order == 1) {  // gather_fluid_ranges: all F rows, then all B rows
+        if (nlist == 2 && a.p.order == 1) {  // gather_fluid_ranges: all F rows, then all B rows
           li = tid / (side * side);
           rr = tid - li * side * side;
         } else {                              // gather_*_cells: per row F then B
@@ -524,9 +519,11 @@ __global__ void __launch_bounds__(NW * 32, 2) k_interact(KArgs a) {
     const int total = s_nseg_tot;
 
     // ---- this warp's targets
-    const int i = i0 + warp * 32 + lane;
-    const bool valid = i < i1;
-    const bool wactive = (i0 + warp * 32) < i1;
+    const int t = warp * 32 + lane;                 // fluid targets first, then boundary
+    const bool isf = t < nf;
+    const int i = isf ? f0 + t : b0 + (t - nf);
+    const bool valid = t < nf + nbt;
+    const bool wactive = warp * 32 < nf + nbt;
     Own<R> o;
     int xlo = 0, xhi = -1;
     if (valid) {
@@ -550,9 +547,10 @@ __global__ void __launch_bounds__(NW * 32, 2) k_interact(KArgs a) {
       for (int k = 0; k < nseg; ++k) {
         const Seg sg = sSeg[k];
         if (sg.g1 <= sg.g0) continue;
+        if (!isf && sg.rowoff < a.ncells) continue;  // boundary targets: fluid rows only
         cand += (unsigned long long)(a.end[sg.rowoff + xhi] - a.beg[sg.rowoff + xlo]);
       }
-      if (FLUID_ITEMS) cand -= 1;  // the reference skips j == i before counting (kernels.py:369-371)
+      if (isf) cand -= 1;  // the reference skips j == i before counting (kernels.py:369-371)
     }
 
     // Lock-step FIFO drain.  Each lane queued only its non-empty mask words (with the staged
@@ -672,7 +670,7 @@ __global__ void __launch_bounds__(NW * 32, 2) k_interact(KArgs a) {
               const uint32_t m1 = d1 >= 32 ? 0xffffffffu : (d1 <= 0 ? 0u : ((1u << d1) - 1u));
               bits &= m0 & m1;
             }
-            bits = valid ? bits : 0u;
+            bits = (valid && (isf || !boundary_list)) ? bits : 0u;  // B-B pairs are never visited
             if (__any_sync(SPHB_FULL, bits != 0u && tail == (uint32_t)RING)) drain();
             if (bits) {
               sts32(smMask + 128u * tail, bits);
@@ -693,7 +691,7 @@ __global__ void __launch_bounds__(NW * 32, 2) k_interact(KArgs a) {
     if (valid) {
       c_cand += cand;
       c_hits += pushed - rej;
-      if (FLUID_ITEMS) c_ff += (pushed - pushed_b) - rej_f;
+      if (isf) c_ff += (pushed - pushed_b) - rej_f;
       if (sizeof(R) == 4 && EQM) {  // the pair loop left the (equal) neighbour mass out
         s.ax *= (R)a.massf;
         s.ay *= (R)a.massf;
@@ -702,7 +700,7 @@ __global__ void __launch_bounds__(NW * 32, 2) k_interact(KArgs a) {
       }
       const double ax = (double)s.ax, ay = (double)s.ay, az = (double)s.az;
       const double dr = (double)s.dr, vd = (double)s.vd;
-      if (FLUID_ITEMS) {
+      if (isf) {
         a.acc[3 * (int64_t)i + 0] = ax;
         a.acc[3 * (int64_t)i + 1] = ay;
         a.acc[3 * (int64_t)i + 2] = az;
@@ -716,7 +714,7 @@ __global__ void __launch_bounds__(NW * 32, 2) k_interact(KArgs a) {
       if (!(isfinite(ax) && isfinite(ay) && isfinite(az) && isfinite(dr)))
         raise_div(a.ctrl, step, SPHB_DIV_NONFINITE_FORCES, 0);
       // compute_dt terms (sim.py:222-229); min is order-free so this is exact
-      if (FLUID_ITEMS) {
+      if (isf) {
         const double fx = xadd(ax, a.p.g[0]), fy = xadd(ay, a.p.g[1]), fz = xadd(az, a.p.g[2]);
         double fmag = __dsqrt_rn(xadd(xadd(xmul(fx, fx), xmul(fy, fy)), xmul(fz, fz)));
         fmag = fmag > 1e-30 ? fmag : 1e-30;
@@ -732,7 +730,7 @@ __global__ void __launch_bounds__(NW * 32, 2) k_interact(KArgs a) {
   c_hits = warp_sum_u64(c_hits);
   c_ff = warp_sum_u64(c_ff);
   if (lane == 0) {
-    if (FLUID_ITEMS && dtf_min < INFINITY) atomic_min_pos(&a.ctrl->dtmin_f, dtf_min);
+    if (dtf_min < INFINITY) atomic_min_pos(&a.ctrl->dtmin_f, dtf_min);
     if (dtcv_min < INFINITY) atomic_min_pos(&a.ctrl->dtmin_cv, dtcv_min);
     if (c_cand) atomicAdd((unsigned long long*)&a.ctrl->counters[0], c_cand);
     if (c_hits) {
@@ -749,38 +747,37 @@ constexpr size_t smem_bytes() {
          sizeof(uint32_t) * NW * RING * 32 + sizeof(uint16_t) * NW * RING * 32;
 }
 
-template <typename R, bool F, bool G7, bool EQM>
+template <typename R, bool G7, bool EQM>
 int launch_kernel(const KArgs& a, int nsm, cudaStream_t s) {
   static int grid = 0;
   const size_t bytes = smem_bytes<R>();
   if (grid == 0) {
-    cudaError_t e = cudaFuncSetAttribute(k_interact<R, F, G7, EQM>,
+    cudaError_t e = cudaFuncSetAttribute(k_interact<R, G7, EQM>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
     if (e != cudaSuccess)
       return sphb_set_error(SPHB_E_CUDA, "smem attribute: %s", cudaGetErrorString(e));
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_interact<R, F, G7, EQM>, NW * 32,
-                                                  bytes);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_interact<R, G7, EQM>, NW * 32, bytes);
     grid = nsm * (per_sm > 0 ? per_sm : 1);
   }
-  k_interact<R, F, G7, EQM><<<grid, NW * 32, bytes, s>>>(a);
+  k_interact<R, G7, EQM><<<grid, NW * 32, bytes, s>>>(a);
   return sphb_check_launch("k_interact");
 }
 
-template <typename R, bool F>
+template <typename R>
 int launch_one(const KArgs& a, int nsm, cudaStream_t s) {
-  if (sizeof(R) == 8) return launch_kernel<R, F, true, false>(a, nsm, s);
+  if (sizeof(R) == 8) return launch_kernel<R, true, false>(a, nsm, s);
   const bool eqm = a.p.mass_fluid == a.p.mass_boundary;
   if (a.gamma7)
-    return eqm ? launch_kernel<R, F, true, true>(a, nsm, s) : launch_kernel<R, F, true, false>(a, nsm, s);
-  return eqm ? launch_kernel<R, F, false, true>(a, nsm, s) : launch_kernel<R, F, false, false>(a, nsm, s);
+    return eqm ? launch_kernel<R, true, true>(a, nsm, s) : launch_kernel<R, true, false>(a, nsm, s);
+  return eqm ? launch_kernel<R, false, true>(a, nsm, s) : launch_kernel<R, false, false>(a, nsm, s);
 }
 
 }  // namespace
 
 int64_t interact_launch_count(int64_t n) {
   (void)n;
-  return 3;
+  return 2;
 }
 
 int launch_interact(sphb_workspace* ws, const sphb_params_t& p, const sphb_grid_t& g, int64_t n,
@@ -828,14 +825,10 @@ int launch_interact(sphb_workspace* ws, const sphb_params_t& p, const sphb_grid_
   const int64_t nrows = (int64_t)g.dims[1] * g.dims[2];
   int gb = (int)((nrows + 255) / 256);
   if (gb > 148 * 8) gb = 148 * 8;
-  k_blocks<<<gb, 256, 0, s>>>(g, a.ncells, beg, end, ws->blocks[0], ws->blocks[1], ctrl);
+  k_blocks<<<gb, 256, 0, s>>>(g, a.ncells, beg, end, ws->blocks, ctrl);
   if (int rc = sphb_check_launch("k_blocks")) return rc;
-  int rc;
-  a.blocks = ws->blocks[0];  // fluid items [nb, n): F-F + F-B
-  rc = p.precision == SPHB_FP64 ? launch_one<double, true>(a, nsm, s)
-                                : launch_one<float, true>(a, nsm, s);
-  if (rc) return rc;
-  a.blocks = ws->blocks[1];  // boundary items [0, nb): B-F only, drho + visc
-  return p.precision == SPHB_FP64 ? launch_one<double, false>(a, nsm, s)
-                                  : launch_one<float, false>(a, nsm, s);
+  // one launch for both item classes: fluid targets (F-F + F-B) and boundary targets (B-F,
+  // drho + visc only) of the same cells share the staged candidates
+  a.blocks = ws->blocks;
+  return p.precision == SPHB_FP64 ? launch_one<double>(a, nsm, s) : launch_one<float>(a, nsm, s);
 }

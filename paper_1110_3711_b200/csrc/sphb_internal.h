@@ -22,7 +22,7 @@ struct sphb_workspace {
   uint32_t* radix_hist = nullptr;   // RADIX * max tiles
   uint32_t* digit_total = nullptr;  // RADIX
   uint32_t* scan_partials = nullptr;
-  int2* blocks[2] = {nullptr, nullptr};  // interaction target blocks (fluid, boundary lists)
+  int4* blocks = nullptr;  // interaction target blocks (fluid i0,i1, boundary i0,i1)
   int64_t max_blocks = 0;
   int64_t max_sort_tiles = 0, max_scan_tiles = 0;
   size_t bytes = 0;
