@@ -34,7 +34,7 @@ BYTES_NL_SU = 324 - 52                # compulsory NL+SU bytes
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default=None, help="c1|c2|c3|c4_1..c4_8 (default c3 at N=1, c4_N above)")
@@ -87,7 +87,7 @@ class Clocks:
         self.proc = None
         try:
             self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                                          "-lms", "200", "-i", str(index)], stdout=subprocess.PIPE,
+                                          "-lms", "100", "-i", str(index)], stdout=subprocess.PIPE,
                                          stderr=subprocess.DEVNULL, text=True)
         except Exception:
             self.proc = None
@@ -394,10 +394,10 @@ def main():
         "pair_evals_per_s": evals * world * args.steps / (total_ms * 1e-3),
         "stage_ms": {"nl": float(np.mean(nl_ms)), "pi": pi_mean, "su": float(np.mean(su_ms))},
         "counters_per_step": {"candidates": cand, "force_evals": evals, "true_pairs": true_pairs},
-        "roofline": {"bound": "fp32", "kernel": "k_interact (fluid + boundary launches)",
+        "roofline": {"bound": "fp32", "kernel": "k_interact_v8 (one launch: fluid + boundary targets)",
                      "achieved": achieved, "peak": fp32, "unit": "TFLOP/s",
                      "frac": achieved / fp32, "traffic": traffic,
-                     "traffic_note": ("dram read+write bytes of the fluid launch, " + traffic_src)
+                     "traffic_note": ("dram read+write bytes of one launch, " + traffic_src)
                      if traffic else None,
                      "algorithmic_bytes": 52 * system.n,
                      "work": f"{FLOP_PER_CAND}*candidates + {FLOP_PER_EVAL}*evals per launch",

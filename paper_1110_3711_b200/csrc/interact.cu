@@ -47,6 +47,9 @@ constexpr int BT = NW * 32;      // targets per block
 #ifndef SPHB_H16
 #define SPHB_H16 1
 #endif
+#ifndef SPHB_V8
+#define SPHB_V8 1  // FP32 path: packed FFMA2 kernel (k_interact_v8); 0 = the generic template
+#endif
 constexpr int RING = SPHB_H16 ? 32 : 48;  // per-lane FIFO entries (non-empty 32-candidate words)
 constexpr int MAXSEG = 128;      // stencil row segments per block (2 lists x (2r+1)^2, r <= 3)
 
@@ -68,6 +71,10 @@ struct Cfg<double> {
 // 1.025.  Valid while |x| <= 4 (the block's x extent <= 8 support radii): coordinate
 // quantisation <= 2^-9, |d(r^2)| <= 1.6e-2 at the cutoff, so no true hit is screened out.
 constexpr float H16_THR = 1.025f;
+// v8 screen (thr - r^2 as one HFMA2 chain): |d(r^2)| <= 9.1e-3 at the cutoff (coordinate
+// rounding 2^-10 per operand, HADD2 2^-12, three FMA roundings 2^-11), so 1.015 keeps a
+// 1.6x margin while admitting fewer false maybes than 1.025.
+constexpr float H16_THR8 = 1.015f;
 constexpr float H16_MAXABS = 4.0f;
 
 struct KArgs {
@@ -741,6 +748,623 @@ __global__ void __launch_bounds__(NW * 32, 2) k_interact(KArgs a) {
   }
 }
 
+// ====================================================================== FP32 kernel (v8)
+// Same block decomposition, staging and FIFO discipline as k_interact, retuned for the
+// issue rate of sm_100a:
+//   * screen: FP16x2, thr - dx^2 - dy^2 - dz^2 as one HADD2/HFMA2 chain per coordinate,
+//     the miss flags are the sign bits, gathered 8 at a time with a sign-replicating PRMT
+//     (2 instructions per 4 candidates instead of a compare + shift/or per candidate).  The
+//     resulting mask is bit-permuted: bit 8j + k <-> candidate 4k + j of the word; pops map
+//     it back with one IMAD + LOP3.  The target itself is cleared from its own row's mask.
+//   * FIFO entries are (mask, staged byte address) pairs, one LDS.64 per refill; pops take
+//     the highest set bit (FLO, no BREV).
+//   * pair math: the two candidates a lane pops per iteration run as one packed FP32x2
+//     chain (FFMA2/FADD2/FMUL2, half the issue slots), with the constants folded
+//     (-alpha h into cs, W(dp)^-4 into the tensile factors, 3 kc/h and the neighbour mass
+//     into the mask factor) and viscosity as max(., 0) (the term is positive iff v.r < 0).
+//     Masked slots read finite staged data and are zeroed through the mask factor.
+//   * counters: hits per lane accumulate in a packed float; ff = sum over fluid targets
+//     minus sum over boundary targets (F-B and B-F hit sets are mirror images).
+// Accumulation order differs from the reference inside each 32-candidate word only; the
+// FP32 path's contract is rel 1e-5 (the FP64 path above stays bit-exact).
+typedef unsigned long long f2_t;
+__device__ __forceinline__ f2_t pk(float a, float b) {
+  f2_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ f2_t bc(float a) { return pk(a, a); }
+__device__ __forceinline__ float lo(f2_t v) {
+  float a, b;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+  return a;
+}
+__device__ __forceinline__ float hi(f2_t v) {
+  float a, b;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+  return b;
+}
+__device__ __forceinline__ f2_t add2(f2_t a, f2_t b) {
+  f2_t r;
+  asm("add.rn.ftz.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ f2_t sub2(f2_t a, f2_t b) {
+  f2_t r;
+  asm("sub.rn.ftz.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ f2_t mul2(f2_t a, f2_t b) {
+  f2_t r;
+  asm("mul.rn.ftz.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ f2_t fma2(f2_t a, f2_t b, f2_t c) {
+  f2_t r;
+  asm("fma.rn.ftz.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+__device__ __forceinline__ void lds_2x64(uint32_t addr, f2_t& a, f2_t& b) {
+  asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "r"(addr));
+}
+__device__ __forceinline__ float rcp_approx(float x) {  // MUFU.RCP, no slow path
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ uint2 lds64u(uint32_t addr) {
+  uint2 v;
+  asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ void sts64u(uint32_t addr, uint32_t x, uint32_t y) {
+  asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(addr), "r"(x), "r"(y));
+}
+// sign-replicating byte permute: result byte n = 0xff if the msb of the selected byte is set
+__device__ __forceinline__ uint32_t prmt_sign(uint32_t a, uint32_t b) {
+  uint32_t r;
+  asm("prmt.b32 %0, %1, %2, 0xFDB9;" : "=r"(r) : "r"(a), "r"(b));
+  return r;
+}
+__device__ __forceinline__ int flo32(uint32_t v) {  // index of the highest set bit, -1 if none
+  int r;
+  asm("bfind.u32 %0, %1;" : "=r"(r) : "r"(v));
+  return r;
+}
+__device__ __forceinline__ uint32_t clear_bit(uint32_t v, int t) {  // bit t is set; t = -1: v
+  uint32_t m;
+  asm("shl.b32 %0, 1, %1;" : "=r"(m) : "r"(t));
+  return v ^ m;
+}
+// bit position of candidate c (0..31) of a word in the permuted screen layout
+__host__ __device__ constexpr int perm_bit(int c) { return 8 * (c & 3) + (c >> 2); }
+struct PermGe {
+  uint32_t v[33];
+};
+__host__ __device__ constexpr PermGe make_perm_ge() {
+  PermGe t{};
+  for (int a = 0; a <= 32; ++a) {
+    uint32_t m = 0;
+    for (int c = a; c < 32; ++c) m |= 1u << perm_bit(c);
+    t.v[a] = m;
+  }
+  return t;
+}
+__constant__ PermGe c_perm_ge = make_perm_ge();  // candidates >= a of a word, permuted bits
+
+struct K32 {  // folded FP32 constants of the v8 pair loop
+  float sup2_lo, sup2_hi, tiny, invh, eta2, kcs, tpos, tneg, nkgc, nkgc_b, cs_exp, ktw4;
+};
+
+struct Own32 {
+  f2_t xy, vxy;
+  float x, y, z, vz, rho, prrho, csn, tenk;  // csn = -alpha h cs_i, tenk = tensil_i / W(dp)^4
+};
+
+struct Acc32 {
+  f2_t axy, az, dr, hits;
+  float vd;
+};
+
+constexpr int V8_ROWS = 2304 + 8;  // staged rows: SCAP candidates + the dummy (row SCAP)
+#ifndef V8_NG
+#define V8_NG 3    // candidate pairs per lane per drain iteration (independent FP32x2 chains)
+#endif
+#ifndef V8_KMIN
+#define V8_KMIN 6  // minimum iterations of a partial drain
+#endif
+
+// NG groups of two popped candidates (staged byte addresses of their A rows) of one lane.
+// Each group is one packed FP32x2 chain; the groups are independent (ILP), and the rare
+// exact re-decision is one warp-uniform branch for all of them.
+struct Geo2 {
+  f2_t a1xy, a1zw, b1zw, a2xy, a2zw, b2zw, dxy1, dxy2, dz, r2, dot;
+};
+
+template <bool G7, bool EQM, int NG>
+__device__ __forceinline__ void eval_v8(const KArgs& a, const K32& c, const Own32& o,
+                                        const uint32_t (&ad)[2 * NG], int xlo, int xhi,
+                                        Acc32 (&s)[NG]) {
+  constexpr uint32_t OFFB = 16u * V8_ROWS;  // A -> B rows
+  Geo2 g[NG];
+  bool ok[2 * NG], cold[2 * NG];
+  bool anycold = false;
+#pragma unroll
+  for (int k = 0; k < NG; ++k) {
+    f2_t b1xy, b2xy;
+    lds_2x64(ad[2 * k], g[k].a1xy, g[k].a1zw);
+    lds_2x64(ad[2 * k + 1], g[k].a2xy, g[k].a2zw);
+    lds_2x64(ad[2 * k] + OFFB, b1xy, g[k].b1zw);
+    lds_2x64(ad[2 * k + 1] + OFFB, b2xy, g[k].b2zw);
+    g[k].dxy1 = sub2(o.xy, g[k].a1xy);
+    g[k].dxy2 = sub2(o.xy, g[k].a2xy);
+    const f2_t dvxy1 = sub2(o.vxy, b1xy), dvxy2 = sub2(o.vxy, b2xy);
+    const f2_t sq1 = mul2(g[k].dxy1, g[k].dxy1), sq2 = mul2(g[k].dxy2, g[k].dxy2);
+    const f2_t dd1 = mul2(dvxy1, g[k].dxy1), dd2 = mul2(dvxy2, g[k].dxy2);
+    g[k].dz = pk(o.z - lo(g[k].a1zw), o.z - lo(g[k].a2zw));
+    const f2_t dvz = pk(o.vz - lo(g[k].b1zw), o.vz - lo(g[k].b2zw));
+    g[k].r2 = fma2(g[k].dz, g[k].dz, pk(lo(sq1) + hi(sq1), lo(sq2) + hi(sq2)));
+    g[k].dot = fma2(dvz, g[k].dz, pk(lo(dd1) + hi(dd1), lo(dd2) + hi(dd2)));
+    // non-short-circuit predicates; an empty slot reads the dummy row (r2 ~ 1e8 sup2):
+    // never a hit, never cold
+    const float r21 = lo(g[k].r2), r22 = hi(g[k].r2);
+    ok[2 * k] = (r21 < c.sup2_lo) & (r21 > c.tiny);
+    ok[2 * k + 1] = (r22 < c.sup2_lo) & (r22 > c.tiny);
+    cold[2 * k] = !ok[2 * k] & (r21 < c.sup2_hi);
+    cold[2 * k + 1] = !ok[2 * k + 1] & (r22 < c.sup2_hi);
+    anycold = anycold | cold[2 * k] | cold[2 * k + 1];
+  }
+  if (__any_sync(SPHB_FULL, anycold)) {
+    // guard band / coincident (lattice ties sit exactly on the cutoff): exact f64 decision,
+    // one candidate per lane per round so the f64 path is issued once, not once per slot
+    uint32_t cm = 0, okm = 0;
+#pragma unroll
+    for (int k = 0; k < 2 * NG; ++k) {
+      cm |= (cold[k] ? 1u : 0u) << k;
+      okm |= (ok[k] ? 1u : 0u) << k;
+    }
+    do {
+      const int k = __ffs(cm) - 1;
+      uint32_t adk = ad[0];
+#pragma unroll
+      for (int kk = 1; kk < 2 * NG; ++kk) adk = k == kk ? ad[kk] : adk;
+      if (cm) {
+        const float4 A = lds4(adk);
+        if (cold_accept(a, o.x, o.y, o.z, A, xlo, xhi)) okm |= 1u << k;
+        cm &= cm - 1u;
+      }
+    } while (__any_sync(SPHB_FULL, cm != 0u));
+#pragma unroll
+    for (int k = 0; k < 2 * NG; ++k) ok[k] = (okm >> k) & 1u;
+  }
+#pragma unroll
+  for (int k = 0; k < NG; ++k) {
+    const bool ok1 = ok[2 * k], ok2 = ok[2 * k + 1];
+    const f2_t OK = pk(ok1 ? 1.0f : 0.0f, ok2 ? 1.0f : 0.0f);
+    const f2_t R2M = pk(ok1 ? lo(g[k].r2) : c.sup2_lo, ok2 ? hi(g[k].r2) : c.sup2_lo);
+    const f2_t RINV = pk(rsqrtf(lo(R2M)), rsqrtf(hi(R2M)));
+    const f2_t Q = mul2(mul2(R2M, RINV), bc(c.invh));
+    const f2_t T = sub2(bc(2.0f), Q);
+    const f2_t UM = sub2(Q, bc(1.0f));
+    const f2_t UN = pk(fminf(lo(UM), 0.0f), fminf(hi(UM), 0.0f));  // -max(1 - q, 0)
+    const f2_t T2Q = mul2(mul2(T, T), bc(0.25f));
+    const f2_t U2 = mul2(UN, UN);
+    const f2_t W = fma2(T2Q, T, mul2(U2, UN));  // t^3/4 - u^3
+    const f2_t DW3 = sub2(U2, T2Q);             // (3 u^2 - 3/4 t^2) / 3
+    const float sr1 = hi(g[k].b1zw), sr2 = hi(g[k].b2zw);
+    const float rj1 = fabsf(sr1), rj2 = fabsf(sr2);
+    const f2_t RHOJ = pk(rj1, rj2);
+    f2_t MJ;  // mask factor: ok * (-3 kc/h) [* m_j]
+    if (EQM) {
+      MJ = mul2(OK, bc(c.nkgc));
+    } else {
+      MJ = mul2(OK, pk(sr1 < 0.0f ? c.nkgc_b : c.nkgc, sr2 < 0.0f ? c.nkgc_b : c.nkgc));
+    }
+    const f2_t GCN = mul2(mul2(DW3, RINV), MJ);  // -gc [m_j], zero when masked
+    f2_t CSJ;                                    // -alpha h cs_j
+    if (G7) {
+      const f2_t RR = mul2(RHOJ, bc(c.kcs));
+      CSJ = mul2(mul2(RR, RR), RR);
+    } else {
+      CSJ = mul2(pk(exp2f(c.cs_exp * __log2f(rj1)), exp2f(c.cs_exp * __log2f(rj2))), bc(c.kcs));
+    }
+    const float pr1 = hi(g[k].a1zw), pr2 = hi(g[k].a2zw);
+    const f2_t TENJ = pk(pr1 * (pr1 > 0.0f ? c.tpos : c.tneg), pr2 * (pr2 > 0.0f ? c.tpos : c.tneg));
+    const f2_t PSUM = pk(o.prrho + pr1, o.prrho + pr2);
+    const f2_t E = add2(R2M, bc(c.eta2));
+    const f2_t MU = mul2(mul2(g[k].dot, pk(rcp_approx(lo(E)), rcp_approx(hi(E)))), OK);  // mu / h
+    const f2_t RS = add2(RHOJ, bc(o.rho));
+    const f2_t VT = mul2(mul2(add2(CSJ, bc(o.csn)), MU), pk(rcp_approx(lo(RS)), rcp_approx(hi(RS))));
+    const f2_t VISC = pk(fmaxf(lo(VT), 0.0f), fmaxf(hi(VT), 0.0f));
+    const f2_t W2 = mul2(W, W);
+    const f2_t PT = fma2(mul2(add2(TENJ, bc(o.tenk)), W2), W2, add2(PSUM, VISC));
+    const f2_t FM = mul2(PT, GCN);
+    s[k].axy = fma2(g[k].dxy1, bc(lo(FM)), s[k].axy);
+    s[k].axy = fma2(g[k].dxy2, bc(hi(FM)), s[k].axy);
+    s[k].az = fma2(g[k].dz, FM, s[k].az);
+    s[k].dr = fma2(GCN, g[k].dot, s[k].dr);
+    s[k].vd = fmaxf(s[k].vd, fmaxf(fabsf(lo(MU)), fabsf(hi(MU))));
+    s[k].hits = add2(s[k].hits, OK);
+  }
+}
+
+template <bool G7, bool EQM>
+__global__ void __launch_bounds__(NW * 32, 2) k_interact_v8(KArgs a, K32 k32) {
+  if (!step_live(a.ctrl)) return;
+  constexpr int SCAP = Cfg<float>::SCAP;
+  constexpr int RINGC = 24;                               // FIFO entries per lane (8 B)
+  constexpr int MASK0 = (32 * V8_ROWS + 6 * SCAP) / 4;  // uint32 offset of the FIFO
+  __shared__ Seg sSeg[MAXSEG];
+  __shared__ int s_blk, s_nseg_tot, s_scan[MAXSEG];
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nx = a.g.dims[0], ny = a.g.dims[1], nz = a.g.dims[2];
+  const int reach = a.g.reach, side = 2 * reach + 1;
+  const uint32_t nblocks = a.ctrl->nblk[0];
+  const int64_t step = a.ctrl->step;
+  // the dummy row popped by empty FIFO slots: far away (r2 ~ 1e8 sup2), at rest, finite
+  if (tid == 0) {
+    const float far = (float)(1e4 * 2.0 * a.p.h);
+    g_sm4[SCAP] = make_float4(far, far, far, 0.f);
+    g_sm4[V8_ROWS + SCAP] = make_float4(0.f, 0.f, 0.f, 1.f);
+  }
+
+  const uint32_t smA = pin_u32(smem_addr(g_sm4));
+  const uint32_t smH = smA + 32u * V8_ROWS;
+  const uint32_t dummy = smA + 16u * SCAP;
+  // FIFO: [NW][RINGC][32 lanes] of (mask u32, staged row address u32)
+  const uint32_t ring = pin_u32(smem_addr(g_sm32 + MASK0) + 8u * (warp * RINGC * 32 + lane));
+  const uint32_t rend = ring + 256u * RINGC;
+
+  unsigned long long c_cand = 0, c_hits = 0;
+  long long c_ff = 0;
+  double dtf_min = INFINITY, dtcv_min = INFINITY;
+
+  for (;;) {
+    __syncthreads();
+    if (tid == 0) s_blk = (int)atomicAdd(&a.ctrl->tile_next[0], 1u);
+    __syncthreads();
+    const uint32_t blk = (uint32_t)s_blk;
+    if (blk >= nblocks) break;
+    const int4 bb = a.blocks[blk];
+    const int f0 = bb.x, nf = bb.y - bb.x, b0 = bb.z, nbt = bb.w - bb.z;
+    const int cfirst = min(nf ? a.cell[f0] : INT_MAX, nbt ? a.cell[b0] : INT_MAX);
+    const int clast = max(nf ? a.cell[f0 + nf - 1] : -1, nbt ? a.cell[b0 + nbt - 1] : -1);
+    const int rowkey = cfirst / nx;
+    const int cxa = cfirst - rowkey * nx, cxb = clast - rowkey * nx;
+    const int nlist = nf ? 2 : 1;
+    const int nseg = nlist * side * side;
+    const int gcz = rowkey / ny, gcy = rowkey - gcz * ny;
+    const int bxlo = max(cxa - reach, 0), bxhi = min(cxb + reach, nx - 1);
+    const double cs = a.g.cell_size;
+    const float h16_s = (float)(0.5 * a.p.invh);
+    const float h16_xc = (float)(a.g.origin[0] + 0.5 * (bxlo + bxhi + 1) * cs);
+    const float h16_yc = (float)(a.g.origin[1] + (gcy + 0.5) * cs);
+    const float h16_zc = (float)(a.g.origin[2] + (gcz + 0.5) * cs);
+    const bool use16 = (0.5 * (bxhi - bxlo + 1) * cs * (0.5 * a.p.invh) <= H16_MAXABS) &&
+                       ((reach + 0.5) * cs * (0.5 * a.p.invh) <= H16_MAXABS);
+    // the fluid targets' own row (fluid list, dy = dz = 0)
+    const int rr_c = reach * side + reach;
+    const int selfseg = nf ? ((nlist == 2 && a.p.order == 1) ? rr_c : rr_c * nlist) : -1;
+
+    if (tid < MAXSEG) {
+      int len = 0;
+      Seg sg = {0, 0, 0, 0};
+      if (tid < nseg) {
+        int li, rr;
+        if (nlist == 2 && a.p.order == 1) {
+          li = tid / (side * side);
+          rr = tid - li * side * side;
+        } else {
+          li = tid % nlist;
+          rr = tid / nlist;
+        }
+        const int dz = rr / side - reach, dy = rr % side - reach;
+        const int zz = gcz + dz, yy = gcy + dy;
+        if (zz >= 0 && zz < nz && yy >= 0 && yy < ny) {
+          const int64_t rowoff = (li == 0 ? a.ncells : 0) + (int64_t)nx * (yy + (int64_t)ny * zz);
+          sg.g0 = a.beg[rowoff + bxlo];
+          sg.g1 = a.end[rowoff + bxhi];
+          sg.rowoff = (int)rowoff;
+          len = max(sg.g1 - sg.g0, 0);
+          if (len == 0) sg.g1 = sg.g0;
+        }
+      }
+      s_scan[tid] = len;
+      sSeg[tid] = sg;
+    }
+    __syncthreads();
+    if (warp == 0) {
+      int v[4], run = 0;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        v[k] = s_scan[lane * 4 + k];
+        run += v[k];
+      }
+      int incl = run;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        int y = __shfl_up_sync(SPHB_FULL, incl, o);
+        if (lane >= o) incl += y;
+      }
+      int ex = incl - run;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        sSeg[lane * 4 + k].pos = ex;
+        ex += v[k];
+      }
+      if (lane == 31) s_nseg_tot = incl;
+    }
+    __syncthreads();
+    const int total = s_nseg_tot;
+
+    const int t = warp * 32 + lane;
+    const bool isf = t < nf;
+    const int i = isf ? f0 + t : b0 + (t - nf);
+    const bool valid = t < nf + nbt;
+    const bool wactive = warp * 32 < nf + nbt;
+    Own32 o;
+    float ocs = 0.f;
+    int xlo = 0, xhi = -1;
+    {
+      float4 pi = make_float4(0.f, 0.f, 0.f, 0.f), vi = make_float4(0.f, 0.f, 0.f, 1.f),
+             xi = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (valid) {
+        pi = a.posp[i];
+        vi = a.velr[i];
+        xi = a.aux[i];
+        const int cxi = a.cell[i] - rowkey * nx;
+        xlo = max(cxi - reach, 0);
+        xhi = min(cxi + reach, nx - 1);
+      }
+      o.x = pi.x; o.y = pi.y; o.z = pi.z; o.vz = vi.z; o.rho = vi.w;
+      o.xy = pk(pi.x, pi.y);
+      o.vxy = pk(vi.x, vi.y);
+      o.prrho = xi.x;
+      ocs = xi.y;
+      o.csn = (float)(-a.p.alpha * a.p.h) * xi.y;
+      o.tenk = xi.z * k32.ktw4;
+    }
+    const int wxlo = __reduce_min_sync(SPHB_FULL, valid ? xlo : INT_MAX);
+    const int wxhi = __reduce_max_sync(SPHB_FULL, valid ? xhi : INT_MIN);
+    Acc32 s[V8_NG];
+#pragma unroll
+    for (int k = 0; k < V8_NG; ++k) {
+      s[k].axy = s[k].az = s[k].dr = s[k].hits = bc(0.0f);
+      s[k].vd = 0.0f;
+    }
+    unsigned long long cand = 0;
+    if (valid) {
+      for (int k = 0; k < nseg; ++k) {
+        const Seg sg = sSeg[k];
+        if (sg.g1 <= sg.g0) continue;
+        if (!isf && sg.rowoff < a.ncells) continue;
+        cand += (unsigned long long)(a.end[sg.rowoff + xhi] - a.beg[sg.rowoff + xlo]);
+      }
+      if (isf) cand -= 1;
+    }
+
+    const __half2 thr16 = __float2half2_rn(H16_THR8);
+    const __half2 ohx = __float2half2_rn((o.x - h16_xc) * h16_s);
+    const __half2 ohy = __float2half2_rn((o.y - h16_yc) * h16_s);
+    const __half2 ohz = __float2half2_rn((o.z - h16_zc) * h16_s);
+
+    // Per-lane circular FIFO of non-empty screen words: (mask, staged row address).  A
+    // partial drain runs K lock-step iterations of 2*V8_NG pops per lane; pend counts the
+    // lane's queued maybes (every pop yields one while pend > 0).
+    // Entries are (mask, row address) pairs, 8 B, RINGC per lane; hp / tp are the lane's read
+    // and write entry addresses (stride 256 B: 32 lanes), cnt the entries queued.  An
+    // exhausted FIFO points cb at the dummy row: the empty pop (bfind = -1) lands on it.
+    uint32_t hp = ring, tp = ring, cnt = 0, pend = 0, cur = 0u, cb = dummy - 0x1b0u;
+    auto pop = [&]() -> uint32_t {
+      const bool need = cur == 0u, have = cnt != 0u;
+      if (need & have) {
+        const uint2 e = lds64u(hp);
+        cur = e.x;
+        cb = e.y;
+        hp = hp + 256u == rend ? ring : hp + 256u;
+        --cnt;
+      }
+      cb = (need & !have) ? dummy - 0x1b0u : cb;
+      const int tb = flo32(cur);
+      cur = clear_bit(cur, tb);
+      // bit 8j + k <-> candidate 4k + j: byte offset 16 (4k + j) = (tb * 66) & 0x1f0
+      return cb + (((uint32_t)tb * 66u) & 0x1f0u);
+    };
+    auto drain = [&](bool full) {
+      __syncwarp();
+      constexpr uint32_t P = 2 * V8_NG;  // pops per lane per iteration
+      const uint32_t mx = __reduce_max_sync(SPHB_FULL, pend);
+      uint32_t K = (mx + P - 1) / P;
+      if (!full) {  // enough to free ring space without idling the lightest busy lane
+        const uint32_t mn = __reduce_min_sync(SPHB_FULL, pend ? pend : 0xffffffffu);
+        K = min(K, max((mn + P - 1) / P, (uint32_t)V8_KMIN));
+      }
+      for (uint32_t it = 0; it < K; ++it) {
+        uint32_t ad[2 * V8_NG];
+#pragma unroll
+        for (int k = 0; k < 2 * V8_NG; ++k) ad[k] = pop();
+        eval_v8<G7, EQM, V8_NG>(a, k32, o, ad, xlo, xhi, s);
+      }
+      pend = pend > P * K ? pend - P * K : 0u;
+      __syncwarp();
+    };
+
+    for (int q0 = 0; q0 < total; q0 += SCAP) {
+      const int q1 = min(q0 + SCAP, total);
+      {
+        // STG rows in flight per thread: all loads of a chunk are issued before its stores
+        constexpr int U = 4;
+        int sk = 0;
+        __half* h = reinterpret_cast<__half*>(g_sm4 + 2 * V8_ROWS);
+        for (int p0 = q0 + tid; p0 < q1; p0 += U * NW * 32) {
+          int jj[U];
+          bool bl[U];
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const int p = p0 + u * NW * 32;
+            jj[u] = -1;
+            bl[u] = false;
+            if (p < q1) {
+              while (sSeg[sk].pos + (sSeg[sk].g1 - sSeg[sk].g0) <= p) ++sk;
+              jj[u] = sSeg[sk].g0 + (p - sSeg[sk].pos);
+              bl[u] = sSeg[sk].rowoff < a.ncells;
+            }
+          }
+          float4 pp[U], vr[U];
+          float xa[U];
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            if (jj[u] >= 0) {
+              pp[u] = __ldg(&a.posp[jj[u]]);
+              vr[u] = __ldg(&a.velr[jj[u]]);
+              xa[u] = __ldg(&a.aux[jj[u]].x);
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const int r = p0 + u * NW * 32 - q0;
+            if (jj[u] >= 0) {
+              g_sm4[r] = make_float4(pp[u].x, pp[u].y, pp[u].z, xa[u]);
+              g_sm4[V8_ROWS + r] = make_float4(vr[u].x, vr[u].y, vr[u].z, bl[u] ? -vr[u].w : vr[u].w);
+              h[r] = __float2half_rn((pp[u].x - h16_xc) * h16_s);
+              h[SCAP + r] = __float2half_rn((pp[u].y - h16_yc) * h16_s);
+              h[2 * SCAP + r] = __float2half_rn((pp[u].z - h16_zc) * h16_s);
+            }
+          }
+        }
+      }
+      __syncthreads();
+      if (wactive) {
+        for (int k = 0; k < nseg; ++k) {
+          const Seg sg = sSeg[k];
+          const int len = sg.g1 - sg.g0;
+          if (len <= 0 || sg.pos >= q1 || sg.pos + len <= q0) continue;
+          const int wg0 = a.beg[sg.rowoff + wxlo], wg1 = a.end[sg.rowoff + wxhi];
+          const int lo_ = max(sg.pos + (wg0 - sg.g0), q0) - q0;
+          const int hi_ = min(sg.pos + (wg1 - sg.g0), q1) - q0;
+          if (hi_ <= lo_) continue;
+          const bool boundary_list = sg.rowoff < a.ncells;
+          const uint32_t lanemask = (valid && (isf || !boundary_list)) ? 0xffffffffu : 0u;
+          const uint32_t lflag = boundary_list ? 1u : 0u;  // (unused by the v8 drain)
+          (void)lflag;
+          // own staged position in the self row (fluid targets), else out of range
+          const int selfpos = (k == selfseg && isf) ? sg.pos + (i - sg.g0) - q0 : INT_MIN / 2;
+          const int lo8 = use16 ? (lo_ & ~7) : lo_;
+          for (int k0 = lo8; k0 < hi_; k0 += 32) {
+            uint32_t miss = 0;
+            if (use16) {
+              const uint32_t hx = smH + 2u * k0, hy = hx + 2u * SCAP, hz = hy + 2u * SCAP;
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                const uint4 vx = lds128u(hx + 16u * q), vy = lds128u(hy + 16u * q),
+                            vz = lds128u(hz + 16u * q);
+                const uint32_t ux[4] = {vx.x, vx.y, vx.z, vx.w}, uy[4] = {vy.x, vy.y, vy.z, vy.w},
+                               uz[4] = {vz.x, vz.y, vz.z, vz.w};
+                uint32_t r[4];
+#pragma unroll
+                for (int w = 0; w < 4; ++w) {
+                  const __half2 dx = __hsub2(ohx, u32_as_h2(ux[w]));
+                  const __half2 dy = __hsub2(ohy, u32_as_h2(uy[w]));
+                  const __half2 dz = __hsub2(ohz, u32_as_h2(uz[w]));
+                  __half2 e = __hfma2(__hneg2(dx), dx, thr16);
+                  e = __hfma2(__hneg2(dy), dy, e);
+                  e = __hfma2(__hneg2(dz), dz, e);
+                  memcpy(&r[w], &e, 4);
+                }
+                // candidates 8q .. 8q+3 -> byte j bit 2q, 8q+4 .. 8q+7 -> bit 2q+1
+                miss |= prmt_sign(r[0], r[1]) & (0x01010101u << (2 * q));
+                miss |= prmt_sign(r[2], r[3]) & (0x01010101u << (2 * q + 1));
+              }
+            } else {
+              const uint32_t sk = smA + 16u * k0;
+#pragma unroll
+              for (int tt = 0; tt < 32; ++tt) {
+                const float4 A = lds4(sk + 16u * tt);
+                const float dx = o.x - A.x, dy = o.y - A.y, dz = o.z - A.z;
+                if (!(fmaf(dz, dz, fmaf(dy, dy, dx * dx)) < k32.sup2_hi)) miss |= 1u << perm_bit(tt);
+              }
+            }
+            uint32_t m = lanemask;
+            if (k0 < lo_ || k0 + 32 > hi_)
+              m &= c_perm_ge.v[max(lo_ - k0, 0)] & ~c_perm_ge.v[min(hi_ - k0, 32)];
+            uint32_t bits = m & ~miss;
+            {
+              const int d = selfpos - k0;
+              if ((unsigned)d < 32u) bits &= ~(1u << perm_bit(d));
+            }
+            if (__any_sync(SPHB_FULL, bits != 0u && cnt == (uint32_t)RINGC)) drain(false);
+            if (bits) {
+              sts64u(tp, bits, smA + 16u * (uint32_t)k0);
+              tp = tp + 256u == rend ? ring : tp + 256u;
+              ++cnt;
+              pend += __popc(bits);
+            }
+          }
+        }
+        drain(true);
+      }
+      __syncthreads();
+    }
+
+    if (valid) {
+#pragma unroll
+      for (int k = 1; k < V8_NG; ++k) {
+        s[0].axy = add2(s[0].axy, s[k].axy);
+        s[0].az = add2(s[0].az, s[k].az);
+        s[0].dr = add2(s[0].dr, s[k].dr);
+        s[0].hits = add2(s[0].hits, s[k].hits);
+        s[0].vd = fmaxf(s[0].vd, s[k].vd);
+      }
+      const int hits = (int)(lo(s[0].hits) + hi(s[0].hits));
+      c_cand += cand;
+      c_hits += (unsigned long long)hits;
+      c_ff += isf ? hits : -hits;  // ff = F targets' hits - B targets' hits (F-B == B-F)
+      const float mfac = EQM ? (float)a.p.mass_fluid : 1.0f;
+      const double ax = (double)(lo(s[0].axy) * mfac), ay = (double)(hi(s[0].axy) * mfac);
+      const double az = (double)((lo(s[0].az) + hi(s[0].az)) * mfac);
+      const double dr = (double)(-(lo(s[0].dr) + hi(s[0].dr)) * mfac);
+      const double vd = (double)(s[0].vd * (float)a.p.h);
+      if (isf) {
+        a.acc[3 * (int64_t)i + 0] = ax;
+        a.acc[3 * (int64_t)i + 1] = ay;
+        a.acc[3 * (int64_t)i + 2] = az;
+      } else {
+        a.acc[3 * (int64_t)i + 0] = 0.0;
+        a.acc[3 * (int64_t)i + 1] = 0.0;
+        a.acc[3 * (int64_t)i + 2] = 0.0;
+      }
+      a.drho[i] = dr;
+      a.visc[i] = vd;
+      if (!(isfinite(ax) && isfinite(ay) && isfinite(az) && isfinite(dr)))
+        raise_div(a.ctrl, step, SPHB_DIV_NONFINITE_FORCES, 0);
+      if (isf) {
+        const double fx = xadd(ax, a.p.g[0]), fy = xadd(ay, a.p.g[1]), fz = xadd(az, a.p.g[2]);
+        double fmag = __dsqrt_rn(xadd(xadd(xmul(fx, fx), xmul(fy, fy)), xmul(fz, fz)));
+        fmag = fmag > 1e-30 ? fmag : 1e-30;
+        dtf_min = fmin(dtf_min, __dsqrt_rn(xdiv(a.p.h, fmag)));
+      }
+      dtcv_min = fmin(dtcv_min, xdiv(a.p.h, xadd((double)ocs, vd)));
+    }
+  }
+
+  dtf_min = warp_min(dtf_min);
+  dtcv_min = warp_min(dtcv_min);
+  c_cand = warp_sum_u64(c_cand);
+  c_hits = warp_sum_u64(c_hits);
+  unsigned long long ffu = warp_sum_u64((unsigned long long)c_ff);
+  if (lane == 0) {
+    if (dtf_min < INFINITY) atomic_min_pos(&a.ctrl->dtmin_f, dtf_min);
+    if (dtcv_min < INFINITY) atomic_min_pos(&a.ctrl->dtmin_cv, dtcv_min);
+    if (c_cand) atomicAdd((unsigned long long*)&a.ctrl->counters[0], c_cand);
+    if (c_hits) {
+      atomicAdd((unsigned long long*)&a.ctrl->counters[1], c_hits);
+      atomicAdd((unsigned long long*)&a.ctrl->counters[2], c_hits);
+    }
+    if (ffu) atomicAdd((unsigned long long*)&a.ctrl->counters[3], ffu);
+  }
+}
+
 template <typename R>
 constexpr size_t smem_bytes() {
   return sizeof(float4) * Cfg<R>::NARR * Cfg<R>::SCAP + (Cfg<R>::H16 ? 6 * Cfg<R>::SCAP : 0) +
@@ -764,13 +1388,57 @@ int launch_kernel(const KArgs& a, int nsm, cudaStream_t s) {
   return sphb_check_launch("k_interact");
 }
 
+template <bool G7, bool EQM>
+int launch_v8(const KArgs& a, const K32& k, int nsm, cudaStream_t s) {
+  static int grid = 0;
+  const size_t bytes = 32 * V8_ROWS + 6 * Cfg<float>::SCAP + 8 * NW * 24 * 32;
+  if (grid == 0) {
+    cudaError_t e = cudaFuncSetAttribute(k_interact_v8<G7, EQM>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (e != cudaSuccess)
+      return sphb_set_error(SPHB_E_CUDA, "smem attribute: %s", cudaGetErrorString(e));
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_interact_v8<G7, EQM>, NW * 32, bytes);
+    grid = nsm * (per_sm > 0 ? per_sm : 1);
+  }
+  k_interact_v8<G7, EQM><<<grid, NW * 32, bytes, s>>>(a, k);
+  return sphb_check_launch("k_interact_v8");
+}
+
 template <typename R>
 int launch_one(const KArgs& a, int nsm, cudaStream_t s) {
-  if (sizeof(R) == 8) return launch_kernel<R, true, false>(a, nsm, s);
-  const bool eqm = a.p.mass_fluid == a.p.mass_boundary;
-  if (a.gamma7)
-    return eqm ? launch_kernel<R, true, true>(a, nsm, s) : launch_kernel<R, true, false>(a, nsm, s);
-  return eqm ? launch_kernel<R, false, true>(a, nsm, s) : launch_kernel<R, false, false>(a, nsm, s);
+  if constexpr (sizeof(R) == 8) {
+    return launch_kernel<R, true, false>(a, nsm, s);
+  } else if constexpr (SPHB_V8) {
+    const sphb_params_t& p = a.p;
+    K32 k;
+    // sure-hit / sure-miss band of the FP32 r^2: |r2_32 / r2_64 - 1| <= 5.1 u (u = 2^-24: the
+    // rounded difference, product, sum and FMA), so +-5e-7 (8.4 u, threshold rounding
+    // included) decides every pair the f64 predicate would, except the ones inside it
+    k.sup2_lo = (float)(p.sup2 * (1.0 - 5e-7));
+    k.sup2_hi = (float)(p.sup2 * (1.0 + 5e-7));
+    k.tiny = a.tiny;
+    k.invh = a.invh;
+    k.eta2 = a.eta2;
+    const double ktw = p.kc * p.invwdp;
+    k.ktw4 = (float)(ktw * ktw * ktw * ktw);
+    k.tpos = (float)(0.01 * ktw * ktw * ktw * ktw);
+    k.tneg = (float)(-0.2 * ktw * ktw * ktw * ktw);
+    const double nalh = -p.alpha * p.h;  // -alpha h folded into cs
+    k.cs_exp = a.cs_exp;
+    k.kcs = a.gamma7 ? (float)(cbrt(p.c0) / p.rho0 * cbrt(nalh))
+                     : (float)(p.c0 * pow(p.rho0, -(p.gamma - 1.0) * 0.5) * nalh);
+    const bool eqm = p.mass_fluid == p.mass_boundary;
+    k.nkgc = (float)(-3.0 * p.kc * p.invh * (eqm ? 1.0 : p.mass_fluid));
+    k.nkgc_b = (float)(-3.0 * p.kc * p.invh * (eqm ? 1.0 : p.mass_boundary));
+    if (a.gamma7) return eqm ? launch_v8<true, true>(a, k, nsm, s) : launch_v8<true, false>(a, k, nsm, s);
+    return eqm ? launch_v8<false, true>(a, k, nsm, s) : launch_v8<false, false>(a, k, nsm, s);
+  } else {
+    const bool eqm = a.p.mass_fluid == a.p.mass_boundary;
+    if (a.gamma7)
+      return eqm ? launch_kernel<R, true, true>(a, nsm, s) : launch_kernel<R, true, false>(a, nsm, s);
+    return eqm ? launch_kernel<R, false, true>(a, nsm, s) : launch_kernel<R, false, false>(a, nsm, s);
+  }
 }
 
 }  // namespace
