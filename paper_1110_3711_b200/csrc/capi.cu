@@ -85,7 +85,7 @@ int sphb_workspace_create(int64_t n_max, int64_t ncells_max, sphb_workspace_t** 
     e = alloc((void**)&ws->scan_partials, sizeof(uint32_t) * (ws->max_scan_tiles + 1));
   // a block never spans two cell rows and holds >= 1 target: #blocks <= n/BT + n
   ws->max_blocks = n1 + n1 / 64 + 16;
-  if (e == cudaSuccess) e = alloc((void**)&ws->blocks, sizeof(int4) * ws->max_blocks);
+  if (e == cudaSuccess) e = alloc((void**)&ws->blocks, 2 * sizeof(int4) * ws->max_blocks);
   if (e == cudaSuccess) e = cudaMemset(ws->cnt, 0, sizeof(uint32_t) * 2 * ncells_max);
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
   ws->bytes = bytes;

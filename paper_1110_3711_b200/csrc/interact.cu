@@ -379,8 +379,12 @@ __device__ __forceinline__ bool screen(const KArgs& a, const C32&, const Own<dou
 // Only cell columns [tx0, tx1) hold targets (the owned slab of an X-slab decomposition;
 // halo columns outside it are candidates only).  A cell with more than BT targets is split
 // into single-list blocks.
-__device__ __forceinline__ void emit_block(sphb_ctrl_t* ctrl, int4* out, int4 b) {
-  out[atomicAdd(&ctrl->nblk[0], 1u)] = b;
+// Block record (2 x int4): (fluid i0, i1, boundary i0, i1), (row, first cell x, last cell x, 0)
+__device__ __forceinline__ void emit_block(sphb_ctrl_t* ctrl, int4* out, int4 b, int row, int xa,
+                                           int xb) {
+  const uint32_t k = atomicAdd(&ctrl->nblk[0], 1u);
+  out[2 * k] = b;
+  out[2 * k + 1] = make_int4(row, xa, xb, 0);
 }
 
 __global__ void __launch_bounds__(256) k_blocks(sphb_grid_t g, int64_t ncells,
@@ -397,24 +401,31 @@ __global__ void __launch_bounds__(256) k_blocks(sphb_grid_t g, int64_t ncells,
     if (end[cf + g.tx1 - 1] <= beg[cf + g.tx0] && end[cb + g.tx1 - 1] <= beg[cb + g.tx0]) continue;
     int32_t f0 = beg[cf + g.tx0], b0 = beg[cb + g.tx0];  // open block
     int32_t fcur = f0, bcur = b0;
+    int xa = -1, xl = -1;  // first / last non-empty cell of the open block
     for (int x = g.tx0; x < g.tx1; ++x) {
       const int32_t fe = end[cf + x], be = end[cb + x];
       if (fe == fcur && be == bcur) continue;  // empty cell
       if ((fe - f0) + (be - b0) > BT && (fcur > f0 || bcur > b0)) {  // close before this cell
-        emit_block(ctrl, blk, make_int4(f0, fcur, b0, bcur));
+        emit_block(ctrl, blk, make_int4(f0, fcur, b0, bcur), (int)r, xa, xl);
         f0 = fcur;
         b0 = bcur;
+        xa = -1;
       }
       if ((fe - f0) + (be - b0) > BT) {  // one oversized cell: single-list chunks of <= BT
-        for (int32_t p = f0; p < fe; p += BT) emit_block(ctrl, blk, make_int4(p, min(p + BT, fe), be, be));
-        for (int32_t p = b0; p < be; p += BT) emit_block(ctrl, blk, make_int4(fe, fe, p, min(p + BT, be)));
+        for (int32_t p = f0; p < fe; p += BT)
+          emit_block(ctrl, blk, make_int4(p, min(p + BT, fe), be, be), (int)r, x, x);
+        for (int32_t p = b0; p < be; p += BT)
+          emit_block(ctrl, blk, make_int4(fe, fe, p, min(p + BT, be)), (int)r, x, x);
         f0 = fe;
         b0 = be;
+      } else {
+        if (xa < 0) xa = x;
+        xl = x;
       }
       fcur = fe;
       bcur = be;
     }
-    if (fcur > f0 || bcur > b0) emit_block(ctrl, blk, make_int4(f0, fcur, b0, bcur));
+    if (fcur > f0 || bcur > b0) emit_block(ctrl, blk, make_int4(f0, fcur, b0, bcur), (int)r, xa, xl);
   }
 }
 
@@ -452,7 +463,7 @@ __global__ void __launch_bounds__(NW * 32, 2) k_interact(KArgs a) {
     __syncthreads();
     const uint32_t blk = (uint32_t)s_blk;
     if (blk >= nblocks) break;
-    const int4 bb = blocks[blk];
+    const int4 bb = blocks[2 * blk];
     const int f0 = bb.x, nf = bb.y - bb.x, b0 = bb.z, nbt = bb.w - bb.z;
     // the block's cells: one row, columns [cxa, cxb] (sorted lists: first/last targets)
     const int cfirst = min(nf ? a.cell[f0] : INT_MAX, nbt ? a.cell[b0] : INT_MAX);
@@ -826,6 +837,24 @@ __device__ __forceinline__ uint32_t prmt_sign(uint32_t a, uint32_t b) {
   asm("prmt.b32 %0, %1, %2, 0xFDB9;" : "=r"(r) : "r"(a), "r"(b));
   return r;
 }
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
+  uint32_t r;
+  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(sel));
+  return r;
+}
+// D = A B + C, m16n8k8, FP16 operands, FP32 accumulation (warp-wide)
+__device__ __forceinline__ void mma_16816(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t b0,
+                                          const float (&c)[4]) {
+  asm("mma.sync.aligned.m16n8k8.row.col.f32.f16.f16.f32 {%0, %1, %2, %3}, {%4, %5}, {%6}, "
+      "{%7, %8, %9, %10};"
+      : "=f"(d[0]), "=f"(d[1]), "=f"(d[2]), "=f"(d[3])
+      : "r"(a0), "r"(a1), "r"(b0), "f"(c[0]), "f"(c[1]), "f"(c[2]), "f"(c[3]));
+}
+__device__ __forceinline__ uint32_t h2u(__half2 h) {
+  uint32_t u;
+  memcpy(&u, &h, 4);
+  return u;
+}
 __device__ __forceinline__ int flo32(uint32_t v) {  // index of the highest set bit, -1 if none
   int r;
   asm("bfind.u32 %0, %1;" : "=r"(r) : "r"(v));
@@ -867,16 +896,36 @@ struct Acc32 {
 };
 
 constexpr int V8_ROWS = 2304 + 8;  // staged rows: SCAP candidates + the dummy (row SCAP)
+// dynamic shared memory of k_interact_v8: A rows | B rows | screen records (8 B) | 64 B of
+// zeros (B fragments of the K = 4..7 lanes) | FIFO
+constexpr int V8_RING = 20;
+constexpr int V8_REC_OFF = 32 * V8_ROWS;
+constexpr int V8_ZERO_OFF = V8_REC_OFF + 8 * 2304;
+constexpr int V8_FIFO_OFF = V8_ZERO_OFF + 64;
+constexpr int V8_SMEM = V8_FIFO_OFF + 8 * NW * V8_RING * 32;
+// tensor-core screen: D = |x_j|^2 - 2 x_i.x_j + (|x_i|^2 - thr) in units of (2h)^2 from FP16
+// block-centred coordinates (|x| <= 4, |x|^2 < 32): coordinate rounding moves r^2 by <= 6.8e-3
+// at the cutoff and the FP16 |x_j|^2 by <= 7.8e-3, so thr = 1.02 never drops a true hit
+constexpr float MMA_THR = 1.02f;
 #ifndef V8_NG
 #define V8_NG 3    // candidate pairs per lane per drain iteration (independent FP32x2 chains)
 #endif
 #ifndef V8_KMIN
 #define V8_KMIN 6  // minimum iterations of a partial drain
 #endif
+// a partial drain pops >= 2 NG KMIN maybes per busy lane, i.e. frees at least its oldest word
+static_assert(2 * V8_NG * V8_KMIN >= 32, "partial drains must free a FIFO entry");
 
 // NG groups of two popped candidates (staged byte addresses of their A rows) of one lane.
 // Each group is one packed FP32x2 chain; the groups are independent (ILP), and the rare
 // exact re-decision is one warp-uniform branch for all of them.
+// r2 inside the FP32 guard band [sup2_lo, sup2_hi) or coincident (r2 <= tiny)
+__device__ __forceinline__ bool in_cold(float r2, const K32& c) {
+  const uint32_t b = __float_as_uint(r2);
+  return (b - __float_as_uint(c.sup2_lo) < __float_as_uint(c.sup2_hi) - __float_as_uint(c.sup2_lo)) |
+         (b <= __float_as_uint(c.tiny));
+}
+
 struct Geo2 {
   f2_t a1xy, a1zw, b1zw, a2xy, a2zw, b2zw, dxy1, dxy2, dz, r2, dot;
 };
@@ -887,7 +936,7 @@ __device__ __forceinline__ void eval_v8(const KArgs& a, const K32& c, const Own3
                                         Acc32 (&s)[NG]) {
   constexpr uint32_t OFFB = 16u * V8_ROWS;  // A -> B rows
   Geo2 g[NG];
-  bool ok[2 * NG], cold[2 * NG];
+  bool ok[2 * NG];
   bool anycold = false;
 #pragma unroll
   for (int k = 0; k < NG; ++k) {
@@ -905,24 +954,26 @@ __device__ __forceinline__ void eval_v8(const KArgs& a, const K32& c, const Own3
     const f2_t dvz = pk(o.vz - lo(g[k].b1zw), o.vz - lo(g[k].b2zw));
     g[k].r2 = fma2(g[k].dz, g[k].dz, pk(lo(sq1) + hi(sq1), lo(sq2) + hi(sq2)));
     g[k].dot = fma2(dvz, g[k].dz, pk(lo(dd1) + hi(dd1), lo(dd2) + hi(dd2)));
-    // non-short-circuit predicates; an empty slot reads the dummy row (r2 ~ 1e8 sup2):
-    // never a hit, never cold
+    // sure hit: r2 < sup2_lo (an empty slot reads the dummy row, r2 ~ 1e8 sup2: never a hit);
+    // cold (exact f64 re-decision): r2 in [sup2_lo, sup2_hi) or r2 <= tiny, tested as
+    // unsigned ranges of the (non-negative) float bits
     const float r21 = lo(g[k].r2), r22 = hi(g[k].r2);
-    ok[2 * k] = (r21 < c.sup2_lo) & (r21 > c.tiny);
-    ok[2 * k + 1] = (r22 < c.sup2_lo) & (r22 > c.tiny);
-    cold[2 * k] = !ok[2 * k] & (r21 < c.sup2_hi);
-    cold[2 * k + 1] = !ok[2 * k + 1] & (r22 < c.sup2_hi);
-    anycold = anycold | cold[2 * k] | cold[2 * k + 1];
+    ok[2 * k] = r21 < c.sup2_lo;
+    ok[2 * k + 1] = r22 < c.sup2_lo;
+    anycold |= in_cold(r21, c) | in_cold(r22, c);
   }
   if (__any_sync(SPHB_FULL, anycold)) {
-    // guard band / coincident (lattice ties sit exactly on the cutoff): exact f64 decision,
-    // one candidate per lane per round so the f64 path is issued once, not once per slot
+    // guard band / coincident (lattice ties sit on the cutoff): exact f64 decision, one
+    // candidate per lane per round so the f64 path is issued once, not once per slot
     uint32_t cm = 0, okm = 0;
 #pragma unroll
-    for (int k = 0; k < 2 * NG; ++k) {
-      cm |= (cold[k] ? 1u : 0u) << k;
-      okm |= (ok[k] ? 1u : 0u) << k;
+    for (int k = 0; k < NG; ++k) {
+      cm |= (in_cold(lo(g[k].r2), c) ? 1u : 0u) << (2 * k);
+      cm |= (in_cold(hi(g[k].r2), c) ? 1u : 0u) << (2 * k + 1);
     }
+#pragma unroll
+    for (int k = 0; k < 2 * NG; ++k) okm |= (ok[k] ? 1u : 0u) << k;
+    okm &= ~cm;
     do {
       const int k = __ffs(cm) - 1;
       uint32_t adk = ad[0];
@@ -992,8 +1043,8 @@ template <bool G7, bool EQM>
 __global__ void __launch_bounds__(NW * 32, 2) k_interact_v8(KArgs a, K32 k32) {
   if (!step_live(a.ctrl)) return;
   constexpr int SCAP = Cfg<float>::SCAP;
-  constexpr int RINGC = 24;                               // FIFO entries per lane (8 B)
-  constexpr int MASK0 = (32 * V8_ROWS + 6 * SCAP) / 4;  // uint32 offset of the FIFO
+  constexpr int RINGC = V8_RING;                          // FIFO entries per lane (8 B)
+  constexpr int MASK0 = V8_FIFO_OFF / 4;                 // uint32 offset of the FIFO
   __shared__ Seg sSeg[MAXSEG];
   __shared__ int s_blk, s_nseg_tot, s_scan[MAXSEG];
 
@@ -1010,8 +1061,20 @@ __global__ void __launch_bounds__(NW * 32, 2) k_interact_v8(KArgs a, K32 k32) {
   }
 
   const uint32_t smA = pin_u32(smem_addr(g_sm4));
-  const uint32_t smH = smA + 32u * V8_ROWS;
+  const uint32_t smR = smA + V8_REC_OFF;  // screen records: half2 (x, y), half2 (z, |x|^2)
   const uint32_t dummy = smA + 16u * SCAP;
+  if (tid < 16) g_sm32[V8_ZERO_OFF / 4 + tid] = 0u;
+  // tensor-core screen lane roles: g = lane / 4 (fragment row / column), t = lane % 4
+  const int fg = lane >> 2, ft = lane & 3;
+  // B fragment (K rows 2t, 2t+1; column g of N-tile n <-> candidate 8 (g/2) + 2n + g%2):
+  // t = 0 reads (x, y), t = 1 reads (z, |x|^2) of the record, t >= 2 reads zeros
+  const uint32_t bl_off = ft < 2 ? 64u * (fg >> 1) + 8u * (fg & 1) + 4u * ft : 0u;
+  const uint32_t bl_kmul = ft < 2 ? 8u : 0u;
+  const uint32_t bl_base = ft < 2 ? smR : smA + V8_ZERO_OFF;
+  // quad byte transpose selectors and the final route (lane r <- lane 4 (r % 8) + r / 8)
+  const uint32_t tsel1 = (ft & 1) ? 0x3715u : 0x6240u;
+  const uint32_t tsel2 = (ft & 2) ? 0x3276u : 0x5410u;
+  const int troute = 4 * (lane & 7) + (lane >> 3);
   // FIFO: [NW][RINGC][32 lanes] of (mask u32, staged row address u32)
   const uint32_t ring = pin_u32(smem_addr(g_sm32 + MASK0) + 8u * (warp * RINGC * 32 + lane));
   const uint32_t rend = ring + 256u * RINGC;
@@ -1020,18 +1083,37 @@ __global__ void __launch_bounds__(NW * 32, 2) k_interact_v8(KArgs a, K32 k32) {
   long long c_ff = 0;
   double dtf_min = INFINITY, dtcv_min = INFINITY;
 
+  // block records are fetched one block ahead by thread 0 (the next record's L2 latency
+  // overlaps the current block)
+  __shared__ int4 s_bb[2];
+  int4 nxt_b = make_int4(0, 0, 0, 0), nxt_m = make_int4(0, 0, 0, 0);
+  uint32_t nxt = 0;
+  if (tid == 0) {
+    nxt = atomicAdd(&a.ctrl->tile_next[0], 1u);
+    if (nxt < nblocks) {
+      nxt_b = a.blocks[2 * nxt];
+      nxt_m = a.blocks[2 * nxt + 1];
+    }
+  }
   for (;;) {
     __syncthreads();
-    if (tid == 0) s_blk = (int)atomicAdd(&a.ctrl->tile_next[0], 1u);
+    if (tid == 0) {
+      s_blk = (int)nxt;
+      s_bb[0] = nxt_b;
+      s_bb[1] = nxt_m;
+      nxt = atomicAdd(&a.ctrl->tile_next[0], 1u);
+      if (nxt < nblocks) {
+        nxt_b = a.blocks[2 * nxt];
+        nxt_m = a.blocks[2 * nxt + 1];
+      }
+    }
     __syncthreads();
     const uint32_t blk = (uint32_t)s_blk;
     if (blk >= nblocks) break;
-    const int4 bb = a.blocks[blk];
+    const int4 bb = s_bb[0], bm = s_bb[1];
     const int f0 = bb.x, nf = bb.y - bb.x, b0 = bb.z, nbt = bb.w - bb.z;
-    const int cfirst = min(nf ? a.cell[f0] : INT_MAX, nbt ? a.cell[b0] : INT_MAX);
-    const int clast = max(nf ? a.cell[f0 + nf - 1] : -1, nbt ? a.cell[b0 + nbt - 1] : -1);
-    const int rowkey = cfirst / nx;
-    const int cxa = cfirst - rowkey * nx, cxb = clast - rowkey * nx;
+    const int rowkey = bm.x;
+    const int cxa = bm.y, cxb = bm.z;
     const int nlist = nf ? 2 : 1;
     const int nseg = nlist * side * side;
     const int gcz = rowkey / ny, gcy = rowkey - gcz * ny;
@@ -1041,8 +1123,10 @@ __global__ void __launch_bounds__(NW * 32, 2) k_interact_v8(KArgs a, K32 k32) {
     const float h16_xc = (float)(a.g.origin[0] + 0.5 * (bxlo + bxhi + 1) * cs);
     const float h16_yc = (float)(a.g.origin[1] + (gcy + 0.5) * cs);
     const float h16_zc = (float)(a.g.origin[2] + (gcz + 0.5) * cs);
-    const bool use16 = (0.5 * (bxhi - bxlo + 1) * cs * (0.5 * a.p.invh) <= H16_MAXABS) &&
-                       ((reach + 0.5) * cs * (0.5 * a.p.invh) <= H16_MAXABS);
+    const double xext = 0.5 * (bxhi - bxlo + 1) * cs * (0.5 * a.p.invh);
+    const double yzext = (reach + 0.5) * cs * (0.5 * a.p.invh);
+    const bool use16 = xext <= H16_MAXABS && yzext <= H16_MAXABS &&
+                       xext * xext + 2.0 * yzext * yzext < 30.0;
     // the fluid targets' own row (fluid list, dy = dz = 0)
     const int rr_c = reach * side + reach;
     const int selfseg = nf ? ((nlist == 2 && a.p.order == 1) ? rr_c : rr_c * nlist) : -1;
@@ -1134,28 +1218,60 @@ __global__ void __launch_bounds__(NW * 32, 2) k_interact_v8(KArgs a, K32 k32) {
       s[k].vd = 0.0f;
     }
     unsigned long long cand = 0;
-    if (valid) {
-      for (int k = 0; k < nseg; ++k) {
-        const Seg sg = sSeg[k];
-        if (sg.g1 <= sg.g0) continue;
-        if (!isf && sg.rowoff < a.ncells) continue;
-        cand += (unsigned long long)(a.end[sg.rowoff + xhi] - a.beg[sg.rowoff + xlo]);
+    if (valid) {  // candidate count = sum of this lane's row-range lengths (loads batched by 6)
+      for (int k0 = 0; k0 < nseg; k0 += 6) {
+        int e[6], b[6];
+#pragma unroll
+        for (int u = 0; u < 6; ++u) {
+          e[u] = b[u] = 0;
+          const int k = k0 + u;
+          if (k < nseg) {
+            const Seg sg = sSeg[k];
+            if (sg.g1 > sg.g0 && (isf || sg.rowoff >= a.ncells)) {
+              e[u] = a.end[sg.rowoff + xhi];
+              b[u] = a.beg[sg.rowoff + xlo];
+            }
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 6; ++u) cand += (unsigned long long)(e[u] - b[u]);
       }
       if (isf) cand -= 1;
     }
 
-    const __half2 thr16 = __float2half2_rn(H16_THR8);
-    const __half2 ohx = __float2half2_rn((o.x - h16_xc) * h16_s);
-    const __half2 ohy = __float2half2_rn((o.y - h16_yc) * h16_s);
-    const __half2 ohz = __float2half2_rn((o.z - h16_zc) * h16_s);
+    // A / C fragments of the tensor-core screen: target row r = 16 m + g (+ 8) holds
+    // K = (-2x, -2y, -2z, 1, 0, 0, 0, 0) and C = |x|^2 - thr of its FP16 block-centred position
+    uint32_t fa[2][2];
+    float fc[2][4];
+    {
+      const __half hx = __float2half_rn((o.x - h16_xc) * h16_s);
+      const __half hy = __float2half_rn((o.y - h16_yc) * h16_s);
+      const __half hz = __float2half_rn((o.z - h16_zc) * h16_s);
+      const float fx = __half2float(hx), fy = __half2float(hy), fz = __half2float(hz);
+      const uint32_t alo = h2u(__floats2half2_rn(-2.0f * fx, -2.0f * fy));
+      const uint32_t ahi = h2u(__floats2half2_rn(-2.0f * fz, 1.0f));
+      const float cv = fmaf(fz, fz, fmaf(fy, fy, fx * fx)) - MMA_THR;
+#pragma unroll
+      for (int m = 0; m < 2; ++m) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int r = 16 * m + 8 * h + fg;
+          const uint32_t vlo = __shfl_sync(SPHB_FULL, alo, r), vhi = __shfl_sync(SPHB_FULL, ahi, r);
+          fa[m][h] = ft == 0 ? vlo : (ft == 1 ? vhi : 0u);
+          const float c = __shfl_sync(SPHB_FULL, cv, r);
+          fc[m][2 * h] = c;
+          fc[m][2 * h + 1] = c;
+        }
+      }
+    }
 
     // Per-lane circular FIFO of non-empty screen words: (mask, staged row address).  A
     // partial drain runs K lock-step iterations of 2*V8_NG pops per lane; pend counts the
     // lane's queued maybes (every pop yields one while pend > 0).
     // Entries are (mask, row address) pairs, 8 B, RINGC per lane; hp / tp are the lane's read
     // and write entry addresses (stride 256 B: 32 lanes), cnt the entries queued.  An
-    // exhausted FIFO points cb at the dummy row: the empty pop (bfind = -1) lands on it.
-    uint32_t hp = ring, tp = ring, cnt = 0, pend = 0, cur = 0u, cb = dummy - 0x1b0u;
+    // exhausted FIFO points cb one row past the dummy: the empty pop (bfind = -1) lands on it.
+    uint32_t hp = ring, tp = ring, cnt = 0, pend = 0, cur = 0u, cb = dummy + 16u;
     auto pop = [&]() -> uint32_t {
       const bool need = cur == 0u, have = cnt != 0u;
       if (need & have) {
@@ -1165,11 +1281,10 @@ __global__ void __launch_bounds__(NW * 32, 2) k_interact_v8(KArgs a, K32 k32) {
         hp = hp + 256u == rend ? ring : hp + 256u;
         --cnt;
       }
-      cb = (need & !have) ? dummy - 0x1b0u : cb;
+      cb = (need & !have) ? dummy + 16u : cb;
       const int tb = flo32(cur);
       cur = clear_bit(cur, tb);
-      // bit 8j + k <-> candidate 4k + j: byte offset 16 (4k + j) = (tb * 66) & 0x1f0
-      return cb + (((uint32_t)tb * 66u) & 0x1f0u);
+      return cb + 16u * (uint32_t)tb;  // bit b <-> candidate k0 + b; empty (-1) -> the dummy
     };
     auto drain = [&](bool full) {
       __syncwarp();
@@ -1196,7 +1311,7 @@ __global__ void __launch_bounds__(NW * 32, 2) k_interact_v8(KArgs a, K32 k32) {
         // STG rows in flight per thread: all loads of a chunk are issued before its stores
         constexpr int U = 4;
         int sk = 0;
-        __half* h = reinterpret_cast<__half*>(g_sm4 + 2 * V8_ROWS);
+        uint2* rec = reinterpret_cast<uint2*>(reinterpret_cast<char*>(g_sm4) + V8_REC_OFF);
         for (int p0 = q0 + tid; p0 < q1; p0 += U * NW * 32) {
           int jj[U];
           bool bl[U];
@@ -1227,71 +1342,93 @@ __global__ void __launch_bounds__(NW * 32, 2) k_interact_v8(KArgs a, K32 k32) {
             if (jj[u] >= 0) {
               g_sm4[r] = make_float4(pp[u].x, pp[u].y, pp[u].z, xa[u]);
               g_sm4[V8_ROWS + r] = make_float4(vr[u].x, vr[u].y, vr[u].z, bl[u] ? -vr[u].w : vr[u].w);
-              h[r] = __float2half_rn((pp[u].x - h16_xc) * h16_s);
-              h[SCAP + r] = __float2half_rn((pp[u].y - h16_yc) * h16_s);
-              h[2 * SCAP + r] = __float2half_rn((pp[u].z - h16_zc) * h16_s);
+              const __half hx = __float2half_rn((pp[u].x - h16_xc) * h16_s);
+              const __half hy = __float2half_rn((pp[u].y - h16_yc) * h16_s);
+              const __half hz = __float2half_rn((pp[u].z - h16_zc) * h16_s);
+              const float fx = __half2float(hx), fy = __half2float(hy), fz = __half2float(hz);
+              rec[r] = make_uint2(h2u(__halves2half2(hx, hy)),
+                                  h2u(__halves2half2(hz, __float2half_rn(fmaf(fz, fz, fmaf(fy, fy, fx * fx))))));
             }
           }
         }
       }
       __syncthreads();
       if (wactive) {
-        for (int k = 0; k < nseg; ++k) {
+        // the warp's part of row k: cells [wxlo, wxhi]; the next row's bounds are loaded while
+        // this row is screened
+        auto live = [&](int k) {
           const Seg sg = sSeg[k];
           const int len = sg.g1 - sg.g0;
-          if (len <= 0 || sg.pos >= q1 || sg.pos + len <= q0) continue;
-          const int wg0 = a.beg[sg.rowoff + wxlo], wg1 = a.end[sg.rowoff + wxhi];
+          return len > 0 && sg.pos < q1 && sg.pos + len > q0;
+        };
+        int kn = 0;
+        while (kn < nseg && !live(kn)) ++kn;
+        int nb0 = 0, nb1 = 0;
+        if (kn < nseg) {
+          nb0 = a.beg[sSeg[kn].rowoff + wxlo];
+          nb1 = a.end[sSeg[kn].rowoff + wxhi];
+        }
+        while (kn < nseg) {
+          const int k = kn;
+          const Seg sg = sSeg[k];
+          const int wg0 = nb0, wg1 = nb1;
+          ++kn;
+          while (kn < nseg && !live(kn)) ++kn;
+          if (kn < nseg) {
+            nb0 = a.beg[sSeg[kn].rowoff + wxlo];
+            nb1 = a.end[sSeg[kn].rowoff + wxhi];
+          }
           const int lo_ = max(sg.pos + (wg0 - sg.g0), q0) - q0;
           const int hi_ = min(sg.pos + (wg1 - sg.g0), q1) - q0;
           if (hi_ <= lo_) continue;
           const bool boundary_list = sg.rowoff < a.ncells;
           const uint32_t lanemask = (valid && (isf || !boundary_list)) ? 0xffffffffu : 0u;
-          const uint32_t lflag = boundary_list ? 1u : 0u;  // (unused by the v8 drain)
-          (void)lflag;
+          const bool selfrow = k == selfseg;
           // own staged position in the self row (fluid targets), else out of range
-          const int selfpos = (k == selfseg && isf) ? sg.pos + (i - sg.g0) - q0 : INT_MIN / 2;
-          const int lo8 = use16 ? (lo_ & ~7) : lo_;
-          for (int k0 = lo8; k0 < hi_; k0 += 32) {
-            uint32_t miss = 0;
+          const int selfpos = (selfrow && isf) ? sg.pos + (i - sg.g0) - q0 : INT_MIN / 2;
+          for (int k0 = lo_; k0 < hi_; k0 += 32) {
+            uint32_t hit;
             if (use16) {
-              const uint32_t hx = smH + 2u * k0, hy = hx + 2u * SCAP, hz = hy + 2u * SCAP;
+              // 32 targets x 32 candidates on the tensor cores: 2 M-tiles x 4 N-tiles
+              const uint32_t wb = bl_base + bl_kmul * (uint32_t)k0 + bl_off;
+              uint32_t fb[4];
 #pragma unroll
-              for (int q = 0; q < 4; ++q) {
-                const uint4 vx = lds128u(hx + 16u * q), vy = lds128u(hy + 16u * q),
-                            vz = lds128u(hz + 16u * q);
-                const uint32_t ux[4] = {vx.x, vx.y, vx.z, vx.w}, uy[4] = {vy.x, vy.y, vy.z, vy.w},
-                               uz[4] = {vz.x, vz.y, vz.z, vz.w};
-                uint32_t r[4];
+              for (int n = 0; n < 4; ++n) fb[n] = lds32(wb + 16u * n);
+              float d[2][4][4];
 #pragma unroll
-                for (int w = 0; w < 4; ++w) {
-                  const __half2 dx = __hsub2(ohx, u32_as_h2(ux[w]));
-                  const __half2 dy = __hsub2(ohy, u32_as_h2(uy[w]));
-                  const __half2 dz = __hsub2(ohz, u32_as_h2(uz[w]));
-                  __half2 e = __hfma2(__hneg2(dx), dx, thr16);
-                  e = __hfma2(__hneg2(dy), dy, e);
-                  e = __hfma2(__hneg2(dz), dz, e);
-                  memcpy(&r[w], &e, 4);
+              for (int m = 0; m < 2; ++m)
+#pragma unroll
+                for (int n = 0; n < 4; ++n) mma_16816(d[m][n], fa[m][0], fa[m][1], fb[n], fc[m]);
+              // sign (D < 0: r^2 < thr) of target slot s = 2m + h, candidate 8t + 2n + e ->
+              // byte s, bit 2n + e
+              uint32_t w = 0;
+#pragma unroll
+              for (int n = 0; n < 4; ++n)
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                  const uint32_t pa = h2u(__floats2half2_rn(d[0][n][e], d[0][n][2 + e]));
+                  const uint32_t pb = h2u(__floats2half2_rn(d[1][n][e], d[1][n][2 + e]));
+                  w |= prmt_sign(pa, pb) & (0x01010101u << (2 * n + e));
                 }
-                // candidates 8q .. 8q+3 -> byte j bit 2q, 8q+4 .. 8q+7 -> bit 2q+1
-                miss |= prmt_sign(r[0], r[1]) & (0x01010101u << (2 * q));
-                miss |= prmt_sign(r[2], r[3]) & (0x01010101u << (2 * q + 1));
-              }
+              // quad byte transpose: lane (g, t) <- target g + 8t, byte j from lane (g, j)
+              w = prmt(w, __shfl_xor_sync(SPHB_FULL, w, 1), tsel1);
+              w = prmt(w, __shfl_xor_sync(SPHB_FULL, w, 2), tsel2);
+              hit = __shfl_sync(SPHB_FULL, w, troute);  // bit b <-> candidate k0 + b
             } else {
               const uint32_t sk = smA + 16u * k0;
+              hit = 0;
 #pragma unroll
               for (int tt = 0; tt < 32; ++tt) {
                 const float4 A = lds4(sk + 16u * tt);
                 const float dx = o.x - A.x, dy = o.y - A.y, dz = o.z - A.z;
-                if (!(fmaf(dz, dz, fmaf(dy, dy, dx * dx)) < k32.sup2_hi)) miss |= 1u << perm_bit(tt);
+                if (fmaf(dz, dz, fmaf(dy, dy, dx * dx)) < k32.sup2_hi) hit |= 1u << tt;
               }
             }
-            uint32_t m = lanemask;
-            if (k0 < lo_ || k0 + 32 > hi_)
-              m &= c_perm_ge.v[max(lo_ - k0, 0)] & ~c_perm_ge.v[min(hi_ - k0, 32)];
-            uint32_t bits = m & ~miss;
-            {
+            uint32_t bits = hit & lanemask;  // k0 >= lo_: only the row's last word is partial
+            if (hi_ - k0 < 32) bits &= (1u << (hi_ - k0)) - 1u;
+            if (selfrow) {
               const int d = selfpos - k0;
-              if ((unsigned)d < 32u) bits &= ~(1u << perm_bit(d));
+              if ((unsigned)d < 32u) bits &= ~(1u << d);
             }
             if (__any_sync(SPHB_FULL, bits != 0u && cnt == (uint32_t)RINGC)) drain(false);
             if (bits) {
@@ -1391,7 +1528,7 @@ int launch_kernel(const KArgs& a, int nsm, cudaStream_t s) {
 template <bool G7, bool EQM>
 int launch_v8(const KArgs& a, const K32& k, int nsm, cudaStream_t s) {
   static int grid = 0;
-  const size_t bytes = 32 * V8_ROWS + 6 * Cfg<float>::SCAP + 8 * NW * 24 * 32;
+  const size_t bytes = V8_SMEM;
   if (grid == 0) {
     cudaError_t e = cudaFuncSetAttribute(k_interact_v8<G7, EQM>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
