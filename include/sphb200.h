@@ -77,8 +77,21 @@ typedef struct {
   int32_t order;                 /* 0: per row F then B (gather_*_cells, kernels.py:326-418)
                                     1: all F rows then all B rows (gather_fluid_ranges 421-497) */
   int32_t precision;             /* SPHB_FP32 (production) | SPHB_FP64 (bit-exact to reference) */
+  /* ---- extensions beyond the reference; the zero values are the
+   * reference's behaviour */
+  int32_t kernel;                /* SPHB_KERNEL_CUBIC (reference, physics.py:25-33) |
+                                    SPHB_KERNEL_WENDLAND (C2, support 2h); kc / invwdp above
+                                    are that kernel's normalisation and 1/W(dp) */
+  int32_t integrator;            /* SPHB_INT_VERLET (reference, sim.py:235-259) |
+                                    SPHB_INT_SYMPLECTIC (two-stage position-Verlet) */
   int32_t pad_;
+  int64_t piston_id0, piston_id1; /* boundary particles with id in [id0, id1) follow the
+                                     piston x(t) = x0 + S/2 (1 - cos 2 pi t/T); id0 == id1: none */
+  double piston_x0, piston_stroke, piston_period;
 } sphb_params_t;
+
+enum { SPHB_KERNEL_CUBIC = 0, SPHB_KERNEL_WENDLAND = 1 };
+enum { SPHB_INT_VERLET = 0, SPHB_INT_SYMPLECTIC = 1 };
 
 /* Device-resident control block (one per simulation, caller allocates 256 B). */
 typedef struct {
@@ -94,7 +107,9 @@ typedef struct {
   int32_t active;        /* 1 while no error and no stop rule fired */
   uint32_t tile_next[2]; /* dynamic work counters of the interaction launches (reset per step) */
   uint32_t nblk[2];      /* target blocks built for the fluid / boundary interaction passes */
-  int32_t pad_[11];
+  int32_t pad_;
+  double dt_stage;              /* symplectic: the step's dt, fixed by the first stage */
+  uint64_t counters_stage[4];   /* symplectic: the first stage's counters (the step's stats) */
 } sphb_ctrl_t;
 
 /* Per-step record written at the end of every step (StepStats, model.py:176-212). */
@@ -178,6 +193,28 @@ int sphb_integrate(sphb_workspace_t* ws, const sphb_params_t* prm, const sphb_gr
                    const void* prev_s, const int64_t* id_s, const double* acc, const double* drho,
                    void* posp, void* velr, void* prev, int64_t* id, uint32_t* keys_next,
                    sphb_ctrl_t* ctrl, sphb_stream_t s);
+
+/* Symplectic integrator (params.integrator == SPHB_INT_SYMPLECTIC), replacing
+ * sphb_integrate: stage 0 (predictor, after the step's first interaction) fixes the step's
+ * dt and counters in ctrl and writes the half-step state r* = r + dt/2 v, v* = v + dt/2 (a+g),
+ * rho* = rho + dt/2 drho with (v, rho) kept in prev; stage 1 (corrector, after the second
+ * interaction on the half-step state) writes v' = v + dt (a*+g), r' = r* + dt/2 v',
+ * rho' = rho + dt drho*.  Both fuse the next assign_cells like sphb_integrate; piston
+ * particles follow their law at t + dt/2 and t + dt. */
+int sphb_integrate_stage(sphb_workspace_t* ws, const sphb_params_t* prm, const sphb_grid_t* grid,
+                         int64_t n, int64_t nb, int32_t stage, const void* posp_s,
+                         const void* velr_s, const void* prev_s, const int64_t* id_s,
+                         const double* acc, const double* drho, void* posp, void* velr,
+                         void* prev, int64_t* id, uint32_t* keys_next, sphb_ctrl_t* ctrl,
+                         sphb_stream_t s);
+
+/* Energy diagnostics (SURVEY.md §8(d) functional, no reference counterpart): out[0..4] =
+ * KE (fluid), PE = sum m |g| z (fluid), IE = sum m (u(rho) - u(rho0)) with the Tait internal
+ * energy u(rho) = B/(gamma-1) rho^(gamma-1)/rho0^gamma + B/rho (all particles), mean fluid rho,
+ * mean rho.  f64, deterministic (fixed-order two-pass reduction).  velr rows (vx,vy,vz,rho),
+ * posp rows (x,y,z,*); boundary rows first.  out is a device pointer to 5 doubles. */
+int sphb_energy(sphb_workspace_t* ws, const sphb_params_t* prm, int64_t n, int64_t nb,
+                const void* posp, const void* velr, double* out, sphb_stream_t s);
 
 /* Closes the step: dt/counters into rec[step % rec_capacity], t_sim += dt, step += 1. */
 int sphb_step_end(sphb_ctrl_t* ctrl, const sphb_params_t* prm, sphb_step_record_t* rec,

@@ -18,6 +18,8 @@ CSRC = os.path.join(HERE, "csrc")
 SPHB_OK, SPHB_E_INVALID, SPHB_E_CUDA, SPHB_E_CAPACITY = 0, -1, -2, -3
 SPHB_DIV_LEFT_DOMAIN, SPHB_DIV_NONFINITE_FORCES, SPHB_DIV_NONFINITE_STATE = 1, 2, 3
 SPHB_FP32, SPHB_FP64 = 0, 1
+SPHB_KERNEL_CUBIC, SPHB_KERNEL_WENDLAND = 0, 1
+SPHB_INT_VERLET, SPHB_INT_SYMPLECTIC = 0, 1
 
 c_i32, c_i64, c_f64, c_p = ctypes.c_int32, ctypes.c_int64, ctypes.c_double, ctypes.c_void_p
 
@@ -31,7 +33,10 @@ class ParamsDesc(ctypes.Structure):
     _fields_ = [(k, c_f64) for k in ("sup2", "h", "invh", "kc", "eta2", "alpha", "invwdp", "c0",
                                      "rho0", "gamma", "mass_fluid", "mass_boundary", "tait_b")] + \
                [("g", c_f64 * 3), ("cfl", c_f64), ("dt_min", c_f64), ("dt_max", c_f64),
-                ("verlet_stride", c_i32), ("order", c_i32), ("precision", c_i32), ("pad_", c_i32)]
+                ("verlet_stride", c_i32), ("order", c_i32), ("precision", c_i32),
+                ("kernel", c_i32), ("integrator", c_i32), ("pad_", c_i32),
+                ("piston_id0", c_i64), ("piston_id1", c_i64), ("piston_x0", c_f64),
+                ("piston_stroke", c_f64), ("piston_period", c_f64)]
 
 
 class StateDesc(ctypes.Structure):
@@ -44,7 +49,8 @@ class StateDesc(ctypes.Structure):
 CTRL_DTYPE = np.dtype([("step", "<i8"), ("max_steps", "<i8"), ("t_sim", "<f8"), ("t_end", "<f8"),
                        ("dt", "<f8"), ("dtmin_f", "<u8"), ("dtmin_cv", "<u8"), ("err", "<u8"),
                        ("counters", "<u8", (4,)), ("active", "<i4"), ("tile_next", "<u4", (2,)),
-                       ("nblk", "<u4", (2,)), ("pad_", "<i4", (11,))])
+                       ("nblk", "<u4", (2,)), ("pad_", "<i4"), ("dt_stage", "<f8"),
+                       ("counters_stage", "<u8", (4,))])
 CTRL_BYTES = 256
 assert CTRL_DTYPE.itemsize <= CTRL_BYTES
 REC_DTYPE = np.dtype([("dt", "<f8"), ("candidate_pairs", "<u8"), ("hits_ordered", "<u8"),
@@ -96,6 +102,9 @@ def lib():
         "sphb_step_begin": ([P, P], c_i32),
         "sphb_integrate": ([P, P, P, c_i64, c_i64, P, P, P, P, P, P, P, P, P, P, P, P, P], c_i32),
         "sphb_step_end": ([P, P, P, c_i64, P], c_i32),
+        "sphb_integrate_stage": ([P, P, P, c_i64, c_i64, c_i32, P, P, P, P, P, P, P, P, P, P, P, P,
+                                  P], c_i32),
+        "sphb_energy": ([P, P, c_i64, c_i64, P, P, P, P], c_i32),
         "sphb_step": ([P, P, P, c_i64, c_i64, P, P, P, c_i64, P], c_i32),
         "sphb_step_launch_count": ([P, c_i64], c_i64),
     }
@@ -111,7 +120,7 @@ EXPORTED = ("sphb_last_error", "sphb_version", "sphb_workspace_create", "sphb_wo
             "sphb_workspace_reset", "sphb_workspace_bytes", "sphb_ctrl_init", "sphb_cell_keys",
             "sphb_sort", "sphb_reorder", "sphb_cell_ranges", "sphb_cell_ranges_from_sorted",
             "sphb_interact", "sphb_step_begin", "sphb_integrate", "sphb_step_end", "sphb_step",
-            "sphb_step_launch_count")
+            "sphb_step_launch_count", "sphb_integrate_stage", "sphb_energy")
 
 
 def check(rc: int, what: str = "") -> None:

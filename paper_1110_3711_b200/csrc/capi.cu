@@ -51,6 +51,17 @@ static int check_grid(const sphb_grid_t* g) {
   return SPHB_OK;
 }
 
+static int check_params(const sphb_params_t* p) {
+  SPHB_NONNULL(p);
+  if (p->kernel != SPHB_KERNEL_CUBIC && p->kernel != SPHB_KERNEL_WENDLAND)
+    return sphb_set_error(SPHB_E_INVALID, "kernel must be SPHB_KERNEL_CUBIC or SPHB_KERNEL_WENDLAND");
+  if (p->integrator != SPHB_INT_VERLET && p->integrator != SPHB_INT_SYMPLECTIC)
+    return sphb_set_error(SPHB_E_INVALID, "integrator must be SPHB_INT_VERLET or SPHB_INT_SYMPLECTIC");
+  if (p->precision != SPHB_FP32 && p->precision != SPHB_FP64)
+    return sphb_set_error(SPHB_E_INVALID, "precision must be SPHB_FP32 or SPHB_FP64");
+  return SPHB_OK;
+}
+
 extern "C" {
 
 const char* sphb_last_error(void) { return g_err; }
@@ -86,6 +97,7 @@ int sphb_workspace_create(int64_t n_max, int64_t ncells_max, sphb_workspace_t** 
   // a block never spans two cell rows and holds >= 1 target: #blocks <= n/BT + n
   ws->max_blocks = n1 + n1 / 64 + 16;
   if (e == cudaSuccess) e = alloc((void**)&ws->blocks, 2 * sizeof(int4) * ws->max_blocks);
+  if (e == cudaSuccess) e = alloc((void**)&ws->energy_part, sizeof(double) * 5 * 592);
   if (e == cudaSuccess) e = cudaMemset(ws->cnt, 0, sizeof(uint32_t) * 2 * ncells_max);
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
   ws->bytes = bytes;
@@ -108,6 +120,7 @@ int sphb_workspace_destroy(sphb_workspace_t* ws) {
   cudaFree(ws->digit_total);
   cudaFree(ws->scan_partials);
   cudaFree(ws->blocks);
+  cudaFree(ws->energy_part);
   delete ws;
   return SPHB_OK;
 }
@@ -205,7 +218,7 @@ int sphb_interact(sphb_workspace_t* ws, const sphb_params_t* prm, const sphb_gri
                   const int32_t* beg, const int32_t* end, double* acc, double* drho, double* visc,
                   sphb_ctrl_t* ctrl, sphb_stream_t s) {
   SPHB_NONNULL(ws);
-  SPHB_NONNULL(prm);
+  if (int rc = check_params(prm)) return rc;
   SPHB_NONNULL(ctrl);
   if (int rc = check_grid(grid)) return rc;
   if (n < 0 || nb < 0 || nb > n) return sphb_set_error(SPHB_E_INVALID, "bad n/nb");
@@ -238,7 +251,7 @@ int sphb_integrate(sphb_workspace_t* ws, const sphb_params_t* prm, const sphb_gr
                    void* posp, void* velr, void* prev, int64_t* id, uint32_t* keys_next,
                    sphb_ctrl_t* ctrl, sphb_stream_t s) {
   SPHB_NONNULL(ws);
-  SPHB_NONNULL(prm);
+  if (int rc = check_params(prm)) return rc;
   SPHB_NONNULL(ctrl);
   if (int rc = check_grid(grid)) return rc;
   if (n < 0 || nb < 0 || nb > n) return sphb_set_error(SPHB_E_INVALID, "bad n/nb");
@@ -259,17 +272,49 @@ int sphb_step_end(sphb_ctrl_t* ctrl, const sphb_params_t* prm, sphb_step_record_
   return launch_step_end(ctrl, *prm, rec, rec_capacity, (cudaStream_t)s);
 }
 
-int sphb_step(sphb_workspace_t* ws, const sphb_params_t* prm, const sphb_grid_t* grid, int64_t n,
-              int64_t nb, const sphb_state_t* st, sphb_ctrl_t* ctrl, sphb_step_record_t* rec,
-              int64_t rec_capacity, sphb_stream_t s) {
+int sphb_integrate_stage(sphb_workspace_t* ws, const sphb_params_t* prm, const sphb_grid_t* grid,
+                         int64_t n, int64_t nb, int32_t stage, const void* posp_s,
+                         const void* velr_s, const void* prev_s, const int64_t* id_s,
+                         const double* acc, const double* drho, void* posp, void* velr,
+                         void* prev, int64_t* id, uint32_t* keys_next, sphb_ctrl_t* ctrl,
+                         sphb_stream_t s) {
   SPHB_NONNULL(ws);
-  SPHB_NONNULL(prm);
-  SPHB_NONNULL(st);
+  if (int rc = check_params(prm)) return rc;
   SPHB_NONNULL(ctrl);
   if (int rc = check_grid(grid)) return rc;
-  cudaStream_t cs = (cudaStream_t)s;
+  if (stage != 0 && stage != 1) return sphb_set_error(SPHB_E_INVALID, "stage must be 0 or 1");
+  if (n < 0 || nb < 0 || nb > n) return sphb_set_error(SPHB_E_INVALID, "bad n/nb");
+  if (n > 0) {
+    SPHB_NONNULL(posp_s); SPHB_NONNULL(velr_s); SPHB_NONNULL(prev_s); SPHB_NONNULL(id_s);
+    SPHB_NONNULL(acc); SPHB_NONNULL(drho); SPHB_NONNULL(posp); SPHB_NONNULL(velr);
+    SPHB_NONNULL(prev); SPHB_NONNULL(id); SPHB_NONNULL(keys_next);
+  }
+  return launch_integrate_mode(ws, *prm, *grid, n, nb, 1 + stage, (const float4*)posp_s,
+                               (const float4*)velr_s, (const float4*)prev_s, id_s, acc, drho,
+                               (float4*)posp, (float4*)velr, (float4*)prev, id, keys_next, ctrl,
+                               (cudaStream_t)s);
+}
+
+int sphb_energy(sphb_workspace_t* ws, const sphb_params_t* prm, int64_t n, int64_t nb,
+                const void* posp, const void* velr, double* out, sphb_stream_t s) {
+  SPHB_NONNULL(ws);
+  SPHB_NONNULL(prm);
+  SPHB_NONNULL(out);
+  if (n < 0 || nb < 0 || nb > n) return sphb_set_error(SPHB_E_INVALID, "bad n/nb");
+  if (n > 0) {
+    SPHB_NONNULL(posp);
+    SPHB_NONNULL(velr);
+  }
+  return launch_energy(ws, *prm, n, nb, (const float4*)posp, (const float4*)velr, out,
+                       (cudaStream_t)s);
+}
+
+// NL -> PI on the primary state, then the system update of `mode` (0 verlet, 1/2 symplectic
+// predictor/corrector)
+static int stage_pass(sphb_workspace_t* ws, const sphb_params_t* prm, const sphb_grid_t* grid,
+                      int64_t n, int64_t nb, const sphb_state_t* st, sphb_ctrl_t* ctrl, int mode,
+                      cudaStream_t cs) {
   int rc;
-  if ((rc = launch_step_begin(ctrl, cs))) return rc;
   if ((rc = launch_sort(ws, *grid, st->keys, n, st->keys_sorted, st->perm, ctrl, cs))) return rc;
   if ((rc = launch_reorder(*prm, *grid, n, st->perm, st->keys_sorted, (const float4*)st->posp,
                            (const float4*)st->velr, (const float4*)st->prev, st->id,
@@ -281,18 +326,36 @@ int sphb_step(sphb_workspace_t* ws, const sphb_params_t* prm, const sphb_grid_t*
                             (const float4*)st->velr_s, (const float4*)st->aux, st->cell_s, st->beg,
                             st->end, st->acc, st->drho, st->visc, ctrl, cs)))
     return rc;
-  if ((rc = launch_integrate(ws, *prm, *grid, n, nb, (const float4*)st->posp_s,
-                             (const float4*)st->velr_s, (const float4*)st->prev_s, st->id_s,
-                             st->acc, st->drho, (float4*)st->posp, (float4*)st->velr,
-                             (float4*)st->prev, st->id, st->keys, ctrl, cs)))
-    return rc;
+  return launch_integrate_mode(ws, *prm, *grid, n, nb, mode, (const float4*)st->posp_s,
+                               (const float4*)st->velr_s, (const float4*)st->prev_s, st->id_s,
+                               st->acc, st->drho, (float4*)st->posp, (float4*)st->velr,
+                               (float4*)st->prev, st->id, st->keys, ctrl, cs);
+}
+
+int sphb_step(sphb_workspace_t* ws, const sphb_params_t* prm, const sphb_grid_t* grid, int64_t n,
+              int64_t nb, const sphb_state_t* st, sphb_ctrl_t* ctrl, sphb_step_record_t* rec,
+              int64_t rec_capacity, sphb_stream_t s) {
+  SPHB_NONNULL(ws);
+  if (int rc = check_params(prm)) return rc;
+  SPHB_NONNULL(st);
+  SPHB_NONNULL(ctrl);
+  if (int rc = check_grid(grid)) return rc;
+  cudaStream_t cs = (cudaStream_t)s;
+  int rc;
+  if ((rc = launch_step_begin(ctrl, cs))) return rc;
+  if (prm->integrator == SPHB_INT_SYMPLECTIC) {
+    if ((rc = stage_pass(ws, prm, grid, n, nb, st, ctrl, 1, cs))) return rc;
+    if ((rc = stage_pass(ws, prm, grid, n, nb, st, ctrl, 2, cs))) return rc;
+  } else {
+    if ((rc = stage_pass(ws, prm, grid, n, nb, st, ctrl, 0, cs))) return rc;
+  }
   return launch_step_end(ctrl, *prm, rec, rec_capacity, cs);
 }
 
 int64_t sphb_step_launch_count(const sphb_grid_t* grid, int64_t n) {
   if (!grid) return 0;
   return 1 /*begin*/ + nl_launch_count(*grid, n) + interact_launch_count(n) + 1 /*integrate*/ +
-         1 /*end*/;
+         1 /*end*/;  // (a symplectic step runs the middle three twice, plus k_stage_mid)
 }
 
 }  // extern "C"

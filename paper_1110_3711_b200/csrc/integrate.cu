@@ -56,6 +56,18 @@ __global__ void k_step_begin(sphb_ctrl_t* c) {
   c->nblk[0] = c->nblk[1] = 0;
 }
 
+// Piston law of the wave tank (extension): x(t) = x0 + S/2 (1 - cos wt),
+// v(t) = S/2 w sin wt, w = 2 pi / T, for boundary ids in [piston_id0, piston_id1).
+__device__ __forceinline__ void piston_at(const sphb_params_t& p, double t, float& x, float& vx) {
+  const double w = xdiv(2.0 * 3.141592653589793, p.piston_period);
+  const double hs = xmul(0.5, p.piston_stroke);
+  x = __double2float_rn(xadd(p.piston_x0, xmul(hs, xsub(1.0, cos(xmul(w, t))))));
+  vx = __double2float_rn(xmul(xmul(hs, w), sin(xmul(w, t))));
+}
+
+// MODE 0: verlet_update (sim.py:235-259), the reference.  MODE 1 / 2: symplectic predictor /
+// corrector (extension).  All fused with the next stage's assign_cells (K1) + histogram.
+template <int MODE>
 __global__ void __launch_bounds__(256) k_integrate(
     sphb_params_t p, sphb_grid_t g, int cellbits, int64_t ncells, int64_t n, int64_t nb,
     const float4* __restrict__ posp_s, const float4* __restrict__ velr_s,
@@ -65,10 +77,14 @@ __global__ void __launch_bounds__(256) k_integrate(
     uint32_t* __restrict__ keys_next, uint32_t* __restrict__ cnt, sphb_ctrl_t* ctrl) {
   if (!step_live(ctrl)) return;
   const int64_t step = ctrl->step;
-  const double dt = step_dt(ctrl, p);
+  const double dt = MODE == 2 ? ctrl->dt_stage : step_dt(ctrl, p);
   const bool corrector = (step % p.verlet_stride) == 0;
   const double c2 = xmul(xmul(0.5, dt), dt);
   const double dt2 = xmul(2.0, dt);
+  const double hdt = xmul(0.5, dt);
+  const bool piston = p.piston_id1 > p.piston_id0;
+  // time the updated state belongs to (the piston law is evaluated there)
+  const double t_new = MODE == 1 ? xadd(ctrl->t_sim, hdt) : xadd(ctrl->t_sim, dt);
   const int lane = threadIdx.x & 31;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n; base += stride) {
@@ -77,45 +93,74 @@ __global__ void __launch_bounds__(256) k_integrate(
     if (i < n) {
       const float4 ps = posp_s[i], vs = velr_s[i], pv = prev_s[i];
       const double dr = drho[i];
-      float4 np, nv;
+      float4 np, nv, nprev;
       double nrho;
-      if (corrector)
-        nrho = xadd((double)vs.w, xmul(dt, dr));
+      if (MODE == 0)
+        nrho = corrector ? xadd((double)vs.w, xmul(dt, dr)) : xadd((double)pv.w, xmul(dt2, dr));
+      else if (MODE == 1)
+        nrho = xadd((double)vs.w, xmul(hdt, dr));
       else
-        nrho = xadd((double)pv.w, xmul(dt2, dr));
+        nrho = xadd((double)pv.w, xmul(dt, dr));
       if (i >= nb) {
         const double ax = xadd(acc[3 * i + 0], p.g[0]);
         const double ay = xadd(acc[3 * i + 1], p.g[1]);
         const double az = xadd(acc[3 * i + 2], p.g[2]);
         const double vx = (double)vs.x, vy = (double)vs.y, vz = (double)vs.z;
-        np.x = __double2float_rn(xadd(xadd((double)ps.x, xmul(dt, vx)), xmul(c2, ax)));
-        np.y = __double2float_rn(xadd(xadd((double)ps.y, xmul(dt, vy)), xmul(c2, ay)));
-        np.z = __double2float_rn(xadd(xadd((double)ps.z, xmul(dt, vz)), xmul(c2, az)));
-        if (corrector) {
-          nv.x = __double2float_rn(xadd(vx, xmul(dt, ax)));
-          nv.y = __double2float_rn(xadd(vy, xmul(dt, ay)));
-          nv.z = __double2float_rn(xadd(vz, xmul(dt, az)));
-        } else {
-          nv.x = __double2float_rn(xadd((double)pv.x, xmul(dt2, ax)));
-          nv.y = __double2float_rn(xadd((double)pv.y, xmul(dt2, ay)));
-          nv.z = __double2float_rn(xadd((double)pv.z, xmul(dt2, az)));
+        if (MODE == 0) {
+          np.x = __double2float_rn(xadd(xadd((double)ps.x, xmul(dt, vx)), xmul(c2, ax)));
+          np.y = __double2float_rn(xadd(xadd((double)ps.y, xmul(dt, vy)), xmul(c2, ay)));
+          np.z = __double2float_rn(xadd(xadd((double)ps.z, xmul(dt, vz)), xmul(c2, az)));
+          if (corrector) {
+            nv.x = __double2float_rn(xadd(vx, xmul(dt, ax)));
+            nv.y = __double2float_rn(xadd(vy, xmul(dt, ay)));
+            nv.z = __double2float_rn(xadd(vz, xmul(dt, az)));
+          } else {
+            nv.x = __double2float_rn(xadd((double)pv.x, xmul(dt2, ax)));
+            nv.y = __double2float_rn(xadd((double)pv.y, xmul(dt2, ay)));
+            nv.z = __double2float_rn(xadd((double)pv.z, xmul(dt2, az)));
+          }
+        } else if (MODE == 1) {  // r* = r + dt/2 v, v* = v + dt/2 (a + g)
+          np.x = __double2float_rn(xadd((double)ps.x, xmul(hdt, vx)));
+          np.y = __double2float_rn(xadd((double)ps.y, xmul(hdt, vy)));
+          np.z = __double2float_rn(xadd((double)ps.z, xmul(hdt, vz)));
+          nv.x = __double2float_rn(xadd(vx, xmul(hdt, ax)));
+          nv.y = __double2float_rn(xadd(vy, xmul(hdt, ay)));
+          nv.z = __double2float_rn(xadd(vz, xmul(hdt, az)));
+        } else {  // v' = v + dt (a* + g), r' = r* + dt/2 v'
+          const double ux = xadd((double)pv.x, xmul(dt, ax));
+          const double uy = xadd((double)pv.y, xmul(dt, ay));
+          const double uz = xadd((double)pv.z, xmul(dt, az));
+          nv.x = __double2float_rn(ux);
+          nv.y = __double2float_rn(uy);
+          nv.z = __double2float_rn(uz);
+          np.x = __double2float_rn(xadd((double)ps.x, xmul(hdt, (double)nv.x)));
+          np.y = __double2float_rn(xadd((double)ps.y, xmul(hdt, (double)nv.y)));
+          np.z = __double2float_rn(xadd((double)ps.z, xmul(hdt, (double)nv.z)));
         }
       } else {
         np.x = ps.x; np.y = ps.y; np.z = ps.z;  // boundary frozen (sim.py:256-258)
         nv.x = vs.x; nv.y = vs.y; nv.z = vs.z;
+        if (piston) {
+          const int64_t pid = id_s[i];
+          if (pid >= p.piston_id0 && pid < p.piston_id1) piston_at(p, t_new, np.x, nv.x);
+        }
       }
       np.w = 0.f;  // press is recomputed by the next step's reorder (K3)
       nv.w = __double2float_rn(nrho);
+      if (MODE == 2)
+        nprev = nv;
+      else
+        nprev = vs;  // history <- current (sim.py:254-255); symplectic: (v, rho) at t
       posp[i] = np;
       velr[i] = nv;
-      prev[i] = vs;  // history <- current (sim.py:254-255)
+      prev[i] = nprev;
       id[i] = id_s[i];
       if (!(isfinite(nv.x) && isfinite(nv.y) && isfinite(nv.z) && isfinite(nv.w)))
         raise_div(ctrl, step, SPHB_DIV_NONFINITE_STATE, 0);
       // next step's assign_cells (K1), fused
       const int32_t c = cell_of(np.x, np.y, np.z, g);
       if (c < 0) {
-        raise_div(ctrl, step + 1, SPHB_DIV_LEFT_DOMAIN, (uint64_t)i);
+        raise_div(ctrl, MODE == 1 ? step : step + 1, SPHB_DIV_LEFT_DOMAIN, (uint64_t)i);
         keys_next[i] = 0xffffffffu;
       } else {
         const uint32_t list = i >= nb ? 1u : 0u;
@@ -128,16 +173,87 @@ __global__ void __launch_bounds__(256) k_integrate(
   }
 }
 
+// symplectic: fix the step's dt and counters after the first stage, reset the per-stage
+// accumulators for the second interaction
+__global__ void k_stage_mid(sphb_ctrl_t* c, sphb_params_t p) {
+  if (!step_live(c)) return;
+  c->dt_stage = step_dt(c, p);
+  for (int k = 0; k < 4; ++k) {
+    c->counters_stage[k] = c->counters[k];
+    c->counters[k] = 0;
+  }
+  c->dtmin_f = (uint64_t)__double_as_longlong(INFINITY);
+  c->dtmin_cv = (uint64_t)__double_as_longlong(INFINITY);
+  c->tile_next[0] = c->tile_next[1] = 0;
+  c->nblk[0] = c->nblk[1] = 0;
+}
+
+// ---------------------------------------------------------------- energy diagnostics
+constexpr int EN_BLOCKS = 592, EN_THREADS = 256;
+
+__device__ __forceinline__ double tait_u(double r, const sphb_params_t& p) {
+  const double B = p.tait_b, gm = p.gamma;
+  return xadd(xdiv(xmul(xdiv(B, xsub(gm, 1.0)), pow(r, xsub(gm, 1.0))), pow(p.rho0, gm)), xdiv(B, r));
+}
+
+__global__ void __launch_bounds__(EN_THREADS) k_energy_part(sphb_params_t p, int64_t n, int64_t nb,
+                                                            const float4* __restrict__ posp,
+                                                            const float4* __restrict__ velr,
+                                                            double* __restrict__ part) {
+  __shared__ double sm[5][EN_THREADS];
+  double a[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+  const double gmag = sqrt(p.g[0] * p.g[0] + p.g[1] * p.g[1] + p.g[2] * p.g[2]);
+  const double u0 = tait_u(p.rho0, p);
+  for (int64_t i = (int64_t)blockIdx.x * EN_THREADS + threadIdx.x; i < n;
+       i += (int64_t)EN_BLOCKS * EN_THREADS) {
+    const float4 v = velr[i];
+    const bool fl = i >= nb;
+    const double m = fl ? p.mass_fluid : p.mass_boundary;
+    const double r = (double)v.w;
+    if (fl) {
+      const double vx = v.x, vy = v.y, vz = v.z;
+      a[0] += m * (vx * vx + vy * vy + vz * vz);
+      a[1] += m * gmag * (double)posp[i].z;
+      a[3] += r;
+    }
+    a[2] += m * (tait_u(r, p) - u0);
+    a[4] += r;
+  }
+  for (int k = 0; k < 5; ++k) sm[k][threadIdx.x] = a[k];
+  __syncthreads();
+  for (int w = EN_THREADS / 2; w > 0; w >>= 1) {  // fixed-shape tree: deterministic
+    if (threadIdx.x < w)
+      for (int k = 0; k < 5; ++k) sm[k][threadIdx.x] += sm[k][threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x < 5) part[blockIdx.x * 5 + threadIdx.x] = sm[threadIdx.x][0];
+}
+
+__global__ void k_energy_final(int64_t n, int64_t nb, const double* __restrict__ part,
+                               double* __restrict__ out) {
+  if (threadIdx.x != 0) return;
+  double a[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+  for (int b = 0; b < EN_BLOCKS; ++b)
+    for (int k = 0; k < 5; ++k) a[k] += part[b * 5 + k];
+  out[0] = 0.5 * a[0];
+  out[1] = a[1];
+  out[2] = a[2];
+  out[3] = n > nb ? a[3] / (double)(n - nb) : 0.0;
+  out[4] = n > 0 ? a[4] / (double)n : 0.0;
+}
+
 __global__ void k_step_end(sphb_ctrl_t* c, sphb_params_t p, sphb_step_record_t* rec, int64_t cap) {
   if (!step_live(c)) return;
-  const double dt = step_dt(c, p);
+  const bool symp = p.integrator == SPHB_INT_SYMPLECTIC;
+  const double dt = symp ? c->dt_stage : step_dt(c, p);
+  const uint64_t* cnt = symp ? c->counters_stage : c->counters;
   if (rec && cap > 0) {
     sphb_step_record_t r;
     r.dt = dt;
-    r.candidate_pairs = c->counters[0];
-    r.hits_ordered = c->counters[1];
-    r.force_evals = c->counters[2];
-    r.ff_force_evals = c->counters[3];
+    r.candidate_pairs = cnt[0];
+    r.hits_ordered = cnt[1];
+    r.force_evals = cnt[2];
+    r.ff_force_evals = cnt[3];
     rec[c->step % cap] = r;
   }
   c->dt = dt;
@@ -157,19 +273,56 @@ int launch_step_begin(sphb_ctrl_t* ctrl, cudaStream_t s) {
   return sphb_check_launch("k_step_begin");
 }
 
+int launch_integrate_mode(sphb_workspace* ws, const sphb_params_t& p, const sphb_grid_t& g,
+                          int64_t n, int64_t nb, int mode, const float4* posp_s,
+                          const float4* velr_s, const float4* prev_s, const int64_t* id_s,
+                          const double* acc, const double* drho, float4* posp, float4* velr,
+                          float4* prev, int64_t* id, uint32_t* keys_next, sphb_ctrl_t* ctrl,
+                          cudaStream_t s) {
+  if (p.verlet_stride < 1) return sphb_set_error(SPHB_E_INVALID, "verlet_corrector_stride must be >= 1");
+  if (p.piston_id1 > p.piston_id0 && !(p.piston_period > 0.0))
+    return sphb_set_error(SPHB_E_INVALID, "piston period must be positive");
+  if (n > 0) {
+    int64_t blocks = (n + 255) / 256;
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    const int cb = cellbits_of(g);
+    const int64_t nc = ncells_of(g);
+    if (mode == 0)
+      k_integrate<0><<<(unsigned)blocks, 256, 0, s>>>(p, g, cb, nc, n, nb, posp_s, velr_s, prev_s,
+                                                      id_s, acc, drho, posp, velr, prev, id,
+                                                      keys_next, ws->cnt, ctrl);
+    else if (mode == 1)
+      k_integrate<1><<<(unsigned)blocks, 256, 0, s>>>(p, g, cb, nc, n, nb, posp_s, velr_s, prev_s,
+                                                      id_s, acc, drho, posp, velr, prev, id,
+                                                      keys_next, ws->cnt, ctrl);
+    else
+      k_integrate<2><<<(unsigned)blocks, 256, 0, s>>>(p, g, cb, nc, n, nb, posp_s, velr_s, prev_s,
+                                                      id_s, acc, drho, posp, velr, prev, id,
+                                                      keys_next, ws->cnt, ctrl);
+    if (int rc = sphb_check_launch("k_integrate")) return rc;
+  }
+  if (mode == 1) {
+    k_stage_mid<<<1, 1, 0, s>>>(ctrl, p);
+    return sphb_check_launch("k_stage_mid");
+  }
+  return SPHB_OK;
+}
+
 int launch_integrate(sphb_workspace* ws, const sphb_params_t& p, const sphb_grid_t& g, int64_t n,
                      int64_t nb, const float4* posp_s, const float4* velr_s, const float4* prev_s,
                      const int64_t* id_s, const double* acc, const double* drho, float4* posp,
                      float4* velr, float4* prev, int64_t* id, uint32_t* keys_next,
                      sphb_ctrl_t* ctrl, cudaStream_t s) {
-  if (n == 0) return SPHB_OK;
-  if (p.verlet_stride < 1) return sphb_set_error(SPHB_E_INVALID, "verlet_corrector_stride must be >= 1");
-  int64_t blocks = (n + 255) / 256;
-  if (blocks > 148 * 16) blocks = 148 * 16;
-  k_integrate<<<(unsigned)blocks, 256, 0, s>>>(p, g, cellbits_of(g), ncells_of(g), n, nb, posp_s,
-                                               velr_s, prev_s, id_s, acc, drho, posp, velr, prev,
-                                               id, keys_next, ws->cnt, ctrl);
-  return sphb_check_launch("k_integrate");
+  return launch_integrate_mode(ws, p, g, n, nb, 0, posp_s, velr_s, prev_s, id_s, acc, drho, posp,
+                               velr, prev, id, keys_next, ctrl, s);
+}
+
+int launch_energy(sphb_workspace* ws, const sphb_params_t& p, int64_t n, int64_t nb,
+                  const float4* posp, const float4* velr, double* out, cudaStream_t s) {
+  k_energy_part<<<EN_BLOCKS, EN_THREADS, 0, s>>>(p, n, nb, posp, velr, ws->energy_part);
+  if (int rc = sphb_check_launch("k_energy_part")) return rc;
+  k_energy_final<<<1, 32, 0, s>>>(n, nb, ws->energy_part, out);
+  return sphb_check_launch("k_energy_final");
 }
 
 int launch_step_end(sphb_ctrl_t* ctrl, const sphb_params_t& p, sphb_step_record_t* rec,

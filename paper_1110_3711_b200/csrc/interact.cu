@@ -254,7 +254,12 @@ __device__ __forceinline__ void pair_eval64(const KArgs& a, const Own<double>& o
   const double q = xmul(r, p.invh);
   const double kc = p.kc;
   double wab, dwdq;
-  if (q < 1.0) {
+  if (p.kernel == SPHB_KERNEL_WENDLAND) {  // W = kc t^4 (2q + 1), dW/dq = -5 kc q t^3
+    const double t = xsub(1.0, xmul(0.5, q));
+    const double t2 = xmul(t, t);
+    wab = xmul(xmul(kc, xmul(t2, t2)), xadd(xmul(2.0, q), 1.0));
+    dwdq = xmul(xmul(xmul(-5.0, kc), q), xmul(t2, t));
+  } else if (q < 1.0) {
     wab = xmul(kc, xadd(xsub(1.0, xmul(xmul(1.5, q), q)), xmul(xmul(xmul(0.75, q), q), q)));
     dwdq = xmul(xmul(kc, xsub(xmul(2.25, q), 3.0)), q);
   } else {
@@ -930,7 +935,7 @@ struct Geo2 {
   f2_t a1xy, a1zw, b1zw, a2xy, a2zw, b2zw, dxy1, dxy2, dz, r2, dot;
 };
 
-template <bool G7, bool EQM, int NG>
+template <bool G7, bool EQM, bool WEND, int NG>
 __device__ __forceinline__ void eval_v8(const KArgs& a, const K32& c, const Own32& o,
                                         const uint32_t (&ad)[2 * NG], int xlo, int xhi,
                                         Acc32 (&s)[NG]) {
@@ -995,13 +1000,21 @@ __device__ __forceinline__ void eval_v8(const KArgs& a, const K32& c, const Own3
     const f2_t R2M = pk(ok1 ? lo(g[k].r2) : c.sup2_lo, ok2 ? hi(g[k].r2) : c.sup2_lo);
     const f2_t RINV = pk(rsqrtf(lo(R2M)), rsqrtf(hi(R2M)));
     const f2_t Q = mul2(mul2(R2M, RINV), bc(c.invh));
-    const f2_t T = sub2(bc(2.0f), Q);
-    const f2_t UM = sub2(Q, bc(1.0f));
-    const f2_t UN = pk(fminf(lo(UM), 0.0f), fminf(hi(UM), 0.0f));  // -max(1 - q, 0)
-    const f2_t T2Q = mul2(mul2(T, T), bc(0.25f));
-    const f2_t U2 = mul2(UN, UN);
-    const f2_t W = fma2(T2Q, T, mul2(U2, UN));  // t^3/4 - u^3
-    const f2_t DW3 = sub2(U2, T2Q);             // (3 u^2 - 3/4 t^2) / 3
+    f2_t W, DWR;  // kernel shape W/kc and the gradient shape (-gc / mask factor)
+    if (WEND) {   // Wendland C2: W = kc t^4 (2q + 1), gc = -5 kc t^3 / h^2, t = 1 - q/2
+      const f2_t T = fma2(Q, bc(-0.5f), bc(1.0f));
+      const f2_t T2 = mul2(T, T);
+      W = mul2(mul2(T2, T2), fma2(Q, bc(2.0f), bc(1.0f)));
+      DWR = mul2(T2, T);
+    } else {      // cubic spline (physics.py:196-205)
+      const f2_t T = sub2(bc(2.0f), Q);
+      const f2_t UM = sub2(Q, bc(1.0f));
+      const f2_t UN = pk(fminf(lo(UM), 0.0f), fminf(hi(UM), 0.0f));  // -max(1 - q, 0)
+      const f2_t T2Q = mul2(mul2(T, T), bc(0.25f));
+      const f2_t U2 = mul2(UN, UN);
+      W = fma2(T2Q, T, mul2(U2, UN));      // t^3/4 - u^3
+      DWR = mul2(sub2(U2, T2Q), RINV);     // (3 u^2 - 3/4 t^2) / (3 r)
+    }
     const float sr1 = hi(g[k].b1zw), sr2 = hi(g[k].b2zw);
     const float rj1 = fabsf(sr1), rj2 = fabsf(sr2);
     const f2_t RHOJ = pk(rj1, rj2);
@@ -1011,7 +1024,7 @@ __device__ __forceinline__ void eval_v8(const KArgs& a, const K32& c, const Own3
     } else {
       MJ = mul2(OK, pk(sr1 < 0.0f ? c.nkgc_b : c.nkgc, sr2 < 0.0f ? c.nkgc_b : c.nkgc));
     }
-    const f2_t GCN = mul2(mul2(DW3, RINV), MJ);  // -gc [m_j], zero when masked
+    const f2_t GCN = mul2(DWR, MJ);  // -gc [m_j], zero when masked
     f2_t CSJ;                                    // -alpha h cs_j
     if (G7) {
       const f2_t RR = mul2(RHOJ, bc(c.kcs));
@@ -1039,7 +1052,7 @@ __device__ __forceinline__ void eval_v8(const KArgs& a, const K32& c, const Own3
   }
 }
 
-template <bool G7, bool EQM>
+template <bool G7, bool EQM, bool WEND>
 __global__ void __launch_bounds__(NW * 32, 2) k_interact_v8(KArgs a, K32 k32) {
   if (!step_live(a.ctrl)) return;
   constexpr int SCAP = Cfg<float>::SCAP;
@@ -1299,7 +1312,7 @@ __global__ void __launch_bounds__(NW * 32, 2) k_interact_v8(KArgs a, K32 k32) {
         uint32_t ad[2 * V8_NG];
 #pragma unroll
         for (int k = 0; k < 2 * V8_NG; ++k) ad[k] = pop();
-        eval_v8<G7, EQM, V8_NG>(a, k32, o, ad, xlo, xhi, s);
+        eval_v8<G7, EQM, WEND, V8_NG>(a, k32, o, ad, xlo, xhi, s);
       }
       pend = pend > P * K ? pend - P * K : 0u;
       __syncwarp();
@@ -1525,21 +1538,28 @@ int launch_kernel(const KArgs& a, int nsm, cudaStream_t s) {
   return sphb_check_launch("k_interact");
 }
 
-template <bool G7, bool EQM>
+template <bool G7, bool EQM, bool WEND>
 int launch_v8(const KArgs& a, const K32& k, int nsm, cudaStream_t s) {
   static int grid = 0;
   const size_t bytes = V8_SMEM;
   if (grid == 0) {
-    cudaError_t e = cudaFuncSetAttribute(k_interact_v8<G7, EQM>,
+    cudaError_t e = cudaFuncSetAttribute(k_interact_v8<G7, EQM, WEND>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
     if (e != cudaSuccess)
       return sphb_set_error(SPHB_E_CUDA, "smem attribute: %s", cudaGetErrorString(e));
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_interact_v8<G7, EQM>, NW * 32, bytes);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_interact_v8<G7, EQM, WEND>, NW * 32, bytes);
     grid = nsm * (per_sm > 0 ? per_sm : 1);
   }
-  k_interact_v8<G7, EQM><<<grid, NW * 32, bytes, s>>>(a, k);
+  k_interact_v8<G7, EQM, WEND><<<grid, NW * 32, bytes, s>>>(a, k);
   return sphb_check_launch("k_interact_v8");
+}
+
+template <bool WEND>
+int launch_v8_kernel(const KArgs& a, const K32& k, bool eqm, int nsm, cudaStream_t s) {
+  if (a.gamma7)
+    return eqm ? launch_v8<true, true, WEND>(a, k, nsm, s) : launch_v8<true, false, WEND>(a, k, nsm, s);
+  return eqm ? launch_v8<false, true, WEND>(a, k, nsm, s) : launch_v8<false, false, WEND>(a, k, nsm, s);
 }
 
 template <typename R>
@@ -1566,10 +1586,12 @@ int launch_one(const KArgs& a, int nsm, cudaStream_t s) {
     k.kcs = a.gamma7 ? (float)(cbrt(p.c0) / p.rho0 * cbrt(nalh))
                      : (float)(p.c0 * pow(p.rho0, -(p.gamma - 1.0) * 0.5) * nalh);
     const bool eqm = p.mass_fluid == p.mass_boundary;
-    k.nkgc = (float)(-3.0 * p.kc * p.invh * (eqm ? 1.0 : p.mass_fluid));
-    k.nkgc_b = (float)(-3.0 * p.kc * p.invh * (eqm ? 1.0 : p.mass_boundary));
-    if (a.gamma7) return eqm ? launch_v8<true, true>(a, k, nsm, s) : launch_v8<true, false>(a, k, nsm, s);
-    return eqm ? launch_v8<false, true>(a, k, nsm, s) : launch_v8<false, false>(a, k, nsm, s);
+    const bool wend = p.kernel == SPHB_KERNEL_WENDLAND;
+    // -gc / (gradient shape): cubic -3 kc/h (shape (u^2 - t^2/4)/r), Wendland 5 kc/h^2 (t^3)
+    const double gk = wend ? 5.0 * p.kc * p.invh * p.invh : -3.0 * p.kc * p.invh;
+    k.nkgc = (float)(gk * (eqm ? 1.0 : p.mass_fluid));
+    k.nkgc_b = (float)(gk * (eqm ? 1.0 : p.mass_boundary));
+    return wend ? launch_v8_kernel<true>(a, k, eqm, nsm, s) : launch_v8_kernel<false>(a, k, eqm, nsm, s);
   } else {
     const bool eqm = a.p.mass_fluid == a.p.mass_boundary;
     if (a.gamma7)

@@ -25,6 +25,7 @@ struct sphb_workspace {
   int4* blocks = nullptr;  // interaction target blocks (fluid i0,i1, boundary i0,i1)
   int64_t max_blocks = 0;
   int64_t max_sort_tiles = 0, max_scan_tiles = 0;
+  double* energy_part = nullptr;  // 592 x 5 partial sums of sphb_energy
   size_t bytes = 0;
 };
 
@@ -60,6 +61,14 @@ int launch_integrate(sphb_workspace* ws, const sphb_params_t& p, const sphb_grid
                      const int64_t* id_s, const double* acc, const double* drho, float4* posp,
                      float4* velr, float4* prev, int64_t* id, uint32_t* keys_next,
                      sphb_ctrl_t* ctrl, cudaStream_t s);
+int launch_integrate_mode(sphb_workspace* ws, const sphb_params_t& p, const sphb_grid_t& g,
+                          int64_t n, int64_t nb, int mode, const float4* posp_s,
+                          const float4* velr_s, const float4* prev_s, const int64_t* id_s,
+                          const double* acc, const double* drho, float4* posp, float4* velr,
+                          float4* prev, int64_t* id, uint32_t* keys_next, sphb_ctrl_t* ctrl,
+                          cudaStream_t s);
+int launch_energy(sphb_workspace* ws, const sphb_params_t& p, int64_t n, int64_t nb,
+                  const float4* posp, const float4* velr, double* out, cudaStream_t s);
 int launch_step_end(sphb_ctrl_t* ctrl, const sphb_params_t& p, sphb_step_record_t* rec, int64_t cap,
                     cudaStream_t s);
 int launch_ctrl_init(sphb_ctrl_t* ctrl, int64_t max_steps, double t_end, cudaStream_t s);

@@ -181,18 +181,19 @@ class DeviceSim:
         self.ws.reset()
         self.first_keys()
 
-    def launch_step(self, events=None):
-        """Enqueue one NL -> PI -> SU step (no host sync).  ``events`` = 4 CUDA events
-        recorded at the stage boundaries (NL | PI | SU)."""
+    @property
+    def symplectic(self) -> bool:
+        return int(self.prm.integrator) == _lib.SPHB_INT_SYMPLECTIC
+
+    def n_stage_events(self) -> int:
+        """Events launch_step records per step: 4 (verlet) or 7 (symplectic)."""
+        return 7 if self.symplectic else 4
+
+    def _stage(self, mode: int, ev):
+        """NL -> PI -> system update ``mode`` (0 verlet, 1/2 symplectic stages); records
+        ev[0] after NL, ev[1] after PI, ev[2] after the update."""
         L, s, ws = _lib.lib(), _stream(), self.ws.handle
         g, p, n, nb = _lib.ref(self.grid), _lib.ref(self.prm), self.n, self.nb
-        if events is None:
-            _lib.check(L.sphb_step(ws, p, g, n, nb, _lib.ref(self._state), _ptr(self.ctrl),
-                                   _ptr(self.rec), self.rec_cap, s), "sphb_step")
-            return
-        e0, e1, e2, e3 = events
-        e0.record()
-        _lib.check(L.sphb_step_begin(_ptr(self.ctrl), s), "sphb_step_begin")
         _lib.check(L.sphb_sort(ws, g, _ptr(self.keys), n, _ptr(self.keys_sorted), _ptr(self.perm),
                                _ptr(self.ctrl), s), "sphb_sort")
         _lib.check(L.sphb_reorder(p, g, n, _ptr(self.perm), _ptr(self.keys_sorted), _ptr(self.posp),
@@ -202,20 +203,53 @@ class DeviceSim:
                    "sphb_reorder")
         _lib.check(L.sphb_cell_ranges(ws, g, _ptr(self.beg), _ptr(self.end), _ptr(self.ctrl), s),
                    "sphb_cell_ranges")
-        e1.record()
+        ev[0].record()
         _lib.check(L.sphb_interact(ws, p, g, n, nb, _ptr(self.posp_s), _ptr(self.velr_s),
                                    _ptr(self.aux), _ptr(self.cell_s), _ptr(self.beg),
                                    _ptr(self.end), _ptr(self.acc), _ptr(self.drho),
                                    _ptr(self.visc), _ptr(self.ctrl), s), "sphb_interact")
-        e2.record()
-        _lib.check(L.sphb_integrate(ws, p, g, n, nb, _ptr(self.posp_s), _ptr(self.velr_s),
-                                    _ptr(self.prev_s), _ptr(self.id_s), _ptr(self.acc),
-                                    _ptr(self.drho), _ptr(self.posp), _ptr(self.velr),
-                                    _ptr(self.prev), _ptr(self.id), _ptr(self.keys),
-                                    _ptr(self.ctrl), s), "sphb_integrate")
+        ev[1].record()
+        args = (_ptr(self.posp_s), _ptr(self.velr_s), _ptr(self.prev_s), _ptr(self.id_s),
+                _ptr(self.acc), _ptr(self.drho), _ptr(self.posp), _ptr(self.velr), _ptr(self.prev),
+                _ptr(self.id), _ptr(self.keys), _ptr(self.ctrl), s)
+        if mode == 0:
+            _lib.check(L.sphb_integrate(ws, p, g, n, nb, *args), "sphb_integrate")
+        else:
+            _lib.check(L.sphb_integrate_stage(ws, p, g, n, nb, mode - 1, *args), "sphb_integrate_stage")
+        ev[2].record()
+
+    def launch_step(self, events=None):
+        """Enqueue one step (no host sync).  ``events``: n_stage_events() CUDA events recorded
+        at the stage boundaries (verlet: start | NL | PI | SU; symplectic: start, then
+        NL | PI | SU of each of the two stages)."""
+        L, s = _lib.lib(), _stream()
+        p = _lib.ref(self.prm)
+        if events is None:
+            _lib.check(L.sphb_step(self.ws.handle, p, _lib.ref(self.grid), self.n, self.nb,
+                                   _lib.ref(self._state), _ptr(self.ctrl), _ptr(self.rec),
+                                   self.rec_cap, s), "sphb_step")
+            return
+        events[0].record()
+        _lib.check(L.sphb_step_begin(_ptr(self.ctrl), s), "sphb_step_begin")
+        if self.symplectic:
+            self._stage(1, events[1:4])
+            self._stage(2, events[4:7])
+        else:
+            self._stage(0, events[1:4])
         _lib.check(L.sphb_step_end(_ptr(self.ctrl), p, _ptr(self.rec), self.rec_cap, s),
                    "sphb_step_end")
-        e3.record()
+        events[-1].record()
+
+    @staticmethod
+    def stage_seconds(events) -> tuple[float, float, float, float]:
+        """(nl, pi, su, wall) seconds of one step's events (launch_step order)."""
+        ms = lambda a, b: a.elapsed_time(b)  # noqa: E731
+        if len(events) == 4:
+            e0, e1, e2, e3 = events
+            return ms(e0, e1) * 1e-3, ms(e1, e2) * 1e-3, ms(e2, e3) * 1e-3, ms(e0, e3) * 1e-3
+        e0, n1, p1, s1, n2, p2, s2 = events
+        return ((ms(e0, n1) + ms(s1, n2)) * 1e-3, (ms(n1, p1) + ms(n2, p2)) * 1e-3,
+                (ms(p1, s1) + ms(p2, s2)) * 1e-3, ms(e0, s2) * 1e-3)
 
     def capture(self, steps: int):
         """Capture ``steps`` whole steps into one CUDA graph (replayed by run_graph)."""
@@ -232,6 +266,47 @@ class DeviceSim:
 
     def launches_per_step(self) -> int:
         return int(_lib.lib().sphb_step_launch_count(_lib.ref(self.grid), self.n))
+
+    # ------------------------------------------------------------------ diagnostics
+    def energy(self) -> dict:
+        """sphb_energy on the primary state: KE, PE, IE (Tait), mean fluid rho, mean rho."""
+        out = torch.zeros(5, dtype=torch.float64, device=self.device)
+        _lib.check(_lib.lib().sphb_energy(self.ws.handle, _lib.ref(self.prm), self.n, self.nb,
+                                          _ptr(self.posp), _ptr(self.velr), _ptr(out), _stream()),
+                   "sphb_energy")
+        v = out.cpu().numpy()
+        return dict(ke=float(v[0]), pe=float(v[1]), ie=float(v[2]), rho_fluid=float(v[3]),
+                    rho_mean=float(v[4]))
+
+    # ------------------------------------------------------------------ checkpoints
+    def save_checkpoint(self, path) -> None:
+        from .snapshots import save_checkpoint
+        torch.cuda.current_stream().synchronize()
+        save_checkpoint(path, self)
+
+    @classmethod
+    def from_checkpoint(cls, path, params, reach: int, max_steps: int | None = None,
+                        t_end: float | None = None, **kw) -> "DeviceSim":
+        """Resume: state, Verlet history, step and simulated time from ``path``; the stop
+        rules are the caller's (None keeps the checkpointed ones)."""
+        from types import SimpleNamespace
+
+        from .snapshots import load_checkpoint
+        z = load_checkpoint(path)
+        n, nb = int(z["n"]), int(z["nb"])
+        posp, velr, prev = z["posp"], z["velr"], z["prev"]
+        system = SimpleNamespace(n=n, count_boundary=nb, mass_fluid=float(z["mass_fluid"]),
+                                 mass_boundary=float(z["mass_boundary"]), pos=posp[:, :3],
+                                 vel=velr[:, :3], rho=velr[:, 3], id=z["id"])
+        sim = cls(system, params, reach, vel_prev=prev[:, :3], rho_prev=prev[:, 3], **kw)
+        c = z["ctrl"].copy()
+        view = c[: _lib.CTRL_DTYPE.itemsize].view(_lib.CTRL_DTYPE)
+        if max_steps is not None:
+            view["max_steps"] = -1 if max_steps < 0 else int(max_steps)
+        if t_end is not None:
+            view["t_end"] = float(t_end)
+        sim.ctrl.copy_(torch.as_tensor(c).to(sim.device))
+        return sim
 
     # ------------------------------------------------------------------ readback
     def ctrl_host(self):

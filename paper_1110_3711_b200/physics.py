@@ -17,20 +17,38 @@ PP_NAMES = ("sup2", "h", "invh", "kc", "eta2", "alpha", "invwdp", "c0", "rho0", 
             "mass_fluid", "mass_boundary")
 
 
-def kernel_w(r, h: float):
-    """Cubic spline W(r) with support 2h, 3-D normalisation kc = 1/(pi h^3) (physics.py:25-33)."""
+def kernel_norm(h: float, kernel: str = "cubic") -> float:
+    """3-D normalisation kc: cubic 1/(pi h^3) (physics.py:25-33), Wendland C2 21/(16 pi h^3)."""
+    if kernel == "wendland":
+        return 21.0 / (16.0 * math.pi * h ** 3)
+    return 1.0 / (math.pi * h ** 3)
+
+
+def kernel_w(r, h: float, kernel: str = "cubic"):
+    """W(r) with support 2h: the reference's cubic spline (physics.py:25-33) or the Wendland
+    C2 kernel kc (1 - q/2)^4 (2q + 1) (extension)."""
     q = np.asarray(r, dtype=np.float64) / h
-    kc = 1.0 / (math.pi * h ** 3)
-    w = np.where(q < 1.0, kc * (1.0 - 1.5 * q * q + 0.75 * q ** 3),
-                 np.where(q < 2.0, 0.25 * kc * (2.0 - q) ** 3, 0.0))
+    kc = kernel_norm(h, kernel)
+    if kernel == "wendland":
+        t = np.maximum(1.0 - 0.5 * q, 0.0)
+        w = kc * t ** 4 * (2.0 * q + 1.0)
+    else:
+        w = np.where(q < 1.0, kc * (1.0 - 1.5 * q * q + 0.75 * q ** 3),
+                     np.where(q < 2.0, 0.25 * kc * (2.0 - q) ** 3, 0.0))
     return w if w.ndim else float(w)
 
 
+def kernel_of(params) -> str:
+    return getattr(params, "kernel", "cubic")
+
+
 def pack_params(params, mass_fluid: float, mass_boundary: float) -> np.ndarray:
-    """The 12 f64 constants of the pair loop, in the reference's order."""
+    """The 12 f64 constants of the pair loop, in the reference's order (kc and 1/W(dp) of the
+    selected kernel; the cubic values are the reference's)."""
     sup = params.support_radius
-    return np.array([sup * sup, params.h, 1.0 / params.h, 1.0 / (math.pi * params.h ** 3),
-                     params.eta2, params.alpha, 1.0 / kernel_w(params.dp, params.h), params.c0,
+    k = kernel_of(params)
+    return np.array([sup * sup, params.h, 1.0 / params.h, kernel_norm(params.h, k),
+                     params.eta2, params.alpha, 1.0 / kernel_w(params.dp, params.h, k), params.c0,
                      params.rho0, params.gamma, mass_fluid, mass_boundary], dtype=np.float64)
 
 
@@ -48,6 +66,13 @@ def params_desc(params, mass_fluid: float, mass_boundary: float, order: int = 0,
     d.verlet_stride = int(params.verlet_corrector_stride)
     d.order = int(order)
     d.precision = int(precision)
+    d.kernel = _lib.SPHB_KERNEL_WENDLAND if kernel_of(params) == "wendland" else _lib.SPHB_KERNEL_CUBIC
+    d.integrator = (_lib.SPHB_INT_SYMPLECTIC if getattr(params, "integrator", "verlet") == "symplectic"
+                    else _lib.SPHB_INT_VERLET)
+    pm = getattr(params, "piston", None)
+    if pm is not None:
+        d.piston_id0, d.piston_id1 = int(pm.id0), int(pm.id1)
+        d.piston_x0, d.piston_stroke, d.piston_period = float(pm.x0), float(pm.stroke), float(pm.period)
     return d
 
 

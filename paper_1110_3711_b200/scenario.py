@@ -13,7 +13,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-from .model import ParticleKind, ParticleSystem, SimParams, validate
+from .model import ParticleKind, ParticleSystem, PistonMotion, SimParams, validate
 
 
 @dataclass
@@ -144,6 +144,59 @@ def build_dam_break(scenario: Scenario, params: SimParams) -> ParticleSystem:
     return system.validate()
 
 
+# ---------------------------------------------------------------- wave tank (C5, extension)
+@dataclass
+class WaveTank(Scenario):
+    """Piston-type wavemaker flume (SURVEY.md §8(d) C5 suggestion; no reference counterpart):
+    a full-length water layer in a long tank whose x = tank_min wall (above the floor) is a
+    piston moving as x0 + stroke/2 (1 - cos(2 pi t / period))."""
+
+    tank_size: np.ndarray = field(default_factory=lambda: np.array([2.4, 0.3, 0.5]))
+    fill_size: np.ndarray = field(default_factory=lambda: np.array([2.4, 0.3, 0.3]))
+    dp: float = 0.02
+    stroke: float = 0.1
+    period: float = 1.0
+
+    def __post_init__(self):
+        super().__post_init__()
+        # the water starts one dp in front of the piston and one dp before the far wall
+        self.fill_offset = np.array([0.5 * self.dp, 0.0, 0.0])
+        self.fill_size = np.array([self.tank_size[0] - self.dp, self.fill_size[1], self.fill_size[2]])
+
+
+def piston_mask(scenario: Scenario, bound_pos: np.ndarray) -> np.ndarray:
+    """Boundary particles of the x = tank_min wall above the floor (the piston)."""
+    x0, z0 = float(scenario.tank_min[0]), float(scenario.tank_min[2])
+    return (np.abs(bound_pos[:, 0] - x0) < 0.25 * scenario.dp) & (bound_pos[:, 2] > z0 + 0.5 * scenario.dp)
+
+
+def make_wave_tank_params(scenario: "WaveTank", **kw) -> SimParams:
+    """make_params for the flume plus its PistonMotion (piston particles get ids [0, np))."""
+    bound = _boundary_positions(scenario)
+    npist = int(piston_mask(scenario, bound).sum())
+    pm = PistonMotion(id0=0, id1=npist, x0=float(scenario.tank_min[0]), stroke=float(scenario.stroke),
+                      period=float(scenario.period))
+    return make_params(scenario, piston=pm, **kw)
+
+
+def build_wave_tank(scenario: "WaveTank", params: SimParams) -> ParticleSystem:
+    """Same lattice generator as build_dam_break (hydrostatic rho, one boundary layer), with
+    the piston particles moved to the front of the boundary list so they hold ids
+    [0, params.piston.id1)."""
+    system = build_dam_break(scenario, params)
+    nb = system.count_boundary
+    m = piston_mask(scenario, system.pos[:nb].astype(np.float64))
+    order = np.concatenate([np.nonzero(m)[0], np.nonzero(~m)[0], np.arange(nb, system.n)])
+    system.pos = np.ascontiguousarray(system.pos[order])
+    system.vel = np.ascontiguousarray(system.vel[order])
+    system.rho = np.ascontiguousarray(system.rho[order])
+    system.id = np.arange(system.n, dtype=np.int64)
+    pm = getattr(params, "piston", None)
+    if pm is not None and (pm.id0, pm.id1) != (0, int(m.sum())):
+        raise ValueError("params.piston ids do not match this wave tank (use make_wave_tank_params)")
+    return system.validate()
+
+
 # Named configurations of BASELINE.json / SURVEY.md §8 (C1-C4; C5 is builder-defined).
 FULL_TANK = dict(tank_size=np.array([1.6, 0.67, 0.6]), fill_size=np.array([0.4, 0.67, 0.3]))
 CONFIGS = {
@@ -161,5 +214,13 @@ CONFIGS = {
 }
 
 
+WAVE_CONFIGS = {
+    "c5": dict(dp=0.00175),          # 40,060,170 fluid (2.4 x 0.3 x 0.3 m layer)
+    "c5_small": dict(dp=0.02),       # test size
+}
+
+
 def named_scenario(name: str) -> Scenario:
+    if name in WAVE_CONFIGS:
+        return WaveTank(**WAVE_CONFIGS[name])
     return Scenario(**CONFIGS[name])

@@ -47,8 +47,9 @@ def compute_derived(rho, params) -> DerivedQuantities:
 
 
 class _Timer:
-    def __init__(self, steps):
-        self.ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(steps)]
+    def __init__(self, steps, per_step=4):
+        self.ev = [[torch.cuda.Event(enable_timing=True) for _ in range(per_step)]
+                   for _ in range(steps)]
 
 
 def make_device_sim(system, params, cfg: EngineConfig, max_steps=None, t_end=None, **kw) -> DeviceSim:
@@ -60,13 +61,19 @@ def make_device_sim(system, params, cfg: EngineConfig, max_steps=None, t_end=Non
 
 def run_simulation(scenario_or_system, params, config: EngineConfig, max_steps: int | None = None,
                    t_end: float | None = None, snapshot_every: int = 0, snapshot_sink=None,
-                   stats_sink=None, *, chunk: int = 256, stage_timing: bool = True):
+                   stats_sink=None, *, chunk: int = 256, stage_timing: bool = True,
+                   checkpoint_every: int = 0, checkpoint_path=None, resume_from=None):
     """NL -> PI -> SU loop on the B200.  Returns (system, stats_list) like sim.py:272-352;
     raises DivergenceError on the first out-of-domain particle or non-finite state.
 
     ``chunk`` bounds how many steps run between host readbacks (the record ring is
     sized for it); ``stage_timing`` records CUDA events at the NL/PI/SU boundaries of
-    every step to fill StepStats.stage_*_s and wall_seconds."""
+    every step to fill StepStats.stage_*_s and wall_seconds.
+
+    Extensions: ``checkpoint_every`` > 0 writes a binary checkpoint (snapshots.save_checkpoint;
+    ``checkpoint_path`` may contain ``{step}``) every that many steps; ``resume_from`` continues
+    bit-identically from such a checkpoint (``scenario_or_system`` may then be None; step
+    numbers and the stop rules continue from the checkpoint's step)."""
     if max_steps is None and t_end is None:
         raise ValueError("need max_steps or t_end")
     validate(params)
@@ -74,17 +81,29 @@ def run_simulation(scenario_or_system, params, config: EngineConfig, max_steps: 
     need = cfg.required_n_subdiv()
     if need is not None and params.n_subdiv != need:
         raise ValueError(f"config {cfg.tag} needs n_subdiv={need}")
-    system = build_dam_break(scenario_or_system, params) if isinstance(scenario_or_system, Scenario) \
-        else scenario_or_system
+    if checkpoint_every and checkpoint_path is None:
+        raise ValueError("checkpoint_every needs checkpoint_path")
     chunk = max(1, int(chunk))
     if snapshot_every and snapshot_sink is not None:
         chunk = int(snapshot_every)  # chunk boundaries land on snapshot steps
-    sim = make_device_sim(system, params, cfg, max_steps, t_end, record_capacity=max(chunk, 1))
+    if checkpoint_every:
+        chunk = math.gcd(chunk, int(checkpoint_every))
+    if resume_from is not None:
+        sim = DeviceSim.from_checkpoint(resume_from, params, reach=cfg.device_reach(params.n_subdiv),
+                                        order=cfg.device_order(), precision=PRECISION_CODE[cfg.precision],
+                                        max_steps=-1 if max_steps is None else int(max_steps),
+                                        t_end=math.inf if t_end is None else float(t_end),
+                                        record_capacity=max(chunk, 1))
+        system = scenario_or_system if scenario_or_system is not None else _shell_system(sim)
+    else:
+        system = build_dam_break(scenario_or_system, params) if isinstance(scenario_or_system, Scenario) \
+            else scenario_or_system
+        sim = make_device_sim(system, params, cfg, max_steps, t_end, record_capacity=max(chunk, 1))
     stats_out: list[StepStats] = []
     nbytes = NEIGHBOR_BYTES[cfg.derived_mode]
-    done_steps = 0
+    done_steps = int(sim.ctrl_host()["step"])
     while True:
-        timer = _Timer(chunk) if stage_timing else None
+        timer = _Timer(chunk, sim.n_stage_events()) if stage_timing else None
         for k in range(chunk):
             sim.launch_step(events=timer.ev[k] if timer else None)
         c = sim.ctrl_host()  # synchronises
@@ -97,11 +116,8 @@ def run_simulation(scenario_or_system, params, config: EngineConfig, max_steps: 
                            force_evals=int(r["force_evals"]), ff_force_evals=int(r["ff_force_evals"]),
                            engine_tag=cfg.tag, neighbor_bytes=nbytes)
             if timer is not None:
-                e0, e1, e2, e3 = timer.ev[k]
-                st.stage_nl_s = e0.elapsed_time(e1) * 1e-3
-                st.stage_pi_s = e1.elapsed_time(e2) * 1e-3
-                st.stage_su_s = e2.elapsed_time(e3) * 1e-3
-                st.wall_seconds = e0.elapsed_time(e3) * 1e-3
+                st.stage_nl_s, st.stage_pi_s, st.stage_su_s, st.wall_seconds = \
+                    DeviceSim.stage_seconds(timer.ev[k])
             if stats_sink is not None:
                 stats_sink(st)
             stats_out.append(st)
@@ -110,14 +126,29 @@ def run_simulation(scenario_or_system, params, config: EngineConfig, max_steps: 
                     and step_no == now:
                 snap = _system_from_device(sim, system)
                 snapshot_sink.emit(step_no, snap, compute_derived(snap.rho, params))
-        done_steps = now
         err = sim.error()
         if err is not None:
             raise divergence_from_device(err)
+        if checkpoint_every and now > done_steps and now % int(checkpoint_every) == 0:
+            sim.save_checkpoint(str(checkpoint_path).format(step=now))
+        done_steps = now
         if not int(c["active"]):
             break
     _write_back(sim, system)
     return system, stats_out
+
+
+def _shell_system(sim: DeviceSim):
+    """A ParticleSystem of the right shape for write-back after a resume."""
+    from .model import ParticleSystem
+    n, nb = sim.n, sim.nb
+    z3 = np.zeros((n, 3), np.float32)
+    return ParticleSystem(count_fluid=n - nb, count_boundary=nb, pos=z3, vel=z3.copy(),
+                          rho=np.ones(n, np.float32), mass_fluid=sim.mass_fluid,
+                          mass_boundary=sim.mass_boundary,
+                          ptype=np.concatenate([np.full(nb, ParticleKind.BOUNDARY, np.uint8),
+                                                np.full(n - nb, ParticleKind.FLUID, np.uint8)]),
+                          id=np.arange(n, dtype=np.int64))
 
 
 def _system_from_device(sim: DeviceSim, like):

@@ -14,6 +14,8 @@ Fixture catalogue (every array keeps the reference dtype):
   eos.npz          compute_derived on edge/random densities
   traj_*.npz       run_simulation trajectories (per-step dt/counters + states)
   drift_c1.npz     1000-step C1 energy/mass diagnostics (survey §8(d))
+  io_small.npz     the reference's snapshot CSV text and stats JSON lines of a short run
+                   (bench/snapshots.py write_snapshot / stats_line), for the I/O surface
 """
 from __future__ import annotations
 
@@ -234,6 +236,38 @@ def drift_fixture(steps=1000, every=10):
     print(f"wrote drift_c1.npz ({out['wall_s']:.1f}s)", flush=True)
 
 
+def io_fixture():
+    """Snapshot CSV + stats lines exactly as the reference writes them (3 steps, dp=0.03)."""
+    import tempfile
+
+    from sphbench.bench.snapshots import snapshot_of, stats_line, write_snapshot
+    sc = Scenario(dp=0.03)
+    params = make_params(sc)
+    captured = {}
+
+    class Sink:
+        def emit(self, step, system, derived):
+            with tempfile.NamedTemporaryFile("r", suffix=".csv", delete=False) as fh:
+                path = fh.name
+            write_snapshot(path, snapshot_of(system, derived))
+            captured[step] = open(path).read()
+            os.unlink(path)
+
+    lines = []
+    system, stats = run_simulation(sc, params, gather_cfg("slowcellsh"), max_steps=3,
+                                   snapshot_every=3, snapshot_sink=Sink(),
+                                   stats_sink=lambda st: lines.append(stats_line(st)))
+    s0 = build_dam_break(sc, params)
+    init_csv_path = os.path.join(OUT, "_tmp_init.csv")
+    write_snapshot(init_csv_path, snapshot_of(s0, physics.compute_derived(s0.rho, params)))
+    init_csv = open(init_csv_path).read()
+    os.unlink(init_csv_path)
+    out = dict(csv_step3=np.array(captured[3]), csv_init=np.array(init_csv),
+               stats_lines=np.array(lines), **system_dict(s0, "init_"), **system_dict(system, "final_"),
+               **params_dict(params))
+    np.savez_compressed(os.path.join(OUT, "io_small.npz"), **out)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--skip-long", action="store_true")
@@ -285,6 +319,8 @@ def main():
         trajectory_fixture("c1_g100", sc, params, gather_cfg("slowcellsh"), 100, keep_states=(1, 10))
     if want("drift") and not a.skip_long:
         drift_fixture()
+    if want("io"):
+        io_fixture()
 
 
 if __name__ == "__main__":
