@@ -191,13 +191,14 @@ def run_reference(args, cfg_name):
 
 # ---------------------------------------------------------------- multi-GPU (X slabs)
 def run_slabs(args, cfg_name, system, prm, prec, world, rank, local):
-    """One slab per GPU: migration + halo exchange over NCCL (torch.distributed send/recv),
-    owned-target interaction, dt allreduce(min) on the device control words."""
+    """One X-slab per GPU (dslab.DeviceSlabSim): device classify/scatter of migrants and halo
+    rows, NCCL send/recv of exact byte counts, owned-target interaction, device all-reduces of
+    the dt minima and counters; one host synchronisation per step (the totals all-gather)."""
     import torch
     import torch.distributed as dist
-    from paper_1110_3711_b200 import slab
+    from paper_1110_3711_b200 import dslab
 
-    sim = slab.device_slab_simulation(system, prm, world, comm=slab.DistComm(), precision=prec)
+    sim = dslab.DeviceSlabSim(system, prm, dslab.DevDistComm(), precision=prec)
     me = sim.ranks[0]
     Ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
     for _ in range(args.warmup):
@@ -216,7 +217,7 @@ def run_slabs(args, cfg_name, system, prm, prec, world, rank, local):
     tt = torch.tensor([t0.elapsed_time(t1)], device="cuda")
     dist.all_reduce(tt, op=dist.ReduceOp.MAX)
     total_ms = float(tt.item())
-    # e2e: the same decomposed step with each rank's owned state round-tripped through pinned
+    # e2e: the same decomposed step with each rank's resident rows round-tripped through pinned
     # host buffers every step (the per-step host boundary of the engine API)
     h2d = d2h = 0
     e2e_value = None
@@ -225,13 +226,13 @@ def run_slabs(args, cfg_name, system, prm, prec, world, rank, local):
         a, b = Ev(), Ev()
         a.record()
         for _ in range(args.e2e_steps):
+            n = me.n
             nbytes = 0
-            for li in (0, 1):
-                hs = me.st[li].to("cpu", non_blocking=False).pin_memory()
-                hi = me.ids[li].to("cpu").pin_memory()
-                nbytes += hs.numel() * 4 + hi.numel() * 8
-                me.st[li] = hs.to(me.st[li].device, non_blocking=True)
-                me.ids[li] = hi.to(me.ids[li].device, non_blocking=True)
+            for f in ("posp", "velr", "prev", "id"):
+                t = getattr(me.a, f)[:n]
+                host = t.to("cpu", non_blocking=False).pin_memory()
+                t.copy_(host, non_blocking=True)
+                nbytes += host.numel() * host.element_size()
             h2d = d2h = nbytes
             sim.step()
         b.record()
@@ -239,11 +240,11 @@ def run_slabs(args, cfg_name, system, prm, prec, world, rank, local):
         te = torch.tensor([a.elapsed_time(b)], device="cuda")
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
         e2e_value = system.n * args.e2e_steps / (float(te.item()) * 1e-3)
-    recs = me.stats[args.warmup:args.warmup + args.steps]
-    true_pairs = float(np.mean([r["true_pairs"] for r in recs]))
-    evals = float(np.mean([r["force_evals"] for r in recs]))
+    recs = sim.records(args.warmup, args.warmup + args.steps)
+    true_pairs = float(np.mean(recs["hits_ordered"].astype(np.float64))) / 2
+    evals = float(np.mean(recs["force_evals"].astype(np.float64)))
     value = system.n * args.steps / (total_ms * 1e-3)
-    owned = torch.tensor([me.n_owned], device="cuda", dtype=torch.int64)
+    owned = torch.tensor([sim.n_owned_max], device="cuda", dtype=torch.int64)
     dist.all_reduce(owned, op=dist.ReduceOp.MAX)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -254,19 +255,19 @@ def run_slabs(args, cfg_name, system, prm, prec, world, rank, local):
                                f"GPUs (~{system.n // world:,} per GPU)",
                    "particles": system.n, "n_subdiv": args.n_subdiv,
                    "l2": "inputs larger than L2",
-                   "parallelism": f"{world} X-slabs (NCCL send/recv halos + migration, "
-                                  "allreduce-min dt)",
+                   "parallelism": f"{world} X-slabs (device-resident exchange: NCCL send/recv of "
+                                  "migrants + halo rows, device all-reduce of dt and counters)",
                    "slab_bounds": [int(v) for v in sim.bounds],
                    "max_owned_per_gpu": int(owned.item())},
         "interactions_per_s": true_pairs * args.steps / (total_ms * 1e-3),
         "pair_evals_per_s": evals * args.steps / (total_ms * 1e-3),
-        "gpu_launches": args.steps * 14,
+        "gpu_launches": args.steps * sim.launches_per_step(),
         "clocks": clk,
     }
     if e2e_value is not None:
         line["e2e"] = {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
                        "d2h_bytes_per_step": d2h, "steps": args.e2e_steps,
-                       "path": "per step: each rank's owned state via pinned host buffers, then the decomposed step"}
+                       "path": "per step: each rank's resident rows via pinned host buffers, then the decomposed step"}
     if rank == 0:
         print(json.dumps(line), flush=True)
     dist.destroy_process_group()

@@ -216,6 +216,33 @@ int sphb_integrate_stage(sphb_workspace_t* ws, const sphb_params_t* prm, const s
 int sphb_energy(sphb_workspace_t* ws, const sphb_params_t* prm, int64_t n, int64_t nb,
                 const void* posp, const void* velr, double* out, sphb_stream_t s);
 
+/* ---- X-slab exchange: device-resident migration + halo packing.
+ * Replaces the exchange phases of a slab decomposition of run_simulation's loop (the reference
+ * has no multi-device path; its Slices geometry is engines/kernels.py:230-323).  After the
+ * system update, a rank's primary arrays (owned rows + last step's halo rows with id < 0, sort
+ * keys from sphb_integrate) are classified by cell column against its slab [x0, x1) into 10
+ * categories c = 2 kind + list (kind 0 keep, 1 migrate left, 2 migrate right, 3 halo left,
+ * 4 halo right; list 0 boundary, 1 fluid); halo = kept rows within grid->reach columns of an
+ * edge.  Last step's halo rows are dropped. */
+int64_t sphb_slab_tiles(int64_t n); /* tile_counts holds 10 * sphb_slab_tiles(n) uint32 */
+/* per-tile category counts, their exclusive scan (in place) and the 10 totals (device). */
+int sphb_slab_count(const sphb_grid_t* grid, int64_t n, int64_t nb, const uint32_t* keys,
+                    const int64_t* id, int32_t x0, int32_t x1, uint32_t* tile_counts,
+                    uint32_t* totals, sphb_stream_t s);
+/* kept rows -> next arrays at keep_bases[list] + rank; migrants / halo copies (id' = -1 - id)
+ * -> packed 64-B rows (float4 posp, velr, prev, int64 id, pad) in send_l / send_r with sections
+ * [mig B | mig F | halo B | halo F]; sections = {l_migF, l_haloB, l_haloF, r_migF, r_haloB,
+ * r_haloF} start rows.  keep_bases and sections are host arrays. */
+int sphb_slab_scatter(const sphb_grid_t* grid, int64_t n, int64_t nb, const uint32_t* keys,
+                      const int64_t* id, int32_t x0, int32_t x1, const uint32_t* tile_offsets,
+                      const void* posp, const void* velr, const void* prev,
+                      const int64_t* keep_bases, void* nposp, void* nvelr, void* nprev,
+                      int64_t* nid, void* send_l, void* send_r, const int64_t* sections,
+                      sphb_stream_t s);
+/* rows [r0, r0 + cnt) of a received packed buffer -> next arrays rows [dst, dst + cnt). */
+int sphb_slab_unpack(const void* buf, int64_t r0, int64_t cnt, int64_t dst, void* nposp,
+                     void* nvelr, void* nprev, int64_t* nid, sphb_stream_t s);
+
 /* Closes the step: dt/counters into rec[step % rec_capacity], t_sim += dt, step += 1. */
 int sphb_step_end(sphb_ctrl_t* ctrl, const sphb_params_t* prm, sphb_step_record_t* rec,
                   int64_t rec_capacity, sphb_stream_t s);

@@ -105,6 +105,11 @@ def lib():
         "sphb_integrate_stage": ([P, P, P, c_i64, c_i64, c_i32, P, P, P, P, P, P, P, P, P, P, P, P,
                                   P], c_i32),
         "sphb_energy": ([P, P, c_i64, c_i64, P, P, P, P], c_i32),
+        "sphb_slab_tiles": ([c_i64], c_i64),
+        "sphb_slab_count": ([P, c_i64, c_i64, P, P, c_i32, c_i32, P, P, P], c_i32),
+        "sphb_slab_scatter": ([P, c_i64, c_i64, P, P, c_i32, c_i32, P, P, P, P, P, P, P, P, P, P,
+                               P, P, P], c_i32),
+        "sphb_slab_unpack": ([P, c_i64, c_i64, c_i64, P, P, P, P, P], c_i32),
         "sphb_step": ([P, P, P, c_i64, c_i64, P, P, P, c_i64, P], c_i32),
         "sphb_step_launch_count": ([P, c_i64], c_i64),
     }
@@ -120,7 +125,8 @@ EXPORTED = ("sphb_last_error", "sphb_version", "sphb_workspace_create", "sphb_wo
             "sphb_workspace_reset", "sphb_workspace_bytes", "sphb_ctrl_init", "sphb_cell_keys",
             "sphb_sort", "sphb_reorder", "sphb_cell_ranges", "sphb_cell_ranges_from_sorted",
             "sphb_interact", "sphb_step_begin", "sphb_integrate", "sphb_step_end", "sphb_step",
-            "sphb_step_launch_count", "sphb_integrate_stage", "sphb_energy")
+            "sphb_step_launch_count", "sphb_integrate_stage", "sphb_energy", "sphb_slab_tiles",
+            "sphb_slab_count", "sphb_slab_scatter", "sphb_slab_unpack")
 
 
 def check(rc: int, what: str = "") -> None:

@@ -352,6 +352,56 @@ int sphb_step(sphb_workspace_t* ws, const sphb_params_t* prm, const sphb_grid_t*
   return launch_step_end(ctrl, *prm, rec, rec_capacity, cs);
 }
 
+int64_t sphb_slab_tiles(int64_t n) { return n > 0 ? slab_tiles(n) : 0; }
+
+int sphb_slab_count(const sphb_grid_t* grid, int64_t n, int64_t nb, const uint32_t* keys,
+                    const int64_t* id, int32_t x0, int32_t x1, uint32_t* tile_counts,
+                    uint32_t* totals, sphb_stream_t s) {
+  if (int rc = check_grid(grid)) return rc;
+  SPHB_NONNULL(totals);
+  if (n < 0 || nb < 0 || nb > n) return sphb_set_error(SPHB_E_INVALID, "bad n/nb");
+  if (x0 < 0 || x1 > grid->dims[0] || x0 >= x1)
+    return sphb_set_error(SPHB_E_INVALID, "slab columns [x0, x1) must lie in [0, dims[0])");
+  if (n > 0) {
+    SPHB_NONNULL(keys); SPHB_NONNULL(id); SPHB_NONNULL(tile_counts);
+  }
+  return launch_slab_count(*grid, n, nb, keys, id, x0, x1, tile_counts, totals, (cudaStream_t)s);
+}
+
+int sphb_slab_scatter(const sphb_grid_t* grid, int64_t n, int64_t nb, const uint32_t* keys,
+                      const int64_t* id, int32_t x0, int32_t x1, const uint32_t* tile_offsets,
+                      const void* posp, const void* velr, const void* prev,
+                      const int64_t* keep_bases, void* nposp, void* nvelr, void* nprev,
+                      int64_t* nid, void* send_l, void* send_r, const int64_t* sections,
+                      sphb_stream_t s) {
+  if (int rc = check_grid(grid)) return rc;
+  SPHB_NONNULL(keep_bases);
+  SPHB_NONNULL(sections);
+  if (n < 0 || nb < 0 || nb > n) return sphb_set_error(SPHB_E_INVALID, "bad n/nb");
+  if (x0 < 0 || x1 > grid->dims[0] || x0 >= x1)
+    return sphb_set_error(SPHB_E_INVALID, "slab columns [x0, x1) must lie in [0, dims[0])");
+  if (n > 0) {
+    SPHB_NONNULL(keys); SPHB_NONNULL(id); SPHB_NONNULL(tile_offsets); SPHB_NONNULL(posp);
+    SPHB_NONNULL(velr); SPHB_NONNULL(prev); SPHB_NONNULL(nposp); SPHB_NONNULL(nvelr);
+    SPHB_NONNULL(nprev); SPHB_NONNULL(nid);
+  }
+  return launch_slab_scatter(*grid, n, nb, keys, id, x0, x1, tile_offsets, (const float4*)posp,
+                             (const float4*)velr, (const float4*)prev, keep_bases, (float4*)nposp,
+                             (float4*)nvelr, (float4*)nprev, nid, send_l, send_r, sections,
+                             (cudaStream_t)s);
+}
+
+int sphb_slab_unpack(const void* buf, int64_t r0, int64_t cnt, int64_t dst, void* nposp,
+                     void* nvelr, void* nprev, int64_t* nid, sphb_stream_t s) {
+  if (cnt < 0 || r0 < 0 || dst < 0) return sphb_set_error(SPHB_E_INVALID, "bad unpack range");
+  if (cnt > 0) {
+    SPHB_NONNULL(buf); SPHB_NONNULL(nposp); SPHB_NONNULL(nvelr); SPHB_NONNULL(nprev);
+    SPHB_NONNULL(nid);
+  }
+  return launch_slab_unpack(buf, r0, cnt, dst, (float4*)nposp, (float4*)nvelr, (float4*)nprev, nid,
+                            (cudaStream_t)s);
+}
+
 int64_t sphb_step_launch_count(const sphb_grid_t* grid, int64_t n) {
   if (!grid) return 0;
   return 1 /*begin*/ + nl_launch_count(*grid, n) + interact_launch_count(n) + 1 /*integrate*/ +

@@ -69,6 +69,19 @@ int launch_integrate_mode(sphb_workspace* ws, const sphb_params_t& p, const sphb
                           cudaStream_t s);
 int launch_energy(sphb_workspace* ws, const sphb_params_t& p, int64_t n, int64_t nb,
                   const float4* posp, const float4* velr, double* out, cudaStream_t s);
+// slab.cu
+int64_t slab_tiles(int64_t n);
+int launch_slab_count(const sphb_grid_t& g, int64_t n, int64_t nb, const uint32_t* keys,
+                      const int64_t* id, int x0, int x1, uint32_t* tile_counts, uint32_t* totals,
+                      cudaStream_t s);
+int launch_slab_scatter(const sphb_grid_t& g, int64_t n, int64_t nb, const uint32_t* keys,
+                        const int64_t* id, int x0, int x1, const uint32_t* tile_offsets,
+                        const float4* posp, const float4* velr, const float4* prev,
+                        const int64_t* keep_bases, float4* nposp, float4* nvelr, float4* nprev,
+                        int64_t* nid, void* send_l, void* send_r, const int64_t* sections,
+                        cudaStream_t s);
+int launch_slab_unpack(const void* buf, int64_t r0, int64_t cnt, int64_t dst, float4* nposp,
+                       float4* nvelr, float4* nprev, int64_t* nid, cudaStream_t s);
 int launch_step_end(sphb_ctrl_t* ctrl, const sphb_params_t& p, sphb_step_record_t* rec, int64_t cap,
                     cudaStream_t s);
 int launch_ctrl_init(sphb_ctrl_t* ctrl, int64_t max_steps, double t_end, cudaStream_t s);

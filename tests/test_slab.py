@@ -132,3 +132,33 @@ def test_gloo_two_ranks_match_single_domain(tmp_path):
     assert stats[0]["true_pairs"] == int(ref[4][0]["counters"][1])
     assert [s["dt"] for s in stats] == pytest.approx([s["dt"] for s in ref[4]], rel=1e-9)
     _compare(host, ref, 1e-9)
+
+
+def test_device_slab_layout_host_logic():
+    """dslab.rank_layout (the host half of the device-resident exchange): next-step layout,
+    send sections and unpack destinations from every rank's 10 category totals."""
+    from paper_1110_3711_b200 import dslab
+    # rank totals: keepB keepF migLB migLF migRB migRF haloLB haloLF haloRB haloRF
+    tab = np.array([[5, 50, 0, 0, 1, 2, 0, 0, 3, 7],
+                    [6, 60, 2, 1, 0, 3, 4, 9, 1, 8],
+                    [4, 40, 1, 4, 0, 0, 2, 6, 0, 0]], np.int64)
+    lay = dslab.rank_layout(tab, 1, 3)
+    in_l = [1, 2, 3, 7]   # rank 0's right sends: migB, migF, haloB, haloF
+    in_r = [1, 4, 2, 6]   # rank 2's left sends
+    assert lay["nb_next"] == 6 + in_l[0] + in_r[0] + in_l[2] + in_r[2]
+    assert lay["n_next"] == lay["nb_next"] + 60 + in_l[1] + in_r[1] + in_l[3] + in_r[3]
+    assert lay["keep_bases"] == (0, lay["nb_next"])
+    assert lay["send_rows"] == (2 + 1 + 4 + 9, 0 + 3 + 1 + 8)
+    assert lay["recv_rows"] == (sum(in_l), sum(in_r))
+    assert lay["sections"] == [2, 3, 7, 0, 3, 4]
+    # unpack destinations tile [0, n_next) exactly once with the kept blocks
+    cover = np.zeros(lay["n_next"], int)
+    cover[0:6] += 1
+    cover[lay["nb_next"]:lay["nb_next"] + 60] += 1
+    for side in lay["unpack"]:
+        for r0, cnt, dst in side:
+            cover[dst:dst + cnt] += 1
+    assert np.all(cover == 1)
+    # edge ranks have no outside neighbours
+    lay0 = dslab.rank_layout(tab, 0, 3)
+    assert lay0["recv_rows"][0] == 0 and lay0["unpack"][0] == [(0, 0, d) for _, _, d in lay0["unpack"][0]]
