@@ -941,7 +941,9 @@ __device__ __forceinline__ void eval_v8(const KArgs& a, const K32& c, const Own3
                                         Acc32 (&s)[NG]) {
   constexpr uint32_t OFFB = 16u * V8_ROWS;  // A -> B rows
   Geo2 g[NG];
-  bool ok[2 * NG];
+  // the sure-hit mask and the clamped r2 live in float registers across the (rare) exact
+  // branch, so the hot path carries no predicate / byte juggling
+  float okf[2 * NG], r2m[2 * NG];
   bool anycold = false;
 #pragma unroll
   for (int k = 0; k < NG; ++k) {
@@ -961,43 +963,53 @@ __device__ __forceinline__ void eval_v8(const KArgs& a, const K32& c, const Own3
     g[k].dot = fma2(dvz, g[k].dz, pk(lo(dd1) + hi(dd1), lo(dd2) + hi(dd2)));
     // sure hit: r2 < sup2_lo (an empty slot reads the dummy row, r2 ~ 1e8 sup2: never a hit);
     // cold (exact f64 re-decision): r2 in [sup2_lo, sup2_hi) or r2 <= tiny, tested as
-    // unsigned ranges of the (non-negative) float bits
+    // unsigned ranges of the (non-negative) float bits; a cold slot is not a sure hit
     const float r21 = lo(g[k].r2), r22 = hi(g[k].r2);
-    ok[2 * k] = r21 < c.sup2_lo;
-    ok[2 * k + 1] = r22 < c.sup2_lo;
-    anycold |= in_cold(r21, c) | in_cold(r22, c);
+    const bool c1 = in_cold(r21, c), c2 = in_cold(r22, c);
+    const bool s1 = (r21 < c.sup2_lo) & !c1, s2 = (r22 < c.sup2_lo) & !c2;
+    okf[2 * k] = s1 ? 1.0f : 0.0f;
+    okf[2 * k + 1] = s2 ? 1.0f : 0.0f;
+    r2m[2 * k] = s1 ? r21 : c.sup2_lo;
+    r2m[2 * k + 1] = s2 ? r22 : c.sup2_lo;
+    anycold |= c1 | c2;
   }
   if (__any_sync(SPHB_FULL, anycold)) {
     // guard band / coincident (lattice ties sit on the cutoff): exact f64 decision, one
     // candidate per lane per round so the f64 path is issued once, not once per slot
-    uint32_t cm = 0, okm = 0;
+    uint32_t cm = 0;
 #pragma unroll
     for (int k = 0; k < NG; ++k) {
       cm |= (in_cold(lo(g[k].r2), c) ? 1u : 0u) << (2 * k);
       cm |= (in_cold(hi(g[k].r2), c) ? 1u : 0u) << (2 * k + 1);
     }
-#pragma unroll
-    for (int k = 0; k < 2 * NG; ++k) okm |= (ok[k] ? 1u : 0u) << k;
-    okm &= ~cm;
     do {
       const int k = __ffs(cm) - 1;
       uint32_t adk = ad[0];
 #pragma unroll
       for (int kk = 1; kk < 2 * NG; ++kk) adk = k == kk ? ad[kk] : adk;
+      bool acc = false;
       if (cm) {
         const float4 A = lds4(adk);
-        if (cold_accept(a, o.x, o.y, o.z, A, xlo, xhi)) okm |= 1u << k;
+        acc = cold_accept(a, o.x, o.y, o.z, A, xlo, xhi);
         cm &= cm - 1u;
       }
-    } while (__any_sync(SPHB_FULL, cm != 0u));
 #pragma unroll
-    for (int k = 0; k < 2 * NG; ++k) ok[k] = (okm >> k) & 1u;
+      for (int kk = 0; kk < NG; ++kk) {
+        if (acc && k == 2 * kk) {
+          okf[2 * kk] = 1.0f;
+          r2m[2 * kk] = lo(g[kk].r2);
+        }
+        if (acc && k == 2 * kk + 1) {
+          okf[2 * kk + 1] = 1.0f;
+          r2m[2 * kk + 1] = hi(g[kk].r2);
+        }
+      }
+    } while (__any_sync(SPHB_FULL, cm != 0u));
   }
 #pragma unroll
   for (int k = 0; k < NG; ++k) {
-    const bool ok1 = ok[2 * k], ok2 = ok[2 * k + 1];
-    const f2_t OK = pk(ok1 ? 1.0f : 0.0f, ok2 ? 1.0f : 0.0f);
-    const f2_t R2M = pk(ok1 ? lo(g[k].r2) : c.sup2_lo, ok2 ? hi(g[k].r2) : c.sup2_lo);
+    const f2_t OK = pk(okf[2 * k], okf[2 * k + 1]);
+    const f2_t R2M = pk(r2m[2 * k], r2m[2 * k + 1]);
     const f2_t RINV = pk(rsqrtf(lo(R2M)), rsqrtf(hi(R2M)));
     const f2_t Q = mul2(mul2(R2M, RINV), bc(c.invh));
     f2_t W, DWR;  // kernel shape W/kc and the gradient shape (-gc / mask factor)
