@@ -18,10 +18,11 @@
  *     when it chooses to (no per-step host sync).
  *
  * Particle state layout in HBM (structure of float4 arrays, one 16-B load per field):
- *   posp  float4 (x, y, z, press)        press = Tait EOS of rho, f32-rounded (physics.py:119-121)
+ *   posp  float4 (x, y, z, w)            w = 0 in the primary arrays; the sorted copy (K3) carries
+ *                                        prrho = press / rho^2 (physics.py:124-134)
  *   velr  float4 (vx, vy, vz, rho)
  *   prev  float4 (vx_prev, vy_prev, vz_prev, rho_prev)   Verlet history (sim.py:31-43)
- *   aux   float4 (prrho, csound, tensil, mass)            derived (physics.py:124-134) + list mass
+ *   aux   float4 (press, csound, tensil, mass)            derived (physics.py:119-134) + list mass
  *   id    int64
  * Boundary particles occupy [0, nb), fluid [nb, n) (model.py:24-32).
  */
@@ -150,7 +151,8 @@ int sphb_sort(sphb_workspace_t* ws, const sphb_grid_t* grid, const uint32_t* key
               sphb_stream_t s);
 
 /* K3 -- reorder gathers (grid.py:111-114) fused with compute_derived (physics.py:96-110):
- * *_out[i] = *_in[perm[i]] for posp, velr, prev, id; posp_out.w = press; aux_out derived;
+ * *_out[i] = *_in[perm[i]] for posp, velr, prev, id; posp_out.w = prrho; aux_out = (press,
+ * csound, tensil, list mass);
  * cell_out[i] = cell of the sorted key.  prev_in/prev_out/id may be NULL. */
 int sphb_reorder(const sphb_params_t* prm, const sphb_grid_t* grid, int64_t n,
                  const int32_t* perm, const uint32_t* keys_sorted, const void* posp_in,

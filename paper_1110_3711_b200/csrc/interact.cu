@@ -553,7 +553,7 @@ __global__ void __launch_bounds__(NW * 32, 2) k_interact(KArgs a) {
       const float4 pi = a.posp[i], vi = a.velr[i], xi = a.aux[i];
       o.x = (R)pi.x; o.y = (R)pi.y; o.z = (R)pi.z;
       o.vx = (R)vi.x; o.vy = (R)vi.y; o.vz = (R)vi.z; o.rho = (R)vi.w;
-      o.prrho = (R)xi.x; o.cs = (R)xi.y; o.ten = (R)xi.z;
+      o.prrho = (R)pi.w; o.cs = (R)xi.y; o.ten = (R)xi.z;
       const int cxi = a.cell[i] - rowkey * nx;
       xlo = max(cxi - reach, 0);
       xhi = min(cxi + reach, nx - 1);
@@ -626,7 +626,7 @@ __global__ void __launch_bounds__(NW * 32, 2) k_interact(KArgs a) {
           const float4 vr = __ldg(&a.velr[j]);
           const float4 xa = __ldg(&a.aux[j]);
           const bool boundary_list = sg.rowoff < a.ncells;
-          g_sm4[p - q0] = make_float4(pp.x, pp.y, pp.z, xa.x);
+          g_sm4[p - q0] = pp;  // (x, y, z, prrho)
           g_sm4[SB + p - q0] = make_float4(vr.x, vr.y, vr.z, boundary_list ? -vr.w : vr.w);
           if (sizeof(R) == 8) g_sm4[SC + p - q0] = make_float4(xa.y, xa.z, 0.f, 0.f);
           if (Cfg<R>::H16) {
@@ -948,10 +948,12 @@ __device__ __forceinline__ void eval_v8(const KArgs& a, const K32& c, const Own3
 #pragma unroll
   for (int k = 0; k < NG; ++k) {
     f2_t b1xy, b2xy;
-    lds_2x64(ad[2 * k], g[k].a1xy, g[k].a1zw);
-    lds_2x64(ad[2 * k + 1], g[k].a2xy, g[k].a2zw);
-    lds_2x64(ad[2 * k] + OFFB, b1xy, g[k].b1zw);
-    lds_2x64(ad[2 * k + 1] + OFFB, b2xy, g[k].b2zw);
+    // non-EQM: bit 0 of a popped address flags a boundary-list candidate (its mass)
+    const uint32_t p1 = EQM ? ad[2 * k] : (ad[2 * k] & ~1u), p2 = EQM ? ad[2 * k + 1] : (ad[2 * k + 1] & ~1u);
+    lds_2x64(p1, g[k].a1xy, g[k].a1zw);
+    lds_2x64(p2, g[k].a2xy, g[k].a2zw);
+    lds_2x64(p1 + OFFB, b1xy, g[k].b1zw);
+    lds_2x64(p2 + OFFB, b2xy, g[k].b2zw);
     g[k].dxy1 = sub2(o.xy, g[k].a1xy);
     g[k].dxy2 = sub2(o.xy, g[k].a2xy);
     const f2_t dvxy1 = sub2(o.vxy, b1xy), dvxy2 = sub2(o.vxy, b2xy);
@@ -989,7 +991,7 @@ __device__ __forceinline__ void eval_v8(const KArgs& a, const K32& c, const Own3
       for (int kk = 1; kk < 2 * NG; ++kk) adk = k == kk ? ad[kk] : adk;
       bool acc = false;
       if (cm) {
-        const float4 A = lds4(adk);
+        const float4 A = lds4(adk & ~1u);
         acc = cold_accept(a, o.x, o.y, o.z, A, xlo, xhi);
         cm &= cm - 1u;
       }
@@ -1034,7 +1036,7 @@ __device__ __forceinline__ void eval_v8(const KArgs& a, const K32& c, const Own3
     if (EQM) {
       MJ = mul2(OK, bc(c.nkgc));
     } else {
-      MJ = mul2(OK, pk(sr1 < 0.0f ? c.nkgc_b : c.nkgc, sr2 < 0.0f ? c.nkgc_b : c.nkgc));
+      MJ = mul2(OK, pk((ad[2 * k] & 1u) ? c.nkgc_b : c.nkgc, (ad[2 * k + 1] & 1u) ? c.nkgc_b : c.nkgc));
     }
     const f2_t GCN = mul2(DWR, MJ);  // -gc [m_j], zero when masked
     f2_t CSJ;                                    // -alpha h cs_j
@@ -1079,10 +1081,15 @@ __global__ void __launch_bounds__(NW * 32, 2) k_interact_v8(KArgs a, K32 k32) {
   const uint32_t nblocks = a.ctrl->nblk[0];
   const int64_t step = a.ctrl->step;
   // the dummy row popped by empty FIFO slots: far away (r2 ~ 1e8 sup2), at rest, finite
+  __shared__ __align__(8) unsigned long long s_mbar;
+  const uint32_t mbar = smem_addr(&s_mbar);
+  uint32_t mphase = 0;
   if (tid == 0) {
     const float far = (float)(1e4 * 2.0 * a.p.h);
     g_sm4[SCAP] = make_float4(far, far, far, 0.f);
     g_sm4[V8_ROWS + SCAP] = make_float4(0.f, 0.f, 0.f, 1.f);
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mbar) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
 
   const uint32_t smA = pin_u32(smem_addr(g_sm4));
@@ -1229,7 +1236,7 @@ __global__ void __launch_bounds__(NW * 32, 2) k_interact_v8(KArgs a, K32 k32) {
       o.x = pi.x; o.y = pi.y; o.z = pi.z; o.vz = vi.z; o.rho = vi.w;
       o.xy = pk(pi.x, pi.y);
       o.vxy = pk(vi.x, vi.y);
-      o.prrho = xi.x;
+      o.prrho = pi.w;
       ocs = xi.y;
       o.csn = (float)(-a.p.alpha * a.p.h) * xi.y;
       o.tenk = xi.z * k32.ktw4;
@@ -1332,49 +1339,52 @@ __global__ void __launch_bounds__(NW * 32, 2) k_interact_v8(KArgs a, K32 k32) {
 
     for (int q0 = 0; q0 < total; q0 += SCAP) {
       const int q1 = min(q0 + SCAP, total);
+      // ---- stage rows [q0, q1): one TMA bulk copy per (stencil row, array) -- the sorted
+      // posp rows are (x, y, z, prrho), velr rows (vx, vy, vz, rho) -- then the 8-B screen
+      // records from shared memory
+      if (tid == 0) {
+        uint32_t bytes = 0;
+        for (int k = 0; k < nseg; ++k) {
+          const Seg sg = sSeg[k];
+          const int lo_p = max(sg.pos, q0), hi_p = min(sg.pos + (sg.g1 - sg.g0), q1);
+          if (hi_p > lo_p) bytes += 32u * (uint32_t)(hi_p - lo_p);
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mbar), "r"(bytes)
+                     : "memory");
+        for (int k = 0; k < nseg; ++k) {
+          const Seg sg = sSeg[k];
+          const int lo_p = max(sg.pos, q0), hi_p = min(sg.pos + (sg.g1 - sg.g0), q1);
+          if (hi_p <= lo_p) continue;
+          const int j0 = sg.g0 + (lo_p - sg.pos);
+          const uint32_t nbytes = 16u * (uint32_t)(hi_p - lo_p);
+          const uint32_t dA = smA + 16u * (uint32_t)(lo_p - q0), dB = dA + 16u * V8_ROWS;
+          asm volatile(
+              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+              ::"r"(dA), "l"(a.posp + j0), "r"(nbytes), "r"(mbar) : "memory");
+          asm volatile(
+              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+              ::"r"(dB), "l"(a.velr + j0), "r"(nbytes), "r"(mbar) : "memory");
+        }
+      }
+      {  // wait for the bytes (phase parity flips per batch)
+        uint32_t done = 0;
+        while (!done)
+          asm volatile(
+              "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+              : "=r"(done) : "r"(mbar), "r"(mphase) : "memory");
+        mphase ^= 1u;
+      }
       {
-        // STG rows in flight per thread: all loads of a chunk are issued before its stores
-        constexpr int U = 4;
-        int sk = 0;
         uint2* rec = reinterpret_cast<uint2*>(reinterpret_cast<char*>(g_sm4) + V8_REC_OFF);
-        for (int p0 = q0 + tid; p0 < q1; p0 += U * NW * 32) {
-          int jj[U];
-          bool bl[U];
-#pragma unroll
-          for (int u = 0; u < U; ++u) {
-            const int p = p0 + u * NW * 32;
-            jj[u] = -1;
-            bl[u] = false;
-            if (p < q1) {
-              while (sSeg[sk].pos + (sSeg[sk].g1 - sSeg[sk].g0) <= p) ++sk;
-              jj[u] = sSeg[sk].g0 + (p - sSeg[sk].pos);
-              bl[u] = sSeg[sk].rowoff < a.ncells;
-            }
-          }
-          float4 pp[U], vr[U];
-          float xa[U];
-#pragma unroll
-          for (int u = 0; u < U; ++u) {
-            if (jj[u] >= 0) {
-              pp[u] = __ldg(&a.posp[jj[u]]);
-              vr[u] = __ldg(&a.velr[jj[u]]);
-              xa[u] = __ldg(&a.aux[jj[u]].x);
-            }
-          }
-#pragma unroll
-          for (int u = 0; u < U; ++u) {
-            const int r = p0 + u * NW * 32 - q0;
-            if (jj[u] >= 0) {
-              g_sm4[r] = make_float4(pp[u].x, pp[u].y, pp[u].z, xa[u]);
-              g_sm4[V8_ROWS + r] = make_float4(vr[u].x, vr[u].y, vr[u].z, bl[u] ? -vr[u].w : vr[u].w);
-              const __half hx = __float2half_rn((pp[u].x - h16_xc) * h16_s);
-              const __half hy = __float2half_rn((pp[u].y - h16_yc) * h16_s);
-              const __half hz = __float2half_rn((pp[u].z - h16_zc) * h16_s);
-              const float fx = __half2float(hx), fy = __half2float(hy), fz = __half2float(hz);
-              rec[r] = make_uint2(h2u(__halves2half2(hx, hy)),
-                                  h2u(__halves2half2(hz, __float2half_rn(fmaf(fz, fz, fmaf(fy, fy, fx * fx))))));
-            }
-          }
+        for (int r = tid; r < q1 - q0; r += NW * 32) {
+          const float4 pp = lds4(smA + 16u * r);
+          const __half hx = __float2half_rn((pp.x - h16_xc) * h16_s);
+          const __half hy = __float2half_rn((pp.y - h16_yc) * h16_s);
+          const __half hz = __float2half_rn((pp.z - h16_zc) * h16_s);
+          const float fx = __half2float(hx), fy = __half2float(hy), fz = __half2float(hz);
+          rec[r] = make_uint2(h2u(__halves2half2(hx, hy)),
+                              h2u(__halves2half2(hz, __float2half_rn(fmaf(fz, fz, fmaf(fy, fy, fx * fx))))));
         }
       }
       __syncthreads();
@@ -1457,7 +1467,7 @@ __global__ void __launch_bounds__(NW * 32, 2) k_interact_v8(KArgs a, K32 k32) {
             }
             if (__any_sync(SPHB_FULL, bits != 0u && cnt == (uint32_t)RINGC)) drain(false);
             if (bits) {
-              sts64u(tp, bits, smA + 16u * (uint32_t)k0);
+              sts64u(tp, bits, smA + 16u * (uint32_t)k0 + ((!EQM && boundary_list) ? 1u : 0u));
               tp = tp + 256u == rend ? ring : tp + 256u;
               ++cnt;
               pend += __popc(bits);

@@ -217,12 +217,12 @@ __global__ void __launch_bounds__(256) k_reorder(
     double rho = (double)vr.w;
     float press = eos_press(rho, p.tait_b, p.rho0, p.gamma);
     Derived d = derive((double)press, rho, p.c0, p.rho0, p.gamma);
-    pp.w = press;
+    // posp.w = prrho: the interaction stages (x, y, z, prrho) rows with one bulk copy
+    pp.w = d.prrho;
     posp_out[i] = pp;
     velr_out[i] = vr;
-    // aux.w carries the list mass so the FP32 pair loop needs no index compare
     const bool boundary = keys_sorted ? ((keys_sorted[i] >> cellbits) & 1u) == 0u : false;
-    aux_out[i] = make_float4(d.prrho, d.csound, d.tensil,
+    aux_out[i] = make_float4(press, d.csound, d.tensil,
                              (float)(boundary ? p.mass_boundary : p.mass_fluid));
     if (prev_in && prev_out) prev_out[i] = prev_in[o];
     if (id_in && id_out) id_out[i] = id_in[o];

@@ -351,8 +351,8 @@ def compute_derived_device(rho: np.ndarray, params):
                                        None, _ptr(aux), None, _ptr(ctrl), _stream()),
                "sphb_reorder")
     a = aux[:n].cpu().numpy()
-    press = posp_o[:n, 3].cpu().numpy()
-    return press, np.ascontiguousarray(a[:, 1]), np.ascontiguousarray(a[:, 0]), np.ascontiguousarray(a[:, 2])
+    prrho = posp_o[:n, 3].cpu().numpy()
+    return np.ascontiguousarray(a[:, 0]), np.ascontiguousarray(a[:, 1]), prrho, np.ascontiguousarray(a[:, 2])
 
 
 def nl_frame(pos: np.ndarray, nb: int, params, reach: int | None = None):

@@ -76,13 +76,14 @@ class B200Engine:
                           PRECISION_CODE[cfg.precision])
         b = self._buffers(n, ncells)
         if n:
-            # pack the caller's frame: posp = (pos, press), velr = (vel, rho), aux = derived
+            # pack the caller's frame as K3 lays it out: posp = (pos, prrho), velr = (vel, rho),
+            # aux = (press, csound, tensil, list mass)
             h = b["host"]
             h[0, :n, :3] = torch.from_numpy(np.ascontiguousarray(system.pos, np.float32))
-            h[0, :n, 3] = torch.from_numpy(np.ascontiguousarray(derived.press, np.float32))
+            h[0, :n, 3] = torch.from_numpy(np.ascontiguousarray(derived.prrho, np.float32))
             h[1, :n, :3] = torch.from_numpy(np.ascontiguousarray(system.vel, np.float32))
             h[1, :n, 3] = torch.from_numpy(np.ascontiguousarray(system.rho, np.float32))
-            h[2, :n, 0] = torch.from_numpy(np.ascontiguousarray(derived.prrho, np.float32))
+            h[2, :n, 0] = torch.from_numpy(np.ascontiguousarray(derived.press, np.float32))
             h[2, :n, 1] = torch.from_numpy(np.ascontiguousarray(derived.csound, np.float32))
             h[2, :n, 2] = torch.from_numpy(np.ascontiguousarray(derived.tensil, np.float32))
             h[2, :nb, 3] = float(np.float32(system.mass_boundary))
