@@ -37,7 +37,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--config", default=None, help="c1|c2|c3|c4_1..c4_8 (default c3 at N=1, c4_N above)")
+    ap.add_argument("--config", default=None,
+                    help="c1|c2|c3|c4_1..c4_8|c5 (default c3 at N=1, c3w_N above)")
     ap.add_argument("--n-subdiv", type=int, default=1)
     ap.add_argument("--precision", default="fp32", choices=["fp32", "fp64"])
     ap.add_argument("--e2e-steps", type=int, default=3)
@@ -70,9 +71,17 @@ def traffic_for(cfg_name):
         return None, None
 
 
+def scenario_kind(sc) -> str:
+    import paper_1110_3711_b200 as sph
+    return "3-D piston wave tank" if isinstance(sc, sph.WaveTank) else "3-D dam break"
+
+
 def workload(name, n_subdiv):
     import paper_1110_3711_b200 as sph
     sc = sph.named_scenario(name)
+    if isinstance(sc, sph.WaveTank):  # C5: piston wavemaker flume
+        prm = sph.make_wave_tank_params(sc, n_subdiv=n_subdiv)
+        return sc, prm, sph.build_wave_tank(sc, prm)
     prm = sph.make_params(sc, n_subdiv=n_subdiv)
     return sc, prm, sph.build_dam_break(sc, prm)
 
@@ -386,7 +395,7 @@ def main():
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
         "scaling": "weak" if world > 1 else "weak", "vs_baseline": None, "dtype": args.precision,
         "data": "synthetic: reference dam-break lattice (Scenario/build_dam_break), hydrostatic rho",
-        "config": {"workload": f"{cfg_name}: 3-D dam break, {system.n:,} particles per GPU "
+        "config": {"workload": f"{cfg_name}: {scenario_kind(sc)}, {system.n:,} particles per GPU "
                                f"({system.count_fluid:,} fluid + {system.count_boundary:,} boundary)",
                    "particles_per_gpu": system.n, "n_subdiv": args.n_subdiv, "variant": variant,
                    "l2": "inputs larger than L2 (resident state ~%.1f GB)" % (sim.n * 184 / 1e9),
