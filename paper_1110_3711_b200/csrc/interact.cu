@@ -931,6 +931,12 @@ __device__ __forceinline__ bool in_cold(float r2, const K32& c) {
          (b <= __float_as_uint(c.tiny));
 }
 
+// sure hit: tiny < r2 < sup2_lo, one unsigned compare of the (non-negative) float bits
+__device__ __forceinline__ bool is_sure(float r2, const K32& c) {
+  const uint32_t t = __float_as_uint(c.tiny);
+  return __float_as_uint(r2) - (t + 1u) < __float_as_uint(c.sup2_lo) - (t + 1u);
+}
+
 struct Geo2 {
   f2_t a1xy, a1zw, b1zw, a2xy, a2zw, b2zw, dxy1, dxy2, dz, r2, dot;
 };
@@ -967,8 +973,8 @@ __device__ __forceinline__ void eval_v8(const KArgs& a, const K32& c, const Own3
     // cold (exact f64 re-decision): r2 in [sup2_lo, sup2_hi) or r2 <= tiny, tested as
     // unsigned ranges of the (non-negative) float bits; a cold slot is not a sure hit
     const float r21 = lo(g[k].r2), r22 = hi(g[k].r2);
-    const bool c1 = in_cold(r21, c), c2 = in_cold(r22, c);
-    const bool s1 = (r21 < c.sup2_lo) & !c1, s2 = (r22 < c.sup2_lo) & !c2;
+    const bool s1 = is_sure(r21, c), s2 = is_sure(r22, c);
+    const bool c1 = !s1 & (r21 < c.sup2_hi), c2 = !s2 & (r22 < c.sup2_hi);
     okf[2 * k] = s1 ? 1.0f : 0.0f;
     okf[2 * k + 1] = s2 ? 1.0f : 0.0f;
     r2m[2 * k] = s1 ? r21 : c.sup2_lo;
@@ -984,6 +990,7 @@ __device__ __forceinline__ void eval_v8(const KArgs& a, const K32& c, const Own3
       cm |= (in_cold(lo(g[k].r2), c) ? 1u : 0u) << (2 * k);
       cm |= (in_cold(hi(g[k].r2), c) ? 1u : 0u) << (2 * k + 1);
     }
+    // (in_cold == !is_sure && r2 < sup2_hi: r2 in [sup2_lo, sup2_hi) or r2 <= tiny)
     do {
       const int k = __ffs(cm) - 1;
       uint32_t adk = ad[0];
@@ -1304,14 +1311,19 @@ __global__ void __launch_bounds__(NW * 32, 2) k_interact_v8(KArgs a, K32 k32) {
     // and write entry addresses (stride 256 B: 32 lanes), cnt the entries queued.  An
     // exhausted FIFO points cb one row past the dummy: the empty pop (bfind = -1) lands on it.
     uint32_t hp = ring, tp = ring, cnt = 0, pend = 0, cur = 0u, cb = dummy + 16u;
+    // the head entry is held in registers (nx_mask, nx_cb): a refill is a register move plus
+    // the load of the following entry, which has several pops to land
+    uint32_t nx_mask = 0u, nx_cb = 0u;
     auto pop = [&]() -> uint32_t {
       const bool need = cur == 0u, have = cnt != 0u;
       if (need & have) {
-        const uint2 e = lds64u(hp);
-        cur = e.x;
-        cb = e.y;
+        cur = nx_mask;
+        cb = nx_cb;
         hp = hp + 256u == rend ? ring : hp + 256u;
         --cnt;
+        const uint2 e = lds64u(hp);  // stale when the ring just emptied: never used then
+        nx_mask = e.x;
+        nx_cb = e.y;
       }
       cb = (need & !have) ? dummy + 16u : cb;
       const int tb = flo32(cur);
@@ -1320,6 +1332,11 @@ __global__ void __launch_bounds__(NW * 32, 2) k_interact_v8(KArgs a, K32 k32) {
     };
     auto drain = [&](bool full) {
       __syncwarp();
+      {
+        const uint2 e = lds64u(hp);  // (re)load the head entry: pushes may have refilled the ring
+        nx_mask = e.x;
+        nx_cb = e.y;
+      }
       constexpr uint32_t P = 2 * V8_NG;  // pops per lane per iteration
       const uint32_t mx = __reduce_max_sync(SPHB_FULL, pend);
       uint32_t K = (mx + P - 1) / P;
