@@ -68,7 +68,10 @@ __device__ __forceinline__ void piston_at(const sphb_params_t& p, double t, floa
 // MODE 0: verlet_update (sim.py:235-259), the reference.  MODE 1 / 2: symplectic predictor /
 // corrector (extension).  All fused with the next stage's assign_cells (K1) + histogram.
 template <int MODE>
-__global__ void __launch_bounds__(256) k_integrate(
+#ifndef SU_MINB
+#define SU_MINB 4  // 64 registers: 2x the resident warps of the default (memory-bound kernel)
+#endif
+__global__ void __launch_bounds__(256, SU_MINB) k_integrate(
     sphb_params_t p, sphb_grid_t g, int cellbits, int64_t ncells, int64_t n, int64_t nb,
     const float4* __restrict__ posp_s, const float4* __restrict__ velr_s,
     const float4* __restrict__ prev_s, const int64_t* __restrict__ id_s,

@@ -201,7 +201,10 @@ __global__ void __launch_bounds__(SORT_BLOCK) k_radix_scatter(
 }
 
 // ------------------------------------------------------------------ K3 reorder + EOS
-__global__ void __launch_bounds__(256) k_reorder(
+#ifndef NL_MINB
+#define NL_MINB 4  // 64 registers: 2x the resident warps of the default (memory-bound kernel)
+#endif
+__global__ void __launch_bounds__(256, NL_MINB) k_reorder(
     sphb_params_t p, uint32_t cellmask, int cellbits, int64_t n, const int32_t* __restrict__ perm,
     const uint32_t* __restrict__ keys_sorted, const float4* __restrict__ posp_in,
     const float4* __restrict__ velr_in, const float4* __restrict__ prev_in,
