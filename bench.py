@@ -44,6 +44,8 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget-s", type=float, default=20.0)
+    ap.add_argument("--rebalance-every", type=int, default=0,
+                    help="N>1: re-place the X-slab bounds from measured per-rank PI time every k steps")
     return ap.parse_args()
 
 
@@ -207,7 +209,8 @@ def run_slabs(args, cfg_name, system, prm, prec, world, rank, local):
     import torch.distributed as dist
     from paper_1110_3711_b200 import dslab
 
-    sim = dslab.DeviceSlabSim(system, prm, dslab.DevDistComm(), precision=prec)
+    sim = dslab.DeviceSlabSim(system, prm, dslab.DevDistComm(), precision=prec,
+                              rebalance_every=args.rebalance_every)
     me = sim.ranks[0]
     Ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
     for _ in range(args.warmup):

@@ -21,6 +21,7 @@ from left | from right][fluid: same]; the K2 sort regroups by cell anyway.  Comm
 """
 from __future__ import annotations
 
+import collections
 import ctypes
 import math
 
@@ -30,7 +31,7 @@ import torch
 from . import _lib
 from .device import Workspace, _ptr, _stream, decode_err, new_ctrl, read_ctrl
 from .physics import grid_desc, grid_dims, params_desc
-from .slab import balanced_bounds, columns_of
+from .slab import balanced_bounds, columns_of, enforce_min_width, rebalance_slices
 
 ROW_WORDS = 16  # packed exchange row: 64 B (posp, velr, prev float4, int64 id, pad)
 NCAT = 10
@@ -144,6 +145,8 @@ class DevRank:
         self.recv = [torch.zeros((1, ROW_WORDS), dtype=torch.float32, device=dev) for _ in range(2)]
         self.n = self.nb = 0
         self.cap = self.cap_ab = 0
+        # (start, end) of the recent interaction launches (since the last rebalance, at most 64)
+        self.pi_events = collections.deque(maxlen=64)
         self._grow(n_hint)
 
     def _grow(self, n):
@@ -221,10 +224,14 @@ class DevRank:
                                   _ptr(self.aux), _ptr(self.cell_s), _ptr(self.ctrl), s), "sphb_reorder")
         _lib.check(L.sphb_cell_ranges(ws, g, _ptr(self.beg), _ptr(self.end), _ptr(self.ctrl), s),
                    "sphb_cell_ranges")
+        ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+        ev[0].record()
         _lib.check(L.sphb_interact(ws, p, g, n, nb, _ptr(self.posp_s), _ptr(self.velr_s),
                                    _ptr(self.aux), _ptr(self.cell_s), _ptr(self.beg), _ptr(self.end),
                                    _ptr(self.acc), _ptr(self.drho), _ptr(self.visc), _ptr(self.ctrl),
                                    s), "sphb_interact")
+        ev[1].record()
+        self.pi_events.append(ev)
 
     def dt_words(self):
         return self.ctrl.view(torch.int64)[5:7]
@@ -314,8 +321,9 @@ class DeviceSlabSim:
     """X-slab stepper of the local ranks of ``comm`` (all on this process's current device)."""
 
     def __init__(self, system, params, comm, reach: int | None = None, precision: int = 0,
-                 bounds=None, order: int = 0):
+                 bounds=None, order: int = 0, rebalance_every: int = 0):
         self.params = params
+        self.rebalance_every = int(rebalance_every)
         self.comm = comm
         self.reach = int(params.n_subdiv if reach is None else reach)
         cs, dims = grid_dims(params)
@@ -345,7 +353,8 @@ class DeviceSlabSim:
         self._halos_built = False
 
     def _exchange(self):
-        """Phases 4-7 (the counts already computed by su_and_count / prime())."""
+        """Phases 4-7 (the counts already computed by su_and_count / prime()); returns the
+        all-gathered totals table (ranks x 10)."""
         gathered = self.comm.allgather([r.status_words() for r in self.ranks])
         tab = gathered[0].cpu().numpy()  # the step's one host synchronisation
         errs = tab[:, NCAT].astype(np.uint64)
@@ -366,6 +375,53 @@ class DeviceSlabSim:
         self.comm.sendrecv(items)
         for r, lay in zip(self.ranks, layouts):
             r.unpack(lay)
+        return tots
+
+    def _count_resident(self):
+        """K1 keys + category counts of the current (assembled) arrays."""
+        L, s = _lib.lib(), _stream()
+        for r in self.ranks:
+            r.ws.reset()
+            _lib.check(L.sphb_cell_keys(r.ws.handle, _lib.ref(r.grid), _ptr(r.a.posp), r.n, r.nb,
+                                        _ptr(r.keys), None, _ptr(r.ctrl), s), "sphb_cell_keys")
+            x0, x1 = r.bounds
+            _lib.check(L.sphb_slab_count(_lib.ref(r.grid), r.n, r.nb, _ptr(r.keys), _ptr(r.a.id), x0, x1,
+                                         _ptr(r.tiles), _ptr(r.totals), s), "sphb_slab_count")
+
+    def measured_pi_ms(self) -> np.ndarray:
+        """Mean interaction time per rank since the last rebalance (all ranks, gathered)."""
+        torch.cuda.synchronize()
+        mine = []
+        for r in self.ranks:
+            ts = [a.elapsed_time(b) for a, b in r.pi_events]
+            mine.append(torch.tensor([float(np.mean(ts)) if ts else 1.0], dtype=torch.float64,
+                                     device=r.dev))
+            r.pi_events.clear()
+        return self.comm.allgather(mine)[0].reshape(-1).cpu().numpy()
+
+    def set_bounds(self, bounds):
+        """Move the slab bounds and re-settle: repeat classify + exchange until no particle
+        sits outside its slab (multi-column moves take several neighbour hops); the last round
+        rebuilds the halos for the new bounds."""
+        bounds = np.asarray(bounds, np.int64)
+        self.bounds = bounds
+        for r in self.ranks:
+            r.bounds = (int(bounds[r.rank]), int(bounds[r.rank + 1]))
+            r.grid = grid_desc(self.params, self.reach, target_cols=r.bounds)
+        for _ in range(self.comm.nranks + 1):
+            self._count_resident()
+            tots = self._exchange()
+            if not np.any(tots[:, MIGL_B:MIGR_F + 1]):
+                break
+
+    def rebalance(self, times=None):
+        """Equal-time slab bounds (slab.rebalance_slices, the reference's balance.py:53-88
+        restated) from the measured (or given) per-rank interaction times; width >= reach."""
+        t = self.measured_pi_ms() if times is None else np.asarray(times, np.float64)
+        new = enforce_min_width(rebalance_slices(self.bounds, t), max(self.reach, 1))
+        if not np.array_equal(new, self.bounds):
+            self.set_bounds(new)
+        return new
 
     def prime(self):
         """Initial halos: classify the uploaded owned rows (keys from K1) and exchange."""
@@ -383,6 +439,8 @@ class DeviceSlabSim:
     def step(self):
         if not self._halos_built:
             self.prime()
+        if self.rebalance_every and self.step_index and self.step_index % self.rebalance_every == 0:
+            self.rebalance()
         for r in self.ranks:
             r.nl_pi()
         self.comm.allreduce([r.dt_words() for r in self.ranks], "min")
