@@ -392,46 +392,111 @@ __device__ __forceinline__ void emit_block(sphb_ctrl_t* ctrl, int4* out, int4 b,
   out[2 * k + 1] = make_int4(row, xa, xb, 0);
 }
 
-__global__ void __launch_bounds__(256) k_blocks(sphb_grid_t g, int64_t ncells,
-                                                const int32_t* __restrict__ beg,
-                                                const int32_t* __restrict__ end,
-                                                int4* __restrict__ blk, sphb_ctrl_t* ctrl) {
+constexpr int KB_BUF = 64;  // block records buffered per row before one range reservation
+
+__global__ void __launch_bounds__(32) k_blocks(sphb_grid_t g, int64_t ncells,
+                                               const int32_t* __restrict__ beg,
+                                               const int32_t* __restrict__ end,
+                                               int4* __restrict__ blk, sphb_ctrl_t* ctrl) {
+  // one warp per cell row: the lanes stage the row's cumulative ends (both lists) in shared
+  // memory, lane 0 makes the greedy cut, and the row's records are written with ONE atomic
+  // range reservation per KB_BUF records (a per-record atomic on one counter serialises ~10^5
+  // atomics per step at the L2)
+  extern __shared__ int32_t s_ends[];  // [span] fluid ends, then [span] boundary ends
+  __shared__ int4 s_rec[2 * KB_BUF];
+  __shared__ int s_nrec;
   if (!step_live(ctrl)) return;
   const int nx = g.dims[0];
   const int64_t nrows = (int64_t)g.dims[1] * g.dims[2];
   if (g.tx1 <= g.tx0) return;
-  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < nrows;
-       r += (int64_t)gridDim.x * blockDim.x) {
+  const int span = g.tx1 - g.tx0, lane = threadIdx.x;
+  auto flush = [&]() {  // all lanes: reserve a range, copy the buffered records
+    __syncwarp();
+    const int nrec = s_nrec;
+    uint32_t base = 0;
+    if (lane == 0 && nrec) base = atomicAdd(&ctrl->nblk[0], (uint32_t)nrec);
+    base = __shfl_sync(SPHB_FULL, base, 0);
+    for (int k = lane; k < 2 * nrec; k += 32) blk[2 * (int64_t)base + k] = s_rec[k];
+    __syncwarp();
+    if (lane == 0) s_nrec = 0;
+    __syncwarp();
+  };
+  if (lane == 0) s_nrec = 0;
+  for (int64_t r = blockIdx.x; r < nrows; r += gridDim.x) {
     const int64_t cb = r * nx, cf = ncells + r * nx;  // row offsets in the B / F tables
     if (end[cf + g.tx1 - 1] <= beg[cf + g.tx0] && end[cb + g.tx1 - 1] <= beg[cb + g.tx0]) continue;
+    for (int k = lane; k < span; k += 32) {
+      s_ends[k] = end[cf + g.tx0 + k];
+      s_ends[span + k] = end[cb + g.tx0 + k];
+    }
+    __syncwarp();
+    // lane 0 cuts; whenever its buffer fills, the warp flushes (k resumes where it stopped)
+    int k = 0;
     int32_t f0 = beg[cf + g.tx0], b0 = beg[cb + g.tx0];  // open block
     int32_t fcur = f0, bcur = b0;
     int xa = -1, xl = -1;  // first / last non-empty cell of the open block
-    for (int x = g.tx0; x < g.tx1; ++x) {
-      const int32_t fe = end[cf + x], be = end[cb + x];
-      if (fe == fcur && be == bcur) continue;  // empty cell
-      if ((fe - f0) + (be - b0) > BT && (fcur > f0 || bcur > b0)) {  // close before this cell
-        emit_block(ctrl, blk, make_int4(f0, fcur, b0, bcur), (int)r, xa, xl);
-        f0 = fcur;
-        b0 = bcur;
-        xa = -1;
+    bool done = false;
+    while (true) {
+      if (lane == 0) {
+        bool direct = false;  // (shadowed per cell below)
+        auto emit_to = [&](bool dir, int4 b, int x0, int x1) {
+          if (dir) {
+            emit_block(ctrl, blk, b, (int)r, x0, x1);
+            return;
+          }
+          const int n = s_nrec;
+          s_rec[2 * n] = b;
+          s_rec[2 * n + 1] = make_int4((int)r, x0, x1, 0);
+          s_nrec = n + 1;
+        };
+        (void)direct;
+        for (; k < span; ++k) {
+          const int x = g.tx0 + k;
+          const int32_t fe = s_ends[k], be = s_ends[span + k];
+          if (fe == fcur && be == bcur) continue;  // empty cell
+          // records this cell can emit (close + oversized chunks); stop and flush when the
+          // buffer cannot take them, unless it is empty (then records go out directly)
+          const int need = 1 + (fe - f0 + BT - 1) / BT + (be - b0 + BT - 1) / BT;
+          if (s_nrec + need > KB_BUF && s_nrec > 0) break;
+          const bool direct = need > KB_BUF;
+          if ((fe - f0) + (be - b0) > BT && (fcur > f0 || bcur > b0)) {  // close before this cell
+            emit_to(direct, make_int4(f0, fcur, b0, bcur), xa, xl);
+            f0 = fcur;
+            b0 = bcur;
+            xa = -1;
+          }
+          if ((fe - f0) + (be - b0) > BT) {  // one oversized cell: single-list chunks of <= BT
+            for (int32_t p = f0; p < fe; p += BT)
+              emit_to(direct, make_int4(p, min(p + BT, fe), be, be), x, x);
+            for (int32_t p = b0; p < be; p += BT)
+              emit_to(direct, make_int4(fe, fe, p, min(p + BT, be)), x, x);
+            f0 = fe;
+            b0 = be;
+          } else {
+            if (xa < 0) xa = x;
+            xl = x;
+          }
+          fcur = fe;
+          bcur = be;
+        }
+        if (k >= span) {
+          if (fcur > f0 || bcur > b0) {
+            if (s_nrec == KB_BUF) {  // no room for the final record: write it directly
+              emit_block(ctrl, blk, make_int4(f0, fcur, b0, bcur), (int)r, xa, xl);
+            } else {
+              emit_to(false, make_int4(f0, fcur, b0, bcur), xa, xl);
+            }
+          }
+          done = true;
+        }
       }
-      if ((fe - f0) + (be - b0) > BT) {  // one oversized cell: single-list chunks of <= BT
-        for (int32_t p = f0; p < fe; p += BT)
-          emit_block(ctrl, blk, make_int4(p, min(p + BT, fe), be, be), (int)r, x, x);
-        for (int32_t p = b0; p < be; p += BT)
-          emit_block(ctrl, blk, make_int4(fe, fe, p, min(p + BT, be)), (int)r, x, x);
-        f0 = fe;
-        b0 = be;
-      } else {
-        if (xa < 0) xa = x;
-        xl = x;
-      }
-      fcur = fe;
-      bcur = be;
+      done = __shfl_sync(SPHB_FULL, done, 0);
+      if (done) break;
+      flush();
     }
-    if (fcur > f0 || bcur > b0) emit_block(ctrl, blk, make_int4(f0, fcur, b0, bcur), (int)r, xa, xl);
+    if (s_nrec >= KB_BUF / 2) flush();
   }
+  flush();
 }
 
 // ------------------------------------------------------------------ the interaction kernel
@@ -1689,9 +1754,12 @@ int launch_interact(sphb_workspace* ws, const sphb_params_t& p, const sphb_grid_
   a.k_cs = a.gamma7 ? (float)(cbrt(p.c0) / p.rho0)
                     : (float)(p.c0 * pow(p.rho0, -(p.gamma - 1.0) * 0.5));
   const int64_t nrows = (int64_t)g.dims[1] * g.dims[2];
-  int gb = (int)((nrows + 255) / 256);
-  if (gb > 148 * 8) gb = 148 * 8;
-  k_blocks<<<gb, 256, 0, s>>>(g, a.ncells, beg, end, ws->blocks, ctrl);
+  // one warp per cell row (rows ~10^4): every SM busy, the row's ends staged in shared memory
+  int gb = (int)(nrows < 148 * 32 ? nrows : 148 * 32);
+  if (gb < 1) gb = 1;
+  const size_t sm_blocks = sizeof(int32_t) * 2 * (size_t)(g.tx1 - g.tx0);
+  if (sm_blocks > 48 * 1024) return sphb_set_error(SPHB_E_INVALID, "more than 6144 cell columns per slab");
+  k_blocks<<<gb, 32, sm_blocks, s>>>(g, a.ncells, beg, end, ws->blocks, ctrl);
   if (int rc = sphb_check_launch("k_blocks")) return rc;
   // one launch for both item classes: fluid targets (F-F + F-B) and boundary targets (B-F,
   // drho + visc only) of the same cells share the staged candidates
