@@ -24,6 +24,12 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+# rank 0's stdout carries exactly one JSON line: NCCL's own messages go to stderr
+# (the image's NCCL_DEBUG=VERSION prints a version banner on stdout; an explicit INFO/WARN/TRACE
+# setting is respected)
+if os.environ.get("NCCL_DEBUG", "VERSION").upper() == "VERSION":
+    os.environ["NCCL_DEBUG"] = "WARN"
+os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
 
 METRIC = "particle-steps/sec and interactions/sec at 1/2/4/8 B200 vs host-CPU ref; % HBM roofline"
 UNIT = "particle-steps/s"
@@ -44,6 +50,8 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget-s", type=float, default=20.0)
+    ap.add_argument("--slab-path", action="store_true",
+                    help="run the X-slab (NCCL) stepper even at one rank (exercises the multi-GPU path)")
     ap.add_argument("--rebalance-every", type=int, default=0,
                     help="N>1: re-place the X-slab bounds from measured per-rank PI time every k steps")
     return ap.parse_args()
@@ -234,6 +242,9 @@ def run_slabs(args, cfg_name, system, prm, prec, world, rank, local):
     h2d = d2h = 0
     e2e_value = None
     if args.e2e_steps > 0:
+        pinned = {f: torch.empty((int(me.n * 1.2) + 1024,) + tuple(getattr(me.a, f).shape[1:]),
+                                 dtype=getattr(me.a, f).dtype, pin_memory=True)
+                  for f in ("posp", "velr", "prev", "id")}  # pinned once, outside the timed region
         torch.cuda.synchronize()
         a, b = Ev(), Ev()
         a.record()
@@ -242,7 +253,11 @@ def run_slabs(args, cfg_name, system, prm, prec, world, rank, local):
             nbytes = 0
             for f in ("posp", "velr", "prev", "id"):
                 t = getattr(me.a, f)[:n]
-                host = t.to("cpu", non_blocking=False).pin_memory()
+                if f not in pinned or pinned[f].shape[0] < n:  # pinned once, reused every step
+                    pinned[f] = torch.empty((int(n * 1.2),) + tuple(t.shape[1:]), dtype=t.dtype,
+                                            pin_memory=True)
+                host = pinned[f][:n]
+                host.copy_(t, non_blocking=False)
                 t.copy_(host, non_blocking=True)
                 nbytes += host.numel() * host.element_size()
             h2d = d2h = nbytes
@@ -300,7 +315,7 @@ def main():
     import torch
     import torch.distributed as dist
     torch.cuda.set_device(local)
-    if world > 1:
+    if world > 1 or args.slab_path:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     import paper_1110_3711_b200 as sph
     from paper_1110_3711_b200 import _lib
@@ -309,7 +324,7 @@ def main():
     sc, prm, system = workload(cfg_name, args.n_subdiv)
     variant = "slowcellsh" if args.n_subdiv == 1 else "slowcellshalf"
     prec = _lib.SPHB_FP64 if args.precision == "fp64" else _lib.SPHB_FP32
-    if world > 1:
+    if world > 1 or args.slab_path:
         run_slabs(args, cfg_name, system, prm, prec, world, rank, local)
         return
     sim = DeviceSim(system, prm, reach=args.n_subdiv, precision=prec,
