@@ -71,10 +71,6 @@ struct Cfg<double> {
 // 1.025.  Valid while |x| <= 4 (the block's x extent <= 8 support radii): coordinate
 // quantisation <= 2^-9, |d(r^2)| <= 1.6e-2 at the cutoff, so no true hit is screened out.
 constexpr float H16_THR = 1.025f;
-// v8 screen (thr - r^2 as one HFMA2 chain): |d(r^2)| <= 9.1e-3 at the cutoff (coordinate
-// rounding 2^-10 per operand, HADD2 2^-12, three FMA roundings 2^-11), so 1.015 keeps a
-// 1.6x margin while admitting fewer false maybes than 1.025.
-constexpr float H16_THR8 = 1.015f;
 constexpr float H16_MAXABS = 4.0f;
 
 struct KArgs {
@@ -830,22 +826,26 @@ __global__ void __launch_bounds__(NW * 32, 2) k_interact(KArgs a) {
 }
 
 // ====================================================================== FP32 kernel (v8)
-// Same block decomposition, staging and FIFO discipline as k_interact, retuned for the
-// issue rate of sm_100a:
-//   * screen: FP16x2, thr - dx^2 - dy^2 - dz^2 as one HADD2/HFMA2 chain per coordinate,
-//     the miss flags are the sign bits, gathered 8 at a time with a sign-replicating PRMT
-//     (2 instructions per 4 candidates instead of a compare + shift/or per candidate).  The
-//     resulting mask is bit-permuted: bit 8j + k <-> candidate 4k + j of the word; pops map
-//     it back with one IMAD + LOP3.  The target itself is cleared from its own row's mask.
-//   * FIFO entries are (mask, staged byte address) pairs, one LDS.64 per refill; pops take
-//     the highest set bit (FLO, no BREV).
-//   * pair math: the two candidates a lane pops per iteration run as one packed FP32x2
-//     chain (FFMA2/FADD2/FMUL2, half the issue slots), with the constants folded
-//     (-alpha h into cs, W(dp)^-4 into the tensile factors, 3 kc/h and the neighbour mass
-//     into the mask factor) and viscosity as max(., 0) (the term is positive iff v.r < 0).
-//     Masked slots read finite staged data and are zeroed through the mask factor.
-//   * counters: hits per lane accumulate in a packed float; ff = sum over fluid targets
-//     minus sum over boundary targets (F-B and B-F hit sets are mirror images).
+// Same block decomposition and FIFO discipline as k_interact, retuned for sm_100a
+// (DESIGN.md §4):
+//   * staging: one TMA bulk copy (cp.async.bulk + mbarrier) per stencil row and array of the
+//     K3-sorted rows (x, y, z, prrho | vx, vy, vz, rho), then 8-B FP16 screen records
+//     (x, y, z, |x|^2 in block-centred units of 2h) built from shared memory;
+//   * screen on the tensor cores: r^2 - thr = |x_j|^2 - 2 x_i.x_j + |x_i|^2 - thr for 32 targets
+//     x 32 candidates per warp as 8 HMMA.1688 (FP32 accumulation); the sign bits are packed
+//     (F2FP + sign-replicating PRMT) and routed to the target lanes by a quad byte transpose,
+//     bit b <-> candidate k0 + b; the target itself is cleared from its own row's mask;
+//   * FIFO entries are (mask, staged row address) pairs in a circular 20-entry ring per lane; a
+//     full ring triggers a partial drain sized to the lightest busy lane;
+//   * pair math: 3 independent groups of 2 popped candidates per lane per iteration, each one
+//     packed FP32x2 chain (FFMA2/FADD2/FMUL2), constants folded (-alpha h into cs, W(dp)^-4
+//     into the tensile factors, kc/h and the neighbour mass into the mask factor), viscosity as
+//     max(., 0) (the term is positive iff v.r < 0); masked slots read a far dummy row and are
+//     zeroed through the mask factor;
+//   * exactness: FP32 r^2 within 5e-7 of sup2 (or coincident) is re-decided with the
+//     reference's f64 predicate, one slot per lane per round;
+//   * counters: hits per lane accumulate in a packed float; ff = sum over fluid targets minus
+//     sum over boundary targets (F-B and B-F hit sets are mirror images).
 // Accumulation order differs from the reference inside each 32-candidate word only; the
 // FP32 path's contract is rel 1e-5 (the FP64 path above stays bit-exact).
 typedef unsigned long long f2_t;
@@ -935,21 +935,6 @@ __device__ __forceinline__ uint32_t clear_bit(uint32_t v, int t) {  // bit t is 
   asm("shl.b32 %0, 1, %1;" : "=r"(m) : "r"(t));
   return v ^ m;
 }
-// bit position of candidate c (0..31) of a word in the permuted screen layout
-__host__ __device__ constexpr int perm_bit(int c) { return 8 * (c & 3) + (c >> 2); }
-struct PermGe {
-  uint32_t v[33];
-};
-__host__ __device__ constexpr PermGe make_perm_ge() {
-  PermGe t{};
-  for (int a = 0; a <= 32; ++a) {
-    uint32_t m = 0;
-    for (int c = a; c < 32; ++c) m |= 1u << perm_bit(c);
-    t.v[a] = m;
-  }
-  return t;
-}
-__constant__ PermGe c_perm_ge = make_perm_ge();  // candidates >= a of a word, permuted bits
 
 struct K32 {  // folded FP32 constants of the v8 pair loop
   float sup2_lo, sup2_hi, tiny, invh, eta2, kcs, tpos, tneg, nkgc, nkgc_b, cs_exp, ktw4;
