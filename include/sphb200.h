@@ -130,6 +130,14 @@ int sphb_workspace_create(int64_t n_max, int64_t ncells_max, sphb_workspace_t** 
 int sphb_workspace_destroy(sphb_workspace_t* ws);
 /* Zeroes the workspace histogram (needed only after an aborted step). */
 int sphb_workspace_reset(sphb_workspace_t* ws, sphb_stream_t s);
+/* Movers-only sort threshold of sphb_step (default 65536, at most min(n_max, 65536)): a
+ * step whose rows changed cell for at most `cap` rows is sorted by counting from the previous
+ * order; otherwise (or cap = -1) by the LSD radix sort.  Both give the identical permutation
+ * (grid.py:107-109 stable order); the choice is made on the device. */
+int sphb_workspace_set_mover_cap(sphb_workspace_t* ws, int64_t cap);
+/* The last sphb_step sort's path (0 movers-only, 1 radix) and mover count (synchronising
+ * read, diagnostics only). */
+int sphb_workspace_sort_info(const sphb_workspace_t* ws, int64_t* movers, int32_t* mode);
 /* Bytes of device memory the workspace holds. */
 int64_t sphb_workspace_bytes(const sphb_workspace_t* ws);
 
@@ -149,6 +157,17 @@ int sphb_cell_keys(sphb_workspace_t* ws, const sphb_grid_t* grid, const void* po
 int sphb_sort(sphb_workspace_t* ws, const sphb_grid_t* grid, const uint32_t* keys, int64_t n,
               uint32_t* keys_sorted_out, int32_t* perm_out, const sphb_ctrl_t* ctrl,
               sphb_stream_t s);
+
+/* K2 + K4 of a step (what sphb_step runs): the stable per-list argsort of the keys K7 wrote
+ * (grid.py:96-109) and this step's cell ranges (grid.py:123-144).  When the rows are still
+ * in the order of the previous sort of this state (keys_sorted, beg, end as that call left
+ * them), only the rows whose key changed are placed (counting, no radix pass); otherwise, or
+ * beyond the workspace's mover cap, the radix sort runs.  The choice is made and checked on
+ * the device; both paths give the identical permutation.  sphb_cell_keys and sphb_sort mark
+ * the previous order as unknown. */
+int sphb_sort_ranges(sphb_workspace_t* ws, const sphb_grid_t* grid, const uint32_t* keys,
+                     int64_t n, uint32_t* keys_sorted, int32_t* perm, int32_t* beg, int32_t* end,
+                     const sphb_ctrl_t* ctrl, sphb_stream_t s);
 
 /* K3 -- reorder gathers (grid.py:111-114) fused with compute_derived (physics.py:96-110):
  * *_out[i] = *_in[perm[i]] for posp, velr, prev, id; posp_out.w = prrho; aux_out = (press,

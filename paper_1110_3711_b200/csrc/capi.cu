@@ -98,6 +98,22 @@ int sphb_workspace_create(int64_t n_max, int64_t ncells_max, sphb_workspace_t** 
   ws->max_blocks = n1 + n1 / 64 + 16;
   if (e == cudaSuccess) e = alloc((void**)&ws->blocks, 2 * sizeof(int4) * ws->max_blocks);
   if (e == cudaSuccess) e = alloc((void**)&ws->energy_part, sizeof(double) * 5 * 592);
+  {
+    const int64_t words = (n1 + MV_TILE_ROWS - 1) / MV_TILE_ROWS * (MV_TILE_ROWS / 32);
+    ws->mover_cap_max = n1 < MOVER_CAP_MAX ? n1 : MOVER_CAP_MAX;
+    ws->mover_cap = ws->mover_cap_max;
+    const size_t mc = (size_t)ws->mover_cap_max;
+    if (e == cudaSuccess) e = alloc((void**)&ws->mv_state, sizeof(uint32_t) * 4);
+    if (e == cudaSuccess) e = alloc((void**)&ws->mv_bits, sizeof(uint32_t) * words);
+    if (e == cudaSuccess) e = alloc((void**)&ws->mv_wpre, sizeof(uint32_t) * words);
+    if (e == cudaSuccess) e = alloc((void**)&ws->mv_tile, sizeof(uint32_t) * (words / 32 + 1));
+    if (e == cudaSuccess) e = alloc((void**)&ws->mv_pos, sizeof(int32_t) * mc);
+    if (e == cudaSuccess) e = alloc((void**)&ws->mv_next, sizeof(int32_t) * mc);
+    if (e == cudaSuccess) e = alloc((void**)&ws->mv_head, sizeof(int32_t) * 2 * ncells_max);
+    if (e == cudaSuccess) e = alloc((void**)&ws->mv_kv, sizeof(int4) * 2 * ncells_max);
+    if (e == cudaSuccess) e = cudaMemset(ws->mv_state, 0, sizeof(uint32_t) * 4);
+    if (e == cudaSuccess) e = cudaMemset(ws->mv_head, 0xff, sizeof(int32_t) * 2 * ncells_max);
+  }
   if (e == cudaSuccess) e = cudaMemset(ws->cnt, 0, sizeof(uint32_t) * 2 * ncells_max);
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
   ws->bytes = bytes;
@@ -121,6 +137,9 @@ int sphb_workspace_destroy(sphb_workspace_t* ws) {
   cudaFree(ws->scan_partials);
   cudaFree(ws->blocks);
   cudaFree(ws->energy_part);
+  for (void* p : {(void*)ws->mv_state, (void*)ws->mv_bits, (void*)ws->mv_wpre, (void*)ws->mv_tile,
+                  (void*)ws->mv_pos, (void*)ws->mv_next, (void*)ws->mv_head, (void*)ws->mv_kv})
+    cudaFree(p);
   delete ws;
   return SPHB_OK;
 }
@@ -128,6 +147,26 @@ int sphb_workspace_destroy(sphb_workspace_t* ws) {
 int sphb_workspace_reset(sphb_workspace_t* ws, sphb_stream_t s) {
   SPHB_NONNULL(ws);
   SPHB_CUDA(cudaMemsetAsync(ws->cnt, 0, sizeof(uint32_t) * 2 * ws->ncells_max, (cudaStream_t)s));
+  SPHB_CUDA(cudaMemsetAsync(ws->mv_state, 0, sizeof(uint32_t) * 4, (cudaStream_t)s));
+  SPHB_CUDA(cudaMemsetAsync(ws->mv_head, 0xff, sizeof(int32_t) * 2 * ws->ncells_max, (cudaStream_t)s));
+  return SPHB_OK;
+}
+
+int sphb_workspace_set_mover_cap(sphb_workspace_t* ws, int64_t cap) {
+  SPHB_NONNULL(ws);
+  if (cap < -1 || cap > ws->mover_cap_max)
+    return sphb_set_error(SPHB_E_INVALID, "mover cap must lie in [-1, %lld]",
+                          (long long)ws->mover_cap_max);
+  ws->mover_cap = cap;
+  return SPHB_OK;
+}
+
+int sphb_workspace_sort_info(const sphb_workspace_t* ws, int64_t* movers, int32_t* mode) {
+  SPHB_NONNULL(ws);
+  uint32_t st[4];
+  SPHB_CUDA(cudaMemcpy(st, ws->mv_state, sizeof(st), cudaMemcpyDeviceToHost));
+  if (movers) *movers = st[3];
+  if (mode) *mode = (int32_t)st[2];
   return SPHB_OK;
 }
 
@@ -164,6 +203,22 @@ int sphb_sort(sphb_workspace_t* ws, const sphb_grid_t* grid, const uint32_t* key
     SPHB_NONNULL(perm_out);
   }
   return launch_sort(ws, *grid, keys, n, keys_sorted_out, perm_out, ctrl, (cudaStream_t)s);
+}
+
+int sphb_sort_ranges(sphb_workspace_t* ws, const sphb_grid_t* grid, const uint32_t* keys,
+                     int64_t n, uint32_t* keys_sorted, int32_t* perm, int32_t* beg, int32_t* end,
+                     const sphb_ctrl_t* ctrl, sphb_stream_t s) {
+  SPHB_NONNULL(ws);
+  if (int rc = check_grid(grid)) return rc;
+  SPHB_NONNULL(ctrl);
+  SPHB_NONNULL(beg);
+  SPHB_NONNULL(end);
+  if (n < 0) return sphb_set_error(SPHB_E_INVALID, "n < 0");
+  if (n > 0) {
+    SPHB_NONNULL(keys); SPHB_NONNULL(keys_sorted); SPHB_NONNULL(perm);
+  }
+  return launch_sort_and_ranges(ws, *grid, keys, n, keys_sorted, perm, beg, end, ctrl,
+                                (cudaStream_t)s);
 }
 
 int sphb_reorder(const sphb_params_t* prm, const sphb_grid_t* grid, int64_t n,
@@ -315,13 +370,14 @@ static int stage_pass(sphb_workspace_t* ws, const sphb_params_t* prm, const sphb
                       int64_t n, int64_t nb, const sphb_state_t* st, sphb_ctrl_t* ctrl, int mode,
                       cudaStream_t cs) {
   int rc;
-  if ((rc = launch_sort(ws, *grid, st->keys, n, st->keys_sorted, st->perm, ctrl, cs))) return rc;
+  if ((rc = launch_sort_and_ranges(ws, *grid, st->keys, n, st->keys_sorted, st->perm, st->beg,
+                                   st->end, ctrl, cs)))
+    return rc;
   if ((rc = launch_reorder(*prm, *grid, n, st->perm, st->keys_sorted, (const float4*)st->posp,
                            (const float4*)st->velr, (const float4*)st->prev, st->id,
                            (float4*)st->posp_s, (float4*)st->velr_s, (float4*)st->prev_s, st->id_s,
                            (float4*)st->aux, st->cell_s, ctrl, cs)))
     return rc;
-  if ((rc = launch_cell_ranges(ws, *grid, st->beg, st->end, ctrl, cs))) return rc;
   if ((rc = launch_interact(ws, *prm, *grid, n, nb, (const float4*)st->posp_s,
                             (const float4*)st->velr_s, (const float4*)st->aux, st->cell_s, st->beg,
                             st->end, st->acc, st->drho, st->visc, ctrl, cs)))

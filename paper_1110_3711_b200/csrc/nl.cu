@@ -109,28 +109,34 @@ __global__ void __launch_bounds__(SORT_BLOCK) k_radix_hist(const uint32_t* __res
                                                            int64_t n, int shift,
                                                            uint32_t* __restrict__ hist,
                                                            int64_t ntiles,
-                                                           const sphb_ctrl_t* ctrl) {
-  if (!step_live(ctrl)) return;
+                                                           const sphb_ctrl_t* ctrl,
+                                                           const uint32_t* skip) {
+  if (!step_live(ctrl) || (skip && *skip == 0u)) return;
   __shared__ uint32_t s[RADIX];
-  for (int d = threadIdx.x; d < RADIX; d += SORT_BLOCK) s[d] = 0;
-  __syncthreads();
   const int lane = threadIdx.x & 31;
-  const int64_t tile0 = (int64_t)blockIdx.x * SORT_TILE;
+  // persistent over tiles: a skipped pass (movers-only sort ran) costs one small launch
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    for (int d = threadIdx.x; d < RADIX; d += SORT_BLOCK) s[d] = 0;
+    __syncthreads();
+    const int64_t tile0 = tile * SORT_TILE;
 #pragma unroll 4
-  for (int r = 0; r < SORT_ITEMS; ++r) {
-    int64_t idx = tile0 + r * SORT_BLOCK + threadIdx.x;
-    uint32_t d = idx < n ? (keys[idx] >> shift) & (RADIX - 1) : RADIX;
-    uint32_t peers = __match_any_sync(SPHB_FULL, d);
-    if (d < RADIX && lane == __ffs(peers) - 1) atomicAdd(&s[d], (uint32_t)__popc(peers));
+    for (int r = 0; r < SORT_ITEMS; ++r) {
+      int64_t idx = tile0 + r * SORT_BLOCK + threadIdx.x;
+      uint32_t d = idx < n ? (keys[idx] >> shift) & (RADIX - 1) : RADIX;
+      uint32_t peers = __match_any_sync(SPHB_FULL, d);
+      if (d < RADIX && lane == __ffs(peers) - 1) atomicAdd(&s[d], (uint32_t)__popc(peers));
+    }
+    __syncthreads();
+    for (int d = threadIdx.x; d < RADIX; d += SORT_BLOCK) hist[(int64_t)d * ntiles + tile] = s[d];
+    __syncthreads();
   }
-  __syncthreads();
-  for (int d = threadIdx.x; d < RADIX; d += SORT_BLOCK) hist[(int64_t)d * ntiles + blockIdx.x] = s[d];
 }
 
 __global__ void __launch_bounds__(1024) k_radix_rowscan(uint32_t* __restrict__ hist, int64_t ntiles,
                                                         uint32_t* __restrict__ digit_total,
-                                                        const sphb_ctrl_t* ctrl) {
-  if (!step_live(ctrl)) return;
+                                                        const sphb_ctrl_t* ctrl,
+                                                        const uint32_t* skip) {
+  if (!step_live(ctrl) || (skip && *skip == 0u)) return;
   __shared__ uint32_t s_warp[32];
   uint32_t* row = hist + (int64_t)blockIdx.x * ntiles;
   uint32_t running = 0;
@@ -150,53 +156,56 @@ __global__ void __launch_bounds__(1024) k_radix_rowscan(uint32_t* __restrict__ h
 __global__ void __launch_bounds__(SORT_BLOCK) k_radix_scatter(
     const uint32_t* __restrict__ keys_in, const int32_t* __restrict__ vals_in, int64_t n, int shift,
     const uint32_t* __restrict__ hist, const uint32_t* __restrict__ digit_total, int64_t ntiles,
-    uint32_t* __restrict__ keys_out, int32_t* __restrict__ vals_out, const sphb_ctrl_t* ctrl) {
-  if (!step_live(ctrl)) return;
+    uint32_t* __restrict__ keys_out, int32_t* __restrict__ vals_out, const sphb_ctrl_t* ctrl,
+    const uint32_t* skip) {
+  if (!step_live(ctrl) || (skip && *skip == 0u)) return;
   constexpr int NW = SORT_BLOCK / 32;
   __shared__ uint32_t s_base[RADIX];
   __shared__ uint32_t s_run[RADIX];
   __shared__ uint32_t s_wc[2][NW][RADIX];
   __shared__ uint32_t s_warp[32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t tile = blockIdx.x;
-  // digit base = exclusive scan of digit totals (RADIX == SORT_BLOCK)
-  {
-    uint32_t v = digit_total[threadIdx.x], total;
-    uint32_t ex = block_exclusive_scan<SORT_BLOCK>(v, &total, s_warp);
-    s_base[threadIdx.x] = ex + hist[(int64_t)threadIdx.x * ntiles + tile];
-    s_run[threadIdx.x] = 0;
-    for (int w = 0; w < NW; ++w) s_wc[0][w][threadIdx.x] = 0;
-  }
-  __syncthreads();
   const uint32_t lt = lanemask_lt();
-  const int64_t tile0 = tile * SORT_TILE;
-  for (int r = 0; r < SORT_ITEMS; ++r) {
-    const int p = r & 1;
-    int64_t idx = tile0 + r * SORT_BLOCK + threadIdx.x;
-    bool valid = idx < n;
-    uint32_t key = valid ? keys_in[idx] : 0u;
-    uint32_t d = valid ? (key >> shift) & (RADIX - 1) : RADIX;
-    uint32_t peers = __match_any_sync(SPHB_FULL, d);
-    uint32_t lrank = __popc(peers & lt);
-    if (valid && lane == __ffs(peers) - 1) s_wc[p][warp][d] = __popc(peers);
-    __syncthreads();
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {  // persistent (see hist)
+    // digit base = exclusive scan of digit totals (RADIX == SORT_BLOCK)
     {
-      uint32_t run = s_run[threadIdx.x];
-#pragma unroll
-      for (int w = 0; w < NW; ++w) {
-        uint32_t c = s_wc[p][w][threadIdx.x];
-        s_wc[p][w][threadIdx.x] = run;
-        run += c;
-        s_wc[p ^ 1][w][threadIdx.x] = 0;
-      }
-      s_run[threadIdx.x] = run;
+      uint32_t v = digit_total[threadIdx.x], total;
+      uint32_t ex = block_exclusive_scan<SORT_BLOCK>(v, &total, s_warp);
+      s_base[threadIdx.x] = ex + hist[(int64_t)threadIdx.x * ntiles + tile];
+      s_run[threadIdx.x] = 0;
+      for (int w = 0; w < NW; ++w) s_wc[0][w][threadIdx.x] = 0;
     }
     __syncthreads();
-    if (valid) {
-      uint32_t pos = s_base[d] + s_wc[p][warp][d] + lrank;
-      keys_out[pos] = key;
-      vals_out[pos] = vals_in ? vals_in[idx] : (int32_t)idx;
+    const int64_t tile0 = tile * SORT_TILE;
+    for (int r = 0; r < SORT_ITEMS; ++r) {
+      const int p = r & 1;
+      int64_t idx = tile0 + r * SORT_BLOCK + threadIdx.x;
+      bool valid = idx < n;
+      uint32_t key = valid ? keys_in[idx] : 0u;
+      uint32_t d = valid ? (key >> shift) & (RADIX - 1) : RADIX;
+      uint32_t peers = __match_any_sync(SPHB_FULL, d);
+      uint32_t lrank = __popc(peers & lt);
+      if (valid && lane == __ffs(peers) - 1) s_wc[p][warp][d] = __popc(peers);
+      __syncthreads();
+      {
+        uint32_t run = s_run[threadIdx.x];
+#pragma unroll
+        for (int w = 0; w < NW; ++w) {
+          uint32_t c = s_wc[p][w][threadIdx.x];
+          s_wc[p][w][threadIdx.x] = run;
+          run += c;
+          s_wc[p ^ 1][w][threadIdx.x] = 0;
+        }
+        s_run[threadIdx.x] = run;
+      }
+      __syncthreads();
+      if (valid) {
+        uint32_t pos = s_base[d] + s_wc[p][warp][d] + lrank;
+        keys_out[pos] = key;
+        vals_out[pos] = vals_in ? vals_in[idx] : (int32_t)idx;
+      }
     }
+    __syncthreads();
   }
 }
 
@@ -265,10 +274,24 @@ __global__ void __launch_bounds__(1024) k_scan_partials(uint32_t* __restrict__ p
   }
 }
 
+// Per-key constants of the movers-only sort (k_mv_scatter), written while the previous ranges
+// are still in beg/end: kv = (SB, MB, ob, head) with ob/oe the old range, nb the new begin,
+// M(p) the movers before p:  SB = nb - ob + M(ob) (stayers: position = SB + i - M(i) + chain),
+// MB = nb + (oe - ob) - (M(oe) - M(ob)) (movers after the old range), head = the key's mover
+// chain (reset here for the next step).
+struct MvApply {
+  int4* kv;
+  int32_t* head;
+  const uint32_t* bits;
+  const uint32_t* wpre;
+  const uint32_t* state;
+  int64_t n;
+};
+
 __global__ void __launch_bounds__(SCAN_BLOCK) k_scan_apply(uint32_t* __restrict__ cnt, int64_t len,
                                                            const uint32_t* __restrict__ partials,
                                                            int32_t* __restrict__ beg,
-                                                           int32_t* __restrict__ end,
+                                                           int32_t* __restrict__ end, MvApply mv,
                                                            const sphb_ctrl_t* ctrl) {
   if (ctrl && !step_live(ctrl)) return;
   __shared__ uint32_t s_warp[32];
@@ -282,14 +305,199 @@ __global__ void __launch_bounds__(SCAN_BLOCK) k_scan_apply(uint32_t* __restrict_
   }
   uint32_t total;
   uint32_t ex = block_exclusive_scan<SCAN_BLOCK>(v, &total, s_warp) + partials[blockIdx.x];
+  const bool movers = mv.kv && mv.state[2] == 0u;
+  const uint32_t m = movers ? mv.state[3] : 0u;
+  auto M = [&](int64_t p) -> int32_t {
+    if (p >= mv.n) return (int32_t)m;
+    const int64_t wi = p >> 5;
+    return (int32_t)(mv.wpre[wi] + __popc(mv.bits[wi] & ((1u << (p & 31)) - 1u)));
+  };
 #pragma unroll
   for (int k = 0; k < SCAN_ITEMS; ++k) {
-    if (base + k < len) {
-      beg[base + k] = (int32_t)ex;
+    const int64_t x = base + k;
+    if (x < len) {
+      if (movers) {
+        const int32_t ob = beg[x], oe = end[x], h = mv.head[x];
+        if (h >= 0) mv.head[x] = -1;
+        if (c[k] != 0u) {
+          const int32_t mob = M(ob);
+          mv.kv[x] = make_int4((int32_t)ex - ob + mob,
+                               (int32_t)ex + (oe - ob) - (M(oe) - mob), ob, h);
+        }
+      }
+      beg[x] = (int32_t)ex;
       ex += c[k];
-      end[base + k] = (int32_t)ex;
-      cnt[base + k] = 0;  // self-cleaning for the next step's histogram
+      end[x] = (int32_t)ex;
+      cnt[x] = 0;  // self-cleaning for the next step's histogram
     }
+  }
+}
+
+// ------------------------------------------------------------------ K2' movers-only sort
+// Inside sphb_step the rows arrive in the previous step's sorted order with K7's new keys, and
+// the previous sort's keys (keys_sorted) and per-cell ranges (beg/end) are still in the state.
+// A row whose key did not change ("stayer") keeps its place inside its old cell range; only
+// the few rows that changed cell ("movers", 0.04% per step on average)
+// need placing.  The stable order (grid.py:107-109: key, then current index) follows by
+// counting, without a radix pass.  With M(p) = movers before position p (bitmap + prefix),
+// [ob, oe) the key's old range and nb its new begin (this step's K4):
+//   stayer i of key k:  position = nb + (i - ob) - (M(i) - M(ob)) + #{movers into k at < i}
+//   mover  i into  k:   position = nb + (i < ob ? 0 : stayers of k) + #{movers into k at < i}
+// Movers into a key are chained in a per-key list (only counts are read, so the chain order
+// does not matter): the result is deterministic and identical to the radix sort.
+//   k_mv_flag     mover bitmap + tile counts; checks the previous order (sorted keys_sorted,
+//                 runs == [beg, end))
+//   k_mv_scan     tile prefix, mover count, path decision
+//   k_mv_compact  mover positions + per-key chains, per-word mover prefix
+//   k_scan_apply  (K4) per-key constants (SB, MB, ob, chain) from the old ranges, then the new
+//   k_mv_scatter  perm / keys_sorted
+// The radix passes run instead (mode 1) unless the previous order is established (set by a
+// sort, cleared by K1 and the standalone sphb_sort), consistent, and movers <= cap.
+// state words: [0] order established, [1] inconsistency seen, [2] mode (0 movers, 1 radix), [3] m
+constexpr int MV_BLOCK = 256, MV_ITEMS = 4, MV_TILE = MV_BLOCK * MV_ITEMS;  // 32 words per tile
+static_assert(MV_TILE == MV_TILE_ROWS, "workspace sizing");
+
+__device__ __forceinline__ uint32_t mv_index(uint32_t key, int cellbits, uint32_t ncells) {
+  return (key >> cellbits) * ncells + (key & ((1u << cellbits) - 1u));
+}
+
+__global__ void __launch_bounds__(MV_BLOCK) k_mv_flag(const uint32_t* __restrict__ keys,
+                                                      const uint32_t* __restrict__ prev, int64_t n,
+                                                      int cellbits, uint32_t ncells,
+                                                      const int32_t* __restrict__ obeg,
+                                                      const int32_t* __restrict__ oend,
+                                                      uint32_t* __restrict__ bits,
+                                                      uint32_t* __restrict__ tile_cnt,
+                                                      uint32_t* state, const sphb_ctrl_t* ctrl) {
+  if (!step_live(ctrl) || state[0] == 0u) return;
+  __shared__ uint32_t s_cnt;
+  if (threadIdx.x == 0) s_cnt = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int64_t t0 = (int64_t)blockIdx.x * MV_TILE;
+  const uint32_t cm = (1u << cellbits) - 1u;
+  auto bad_key = [&](uint32_t k) { return (k >> cellbits) > 1u || (k & cm) >= ncells; };
+  bool bad = false;
+  uint32_t c = 0;
+#pragma unroll
+  for (int r = 0; r < MV_ITEMS; ++r) {
+    const int64_t i = t0 + r * MV_BLOCK + threadIdx.x;
+    const bool in = i < n;
+    const uint32_t k = in ? keys[i] : 0u, kp = in ? prev[i] : 0u;
+    // consistency of the previous order (keys_sorted, beg, end of the last sort): keys_sorted
+    // ascending and every run of equal keys exactly its [beg, end) -- checked at run ends
+    uint32_t kl = __shfl_up_sync(SPHB_FULL, kp, 1), kr = __shfl_down_sync(SPHB_FULL, kp, 1);
+    if (lane == 0 && in && i > 0) kl = prev[i - 1];
+    if (lane == 31 && i + 1 < n) kr = prev[i + 1];
+    const bool mv = in && k != kp;
+    if (in) {
+      if (bad_key(k) || bad_key(kp)) {
+        bad = true;  // out-of-domain key (the step is aborting) or no previous order
+      } else {
+        const uint32_t x = (kp >> cellbits) * ncells + (kp & cm);
+        if (i == 0 || kl != kp) bad |= (i > 0 && kl > kp) || obeg[x] != (int32_t)i;
+        if (i + 1 == n || kr != kp) bad |= oend[x] != (int32_t)(i + 1);
+      }
+    }
+    const uint32_t w = __ballot_sync(SPHB_FULL, mv);
+    if (lane == 0) bits[(t0 + r * MV_BLOCK + threadIdx.x) >> 5] = w;
+    c += __popc(w);
+  }
+  if (lane == 0 && c) atomicAdd(&s_cnt, c);
+  if (__any_sync(SPHB_FULL, bad) && lane == 0) atomicOr(&state[1], 1u);
+  __syncthreads();
+  if (threadIdx.x == 0) tile_cnt[blockIdx.x] = s_cnt;
+}
+
+// one block: exclusive scan of the tile counts, mover total, path decision
+__global__ void __launch_bounds__(1024) k_mv_scan(uint32_t* __restrict__ tile_cnt, int64_t ntiles,
+                                                  int64_t cap, uint32_t* state,
+                                                  const sphb_ctrl_t* ctrl) {
+  if (!step_live(ctrl)) return;
+  __shared__ uint32_t s_warp[32];
+  const bool ordered = state[0] != 0u && state[1] == 0u && cap >= 0;
+  uint32_t running = 0;
+  if (ordered) {
+    for (int64_t base = 0; base < ntiles; base += 1024) {
+      const int64_t k = base + threadIdx.x;
+      const uint32_t v = k < ntiles ? tile_cnt[k] : 0u;
+      uint32_t total;
+      const uint32_t ex = block_exclusive_scan<1024>(v, &total, s_warp);
+      if (k < ntiles) tile_cnt[k] = running + ex;
+      running += total;
+    }
+  }
+  if (threadIdx.x == 0) {
+    state[2] = (ordered && (int64_t)running <= cap) ? 0u : 1u;
+    state[3] = ordered ? running : 0u;
+    state[1] = 0u;
+    state[0] = 1u;  // this step's sort (either path) establishes the order for the next one
+  }
+}
+
+// movers -> (position, key) list in index order + per-key chains; per-word mover prefix
+__global__ void __launch_bounds__(MV_BLOCK) k_mv_compact(
+    const uint32_t* __restrict__ keys, int cellbits, uint32_t ncells,
+    const uint32_t* __restrict__ bits, const uint32_t* __restrict__ tile_pre,
+    uint32_t* __restrict__ wpre, int32_t* __restrict__ mv_pos,
+    int32_t* __restrict__ mv_next, int32_t* __restrict__ mv_head, const uint32_t* state,
+    const sphb_ctrl_t* ctrl) {
+  if (!step_live(ctrl) || state[2] != 0u) return;
+  __shared__ uint32_t s_w[32], s_pre[32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t w0 = (int64_t)blockIdx.x * (MV_TILE / 32);
+  if (warp == 0) {
+    const uint32_t w = bits[w0 + lane];
+    const uint32_t c = __popc(w);
+    uint32_t x = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(SPHB_FULL, x, o);
+      if (lane >= o) x += y;
+    }
+    const uint32_t pre = tile_pre[blockIdx.x] + x - c;
+    wpre[w0 + lane] = pre;
+    s_w[lane] = w;
+    s_pre[lane] = pre;
+  }
+  __syncthreads();
+  const uint32_t lt = lanemask_lt();
+#pragma unroll
+  for (int r = 0; r < MV_ITEMS; ++r) {
+    const int wi = r * (MV_BLOCK / 32) + warp;
+    const uint32_t w = s_w[wi];
+    if ((w >> lane) & 1u) {
+      const int64_t i = (int64_t)blockIdx.x * MV_TILE + r * MV_BLOCK + threadIdx.x;
+      const int32_t j = (int32_t)(s_pre[wi] + __popc(w & lt));
+      const uint32_t k = keys[i];
+      mv_pos[j] = (int32_t)i;
+      mv_next[j] = atomicExch(&mv_head[mv_index(k, cellbits, ncells)], j);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) k_mv_scatter(
+    const uint32_t* __restrict__ keys, int64_t n, int cellbits, uint32_t ncells,
+    const uint32_t* __restrict__ bits, const uint32_t* __restrict__ wpre,
+    const int4* __restrict__ kv, const int32_t* __restrict__ nbeg,
+    const int32_t* __restrict__ mv_pos, const int32_t* __restrict__ mv_next,
+    const uint32_t* state, uint32_t* __restrict__ keys_sorted, int32_t* __restrict__ perm,
+    const sphb_ctrl_t* ctrl) {
+  if (!step_live(ctrl) || state[2] != 0u) return;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const uint32_t k = keys[i];
+    const uint32_t x = mv_index(k, cellbits, ncells);
+    const uint32_t w = bits[i >> 5];
+    const int4 q = kv[x];  // (SB, MB, ob, head)
+    int64_t pos;
+    if (!((w >> (i & 31)) & 1u))
+      pos = (int64_t)q.x + i - (int64_t)(wpre[i >> 5] + __popc(w & ((1u << (i & 31)) - 1u)));
+    else
+      pos = i < q.z ? nbeg[x] : q.y;
+    for (int32_t j = q.w; j >= 0; j = mv_next[j]) pos += mv_pos[j] < i;
+    perm[pos] = (int32_t)i;
+    keys_sorted[pos] = k;
   }
 }
 
@@ -303,7 +511,8 @@ int sort_pass_count(const sphb_grid_t& g) {
 
 int64_t nl_launch_count(const sphb_grid_t& g, int64_t n) {
   (void)n;
-  return 3 * sort_pass_count(g) + 1 /*reorder*/ + 3 /*scan*/;
+  // movers-only path (4) + the radix passes (no-ops when the movers path ran) + K3 + K4
+  return 4 + 3 * sort_pass_count(g) + 1 /*reorder*/ + 3 /*scan*/;
 }
 
 int launch_cell_keys(sphb_workspace* ws, const sphb_grid_t& g, const float4* posp, int64_t n,
@@ -315,6 +524,9 @@ int launch_cell_keys(sphb_workspace* ws, const sphb_grid_t& g, const float4* pos
                           (long long)n, (long long)nc, (long long)ws->n_max,
                           (long long)ws->ncells_max);
   if (n == 0) return SPHB_OK;
+  // rows written from outside: the next sphb_step sort cannot trust the previous order
+  if (cudaError_t e = cudaMemsetAsync(ws->mv_state, 0, sizeof(uint32_t), s))
+    return sphb_set_error(SPHB_E_CUDA, "mv_state reset: %s", cudaGetErrorString(e));
   k_cell_keys<<<grid_for(n, 256), 256, 0, s>>>(g, posp, n, nb, cellbits_of(g), keys, cell_out,
                                                 ws->cnt, nc, ctrl);
   return sphb_check_launch("k_cell_keys");
@@ -330,10 +542,9 @@ int launch_hist_from_sorted(sphb_workspace* ws, const sphb_grid_t& g, const int3
   return sphb_check_launch("k_hist_sorted");
 }
 
-int launch_sort(sphb_workspace* ws, const sphb_grid_t& g, const uint32_t* keys, int64_t n,
-                uint32_t* keys_sorted, int32_t* perm, const sphb_ctrl_t* ctrl, cudaStream_t s) {
-  if (n > ws->n_max) return sphb_set_error(SPHB_E_CAPACITY, "n exceeds workspace");
-  if (n == 0) return SPHB_OK;
+static void radix_passes(sphb_workspace* ws, const sphb_grid_t& g, const uint32_t* keys,
+                         int64_t n, uint32_t* keys_sorted, int32_t* perm,
+                         const sphb_ctrl_t* ctrl, const uint32_t* skip, cudaStream_t s) {
   const int passes = sort_pass_count(g);
   const int64_t ntiles = (n + SORT_TILE - 1) / SORT_TILE;
   const uint32_t* kin = keys;
@@ -343,15 +554,57 @@ int launch_sort(sphb_workspace* ws, const sphb_grid_t& g, const uint32_t* keys, 
     uint32_t* kout = last ? (keys_sorted ? keys_sorted : ws->keys_tmp[pass & 1]) : ws->keys_tmp[pass & 1];
     int32_t* vout = last ? perm : ws->vals_tmp[pass & 1];
     const int shift = pass * RADIX_BITS;
-    k_radix_hist<<<(unsigned)ntiles, SORT_BLOCK, 0, s>>>(kin, n, shift, ws->radix_hist, ntiles, ctrl);
-    k_radix_rowscan<<<RADIX, 1024, 0, s>>>(ws->radix_hist, ntiles, ws->digit_total, ctrl);
-    k_radix_scatter<<<(unsigned)ntiles, SORT_BLOCK, 0, s>>>(kin, vin, n, shift, ws->radix_hist,
+    const unsigned grid = (unsigned)(ntiles < 148 * 8 ? ntiles : 148 * 8);
+    k_radix_hist<<<grid, SORT_BLOCK, 0, s>>>(kin, n, shift, ws->radix_hist, ntiles, ctrl, skip);
+    k_radix_rowscan<<<RADIX, 1024, 0, s>>>(ws->radix_hist, ntiles, ws->digit_total, ctrl, skip);
+    k_radix_scatter<<<grid, SORT_BLOCK, 0, s>>>(kin, vin, n, shift, ws->radix_hist,
                                                             ws->digit_total, ntiles, kout, vout,
-                                                            ctrl);
+                                                            ctrl, skip);
     kin = kout;
     vin = vout;
   }
+}
+
+int launch_sort(sphb_workspace* ws, const sphb_grid_t& g, const uint32_t* keys, int64_t n,
+                uint32_t* keys_sorted, int32_t* perm, const sphb_ctrl_t* ctrl, cudaStream_t s) {
+  if (n > ws->n_max) return sphb_set_error(SPHB_E_CAPACITY, "n exceeds workspace");
+  if (n == 0) return SPHB_OK;
+  // arbitrary buffers: the movers-only path of the next sphb_step must not trust them
+  if (cudaError_t e = cudaMemsetAsync(ws->mv_state, 0, sizeof(uint32_t), s))
+    return sphb_set_error(SPHB_E_CUDA, "mv_state reset: %s", cudaGetErrorString(e));
+  radix_passes(ws, g, keys, n, keys_sorted, perm, ctrl, nullptr, s);
   return sphb_check_launch("radix sort");
+}
+
+int launch_sort_and_ranges(sphb_workspace* ws, const sphb_grid_t& g, const uint32_t* keys,
+                           int64_t n, uint32_t* keys_sorted, int32_t* perm, int32_t* beg,
+                           int32_t* end, const sphb_ctrl_t* ctrl, cudaStream_t s) {
+  if (n > ws->n_max) return sphb_set_error(SPHB_E_CAPACITY, "n exceeds workspace");
+  const int64_t nc = ncells_of(g);
+  const int64_t len = 2 * nc;
+  const int64_t nscan = (len + SCAN_TILE - 1) / SCAN_TILE;
+  if (nscan > ws->max_scan_tiles) return sphb_set_error(SPHB_E_CAPACITY, "ncells exceeds workspace");
+  if (n == 0) return launch_cell_ranges(ws, g, beg, end, ctrl, s);
+  const int cb = cellbits_of(g);
+  const int64_t tiles = (n + MV_TILE - 1) / MV_TILE;
+  uint32_t* st = ws->mv_state;
+  k_mv_flag<<<(unsigned)tiles, MV_BLOCK, 0, s>>>(keys, keys_sorted, n, cb, (uint32_t)nc, beg, end,
+                                                 ws->mv_bits, ws->mv_tile, st, ctrl);
+  k_mv_scan<<<1, 1024, 0, s>>>(ws->mv_tile, tiles, ws->mover_cap, st, ctrl);
+  k_mv_compact<<<(unsigned)tiles, MV_BLOCK, 0, s>>>(keys, cb, (uint32_t)nc, ws->mv_bits, ws->mv_tile,
+                                                    ws->mv_wpre, ws->mv_pos,
+                                                    ws->mv_next, ws->mv_head, st, ctrl);
+  // K4 for this step, keeping the previous ranges for the scatter
+  k_scan_reduce<<<(unsigned)nscan, SCAN_BLOCK, 0, s>>>(ws->cnt, len, ws->scan_partials, ctrl);
+  k_scan_partials<<<1, 1024, 0, s>>>(ws->scan_partials, nscan, ctrl);
+  const MvApply mva{ws->mv_kv, ws->mv_head, ws->mv_bits, ws->mv_wpre, st, n};
+  k_scan_apply<<<(unsigned)nscan, SCAN_BLOCK, 0, s>>>(ws->cnt, len, ws->scan_partials, beg, end,
+                                                      mva, ctrl);
+  k_mv_scatter<<<grid_for(n, 256), 256, 0, s>>>(keys, n, cb, (uint32_t)nc, ws->mv_bits, ws->mv_wpre,
+                                               ws->mv_kv, beg, ws->mv_pos, ws->mv_next, st,
+                                               keys_sorted, perm, ctrl);
+  radix_passes(ws, g, keys, n, keys_sorted, perm, ctrl, st + 2, s);  // mode 1 only
+  return sphb_check_launch("sort + cell ranges");
 }
 
 int launch_reorder(const sphb_params_t& p, const sphb_grid_t& g, int64_t n, const int32_t* perm,
@@ -375,6 +628,6 @@ int launch_cell_ranges(sphb_workspace* ws, const sphb_grid_t& g, int32_t* beg, i
   k_scan_reduce<<<(unsigned)ntiles, SCAN_BLOCK, 0, s>>>(ws->cnt, len, ws->scan_partials, ctrl);
   k_scan_partials<<<1, 1024, 0, s>>>(ws->scan_partials, ntiles, ctrl);
   k_scan_apply<<<(unsigned)ntiles, SCAN_BLOCK, 0, s>>>(ws->cnt, len, ws->scan_partials, beg, end,
-                                                       ctrl);
+                                                       MvApply{}, ctrl);
   return sphb_check_launch("cell ranges scan");
 }

@@ -13,6 +13,8 @@ constexpr int RADIX = 1 << RADIX_BITS;
 constexpr int SCAN_BLOCK = 256;
 constexpr int SCAN_ITEMS = 4;
 constexpr int SCAN_TILE = SCAN_BLOCK * SCAN_ITEMS;
+constexpr int MV_TILE_ROWS = 1024;          // rows per movers-only sort tile (32 bitmap words)
+constexpr int64_t MOVER_CAP_MAX = 1 << 16;  // movers per step the movers-only sort accepts
 
 struct sphb_workspace {
   int64_t n_max = 0, ncells_max = 0;
@@ -26,6 +28,17 @@ struct sphb_workspace {
   int64_t max_blocks = 0;
   int64_t max_sort_tiles = 0, max_scan_tiles = 0;
   double* energy_part = nullptr;  // 592 x 5 partial sums of sphb_energy
+  // movers-only sort (nl.cu, k_mv_*): state words, per-32-row mover bitmap and prefix, tile
+  // counts, the mover list and per-key chains, per-key placement constants
+  uint32_t* mv_state = nullptr;  // [order established, inconsistency, mode, movers]
+  uint32_t* mv_bits = nullptr;
+  uint32_t* mv_wpre = nullptr;
+  uint32_t* mv_tile = nullptr;
+  int32_t* mv_pos = nullptr;
+  int32_t* mv_next = nullptr;
+  int32_t* mv_head = nullptr;  // 2*ncells_max, -1 between steps
+  int4* mv_kv = nullptr;       // 2*ncells_max per-key (SB, MB, old begin, chain head)
+  int64_t mover_cap_max = 0, mover_cap = 0;
   size_t bytes = 0;
 };
 
@@ -42,6 +55,10 @@ int launch_reorder(const sphb_params_t& p, const sphb_grid_t& g, int64_t n, cons
                    int32_t* cell_out, const sphb_ctrl_t* ctrl, cudaStream_t s);
 int launch_cell_ranges(sphb_workspace* ws, const sphb_grid_t& g, int32_t* beg, int32_t* end,
                        const sphb_ctrl_t* ctrl, cudaStream_t s);
+// sphb_step's NL: movers-only stable sort (radix fallback on the device) + K4
+int launch_sort_and_ranges(sphb_workspace* ws, const sphb_grid_t& g, const uint32_t* keys,
+                           int64_t n, uint32_t* keys_sorted, int32_t* perm, int32_t* beg,
+                           int32_t* end, const sphb_ctrl_t* ctrl, cudaStream_t s);
 int launch_hist_from_sorted(sphb_workspace* ws, const sphb_grid_t& g, const int32_t* cell_sorted,
                             int64_t n, int64_t nb, cudaStream_t s);
 int sort_pass_count(const sphb_grid_t& g);

@@ -60,6 +60,18 @@ class Workspace:
     def reset(self):
         _lib.check(_lib.lib().sphb_workspace_reset(self._h, _stream()), "sphb_workspace_reset")
 
+    def set_mover_cap(self, cap: int):
+        """Movers-only sort threshold of sphb_step (-1: always the radix sort)."""
+        _lib.check(_lib.lib().sphb_workspace_set_mover_cap(self._h, int(cap)),
+                   "sphb_workspace_set_mover_cap")
+
+    def sort_info(self) -> tuple[int, int]:
+        """(movers, mode) of the last sphb_step sort; mode 0 movers-only, 1 radix."""
+        m, mode = ctypes.c_int64(), ctypes.c_int32()
+        _lib.check(_lib.lib().sphb_workspace_sort_info(self._h, ctypes.byref(m), ctypes.byref(mode)),
+                   "sphb_workspace_sort_info")
+        return int(m.value), int(mode.value)
+
     def __del__(self):
         try:
             if self._h:
@@ -194,15 +206,14 @@ class DeviceSim:
         ev[0] after NL, ev[1] after PI, ev[2] after the update."""
         L, s, ws = _lib.lib(), _stream(), self.ws.handle
         g, p, n, nb = _lib.ref(self.grid), _lib.ref(self.prm), self.n, self.nb
-        _lib.check(L.sphb_sort(ws, g, _ptr(self.keys), n, _ptr(self.keys_sorted), _ptr(self.perm),
-                               _ptr(self.ctrl), s), "sphb_sort")
+        _lib.check(L.sphb_sort_ranges(ws, g, _ptr(self.keys), n, _ptr(self.keys_sorted),
+                                      _ptr(self.perm), _ptr(self.beg), _ptr(self.end),
+                                      _ptr(self.ctrl), s), "sphb_sort_ranges")
         _lib.check(L.sphb_reorder(p, g, n, _ptr(self.perm), _ptr(self.keys_sorted), _ptr(self.posp),
                                   _ptr(self.velr), _ptr(self.prev), _ptr(self.id), _ptr(self.posp_s),
                                   _ptr(self.velr_s), _ptr(self.prev_s), _ptr(self.id_s),
                                   _ptr(self.aux), _ptr(self.cell_s), _ptr(self.ctrl), s),
                    "sphb_reorder")
-        _lib.check(L.sphb_cell_ranges(ws, g, _ptr(self.beg), _ptr(self.end), _ptr(self.ctrl), s),
-                   "sphb_cell_ranges")
         ev[0].record()
         _lib.check(L.sphb_interact(ws, p, g, n, nb, _ptr(self.posp_s), _ptr(self.velr_s),
                                    _ptr(self.aux), _ptr(self.cell_s), _ptr(self.beg),

@@ -311,6 +311,40 @@ def test_graph_capture_matches_eager():
     assert np.array_equal(v, z["final_vel"]) and np.array_equal(r, z["final_rho"])
 
 
+def test_movers_only_sort_matches_radix():
+    """sphb_step's movers-only sort (nl.cu k_mv_*) gives the radix sort's permutation
+    (grid.py:107-109 stable order) at every step; cap -1 forces the radix path, a small cap
+    mixes both paths from step to step."""
+    sc = sph.named_scenario("c1")
+    prm = sph.make_params(sc)
+    system = sph.build_dam_break(sc, prm)
+    sims = []
+    for cap in (None, -1, 40):
+        sim = D.DeviceSim(system, prm, reach=1, precision=0)
+        if cap is not None:
+            sim.ws.set_mover_cap(cap)
+        sims.append(sim)
+    modes = {0: [], 1: [], 2: []}
+    for step in range(60):
+        for k, sim in enumerate(sims):
+            sim.launch_step()
+            modes[k].append(sim.ws.sort_info())
+        a = sims[0]
+        for b in sims[1:]:
+            assert np.array_equal(a.perm[:a.n].cpu().numpy(), b.perm[:b.n].cpu().numpy()), step
+            assert np.array_equal(a.keys_sorted[:a.n].cpu().numpy(), b.keys_sorted[:b.n].cpu().numpy())
+            assert np.array_equal(a.beg.cpu().numpy(), b.beg.cpu().numpy())
+        ks = a.keys_sorted[:a.n].cpu().numpy().view(np.uint32)
+        assert np.all(ks[1:] >= ks[:-1])
+    assert modes[0][0][1] == 1  # first step after upload: no previous order -> radix
+    assert all(m == 0 for _, m in modes[0][1:]) and sum(mv for mv, _ in modes[0]) > 0
+    assert all(m == 1 for _, m in modes[1])
+    assert all(m == int(mv > 40) for mv, m in modes[2][1:])  # the cap decides per step
+    fa, fb = sims[0].download(), sims[1].download()
+    for x, y in zip(fa, fb):
+        assert np.array_equal(x, y)
+
+
 # ------------------------------------------------------------------ full sizes
 def _device_counters(name, n_subdiv, precision="fp32"):
     sc = sph.named_scenario(name)

@@ -14,5 +14,8 @@ ncu) timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 20
        --log-file $OUT/launches.csv python bench.py --steps 3 --warmup 3 --no-cpu-baseline --e2e-steps 0 > $OUT/ncu_bench.log 2>&1 ;;
 full) timeout 1200 ncu --set full --clock-control none --import-source on -k regex:k_interact -s 2 -c 1 \
        -o $OUT/interact python bench.py --steps 1 --warmup 3 --no-cpu-baseline --e2e-steps 0 > $OUT/ncu_full.log 2>&1 ;;
+nlsu) timeout 1200 ncu --set full --clock-control none --import-source on \
+       -k "regex:k_reorder|k_integrate|k_radix|k_cell_keys|k_scan" -s 12 -c 10 \
+       -o $OUT/nlsu python bench.py --steps 1 --warmup 3 --no-cpu-baseline --e2e-steps 0 > $OUT/ncu_nlsu.log 2>&1 ;;
 esac; done
 ls -la $OUT
