@@ -57,7 +57,10 @@ template <typename R>
 struct Cfg;
 template <>
 struct Cfg<float> {
-  static constexpr int SCAP = 2304;  // staged candidates (A, B float4 [+ x/y/z FP16 copies])
+#ifndef V8_SCAP
+#define V8_SCAP 2304
+#endif
+  static constexpr int SCAP = V8_SCAP;  // staged candidates (A, B float4 [+ x/y/z FP16 copies])
   static constexpr int NARR = 2;
   static constexpr int H16 = SPHB_H16;
 };
@@ -950,12 +953,14 @@ struct Acc32 {
   float vd;
 };
 
-constexpr int V8_ROWS = 2304 + 8;  // staged rows: SCAP candidates + the dummy (row SCAP)
+constexpr int V8_ROWS = V8_SCAP + 8;  // staged rows: SCAP candidates + the dummy (row SCAP)
 // dynamic shared memory of k_interact_v8: A rows | B rows | screen records (8 B) | 64 B of
 // zeros (B fragments of the K = 4..7 lanes) | FIFO
-constexpr int V8_RING = 20;
+#ifndef V8_RING
+#define V8_RING 20
+#endif
 constexpr int V8_REC_OFF = 32 * V8_ROWS;
-constexpr int V8_ZERO_OFF = V8_REC_OFF + 8 * 2304;
+constexpr int V8_ZERO_OFF = V8_REC_OFF + 8 * V8_SCAP;
 constexpr int V8_FIFO_OFF = V8_ZERO_OFF + 64;
 constexpr int V8_SMEM = V8_FIFO_OFF + 8 * NW * V8_RING * 32;
 // tensor-core screen: D = |x_j|^2 - 2 x_i.x_j + (|x_i|^2 - thr) in units of (2h)^2 from FP16
@@ -963,10 +968,11 @@ constexpr int V8_SMEM = V8_FIFO_OFF + 8 * NW * V8_RING * 32;
 // at the cutoff and the FP16 |x_j|^2 by <= 7.8e-3, so thr = 1.02 never drops a true hit
 constexpr float MMA_THR = 1.02f;
 #ifndef V8_NG
-#define V8_NG 3    // candidate pairs per lane per drain iteration (independent FP32x2 chains)
+#define V8_NG 2    // candidate pairs per lane per drain iteration (independent FP32x2 chains;
+                   // 2 beat 3 by ~1% at C3: 185 vs 217 registers)
 #endif
 #ifndef V8_KMIN
-#define V8_KMIN 6  // minimum iterations of a partial drain
+#define V8_KMIN 8  // minimum iterations of a partial drain
 #endif
 // a partial drain pops >= 2 NG KMIN maybes per busy lane, i.e. frees at least its oldest word
 static_assert(2 * V8_NG * V8_KMIN >= 32, "partial drains must free a FIFO entry");
@@ -1124,7 +1130,10 @@ __device__ __forceinline__ void eval_v8(const KArgs& a, const K32& c, const Own3
 }
 
 template <bool G7, bool EQM, bool WEND>
-__global__ void __launch_bounds__(NW * 32, 2) k_interact_v8(KArgs a, K32 k32) {
+#ifndef V8_MINB
+#define V8_MINB 2  // CTAs per SM: shared memory (V8_SMEM) and registers allow 2
+#endif
+__global__ void __launch_bounds__(NW * 32, V8_MINB) k_interact_v8(KArgs a, K32 k32) {
   if (!step_live(a.ctrl)) return;
   constexpr int SCAP = Cfg<float>::SCAP;
   constexpr int RINGC = V8_RING;                          // FIFO entries per lane (8 B)
