@@ -42,7 +42,10 @@ using namespace sphb;
 
 namespace {
 
-constexpr int NW = 4;            // warps per CTA (two CTAs per SM)
+#ifndef SPHB_NW
+#define SPHB_NW 4
+#endif
+constexpr int NW = SPHB_NW;      // warps per CTA (two CTAs per SM)
 constexpr int BT = NW * 32;      // targets per block
 #ifndef SPHB_H16
 #define SPHB_H16 1
