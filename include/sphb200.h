@@ -89,6 +89,11 @@ typedef struct {
   int64_t piston_id0, piston_id1; /* boundary particles with id in [id0, id1) follow the
                                      piston x(t) = x0 + S/2 (1 - cos 2 pi t/T); id0 == id1: none */
   double piston_x0, piston_stroke, piston_period;
+  /* repulsive boundary force (Monaghan 1994 Lennard-Jones form), per unit mass, on fluid
+   * particles from boundary particles closer than wall_r0 (<= 2h):
+   *   a_i += wall_d ((r0/r)^p1 - (r0/r)^p2) r_ij / r^2;  wall_d == 0: none (the reference) */
+  double wall_d, wall_r0;
+  int32_t wall_p1, wall_p2;
 } sphb_params_t;
 
 enum { SPHB_KERNEL_CUBIC = 0, SPHB_KERNEL_WENDLAND = 1 };

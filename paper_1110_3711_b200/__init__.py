@@ -9,7 +9,7 @@ raise.
 """
 from .config import EngineConfig, ForceOutput
 from .engine import B200Engine, compute_forces_cellpairs, compute_forces_gather, make_engine
-from .model import (DerivedQuantities, ParticleKind, ParticleSystem, PistonMotion, SimParams,
+from .model import (BoundaryForce, DerivedQuantities, ParticleKind, ParticleSystem, PistonMotion, SimParams,
                     StepStats, validate)
 from .scenario import (Scenario, WaveTank, build_dam_break, build_wave_tank, make_params,
                        make_wave_tank_params, named_scenario)
@@ -22,5 +22,5 @@ __all__ = [
     "compute_forces_cellpairs", "DerivedQuantities", "ParticleKind", "ParticleSystem",
     "SimParams", "StepStats", "validate", "Scenario", "build_dam_break", "make_params",
     "named_scenario", "run_simulation", "DivergenceError", "compute_derived", "__version__",
-    "PistonMotion", "WaveTank", "build_wave_tank", "make_wave_tank_params",
+    "PistonMotion", "BoundaryForce", "WaveTank", "build_wave_tank", "make_wave_tank_params",
 ]

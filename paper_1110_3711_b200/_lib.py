@@ -36,7 +36,8 @@ class ParamsDesc(ctypes.Structure):
                 ("verlet_stride", c_i32), ("order", c_i32), ("precision", c_i32),
                 ("kernel", c_i32), ("integrator", c_i32), ("pad_", c_i32),
                 ("piston_id0", c_i64), ("piston_id1", c_i64), ("piston_x0", c_f64),
-                ("piston_stroke", c_f64), ("piston_period", c_f64)]
+                ("piston_stroke", c_f64), ("piston_period", c_f64),
+                ("wall_d", c_f64), ("wall_r0", c_f64), ("wall_p1", c_i32), ("wall_p2", c_i32)]
 
 
 class StateDesc(ctypes.Structure):

@@ -59,6 +59,13 @@ static int check_params(const sphb_params_t* p) {
     return sphb_set_error(SPHB_E_INVALID, "integrator must be SPHB_INT_VERLET or SPHB_INT_SYMPLECTIC");
   if (p->precision != SPHB_FP32 && p->precision != SPHB_FP64)
     return sphb_set_error(SPHB_E_INVALID, "precision must be SPHB_FP32 or SPHB_FP64");
+  if (!(p->wall_d >= 0.0)) return sphb_set_error(SPHB_E_INVALID, "wall_d must be >= 0");
+  if (p->wall_d > 0.0) {
+    if (!(p->wall_r0 > 0.0 && p->wall_r0 <= 2.0 * p->h))
+      return sphb_set_error(SPHB_E_INVALID, "wall_r0 must lie in (0, 2h]");
+    if (!(p->wall_p2 >= 1 && p->wall_p1 > p->wall_p2 && p->wall_p1 <= 16))
+      return sphb_set_error(SPHB_E_INVALID, "wall exponents need 1 <= p2 < p1 <= 16");
+  }
   return SPHB_OK;
 }
 

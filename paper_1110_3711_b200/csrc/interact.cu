@@ -1701,6 +1701,76 @@ int launch_one(const KArgs& a, int nsm, cudaStream_t s) {
   }
 }
 
+// ------------------------------------------------------------------ boundary repulsion
+// Extension (off by default): Monaghan's (1994) Lennard-Jones wall
+// force per unit mass on fluid targets from boundary particles closer than r0 (<= 2h, so the
+// interaction stencil holds them all):  a_i += D ((r0/r)^p1 - (r0/r)^p2) r_ij / r^2.  f64,
+// added to the PI accelerations; the fluid dt term sqrt(h / |a + g|) of every target it
+// touches joins the minimum (the SPH-only term is already in it: dt stays conservative).
+__device__ __forceinline__ double ipow(double q, int k) {
+  double r = 1.0;
+  for (int e = 0; e < k; ++e) r = xmul(r, q);
+  return r;
+}
+
+__global__ void __launch_bounds__(256) k_wall_force(sphb_params_t p, sphb_grid_t g, int64_t n,
+                                                    int64_t nb, int64_t ncells,
+                                                    const float4* __restrict__ posp,
+                                                    const int32_t* __restrict__ cell,
+                                                    const int32_t* __restrict__ beg,
+                                                    const int32_t* __restrict__ end,
+                                                    double* __restrict__ acc, sphb_ctrl_t* ctrl) {
+  if (!step_live(ctrl)) return;
+  (void)ncells;
+  const int nx = g.dims[0], ny = g.dims[1], nz = g.dims[2], R = g.reach;
+  const double r02 = xmul(p.wall_r0, p.wall_r0);
+  double dtf_min = INFINITY;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = nb + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const int c = cell[i];
+    const int cx = c % nx, cy = (c / nx) % ny, cz = c / (nx * ny);
+    if (cx < g.tx0 || cx >= g.tx1) continue;
+    const float4 pi = posp[i];
+    const int x0 = max(cx - R, 0), x1 = min(cx + R, nx - 1);
+    double fx = 0.0, fy = 0.0, fz = 0.0;
+    bool hit = false;
+    for (int z = max(cz - R, 0); z <= min(cz + R, nz - 1); ++z) {
+      for (int y = max(cy - R, 0); y <= min(cy + R, ny - 1); ++y) {
+        const int64_t row = ((int64_t)z * ny + y) * nx;
+        const int32_t j1 = end[row + x1];  // boundary list: the first ncells entries
+        for (int32_t j = beg[row + x0]; j < j1; ++j) {
+          const float4 pj = posp[j];
+          const double dx = xsub((double)pi.x, (double)pj.x);
+          const double dy = xsub((double)pi.y, (double)pj.y);
+          const double dz = xsub((double)pi.z, (double)pj.z);
+          const double r2 = xadd(xadd(xmul(dx, dx), xmul(dy, dy)), xmul(dz, dz));
+          if (!(r2 > 0.0 && r2 < r02)) continue;
+          const double q = xdiv(p.wall_r0, __dsqrt_rn(r2));
+          const double f = xdiv(xmul(p.wall_d, xsub(ipow(q, p.wall_p1), ipow(q, p.wall_p2))), r2);
+          fx = xadd(fx, xmul(f, dx));
+          fy = xadd(fy, xmul(f, dy));
+          fz = xadd(fz, xmul(f, dz));
+          hit = true;
+        }
+      }
+    }
+    if (!hit) continue;
+    const double ax = xadd(acc[3 * i + 0], fx), ay = xadd(acc[3 * i + 1], fy),
+                 az = xadd(acc[3 * i + 2], fz);
+    acc[3 * i + 0] = ax;
+    acc[3 * i + 1] = ay;
+    acc[3 * i + 2] = az;
+    const double gx = xadd(ax, p.g[0]), gy = xadd(ay, p.g[1]), gz = xadd(az, p.g[2]);
+    double fmag = __dsqrt_rn(xadd(xadd(xmul(gx, gx), xmul(gy, gy)), xmul(gz, gz)));
+    fmag = fmag > 1e-30 ? fmag : 1e-30;
+    dtf_min = fmin(dtf_min, __dsqrt_rn(xdiv(p.h, fmag)));
+    if (!(isfinite(ax) && isfinite(ay) && isfinite(az)))
+      raise_div(ctrl, ctrl->step, SPHB_DIV_NONFINITE_FORCES, 0);
+  }
+  dtf_min = warp_min(dtf_min);
+  if ((threadIdx.x & 31) == 0 && dtf_min < INFINITY) atomic_min_pos(&ctrl->dtmin_f, dtf_min);
+}
+
 }  // namespace
 
 int64_t interact_launch_count(int64_t n) {
@@ -1761,5 +1831,9 @@ int launch_interact(sphb_workspace* ws, const sphb_params_t& p, const sphb_grid_
   // one launch for both item classes: fluid targets (F-F + F-B) and boundary targets (B-F,
   // drho + visc only) of the same cells share the staged candidates
   a.blocks = ws->blocks;
-  return p.precision == SPHB_FP64 ? launch_one<double>(a, nsm, s) : launch_one<float>(a, nsm, s);
+  const int rc = p.precision == SPHB_FP64 ? launch_one<double>(a, nsm, s) : launch_one<float>(a, nsm, s);
+  if (rc || !(p.wall_d > 0.0) || n <= nb) return rc;
+  k_wall_force<<<(unsigned)std::min<int64_t>((n - nb + 255) / 256, 148 * 16), 256, 0, s>>>(
+      p, g, n, nb, a.ncells, posp, cell_sorted, beg, end, acc, ctrl);
+  return sphb_check_launch("k_wall_force");
 }

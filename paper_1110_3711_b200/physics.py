@@ -73,6 +73,10 @@ def params_desc(params, mass_fluid: float, mass_boundary: float, order: int = 0,
     if pm is not None:
         d.piston_id0, d.piston_id1 = int(pm.id0), int(pm.id1)
         d.piston_x0, d.piston_stroke, d.piston_period = float(pm.x0), float(pm.stroke), float(pm.period)
+    bf = getattr(params, "boundary_force", None)
+    if bf is not None:
+        d.wall_d, d.wall_r0 = float(bf.d), float(bf.r0)
+        d.wall_p1, d.wall_p2 = int(bf.p1), int(bf.p2)
     return d
 
 

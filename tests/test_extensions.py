@@ -187,3 +187,50 @@ def test_wave_tank_piston_follows_law():
     assert np.array_equal(pos[other], s0.pos[other]) and np.all(vel[other] == 0)
     fluid = np.arange(s0.count_boundary, s0.n)
     assert vel[fluid, 0].mean() > 0  # the piston pushes the water layer
+
+
+# ------------------------------------------------------------------ repulsive boundary force
+@pytest.mark.parametrize("frame", ["frame_small_n1.npz", "frame_c1mid_n1.npz"])
+def test_boundary_force_matches_restatement(frame):
+    """accel(with) - accel(without) == oracle.wall_accel (f64 restatement); boundary rows
+    stay 0, counters and drho/visc are untouched; FP32 adds the same f64 term."""
+    import types
+    z = golden(frame)
+    p0 = oracle.params_from_npz(z)
+    kw = dict(h=p0.h, dp=p0.dp, rho0=p0.rho0, c0=p0.c0, gamma=p0.gamma, alpha=p0.alpha, g=p0.g,
+              cfl=p0.cfl, domain_min=p0.domain_min, domain_max=p0.domain_max, n_subdiv=p0.n_subdiv)
+    r0, d = 1.5 * p0.dp, 5.0 * 9.81 * 0.15
+    plain = sph.SimParams(**kw)
+    walled = sph.SimParams(**kw, boundary_force=sph.BoundaryForce(d=d, r0=r0))
+    nb, nf = int(z["s_nb"]), int(z["s_nf"])
+    system = sph.ParticleSystem(count_fluid=nf, count_boundary=nb, pos=z["s_pos"], vel=z["s_vel"],
+                                rho=z["s_rho"], mass_fluid=float(z["s_mass_fluid"]),
+                                mass_boundary=float(z["s_mass_boundary"]), ptype=z["s_ptype"],
+                                id=z["s_id"])
+    derived = sph.compute_derived(z["s_rho"], plain)
+    grid = types.SimpleNamespace(cell_of=z["cell_of"], dims=z["dims"])
+    ref = oracle.wall_accel(z["s_pos"], nb, r0, d)
+    assert np.count_nonzero(ref[nb:, 0] != 0.0) > 0  # the frame has fluid within r0 of a wall
+    for precision in ("fp64", "fp32"):
+        eng = sph.make_engine(cfg(precision))
+        a = eng.compute(system, derived, grid, types.SimpleNamespace(), plain)
+        b = eng.compute(system, derived, grid, types.SimpleNamespace(), walled)
+        assert np.all(b.accel[:nb] == 0.0)
+        assert np.array_equal(a.drho_dt, b.drho_dt) and np.array_equal(a.visc_dt, b.visc_dt)
+        assert (a.stats.true_pairs, a.stats.force_evals) == (b.stats.true_pairs, b.stats.force_evals)
+        scale = max(np.abs(ref).max(), np.abs(a.accel).max())
+        assert np.abs((b.accel - a.accel) - ref).max() <= 1e-12 * scale, precision
+
+
+def test_boundary_force_keeps_fluid_off_the_floor():
+    sc, prm, _ = small_system(0.02)
+    wall = sph.BoundaryForce(d=5.0 * 9.81 * sc.fill_height, r0=prm.dp)
+    prm_w = dataclasses.replace(prm, boundary_force=wall)
+    s0, st0 = sph.run_simulation(sc, prm, cfg(), max_steps=150)
+    s1, st1 = sph.run_simulation(sc, prm_w, cfg(), max_steps=150)
+    nb = s1.count_boundary
+    assert np.isfinite(s1.pos).all()
+    # the repulsion only pushes fluid away from walls: the lowest fluid particle is not lower
+    assert s1.pos[nb:, 2].min() >= s0.pos[nb:, 2].min() - 1e-6
+    # dt stays conservative: the SPH-only fluid term is still in the minimum
+    assert all(b.dt <= a.dt * (1 + 1e-12) for a, b in zip(st0[:1], st1[:1]))

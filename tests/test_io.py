@@ -143,3 +143,25 @@ def test_symplectic_restatement_free_motion():
     assert np.array_equal(v2, vel) and np.array_equal(r2, rho)
     np.testing.assert_allclose(p2[1], pos[1] + dt * vel[1], rtol=0, atol=1e-7)
     assert np.array_equal(p2[0], pos[0])  # boundary row untouched
+
+
+def test_boundary_force_validation_and_restatement():
+    import oracle
+    sc = sph.Scenario(dp=0.02)
+    prm = sph.make_params(sc)
+    for bad in (sph.BoundaryForce(d=0.0, r0=0.01), sph.BoundaryForce(d=1.0, r0=3 * prm.h),
+                sph.BoundaryForce(d=1.0, r0=0.01, p1=4, p2=4)):
+        with pytest.raises(ValueError, match="boundary force"):
+            sph.make_params(sc, boundary_force=bad)
+    from paper_1110_3711_b200.physics import params_desc
+    d = params_desc(sph.make_params(sc, boundary_force=sph.BoundaryForce(d=2.0, r0=0.01)), 1.0, 1.0, 0, 0)
+    assert (d.wall_d, d.wall_r0, d.wall_p1, d.wall_p2) == (2.0, 0.01, 12, 4)
+    assert params_desc(prm, 1.0, 1.0, 0, 0).wall_d == 0.0  # off by default: the reference
+    # one pair at r = 0.8 r0 along x: analytic Lennard-Jones magnitude, repulsive (+x)
+    pos = np.array([[0.0, 0.0, 0.0], [0.008, 0.0, 0.0]], np.float32)
+    a = oracle.wall_accel(pos, 1, 0.01, 2.0)
+    r = float(np.float32(0.008))
+    assert a[0].tolist() == [0.0, 0.0, 0.0]
+    assert abs(a[1, 0] - 2.0 * ((0.01 / r) ** 12 - (0.01 / r) ** 4) / r) < 1e-9 * a[1, 0] and a[1, 0] > 0
+    bf = sph.BoundaryForce(d=2.0, r0=0.01)
+    assert abs(bf.accel(np.array([r, 0.0, 0.0]), np.array(r * r))[0] - a[1, 0]) < 1e-9 * a[1, 0]
