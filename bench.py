@@ -47,7 +47,9 @@ def parse():
                     help="c1|c2|c3|c4_1..c4_8|c5 (default c3 at N=1, c3w_N above)")
     ap.add_argument("--n-subdiv", type=int, default=1)
     ap.add_argument("--precision", default="fp32", choices=["fp32", "fp64"])
-    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-steps", type=int, default=6)
+    ap.add_argument("--e2e-chunks", type=int, default=8,
+                    help="row chunks of the pipelined H2D/D2H state round trip (1 = serial)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget-s", type=float, default=20.0)
     ap.add_argument("--slab-path", action="store_true",
@@ -375,6 +377,10 @@ def main():
     nlsu_gbs = BYTES_NL_SU * system.n / (nl_su_ms * 1e-3) / 1e9
 
     # ---- e2e: the same step through the C ABI with HOST buffers (H2D state in, D2H state out)
+    # Every step copies its input state H2D from pinned host memory and its result state D2H.
+    # The round trip is pipelined in row chunks over the full-duplex PCIe link: the H2D of
+    # chunk c for step k+1 starts as soon as the D2H of chunk c of step k has landed (copy
+    # streams + events), so the two directions overlap instead of running back to back.
     h2d = d2h = 0
     e2e_value = None
     if args.e2e_steps > 0:
@@ -384,20 +390,48 @@ def main():
         for hbuf, dbuf in zip(hosts, (sim.posp, sim.velr, sim.prev)):
             hbuf.copy_(dbuf[:n])
         hid.copy_(sim.id[:n])
-        dev_bufs = (sim.posp, sim.velr, sim.prev)
-        h2d = d2h = sum(h.numel() * h.element_size() for h in hosts) + hid.numel() * 8
+        pairs = list(zip(hosts + [hid], [sim.posp, sim.velr, sim.prev, sim.id]))
+        h2d = d2h = sum(h.numel() * h.element_size() for h, _ in pairs)
+        nchunk = max(1, min(args.e2e_chunks, n))
+        bounds = [(n * c // nchunk, n * (c + 1) // nchunk) for c in range(nchunk)]
+        comp = torch.cuda.current_stream()
+        s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
+        ev_in = [torch.cuda.Event() for _ in bounds]
+        ev_out = [torch.cuda.Event() for _ in bounds]
+        ev_step = torch.cuda.Event()
+
+        def h2d_chunk(c):
+            lo, hi = bounds[c]
+            for hbuf, dbuf in pairs:
+                dbuf[lo:hi].copy_(hbuf[lo:hi], non_blocking=True)
+
         torch.cuda.synchronize()
         a, b = Ev(), Ev()
         a.record()
-        for _ in range(args.e2e_steps):
-            for hbuf, dbuf in zip(hosts, dev_bufs):
-                dbuf[:n].copy_(hbuf, non_blocking=True)
-            sim.id[:n].copy_(hid, non_blocking=True)
+        s_in.wait_stream(comp)
+        with torch.cuda.stream(s_in):
+            for c in range(nchunk):
+                h2d_chunk(c)
+                ev_in[c].record(s_in)
+        for k in range(args.e2e_steps):
+            for c in range(nchunk):
+                comp.wait_event(ev_in[c])
             sim.first_keys_resync()
             sim.launch_step()
-            for hbuf, dbuf in zip(hosts, dev_bufs):
-                hbuf.copy_(dbuf[:n], non_blocking=True)
-            hid.copy_(sim.id[:n], non_blocking=True)
+            ev_step.record(comp)
+            s_out.wait_event(ev_step)
+            with torch.cuda.stream(s_out):
+                for c, (lo, hi) in enumerate(bounds):
+                    for hbuf, dbuf in pairs:
+                        hbuf[lo:hi].copy_(dbuf[lo:hi], non_blocking=True)
+                    ev_out[c].record(s_out)
+            if k + 1 < args.e2e_steps:
+                with torch.cuda.stream(s_in):
+                    for c in range(nchunk):
+                        s_in.wait_event(ev_out[c])
+                        h2d_chunk(c)
+                        ev_in[c].record(s_in)
+        comp.wait_stream(s_out)
         b.record()
         torch.cuda.synchronize()
         e2e_ms = a.elapsed_time(b)
@@ -440,7 +474,9 @@ def main():
     if e2e_value is not None:
         line["e2e"] = {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
                        "d2h_bytes_per_step": d2h, "steps": args.e2e_steps,
-                       "path": "per step: pinned host state -> H2D -> sphb_* step -> D2H state"}
+                       "path": "per step: pinned host state -> H2D -> sphb_* step -> D2H state, "
+                               f"round trip pipelined in {args.e2e_chunks} row chunks over "
+                               "full-duplex PCIe (H2D of step k+1 chunk c after D2H of step k chunk c)"}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cb = cpu_reference(system, prm, args.n_subdiv, args.cpu_budget_s)
         cb.pop("step_s", None)
