@@ -83,6 +83,22 @@ def traffic_for(cfg_name):
         return None, None
 
 
+def composite_roofline(n, cand, evals, hbm_gbs, fp32_tflops, ms_step):
+    """the step's floor = sum over kernels of max(bytes/BW, flop/P_fp32,
+    mufu/P_mufu): NL+SU bytes at the measured HBM bandwidth, PI at max(FP32, MUFU) with
+    4 MUFU per evaluated pair (measured MUFU.RSQ peak, profiles/peaks_r01.json)."""
+    try:
+        mufu = json.load(open(os.path.join(ROOT, "profiles", "peaks_r01.json")))["mufu_rsqrt_tops"]
+    except Exception:
+        mufu = 4.55
+    t_mem = BYTES_NL_SU * n / (hbm_gbs * 1e9) * 1e3
+    t_fp32 = (FLOP_PER_CAND * cand + FLOP_PER_EVAL * evals) / (fp32_tflops * 1e12) * 1e3
+    t_mufu = 4.0 * evals / (mufu * 1e12) * 1e3
+    floor = t_mem + max(t_fp32, t_mufu)
+    return {"floor_ms": floor, "nl_su_hbm_ms": t_mem, "pi_fp32_ms": t_fp32, "pi_mufu_ms": t_mufu,
+            "frac": floor / ms_step}
+
+
 def scenario_kind(sc) -> str:
     import paper_1110_3711_b200 as sph
     return "3-D piston wave tank" if isinstance(sc, sph.WaveTank) else "3-D dam break"
@@ -468,6 +484,7 @@ def main():
                                "frac": nlsu_gbs / hbm, "traffic": None,
                                "work": f"{BYTES_NL_SU} B/particle-step over NL+SU stages",
                                "peak_source": hbm_src},
+        "roofline_composite": composite_roofline(system.n, cand, evals, hbm, fp32, ms_step),
         "gpu_launches": launches,
         "clocks": clk,
     }
