@@ -316,10 +316,11 @@ __global__ void __launch_bounds__(SCAN_BLOCK) k_scan_apply(uint32_t* __restrict_
   for (int k = 0; k < SCAN_ITEMS; ++k) {
     const int64_t x = base + k;
     if (x < len) {
-      if (movers) {
+      if (mv.kv) {
+        // chains are reset whatever the mode (k_mv_compact may have switched to the radix)
         const int32_t ob = beg[x], oe = end[x], h = mv.head[x];
         if (h >= 0) mv.head[x] = -1;
-        if (c[k] != 0u) {
+        if (movers && c[k] != 0u) {
           const int32_t mob = M(ob);
           mv.kv[x] = make_int4((int32_t)ex - ob + mob,
                                (int32_t)ex + (oe - ob) - (M(oe) - mob), ob, h);
@@ -440,7 +441,8 @@ __global__ void __launch_bounds__(MV_BLOCK) k_mv_compact(
     const uint32_t* __restrict__ keys, int cellbits, uint32_t ncells,
     const uint32_t* __restrict__ bits, const uint32_t* __restrict__ tile_pre,
     uint32_t* __restrict__ wpre, int32_t* __restrict__ mv_pos,
-    int32_t* __restrict__ mv_next, int32_t* __restrict__ mv_head, const uint32_t* state,
+    int32_t* __restrict__ mv_next, int32_t* __restrict__ mv_head, const uint32_t* __restrict__ prev,
+    const int32_t* __restrict__ obeg, const int32_t* __restrict__ oend, uint32_t* state,
     const sphb_ctrl_t* ctrl) {
   if (!step_live(ctrl) || state[2] != 0u) return;
   __shared__ uint32_t s_w[32], s_pre[32];
@@ -470,8 +472,13 @@ __global__ void __launch_bounds__(MV_BLOCK) k_mv_compact(
       const int64_t i = (int64_t)blockIdx.x * MV_TILE + r * MV_BLOCK + threadIdx.x;
       const int32_t j = (int32_t)(s_pre[wi] + __popc(w & lt));
       const uint32_t k = keys[i];
+      const uint32_t x = mv_index(k, cellbits, ncells);
       mv_pos[j] = (int32_t)i;
-      mv_next[j] = atomicExch(&mv_head[mv_index(k, cellbits, ncells)], j);
+      mv_next[j] = atomicExch(&mv_head[x], j);
+      // a key absent from the previous order must have an empty old range (the run check of
+      // k_mv_flag covers the keys present); otherwise fall back to the radix passes
+      const int32_t ob = obeg[x];
+      if (ob < oend[x] && prev[ob] != k) state[2] = 1u;
     }
   }
 }
@@ -593,7 +600,8 @@ int launch_sort_and_ranges(sphb_workspace* ws, const sphb_grid_t& g, const uint3
   k_mv_scan<<<1, 1024, 0, s>>>(ws->mv_tile, tiles, ws->mover_cap, st, ctrl);
   k_mv_compact<<<(unsigned)tiles, MV_BLOCK, 0, s>>>(keys, cb, (uint32_t)nc, ws->mv_bits, ws->mv_tile,
                                                     ws->mv_wpre, ws->mv_pos,
-                                                    ws->mv_next, ws->mv_head, st, ctrl);
+                                                    ws->mv_next, ws->mv_head, keys_sorted, beg,
+                                                    end, st, ctrl);
   // K4 for this step, keeping the previous ranges for the scatter
   k_scan_reduce<<<(unsigned)nscan, SCAN_BLOCK, 0, s>>>(ws->cnt, len, ws->scan_partials, ctrl);
   k_scan_partials<<<1, 1024, 0, s>>>(ws->scan_partials, nscan, ctrl);

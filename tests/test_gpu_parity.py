@@ -11,6 +11,7 @@ pinned to them (oracle/, tests/test_oracle.py), and reference-measured counts at
 import types
 
 import numpy as np
+import torch
 import pytest
 
 import oracle
@@ -342,6 +343,38 @@ def test_movers_only_sort_matches_radix():
     assert all(m == int(mv > 40) for mv, m in modes[2][1:])  # the cap decides per step
     fa, fb = sims[0].download(), sims[1].download()
     for x, y in zip(fa, fb):
+        assert np.array_equal(x, y)
+
+
+def test_movers_only_sort_rejects_an_inconsistent_previous_order():
+    """sphb_sort_ranges trusts keys_sorted / beg / end only after checking them on the device:
+    corrupted, the step falls back to the radix passes and still sorts correctly."""
+    sc = sph.named_scenario("c1")
+    prm = sph.make_params(sc)
+    system = sph.build_dam_break(sc, prm)
+    a = D.DeviceSim(system, prm, reach=1, precision=0)
+    b = D.DeviceSim(system, prm, reach=1, precision=0)
+    b.ws.set_mover_cap(-1)
+    for _ in range(5):
+        a.launch_step()
+        b.launch_step()
+    n = a.n
+    for corrupt in ("swap", "range"):
+        if corrupt == "swap":  # keys_sorted no longer ascending
+            ks = a.keys_sorted[:n].clone()
+            a.keys_sorted[:1] = ks[n - 1:n]
+            a.keys_sorted[n - 1:n] = ks[:1]
+        else:  # a present key's old range shifted by one row
+            nz = torch.nonzero(a.end - a.beg > 1).flatten()
+            a.beg[int(nz[len(nz) // 2])] += 1
+        a.launch_step()
+        b.launch_step()
+        assert a.ws.sort_info()[1] == 1, corrupt  # radix fallback
+        assert np.array_equal(a.perm[:n].cpu().numpy(), b.perm[:n].cpu().numpy()), corrupt
+        a.launch_step()
+        b.launch_step()
+        assert a.ws.sort_info()[1] == 0  # the fallback re-established the order
+    for x, y in zip(a.download(), b.download()):
         assert np.array_equal(x, y)
 
 
