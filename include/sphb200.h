@@ -177,7 +177,10 @@ int sphb_sort_ranges(sphb_workspace_t* ws, const sphb_grid_t* grid, const uint32
 /* K3 -- reorder gathers (grid.py:111-114) fused with compute_derived (physics.py:96-110):
  * *_out[i] = *_in[perm[i]] for posp, velr, prev, id; posp_out.w = prrho; aux_out = (press,
  * csound, tensil, list mass);
- * cell_out[i] = cell of the sorted key.  prev_in/prev_out/id may be NULL. */
+ * cell_out[i] = cell of the sorted key.  prev_in/prev_out/id may be NULL.
+ * The derived values are the reference's (f64 pow, f32-rounded, bit-identical) for
+ * prm->precision == SPHB_FP64; SPHB_FP32 with gamma = 7 evaluates (rho/rho0)^7 and ^3 by
+ * multiplication (press / csound within 1 f32 ulp; the FP32 force tolerance is 1e-5). */
 int sphb_reorder(const sphb_params_t* prm, const sphb_grid_t* grid, int64_t n,
                  const int32_t* perm, const uint32_t* keys_sorted, const void* posp_in,
                  const void* velr_in, const void* prev_in, const int64_t* id_in, void* posp_out,

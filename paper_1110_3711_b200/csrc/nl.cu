@@ -213,6 +213,11 @@ __global__ void __launch_bounds__(SORT_BLOCK) k_radix_scatter(
 #ifndef NL_MINB
 #define NL_MINB 4  // 64 registers: 2x the resident warps of the default (memory-bound kernel)
 #endif
+// FAST (FP32 precision with gamma = 7, the reference default): x^7 and x^3 by multiplication
+// instead of two f64 pow calls -- press/csound then differ from the reference's pow in the
+// last f32 bit at most, far inside the FP32 tolerance, and the kernel keeps all loads in
+// flight (no calls).  The FP64 precision keeps pow: its results are bit-identical.
+template <bool FAST>
 __global__ void __launch_bounds__(256, NL_MINB) k_reorder(
     sphb_params_t p, uint32_t cellmask, int cellbits, int64_t n, const int32_t* __restrict__ perm,
     const uint32_t* __restrict__ keys_sorted, const float4* __restrict__ posp_in,
@@ -222,23 +227,41 @@ __global__ void __launch_bounds__(256, NL_MINB) k_reorder(
     int32_t* __restrict__ cell_out, const sphb_ctrl_t* ctrl) {
   if (!step_live(ctrl)) return;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const double inv_rho0 = 1.0 / p.rho0;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
-    int32_t o = perm ? perm[i] : (int32_t)i;
+    const int32_t o = perm ? perm[i] : (int32_t)i;
+    const uint32_t ks = keys_sorted ? keys_sorted[i] : 0u;
     float4 pp = posp_in[o];
-    float4 vr = velr_in[o];
-    double rho = (double)vr.w;
-    float press = eos_press(rho, p.tait_b, p.rho0, p.gamma);
-    Derived d = derive((double)press, rho, p.c0, p.rho0, p.gamma);
+    const float4 vr = velr_in[o];
+    const bool has_prev = prev_in && prev_out, has_id = id_in && id_out;
+    float4 pv;
+    long long id = 0;
+    if (has_prev) pv = prev_in[o];
+    if (has_id) id = id_in[o];
+    const double rho = (double)vr.w;
+    float press;
+    Derived d;
+    if (FAST) {
+      const double x = rho * inv_rho0, x3 = x * x * x;
+      press = __double2float_rn(p.tait_b * (x3 * x3 * x - 1.0));
+      const double inv_rho2 = 1.0 / (rho * rho);
+      d.prrho = __double2float_rn((double)press * inv_rho2);
+      d.csound = __double2float_rn(p.c0 * x3);
+      d.tensil = __double2float_rn((press > 0.0f ? 0.01 : -0.2) * (double)press * inv_rho2);
+    } else {
+      press = eos_press(rho, p.tait_b, p.rho0, p.gamma);
+      d = derive((double)press, rho, p.c0, p.rho0, p.gamma);
+    }
     // posp.w = prrho: the interaction stages (x, y, z, prrho) rows with one bulk copy
     pp.w = d.prrho;
     posp_out[i] = pp;
     velr_out[i] = vr;
-    const bool boundary = keys_sorted ? ((keys_sorted[i] >> cellbits) & 1u) == 0u : false;
+    const bool boundary = keys_sorted ? ((ks >> cellbits) & 1u) == 0u : false;
     aux_out[i] = make_float4(press, d.csound, d.tensil,
                              (float)(boundary ? p.mass_boundary : p.mass_fluid));
-    if (prev_in && prev_out) prev_out[i] = prev_in[o];
-    if (id_in && id_out) id_out[i] = id_in[o];
-    if (cell_out && keys_sorted) cell_out[i] = (int32_t)(keys_sorted[i] & cellmask);
+    if (has_prev) prev_out[i] = pv;
+    if (has_id) id_out[i] = id;
+    if (cell_out && keys_sorted) cell_out[i] = (int32_t)(ks & cellmask);
   }
 }
 
@@ -622,9 +645,10 @@ int launch_reorder(const sphb_params_t& p, const sphb_grid_t& g, int64_t n, cons
                    int32_t* cell_out, const sphb_ctrl_t* ctrl, cudaStream_t s) {
   if (n == 0) return SPHB_OK;
   uint32_t cellmask = (1u << cellbits_of(g)) - 1u;
-  k_reorder<<<grid_for(n, 256), 256, 0, s>>>(p, cellmask, cellbits_of(g), n, perm, keys_sorted, posp_in, velr_in,
-                                             prev_in, id_in, posp_out, velr_out, prev_out, id_out,
-                                             aux_out, cell_out, ctrl);
+  auto kern = (p.precision == SPHB_FP32 && p.gamma == 7.0) ? k_reorder<true> : k_reorder<false>;
+  kern<<<grid_for(n, 256), 256, 0, s>>>(p, cellmask, cellbits_of(g), n, perm, keys_sorted, posp_in,
+                                        velr_in, prev_in, id_in, posp_out, velr_out, prev_out,
+                                        id_out, aux_out, cell_out, ctrl);
   return sphb_check_launch("k_reorder");
 }
 

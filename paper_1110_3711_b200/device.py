@@ -354,7 +354,7 @@ def compute_derived_device(rho: np.ndarray, params):
         velr[:n, 3] = torch.as_tensor(np.ascontiguousarray(rho, np.float32)).to(dev)
     posp = torch.zeros_like(velr)
     posp_o, velr_o, aux = torch.empty_like(velr), torch.empty_like(velr), torch.empty_like(velr)
-    prm = params_desc(params, 1.0, 1.0)
+    prm = params_desc(params, 1.0, 1.0, precision=_lib.SPHB_FP64)  # the exact (pow) EOS
     g = grid_desc(params)
     ctrl = new_ctrl(dev)
     _lib.check(_lib.lib().sphb_reorder(_lib.ref(prm), _lib.ref(g), n, None, None, _ptr(posp),
