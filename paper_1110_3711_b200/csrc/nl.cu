@@ -378,55 +378,79 @@ __global__ void __launch_bounds__(SCAN_BLOCK) k_scan_apply(uint32_t* __restrict_
 // The radix passes run instead (mode 1) unless the previous order is established (set by a
 // sort, cleared by K1 and the standalone sphb_sort), consistent, and movers <= cap.
 // state words: [0] order established, [1] inconsistency seen, [2] mode (0 movers, 1 radix), [3] m
-constexpr int MV_BLOCK = 256, MV_ITEMS = 4, MV_TILE = MV_BLOCK * MV_ITEMS;  // 32 words per tile
+constexpr int MV_BLOCK = 256, MV_ITEMS = 16, MV_TILE = MV_BLOCK * MV_ITEMS;  // 128 words per tile
 static_assert(MV_TILE == MV_TILE_ROWS, "workspace sizing");
 
 __device__ __forceinline__ uint32_t mv_index(uint32_t key, int cellbits, uint32_t ncells) {
   return (key >> cellbits) * ncells + (key & ((1u << cellbits) - 1u));
 }
 
+// Each thread checks 4 consecutive rows per round (one 16-B load of keys and of keys_sorted
+// when both are 16-B aligned), MV_ITEMS / 4 rounds per tile; the 4-row nibbles of 8 lanes
+// make one bitmap word.
 __global__ void __launch_bounds__(MV_BLOCK) k_mv_flag(const uint32_t* __restrict__ keys,
                                                       const uint32_t* __restrict__ prev, int64_t n,
                                                       int cellbits, uint32_t ncells,
                                                       const int32_t* __restrict__ obeg,
                                                       const int32_t* __restrict__ oend,
                                                       uint32_t* __restrict__ bits,
-                                                      uint32_t* __restrict__ tile_cnt,
+                                                      uint32_t* __restrict__ tile_cnt, bool vec,
                                                       uint32_t* state, const sphb_ctrl_t* ctrl) {
   if (!step_live(ctrl) || state[0] == 0u) return;
   __shared__ uint32_t s_cnt;
   if (threadIdx.x == 0) s_cnt = 0;
   __syncthreads();
-  const int lane = threadIdx.x & 31;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t t0 = (int64_t)blockIdx.x * MV_TILE;
   const uint32_t cm = (1u << cellbits) - 1u;
   auto bad_key = [&](uint32_t k) { return (k >> cellbits) > 1u || (k & cm) >= ncells; };
   bool bad = false;
   uint32_t c = 0;
+  constexpr int RROWS = 4 * MV_BLOCK;  // rows per round
+  for (int r = 0; r < MV_TILE / RROWS; ++r) {
+    const int64_t e0 = t0 + (int64_t)r * RROWS + 4 * threadIdx.x;
+    uint32_t k[4], kp[4];
+    if (vec && e0 + 3 < n) {
+      const uint4 a = reinterpret_cast<const uint4*>(keys)[e0 >> 2];
+      const uint4 b = reinterpret_cast<const uint4*>(prev)[e0 >> 2];
+      k[0] = a.x; k[1] = a.y; k[2] = a.z; k[3] = a.w;
+      kp[0] = b.x; kp[1] = b.y; kp[2] = b.z; kp[3] = b.w;
+    } else {
 #pragma unroll
-  for (int r = 0; r < MV_ITEMS; ++r) {
-    const int64_t i = t0 + r * MV_BLOCK + threadIdx.x;
-    const bool in = i < n;
-    const uint32_t k = in ? keys[i] : 0u, kp = in ? prev[i] : 0u;
-    // consistency of the previous order (keys_sorted, beg, end of the last sort): keys_sorted
-    // ascending and every run of equal keys exactly its [beg, end) -- checked at run ends
-    uint32_t kl = __shfl_up_sync(SPHB_FULL, kp, 1), kr = __shfl_down_sync(SPHB_FULL, kp, 1);
-    if (lane == 0 && in && i > 0) kl = prev[i - 1];
-    if (lane == 31 && i + 1 < n) kr = prev[i + 1];
-    const bool mv = in && k != kp;
-    if (in) {
-      if (bad_key(k) || bad_key(kp)) {
-        bad = true;  // out-of-domain key (the step is aborting) or no previous order
-      } else {
-        const uint32_t x = (kp >> cellbits) * ncells + (kp & cm);
-        if (i == 0 || kl != kp) bad |= (i > 0 && kl > kp) || obeg[x] != (int32_t)i;
-        if (i + 1 == n || kr != kp) bad |= oend[x] != (int32_t)(i + 1);
+      for (int j = 0; j < 4; ++j) {
+        const bool in = e0 + j < n;
+        k[j] = in ? keys[e0 + j] : 0u;
+        kp[j] = in ? prev[e0 + j] : 0u;
       }
     }
-    const uint32_t w = __ballot_sync(SPHB_FULL, mv);
-    if (lane == 0) bits[(t0 + r * MV_BLOCK + threadIdx.x) >> 5] = w;
-    c += __popc(w);
+    // consistency of the previous order (keys_sorted, beg, end of the last sort): keys_sorted
+    // ascending and every run of equal keys exactly its [beg, end) -- checked at run ends
+    uint32_t kl = __shfl_up_sync(SPHB_FULL, kp[3], 1), kr = __shfl_down_sync(SPHB_FULL, kp[0], 1);
+    if (lane == 0 && e0 > 0 && e0 < n) kl = prev[e0 - 1];
+    if (lane == 31 && e0 + 4 < n) kr = prev[e0 + 4];
+    uint32_t nib = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int64_t e = e0 + j;
+      if (e >= n) break;
+      nib |= (k[j] != kp[j] ? 1u : 0u) << j;
+      if (bad_key(k[j]) || bad_key(kp[j])) {
+        bad = true;  // out-of-domain key (the step is aborting) or no previous order
+        continue;
+      }
+      const uint32_t left = j ? kp[j - 1] : kl, right = j < 3 ? kp[j + 1] : kr;
+      const uint32_t x = (kp[j] >> cellbits) * ncells + (kp[j] & cm);
+      if (e == 0 || left != kp[j]) bad |= (e > 0 && left > kp[j]) || obeg[x] != (int32_t)e;
+      if (e + 1 == n || right != kp[j]) bad |= oend[x] != (int32_t)(e + 1);
+    }
+    c += __popc(nib);
+    uint32_t w = nib << (4 * (lane & 7));
+    w |= __shfl_xor_sync(SPHB_FULL, w, 1);
+    w |= __shfl_xor_sync(SPHB_FULL, w, 2);
+    w |= __shfl_xor_sync(SPHB_FULL, w, 4);
+    if ((lane & 7) == 0) bits[((t0 + (int64_t)r * RROWS + warp * 128) >> 5) + (lane >> 3)] = w;
   }
+  c = __reduce_add_sync(SPHB_FULL, c);
   if (lane == 0 && c) atomicAdd(&s_cnt, c);
   if (__any_sync(SPHB_FULL, bad) && lane == 0) atomicOr(&state[1], 1u);
   __syncthreads();
@@ -468,11 +492,13 @@ __global__ void __launch_bounds__(MV_BLOCK) k_mv_compact(
     const int32_t* __restrict__ obeg, const int32_t* __restrict__ oend, uint32_t* state,
     const sphb_ctrl_t* ctrl) {
   if (!step_live(ctrl) || state[2] != 0u) return;
-  __shared__ uint32_t s_w[32], s_pre[32];
+  constexpr int NWORD = MV_TILE / 32;  // bitmap words per tile
+  static_assert(NWORD <= MV_BLOCK, "one word per thread");
+  __shared__ uint32_t s_w[NWORD], s_pre[NWORD], s_wsum[MV_BLOCK / 32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t w0 = (int64_t)blockIdx.x * (MV_TILE / 32);
-  if (warp == 0) {
-    const uint32_t w = bits[w0 + lane];
+  const int64_t w0 = (int64_t)blockIdx.x * NWORD;
+  {  // exclusive prefix of the tile's word popcounts (one word per thread)
+    const uint32_t w = threadIdx.x < NWORD ? bits[w0 + threadIdx.x] : 0u;
     const uint32_t c = __popc(w);
     uint32_t x = c;
 #pragma unroll
@@ -480,10 +506,16 @@ __global__ void __launch_bounds__(MV_BLOCK) k_mv_compact(
       const uint32_t y = __shfl_up_sync(SPHB_FULL, x, o);
       if (lane >= o) x += y;
     }
-    const uint32_t pre = tile_pre[blockIdx.x] + x - c;
-    wpre[w0 + lane] = pre;
-    s_w[lane] = w;
-    s_pre[lane] = pre;
+    if (lane == 31) s_wsum[warp] = x;
+    __syncthreads();
+    uint32_t before = tile_pre[blockIdx.x];
+    for (int k = 0; k < warp; ++k) before += s_wsum[k];
+    if (threadIdx.x < NWORD) {
+      const uint32_t pre = before + x - c;
+      wpre[w0 + threadIdx.x] = pre;
+      s_w[threadIdx.x] = w;
+      s_pre[threadIdx.x] = pre;
+    }
   }
   __syncthreads();
   const uint32_t lt = lanemask_lt();
@@ -506,6 +538,8 @@ __global__ void __launch_bounds__(MV_BLOCK) k_mv_compact(
   }
 }
 
+// 4 rows per thread, 32 apart (loads and stores stay coalesced; the 4 dependent load chains
+// keys -> kv -> chains overlap)
 __global__ void __launch_bounds__(256) k_mv_scatter(
     const uint32_t* __restrict__ keys, int64_t n, int cellbits, uint32_t ncells,
     const uint32_t* __restrict__ bits, const uint32_t* __restrict__ wpre,
@@ -514,20 +548,38 @@ __global__ void __launch_bounds__(256) k_mv_scatter(
     const uint32_t* state, uint32_t* __restrict__ keys_sorted, int32_t* __restrict__ perm,
     const sphb_ctrl_t* ctrl) {
   if (!step_live(ctrl) || state[2] != 0u) return;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
-    const uint32_t k = keys[i];
-    const uint32_t x = mv_index(k, cellbits, ncells);
-    const uint32_t w = bits[i >> 5];
-    const int4 q = kv[x];  // (SB, MB, ob, head)
-    int64_t pos;
-    if (!((w >> (i & 31)) & 1u))
-      pos = (int64_t)q.x + i - (int64_t)(wpre[i >> 5] + __popc(w & ((1u << (i & 31)) - 1u)));
-    else
-      pos = i < q.z ? nbeg[x] : q.y;
-    for (int32_t j = q.w; j >= 0; j = mv_next[j]) pos += mv_pos[j] < i;
-    perm[pos] = (int32_t)i;
-    keys_sorted[pos] = k;
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = (n + 127) >> 7;  // 128-row warp chunks
+  const int64_t wstride = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t cw = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); cw < nw;
+       cw += wstride) {
+    uint32_t k[4], x[4], w[4], wp[4];
+    int4 c[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t i = (cw << 7) + 32 * u + lane;
+      k[u] = i < n ? keys[i] : 0u;
+      w[u] = bits[(cw << 2) + u];
+      wp[u] = wpre[(cw << 2) + u];
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      x[u] = mv_index(k[u], cellbits, ncells);
+      if ((cw << 7) + 32 * u + lane < n) c[u] = kv[x[u]];  // (SB, MB, ob, head)
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t i = (cw << 7) + 32 * u + lane;
+      if (i >= n) break;
+      int64_t pos;
+      if (!((w[u] >> lane) & 1u))
+        pos = (int64_t)c[u].x + i - (int64_t)(wp[u] + __popc(w[u] & ((1u << lane) - 1u)));
+      else
+        pos = i < c[u].z ? nbeg[x[u]] : c[u].y;
+      for (int32_t m = c[u].w; m >= 0; m = mv_next[m]) pos += mv_pos[m] < i;
+      perm[pos] = (int32_t)i;
+      keys_sorted[pos] = k[u];
+    }
   }
 }
 
@@ -618,8 +670,9 @@ int launch_sort_and_ranges(sphb_workspace* ws, const sphb_grid_t& g, const uint3
   const int cb = cellbits_of(g);
   const int64_t tiles = (n + MV_TILE - 1) / MV_TILE;
   uint32_t* st = ws->mv_state;
+  const bool vec = ((reinterpret_cast<uintptr_t>(keys) | reinterpret_cast<uintptr_t>(keys_sorted)) & 15u) == 0;
   k_mv_flag<<<(unsigned)tiles, MV_BLOCK, 0, s>>>(keys, keys_sorted, n, cb, (uint32_t)nc, beg, end,
-                                                 ws->mv_bits, ws->mv_tile, st, ctrl);
+                                                 ws->mv_bits, ws->mv_tile, vec, st, ctrl);
   k_mv_scan<<<1, 1024, 0, s>>>(ws->mv_tile, tiles, ws->mover_cap, st, ctrl);
   k_mv_compact<<<(unsigned)tiles, MV_BLOCK, 0, s>>>(keys, cb, (uint32_t)nc, ws->mv_bits, ws->mv_tile,
                                                     ws->mv_wpre, ws->mv_pos,
@@ -631,9 +684,9 @@ int launch_sort_and_ranges(sphb_workspace* ws, const sphb_grid_t& g, const uint3
   const MvApply mva{ws->mv_kv, ws->mv_head, ws->mv_bits, ws->mv_wpre, st, n};
   k_scan_apply<<<(unsigned)nscan, SCAN_BLOCK, 0, s>>>(ws->cnt, len, ws->scan_partials, beg, end,
                                                       mva, ctrl);
-  k_mv_scatter<<<grid_for(n, 256), 256, 0, s>>>(keys, n, cb, (uint32_t)nc, ws->mv_bits, ws->mv_wpre,
-                                               ws->mv_kv, beg, ws->mv_pos, ws->mv_next, st,
-                                               keys_sorted, perm, ctrl);
+  k_mv_scatter<<<grid_for((n + 3) / 4, 256), 256, 0, s>>>(keys, n, cb, (uint32_t)nc, ws->mv_bits,
+                                                         ws->mv_wpre, ws->mv_kv, beg, ws->mv_pos,
+                                                         ws->mv_next, st, keys_sorted, perm, ctrl);
   radix_passes(ws, g, keys, n, keys_sorted, perm, ctrl, st + 2, s);  // mode 1 only
   return sphb_check_launch("sort + cell ranges");
 }

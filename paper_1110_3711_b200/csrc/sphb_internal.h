@@ -13,7 +13,7 @@ constexpr int RADIX = 1 << RADIX_BITS;
 constexpr int SCAN_BLOCK = 256;
 constexpr int SCAN_ITEMS = 4;
 constexpr int SCAN_TILE = SCAN_BLOCK * SCAN_ITEMS;
-constexpr int MV_TILE_ROWS = 1024;          // rows per movers-only sort tile (32 bitmap words)
+constexpr int MV_TILE_ROWS = 4096;          // rows per movers-only sort tile (128 bitmap words)
 constexpr int64_t MOVER_CAP_MAX = 1 << 16;  // movers per step the movers-only sort accepts
 
 struct sphb_workspace {
