@@ -47,7 +47,7 @@ def parse():
                     help="c1|c2|c3|c4_1..c4_8|c5 (default c3 at N=1, c3w_N above)")
     ap.add_argument("--n-subdiv", type=int, default=1)
     ap.add_argument("--precision", default="fp32", choices=["fp32", "fp64"])
-    ap.add_argument("--e2e-steps", type=int, default=6)
+    ap.add_argument("--e2e-steps", type=int, default=20)
     ap.add_argument("--e2e-chunks", type=int, default=8,
                     help="row chunks of the pipelined H2D/D2H state round trip (1 = serial)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
