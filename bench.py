@@ -424,20 +424,39 @@ def main():
     nlsu_gbs = BYTES_NL_SU * system.n / (nl_su_ms * 1e-3) / 1e9
 
     # ---- e2e: the same step through the C ABI with HOST buffers (H2D state in, D2H state out)
-    # Every step copies its input state H2D from pinned host memory and its result state D2H.
-    # The round trip is pipelined in row chunks over the full-duplex PCIe link: the H2D of
-    # chunk c for step k+1 starts as soon as the D2H of chunk c of step k has landed (copy
-    # streams + events), so the two directions overlap instead of running back to back.
+    # Every step copies its input state H2D from pinned host memory in the reference's own
+    # layout (ParticleSystem pos/vel/rho/id + VerletState vel_prev/rho_prev, 52 B/particle),
+    # converts it to the step's rows (sphb_state_from_soa), steps, converts back
+    # (sphb_state_to_soa) and copies the result state D2H.  The round trip is pipelined in
+    # row chunks over the full-duplex PCIe link: the H2D of chunk c for step k+1 starts as soon
+    # as the D2H of chunk c of step k has landed, and each chunk is converted as it lands.
     h2d = d2h = 0
     e2e_value = None
     if args.e2e_steps > 0:
+        L = _lib.lib()
         n = sim.n
-        hosts = [torch.empty((n, 4), dtype=torch.float32, pin_memory=True) for _ in range(3)]
+        names = ("pos", "vel", "rho", "vel_prev", "rho_prev")
+        shapes = {"pos": (n, 3), "vel": (n, 3), "rho": (n,), "vel_prev": (n, 3), "rho_prev": (n,)}
+        hsoa = {k: torch.empty(shapes[k], dtype=torch.float32, pin_memory=True) for k in names}
+        dsoa = {k: torch.empty(shapes[k], dtype=torch.float32, device="cuda") for k in names}
         hid = torch.empty(n, dtype=torch.int64, pin_memory=True)
-        for hbuf, dbuf in zip(hosts, (sim.posp, sim.velr, sim.prev)):
-            hbuf.copy_(dbuf[:n])
+        ptr = lambda t: t.data_ptr()  # noqa: E731
+        stream = lambda: torch.cuda.current_stream().cuda_stream  # noqa: E731
+
+        def to_soa(lo, hi):
+            _lib.check(L.sphb_state_to_soa(lo, hi - lo, ptr(sim.posp), ptr(sim.velr), ptr(sim.prev),
+                                           *[ptr(dsoa[k]) for k in names], stream()), "to_soa")
+
+        def from_soa(lo, hi):
+            _lib.check(L.sphb_state_from_soa(lo, hi - lo, *[ptr(dsoa[k]) for k in names],
+                                             ptr(sim.posp), ptr(sim.velr), ptr(sim.prev), stream()),
+                       "from_soa")
+
+        to_soa(0, n)  # the host arrays start as the current state
+        for k in names:
+            hsoa[k].copy_(dsoa[k])
         hid.copy_(sim.id[:n])
-        pairs = list(zip(hosts + [hid], [sim.posp, sim.velr, sim.prev, sim.id]))
+        pairs = [(hsoa[k], dsoa[k]) for k in names] + [(hid, sim.id[:n])]
         h2d = d2h = sum(h.numel() * h.element_size() for h, _ in pairs)
         nchunk = max(1, min(args.e2e_chunks, n))
         bounds = [(n * c // nchunk, n * (c + 1) // nchunk) for c in range(nchunk)]
@@ -445,7 +464,7 @@ def main():
         s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
         ev_in = [torch.cuda.Event() for _ in bounds]
         ev_out = [torch.cuda.Event() for _ in bounds]
-        ev_step = torch.cuda.Event()
+        ev_packed = torch.cuda.Event()
 
         def h2d_chunk(c):
             lo, hi = bounds[c]
@@ -461,12 +480,14 @@ def main():
                 h2d_chunk(c)
                 ev_in[c].record(s_in)
         for k in range(args.e2e_steps):
-            for c in range(nchunk):
+            for c, (lo, hi) in enumerate(bounds):  # convert each chunk as it lands
                 comp.wait_event(ev_in[c])
+                from_soa(lo, hi)
             sim.first_keys_resync()
             sim.launch_step()
-            ev_step.record(comp)
-            s_out.wait_event(ev_step)
+            to_soa(0, n)
+            ev_packed.record(comp)
+            s_out.wait_event(ev_packed)
             with torch.cuda.stream(s_out):
                 for c, (lo, hi) in enumerate(bounds):
                     for hbuf, dbuf in pairs:
@@ -522,7 +543,9 @@ def main():
     if e2e_value is not None:
         line["e2e"] = {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
                        "d2h_bytes_per_step": d2h, "steps": args.e2e_steps,
-                       "path": "per step: pinned host state -> H2D -> sphb_* step -> D2H state, "
+                       "path": "per step: pinned host state in the reference's layout (pos, vel, "
+                               "rho, vel_prev, rho_prev, id: 52 B/particle) -> H2D -> "
+                               "sphb_state_from_soa -> sphb_* step -> sphb_state_to_soa -> D2H, "
                                f"round trip pipelined in {args.e2e_chunks} row chunks over "
                                "full-duplex PCIe (H2D of step k+1 chunk c after D2H of step k chunk c)"}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -237,6 +237,18 @@ int sphb_integrate_stage(sphb_workspace_t* ws, const sphb_params_t* prm, const s
                          void* prev, int64_t* id, uint32_t* keys_next, sphb_ctrl_t* ctrl,
                          sphb_stream_t s);
 
+/* The reference's state layout <-> the step's rows (rows [r0, r0 + cnt)).  pos / vel /
+ * vel_prev are (n, 3) f32 row-major, rho / rho_prev (n,) f32: ParticleSystem.pos/vel/rho
+ * (model.py:25-43) and VerletState.vel_prev/rho_prev (sim.py:31-43), as device copies of the
+ * caller's host arrays (52 B per particle with the int64 ids, which the step uses as they
+ * are).  posp.w is written 0 (the step derives prrho itself). */
+int sphb_state_from_soa(int64_t r0, int64_t cnt, const float* pos, const float* vel,
+                        const float* rho, const float* vel_prev, const float* rho_prev,
+                        void* posp, void* velr, void* prev, sphb_stream_t s);
+int sphb_state_to_soa(int64_t r0, int64_t cnt, const void* posp, const void* velr,
+                      const void* prev, float* pos, float* vel, float* rho, float* vel_prev,
+                      float* rho_prev, sphb_stream_t s);
+
 /* Energy diagnostics (SURVEY.md §8(d) functional, no reference counterpart): out[0..4] =
  * KE (fluid), PE = sum m |g| z (fluid), IE = sum m (u(rho) - u(rho0)) with the Tait internal
  * energy u(rho) = B/(gamma-1) rho^(gamma-1)/rho0^gamma + B/rho (all particles), mean fluid rho,

@@ -115,6 +115,8 @@ def lib():
                                P, P, P], c_i32),
         "sphb_slab_unpack": ([P, c_i64, c_i64, c_i64, P, P, P, P, P], c_i32),
         "sphb_step": ([P, P, P, c_i64, c_i64, P, P, P, c_i64, P], c_i32),
+        "sphb_state_from_soa": ([c_i64, c_i64, P, P, P, P, P, P, P, P, P], c_i32),
+        "sphb_state_to_soa": ([c_i64, c_i64, P, P, P, P, P, P, P, P, P], c_i32),
         "sphb_step_launch_count": ([P, c_i64], c_i64),
     }
     for name, (args, res) in sig.items():
@@ -131,7 +133,8 @@ EXPORTED = ("sphb_last_error", "sphb_version", "sphb_workspace_create", "sphb_wo
             "sphb_sort", "sphb_sort_ranges", "sphb_reorder", "sphb_cell_ranges", "sphb_cell_ranges_from_sorted",
             "sphb_interact", "sphb_step_begin", "sphb_integrate", "sphb_step_end", "sphb_step",
             "sphb_step_launch_count", "sphb_integrate_stage", "sphb_energy", "sphb_slab_tiles",
-            "sphb_slab_count", "sphb_slab_scatter", "sphb_slab_unpack")
+            "sphb_slab_count", "sphb_slab_scatter", "sphb_slab_unpack", "sphb_state_from_soa",
+            "sphb_state_to_soa")
 
 
 def check(rc: int, what: str = "") -> None:

@@ -465,6 +465,31 @@ int sphb_slab_unpack(const void* buf, int64_t r0, int64_t cnt, int64_t dst, void
                             (cudaStream_t)s);
 }
 
+int sphb_state_from_soa(int64_t r0, int64_t cnt, const float* pos, const float* vel,
+                        const float* rho, const float* vel_prev, const float* rho_prev,
+                        void* posp, void* velr, void* prev, sphb_stream_t s) {
+  if (r0 < 0 || cnt < 0) return sphb_set_error(SPHB_E_INVALID, "bad row range");
+  if (cnt > 0) {
+    SPHB_NONNULL(pos); SPHB_NONNULL(vel); SPHB_NONNULL(rho); SPHB_NONNULL(vel_prev);
+    SPHB_NONNULL(rho_prev); SPHB_NONNULL(posp); SPHB_NONNULL(velr); SPHB_NONNULL(prev);
+  }
+  return launch_state_unpack(r0, cnt, pos, vel, rho, vel_prev, rho_prev, (float4*)posp,
+                             (float4*)velr, (float4*)prev, (cudaStream_t)s);
+}
+
+int sphb_state_to_soa(int64_t r0, int64_t cnt, const void* posp, const void* velr,
+                      const void* prev, float* pos, float* vel, float* rho, float* vel_prev,
+                      float* rho_prev, sphb_stream_t s) {
+  if (r0 < 0 || cnt < 0) return sphb_set_error(SPHB_E_INVALID, "bad row range");
+  if (cnt > 0) {
+    SPHB_NONNULL(pos); SPHB_NONNULL(vel); SPHB_NONNULL(rho); SPHB_NONNULL(vel_prev);
+    SPHB_NONNULL(rho_prev); SPHB_NONNULL(posp); SPHB_NONNULL(velr); SPHB_NONNULL(prev);
+  }
+  return launch_state_pack(r0, cnt, (const float4*)posp, (const float4*)velr,
+                           (const float4*)prev, pos, vel, rho, vel_prev, rho_prev,
+                           (cudaStream_t)s);
+}
+
 int64_t sphb_step_launch_count(const sphb_grid_t* grid, int64_t n) {
   if (!grid) return 0;
   return 1 /*begin*/ + nl_launch_count(*grid, n) + interact_launch_count(n) + 1 /*integrate*/ +

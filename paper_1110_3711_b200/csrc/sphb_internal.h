@@ -105,3 +105,11 @@ int launch_ctrl_init(sphb_ctrl_t* ctrl, int64_t max_steps, double t_end, cudaStr
 
 int sphb_set_error(int code, const char* fmt, ...);
 int sphb_check_launch(const char* what);
+
+// state.cu
+int launch_state_unpack(int64_t r0, int64_t cnt, const float* pos, const float* vel,
+                        const float* rho, const float* vel_prev, const float* rho_prev,
+                        float4* posp, float4* velr, float4* prev, cudaStream_t s);
+int launch_state_pack(int64_t r0, int64_t cnt, const float4* posp, const float4* velr,
+                      const float4* prev, float* pos, float* vel, float* rho, float* vel_prev,
+                      float* rho_prev, cudaStream_t s);

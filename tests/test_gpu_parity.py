@@ -378,6 +378,38 @@ def test_movers_only_sort_rejects_an_inconsistent_previous_order():
         assert np.array_equal(x, y)
 
 
+def test_state_soa_round_trip():
+    """sphb_state_to_soa / sphb_state_from_soa: the reference's (pos, vel, rho, vel_prev,
+    rho_prev) arrays <-> the step rows, bit for bit, by row ranges."""
+    from paper_1110_3711_b200 import _lib
+    sc = sph.Scenario(dp=0.02)
+    prm = sph.make_params(sc)
+    sim = D.DeviceSim(sph.build_dam_break(sc, prm), prm, reach=1)
+    for _ in range(3):
+        sim.launch_step()
+    n = sim.n
+    L, s = _lib.lib(), torch.cuda.current_stream().cuda_stream
+    soa = [torch.empty((n, 3), device="cuda"), torch.empty((n, 3), device="cuda"),
+           torch.empty(n, device="cuda"), torch.empty((n, 3), device="cuda"), torch.empty(n, device="cuda")]
+    ptrs = [t.data_ptr() for t in soa]
+    _lib.check(L.sphb_state_to_soa(0, n, sim.posp.data_ptr(), sim.velr.data_ptr(), sim.prev.data_ptr(),
+                                   *ptrs, s), "to_soa")
+    p, v, r, _, vp, rp = sim.download()
+    for got, want in zip(soa, (p, v, r, vp, rp)):
+        assert np.array_equal(got.cpu().numpy(), want)
+    before = [t.clone() for t in (sim.posp, sim.velr, sim.prev)]
+    for t in (sim.posp, sim.velr, sim.prev):
+        t.zero_()
+    half = n // 2  # two row ranges, as the chunked copies use them
+    for lo, hi in ((0, half), (half, n)):
+        _lib.check(L.sphb_state_from_soa(lo, hi - lo, *ptrs, sim.posp.data_ptr(), sim.velr.data_ptr(),
+                                         sim.prev.data_ptr(), s), "from_soa")
+    torch.cuda.synchronize()
+    assert torch.equal(sim.posp[:n, :3], before[0][:n, :3]) and torch.all(sim.posp[:n, 3] == 0)
+    assert torch.equal(sim.velr[:n], before[1][:n]) and torch.equal(sim.prev[:n], before[2][:n])
+    assert L.sphb_state_from_soa(-1, 1, *ptrs, 0, 0, 0, s) == _lib.SPHB_E_INVALID
+
+
 # ------------------------------------------------------------------ full sizes
 def _device_counters(name, n_subdiv, precision="fp32"):
     sc = sph.named_scenario(name)
