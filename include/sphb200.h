@@ -135,11 +135,16 @@ int sphb_workspace_create(int64_t n_max, int64_t ncells_max, sphb_workspace_t** 
 int sphb_workspace_destroy(sphb_workspace_t* ws);
 /* Zeroes the workspace histogram (needed only after an aborted step). */
 int sphb_workspace_reset(sphb_workspace_t* ws, sphb_stream_t s);
-/* Movers-only sort threshold of sphb_step (default 65536, at most min(n_max, 65536)): a
+/* Movers-only sort threshold of sphb_step (default and maximum min(n_max, 2^20)): a
  * step whose rows changed cell for at most `cap` rows is sorted by counting from the previous
  * order; otherwise (or cap = -1) by the LSD radix sort.  Both give the identical permutation
  * (grid.py:107-109 stable order); the choice is made on the device. */
 int sphb_workspace_set_mover_cap(sphb_workspace_t* ws, int64_t cap);
+/* Targets per interaction block of the FP32 kernel: 128 (default: 4-warp CTAs, two per SM,
+ * <= 2,304 staged candidates) or 256 (8-warp CTAs, one per SM, <= 3,456 staged candidates:
+ * fewer idle lanes when cells hold uneven particle counts, e.g. after a dam collapses).
+ * Results agree within the FP32 tolerance (accumulation order); FP64 always uses 128. */
+int sphb_workspace_set_pi_block(sphb_workspace_t* ws, int32_t targets);
 /* The last sphb_step sort's path (0 movers-only, 1 radix) and mover count (synchronising
  * read, diagnostics only). */
 int sphb_workspace_sort_info(const sphb_workspace_t* ws, int64_t* movers, int32_t* mode);

@@ -95,6 +95,7 @@ def lib():
         "sphb_workspace_bytes": ([P], c_i64),
         "sphb_workspace_set_mover_cap": ([P, c_i64], c_i32),
         "sphb_workspace_sort_info": ([P, P, P], c_i32),
+        "sphb_workspace_set_pi_block": ([P, c_i32], c_i32),
         "sphb_ctrl_init": ([P, c_i64, c_f64, P], c_i32),
         "sphb_cell_keys": ([P, P, P, c_i64, c_i64, P, P, P, P], c_i32),
         "sphb_sort": ([P, P, P, c_i64, P, P, P, P], c_i32),
@@ -129,7 +130,7 @@ def lib():
 
 EXPORTED = ("sphb_last_error", "sphb_version", "sphb_workspace_create", "sphb_workspace_destroy",
             "sphb_workspace_reset", "sphb_workspace_bytes",
-            "sphb_workspace_set_mover_cap", "sphb_workspace_sort_info", "sphb_ctrl_init", "sphb_cell_keys",
+            "sphb_workspace_set_mover_cap", "sphb_workspace_sort_info", "sphb_workspace_set_pi_block", "sphb_ctrl_init", "sphb_cell_keys",
             "sphb_sort", "sphb_sort_ranges", "sphb_reorder", "sphb_cell_ranges", "sphb_cell_ranges_from_sorted",
             "sphb_interact", "sphb_step_begin", "sphb_integrate", "sphb_step_end", "sphb_step",
             "sphb_step_launch_count", "sphb_integrate_stage", "sphb_energy", "sphb_slab_tiles",

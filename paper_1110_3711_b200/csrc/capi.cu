@@ -69,6 +69,19 @@ static int check_params(const sphb_params_t* p) {
   return SPHB_OK;
 }
 
+int launch_interact(sphb_workspace* ws, const sphb_params_t& p, const sphb_grid_t& g, int64_t n,
+                    int64_t nb, const float4* posp, const float4* velr, const float4* aux,
+                    const int32_t* cell_sorted, const int32_t* beg, const int32_t* end,
+                    double* acc, double* drho, double* visc, sphb_ctrl_t* ctrl, cudaStream_t s) {
+  if (ws->pi_block == 256 && p.precision == SPHB_FP32)
+    return pi256::launch_interact(ws, p, g, n, nb, posp, velr, aux, cell_sorted, beg, end, acc,
+                                  drho, visc, ctrl, s);
+  return pi128::launch_interact(ws, p, g, n, nb, posp, velr, aux, cell_sorted, beg, end, acc, drho,
+                                visc, ctrl, s);
+}
+
+int64_t interact_launch_count(int64_t n) { return pi128::interact_launch_count(n); }
+
 extern "C" {
 
 const char* sphb_last_error(void) { return g_err; }
@@ -165,6 +178,14 @@ int sphb_workspace_set_mover_cap(sphb_workspace_t* ws, int64_t cap) {
     return sphb_set_error(SPHB_E_INVALID, "mover cap must lie in [-1, %lld]",
                           (long long)ws->mover_cap_max);
   ws->mover_cap = cap;
+  return SPHB_OK;
+}
+
+int sphb_workspace_set_pi_block(sphb_workspace_t* ws, int32_t targets) {
+  SPHB_NONNULL(ws);
+  if (targets != 128 && targets != 256)
+    return sphb_set_error(SPHB_E_INVALID, "interaction block must be 128 or 256 targets");
+  ws->pi_block = targets;
   return SPHB_OK;
 }
 

@@ -1773,6 +1773,11 @@ __global__ void __launch_bounds__(256) k_wall_force(sphb_params_t p, sphb_grid_t
 
 }  // namespace
 
+#ifndef SPHB_PI_NS
+#define SPHB_PI_NS pi128  // this build's blocking (see sphb_internal.h: pi128 / pi256)
+#endif
+namespace SPHB_PI_NS {
+
 int64_t interact_launch_count(int64_t n) {
   (void)n;
   return 2;
@@ -1837,3 +1842,5 @@ int launch_interact(sphb_workspace* ws, const sphb_params_t& p, const sphb_grid_
       p, g, n, nb, a.ncells, posp, cell_sorted, beg, end, acc, ctrl);
   return sphb_check_launch("k_wall_force");
 }
+
+}  // namespace SPHB_PI_NS

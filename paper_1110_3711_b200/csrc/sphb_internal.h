@@ -14,7 +14,7 @@ constexpr int SCAN_BLOCK = 256;
 constexpr int SCAN_ITEMS = 4;
 constexpr int SCAN_TILE = SCAN_BLOCK * SCAN_ITEMS;
 constexpr int MV_TILE_ROWS = 4096;          // rows per movers-only sort tile (128 bitmap words)
-constexpr int64_t MOVER_CAP_MAX = 1 << 16;  // movers per step the movers-only sort accepts
+constexpr int64_t MOVER_CAP_MAX = 1 << 20;  // movers per step the movers-only sort accepts
 
 struct sphb_workspace {
   int64_t n_max = 0, ncells_max = 0;
@@ -39,6 +39,7 @@ struct sphb_workspace {
   int32_t* mv_head = nullptr;  // 2*ncells_max, -1 between steps
   int4* mv_kv = nullptr;       // 2*ncells_max per-key (SB, MB, old begin, chain head)
   int64_t mover_cap_max = 0, mover_cap = 0;
+  int32_t pi_block = 128;  // targets per interaction block: 128 (pi128) or 256 (pi256)
   size_t bytes = 0;
 };
 
@@ -64,7 +65,21 @@ int launch_hist_from_sorted(sphb_workspace* ws, const sphb_grid_t& g, const int3
 int sort_pass_count(const sphb_grid_t& g);
 int64_t nl_launch_count(const sphb_grid_t& g, int64_t n);
 
-// interact.cu
+// interact.cu, compiled twice: pi128 (4-warp CTAs, 128-target blocks over <= 2,304 staged
+// candidates, 2 CTAs/SM; the default) and pi256 (8-warp CTAs, 256-target blocks over <= 3,456
+// staged candidates, 1 CTA/SM: fewer idle lanes once cells fill unevenly)
+#define SPHB_DECLARE_PI(NS)                                                                     \
+  namespace NS {                                                                                \
+  int launch_interact(sphb_workspace* ws, const sphb_params_t& p, const sphb_grid_t& g,       \
+                      int64_t n, int64_t nb, const float4* posp, const float4* velr,           \
+                      const float4* aux, const int32_t* cell_sorted, const int32_t* beg,       \
+                      const int32_t* end, double* acc, double* drho, double* visc,             \
+                      sphb_ctrl_t* ctrl, cudaStream_t s);                                      \
+  int64_t interact_launch_count(int64_t n);                                                    \
+  }
+SPHB_DECLARE_PI(pi128)
+SPHB_DECLARE_PI(pi256)
+// the workspace's blocking (FP64 always pi128)
 int launch_interact(sphb_workspace* ws, const sphb_params_t& p, const sphb_grid_t& g, int64_t n, int64_t nb,
                     const float4* posp, const float4* velr, const float4* aux,
                     const int32_t* cell_sorted, const int32_t* beg, const int32_t* end,

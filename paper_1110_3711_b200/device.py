@@ -65,6 +65,10 @@ class Workspace:
         _lib.check(_lib.lib().sphb_workspace_set_mover_cap(self._h, int(cap)),
                    "sphb_workspace_set_mover_cap")
 
+    def set_pi_block(self, targets: int):
+        _lib.check(_lib.lib().sphb_workspace_set_pi_block(self._h, int(targets)),
+                   "sphb_workspace_set_pi_block")
+
     def sort_info(self) -> tuple[int, int]:
         """(movers, mode) of the last sphb_step sort; mode 0 movers-only, 1 radix."""
         m, mode = ctypes.c_int64(), ctypes.c_int32()
@@ -146,6 +150,20 @@ class DeviceSim:
         self.first_keys()
         self._graph = None
         self._graph_steps = 0
+        self.pi_block = 128
+
+    def set_pi_block(self, targets: int):
+        """Targets per FP32 interaction block: 128 (4-warp CTAs, the default) or 256 (8-warp
+        CTAs: fewer idle lanes when cells hold uneven counts).  Drops a captured graph."""
+        self.ws.set_pi_block(targets)
+        self.pi_block = int(targets)
+        self._graph = None
+
+    def pi_lane_use(self, ctrl=None) -> float:
+        """Targets / (blocks x block size) of the last interaction launch."""
+        c = self.ctrl_host() if ctrl is None else ctrl
+        nblk = int(c["nblk"][0])
+        return self.n / (self.pi_block * nblk) if nblk else 1.0
 
     # ------------------------------------------------------------------ host <-> device
     def upload(self, system, vel_prev=None, rho_prev=None, stream_copy=True):
@@ -317,6 +335,8 @@ class DeviceSim:
         if t_end is not None:
             view["t_end"] = float(t_end)
         sim.ctrl.copy_(torch.as_tensor(c).to(sim.device))
+        if "pi_block" in z:  # the interaction blocking in use when the checkpoint was written
+            sim.set_pi_block(int(z["pi_block"]))
         return sim
 
     # ------------------------------------------------------------------ readback

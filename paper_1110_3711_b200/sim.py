@@ -40,6 +40,12 @@ def divergence_from_device(err) -> DivergenceError:
     return DivergenceError(f"non-finite state at step {step}", step)
 
 
+# 128-target blocks whose lanes are filled below this fraction run slower than the 256-target
+# blocking (C3 10k-step dam break: equal near 0.8, 128 wins at rest, 256 by 8% once collapsed)
+PI_LANE_SWITCH = 0.78
+PI_DECIDE_EVERY = 256  # the "auto" blocking is decided at these step multiples only (chunk-proof)
+
+
 def compute_derived(rho, params) -> DerivedQuantities:
     """physics.compute_derived (physics.py:96-110) on the device EOS."""
     press, csound, prrho, tensil = compute_derived_device(np.asarray(rho), params)
@@ -62,7 +68,8 @@ def make_device_sim(system, params, cfg: EngineConfig, max_steps=None, t_end=Non
 def run_simulation(scenario_or_system, params, config: EngineConfig, max_steps: int | None = None,
                    t_end: float | None = None, snapshot_every: int = 0, snapshot_sink=None,
                    stats_sink=None, *, chunk: int = 256, stage_timing: bool = True,
-                   checkpoint_every: int = 0, checkpoint_path=None, resume_from=None):
+                   checkpoint_every: int = 0, checkpoint_path=None, resume_from=None,
+                   pi_block="auto"):
     """NL -> PI -> SU loop on the B200.  Returns (system, stats_list) like sim.py:272-352;
     raises DivergenceError on the first out-of-domain particle or non-finite state.
 
@@ -73,7 +80,13 @@ def run_simulation(scenario_or_system, params, config: EngineConfig, max_steps: 
     Extensions: ``checkpoint_every`` > 0 writes a binary checkpoint (snapshots.save_checkpoint;
     ``checkpoint_path`` may contain ``{step}``) every that many steps; ``resume_from`` continues
     bit-identically from such a checkpoint (``scenario_or_system`` may then be None; step
-    numbers and the stop rules continue from the checkpoint's step)."""
+    numbers and the stop rules continue from the checkpoint's step).
+
+    ``pi_block``: targets per FP32 interaction block, 128, 256 or "auto" (start at 128 and
+    switch to 256 for good once fewer than PI_LANE_SWITCH of the 128-target blocks' lanes
+    hold a target, e.g. after a dam collapses; decided every PI_DECIDE_EVERY steps from that
+    step's launch, so the choice does not depend on ``chunk``; recorded in checkpoints so
+    resumed runs follow the same blocking)."""
     if max_steps is None and t_end is None:
         raise ValueError("need max_steps or t_end")
     validate(params)
@@ -99,6 +112,13 @@ def run_simulation(scenario_or_system, params, config: EngineConfig, max_steps: 
         system = build_dam_break(scenario_or_system, params) if isinstance(scenario_or_system, Scenario) \
             else scenario_or_system
         sim = make_device_sim(system, params, cfg, max_steps, t_end, record_capacity=max(chunk, 1))
+    if pi_block not in (128, 256, "auto"):
+        raise ValueError("pi_block must be 128, 256 or 'auto'")
+    if pi_block != "auto" and resume_from is None:
+        sim.set_pi_block(int(pi_block))
+    adapt = pi_block == "auto" and cfg.precision == "fp32"
+    if adapt:  # readbacks at every decision step, whatever else sets the chunk
+        chunk = math.gcd(chunk, PI_DECIDE_EVERY)
     stats_out: list[StepStats] = []
     nbytes = NEIGHBOR_BYTES[cfg.derived_mode]
     done_steps = int(sim.ctrl_host()["step"])
@@ -129,6 +149,9 @@ def run_simulation(scenario_or_system, params, config: EngineConfig, max_steps: 
         err = sim.error()
         if err is not None:
             raise divergence_from_device(err)
+        if adapt and sim.pi_block == 128 and now > done_steps and now % PI_DECIDE_EVERY == 0 \
+                and sim.pi_lane_use(c) < PI_LANE_SWITCH:
+            sim.set_pi_block(256)
         if checkpoint_every and now > done_steps and now % int(checkpoint_every) == 0:
             sim.save_checkpoint(str(checkpoint_path).format(step=now))
         done_steps = now

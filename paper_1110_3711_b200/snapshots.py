@@ -229,7 +229,8 @@ def save_checkpoint(path, sim) -> None:
     np.savez(path, magic=np.array(CHECKPOINT_MAGIC), n=np.int64(n), nb=np.int64(sim.nb),
              mass_fluid=np.float64(sim.mass_fluid), mass_boundary=np.float64(sim.mass_boundary),
              posp=sim.posp[:n].cpu().numpy(), velr=sim.velr[:n].cpu().numpy(),
-             prev=sim.prev[:n].cpu().numpy(), id=sim.id[:n].cpu().numpy(), ctrl=ctrl)
+             prev=sim.prev[:n].cpu().numpy(), id=sim.id[:n].cpu().numpy(), ctrl=ctrl,
+             pi_block=np.int32(getattr(sim, "pi_block", 128)))
 
 
 def load_checkpoint(path) -> dict:

@@ -410,6 +410,43 @@ def test_state_soa_round_trip():
     assert L.sphb_state_from_soa(-1, 1, *ptrs, 0, 0, 0, s) == _lib.SPHB_E_INVALID
 
 
+@pytest.mark.parametrize("name", ["c1", "c2"])
+def test_pi_block_256_matches_128(name):
+    """The 256-target blocking (pi256: 8-warp CTAs) gives the 128-target one's counters
+    exactly and its forces within the FP32 tolerance, step after step."""
+    sc = sph.named_scenario(name)
+    prm = sph.make_params(sc)
+    system = sph.build_dam_break(sc, prm)
+    a = D.DeviceSim(system, prm, reach=1, precision=0)
+    b = D.DeviceSim(system, prm, reach=1, precision=0)
+    b.set_pi_block(256)
+    for step in range(4):
+        a.launch_step()
+        b.launch_step()
+        ra, rb = a.records(step, step + 1), b.records(step, step + 1)
+        for f in ("candidate_pairs", "hits_ordered", "force_evals", "ff_force_evals"):
+            assert int(ra[f][0]) == int(rb[f][0]), f
+        for x, y in ((a.acc, b.acc), (a.drho, b.drho), (a.visc, b.visc)):
+            assert oracle.rel_linf(x[:a.n].cpu().numpy(), y[:b.n].cpu().numpy()) <= FP32_TOL
+        assert abs(float(ra["dt"][0]) / float(rb["dt"][0]) - 1.0) <= 1e-6
+    assert 0.0 < b.pi_lane_use() <= 1.0 and int(b.ctrl_host()["nblk"][0]) < int(a.ctrl_host()["nblk"][0])
+
+
+def test_run_simulation_switches_blocking_when_lanes_idle(monkeypatch):
+    from paper_1110_3711_b200 import sim as S
+    monkeypatch.setattr(S, "PI_DECIDE_EVERY", 10)
+    sc = sph.Scenario(dp=0.02)
+    prm = sph.make_params(sc)
+    cfg = sph.EngineConfig(engine="gather", symmetry=False, gather_variant="slowcellsh")
+    s_auto, st_auto = sph.run_simulation(sc, prm, cfg, max_steps=40, chunk=10)
+    s_128, st_128 = sph.run_simulation(sc, prm, cfg, max_steps=40, chunk=10, pi_block=128)
+    assert [x.true_pairs for x in st_auto[:10]] == [x.true_pairs for x in st_128[:10]]
+    for f in ("pos", "vel", "rho"):
+        assert oracle.rel_linf(getattr(s_auto, f), getattr(s_128, f)) <= 1e-4, f
+    with pytest.raises(ValueError, match="pi_block"):
+        sph.run_simulation(sc, prm, cfg, max_steps=1, pi_block=64)
+
+
 # ------------------------------------------------------------------ full sizes
 def _device_counters(name, n_subdiv, precision="fp32"):
     sc = sph.named_scenario(name)
