@@ -48,6 +48,8 @@ def parse():
     ap.add_argument("--n-subdiv", type=int, default=1)
     ap.add_argument("--precision", default="fp32", choices=["fp32", "fp64"])
     ap.add_argument("--e2e-steps", type=int, default=20)
+    ap.add_argument("--pi-block", default="auto", choices=["auto", "128", "256"],
+                    help="targets per interaction block (auto: chosen from the warm-up's lane use)")
     ap.add_argument("--e2e-chunks", type=int, default=8,
                     help="row chunks of the pipelined H2D/D2H state round trip (1 = serial)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -382,6 +384,18 @@ def main():
     for _ in range(args.warmup):
         sim.launch_step()
     torch.cuda.synchronize()
+    # interaction blocking from the warm-up (run_simulation's policy, sim.py): 128-target
+    # blocks unless their lanes are mostly idle; one more untimed step after a switch
+    if args.pi_block == "auto" and prec == _lib.SPHB_FP32:
+        from paper_1110_3711_b200.sim import PI_LANE_SWITCH
+        if sim.pi_lane_use() < PI_LANE_SWITCH:
+            sim.set_pi_block(256)
+            sim.launch_step()
+            torch.cuda.synchronize()
+    elif args.pi_block != "auto":
+        sim.set_pi_block(int(args.pi_block))
+        sim.launch_step()
+        torch.cuda.synchronize()
     first = int(sim.ctrl_host()["step"])
     if world > 1:
         dist.barrier()
@@ -519,7 +533,8 @@ def main():
                                f"({system.count_fluid:,} fluid + {system.count_boundary:,} boundary)",
                    "particles_per_gpu": system.n, "n_subdiv": args.n_subdiv, "variant": variant,
                    "l2": "inputs larger than L2 (resident state ~%.1f GB)" % (sim.n * 184 / 1e9),
-                   "parallelism": f"{world} GPU" + (" replicas" if world > 1 else "")},
+                   "parallelism": f"{world} GPU" + (" replicas" if world > 1 else ""),
+                   "pi_block": sim.pi_block},
         "interactions_per_s": true_pairs * world * args.steps / (total_ms * 1e-3),
         "pair_evals_per_s": evals * world * args.steps / (total_ms * 1e-3),
         "stage_ms": {"nl": float(np.mean(nl_ms)), "pi": pi_mean, "su": float(np.mean(su_ms))},
