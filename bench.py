@@ -266,7 +266,7 @@ def run_slabs(args, cfg_name, system, prm, prec, world, rank, local):
     the dt minima and counters; one host synchronisation per step (the totals all-gather)."""
     import torch
     import torch.distributed as dist
-    from paper_1110_3711_b200 import dslab
+    from paper_1110_3711_b200 import _lib, dslab
 
     sim = dslab.DeviceSlabSim(system, prm, dslab.DevDistComm(), precision=prec,
                               rebalance_every=args.rebalance_every)
@@ -275,6 +275,14 @@ def run_slabs(args, cfg_name, system, prm, prec, world, rank, local):
     for _ in range(args.warmup):
         sim.step()
     torch.cuda.synchronize()
+    pi_blocks = [128]
+    first = args.warmup
+    if args.pi_block == "auto" and prec == _lib.SPHB_FP32:  # as the single-GPU path
+        from paper_1110_3711_b200.sim import PI_LANE_SWITCH
+        pi_blocks = sim.choose_pi_block(PI_LANE_SWITCH)
+        sim.step()
+        first += 1
+        torch.cuda.synchronize()
     dist.barrier()
     clocks = Clocks(local)
     t0, t1 = Ev(), Ev()
@@ -318,7 +326,7 @@ def run_slabs(args, cfg_name, system, prm, prec, world, rank, local):
         te = torch.tensor([a.elapsed_time(b)], device="cuda")
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
         e2e_value = system.n * args.e2e_steps / (float(te.item()) * 1e-3)
-    recs = sim.records(args.warmup, args.warmup + args.steps)
+    recs = sim.records(first, first + args.steps)
     true_pairs = float(np.mean(recs["hits_ordered"].astype(np.float64))) / 2
     evals = float(np.mean(recs["force_evals"].astype(np.float64)))
     value = system.n * args.steps / (total_ms * 1e-3)
@@ -336,6 +344,7 @@ def run_slabs(args, cfg_name, system, prm, prec, world, rank, local):
                    "parallelism": f"{world} X-slabs (device-resident exchange: NCCL send/recv of "
                                   "migrants + halo rows, device all-reduce of dt and counters)",
                    "slab_bounds": [int(v) for v in sim.bounds],
+                   "pi_block_rank0": int(pi_blocks[0]),
                    "max_owned_per_gpu": int(owned.item())},
         "interactions_per_s": true_pairs * args.steps / (total_ms * 1e-3),
         "pair_evals_per_s": evals * args.steps / (total_ms * 1e-3),
