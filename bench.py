@@ -297,28 +297,57 @@ def run_slabs(args, cfg_name, system, prm, prec, world, rank, local):
     dist.all_reduce(tt, op=dist.ReduceOp.MAX)
     total_ms = float(tt.item())
     # e2e: the same decomposed step with each rank's resident rows round-tripped through pinned
-    # host buffers every step (the per-step host boundary of the engine API)
+    # host buffers every step, in the reference's state layout (pos, vel, rho, vel_prev,
+    # rho_prev, id: 52 B/row; sphb_state_to_soa / sphb_state_from_soa) and pipelined in row
+    # chunks over the full-duplex PCIe link (as the single-GPU path)
     h2d = d2h = 0
     e2e_value = None
     if args.e2e_steps > 0:
-        pinned = {f: torch.empty((int(me.n * 1.2) + 1024,) + tuple(getattr(me.a, f).shape[1:]),
-                                 dtype=getattr(me.a, f).dtype, pin_memory=True)
-                  for f in ("posp", "velr", "prev", "id")}  # pinned once, outside the timed region
+        L = _lib.lib()
+        cap = int(me.n * 1.5) + 1024
+        names = ("pos", "vel", "rho", "vel_prev", "rho_prev")
+        width = {"pos": 3, "vel": 3, "rho": 1, "vel_prev": 3, "rho_prev": 1}
+        mk = lambda w, **kw: torch.empty((cap, w) if w > 1 else (cap,), dtype=torch.float32, **kw)  # noqa: E731
+        hsoa = {k: mk(width[k], pin_memory=True) for k in names}
+        dsoa = {k: mk(width[k], device="cuda") for k in names}
+        hid = torch.empty(cap, dtype=torch.int64, pin_memory=True)
+        nchunk = max(1, args.e2e_chunks)
+        s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
+        ev_in = [torch.cuda.Event() for _ in range(nchunk)]
+        ev_out = [torch.cuda.Event() for _ in range(nchunk)]
+        ev_packed = torch.cuda.Event()
         torch.cuda.synchronize()
         a, b = Ev(), Ev()
         a.record()
+        nbytes = 0
         for _ in range(args.e2e_steps):
+            comp = torch.cuda.current_stream()
             n = me.n
-            nbytes = 0
-            for f in ("posp", "velr", "prev", "id"):
-                t = getattr(me.a, f)[:n]
-                if f not in pinned or pinned[f].shape[0] < n:  # pinned once, reused every step
-                    pinned[f] = torch.empty((int(n * 1.2),) + tuple(t.shape[1:]), dtype=t.dtype,
-                                            pin_memory=True)
-                host = pinned[f][:n]
-                host.copy_(t, non_blocking=False)
-                t.copy_(host, non_blocking=True)
-                nbytes += host.numel() * host.element_size()
+            if n > cap:
+                raise RuntimeError("e2e staging too small for this rank's rows")
+            _lib.check(L.sphb_state_to_soa(0, n, me.a.posp.data_ptr(), me.a.velr.data_ptr(),
+                                           me.a.prev.data_ptr(), *[dsoa[k].data_ptr() for k in names],
+                                           comp.cuda_stream), "to_soa")
+            ev_packed.record(comp)
+            bounds = [(n * c // nchunk, n * (c + 1) // nchunk) for c in range(nchunk)]
+            pairs = [(hsoa[k], dsoa[k]) for k in names] + [(hid, me.a.id)]
+            s_out.wait_event(ev_packed)
+            for c, (lo, hi) in enumerate(bounds):
+                with torch.cuda.stream(s_out):
+                    for hbuf, dbuf in pairs:
+                        hbuf[lo:hi].copy_(dbuf[lo:hi], non_blocking=True)
+                    ev_out[c].record(s_out)
+                with torch.cuda.stream(s_in):
+                    s_in.wait_event(ev_out[c])
+                    for hbuf, dbuf in pairs:
+                        dbuf[lo:hi].copy_(hbuf[lo:hi], non_blocking=True)
+                    ev_in[c].record(s_in)
+            for c, (lo, hi) in enumerate(bounds):
+                comp.wait_event(ev_in[c])
+                _lib.check(L.sphb_state_from_soa(lo, hi - lo, *[dsoa[k].data_ptr() for k in names],
+                                                 me.a.posp.data_ptr(), me.a.velr.data_ptr(),
+                                                 me.a.prev.data_ptr(), comp.cuda_stream), "from_soa")
+            nbytes = n * 52
             h2d = d2h = nbytes
             sim.step()
         b.record()
@@ -354,7 +383,9 @@ def run_slabs(args, cfg_name, system, prm, prec, world, rank, local):
     if e2e_value is not None:
         line["e2e"] = {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
                        "d2h_bytes_per_step": d2h, "steps": args.e2e_steps,
-                       "path": "per step: each rank's resident rows via pinned host buffers, then the decomposed step"}
+                       "path": "per step: each rank's resident rows through pinned host buffers in the "
+                               "reference's layout (52 B/row), chunk-pipelined D2H/H2D, then the "
+                               "decomposed step"}
     if rank == 0:
         print(json.dumps(line), flush=True)
     dist.destroy_process_group()
