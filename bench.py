@@ -35,6 +35,7 @@ METRIC = "particle-steps/sec and interactions/sec at 1/2/4/8 B200 vs host-CPU re
 UNIT = "particle-steps/s"
 FLOP_PER_CAND, FLOP_PER_EVAL = 9, 70  # SURVEY.md §8(d) algorithmic units
 BYTES_NL_SU = 324 - 52                # compulsory NL+SU bytes per particle-step
+GRAPH_BELOW = 2_000_000               # systems this small are launch-bound: graph replay
 
 
 def parse():
@@ -48,6 +49,8 @@ def parse():
     ap.add_argument("--n-subdiv", type=int, default=1)
     ap.add_argument("--precision", default="fp32", choices=["fp32", "fp64"])
     ap.add_argument("--e2e-steps", type=int, default=20)
+    ap.add_argument("--graph", default="auto", choices=["auto", "on", "off"],
+                    help="replay the timed steps as one CUDA graph (auto: below 2M particles)")
     ap.add_argument("--pi-block", default="auto", choices=["auto", "128", "256"],
                     help="targets per interaction block (auto: chosen from the warm-up's lane use)")
     ap.add_argument("--e2e-chunks", type=int, default=8,
@@ -419,7 +422,7 @@ def main():
         run_slabs(args, cfg_name, system, prm, prec, world, rank, local)
         return
     sim = DeviceSim(system, prm, reach=args.n_subdiv, precision=prec,
-                    record_capacity=max(64, args.warmup + args.steps + 8))
+                    record_capacity=max(64, args.warmup + 2 * args.steps + 16))
     Ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
     for _ in range(args.warmup):
         sim.launch_step()
@@ -439,13 +442,25 @@ def main():
     first = int(sim.ctrl_host()["step"])
     if world > 1:
         dist.barrier()
-    clocks = Clocks(local)
+    # launch-bound small systems replay the timed steps as one CUDA graph; their NL / PI / SU
+    # stage times then come from an eager pass of the same length right before (untimed)
+    use_graph = args.graph == "on" or (args.graph == "auto" and sim.n < GRAPH_BELOW)
     ev = [[Ev() for _ in range(4)] for _ in range(args.steps)]
+    if use_graph:
+        for k in range(args.steps):
+            sim.launch_step(events=ev[k])
+        torch.cuda.synchronize()
+        sim.capture(args.steps)
+        first = int(sim.ctrl_host()["step"])
+    clocks = Clocks(local)
     t0, t1 = Ev(), Ev()
     torch.cuda.synchronize()
     t0.record()
-    for k in range(args.steps):
-        sim.launch_step(events=ev[k])
+    if use_graph:
+        sim.run_graph()
+    else:
+        for k in range(args.steps):
+            sim.launch_step(events=ev[k])
     t1.record()
     torch.cuda.synchronize()
     if world > 1:
@@ -574,7 +589,7 @@ def main():
                    "particles_per_gpu": system.n, "n_subdiv": args.n_subdiv, "variant": variant,
                    "l2": "inputs larger than L2 (resident state ~%.1f GB)" % (sim.n * 184 / 1e9),
                    "parallelism": f"{world} GPU" + (" replicas" if world > 1 else ""),
-                   "pi_block": sim.pi_block},
+                   "pi_block": sim.pi_block, "cuda_graph": use_graph},
         "interactions_per_s": true_pairs * world * args.steps / (total_ms * 1e-3),
         "pair_evals_per_s": evals * world * args.steps / (total_ms * 1e-3),
         "stage_ms": {"nl": float(np.mean(nl_ms)), "pi": pi_mean, "su": float(np.mean(su_ms))},
