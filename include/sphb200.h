@@ -179,6 +179,14 @@ int sphb_sort_ranges(sphb_workspace_t* ws, const sphb_grid_t* grid, const uint32
                      int64_t n, uint32_t* keys_sorted, int32_t* perm, int32_t* beg, int32_t* end,
                      const sphb_ctrl_t* ctrl, sphb_stream_t s);
 
+/* K1 + K2 + K4 in one call (SURVEY.md §8(b)'s sphb_nl_build): cell keys of the rows as they
+ * are, the stable per-list permutation (radix) and both lists' per-cell [beg, end).  The
+ * first out-of-domain row is recorded in ctrl->err (SPHB_DIV_LEFT_DOMAIN) and the step's
+ * later kernels skip.  Equivalent to sphb_cell_keys, sphb_sort, sphb_cell_ranges. */
+int sphb_nl_build(sphb_workspace_t* ws, const sphb_grid_t* grid, const void* posp, int64_t n,
+                  int64_t nb, uint32_t* keys_out, uint32_t* keys_sorted_out, int32_t* perm_out,
+                  int32_t* beg, int32_t* end, sphb_ctrl_t* ctrl, sphb_stream_t s);
+
 /* K3 -- reorder gathers (grid.py:111-114) fused with compute_derived (physics.py:96-110):
  * *_out[i] = *_in[perm[i]] for posp, velr, prev, id; posp_out.w = prrho; aux_out = (press,
  * csound, tensil, list mass);

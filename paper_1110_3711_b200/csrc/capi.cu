@@ -270,6 +270,27 @@ int sphb_reorder(const sphb_params_t* prm, const sphb_grid_t* grid, int64_t n,
                         ctrl, (cudaStream_t)s);
 }
 
+int sphb_nl_build(sphb_workspace_t* ws, const sphb_grid_t* grid, const void* posp, int64_t n,
+                  int64_t nb, uint32_t* keys_out, uint32_t* keys_sorted_out, int32_t* perm_out,
+                  int32_t* beg, int32_t* end, sphb_ctrl_t* ctrl, sphb_stream_t s) {
+  SPHB_NONNULL(ws);
+  SPHB_NONNULL(ctrl);
+  SPHB_NONNULL(beg);
+  SPHB_NONNULL(end);
+  if (int rc = check_grid(grid)) return rc;
+  if (n < 0 || nb < 0 || nb > n) return sphb_set_error(SPHB_E_INVALID, "bad n/nb");
+  if (n > 0) {
+    SPHB_NONNULL(posp); SPHB_NONNULL(keys_out); SPHB_NONNULL(keys_sorted_out);
+    SPHB_NONNULL(perm_out);
+  }
+  cudaStream_t cs = (cudaStream_t)s;
+  int rc;
+  if ((rc = launch_cell_keys(ws, *grid, (const float4*)posp, n, nb, keys_out, nullptr, ctrl, cs)))
+    return rc;
+  if ((rc = launch_sort(ws, *grid, keys_out, n, keys_sorted_out, perm_out, ctrl, cs))) return rc;
+  return launch_cell_ranges(ws, *grid, beg, end, ctrl, cs);
+}
+
 int sphb_cell_ranges(sphb_workspace_t* ws, const sphb_grid_t* grid, int32_t* beg, int32_t* end,
                      const sphb_ctrl_t* ctrl, sphb_stream_t s) {
   SPHB_NONNULL(ws);

@@ -68,6 +68,36 @@ def test_device_nl_bit_exact(name):
         assert np.array_equal(out[k], z[k]), k
 
 
+@pytest.mark.parametrize("name", ["frame_small_n1.npz", "frame_mid5k_n2.npz"])
+def test_device_nl_build_one_call(name):
+    """sphb_nl_build (K1 + K2 + K4 in one call) equals the reference's NL outputs."""
+    from paper_1110_3711_b200 import _lib
+    from paper_1110_3711_b200.physics import grid_desc, grid_dims
+    z = golden(name)
+    prm = oracle.params_from_npz(z)
+    nb = int(z["in_nb"])
+    pos = np.asarray(z["in_pos"], np.float32)
+    n = pos.shape[0]
+    _, dims = grid_dims(prm)
+    ncells = int(np.prod(dims))
+    posp = torch.zeros((n, 4), dtype=torch.float32, device="cuda")
+    posp[:, :3] = torch.as_tensor(pos).cuda()
+    i32 = lambda m: torch.empty(m, dtype=torch.int32, device="cuda")  # noqa: E731
+    keys, ksort, perm = i32(n), i32(n), i32(n)
+    beg, end = i32(2 * ncells), i32(2 * ncells)
+    ws = D.Workspace(n, ncells)
+    ctrl = D.new_ctrl(torch.device("cuda"))
+    g = grid_desc(prm, prm.n_subdiv)
+    L = _lib.lib()
+    _lib.check(L.sphb_nl_build(ws.handle, _lib.ref(g), posp.data_ptr(), n, nb, keys.data_ptr(),
+                               ksort.data_ptr(), perm.data_ptr(), beg.data_ptr(), end.data_ptr(),
+                               ctrl.data_ptr(), torch.cuda.current_stream().cuda_stream), "nl_build")
+    assert np.array_equal(perm.cpu().numpy().astype(np.int64), z["sort_perm"])
+    b, e = beg.cpu().numpy().astype(np.int64), end.cpu().numpy().astype(np.int64)
+    for got, key in ((b[:ncells], "bbeg"), (e[:ncells], "bend"), (b[ncells:], "fbeg"), (e[ncells:], "fend")):
+        assert np.array_equal(got, z[key]), key
+
+
 def _grid_params(cell=0.5, n_subdiv=1):
     h = cell * n_subdiv / 2.0
     return oracle.Params(h=h, dp=h / 2, rho0=1000.0, c0=20.0, gamma=7.0, alpha=0.25,
