@@ -496,6 +496,7 @@ __global__ void __launch_bounds__(32) k_blocks(sphb_grid_t g, int64_t ncells,
       if (done) break;
       flush();
     }
+    __syncwarp();  // lane 0's record-count writes are visible to the warp (racecheck)
     if (s_nrec >= KB_BUF / 2) flush();
   }
   flush();

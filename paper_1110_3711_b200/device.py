@@ -85,7 +85,7 @@ class Workspace:
 
 
 def new_ctrl(device, max_steps: int = -1, t_end: float = math.inf) -> torch.Tensor:
-    ctrl = torch.empty(_lib.CTRL_BYTES, dtype=torch.uint8, device=device)
+    ctrl = torch.zeros(_lib.CTRL_BYTES, dtype=torch.uint8, device=device)  # pad bytes defined
     _lib.check(_lib.lib().sphb_ctrl_init(_ptr(ctrl), int(max_steps), float(t_end), _stream()),
                "sphb_ctrl_init")
     return ctrl

@@ -1,0 +1,38 @@
+"""A few steps of a small dam break through every kernel family, for compute-sanitizer:
+FP32 (pi128 and pi256 interaction builds, movers-only + radix sorts, symplectic, wall force,
+energy, SoA state conversion) and FP64.
+
+  compute-sanitizer --tool memcheck|racecheck|synccheck|initcheck python tools/sanitize_steps.py
+"""
+import sys
+
+import torch
+
+sys.path.insert(0, ".")
+import paper_1110_3711_b200 as sph  # noqa: E402
+from paper_1110_3711_b200 import _lib  # noqa: E402
+from paper_1110_3711_b200.device import DeviceSim  # noqa: E402
+
+sc = sph.Scenario(dp=0.02)
+prm = sph.make_params(sc, boundary_force=sph.BoundaryForce(d=5.0 * 9.81 * sc.fill_height, r0=sc.dp))
+system = sph.build_dam_break(sc, prm)
+for precision, block, integ in ((0, 128, "verlet"), (0, 256, "verlet"), (1, 128, "verlet"),
+                                (0, 128, "symplectic")):
+    p = sph.make_params(sc, integrator=integ,
+                        boundary_force=sph.BoundaryForce(d=5.0 * 9.81 * sc.fill_height, r0=sc.dp))
+    sim = DeviceSim(system, p, reach=1, precision=precision)
+    sim.set_pi_block(block)
+    for _ in range(4):
+        sim.launch_step()
+    sim.energy()
+    n = sim.n
+    soa = [torch.empty((n, 3), device="cuda"), torch.empty((n, 3), device="cuda"),
+           torch.empty(n, device="cuda"), torch.empty((n, 3), device="cuda"), torch.empty(n, device="cuda")]
+    L, s = _lib.lib(), torch.cuda.current_stream().cuda_stream
+    _lib.check(L.sphb_state_to_soa(0, n, sim.posp.data_ptr(), sim.velr.data_ptr(), sim.prev.data_ptr(),
+                                   *[t.data_ptr() for t in soa], s), "to_soa")
+    _lib.check(L.sphb_state_from_soa(0, n, *[t.data_ptr() for t in soa], sim.posp.data_ptr(),
+                                     sim.velr.data_ptr(), sim.prev.data_ptr(), s), "from_soa")
+    torch.cuda.synchronize()
+    assert sim.error() is None, sim.error()
+    print("ok", precision, block, integ, sim.ws.sort_info(), flush=True)
