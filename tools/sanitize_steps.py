@@ -36,3 +36,12 @@ for precision, block, integ in ((0, 128, "verlet"), (0, 256, "verlet"), (1, 128,
     torch.cuda.synchronize()
     assert sim.error() is None, sim.error()
     print("ok", precision, block, integ, sim.ws.sort_info(), flush=True)
+
+# the X-slab exchange kernels (slab.cu) through two virtual ranks on this GPU
+from paper_1110_3711_b200 import dslab  # noqa: E402
+
+ds = dslab.DeviceSlabSim(system, prm, dslab.DevLoopbackComm(2), precision=0)
+for _ in range(4):
+    ds.step()
+torch.cuda.synchronize()
+print("ok slabs", flush=True)
