@@ -361,7 +361,14 @@ def run_slabs(args, cfg_name, system, prm, prec, world, rank, local):
     recs = sim.records(first, first + args.steps)
     true_pairs = float(np.mean(recs["hits_ordered"].astype(np.float64))) / 2
     evals = float(np.mean(recs["force_evals"].astype(np.float64)))
+    cand = float(np.mean(recs["candidate_pairs"].astype(np.float64)))
     value = system.n * args.steps / (total_ms * 1e-3)
+    # roofline of the interaction kernel per GPU: the all-reduced counters over the ranks'
+    # mean interaction time (CUDA events around each rank's launch, the last <= 64 steps)
+    pi_rank_ms = sim.measured_pi_ms()
+    hbm, hbm_src, fp32, fp32_src = peaks()
+    achieved = (FLOP_PER_CAND * cand + FLOP_PER_EVAL * evals) / world / \
+        (float(np.mean(pi_rank_ms)) * 1e-3) / 1e12
     owned = torch.tensor([sim.n_owned_max], device="cuda", dtype=torch.int64)
     dist.all_reduce(owned, op=dist.ReduceOp.MAX)
     line = {
@@ -381,6 +388,11 @@ def run_slabs(args, cfg_name, system, prm, prec, world, rank, local):
         "interactions_per_s": true_pairs * args.steps / (total_ms * 1e-3),
         "pair_evals_per_s": evals * args.steps / (total_ms * 1e-3),
         "gpu_launches": args.steps * sim.launches_per_step(),
+        "roofline": {"bound": "fp32", "kernel": "k_interact_v8 (per GPU, owned targets)",
+                     "achieved": achieved, "peak": fp32, "unit": "TFLOP/s", "frac": achieved / fp32,
+                     "traffic": None,
+                     "work": f"{FLOP_PER_CAND}*candidates + {FLOP_PER_EVAL}*evals per step / GPUs",
+                     "pi_ms_per_rank": [float(v) for v in pi_rank_ms], "peak_source": fp32_src},
         "clocks": clk,
     }
     if e2e_value is not None:
