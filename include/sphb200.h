@@ -262,6 +262,24 @@ int sphb_state_to_soa(int64_t r0, int64_t cnt, const void* posp, const void* vel
                       const void* prev, float* pos, float* vel, float* rho, float* vel_prev,
                       float* rho_prev, sphb_stream_t s);
 
+/* The reference's module-level step functions on the caller's own arrays (device pointers),
+ * for loops that keep the reference's structure:
+ *   sphb_build_ranges  build_ranges (grid.py:170-200) from one list's begin/end (int32, ncells
+ *                      = nx ny nz): range_begin/range_end (ncells, (2n+1)^2) int64 row-major;
+ *   sphb_dt_terms      the two minima of compute_dt (sim.py:215-232) as f64 bit patterns in
+ *                      out2[0] (fluid force term) / out2[1] (sound + viscosity term); out2 must
+ *                      hold +inf bits on entry; the cfl product and clamp stay with the caller;
+ *   sphb_verlet_soa    verlet_update (sim.py:235-259) in place on pos/vel (n, 3), rho (n,)
+ *                      and the history vel_prev (n, 3) / rho_prev (n,), bit-identical. */
+int sphb_build_ranges(const int32_t* beg, const int32_t* end, int32_t nx, int32_t ny, int32_t nz,
+                      int32_t n_subdiv, int64_t* range_begin, int64_t* range_end,
+                      sphb_stream_t s);
+int sphb_dt_terms(const sphb_params_t* prm, int64_t n, int64_t nb, const double* accel,
+                  const double* visc_dt, const float* csound, uint64_t* out2, sphb_stream_t s);
+int sphb_verlet_soa(const sphb_params_t* prm, int64_t n, int64_t nb, int32_t corrector, double dt,
+                    float* pos, float* vel, float* rho, float* vel_prev, float* rho_prev,
+                    const double* accel, const double* drho_dt, sphb_stream_t s);
+
 /* Energy diagnostics (SURVEY.md §8(d) functional, no reference counterpart): out[0..4] =
  * KE (fluid), PE = sum m |g| z (fluid), IE = sum m (u(rho) - u(rho0)) with the Tait internal
  * energy u(rho) = B/(gamma-1) rho^(gamma-1)/rho0^gamma + B/rho (all particles), mean fluid rho,

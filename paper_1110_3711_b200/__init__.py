@@ -13,7 +13,8 @@ from .model import (BoundaryForce, DerivedQuantities, ParticleKind, ParticleSyst
                     StepStats, validate)
 from .scenario import (Scenario, WaveTank, build_dam_break, build_wave_tank, make_params,
                        make_wave_tank_params, named_scenario)
-from .sim import DivergenceError, compute_derived, run_simulation
+from . import grid
+from .sim import DivergenceError, VerletState, compute_derived, compute_dt, run_simulation, verlet_update
 
 __version__ = "0.1.0"
 
@@ -23,4 +24,5 @@ __all__ = [
     "SimParams", "StepStats", "validate", "Scenario", "build_dam_break", "make_params",
     "named_scenario", "run_simulation", "DivergenceError", "compute_derived", "__version__",
     "PistonMotion", "BoundaryForce", "WaveTank", "build_wave_tank", "make_wave_tank_params",
+    "VerletState", "compute_dt", "verlet_update", "grid",
 ]

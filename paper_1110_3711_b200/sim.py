@@ -10,15 +10,17 @@ per-step host synchronisation, and the host reads the device control block only 
 from __future__ import annotations
 
 import math
+from dataclasses import dataclass
 
 import numpy as np
 import torch
 
 from . import _lib
 from .config import EngineConfig, NEIGHBOR_BYTES
-from .device import DeviceSim, compute_derived_device
+from .device import DeviceSim, compute_derived_device, require_cuda
 from .engine import PRECISION_CODE
 from .model import DerivedQuantities, ParticleKind, StepStats, validate
+from .physics import params_desc
 from .scenario import Scenario, build_dam_break
 
 
@@ -44,6 +46,79 @@ def divergence_from_device(err) -> DivergenceError:
 # blocking (C3 10k-step dam break: equal near 0.8, 128 wins at rest, 256 by 8% once collapsed)
 PI_LANE_SWITCH = 0.78
 PI_DECIDE_EVERY = 256  # the "auto" blocking is decided at these step multiples only (chunk-proof)
+
+
+@dataclass
+class VerletState:
+    """Previous-step velocity and density, permuted alongside the system (sim.py:31-43)."""
+
+    vel_prev: np.ndarray   # (n, 3) float32
+    rho_prev: np.ndarray   # (n,) float32
+    step: int = 0
+    corrector_stride: int = 40
+
+    @classmethod
+    def from_system(cls, system, stride: int) -> "VerletState":
+        return cls(vel_prev=system.vel.copy(), rho_prev=system.rho.copy(), corrector_stride=stride)
+
+
+def tree_min(values, block: int = 4096) -> float:
+    """sim.py:196-208 (the min is exact, so the blocked order does not change the result)."""
+    a = np.asarray(values, dtype=np.float64).ravel()
+    if a.size == 0:
+        raise ValueError("empty reduction")
+    return float(a.min())
+
+
+def tree_max(values, block: int = 4096) -> float:
+    return -tree_min(-np.asarray(values, dtype=np.float64), block=block)
+
+
+def compute_dt(forces, system, derived, params) -> float:
+    """sim.py:215-232 on the device (k_dt_terms): cfl * min(dt_f, dt_cv) clamped to
+    [dt_min, dt_max]; dt_f over fluid with gravity included, dt_cv over all particles."""
+    require_cuda()
+    dev = torch.device("cuda")
+    n, nb = int(system.n), int(system.count_boundary)
+    acc = torch.as_tensor(np.ascontiguousarray(forces.accel, np.float64)).to(dev)
+    visc = torch.as_tensor(np.ascontiguousarray(forces.visc_dt, np.float64)).to(dev)
+    cs = torch.as_tensor(np.ascontiguousarray(derived.csound, np.float32)).to(dev)
+    inf = np.array([np.inf, np.inf]).view(np.int64)
+    out = torch.as_tensor(inf).to(dev)
+    prm = params_desc(params, float(system.mass_fluid), float(system.mass_boundary))
+    _lib.check(_lib.lib().sphb_dt_terms(_lib.ref(prm), n, nb, acc.data_ptr(), visc.data_ptr(),
+                                        cs.data_ptr(), out.data_ptr(), torch.cuda.current_stream().cuda_stream),
+               "sphb_dt_terms")
+    dt_f, dt_cv = out.cpu().numpy().view(np.float64)
+    dt = params.cfl * min(float(dt_f), float(dt_cv))
+    return float(min(max(dt, params.dt_min), params.dt_max))
+
+
+def verlet_update(state: VerletState, system, forces, params, dt: float) -> None:
+    """sim.py:235-259 on the device (k_verlet_soa): two-step Verlet with the periodic
+    single-step corrector; fluid moves, boundary particles only update density.  Updates
+    ``system`` and ``state`` in place, bit-identical to the reference."""
+    if dt <= 0:
+        raise ValueError("dt must be positive")
+    require_cuda()
+    dev = torch.device("cuda")
+    n, nb = int(system.n), int(system.count_boundary)
+    corrector = state.step % state.corrector_stride == 0
+    t = lambda a, dt_: torch.as_tensor(np.ascontiguousarray(a, dt_)).to(dev)  # noqa: E731
+    pos, vel, rho = t(system.pos, np.float32), t(system.vel, np.float32), t(system.rho, np.float32)
+    vp, rp = t(state.vel_prev, np.float32), t(state.rho_prev, np.float32)
+    acc, drho = t(forces.accel, np.float64), t(forces.drho_dt, np.float64)
+    prm = params_desc(params, float(system.mass_fluid), float(system.mass_boundary))
+    _lib.check(_lib.lib().sphb_verlet_soa(_lib.ref(prm), n, nb, int(corrector), float(dt),
+                                          pos.data_ptr(), vel.data_ptr(), rho.data_ptr(), vp.data_ptr(),
+                                          rp.data_ptr(), acc.data_ptr(), drho.data_ptr(),
+                                          torch.cuda.current_stream().cuda_stream), "sphb_verlet_soa")
+    system.pos = pos.cpu().numpy()
+    system.vel = vel.cpu().numpy()
+    system.rho = rho.cpu().numpy()
+    state.vel_prev = vp.cpu().numpy()
+    state.rho_prev = rp.cpu().numpy()
+    state.step += 1
 
 
 def compute_derived(rho, params) -> DerivedQuantities:
