@@ -45,3 +45,19 @@ for _ in range(4):
     ds.step()
 torch.cuda.synchronize()
 print("ok slabs", flush=True)
+
+# the module-level step functions (stepfn.cu, grid.py)
+import types  # noqa: E402
+
+import numpy as np  # noqa: E402
+
+s2 = sph.build_dam_break(sc, prm)
+g2 = sph.grid.assign_cells(s2.pos, prm)
+s2, _ = sph.grid.reorder(s2, g2)
+ci = sph.grid.build_cell_index(s2, g2)
+sph.grid.build_dual_ranges(ci, g2.dims, 1)
+f2 = types.SimpleNamespace(accel=np.zeros((s2.n, 3)), drho_dt=np.zeros(s2.n), visc_dt=np.zeros(s2.n))
+dt2 = sph.compute_dt(f2, s2, sph.compute_derived(s2.rho, prm), prm)
+sph.verlet_update(sph.VerletState.from_system(s2, 40), s2, f2, prm, dt2)
+torch.cuda.synchronize()
+print("ok step functions", flush=True)
