@@ -112,3 +112,35 @@ def test_compute_dt_and_verlet_match_reference(name, variant):
     assert np.array_equal(system.rho, z[f"{variant}_step1nc_rho"])
     with pytest.raises(ValueError, match="dt must be positive"):
         sph.verlet_update(st, system, forces, prm, 0.0)
+
+
+def test_reference_loop_structure_with_device_functions():
+    """sim.py:300-350's loop written with this package's module-level functions and engine
+    (FP64) reproduces the reference's own 45-step trajectory bit for bit (dt per step, final
+    state): the parity trick of SURVEY.md §8(b) on the GPU box, where the reference is absent."""
+    from conftest import initial_state
+    z = golden("traj_dp025_g.npz")
+    prm = oracle.params_from_npz(z)
+    pos, vel, rho, ids, nb, mf, mb = initial_state(z)
+    n = pos.shape[0]
+    system = sph.ParticleSystem(count_fluid=n - nb, count_boundary=nb, pos=pos.copy(), vel=vel.copy(),
+                                rho=rho.copy(), mass_fluid=mf, mass_boundary=mb,
+                                ptype=np.r_[np.zeros(nb, np.uint8), np.ones(n - nb, np.uint8)],
+                                id=ids.copy())
+    state = sph.VerletState.from_system(system, prm.verlet_corrector_stride)
+    engine = sph.make_engine(sph.EngineConfig(engine="gather", symmetry=False,
+                                              gather_variant="slowcellsh", precision="fp64"))
+    dts = []
+    for step in range(int(z["dt"].shape[0])):
+        grid = G.assign_cells(system.pos, prm)
+        assert grid.out_of_domain.size == 0
+        G.reorder(system, grid, extra_arrays=(state.vel_prev, state.rho_prev))
+        cindex = G.build_cell_index(system, grid)
+        derived = sph.compute_derived(system.rho, prm)
+        forces = engine.compute(system, derived, grid, cindex, prm)
+        dt = sph.compute_dt(forces, system, derived, prm)
+        sph.verlet_update(state, system, forces, prm, dt)
+        dts.append(dt)
+    assert np.array_equal(np.array(dts), z["dt"])
+    for f, key in (("pos", "final_pos"), ("vel", "final_vel"), ("rho", "final_rho"), ("id", "final_id")):
+        assert np.array_equal(getattr(system, f), z[key]), f
