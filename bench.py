@@ -420,9 +420,16 @@ def main():
         return
     import torch
     import torch.distributed as dist
+    # SPHB_DIST_BACKEND=gloo runs the N-rank path with ranks sharing the visible GPUs (a code-
+    # path check on a single-GPU box; the numbers are not scaling numbers)
+    backend = os.environ.get("SPHB_DIST_BACKEND", "nccl")
+    local = local % max(1, torch.cuda.device_count()) if backend != "nccl" else local
     torch.cuda.set_device(local)
     if world > 1 or args.slab_path:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     import paper_1110_3711_b200 as sph
     from paper_1110_3711_b200 import _lib
     from paper_1110_3711_b200.device import DeviceSim

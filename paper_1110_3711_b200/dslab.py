@@ -75,7 +75,9 @@ class DevLoopbackComm:
 
 
 class DevDistComm:
-    """One rank per process over torch.distributed (NCCL: device buffers, no host copies)."""
+    """One rank per process over torch.distributed.  NCCL (the production transport) moves the
+    device buffers directly; over gloo (several processes sharing one GPU, the multi-process
+    test on a single-GPU box) the same calls stage through host memory."""
 
     def __init__(self):
         import torch.distributed as dist
@@ -83,39 +85,54 @@ class DevDistComm:
         self.rank = dist.get_rank()
         self.nranks = dist.get_world_size()
         self.local_ranks = [self.rank]
+        self.host = dist.get_backend() != "nccl"
 
     def allreduce(self, tensors, op: str):
         d = self.dist
-        d.all_reduce(tensors[0], op={"min": d.ReduceOp.MIN, "max": d.ReduceOp.MAX,
-                                      "sum": d.ReduceOp.SUM}[op])
+        rop = {"min": d.ReduceOp.MIN, "max": d.ReduceOp.MAX, "sum": d.ReduceOp.SUM}[op]
+        t = tensors[0]
+        if self.host:
+            h = t.cpu()
+            d.all_reduce(h, op=rop)
+            t.copy_(h)
+        else:
+            d.all_reduce(t, op=rop)
 
     def allgather(self, tensors):
-        t = tensors[0]
+        t = tensors[0].contiguous()
+        if self.host:
+            h = t.cpu()
+            parts = [torch.empty_like(h) for _ in range(self.nranks)]
+            self.dist.all_gather(parts, h)
+            return [torch.stack(parts).to(t.device)]
         out = torch.empty((self.nranks,) + tuple(t.shape), dtype=t.dtype, device=t.device)
-        self.dist.all_gather_into_tensor(out, t.contiguous())
+        self.dist.all_gather_into_tensor(out, t)
         return [out]
 
     def sendrecv(self, items):
         d, r, n = self.dist, self.rank, self.nranks
         it = items[0]
-        ops = []
-        if r > 0:
-            buf, rows = it["send_l"]
+        ops, landing = [], []
+        for side, peer, ok in (("l", r - 1, r > 0), ("r", r + 1, r < n - 1)):
+            if not ok:
+                continue
+            buf, rows = it["send_" + side]
             if rows:
-                ops.append(d.P2POp(d.isend, buf[:rows], r - 1))
-            buf, rows = it["recv_l"]
+                src = buf[:rows].cpu() if self.host else buf[:rows]
+                ops.append(d.P2POp(d.isend, src, peer))
+            buf, rows = it["recv_" + side]
             if rows:
-                ops.append(d.P2POp(d.irecv, buf[:rows], r - 1))
-        if r < n - 1:
-            buf, rows = it["send_r"]
-            if rows:
-                ops.append(d.P2POp(d.isend, buf[:rows], r + 1))
-            buf, rows = it["recv_r"]
-            if rows:
-                ops.append(d.P2POp(d.irecv, buf[:rows], r + 1))
+                if self.host:
+                    tmp = torch.empty(buf[:rows].shape, dtype=buf.dtype)
+                    landing.append((buf, rows, tmp))
+                    ops.append(d.P2POp(d.irecv, tmp, peer))
+                else:
+                    ops.append(d.P2POp(d.irecv, buf[:rows], peer))
         if ops:
             for w in d.batch_isend_irecv(ops):
                 w.wait()
+        for buf, rows, tmp in landing:
+            buf[:rows].copy_(tmp)
 
 
 # ------------------------------------------------------------------ one rank

@@ -605,6 +605,41 @@ def test_device_resident_slabs_match_single_domain(nslabs, precision):
     assert int(fl.sum()) == system.count_fluid
 
 
+def test_device_slabs_two_processes(tmp_path):
+    """DeviceSlabSim with DevDistComm across two real processes (torchrun, gloo: they share
+    this box's GPU; NCCL only changes the transport): every step's dt and counters equal the
+    single-domain FP64 run's, the id set is conserved and the 20-step state matches."""
+    import os
+    import socket
+    import subprocess
+    import sys
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    out = tmp_path / "mp.npz"
+    steps = 20
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    proc = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                           "--nproc-per-node", "2", "--master-addr", "127.0.0.1", "--master-port",
+                           str(port), os.path.join(root, "tests", "slab_mp_worker.py"), str(out),
+                           str(steps)], capture_output=True, text=True, timeout=600, cwd=root)
+    assert proc.returncode == 0, proc.stderr[-3000:]
+    z = np.load(out)
+    sc = sph.Scenario(dp=0.006)
+    prm = sph.make_params(sc)
+    ref, stats = sph.run_simulation(sph.build_dam_break(sc, prm), prm, gather_cfg("slowcellsh", "fp64"),
+                                    max_steps=steps, stage_timing=False)
+    assert len(z["bounds"]) == 3
+    assert np.array_equal(z["dt"], np.array([s.dt for s in stats]))
+    got = np.stack([z["cand"], z["hits"] // 2, z["evals"], z["ff"]], 1).astype(np.int64)
+    want = np.array([[s.candidate_pairs, s.true_pairs, s.force_evals, s.ff_force_evals] for s in stats])
+    assert np.array_equal(got, want)
+    b = np.argsort(ref.id)
+    assert np.array_equal(z["id"], ref.id[b])
+    for f in ("pos", "vel", "rho"):
+        assert oracle.rel_linf(z[f], getattr(ref, f)[b]) <= 1e-9, f
+
+
 def test_device_slabs_rebalance_keeps_results():
     """Time-balanced slab bounds (DeviceSlabSim.rebalance): forced uneven times move the
     bounds by several columns (multi-hop settle), a measured rebalance runs every 6 steps; ids
