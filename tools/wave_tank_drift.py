@@ -1,7 +1,7 @@
 """C5 (BASELINE.json config 5): piston wave tank, 1000 steps, energy / mass drift from the
 device diagnostics (sphb_energy), on one GPU.  Writes a JSON summary (argv[2]).
 
-  python tools/wave_tank_drift.py [c5|c5_small] [out.json] [steps] [every]
+  python tools/wave_tank_drift.py [c5|c5_small] [out.json] [steps] [every] [128|256|auto]
 """
 import json
 import sys
@@ -18,12 +18,15 @@ name = sys.argv[1] if len(sys.argv) > 1 else "c5"
 out = sys.argv[2] if len(sys.argv) > 2 else None
 steps = int(sys.argv[3]) if len(sys.argv) > 3 else 1000
 every = int(sys.argv[4]) if len(sys.argv) > 4 else 50
+blocking = sys.argv[5] if len(sys.argv) > 5 else "auto"
 t0 = time.time()
 sc = sph.named_scenario(name)
 prm = sph.make_wave_tank_params(sc)
 system = sph.build_wave_tank(sc, prm)
 t_build = time.time() - t0
 sim = DeviceSim(system, prm, reach=1, record_capacity=steps + 8)
+if blocking != "auto":
+    sim.set_pi_block(int(blocking))
 rows = []
 e = sim.energy()
 rows.append(dict(step=0, t=0.0, **e))
@@ -41,6 +44,8 @@ while done < steps:
     gpu_ms += ev0.elapsed_time(ev1)
     done += k
     c = sim.ctrl_host()
+    if blocking == "auto" and sim.pi_block == 128 and sim.pi_lane_use(c) < sph.sim.PI_LANE_SWITCH:
+        sim.set_pi_block(256)  # run_simulation's rule
     err = sim.error()
     if err is not None:
         raise SystemExit(f"diverged: {err}")
@@ -53,7 +58,7 @@ final = rows[-1]
 summary = dict(
     config=name, particles=system.n, fluid=system.count_fluid, boundary=system.count_boundary,
     piston_particles=pm.id1 - pm.id0, piston=dict(stroke=pm.stroke, period=pm.period),
-    steps=steps, t_end=final["t"], host_build_s=t_build, gpu_ms_per_step=gpu_ms / steps,
+    steps=steps, blocking=blocking, pi_block_final=sim.pi_block, t_end=final["t"], host_build_s=t_build, gpu_ms_per_step=gpu_ms / steps,
     particle_steps_per_s=system.n * steps / (gpu_ms * 1e-3),
     mean_true_pairs=float(np.mean(recs["hits_ordered"])) / 2,
     energy0=e0, energy_final=final,
