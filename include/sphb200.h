@@ -141,7 +141,7 @@ int sphb_workspace_reset(sphb_workspace_t* ws, sphb_stream_t s);
  * (grid.py:107-109 stable order); the choice is made on the device. */
 int sphb_workspace_set_mover_cap(sphb_workspace_t* ws, int64_t cap);
 /* Targets per interaction block of the FP32 kernel: 128 (default: 4-warp CTAs, two per SM,
- * <= 2,304 staged candidates) or 256 (8-warp CTAs, one per SM, <= 3,456 staged candidates:
+ * <= 2,304 staged candidates) or 256 (8-warp CTAs, one per SM, <= 4,224 staged candidates:
  * fewer idle lanes when cells hold uneven particle counts, e.g. after a dam collapses).
  * Results agree within the FP32 tolerance (accumulation order); FP64 always uses 128. */
 int sphb_workspace_set_pi_block(sphb_workspace_t* ws, int32_t targets);

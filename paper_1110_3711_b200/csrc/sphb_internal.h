@@ -66,7 +66,7 @@ int sort_pass_count(const sphb_grid_t& g);
 int64_t nl_launch_count(const sphb_grid_t& g, int64_t n);
 
 // interact.cu, compiled twice: pi128 (4-warp CTAs, 128-target blocks over <= 2,304 staged
-// candidates, 2 CTAs/SM; the default) and pi256 (8-warp CTAs, 256-target blocks over <= 3,456
+// candidates, 2 CTAs/SM; the default) and pi256 (8-warp CTAs, 256-target blocks over <= 4,224
 // staged candidates, 1 CTA/SM: fewer idle lanes once cells fill unevenly)
 #define SPHB_DECLARE_PI(NS)                                                                     \
   namespace NS {                                                                                \
