@@ -16,6 +16,7 @@ def test_usage_error_exit_code(capsys):
     assert cli.main(["run", "--engine", "warp"]) == cli.EXIT_USAGE
     assert cli.main(["run", "--dp", "0.03"]) == cli.EXIT_USAGE  # neither --steps nor --tend
     assert cli.main(["run", "--steps", "1", "--precision", "fp16"]) == cli.EXIT_USAGE
+    assert cli.main(["run", "--steps", "1", "--pi-block", "64"]) == cli.EXIT_USAGE
     assert "error" in capsys.readouterr().err
 
 
@@ -111,6 +112,7 @@ def test_run_command_writes_snapshots_and_stats(tmp_path, capsys):
 @pytest.mark.gpu
 def test_run_command_gather_cells_and_verify(capsys):
     assert cli.main(["run", "--dp", "0.03", "--steps", "2", "--cells", "h/2"]) == 0
+    assert cli.main(["run", "--dp", "0.03", "--steps", "2", "--pi-block", "256"]) == 0
     assert cli.main(["run", "--dp", "0.03", "--steps", "2", "--engine", "gather", "--symmetry",
                      "off", "--gather-variant", "slowcellsh"]) == 0
     assert cli.main(["run", "--dp", "0.03", "--steps", "3", "--verify"]) == 0
