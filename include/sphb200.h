@@ -200,6 +200,11 @@ int sphb_reorder(const sphb_params_t* prm, const sphb_grid_t* grid, int64_t n,
                  void* velr_out, void* prev_out, int64_t* id_out, void* aux_out,
                  int32_t* cell_out, const sphb_ctrl_t* ctrl, sphb_stream_t s);
 
+/* The per-list per-cell histogram of sort keys that are already known (e.g. carried through a
+ * slab exchange), accumulated into the workspace for sphb_cell_ranges / sphb_sort_ranges. */
+int sphb_cell_hist(sphb_workspace_t* ws, const sphb_grid_t* grid, const uint32_t* keys, int64_t n,
+                   const sphb_ctrl_t* ctrl, sphb_stream_t s);
+
 /* K4 -- build_cell_index (grid.py:123-144): warp-level exclusive scan of the per-list
  * histogram from sphb_cell_keys.  beg/end hold 2*ncells int32: [0,ncells) boundary list,
  * [ncells, 2*ncells) fluid list already offset by nb; empty cells carry the running prefix.
@@ -309,11 +314,13 @@ int sphb_slab_scatter(const sphb_grid_t* grid, int64_t n, int64_t nb, const uint
                       const int64_t* id, int32_t x0, int32_t x1, const uint32_t* tile_offsets,
                       const void* posp, const void* velr, const void* prev,
                       const int64_t* keep_bases, void* nposp, void* nvelr, void* nprev,
-                      int64_t* nid, void* send_l, void* send_r, const int64_t* sections,
-                      sphb_stream_t s);
-/* rows [r0, r0 + cnt) of a received packed buffer -> next arrays rows [dst, dst + cnt). */
+                      int64_t* nid, uint32_t* nkeys, void* send_l, void* send_r,
+                      const int64_t* sections, sphb_stream_t s);
+/* rows [r0, r0 + cnt) of a received packed buffer -> next arrays rows [dst, dst + cnt).
+ * The packed rows carry the sender's sort keys: with nkeys (and nkeys of the scatter) the next
+ * step needs no K1, only sphb_cell_hist on those keys. */
 int sphb_slab_unpack(const void* buf, int64_t r0, int64_t cnt, int64_t dst, void* nposp,
-                     void* nvelr, void* nprev, int64_t* nid, sphb_stream_t s);
+                     void* nvelr, void* nprev, int64_t* nid, uint32_t* nkeys, sphb_stream_t s);
 
 /* Closes the step: dt/counters into rec[step % rec_capacity], t_sim += dt, step += 1. */
 int sphb_step_end(sphb_ctrl_t* ctrl, const sphb_params_t* prm, sphb_step_record_t* rec,

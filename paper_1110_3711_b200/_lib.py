@@ -114,8 +114,9 @@ def lib():
         "sphb_slab_tiles": ([c_i64], c_i64),
         "sphb_slab_count": ([P, c_i64, c_i64, P, P, c_i32, c_i32, P, P, P], c_i32),
         "sphb_slab_scatter": ([P, c_i64, c_i64, P, P, c_i32, c_i32, P, P, P, P, P, P, P, P, P, P,
-                               P, P, P], c_i32),
-        "sphb_slab_unpack": ([P, c_i64, c_i64, c_i64, P, P, P, P, P], c_i32),
+                               P, P, P, P], c_i32),
+        "sphb_slab_unpack": ([P, c_i64, c_i64, c_i64, P, P, P, P, P, P], c_i32),
+        "sphb_cell_hist": ([P, P, P, c_i64, P, P], c_i32),
         "sphb_step": ([P, P, P, c_i64, c_i64, P, P, P, c_i64, P], c_i32),
         "sphb_state_from_soa": ([c_i64, c_i64, P, P, P, P, P, P, P, P, P], c_i32),
         "sphb_state_to_soa": ([c_i64, c_i64, P, P, P, P, P, P, P, P, P], c_i32),
@@ -135,7 +136,8 @@ def lib():
 EXPORTED = ("sphb_last_error", "sphb_version", "sphb_workspace_create", "sphb_workspace_destroy",
             "sphb_workspace_reset", "sphb_workspace_bytes",
             "sphb_workspace_set_mover_cap", "sphb_workspace_sort_info", "sphb_workspace_set_pi_block", "sphb_ctrl_init", "sphb_cell_keys",
-            "sphb_sort", "sphb_sort_ranges", "sphb_nl_build", "sphb_reorder", "sphb_cell_ranges", "sphb_cell_ranges_from_sorted",
+            "sphb_sort", "sphb_sort_ranges", "sphb_nl_build", "sphb_reorder", "sphb_cell_ranges",
+            "sphb_cell_ranges_from_sorted", "sphb_cell_hist",
             "sphb_interact", "sphb_step_begin", "sphb_integrate", "sphb_step_end", "sphb_step",
             "sphb_step_launch_count", "sphb_integrate_stage", "sphb_energy", "sphb_slab_tiles",
             "sphb_slab_count", "sphb_slab_scatter", "sphb_slab_unpack", "sphb_state_from_soa",

@@ -291,6 +291,15 @@ int sphb_nl_build(sphb_workspace_t* ws, const sphb_grid_t* grid, const void* pos
   return launch_cell_ranges(ws, *grid, beg, end, ctrl, cs);
 }
 
+int sphb_cell_hist(sphb_workspace_t* ws, const sphb_grid_t* grid, const uint32_t* keys, int64_t n,
+                   const sphb_ctrl_t* ctrl, sphb_stream_t s) {
+  SPHB_NONNULL(ws);
+  if (int rc = check_grid(grid)) return rc;
+  if (n < 0) return sphb_set_error(SPHB_E_INVALID, "n < 0");
+  if (n > 0) SPHB_NONNULL(keys);
+  return launch_cell_hist(ws, *grid, keys, n, ctrl, (cudaStream_t)s);
+}
+
 int sphb_cell_ranges(sphb_workspace_t* ws, const sphb_grid_t* grid, int32_t* beg, int32_t* end,
                      const sphb_ctrl_t* ctrl, sphb_stream_t s) {
   SPHB_NONNULL(ws);
@@ -477,8 +486,8 @@ int sphb_slab_scatter(const sphb_grid_t* grid, int64_t n, int64_t nb, const uint
                       const int64_t* id, int32_t x0, int32_t x1, const uint32_t* tile_offsets,
                       const void* posp, const void* velr, const void* prev,
                       const int64_t* keep_bases, void* nposp, void* nvelr, void* nprev,
-                      int64_t* nid, void* send_l, void* send_r, const int64_t* sections,
-                      sphb_stream_t s) {
+                      int64_t* nid, uint32_t* nkeys, void* send_l, void* send_r,
+                      const int64_t* sections, sphb_stream_t s) {
   if (int rc = check_grid(grid)) return rc;
   SPHB_NONNULL(keep_bases);
   SPHB_NONNULL(sections);
@@ -492,19 +501,19 @@ int sphb_slab_scatter(const sphb_grid_t* grid, int64_t n, int64_t nb, const uint
   }
   return launch_slab_scatter(*grid, n, nb, keys, id, x0, x1, tile_offsets, (const float4*)posp,
                              (const float4*)velr, (const float4*)prev, keep_bases, (float4*)nposp,
-                             (float4*)nvelr, (float4*)nprev, nid, send_l, send_r, sections,
-                             (cudaStream_t)s);
+                             (float4*)nvelr, (float4*)nprev, nid, nkeys, send_l, send_r,
+                             sections, (cudaStream_t)s);
 }
 
 int sphb_slab_unpack(const void* buf, int64_t r0, int64_t cnt, int64_t dst, void* nposp,
-                     void* nvelr, void* nprev, int64_t* nid, sphb_stream_t s) {
+                     void* nvelr, void* nprev, int64_t* nid, uint32_t* nkeys, sphb_stream_t s) {
   if (cnt < 0 || r0 < 0 || dst < 0) return sphb_set_error(SPHB_E_INVALID, "bad unpack range");
   if (cnt > 0) {
     SPHB_NONNULL(buf); SPHB_NONNULL(nposp); SPHB_NONNULL(nvelr); SPHB_NONNULL(nprev);
     SPHB_NONNULL(nid);
   }
   return launch_slab_unpack(buf, r0, cnt, dst, (float4*)nposp, (float4*)nvelr, (float4*)nprev, nid,
-                            (cudaStream_t)s);
+                            nkeys, (cudaStream_t)s);
 }
 
 int sphb_state_from_soa(int64_t r0, int64_t cnt, const float* pos, const float* vel,

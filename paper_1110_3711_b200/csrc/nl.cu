@@ -60,6 +60,27 @@ __global__ void __launch_bounds__(256) k_cell_keys(sphb_grid_t g, const float4* 
   }
 }
 
+// per-list per-cell histogram of known sort keys (key = list << cellbits | cell)
+__global__ void __launch_bounds__(256) k_hist_keys(const uint32_t* __restrict__ keys, int64_t n,
+                                                   int cellbits, int64_t ncells,
+                                                   uint32_t* __restrict__ cnt,
+                                                   const sphb_ctrl_t* ctrl) {
+  if (ctrl && !step_live(ctrl)) return;
+  const int lane = threadIdx.x & 31;
+  const uint32_t cm = (1u << cellbits) - 1u;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n; base += stride) {
+    const int64_t i = base + threadIdx.x;
+    int64_t slot = -1;
+    if (i < n) {
+      const uint32_t k = keys[i];
+      if ((k >> cellbits) <= 1u && (k & cm) < (uint32_t)ncells) slot = (k >> cellbits) * ncells + (k & cm);
+    }
+    const uint32_t peers = __match_any_sync(SPHB_FULL, (unsigned long long)slot);
+    if (slot >= 0 && lane == __ffs(peers) - 1) atomicAdd(&cnt[slot], (uint32_t)__popc(peers));
+  }
+}
+
 __global__ void __launch_bounds__(256) k_hist_sorted(const int32_t* __restrict__ cell, int64_t n,
                                                      int64_t nb, uint32_t* __restrict__ cnt,
                                                      int64_t ncells) {
@@ -612,6 +633,15 @@ int launch_cell_keys(sphb_workspace* ws, const sphb_grid_t& g, const float4* pos
   k_cell_keys<<<grid_for(n, 256), 256, 0, s>>>(g, posp, n, nb, cellbits_of(g), keys, cell_out,
                                                 ws->cnt, nc, ctrl);
   return sphb_check_launch("k_cell_keys");
+}
+
+int launch_cell_hist(sphb_workspace* ws, const sphb_grid_t& g, const uint32_t* keys, int64_t n,
+                     const sphb_ctrl_t* ctrl, cudaStream_t s) {
+  const int64_t nc = ncells_of(g);
+  if (n > ws->n_max || nc > ws->ncells_max) return sphb_set_error(SPHB_E_CAPACITY, "n/ncells exceed workspace");
+  if (n == 0) return SPHB_OK;
+  k_hist_keys<<<grid_for(n, 256), 256, 0, s>>>(keys, n, cellbits_of(g), nc, ws->cnt, ctrl);
+  return sphb_check_launch("k_hist_keys");
 }
 
 int launch_hist_from_sorted(sphb_workspace* ws, const sphb_grid_t& g, const int32_t* cell_sorted,

@@ -31,7 +31,8 @@ constexpr int NCAT = 10;  // category c = 2 * kind + list, kind in {keep, migL, 
 struct SlabRow {  // 64 B packed exchange row
   float4 posp, velr, prev;
   long long id;
-  long long pad;
+  uint32_t key;  // the sender's K7 sort key (global grid): the receiver needs no K1
+  uint32_t pad;
 };
 
 __device__ __forceinline__ int col_of_key(uint32_t key, uint32_t cellmask, int nx) {
@@ -98,7 +99,8 @@ __global__ void __launch_bounds__(ST) k_slab_scatter(
     const uint32_t* tile_offsets, const float4* __restrict__ posp, const float4* __restrict__ velr,
     const float4* __restrict__ prev, const int64_t* __restrict__ id, int64_t keep_base_b,
     int64_t keep_base_f, float4* __restrict__ nposp, float4* __restrict__ nvelr,
-    float4* __restrict__ nprev, int64_t* __restrict__ nid, SlabRow* __restrict__ send_l,
+    float4* __restrict__ nprev, int64_t* __restrict__ nid, uint32_t* __restrict__ nkeys,
+    SlabRow* __restrict__ send_l,
     SlabRow* __restrict__ send_r, int64_t sec_l_migf, int64_t sec_l_halob, int64_t sec_l_halof,
     int64_t sec_r_migf, int64_t sec_r_halob, int64_t sec_r_halof) {
   __shared__ uint32_t swarp[ST / 32][NCAT];
@@ -119,6 +121,7 @@ __global__ void __launch_bounds__(ST) k_slab_scatter(
   row.velr = velr[i];
   row.prev = prev[i];
   row.id = id[i];
+  row.key = keys[i];
   row.pad = 0;
 #pragma unroll
   for (int c = 0; c < NCAT; ++c) {
@@ -132,6 +135,7 @@ __global__ void __launch_bounds__(ST) k_slab_scatter(
       nvelr[o] = row.velr;
       nprev[o] = row.prev;
       nid[o] = row.id;
+      if (nkeys) nkeys[o] = row.key;
     } else if (kind == 1 || kind == 3) {  // to the left neighbour
       const int64_t o = kind == 1 ? (list ? sec_l_migf : 0) + r : (list ? sec_l_halof : sec_l_halob) + r;
       SlabRow q = row;
@@ -149,13 +153,15 @@ __global__ void __launch_bounds__(ST) k_slab_scatter(
 // rows [r0, r0 + cnt) of a received buffer -> next arrays at dst
 __global__ void __launch_bounds__(ST) k_slab_unpack(const SlabRow* __restrict__ buf, int64_t r0,
                                                     int64_t cnt, int64_t dst, float4* nposp,
-                                                    float4* nvelr, float4* nprev, int64_t* nid) {
+                                                    float4* nvelr, float4* nprev, int64_t* nid,
+                                                    uint32_t* nkeys) {
   for (int64_t k = (int64_t)blockIdx.x * ST + threadIdx.x; k < cnt; k += (int64_t)gridDim.x * ST) {
     const SlabRow q = buf[r0 + k];
     nposp[dst + k] = q.posp;
     nvelr[dst + k] = q.velr;
     nprev[dst + k] = q.prev;
     nid[dst + k] = q.id;
+    if (nkeys) nkeys[dst + k] = q.key;
   }
 }
 
@@ -181,24 +187,25 @@ int launch_slab_scatter(const sphb_grid_t& g, int64_t n, int64_t nb, const uint3
                         const int64_t* id, int x0, int x1, const uint32_t* tile_offsets,
                         const float4* posp, const float4* velr, const float4* prev,
                         const int64_t* keep_bases, float4* nposp, float4* nvelr, float4* nprev,
-                        int64_t* nid, void* send_l, void* send_r, const int64_t* sections,
-                        cudaStream_t s) {
+                        int64_t* nid, uint32_t* nkeys, void* send_l, void* send_r,
+                        const int64_t* sections, cudaStream_t s) {
   const int64_t nt = slab_tiles(n);
   if (nt == 0) return SPHB_OK;
   const uint32_t cellmask = (1u << cellbits_of(g)) - 1u;
   k_slab_scatter<<<(unsigned)nt, ST, 0, s>>>(
       n, nb, keys, cellmask, g.dims[0], x0, x1, g.reach, tile_offsets, posp, velr, prev, id,
-      keep_bases[0], keep_bases[1], nposp, nvelr, nprev, nid, (SlabRow*)send_l, (SlabRow*)send_r,
+      keep_bases[0], keep_bases[1], nposp, nvelr, nprev, nid, nkeys, (SlabRow*)send_l, (SlabRow*)send_r,
       sections[0], sections[1], sections[2], sections[3], sections[4], sections[5]);
   return sphb_check_launch("k_slab_scatter");
 }
 
 int launch_slab_unpack(const void* buf, int64_t r0, int64_t cnt, int64_t dst, float4* nposp,
-                       float4* nvelr, float4* nprev, int64_t* nid, cudaStream_t s) {
+                       float4* nvelr, float4* nprev, int64_t* nid, uint32_t* nkeys,
+                       cudaStream_t s) {
   if (cnt <= 0) return SPHB_OK;
   int64_t blocks = (cnt + ST - 1) / ST;
   if (blocks > 148 * 8) blocks = 148 * 8;
   k_slab_unpack<<<(unsigned)blocks, ST, 0, s>>>((const SlabRow*)buf, r0, cnt, dst, nposp, nvelr,
-                                                nprev, nid);
+                                                nprev, nid, nkeys);
   return sphb_check_launch("k_slab_unpack");
 }

@@ -110,10 +110,13 @@ int launch_slab_scatter(const sphb_grid_t& g, int64_t n, int64_t nb, const uint3
                         const int64_t* id, int x0, int x1, const uint32_t* tile_offsets,
                         const float4* posp, const float4* velr, const float4* prev,
                         const int64_t* keep_bases, float4* nposp, float4* nvelr, float4* nprev,
-                        int64_t* nid, void* send_l, void* send_r, const int64_t* sections,
-                        cudaStream_t s);
+                        int64_t* nid, uint32_t* nkeys, void* send_l, void* send_r,
+                        const int64_t* sections, cudaStream_t s);
 int launch_slab_unpack(const void* buf, int64_t r0, int64_t cnt, int64_t dst, float4* nposp,
-                       float4* nvelr, float4* nprev, int64_t* nid, cudaStream_t s);
+                       float4* nvelr, float4* nprev, int64_t* nid, uint32_t* nkeys,
+                       cudaStream_t s);
+int launch_cell_hist(sphb_workspace* ws, const sphb_grid_t& g, const uint32_t* keys, int64_t n,
+                     const sphb_ctrl_t* ctrl, cudaStream_t s);
 int launch_step_end(sphb_ctrl_t* ctrl, const sphb_params_t& p, sphb_step_record_t* rec, int64_t cap,
                     cudaStream_t s);
 int launch_ctrl_init(sphb_ctrl_t* ctrl, int64_t max_steps, double t_end, cudaStream_t s);

@@ -4,8 +4,9 @@ Same decomposition as ``slab.SlabSimulation`` (whose torch implementation is kep
 host-logic restatement the CPU / gloo tests run), but the state never leaves the engine's SoA
 arrays: per step and per rank
 
-  1. K1 keys of the assembled arrays (owned rows + halo rows with id < 0), NL, interaction of
-     the owned target columns [x0, x1) only;
+  1. NL of the assembled arrays (owned rows + halo rows with id < 0) on the sort keys that
+     travelled with the rows (K7 wrote them; K1 only on upload), interaction of the owned
+     target columns [x0, x1) only;
   2. device all-reduces of the two dt minima (MIN) and the four counters (SUM);
   3. K7 into the primary arrays (sphb_integrate);
   4. ``sphb_slab_count``: per-category tile counts + totals on the device;
@@ -33,7 +34,7 @@ from .device import Workspace, _ptr, _stream, decode_err, new_ctrl, read_ctrl
 from .physics import grid_desc, grid_dims, params_desc
 from .slab import balanced_bounds, columns_of, enforce_min_width, rebalance_slices
 
-ROW_WORDS = 16  # packed exchange row: 64 B (posp, velr, prev float4, int64 id, pad)
+ROW_WORDS = 16  # packed exchange row: 64 B (posp, velr, prev float4, int64 id, u32 key, pad)
 NCAT = 10
 KEEP_B, KEEP_F, MIGL_B, MIGL_F, MIGR_B, MIGR_F, HALOL_B, HALOL_F, HALOR_B, HALOR_F = range(10)
 
@@ -142,6 +143,7 @@ class _Arrays:
         self.velr = torch.zeros((cap, 4), dtype=torch.float32, device=dev)
         self.prev = torch.zeros((cap, 4), dtype=torch.float32, device=dev)
         self.id = torch.zeros(cap, dtype=torch.int64, device=dev)
+        self.key = torch.zeros(cap, dtype=torch.int32, device=dev)  # K7's sort key, carried
 
 
 class DevRank:
@@ -174,7 +176,7 @@ class DevRank:
             self.a, self.b = _Arrays(cap, self.dev), _Arrays(cap, self.dev)
             for old, new in ((old_a, self.a), (old_b, self.b)):
                 if old is not None and self.n:  # keep the current rows (a) during an exchange
-                    for f in ("posp", "velr", "prev", "id"):
+                    for f in ("posp", "velr", "prev", "id", "key"):
                         getattr(new, f)[: self.n].copy_(getattr(old, f)[: self.n])
             self.cap_ab = cap
         self._ensure_engine(n)
@@ -230,10 +232,11 @@ class DevRank:
         L, s, ws = _lib.lib(), _stream(), self.ws.handle
         g, p, n, nb, a = _lib.ref(self.grid), _lib.ref(self.prm), self.n, self.nb, self.a
         self.ws.reset()
-        _lib.check(L.sphb_cell_keys(ws, g, _ptr(a.posp), n, nb, _ptr(self.keys), None,
-                                    _ptr(self.ctrl), s), "sphb_cell_keys")
+        # the keys travelled with the rows (K7 of the previous step, on whichever rank owned
+        # the row): only the per-cell histogram is rebuilt, no K1 pass over the positions
+        _lib.check(L.sphb_cell_hist(ws, g, _ptr(a.key), n, _ptr(self.ctrl), s), "sphb_cell_hist")
         _lib.check(L.sphb_step_begin(_ptr(self.ctrl), s), "sphb_step_begin")
-        _lib.check(L.sphb_sort(ws, g, _ptr(self.keys), n, _ptr(self.keys_sorted), _ptr(self.perm),
+        _lib.check(L.sphb_sort(ws, g, _ptr(a.key), n, _ptr(self.keys_sorted), _ptr(self.perm),
                                _ptr(self.ctrl), s), "sphb_sort")
         _lib.check(L.sphb_reorder(p, g, n, _ptr(self.perm), _ptr(self.keys_sorted), _ptr(a.posp),
                                   _ptr(a.velr), _ptr(a.prev), _ptr(a.id), _ptr(self.posp_s),
@@ -282,7 +285,8 @@ class DevRank:
         sr = self._buf("send", 1, layout["send_rows"][1])
         _lib.check(L.sphb_slab_scatter(g, n, nb, _ptr(self.keys), _ptr(a.id), x0, x1, _ptr(self.tiles),
                                        _ptr(a.posp), _ptr(a.velr), _ptr(a.prev), kb, _ptr(b.posp),
-                                       _ptr(b.velr), _ptr(b.prev), _ptr(b.id), _ptr(sl), _ptr(sr), sec, s),
+                                       _ptr(b.velr), _ptr(b.prev), _ptr(b.id), _ptr(b.key), _ptr(sl), _ptr(sr),
+                                       sec, s),
                    "sphb_slab_scatter")
 
     def unpack(self, layout):
@@ -292,7 +296,8 @@ class DevRank:
             for r0, cnt, dst in layout["unpack"][side]:
                 if cnt:
                     _lib.check(L.sphb_slab_unpack(_ptr(buf), r0, cnt, dst, _ptr(b.posp), _ptr(b.velr),
-                                                  _ptr(b.prev), _ptr(b.id), s), "sphb_slab_unpack")
+                                                  _ptr(b.prev), _ptr(b.id), _ptr(b.key), s),
+                               "sphb_slab_unpack")
         self.a, self.b = self.b, self.a
         self.n, self.nb = layout["n_next"], layout["nb_next"]
 
