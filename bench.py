@@ -51,8 +51,8 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=20)
     ap.add_argument("--graph", default="auto", choices=["auto", "on", "off"],
                     help="replay the timed steps as one CUDA graph (auto: below 2M particles)")
-    ap.add_argument("--pi-block", default="auto", choices=["auto", "128", "256"],
-                    help="targets per interaction block (auto: chosen from the warm-up's lane use)")
+    ap.add_argument("--pi-block", default="auto", choices=["auto", "128", "256", "384"],
+                    help="targets per interaction block (auto: sim.initial_pi_block)")
     ap.add_argument("--e2e-chunks", type=int, default=8,
                     help="row chunks of the pipelined H2D/D2H state round trip (1 = serial)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -281,8 +281,8 @@ def run_slabs(args, cfg_name, system, prm, prec, world, rank, local):
     pi_blocks = [128]
     first = args.warmup
     if args.pi_block == "auto" and prec == _lib.SPHB_FP32:  # as the single-GPU path
-        from paper_1110_3711_b200.sim import PI_LANE_SWITCH
-        pi_blocks = sim.choose_pi_block(PI_LANE_SWITCH)
+        from paper_1110_3711_b200.sim import PI_LARGE_MIN_TARGETS
+        pi_blocks = sim.choose_pi_block(PI_LARGE_MIN_TARGETS)
         sim.step()
         first += 1
         torch.cuda.synchronize()
@@ -443,21 +443,15 @@ def main():
     sim = DeviceSim(system, prm, reach=args.n_subdiv, precision=prec,
                     record_capacity=max(64, args.warmup + 2 * args.steps + 16))
     Ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+    # interaction blocking before the warm-up (run_simulation's policy, sim.py)
+    if args.pi_block == "auto" and prec == _lib.SPHB_FP32:
+        from paper_1110_3711_b200.sim import initial_pi_block
+        sim.set_pi_block(initial_pi_block(sim.n))
+    elif args.pi_block != "auto":
+        sim.set_pi_block(int(args.pi_block))
     for _ in range(args.warmup):
         sim.launch_step()
     torch.cuda.synchronize()
-    # interaction blocking from the warm-up (run_simulation's policy, sim.py): 128-target
-    # blocks unless their lanes are mostly idle; one more untimed step after a switch
-    if args.pi_block == "auto" and prec == _lib.SPHB_FP32:
-        from paper_1110_3711_b200.sim import PI_LANE_SWITCH
-        if sim.pi_lane_use() < PI_LANE_SWITCH:
-            sim.set_pi_block(256)
-            sim.launch_step()
-            torch.cuda.synchronize()
-    elif args.pi_block != "auto":
-        sim.set_pi_block(int(args.pi_block))
-        sim.launch_step()
-        torch.cuda.synchronize()
     first = int(sim.ctrl_host()["step"])
     if world > 1:
         dist.barrier()
@@ -608,7 +602,8 @@ def main():
                    "particles_per_gpu": system.n, "n_subdiv": args.n_subdiv, "variant": variant,
                    "l2": "inputs larger than L2 (resident state ~%.1f GB)" % (sim.n * 184 / 1e9),
                    "parallelism": f"{world} GPU" + (" replicas" if world > 1 else ""),
-                   "pi_block": sim.pi_block, "cuda_graph": use_graph},
+                   "pi_block": sim.pi_block, "pi_lane_use": round(sim.pi_lane_use(), 4),
+                   "cuda_graph": use_graph},
         "interactions_per_s": true_pairs * world * args.steps / (total_ms * 1e-3),
         "pair_evals_per_s": evals * world * args.steps / (total_ms * 1e-3),
         "stage_ms": {"nl": float(np.mean(nl_ms)), "pi": pi_mean, "su": float(np.mean(su_ms))},

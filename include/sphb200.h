@@ -141,8 +141,9 @@ int sphb_workspace_reset(sphb_workspace_t* ws, sphb_stream_t s);
  * (grid.py:107-109 stable order); the choice is made on the device. */
 int sphb_workspace_set_mover_cap(sphb_workspace_t* ws, int64_t cap);
 /* Targets per interaction block of the FP32 kernel: 128 (default: 4-warp CTAs, two per SM,
- * <= 2,304 staged candidates) or 256 (8-warp CTAs, one per SM, <= 4,224 staged candidates:
- * fewer idle lanes when cells hold uneven particle counts, e.g. after a dam collapses).
+ * <= 2,304 staged candidates), 256 (8-warp CTAs, one per SM, <= 4,224: small systems) or 384 (12-warp CTAs, one per SM, <= 4,608 staged candidates:
+ * more resident warps, less screen work per target, fewer idle lanes when cells hold uneven
+ * particle counts, e.g. after a dam collapses).
  * Results agree within the FP32 tolerance (accumulation order); FP64 always uses 128. */
 int sphb_workspace_set_pi_block(sphb_workspace_t* ws, int32_t targets);
 /* The last sphb_step sort's path (0 movers-only, 1 radix) and mover count (synchronising

@@ -76,6 +76,9 @@ int launch_interact(sphb_workspace* ws, const sphb_params_t& p, const sphb_grid_
   if (ws->pi_block == 256 && p.precision == SPHB_FP32)
     return pi256::launch_interact(ws, p, g, n, nb, posp, velr, aux, cell_sorted, beg, end, acc,
                                   drho, visc, ctrl, s);
+  if (ws->pi_block == PI_LARGE_BLOCK && p.precision == SPHB_FP32)
+    return pi384::launch_interact(ws, p, g, n, nb, posp, velr, aux, cell_sorted, beg, end, acc,
+                                  drho, visc, ctrl, s);
   return pi128::launch_interact(ws, p, g, n, nb, posp, velr, aux, cell_sorted, beg, end, acc, drho,
                                 visc, ctrl, s);
 }
@@ -183,8 +186,9 @@ int sphb_workspace_set_mover_cap(sphb_workspace_t* ws, int64_t cap) {
 
 int sphb_workspace_set_pi_block(sphb_workspace_t* ws, int32_t targets) {
   SPHB_NONNULL(ws);
-  if (targets != 128 && targets != 256)
-    return sphb_set_error(SPHB_E_INVALID, "interaction block must be 128 or 256 targets");
+  if (targets != 128 && targets != 256 && targets != PI_LARGE_BLOCK)
+    return sphb_set_error(SPHB_E_INVALID, "interaction block must be 128, 256 or %d targets",
+                          PI_LARGE_BLOCK);
   ws->pi_block = targets;
   return SPHB_OK;
 }

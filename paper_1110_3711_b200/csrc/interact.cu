@@ -45,7 +45,7 @@ namespace {
 #ifndef SPHB_NW
 #define SPHB_NW 4
 #endif
-constexpr int NW = SPHB_NW;      // warps per CTA (two CTAs per SM)
+constexpr int NW = SPHB_NW;      // warps per CTA (pi128: 4, two CTAs per SM; pi384: 12, one)
 constexpr int BT = NW * 32;      // targets per block
 #ifndef SPHB_H16
 #define SPHB_H16 1
@@ -1775,7 +1775,10 @@ __global__ void __launch_bounds__(256) k_wall_force(sphb_params_t p, sphb_grid_t
 }  // namespace
 
 #ifndef SPHB_PI_NS
-#define SPHB_PI_NS pi128  // this build's blocking (see sphb_internal.h: pi128 / pi256)
+#define SPHB_PI_NS pi128  // this build's blocking (see sphb_internal.h: pi128 / pi256 / pi384)
+#endif
+#ifdef SPHB_PI_LARGE
+static_assert(BT == PI_LARGE_BLOCK, "the large build's block size is sphb_internal.h's");
 #endif
 namespace SPHB_PI_NS {
 

@@ -39,7 +39,7 @@ struct sphb_workspace {
   int32_t* mv_head = nullptr;  // 2*ncells_max, -1 between steps
   int4* mv_kv = nullptr;       // 2*ncells_max per-key (SB, MB, old begin, chain head)
   int64_t mover_cap_max = 0, mover_cap = 0;
-  int32_t pi_block = 128;  // targets per interaction block: 128 (pi128) or 256 (pi256)
+  int32_t pi_block = 128;  // targets per interaction block: 128, 256 or 384 (pi128/256/384)
   size_t bytes = 0;
 };
 
@@ -65,9 +65,12 @@ int launch_hist_from_sorted(sphb_workspace* ws, const sphb_grid_t& g, const int3
 int sort_pass_count(const sphb_grid_t& g);
 int64_t nl_launch_count(const sphb_grid_t& g, int64_t n);
 
-// interact.cu, compiled twice: pi128 (4-warp CTAs, 128-target blocks over <= 2,304 staged
-// candidates, 2 CTAs/SM; the default) and pi256 (8-warp CTAs, 256-target blocks over <= 4,224
-// staged candidates, 1 CTA/SM: fewer idle lanes once cells fill unevenly)
+// interact.cu, compiled three times: pi128 (4-warp CTAs, 128-target blocks over <= 2,304 staged
+// candidates, 2 CTAs/SM), pi256 (8-warp CTAs, 256 targets over <= 4,224, 1 CTA/SM: small
+// systems, where 384-target blocks leave SMs idle) and pi384 (12-warp CTAs, 384-target blocks over <= 4,608 staged
+// candidates, 1 CTA/SM: more resident warps, 25% less screen work per target, fewer idle
+// lanes once cells fill unevenly)
+constexpr int PI_LARGE_BLOCK = 384;
 #define SPHB_DECLARE_PI(NS)                                                                     \
   namespace NS {                                                                                \
   int launch_interact(sphb_workspace* ws, const sphb_params_t& p, const sphb_grid_t& g,       \
@@ -79,6 +82,7 @@ int64_t nl_launch_count(const sphb_grid_t& g, int64_t n);
   }
 SPHB_DECLARE_PI(pi128)
 SPHB_DECLARE_PI(pi256)
+SPHB_DECLARE_PI(pi384)
 // the workspace's blocking (FP64 always pi128)
 int launch_interact(sphb_workspace* ws, const sphb_params_t& p, const sphb_grid_t& g, int64_t n, int64_t nb,
                     const float4* posp, const float4* velr, const float4* aux,

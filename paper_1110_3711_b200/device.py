@@ -153,8 +153,9 @@ class DeviceSim:
         self.pi_block = 128
 
     def set_pi_block(self, targets: int):
-        """Targets per FP32 interaction block: 128 (4-warp CTAs, the default) or 256 (8-warp
-        CTAs: fewer idle lanes when cells hold uneven counts).  Drops a captured graph."""
+        """Targets per FP32 interaction block: 128 (4-warp CTAs, the default), 256 (8-warp CTAs)
+        or 384 (12-warp CTAs, one per SM: more resident warps, fewer idle lanes when cells hold
+        uneven counts); sim.initial_pi_block is the run policy.  Drops a captured graph."""
         self.ws.set_pi_block(targets)
         self.pi_block = int(targets)
         self._graph = None

@@ -505,20 +505,14 @@ class DeviceSlabSim:
     def n_owned_max(self) -> int:
         return max(int((r.a.id[: r.n] >= 0).sum().item()) for r in self.ranks)
 
-    def choose_pi_block(self, threshold: float) -> list[int]:
-        """Per rank: switch the interaction to 256-target blocks when the last step's
-        128-target blocks held fewer than ``threshold`` of their lanes' targets (the rule of
-        run_simulation); returns each local rank's blocking."""
+    def choose_pi_block(self, large_min: int) -> list[int]:
+        """Per rank, run_simulation's rule: 384-target blocks when the rank owns at least
+        ``large_min`` targets, else 256; returns each local rank's blocking."""
         out = []
         for r in self.ranks:
-            c = read_ctrl(r.ctrl)
-            nblk = int(c["nblk"][0])
             owned = int((r.a.id[: r.n] >= 0).sum().item())
-            if nblk and owned / (128.0 * nblk) < threshold:
-                r.ws.set_pi_block(256)
-                out.append(256)
-            else:
-                out.append(128)
+            r.ws.set_pi_block(384 if owned >= large_min else 256)
+            out.append(384 if owned >= large_min else 256)
         return out
 
     def launches_per_step(self) -> int:

@@ -42,10 +42,18 @@ def divergence_from_device(err) -> DivergenceError:
     return DivergenceError(f"non-finite state at step {step}", step)
 
 
-# 128-target blocks whose lanes are filled below this fraction run slower than the 256-target
-# blocking (C3 10k-step dam break: equal near 0.8, 128 wins at rest, 256 by 8% once collapsed)
-PI_LANE_SWITCH = 0.78
-PI_DECIDE_EVERY = 256  # the "auto" blocking is decided at these step multiples only (chunk-proof)
+# Interaction blocking (tools/block_matrix.sh, profiles/r01k_block_matrix.txt): the 384-target
+# build (12-warp CTAs, one per SM) beats the 128-target one at rest on every BASELINE
+# configuration but C1, whose 25k particles make only ~65 such blocks for 148 SMs (C1 ms/step:
+# 0.131 with 256-target blocks on 8-warp CTAs, 0.147 with 128, 0.174 with 384); it also wins
+# over a whole 10,000-step collapse (profiles/r01k_c3_10000steps_auto.json).  "auto" = 384
+# from PI_LARGE_MIN_TARGETS targets (4 blocks per SM) up, 256 below, fixed for the run.
+PI_LARGE_MIN_TARGETS = 4 * 148 * 384
+
+
+def initial_pi_block(n_targets: int) -> int:
+    """The "auto" blocking's starting point for ``n_targets`` interaction targets."""
+    return 384 if n_targets >= PI_LARGE_MIN_TARGETS else 256
 
 
 @dataclass
@@ -157,11 +165,8 @@ def run_simulation(scenario_or_system, params, config: EngineConfig, max_steps: 
     bit-identically from such a checkpoint (``scenario_or_system`` may then be None; step
     numbers and the stop rules continue from the checkpoint's step).
 
-    ``pi_block``: targets per FP32 interaction block, 128, 256 or "auto" (start at 128 and
-    switch to 256 for good once fewer than PI_LANE_SWITCH of the 128-target blocks' lanes
-    hold a target, e.g. after a dam collapses; decided every PI_DECIDE_EVERY steps from that
-    step's launch, so the choice does not depend on ``chunk``; recorded in checkpoints so
-    resumed runs follow the same blocking)."""
+    ``pi_block``: targets per FP32 interaction block, 128, 256, 384 or "auto" (initial_pi_block of
+    the particle count; recorded in checkpoints so resumed runs keep the same blocking)."""
     if max_steps is None and t_end is None:
         raise ValueError("need max_steps or t_end")
     validate(params)
@@ -187,13 +192,11 @@ def run_simulation(scenario_or_system, params, config: EngineConfig, max_steps: 
         system = build_dam_break(scenario_or_system, params) if isinstance(scenario_or_system, Scenario) \
             else scenario_or_system
         sim = make_device_sim(system, params, cfg, max_steps, t_end, record_capacity=max(chunk, 1))
-    if pi_block not in (128, 256, "auto"):
-        raise ValueError("pi_block must be 128, 256 or 'auto'")
-    if pi_block != "auto" and resume_from is None:
-        sim.set_pi_block(int(pi_block))
+    if pi_block not in (128, 256, 384, "auto"):
+        raise ValueError("pi_block must be 128, 256, 384 or 'auto'")
     adapt = pi_block == "auto" and cfg.precision == "fp32"
-    if adapt:  # readbacks at every decision step, whatever else sets the chunk
-        chunk = math.gcd(chunk, PI_DECIDE_EVERY)
+    if resume_from is None and (pi_block != "auto" or adapt):
+        sim.set_pi_block(initial_pi_block(sim.n) if adapt else int(pi_block))
     stats_out: list[StepStats] = []
     nbytes = NEIGHBOR_BYTES[cfg.derived_mode]
     done_steps = int(sim.ctrl_host()["step"])
@@ -224,9 +227,6 @@ def run_simulation(scenario_or_system, params, config: EngineConfig, max_steps: 
         err = sim.error()
         if err is not None:
             raise divergence_from_device(err)
-        if adapt and sim.pi_block == 128 and now > done_steps and now % PI_DECIDE_EVERY == 0 \
-                and sim.pi_lane_use(c) < PI_LANE_SWITCH:
-            sim.set_pi_block(256)
         if checkpoint_every and now > done_steps and now % int(checkpoint_every) == 0:
             sim.save_checkpoint(str(checkpoint_path).format(step=now))
         done_steps = now

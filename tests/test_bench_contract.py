@@ -9,7 +9,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 def _line():
-    with open(os.path.join(ROOT, "profiles", "r01j_bench_default.json")) as fh:
+    with open(os.path.join(ROOT, "profiles", "r01l_bench_default.json")) as fh:
         return json.loads(fh.read().splitlines()[0])
 
 

@@ -112,7 +112,7 @@ def test_run_command_writes_snapshots_and_stats(tmp_path, capsys):
 @pytest.mark.gpu
 def test_run_command_gather_cells_and_verify(capsys):
     assert cli.main(["run", "--dp", "0.03", "--steps", "2", "--cells", "h/2"]) == 0
-    assert cli.main(["run", "--dp", "0.03", "--steps", "2", "--pi-block", "256"]) == 0
+    assert cli.main(["run", "--dp", "0.03", "--steps", "2", "--pi-block", "384"]) == 0
     assert cli.main(["run", "--dp", "0.03", "--steps", "2", "--engine", "gather", "--symmetry",
                      "off", "--gather-variant", "slowcellsh"]) == 0
     assert cli.main(["run", "--dp", "0.03", "--steps", "3", "--verify"]) == 0

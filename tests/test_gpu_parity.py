@@ -440,16 +440,17 @@ def test_state_soa_round_trip():
     assert L.sphb_state_from_soa(-1, 1, *ptrs, 0, 0, 0, s) == _lib.SPHB_E_INVALID
 
 
+@pytest.mark.parametrize("block", [256, 384])
 @pytest.mark.parametrize("name", ["c1", "c2"])
-def test_pi_block_256_matches_128(name):
-    """The 256-target blocking (pi256: 8-warp CTAs) gives the 128-target one's counters
+def test_pi_block_matches_128(name, block):
+    """The 256- and 384-target blockings (pi256 / pi384: 8- / 12-warp CTAs) gives the 128-target one's counters
     exactly and its forces within the FP32 tolerance, step after step."""
     sc = sph.named_scenario(name)
     prm = sph.make_params(sc)
     system = sph.build_dam_break(sc, prm)
     a = D.DeviceSim(system, prm, reach=1, precision=0)
     b = D.DeviceSim(system, prm, reach=1, precision=0)
-    b.set_pi_block(256)
+    b.set_pi_block(block)
     for step in range(4):
         a.launch_step()
         b.launch_step()
@@ -462,17 +463,23 @@ def test_pi_block_256_matches_128(name):
     assert 0.0 < b.pi_lane_use() <= 1.0 and int(b.ctrl_host()["nblk"][0]) < int(a.ctrl_host()["nblk"][0])
 
 
-def test_run_simulation_switches_blocking_when_lanes_idle(monkeypatch):
-    from paper_1110_3711_b200 import sim as S
-    monkeypatch.setattr(S, "PI_DECIDE_EVERY", 10)
+def test_run_simulation_auto_blocking_follows_the_size_rule():
+    """pi_block="auto" = sim.initial_pi_block(n) for the whole run (256 below 4 large blocks
+    per SM); explicit 384 on a small case agrees with 128 (counters exact, FP32 tolerance)."""
     sc = sph.Scenario(dp=0.02)
     prm = sph.make_params(sc)
     cfg = sph.EngineConfig(engine="gather", symmetry=False, gather_variant="slowcellsh")
-    s_auto, st_auto = sph.run_simulation(sc, prm, cfg, max_steps=40, chunk=10)
-    s_128, st_128 = sph.run_simulation(sc, prm, cfg, max_steps=40, chunk=10, pi_block=128)
-    assert [x.true_pairs for x in st_auto[:10]] == [x.true_pairs for x in st_128[:10]]
+    s_auto, st_auto = sph.run_simulation(sc, prm, cfg, max_steps=20, chunk=10)
+    s_256, st_256 = sph.run_simulation(sc, prm, cfg, max_steps=20, chunk=10, pi_block=256)
+    s_128, st_128 = sph.run_simulation(sc, prm, cfg, max_steps=20, chunk=10, pi_block=128)
+    s_384, st_384 = sph.run_simulation(sc, prm, cfg, max_steps=20, chunk=10, pi_block=384)
+    assert s_auto.n < sph.sim.PI_LARGE_MIN_TARGETS
+    assert [x.true_pairs for x in st_auto] == [x.true_pairs for x in st_256]
     for f in ("pos", "vel", "rho"):
-        assert oracle.rel_linf(getattr(s_auto, f), getattr(s_128, f)) <= 1e-4, f
+        assert np.array_equal(getattr(s_auto, f), getattr(s_256, f)), f
+    assert [x.true_pairs for x in st_384[:5]] == [x.true_pairs for x in st_128[:5]]
+    for f in ("pos", "vel", "rho"):
+        assert oracle.rel_linf(getattr(s_384, f), getattr(s_128, f)) <= 1e-4, f
     with pytest.raises(ValueError, match="pi_block"):
         sph.run_simulation(sc, prm, cfg, max_steps=1, pi_block=64)
 

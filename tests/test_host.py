@@ -148,3 +148,15 @@ def test_abi_rejects_bad_arguments_without_gpu():
     rc = L.sphb_interact(None, None, None, 0, 0, None, None, None, None, None, None, None, None,
                          None, None, None)
     assert rc == _lib.SPHB_E_INVALID
+
+
+def test_auto_interaction_blocking_policy():
+    """sim.initial_pi_block: 384-target blocks once there are >= 4 per SM, 256 below (the
+    blockings' parity: test_pi_block_matches_128 on the GPU)."""
+    from paper_1110_3711_b200 import sim as S
+    assert S.PI_LARGE_MIN_TARGETS == 4 * 148 * 384
+    assert S.initial_pi_block(25_000) == 256            # C1: ~65 large blocks for 148 SMs
+    assert S.initial_pi_block(1_180_000) == 384         # C2
+    assert S.initial_pi_block(10_200_478) == 384        # C3
+    assert S.initial_pi_block(S.PI_LARGE_MIN_TARGETS) == 384
+    assert S.initial_pi_block(S.PI_LARGE_MIN_TARGETS - 1) == 256

@@ -1,5 +1,5 @@
 """C3 after K steps (collapsed column): mean ms/step and PI ms over M more steps, for A/B of
-the interaction builds.  python tools/collapsed_bench.py [K] [M] [128|256]"""
+the interaction builds.  python tools/collapsed_bench.py [K] [M] [128|384]"""
 import sys
 
 import numpy as np
@@ -11,7 +11,7 @@ from paper_1110_3711_b200.device import DeviceSim  # noqa: E402
 
 K = int(sys.argv[1]) if len(sys.argv) > 1 else 5000
 M = int(sys.argv[2]) if len(sys.argv) > 2 else 200
-block = int(sys.argv[3]) if len(sys.argv) > 3 else 256
+block = int(sys.argv[3]) if len(sys.argv) > 3 else 384
 sc = sph.named_scenario("c3")
 prm = sph.make_params(sc)
 sim = DeviceSim(sph.build_dam_break(sc, prm), prm, reach=1, record_capacity=K + M + 8)

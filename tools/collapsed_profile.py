@@ -1,5 +1,5 @@
 """Run C3 for K steps (the column collapses), then one profiled step (for ncu
---profile-from-start off):  python tools/collapsed_profile.py [steps] [128|256]"""
+--profile-from-start off):  python tools/collapsed_profile.py [steps] [128|384]"""
 import sys
 
 import torch

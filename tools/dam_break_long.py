@@ -1,7 +1,7 @@
 """C3 dam break over a long run on one GPU: how the step cost evolves as the column collapses
 (cells fill unevenly, more rows change cell per step), with the energy diagnostics.
 
-  python tools/dam_break_long.py [c3] [out.json] [steps] [every] [128|256|auto]
+  python tools/dam_break_long.py [c3] [out.json] [steps] [every] [128|384|auto]
 
 Per window of ``every`` steps: mean ms/step and NL / PI / SU stage means (CUDA events), the
 movers-only sort's mover count and path on the window's last step, t_sim, KE/PE/IE.
@@ -27,6 +27,8 @@ sc = sph.named_scenario(name)
 prm = sph.make_params(sc)
 system = sph.build_dam_break(sc, prm)
 sim = DeviceSim(system, prm, reach=1, record_capacity=steps + 8)
+if blocking == "auto":
+    sim.set_pi_block(sph.sim.initial_pi_block(sim.n))
 if blocking != "auto":
     sim.set_pi_block(int(blocking))
 n = sim.n
@@ -50,8 +52,6 @@ while done < steps:
     nblk = int(c["nblk"][0])
     lane = sim.pi_lane_use(c)
     block_now = sim.pi_block
-    if blocking == "auto" and sim.pi_block == 128 and lane < sph.sim.PI_LANE_SWITCH:
-        sim.set_pi_block(256)  # run_simulation's policy (sim.py)
     rows.append(dict(step=done, t_sim=float(c["t_sim"]), ms_per_step=float(st[:, 3].mean()),
                      pi_block=block_now, pi_blocks=nblk, lane_use=lane,
                      nl_ms=float(st[:, 0].mean()), pi_ms=float(st[:, 1].mean()),

@@ -1,5 +1,5 @@
 """A few steps of a small dam break through every kernel family, for compute-sanitizer:
-FP32 (pi128 and pi256 interaction builds, movers-only + radix sorts, symplectic, wall force,
+FP32 (pi128, pi256 and pi384 interaction builds, movers-only + radix sorts, symplectic, wall force,
 energy, SoA state conversion) and FP64.
 
   compute-sanitizer --tool memcheck|racecheck|synccheck|initcheck python tools/sanitize_steps.py
@@ -16,7 +16,7 @@ from paper_1110_3711_b200.device import DeviceSim  # noqa: E402
 sc = sph.Scenario(dp=0.02)
 prm = sph.make_params(sc, boundary_force=sph.BoundaryForce(d=5.0 * 9.81 * sc.fill_height, r0=sc.dp))
 system = sph.build_dam_break(sc, prm)
-for precision, block, integ in ((0, 128, "verlet"), (0, 256, "verlet"), (1, 128, "verlet"),
+for precision, block, integ in ((0, 128, "verlet"), (0, 256, "verlet"), (0, 384, "verlet"), (1, 128, "verlet"),
                                 (0, 128, "symplectic")):
     p = sph.make_params(sc, integrator=integ,
                         boundary_force=sph.BoundaryForce(d=5.0 * 9.81 * sc.fill_height, r0=sc.dp))

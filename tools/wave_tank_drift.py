@@ -1,7 +1,7 @@
 """C5 (BASELINE.json config 5): piston wave tank, 1000 steps, energy / mass drift from the
 device diagnostics (sphb_energy), on one GPU.  Writes a JSON summary (argv[2]).
 
-  python tools/wave_tank_drift.py [c5|c5_small] [out.json] [steps] [every] [128|256|auto]
+  python tools/wave_tank_drift.py [c5|c5_small] [out.json] [steps] [every] [128|384|auto]
 """
 import json
 import sys
@@ -25,6 +25,8 @@ prm = sph.make_wave_tank_params(sc)
 system = sph.build_wave_tank(sc, prm)
 t_build = time.time() - t0
 sim = DeviceSim(system, prm, reach=1, record_capacity=steps + 8)
+if blocking == "auto":
+    sim.set_pi_block(sph.sim.initial_pi_block(sim.n))
 if blocking != "auto":
     sim.set_pi_block(int(blocking))
 rows = []
@@ -44,8 +46,6 @@ while done < steps:
     gpu_ms += ev0.elapsed_time(ev1)
     done += k
     c = sim.ctrl_host()
-    if blocking == "auto" and sim.pi_block == 128 and sim.pi_lane_use(c) < sph.sim.PI_LANE_SWITCH:
-        sim.set_pi_block(256)  # run_simulation's rule
     err = sim.error()
     if err is not None:
         raise SystemExit(f"diverged: {err}")
