@@ -282,7 +282,7 @@ def run_slabs(args, cfg_name, system, prm, prec, world, rank, local):
     first = args.warmup
     if args.pi_block == "auto" and prec == _lib.SPHB_FP32:  # as the single-GPU path
         from paper_1110_3711_b200.sim import PI_LARGE_MIN_TARGETS
-        pi_blocks = sim.choose_pi_block(PI_LARGE_MIN_TARGETS)
+        pi_blocks = sim.choose_pi_block(PI_LARGE_MIN_TARGETS if args.n_subdiv == 1 else None)
         sim.step()
         first += 1
         torch.cuda.synchronize()
@@ -446,7 +446,7 @@ def main():
     # interaction blocking before the warm-up (run_simulation's policy, sim.py)
     if args.pi_block == "auto" and prec == _lib.SPHB_FP32:
         from paper_1110_3711_b200.sim import initial_pi_block
-        sim.set_pi_block(initial_pi_block(sim.n))
+        sim.set_pi_block(initial_pi_block(sim.n, args.n_subdiv))
     elif args.pi_block != "auto":
         sim.set_pi_block(int(args.pi_block))
     for _ in range(args.warmup):

@@ -505,14 +505,16 @@ class DeviceSlabSim:
     def n_owned_max(self) -> int:
         return max(int((r.a.id[: r.n] >= 0).sum().item()) for r in self.ranks)
 
-    def choose_pi_block(self, large_min: int) -> list[int]:
+    def choose_pi_block(self, large_min) -> list[int]:
         """Per rank, run_simulation's rule: 384-target blocks when the rank owns at least
-        ``large_min`` targets, else 256; returns each local rank's blocking."""
+        ``large_min`` targets, else 256; 128 when ``large_min`` is None (h/2 cells); returns
+        each local rank's blocking."""
         out = []
         for r in self.ranks:
             owned = int((r.a.id[: r.n] >= 0).sum().item())
-            r.ws.set_pi_block(384 if owned >= large_min else 256)
-            out.append(384 if owned >= large_min else 256)
+            blk = 128 if large_min is None else 384 if owned >= large_min else 256
+            r.ws.set_pi_block(blk)
+            out.append(blk)
         return out
 
     def launches_per_step(self) -> int:

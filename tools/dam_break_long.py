@@ -28,7 +28,7 @@ prm = sph.make_params(sc)
 system = sph.build_dam_break(sc, prm)
 sim = DeviceSim(system, prm, reach=1, record_capacity=steps + 8)
 if blocking == "auto":
-    sim.set_pi_block(sph.sim.initial_pi_block(sim.n))
+    sim.set_pi_block(sph.sim.initial_pi_block(sim.n, prm.n_subdiv))
 if blocking != "auto":
     sim.set_pi_block(int(blocking))
 n = sim.n

@@ -26,7 +26,7 @@ system = sph.build_wave_tank(sc, prm)
 t_build = time.time() - t0
 sim = DeviceSim(system, prm, reach=1, record_capacity=steps + 8)
 if blocking == "auto":
-    sim.set_pi_block(sph.sim.initial_pi_block(sim.n))
+    sim.set_pi_block(sph.sim.initial_pi_block(sim.n, prm.n_subdiv))
 if blocking != "auto":
     sim.set_pi_block(int(blocking))
 rows = []
