@@ -2,6 +2,7 @@
 //
 // Thin: argument checks, workspace management, error strings; the kernels live in
 // nl.cu / interact.cu / integrate.cu.  No C++ exception crosses the ABI.
+#include <nvtx3/nvToolsExt.h>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -9,6 +10,12 @@
 
 #include "sphb_common.cuh"
 #include "sphb_internal.h"
+
+// NVTX stage ranges (header-only NVTX v3: free unless a tool such as nsys / ncu --nvtx attaches)
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
 
 static thread_local char g_err[512] = "";
 
@@ -432,18 +439,25 @@ static int stage_pass(sphb_workspace_t* ws, const sphb_params_t* prm, const sphb
                       int64_t n, int64_t nb, const sphb_state_t* st, sphb_ctrl_t* ctrl, int mode,
                       cudaStream_t cs) {
   int rc;
-  if ((rc = launch_sort_and_ranges(ws, *grid, st->keys, n, st->keys_sorted, st->perm, st->beg,
-                                   st->end, ctrl, cs)))
-    return rc;
-  if ((rc = launch_reorder(*prm, *grid, n, st->perm, st->keys_sorted, (const float4*)st->posp,
-                           (const float4*)st->velr, (const float4*)st->prev, st->id,
-                           (float4*)st->posp_s, (float4*)st->velr_s, (float4*)st->prev_s, st->id_s,
-                           (float4*)st->aux, st->cell_s, ctrl, cs)))
-    return rc;
-  if ((rc = launch_interact(ws, *prm, *grid, n, nb, (const float4*)st->posp_s,
-                            (const float4*)st->velr_s, (const float4*)st->aux, st->cell_s, st->beg,
-                            st->end, st->acc, st->drho, st->visc, ctrl, cs)))
-    return rc;
+  {
+    NvtxRange r("sphb NL");  // stage ranges (the reference's perf_counter stages, sim.py:306-348)
+    if ((rc = launch_sort_and_ranges(ws, *grid, st->keys, n, st->keys_sorted, st->perm, st->beg,
+                                     st->end, ctrl, cs)))
+      return rc;
+    if ((rc = launch_reorder(*prm, *grid, n, st->perm, st->keys_sorted, (const float4*)st->posp,
+                             (const float4*)st->velr, (const float4*)st->prev, st->id,
+                             (float4*)st->posp_s, (float4*)st->velr_s, (float4*)st->prev_s, st->id_s,
+                             (float4*)st->aux, st->cell_s, ctrl, cs)))
+      return rc;
+  }
+  {
+    NvtxRange r("sphb PI");
+    if ((rc = launch_interact(ws, *prm, *grid, n, nb, (const float4*)st->posp_s,
+                              (const float4*)st->velr_s, (const float4*)st->aux, st->cell_s, st->beg,
+                              st->end, st->acc, st->drho, st->visc, ctrl, cs)))
+      return rc;
+  }
+  NvtxRange r("sphb SU");
   return launch_integrate_mode(ws, *prm, *grid, n, nb, mode, (const float4*)st->posp_s,
                                (const float4*)st->velr_s, (const float4*)st->prev_s, st->id_s,
                                st->acc, st->drho, (float4*)st->posp, (float4*)st->velr,

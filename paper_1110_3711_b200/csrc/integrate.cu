@@ -44,11 +44,15 @@ __global__ void k_ctrl_init(sphb_ctrl_t* c, int64_t max_steps, double t_end) {
 }
 
 __global__ void k_step_begin(sphb_ctrl_t* c) {
-  if (!step_live(c)) return;
+  if (!c->active) return;
+  // the stop rule first (sim.py:302-305 runs before assign_cells at 309-314): a particle that
+  // left the domain during the final step (K7 records it against step + 1) ends the run
+  // normally, as in the reference; the host ignores that record (DeviceSim.error)
   if ((c->max_steps >= 0 && c->step >= c->max_steps) || (c->t_sim >= c->t_end)) {
     c->active = 0;
     return;
   }
+  if (!step_live(c)) return;
   c->dtmin_f = (uint64_t)__double_as_longlong(INFINITY);
   c->dtmin_cv = (uint64_t)__double_as_longlong(INFINITY);
   for (int k = 0; k < 4; ++k) c->counters[k] = 0;

@@ -225,6 +225,8 @@ class DeviceSim:
         ev[0] after NL, ev[1] after PI, ev[2] after the update."""
         L, s, ws = _lib.lib(), _stream(), self.ws.handle
         g, p, n, nb = _lib.ref(self.grid), _lib.ref(self.prm), self.n, self.nb
+        nvtx = torch.cuda.nvtx
+        nvtx.range_push("sphb NL")
         _lib.check(L.sphb_sort_ranges(ws, g, _ptr(self.keys), n, _ptr(self.keys_sorted),
                                       _ptr(self.perm), _ptr(self.beg), _ptr(self.end),
                                       _ptr(self.ctrl), s), "sphb_sort_ranges")
@@ -234,11 +236,15 @@ class DeviceSim:
                                   _ptr(self.aux), _ptr(self.cell_s), _ptr(self.ctrl), s),
                    "sphb_reorder")
         ev[0].record()
+        nvtx.range_pop()
+        nvtx.range_push("sphb PI")
         _lib.check(L.sphb_interact(ws, p, g, n, nb, _ptr(self.posp_s), _ptr(self.velr_s),
                                    _ptr(self.aux), _ptr(self.cell_s), _ptr(self.beg),
                                    _ptr(self.end), _ptr(self.acc), _ptr(self.drho),
                                    _ptr(self.visc), _ptr(self.ctrl), s), "sphb_interact")
         ev[1].record()
+        nvtx.range_pop()
+        nvtx.range_push("sphb SU")
         args = (_ptr(self.posp_s), _ptr(self.velr_s), _ptr(self.prev_s), _ptr(self.id_s),
                 _ptr(self.acc), _ptr(self.drho), _ptr(self.posp), _ptr(self.velr), _ptr(self.prev),
                 _ptr(self.id), _ptr(self.keys), _ptr(self.ctrl), s)
@@ -247,6 +253,7 @@ class DeviceSim:
         else:
             _lib.check(L.sphb_integrate_stage(ws, p, g, n, nb, mode - 1, *args), "sphb_integrate_stage")
         ev[2].record()
+        nvtx.range_pop()
 
     def launch_step(self, events=None):
         """Enqueue one step (no host sync).  ``events``: n_stage_events() CUDA events recorded
@@ -361,6 +368,12 @@ class DeviceSim:
         if d is None:
             return None
         step, code, index = d
+        stop = (int(c["max_steps"]) >= 0 and int(c["step"]) >= int(c["max_steps"])) or \
+            float(c["t_sim"]) >= float(c["t_end"])
+        if code == _lib.SPHB_DIV_LEFT_DOMAIN and step == int(c["step"]) and stop:
+            # escaped during the final step: the stop rule ended the run before that step's
+            # assign_cells would have seen it (sim.py:302-315), so the reference returns normally
+            return None
         pid = int(self.id[index].item()) if code == _lib.SPHB_DIV_LEFT_DOMAIN else None
         return step, code, index, pid
 

@@ -204,6 +204,8 @@ class DevRank:
             self.keys[: old_keys.shape[0]].copy_(old_keys)
             self.tiles[: old_tiles.shape[0]].copy_(old_tiles)
         self.ws = Workspace(cap, self.ncells)
+        if getattr(self, "pi_block", None):  # a regrown workspace keeps the chosen blocking
+            self.ws.set_pi_block(self.pi_block)
         self.cap = cap
 
     def _buf(self, which, side, rows):
@@ -513,6 +515,7 @@ class DeviceSlabSim:
         for r in self.ranks:
             owned = int((r.a.id[: r.n] >= 0).sum().item())
             blk = 128 if large_min is None else 384 if owned >= large_min else 256
+            r.pi_block = blk
             r.ws.set_pi_block(blk)
             out.append(blk)
         return out

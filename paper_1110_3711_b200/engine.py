@@ -25,8 +25,15 @@ PRECISION_CODE = {"fp32": _lib.SPHB_FP32, "fp64": _lib.SPHB_FP64}
 class B200Engine:
     """Device gather engine; holds its device buffers across calls (resized on demand)."""
 
-    def __init__(self, config: EngineConfig):
+    def __init__(self, config: EngineConfig, pi_block="auto"):
+        """``pi_block``: targets per FP32 interaction block (128, 256, 384) or "auto", the
+        production rule of run_simulation (sim.initial_pi_block of the frame's particle count
+        and n_subdiv), so the engine path runs the same interaction build as the stepper."""
         self.config = config.validated()
+        if pi_block not in (128, 256, 384, "auto"):
+            raise ValueError("pi_block must be 128, 256, 384 or 'auto'")
+        self.pi_block = pi_block
+        self.last_pi_block = None
         self._buf = None
         self._ws = None
         self.last_kernel_ms = None
@@ -91,6 +98,13 @@ class B200Engine:
             b["hcell"][:n] = torch.from_numpy(cell_of.astype(np.int32))
             b["dev4"][:, :n].copy_(h[:, :n], non_blocking=True)
             b["cell"][:n].copy_(b["hcell"][:n], non_blocking=True)
+        if self.pi_block == "auto":
+            from .sim import initial_pi_block
+            blk = initial_pi_block(n, params.n_subdiv)
+        else:
+            blk = int(self.pi_block)
+        self._ws.set_pi_block(blk)
+        self.last_pi_block = blk
         ctrl = new_ctrl(torch.device("cuda"))
         L, s = _lib.lib(), _stream()
         d4 = b["dev4"]
@@ -122,9 +136,9 @@ class B200Engine:
                            visc_dt=np.ascontiguousarray(o[:, 4]), stats=stats)
 
 
-def make_engine(config: EngineConfig) -> B200Engine:
+def make_engine(config: EngineConfig, pi_block="auto") -> B200Engine:
     """engines/__init__.py:30-34 -- every validated config runs on the B200."""
-    return B200Engine(config.validated())
+    return B200Engine(config.validated(), pi_block=pi_block)
 
 
 def compute_forces_gather(system, derived, grid, cindex, ranges, params,

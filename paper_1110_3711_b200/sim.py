@@ -206,8 +206,11 @@ def run_simulation(scenario_or_system, params, config: EngineConfig, max_steps: 
     nbytes = NEIGHBOR_BYTES[cfg.derived_mode]
     done_steps = int(sim.ctrl_host()["step"])
     while True:
-        timer = _Timer(chunk, sim.n_stage_events()) if stage_timing else None
-        for k in range(chunk):
+        # chunks end on multiples of ``chunk`` (snapshot / checkpoint steps), also after a
+        # resume from a step that is not one
+        this = chunk - done_steps % chunk
+        timer = _Timer(this, sim.n_stage_events()) if stage_timing else None
+        for k in range(this):
             sim.launch_step(events=timer.ev[k] if timer else None)
         c = sim.ctrl_host()  # synchronises
         now = int(c["step"])
@@ -221,14 +224,15 @@ def run_simulation(scenario_or_system, params, config: EngineConfig, max_steps: 
             if timer is not None:
                 st.stage_nl_s, st.stage_pi_s, st.stage_su_s, st.wall_seconds = \
                     DeviceSim.stage_seconds(timer.ev[k])
-            if stats_sink is not None:
-                stats_sink(st)
-            stats_out.append(st)
             step_no = done_steps + k + 1
+            # snapshot first, then the stats record (sim.py:345-351)
             if snapshot_every and step_no % snapshot_every == 0 and snapshot_sink is not None \
                     and step_no == now:
                 snap = _system_from_device(sim, system)
                 snapshot_sink.emit(step_no, snap, compute_derived(snap.rho, params))
+            if stats_sink is not None:
+                stats_sink(st)
+            stats_out.append(st)
         err = sim.error()
         if err is not None:
             raise divergence_from_device(err)

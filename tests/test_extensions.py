@@ -73,6 +73,28 @@ def test_checkpoint_resume_bit_identical(tmp_path, precision):
         assert np.array_equal(getattr(straight, f), getattr(resumed, f)), f
 
 
+def test_snapshots_after_a_resume_land_on_their_multiples(tmp_path):
+    """Resumed at step 30 with snapshot_every=20: snapshots at 40 and 60 (the chunks realign to
+    the multiples), each emitted before that step's stats record (sim.py:345-351)."""
+    sc, prm, _ = small_system(0.025)
+    path = str(tmp_path / "ck_{step}")
+    sph.run_simulation(sc, prm, cfg(), max_steps=30, checkpoint_every=30, checkpoint_path=path)
+    order = []
+
+    class Sink:
+        def emit(self, step, system, derived):
+            order.append(("snap", step))
+
+    sph.run_simulation(None, prm, cfg(), max_steps=70, resume_from=path.format(step=30),
+                       snapshot_every=20, snapshot_sink=Sink(),
+                       stats_sink=lambda st: order.append(("stats", st.step + 1)))
+    assert [s for k, s in order if k == "snap"] == [40, 60]
+    assert [s for k, s in order if k == "stats"] == list(range(31, 71))
+    for s in (40, 60):
+        i = order.index(("snap", s))
+        assert order[i + 1] == ("stats", s)
+
+
 def test_checkpoint_rejects_foreign_file(tmp_path):
     p = str(tmp_path / "x.npz")
     np.savez(p, magic=np.array("something else"))

@@ -176,6 +176,36 @@ def test_interact_fp32_within_tolerance(name, variant):
     out.stats.validate()
 
 
+@pytest.mark.parametrize("block", [128, 256, 384])
+@pytest.mark.parametrize("name,variant", FRAMES)
+def test_interact_fp32_each_blocking_vs_reference(name, variant, block):
+    """Every FP32 interaction build (pi128 / pi256 / pi384: 4-, 8-, 12-warp CTAs), selected
+    through the engine's ``pi_block``, against the reference's own gather output: forces within
+    1e-5, counters bit-exact.  The n2 frames run reach 2 (25 stencil rows), where the larger
+    blocks stage their candidates in several batches with partial drains."""
+    z = golden(name)
+    system, derived, grid, cindex, prm = frame_objects(z)
+    eng = sph.make_engine(gather_cfg(variant, "fp32"), pi_block=block)
+    out = eng.compute(system, derived, grid, cindex, prm, ranges=object())
+    assert eng.last_pi_block == block
+    nb = system.count_boundary
+    assert np.all(out.accel[:nb] == 0.0)
+    for a, f in ((out.accel, "accel"), (out.drho_dt, "drho"), (out.visc_dt, "visc")):
+        assert oracle.rel_linf(a, z[f"{variant}_{f}"]) <= FP32_TOL, f
+    assert [out.stats.candidate_pairs, out.stats.true_pairs, out.stats.force_evals,
+            out.stats.ff_force_evals] == list(z[f"{variant}_counters"])
+
+
+def test_engine_auto_blocking_is_the_run_rule():
+    z = golden("frame_c1_n1.npz")
+    system, derived, grid, cindex, prm = frame_objects(z)
+    eng = sph.make_engine(gather_cfg("slowcellsh", "fp32"))
+    eng.compute(system, derived, grid, cindex, prm)
+    assert eng.last_pi_block == sph.sim.initial_pi_block(system.n, prm.n_subdiv)
+    with pytest.raises(ValueError, match="pi_block"):
+        sph.make_engine(gather_cfg("slowcellsh", "fp32"), pi_block=64)
+
+
 def test_interact_deterministic_and_momentum():
     z = golden("frame_uniform3k_n1.npz")  # fluid only
     system, derived, grid, cindex, prm = frame_objects(z)
@@ -236,8 +266,10 @@ def test_run_simulation_fp32_one_step_and_short_trajectory():
     np.testing.assert_allclose(dts, z["dt"][:10], rtol=1e-5)
 
 
-def test_drift_1000_steps_fp32_vs_reference():
-    """SURVEY.md §8(d) drift bar: E = KE + PE + IE; tolerances stated in DESIGN.md."""
+@pytest.mark.parametrize("pi_block", ["auto", 384])
+def test_drift_1000_steps_fp32_vs_reference(pi_block):
+    """SURVEY.md §8(d) drift bar: E = KE + PE + IE; tolerances stated in DESIGN.md.  Run with
+    the size rule's build (C1: pi256) and with the production 384-target build forced."""
     z = golden("drift_c1.npz")
     prm = oracle.params_from_npz(z)
     sc = sph.Scenario(dp=0.006)
@@ -250,7 +282,8 @@ def test_drift_1000_steps_fp32_vs_reference():
                                                       system.mass_boundary, prm))
 
     system, stats = sph.run_simulation(sc, prm, gather_cfg("slowcellsh", "fp32"), max_steps=1000,
-                                       snapshot_every=10, snapshot_sink=Sink(), stage_timing=False)
+                                       snapshot_every=10, snapshot_sink=Sink(), stage_timing=False,
+                                       pi_block=pi_block)
     got = np.array(rows)
     ref = z["diag"][1:]
     assert got.shape == ref.shape and np.array_equal(got[:, 0], ref[:, 0])
@@ -278,6 +311,25 @@ def test_divergence_escaped_particle():
     assert err.value.step == 0
     assert err.value.particle_id == int(system.id[-1])
     assert "left the domain" in str(err.value)
+
+
+@pytest.mark.parametrize("chunk", [1, 256])
+def test_particle_escaping_during_the_final_step_ends_normally(chunk):
+    """The reference checks the stop rule before assign_cells (sim.py:302-315): a particle that
+    leaves the domain during the last step does not raise; one more step does."""
+    sc = sph.Scenario(dp=0.025)
+    prm = sph.make_params(sc)
+    system = sph.build_dam_break(sc, prm)
+    dmax = np.asarray(prm.domain_max, np.float64)
+    system.pos[-1] = (dmax - 1e-6).astype(np.float32)
+    system.vel[-1] = np.float32(5.0)
+    pid = int(system.id[-1])
+    out, stats = sph.run_simulation(system.copy(), prm, sph.EngineConfig(), max_steps=1, chunk=chunk)
+    assert len(stats) == 1
+    assert np.any(out.pos[out.id == pid] > dmax.astype(np.float32))
+    with pytest.raises(sph.DivergenceError) as err:
+        sph.run_simulation(system.copy(), prm, sph.EngineConfig(), max_steps=2, chunk=chunk)
+    assert err.value.step == 1 and err.value.particle_id == pid
 
 
 def test_divergence_nonfinite_state():
@@ -485,6 +537,52 @@ def test_run_simulation_auto_blocking_follows_the_size_rule():
 
 
 # ------------------------------------------------------------------ full sizes
+def _sorted_frame(system, prm):
+    """The device-NL-sorted frame of ``system`` with its derived quantities."""
+    nl = D.nl_frame(system.pos, system.count_boundary, prm)
+    perm = nl["sort_perm"]
+    ss = sph.ParticleSystem(count_fluid=system.count_fluid, count_boundary=system.count_boundary,
+                            pos=system.pos[perm], vel=system.vel[perm], rho=system.rho[perm],
+                            mass_fluid=system.mass_fluid, mass_boundary=system.mass_boundary,
+                            ptype=system.ptype[perm], id=system.id[perm])
+    return ss, sph.compute_derived(ss.rho, prm), nl
+
+
+def _oracle_frame(system, prm):
+    """Oracle NL (numpy restatement of grid.py, pinned to the reference) + the oracle C gather
+    (bit-exact to the reference's gather kernels) on ``system``'s sorted frame."""
+    cell, dims, _ = oracle.assign_cells(system.pos, prm)
+    perm = oracle.sort_perm(cell, system.count_boundary)
+    cidx = oracle.cell_index(cell[perm], system.count_boundary, int(np.prod(dims)))
+    ref = oracle.gather(system.pos[perm], system.vel[perm], system.rho[perm], system.count_boundary,
+                        system.mass_fluid, system.mass_boundary, cell[perm], dims, cidx, prm,
+                        variant="slowcellsh" if prm.n_subdiv == 1 else "slowcellshalf")
+    return cell, perm, cidx, ref
+
+
+def _check_vs_oracle(out, ref, tol=FP32_TOL):
+    assert [out.stats.candidate_pairs, out.stats.true_pairs, out.stats.force_evals,
+            out.stats.ff_force_evals] == list(ref["counters"])
+    for a, b, f in ((out.accel, ref["accel"], "accel"), (out.drho_dt, ref["drho_dt"], "drho"),
+                    (out.visc_dt, ref["visc_dt"], "visc")):
+        assert oracle.rel_linf(a, b) <= tol, f
+
+
+@pytest.fixture(scope="module")
+def c2_frames():
+    cache = {}
+
+    def get(n_subdiv):
+        if n_subdiv not in cache:
+            sc = sph.named_scenario("c2")
+            prm = sph.make_params(sc, n_subdiv=n_subdiv)
+            system = sph.build_dam_break(sc, prm)
+            ss, der, nl = _sorted_frame(system, prm)
+            cache[n_subdiv] = (system, prm, ss, der, nl, _oracle_frame(system, prm))
+        return cache[n_subdiv]
+    return get
+
+
 def _device_counters(name, n_subdiv, precision="fp32"):
     sc = sph.named_scenario(name)
     prm = sph.make_params(sc, n_subdiv=n_subdiv)
@@ -500,6 +598,62 @@ def _device_counters(name, n_subdiv, precision="fp32"):
     variant = "slowcellsh" if n_subdiv == 1 else "slowcellshalf"
     out = sph.make_engine(gather_cfg(variant, precision)).compute(ss, der, grid, None, prm)
     return ss, der, nl, prm, out
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("n_subdiv,block", [(1, 128), (1, 256), (1, 384), (2, 128), (2, 384)])
+def test_c2_each_blocking_vs_oracle(c2_frames, n_subdiv, block):
+    """C2 (1,142,622 particles) through the engine with each FP32 build forced: counters
+    bit-exact and forces within 1e-5 of the oracle gather (bit-exact to the reference).  At
+    n_subdiv 2 (reach 2, 25 stencil rows of h-cells) the larger blocks need several staging
+    batches per block."""
+    system, prm, ss, der, nl, (cell, perm, cidx, ref) = c2_frames(n_subdiv)
+    assert np.array_equal(nl["sort_perm"], perm)
+    variant = "slowcellsh" if n_subdiv == 1 else "slowcellshalf"
+    eng = sph.make_engine(gather_cfg(variant, "fp32"), pi_block=block)
+    out = eng.compute(ss, der, types.SimpleNamespace(cell_of=nl["cell_of"]), None, prm)
+    assert eng.last_pi_block == block
+    _check_vs_oracle(out, ref)
+
+
+@pytest.mark.slow
+def test_c3_10m_production_build_vs_oracle():
+    """C3 (10,200,478 particles, the bench workload), initial frame, the production FP32 build
+    (engine "auto" = pi384 at this size, the build bench.py times) against the oracle gather
+    on the oracle's own NL: counters bit-exact, accel / drho_dt / visc_dt within 1e-5."""
+    sc = sph.named_scenario("c3")
+    prm = sph.make_params(sc)
+    system = sph.build_dam_break(sc, prm)
+    ss, der, nl = _sorted_frame(system, prm)
+    cell, perm, cidx, ref = _oracle_frame(system, prm)
+    assert np.array_equal(nl["sort_perm"], perm)
+    eng = sph.make_engine(gather_cfg("slowcellsh", "fp32"))
+    out = eng.compute(ss, der, types.SimpleNamespace(cell_of=nl["cell_of"]), None, prm)
+    assert eng.last_pi_block == 384
+    _check_vs_oracle(out, ref)
+
+
+@pytest.mark.slow
+def test_collapsed_c2_production_build_vs_fp64():
+    """A collapsed frame (C2 after 2,000 FP32 steps, t ~ 0.14 s: the column is falling, cells
+    hold 30-100 particles): the production FP32 build against the FP64 kernel, which is
+    bit-identical to the reference's gather, and against the oracle gather on the oracle NL."""
+    sc = sph.named_scenario("c2")
+    prm = sph.make_params(sc)
+    cfg = gather_cfg("slowcellsh", "fp32")
+    system, _ = sph.run_simulation(sc, prm, cfg, max_steps=2000, stage_timing=False)
+    ss, der, nl = _sorted_frame(system, prm)
+    grid = types.SimpleNamespace(cell_of=nl["cell_of"])
+    counts = np.bincount(nl["cell_of"][ss.count_boundary:])
+    assert counts.max() > 64  # no longer the lattice
+    o64 = sph.make_engine(gather_cfg("slowcellsh", "fp64")).compute(ss, der, grid, None, prm)
+    cell, perm, cidx, ref = _oracle_frame(system, prm)
+    assert np.array_equal(nl["sort_perm"], perm)
+    assert np.array_equal(o64.accel, ref["accel"]) and np.array_equal(o64.drho_dt, ref["drho_dt"])
+    for block in (384, 128):
+        eng = sph.make_engine(cfg, pi_block=block)
+        out = eng.compute(ss, der, grid, None, prm)
+        _check_vs_oracle(out, ref)
 
 
 @pytest.mark.slow
