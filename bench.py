@@ -159,17 +159,87 @@ class Clocks:
 
 # ---------------------------------------------------------------- CPU reference (oracle port)
 _NL_CACHE = {}
-FULL_NL_SU_MAX = 12_000_000  # above this, NL and SU are timed on a bounded prefix and scaled
+FULL_NL_SU_MAX = 12_000_000  # above this, one CPU step is a bounded sample (see cpu_reference)
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def workload_config(cfg_name, sc, system, n_subdiv, world):
+    """The ``config`` object of both arms (identical for the same workload)."""
+    variant = "slowcellsh" if n_subdiv == 1 else "slowcellshalf"
+    n = system.n
+    if world > 1:
+        wl = f"{cfg_name}: {scenario_kind(sc)}, {n:,} particles over {world} GPUs (~{n // world:,} per GPU)"
+        par = f"{world} X-slabs (NCCL send/recv of migrants + halo rows)"
+    else:
+        wl = (f"{cfg_name}: {scenario_kind(sc)}, {n:,} particles per GPU "
+              f"({system.count_fluid:,} fluid + {system.count_boundary:,} boundary)")
+        par = "1 GPU"
+    return {"workload": wl, "particles": n, "particles_per_gpu": n // max(world, 1),
+            "n_subdiv": n_subdiv, "variant": variant,
+            "l2": ("inputs larger than L2 (resident state ~%.2f GB per GPU, no flush needed)"
+                   if n / max(world, 1) * 184 > 126e6 else
+                   "inputs smaller than L2 (resident state ~%.3f GB; parity-size configuration, no flush)")
+            % (n / max(world, 1) * 184 / 1e9),
+            "parallelism": par}
+
+
+class CpuStepper:
+    """The reference step loop (sim.py:300-351 with GatherEngine, gather.py:42-110) on the
+    oracle's bit-exact CPU restatement: numpy NL and SU as the reference runs them, the
+    gather kernels in C on all host threads (the reference's numba kernels, nogil, one
+    ThreadPoolExecutor worker per core).  Each ``step()`` advances the state, so timed steps
+    see the evolving system, as harness.py:123-128 times them."""
+
+    def __init__(self, system, prm, n_subdiv, cores):
+        import oracle
+        self.o, self.prm, self.cores = oracle, prm, cores
+        self.variant = "slowcellsh" if n_subdiv == 1 else "slowcellshalf"
+        self.pos, self.vel, self.rho = system.pos.copy(), system.vel.copy(), system.rho.copy()
+        self.ids = np.asarray(system.id).copy()
+        self.vel_prev, self.rho_prev = self.vel.copy(), self.rho.copy()
+        self.nb, self.mf, self.mb = system.count_boundary, system.mass_fluid, system.mass_boundary
+        self.step_no = 0
+
+    def step(self):
+        o, prm, nb = self.o, self.prm, self.nb
+        t0 = time.perf_counter()
+        cell, dims, _ = o.assign_cells(self.pos, prm)
+        if np.any(cell == o.OUT_OF_DOMAIN):
+            raise RuntimeError("reference arm: particle left the domain")
+        perm = o.sort_perm(cell, nb)
+        self.pos, self.vel, self.rho, self.ids = (a[perm] for a in (self.pos, self.vel, self.rho, self.ids))
+        self.vel_prev, self.rho_prev = self.vel_prev[perm], self.rho_prev[perm]
+        cs = cell[perm]
+        cidx = o.cell_index(cs, nb, int(np.prod(dims)))
+        t1 = time.perf_counter()
+        out = o.gather(self.pos, self.vel, self.rho, nb, self.mf, self.mb, cs, dims, cidx, prm,
+                       variant=self.variant, nthreads=self.cores)
+        t2 = time.perf_counter()
+        dt = o.compute_dt(out["accel"], out["visc_dt"], out["derived"][1], nb, prm)
+        self.pos, self.vel, self.rho, self.vel_prev, self.rho_prev = o.verlet_update(
+            self.step_no, self.pos, self.vel, self.rho, self.vel_prev, self.rho_prev, out["accel"],
+            out["drho_dt"], nb, prm, dt)
+        t3 = time.perf_counter()
+        self.step_no += 1
+        self.last = dict(cidx=cidx, dims=dims)
+        return dict(nl=t1 - t0, pi=t2 - t1, su=t3 - t2, step_s=t3 - t0, counters=out["counters"])
 
 
 def cpu_reference(system, prm, n_subdiv, budget_s, repeats=1):
-    """Time the reference algorithm's CPU restatement (oracle/: numpy NL/SU, C OpenMP gather,
-    bit-exact to the reference) on this host.  Up to FULL_NL_SU_MAX particles NL and SU run
-    in full; above it (the multi-GPU weak-scaling and wave-tank workloads) they run on the
-    first FULL_NL_SU_MAX rows and are scaled by n / m (n log n for the sort), so one step
-    stays a bounded sample.  PI runs on every ``stride``-th target of both passes (a
-    spatially uniform sample, sized so PI takes about ``budget_s``) and is scaled by the
-    stride (stride 1 = the full pass)."""
+    """Bounded sample of one reference step for workloads above FULL_NL_SU_MAX particles (the
+    multi-GPU weak-scaling and wave-tank workloads, timed on rank 0 alone): NL and SU on the
+    first FULL_NL_SU_MAX rows scaled by n / m (n log n for the sort); PI on every
+    ``stride``-th target (a spatially uniform sample sized to about ``budget_s``) scaled by the
+    stride.  The state is not advanced (one step of the initial frame)."""
     import oracle
     cores = len(os.sched_getaffinity(0))
     variant = "slowcellsh" if n_subdiv == 1 else "slowcellshalf"
@@ -189,18 +259,11 @@ def cpu_reference(system, prm, n_subdiv, budget_s, repeats=1):
     times = []
     for _ in range(repeats):
         t0 = time.perf_counter()
-        if m == n:
-            cell, dims_t, _ = oracle.assign_cells(system.pos, prm)
-            p_t = oracle.sort_perm(cell, nb)
-            c_t = cell[p_t]
-            oracle.cell_index(c_t, nb, int(np.prod(dims_t)))
-            t_nl = time.perf_counter() - t0
-        else:
-            sub = system.pos[:m]
-            cell, dims_t, _ = oracle.assign_cells(sub, prm)
-            p_t = oracle.sort_perm(cell, min(nb, m))
-            oracle.cell_index(cell[p_t], min(nb, m), int(np.prod(dims_t)))
-            t_nl = (time.perf_counter() - t0) * scale_sort
+        sub = system.pos[:m]
+        cell, dims_t, _ = oracle.assign_cells(sub, prm)
+        p_t = oracle.sort_perm(cell, min(nb, m))
+        oracle.cell_index(cell[p_t], min(nb, m), int(np.prod(dims_t)))
+        t_nl = (time.perf_counter() - t0) * scale_sort
         args = (pos, vel, rho, nb, system.mass_fluid, system.mass_boundary, cs, dims, cidx, prm)
         idx = np.arange(n)
         if ("pi", key) not in _NL_CACHE:
@@ -230,40 +293,101 @@ def cpu_reference(system, prm, n_subdiv, budget_s, repeats=1):
     t_nl, t_pi, t_su, stride = min(times, key=lambda t: t[0] + t[1] + t[2])
     step_s = t_nl + t_pi + t_su
     what = "every item" if stride == 1 else f"every {stride}th item (uniform sample, scaled x{stride})"
-    nlsu = ("full NL+SU (numpy, as the reference)" if m == n else
-            f"NL+SU (numpy, as the reference) on the first {m} rows, scaled to {n}")
     return dict(value=n / step_s, unit=UNIT, cores=cores, kind="port",
-                sample=f"one {variant} step of this workload on {cores} threads: {nlsu}, "
+                sample=f"one {variant} step of the initial frame on {cores} threads ({cpu_model()}): "
+                       f"NL+SU (numpy, as the reference) on the first {m} rows, scaled to {n}; "
                        f"PI (oracle C, OpenMP) on {what}; "
                        f"stage s NL {t_nl:.2f} PI {t_pi:.2f} SU {t_su:.2f}",
-                step_s=step_s)
+                step_s=step_s, exact=False)
+
+
+def cpu_steps(system, prm, n_subdiv, warmup, steps):
+    """``warmup`` + ``steps`` whole reference steps (CpuStepper) on all host cores; returns the
+    mean of the timed ones."""
+    cores = len(os.sched_getaffinity(0))
+    st = CpuStepper(system, prm, n_subdiv, cores)
+    for _ in range(warmup):
+        st.step()
+    t = [st.step() for _ in range(steps)]
+    mean = lambda k: float(np.mean([x[k] for x in t]))  # noqa: E731
+    step_s = mean("step_s")
+    return dict(value=system.n / step_s, unit=UNIT, cores=cores, kind="port",
+                sample=f"{steps} whole {st.variant} steps (after {warmup} warm-up), state advanced "
+                       f"each step, on {cores} threads ({cpu_model()}): NL and SU numpy as the "
+                       f"reference, PI the reference's gather kernels in C (OpenMP); mean stage s "
+                       f"NL {mean('nl'):.2f} PI {mean('pi'):.2f} SU {mean('su'):.2f}",
+                step_s=step_s, exact=True, stages_s={k: mean(k) for k in ("nl", "pi", "su")},
+                stepper=st)
+
+
+def cpu_engine_extras(stepper, prm, cores, budget_s=6.0):
+    """The reference's other CPU strategies on the stepper's current frame (cellpairs.py):
+    symmetric pair evaluation with private accumulators on all cores (the paper's best CPU
+    strategy, cellpairs.py:132-164) and single-threaded symmetric (cellpairs.py:59-69).  Their
+    PI pass runs on a uniform sample of cells (every k-th cell) and is scaled; the per-pass fixed
+    cost (private buffers, merge) is measured with an empty sample.  NL + SU are the gather
+    steps' (same code in the reference)."""
+    o = stepper.o
+    st, last = stepper, stepper.last
+    args = (st.pos, st.vel, st.rho, st.nb, st.mf, st.mb, last["dims"], last["cidx"], prm)
+    ncells = int(np.prod(last["dims"]))
+    out = {}
+    for name, threads in (("symmetric_x%d" % cores, cores), ("symmetric_1core", 1)):
+        t0 = time.perf_counter()
+        o.cellpairs(*args, symmetric=True, threads=threads, cells_mask=np.zeros(ncells, np.uint8))
+        t_fixed = time.perf_counter() - t0
+        probe = 64
+        t0 = time.perf_counter()
+        o.cellpairs(*args, symmetric=True, threads=threads,
+                    cells_mask=(np.arange(ncells) % probe == 0).astype(np.uint8))
+        est = t_fixed + max(time.perf_counter() - t0 - t_fixed, 0.0) * probe
+        stride = max(1, int(math.ceil(est / budget_s)))
+        t0 = time.perf_counter()
+        o.cellpairs(*args, symmetric=True, threads=threads,
+                    cells_mask=(np.arange(ncells) % stride == 0).astype(np.uint8) if stride > 1 else None)
+        t_pi = t_fixed + max(time.perf_counter() - t0 - t_fixed, 0.0) * stride
+        out[name] = {"pi_s": t_pi, "cells_sample": f"every {stride}th cell, scaled x{stride}",
+                     "threads": threads}
+    return out
 
 
 def run_reference(args, cfg_name):
     rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
         return
     sc, prm, system = workload(cfg_name, args.n_subdiv)
-    for _ in range(args.warmup):
-        cpu_reference(system, prm, args.n_subdiv, budget_s=1.5)
-    t = [cpu_reference(system, prm, args.n_subdiv, budget_s=1.5) for _ in range(args.steps)]
-    step_s = float(np.mean([x["step_s"] for x in t]))
+    extras = None
+    if system.n <= FULL_NL_SU_MAX:
+        r = cpu_steps(system, prm, args.n_subdiv, args.warmup, args.steps)
+        if world == 1:
+            ex = cpu_engine_extras(r["stepper"], prm, r["cores"])
+            nl_su = r["stages_s"]["nl"] + r["stages_s"]["su"]
+            extras = {k: dict(v, value=system.n / (nl_su + v["pi_s"]), unit=UNIT) for k, v in ex.items()}
+        step_s = r["step_s"]
+    else:
+        for _ in range(args.warmup):
+            cpu_reference(system, prm, args.n_subdiv, budget_s=1.5)
+        t = [cpu_reference(system, prm, args.n_subdiv, budget_s=1.5) for _ in range(args.steps)]
+        step_s = float(np.mean([x["step_s"] for x in t]))
+        r = dict(t[-1])
     value = system.n / step_s
-    cb = dict(t[-1])
+    cb = {k: r[k] for k in ("unit", "cores", "kind", "sample")}
     cb["value"] = value
-    cb.pop("step_s", None)
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_s * 1e3,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic dam break (reference Scenario/build_dam_break lattice)",
-            "config": {"workload": cfg_name, "particles": system.n, "n_subdiv": args.n_subdiv},
+            "data": "synthetic: reference dam-break lattice (Scenario/build_dam_break), hydrostatic rho",
+            "config": workload_config(cfg_name, sc, system, args.n_subdiv, args.gpus),
             "cpu_baseline": cb,
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    if extras:
+        line["cpu_engines"] = extras
     print(json.dumps(line), flush=True)
 
 
 # ---------------------------------------------------------------- multi-GPU (X slabs)
-def run_slabs(args, cfg_name, system, prm, prec, world, rank, local):
+def run_slabs(args, cfg_name, sc, system, prm, prec, world, rank, local):
     """One X-slab per GPU (dslab.DeviceSlabSim): device classify/scatter of migrants and halo
     rows, NCCL send/recv of exact byte counts, owned-target interaction, device all-reduces of
     the dt minima and counters; one host synchronisation per step (the totals all-gather)."""
@@ -376,15 +500,11 @@ def run_slabs(args, cfg_name, system, prm, prec, world, rank, local):
         "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": args.precision,
         "data": "synthetic: reference dam-break lattice (Scenario/build_dam_break), hydrostatic rho",
-        "config": {"workload": f"{cfg_name}: 3-D dam break, {system.n:,} particles over {world} "
-                               f"GPUs (~{system.n // world:,} per GPU)",
-                   "particles": system.n, "n_subdiv": args.n_subdiv,
-                   "l2": "inputs larger than L2",
-                   "parallelism": f"{world} X-slabs (device-resident exchange: NCCL send/recv of "
-                                  "migrants + halo rows, device all-reduce of dt and counters)",
-                   "slab_bounds": [int(v) for v in sim.bounds],
-                   "pi_block_rank0": int(pi_blocks[0]),
-                   "max_owned_per_gpu": int(owned.item())},
+        "config": workload_config(cfg_name, sc, system, args.n_subdiv, world),
+        "build": {"slab_bounds": [int(v) for v in sim.bounds], "pi_block_rank0": int(pi_blocks[0]),
+                  "max_owned_per_gpu": int(owned.item()),
+                  "exchange": "device-resident: NCCL send/recv of migrants + halo rows, device "
+                              "all-reduce of dt and counters"},
         "interactions_per_s": true_pairs * args.steps / (total_ms * 1e-3),
         "pair_evals_per_s": evals * args.steps / (total_ms * 1e-3),
         "gpu_launches": args.steps * sim.launches_per_step(),
@@ -438,7 +558,7 @@ def main():
     variant = "slowcellsh" if args.n_subdiv == 1 else "slowcellshalf"
     prec = _lib.SPHB_FP64 if args.precision == "fp64" else _lib.SPHB_FP32
     if world > 1 or args.slab_path:
-        run_slabs(args, cfg_name, system, prm, prec, world, rank, local)
+        run_slabs(args, cfg_name, sc, system, prm, prec, world, rank, local)
         return
     sim = DeviceSim(system, prm, reach=args.n_subdiv, precision=prec,
                     record_capacity=max(64, args.warmup + 2 * args.steps + 16))
@@ -597,13 +717,9 @@ def main():
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
         "scaling": "weak" if world > 1 else "weak", "vs_baseline": None, "dtype": args.precision,
         "data": "synthetic: reference dam-break lattice (Scenario/build_dam_break), hydrostatic rho",
-        "config": {"workload": f"{cfg_name}: {scenario_kind(sc)}, {system.n:,} particles per GPU "
-                               f"({system.count_fluid:,} fluid + {system.count_boundary:,} boundary)",
-                   "particles_per_gpu": system.n, "n_subdiv": args.n_subdiv, "variant": variant,
-                   "l2": "inputs larger than L2 (resident state ~%.1f GB)" % (sim.n * 184 / 1e9),
-                   "parallelism": f"{world} GPU" + (" replicas" if world > 1 else ""),
-                   "pi_block": sim.pi_block, "pi_lane_use": round(sim.pi_lane_use(), 4),
-                   "cuda_graph": use_graph},
+        "config": workload_config(cfg_name, sc, system, args.n_subdiv, world),
+        "build": {"pi_block": sim.pi_block, "pi_lane_use": round(sim.pi_lane_use(), 4),
+                  "cuda_graph": use_graph},
         "interactions_per_s": true_pairs * world * args.steps / (total_ms * 1e-3),
         "pair_evals_per_s": evals * world * args.steps / (total_ms * 1e-3),
         "stage_ms": {"nl": float(np.mean(nl_ms)), "pi": pi_mean, "su": float(np.mean(su_ms))},
@@ -633,9 +749,11 @@ def main():
                                f"round trip pipelined in {args.e2e_chunks} row chunks over "
                                "full-duplex PCIe (H2D of step k+1 chunk c after D2H of step k chunk c)"}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cb = cpu_reference(system, prm, args.n_subdiv, args.cpu_budget_s)
-        cb.pop("step_s", None)
-        line["cpu_baseline"] = cb
+        if system.n <= FULL_NL_SU_MAX:  # ~3 whole reference steps (C3: ~15-20 s of CPU work)
+            cb = cpu_steps(system, prm, args.n_subdiv, 1, 2)
+        else:
+            cb = cpu_reference(system, prm, args.n_subdiv, args.cpu_budget_s)
+        line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:

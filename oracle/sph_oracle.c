@@ -27,6 +27,13 @@
  *   gather_fluid_ranges    engines/kernels.py:421-497  (order=1: all fluid rows, then boundary rows)
  *   gather_boundary_cells  engines/kernels.py:500-555
  *   counter normalisation  engines/gather.py:103-109 (done by the Python caller)
+ *   eval_scatter           engines/kernels.py:29-68
+ *   scan_block (lanes=1)   engines/kernels.py:71-118 (lanes=4 evaluates the same pairs in the
+ *                          same order, only delayed within the block: identical sums)
+ *   run_cells_symmetric    engines/kernels.py:121-175
+ *   run_cells_asymmetric   engines/kernels.py:178-223
+ *   symmetric threading    engines/cellpairs.py:132-164 + balance.py:12-43 (private buffers,
+ *                          cyclic blocks of cells, merged in thread order)
  */
 #include <math.h>
 #include <stdint.h>
@@ -235,6 +242,211 @@ void oracle_gather_pass(int fluid_items, int order, int64_t i_lo, int64_t i_hi, 
   counters_out[1] = c_true;
   counters_out[2] = c_eval;
   counters_out[3] = c_ff;
+}
+
+/* ---------------------------------------------------------------- cell-pair engines */
+typedef struct {
+  int64_t cand, tru, evals, ff;
+} cnt_t;
+
+/* kernels.py:29-68: pair (i, j) evaluated once, scattered to i and (both) to j */
+static inline void eval_scatter(const state_t* s, int64_t i, int64_t j, int both, int64_t nb,
+                                double* acc, double* drho, double* viscdt, cnt_t* c) {
+  const double* pp = s->pp;
+  side_t si, sj;
+  load_side(s, i, &si);
+  load_side(s, j, &sj);
+  double dx = si.x - sj.x;
+  double dy = si.y - sj.y;
+  double dz = si.z - sj.z;
+  double r2 = dx * dx + dy * dy + dz * dz;
+  double fx, fy, fz, drc, mu;
+  pair_eval(dx, dy, dz, r2, si.vx - sj.vx, si.vy - sj.vy, si.vz - sj.vz, si.rh, sj.rh, si.pr,
+            sj.pr, si.cs, sj.cs, si.te, sj.te, pp, &fx, &fy, &fz, &drc, &mu);
+  double mi = i < nb ? pp[PP_MASSB] : pp[PP_MASSF];
+  double mj = j < nb ? pp[PP_MASSB] : pp[PP_MASSF];
+  if (i >= nb) {
+    acc[3 * i + 0] -= mj * fx;
+    acc[3 * i + 1] -= mj * fy;
+    acc[3 * i + 2] -= mj * fz;
+  }
+  drho[i] += mj * drc;
+  if (mu > viscdt[i]) viscdt[i] = mu;
+  c->evals += 1;
+  if (i >= nb && j >= nb) c->ff += 1;
+  if (both) {
+    if (j >= nb) {
+      acc[3 * j + 0] += mi * fx;
+      acc[3 * j + 1] += mi * fy;
+      acc[3 * j + 2] += mi * fz;
+    }
+    drho[j] += mi * drc;
+    if (mu > viscdt[j]) viscdt[j] = mu;
+  }
+}
+
+/* kernels.py:71-118 with lanes == 1 */
+static inline void scan_block(const state_t* s, int64_t i0, int64_t i1, int64_t j0, int64_t j1,
+                              int ordered, int skip_self, int both, int64_t nb, double* acc,
+                              double* drho, double* viscdt, cnt_t* c) {
+  const double sup2 = s->pp[PP_SUP2];
+  for (int64_t i = i0; i < i1; ++i) {
+    double xi = (double)s->pos[3 * i + 0], yi = (double)s->pos[3 * i + 1],
+           zi = (double)s->pos[3 * i + 2];
+    int64_t js = ordered ? i + 1 : j0;
+    for (int64_t j = js; j < j1; ++j) {
+      if (skip_self && j == i) continue;
+      c->cand += 1;
+      double dx = xi - (double)s->pos[3 * j + 0];
+      double dy = yi - (double)s->pos[3 * j + 1];
+      double dz = zi - (double)s->pos[3 * j + 2];
+      double r2 = dx * dx + dy * dy + dz * dz;
+      if (r2 < sup2 && r2 > 0.0) {
+        c->tru += 1;
+        eval_scatter(s, i, j, both, nb, acc, drho, viscdt, c);
+      }
+    }
+  }
+}
+
+/* kernels.py:121-175 (symmetric) / 178-223 (asymmetric) over cells[0..ncl) */
+static void run_cells(const state_t* s, int symmetric, const int64_t* cells, int64_t ncl,
+                      int64_t nx, int64_t ny, int64_t nz, int reach, const int64_t* fbeg,
+                      const int64_t* fend, const int64_t* bbeg, const int64_t* bend, int64_t nb,
+                      double* acc, double* drho, double* viscdt, cnt_t* c) {
+  const int64_t nxy = nx * ny;
+  for (int64_t t = 0; t < ncl; ++t) {
+    int64_t cc = cells[t];
+    int64_t cz = cc / nxy, rem = cc - cz * (nx * ny), cy = rem / nx, cx = rem - cy * nx;
+    int64_t cf0 = fbeg[cc], cf1 = fend[cc], cb0 = bbeg[cc], cb1 = bend[cc];
+    if (cf1 == cf0 && cb1 == cb0) continue;
+    if (symmetric) {
+      scan_block(s, cf0, cf1, cf0, cf1, 1, 0, 1, nb, acc, drho, viscdt, c);
+      scan_block(s, cf0, cf1, cb0, cb1, 0, 0, 1, nb, acc, drho, viscdt, c);
+      for (int64_t dz = 0; dz <= reach; ++dz) {
+        int64_t zz = cz + dz;
+        if (zz >= nz) continue;
+        for (int64_t dy = dz > 0 ? -reach : 0; dy <= reach; ++dy) {
+          int64_t yy = cy + dy;
+          if (yy < 0 || yy >= ny) continue;
+          for (int64_t dxo = (dz > 0 || dy > 0) ? -reach : 1; dxo <= reach; ++dxo) {
+            int64_t xx = cx + dxo;
+            if (xx < 0 || xx >= nx) continue;
+            int64_t d = xx + nx * (yy + ny * zz);
+            scan_block(s, cf0, cf1, fbeg[d], fend[d], 0, 0, 1, nb, acc, drho, viscdt, c);
+            scan_block(s, cf0, cf1, bbeg[d], bend[d], 0, 0, 1, nb, acc, drho, viscdt, c);
+            scan_block(s, cb0, cb1, fbeg[d], fend[d], 0, 0, 1, nb, acc, drho, viscdt, c);
+          }
+        }
+      }
+    } else {
+      int64_t xlo = cx - reach > 0 ? cx - reach : 0;
+      int64_t xhi = cx + reach < nx - 1 ? cx + reach : nx - 1;
+      for (int64_t dz = -reach; dz <= reach; ++dz) {
+        int64_t zz = cz + dz;
+        if (zz < 0 || zz >= nz) continue;
+        for (int64_t dy = -reach; dy <= reach; ++dy) {
+          int64_t yy = cy + dy;
+          if (yy < 0 || yy >= ny) continue;
+          int64_t base = nx * (yy + ny * zz);
+          int64_t jf0 = fbeg[xlo + base], jf1 = fend[xhi + base];
+          int64_t jb0 = bbeg[xlo + base], jb1 = bend[xhi + base];
+          scan_block(s, cf0, cf1, jf0, jf1, 0, 1, 0, nb, acc, drho, viscdt, c);
+          scan_block(s, cf0, cf1, jb0, jb1, 0, 0, 0, nb, acc, drho, viscdt, c);
+          scan_block(s, cb0, cb1, jf0, jf1, 0, 0, 0, nb, acc, drho, viscdt, c);
+        }
+      }
+    }
+  }
+}
+
+/*
+ * CellPairsEngine.compute (cellpairs.py:41-90) for threading "single" (nthreads_logical <= 1:
+ * all cells in order into the outputs) and "symmetric" (nthreads_logical = T: blocks of
+ * block_of_cells cells dealt cyclically to T private accumulators, merged in thread order --
+ * bit-identical to the reference at the same T).  cells_mask (may be NULL) restricts the
+ * traversal to a subset of cells (bounded CPU-baseline samples).  counters_out = raw counters
+ * (symmetric: unordered; asymmetric: ordered, the caller halves `true`).
+ */
+void oracle_cellpairs(int symmetric, int nthreads_logical, int64_t block_of_cells, int reach,
+                      int64_t nx, int64_t ny, int64_t nz, const int64_t* fbeg, const int64_t* fend,
+                      const int64_t* bbeg, const int64_t* bend, int64_t n, int64_t nb, int dmode,
+                      const float* pos, const float* vel, const float* rho, const float* press,
+                      const float* prrho, const float* csound, const float* tensil,
+                      const double* pp, const uint8_t* cells_mask, double* acc, double* drho,
+                      double* viscdt, int64_t* counters_out) {
+  state_t s = {pos, vel, rho, press, prrho, csound, tensil, pp, dmode};
+  const int64_t ncells = nx * ny * nz;
+  int T = nthreads_logical > 1 ? nthreads_logical : 1;
+  int64_t* cells = (int64_t*)malloc(sizeof(int64_t) * (ncells > 0 ? ncells : 1));
+  cnt_t total = {0, 0, 0, 0};
+  if (T == 1) {
+    int64_t m = 0;
+    for (int64_t c = 0; c < ncells; ++c)
+      if (!cells_mask || cells_mask[c]) cells[m++] = c;
+    run_cells(&s, symmetric, cells, m, nx, ny, nz, reach, fbeg, fend, bbeg, bend, nb, acc, drho,
+              viscdt, &total);
+  } else {
+    /* thread t's cell list = blocks t, t + T, t + 2T, ... in order (cellpairs.py:141-146) */
+    int64_t nblocks = (ncells + block_of_cells - 1) / block_of_cells;
+    int64_t* start = (int64_t*)malloc(sizeof(int64_t) * (T + 1));
+    int64_t m = 0;
+    for (int t = 0; t < T; ++t) {
+      start[t] = m;
+      for (int64_t b = t; b < nblocks; b += T)
+        for (int64_t c = b * block_of_cells; c < (b + 1) * block_of_cells && c < ncells; ++c)
+          if (!cells_mask || cells_mask[c]) cells[m++] = c;
+    }
+    start[T] = m;
+    double** pa = (double**)malloc(sizeof(double*) * T);
+    double** pd = (double**)malloc(sizeof(double*) * T);
+    double** pv = (double**)malloc(sizeof(double*) * T);
+    cnt_t* pc = (cnt_t*)calloc(T, sizeof(cnt_t));
+#ifdef _OPENMP
+#pragma omp parallel for schedule(static, 1)
+#endif
+    for (int t = 0; t < T; ++t) {
+      pa[t] = t == 0 ? acc : (double*)calloc(3 * n, sizeof(double));
+      pd[t] = t == 0 ? drho : (double*)calloc(n, sizeof(double));
+      pv[t] = t == 0 ? viscdt : (double*)calloc(n, sizeof(double));
+      run_cells(&s, symmetric, cells + start[t], start[t + 1] - start[t], nx, ny, nz, reach, fbeg,
+                fend, bbeg, bend, nb, pa[t], pd[t], pv[t], &pc[t]);
+    }
+    /* merge_accumulators: out = acc[0]; out += acc[1]; ... elementwise, thread order */
+#ifdef _OPENMP
+#pragma omp parallel for schedule(static)
+#endif
+    for (int64_t i = 0; i < n; ++i) {
+      for (int t = 1; t < T; ++t) {
+        acc[3 * i + 0] += pa[t][3 * i + 0];
+        acc[3 * i + 1] += pa[t][3 * i + 1];
+        acc[3 * i + 2] += pa[t][3 * i + 2];
+        drho[i] += pd[t][i];
+        if (pv[t][i] > viscdt[i]) viscdt[i] = pv[t][i];
+      }
+    }
+    for (int t = 0; t < T; ++t) {
+      total.cand += pc[t].cand;
+      total.tru += pc[t].tru;
+      total.evals += pc[t].evals;
+      total.ff += pc[t].ff;
+      if (t) {
+        free(pa[t]);
+        free(pd[t]);
+        free(pv[t]);
+      }
+    }
+    free(pa);
+    free(pd);
+    free(pv);
+    free(pc);
+    free(start);
+  }
+  free(cells);
+  counters_out[0] = total.cand;
+  counters_out[1] = total.tru;
+  counters_out[2] = total.evals;
+  counters_out[3] = total.ff;
 }
 
 int oracle_max_threads(void) {

@@ -139,3 +139,37 @@ def test_brute_force_agrees_with_gather():
     assert bf["true_pairs"] == int(z["slowcellsh_counters"][1])
     assert oracle.rel_linf(bf["accel"], z["slowcellsh_accel"]) < 1e-4
     assert oracle.rel_linf(bf["drho_dt"], z["slowcellsh_drho"]) < 1e-4
+
+
+# ------------------------------------------------------------------ cell-pair engines
+SYM_FRAMES = ["small_n1", "small_n2", "mid5k_n1", "mid5k_n2", "uniform3k_n1", "c1mid_n1"]
+
+
+@pytest.mark.parametrize("name", SYM_FRAMES)
+@pytest.mark.parametrize("tag,symmetric,threads", [("sym1", True, 1), ("symT", True, 4),
+                                                   ("asym1", False, 1)])
+def test_cellpairs_bit_exact(name, tag, symmetric, threads):
+    """oracle.cellpairs == the reference's CellPairsEngine (run_cells_symmetric /
+    run_cells_asymmetric, private-accumulator threading at T = 4), bit for bit, on the
+    frames' sorted state (tests/golden/make_golden_sym.py ran the reference)."""
+    z = golden(f"frame_{name}.npz")
+    g = golden(f"sym_{name}.npz")
+    prm = oracle.params_from_npz(z)
+    out = oracle.cellpairs(z["s_pos"], z["s_vel"], z["s_rho"], int(z["s_nb"]),
+                           float(z["s_mass_fluid"]), float(z["s_mass_boundary"]), z["dims"],
+                           (z["fbeg"], z["fend"], z["bbeg"], z["bend"]), prm,
+                           symmetric=symmetric, threads=threads, block_of_cells=10)
+    assert np.array_equal(out["counters"], g[f"{tag}_counters"])
+    assert np.array_equal(out["accel"], g[f"{tag}_accel"])
+    assert np.array_equal(out["drho_dt"], g[f"{tag}_drho"])
+    assert np.array_equal(out["visc_dt"], g[f"{tag}_visc"])
+
+
+@pytest.mark.parametrize("name", SYM_FRAMES)
+def test_symmetric_counters_relate_to_gather(name):
+    """The reference's counter contract between traversals: same unordered true pairs,
+    symmetric evals = true (each pair evaluated once), ff halves (ordered -> unordered)."""
+    g = golden(f"sym_{name}.npz")
+    s, a = g["sym1_counters"], g["asym1_counters"]
+    assert s[1] == a[1] and s[2] == s[1] and a[2] == 2 * a[1] and 2 * s[3] == a[3]
+    assert np.array_equal(g["symT_counters"], s)
