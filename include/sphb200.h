@@ -219,16 +219,30 @@ int sphb_cell_ranges_from_sorted(sphb_workspace_t* ws, const sphb_grid_t* grid,
                                  const int32_t* cell_sorted, int64_t n, int64_t nb, int32_t* beg,
                                  int32_t* end, sphb_stream_t s);
 
+/* Force buffers (acc, drho, visc) of sphb_interact / sphb_integrate* / sphb_step.  Callers
+ * size them for the FP64 layout (24 + 8 + 8 B per particle); what is stored depends on
+ * prm->precision:
+ *   SPHB_FP64  the ForceOutput layout (config.py:94-103): acc (n,3) f64 (boundary rows 0),
+ *              drho (n) f64, visc (n) f64 -- bit-identical to the reference;
+ *   SPHB_FP32  acc holds one float4 (ax, ay, az, drho) per particle, visc one float per
+ *              particle; drho is unused (may be NULL).  20 B per particle written by PI and
+ *              16 B read by K7; sphb_forces_f64 widens it (exactly) to the FP64 layout. */
+
 /* K5/K5b/K6 -- GatherEngine.compute (engines/gather.py:42-110): fused fluid pass
  * (gather_fluid_cells / _ranges, kernels.py:326-497) and boundary pass (gather_boundary_*,
  * kernels.py:500-596), plus the compute_dt reductions (sim.py:215-232) in the epilogue.
- * acc: (n,3) f64 (boundary rows 0), drho: (n) f64, visc: (n) f64 (ForceOutput, config.py:94-103).
  * Raw counters and the two dt minima accumulate into ctrl. */
 int sphb_interact(sphb_workspace_t* ws, const sphb_params_t* prm, const sphb_grid_t* grid,
                   int64_t n, int64_t nb,
                   const void* posp, const void* velr, const void* aux, const int32_t* cell_sorted,
-                  const int32_t* beg, const int32_t* end, double* acc, double* drho, double* visc,
+                  const int32_t* beg, const int32_t* end, void* acc, void* drho, void* visc,
                   sphb_ctrl_t* ctrl, sphb_stream_t s);
+
+/* The force buffers of prm->precision widened to the ForceOutput layout (f64 acc (n,3), drho,
+ * visc), rows [0, n); the FP32 -> f64 conversion is exact.  (gather.py:103-110 returns f64.) */
+int sphb_forces_f64(const sphb_params_t* prm, int64_t n, const void* acc, const void* drho,
+                    const void* visc, double* acc64, double* drho64, double* visc64,
+                    sphb_stream_t s);
 
 /* Resets the per-step accumulators (dt minima, counters) and evaluates the stop rules. */
 int sphb_step_begin(sphb_ctrl_t* ctrl, sphb_stream_t s);
@@ -238,7 +252,7 @@ int sphb_step_begin(sphb_ctrl_t* ctrl, sphb_stream_t s);
  * (unsorted-for-next-step) arrays.  Flags non-finite state / out-of-domain in ctrl. */
 int sphb_integrate(sphb_workspace_t* ws, const sphb_params_t* prm, const sphb_grid_t* grid,
                    int64_t n, int64_t nb, const void* posp_s, const void* velr_s,
-                   const void* prev_s, const int64_t* id_s, const double* acc, const double* drho,
+                   const void* prev_s, const int64_t* id_s, const void* acc, const void* drho,
                    void* posp, void* velr, void* prev, int64_t* id, uint32_t* keys_next,
                    sphb_ctrl_t* ctrl, sphb_stream_t s);
 
@@ -252,7 +266,7 @@ int sphb_integrate(sphb_workspace_t* ws, const sphb_params_t* prm, const sphb_gr
 int sphb_integrate_stage(sphb_workspace_t* ws, const sphb_params_t* prm, const sphb_grid_t* grid,
                          int64_t n, int64_t nb, int32_t stage, const void* posp_s,
                          const void* velr_s, const void* prev_s, const int64_t* id_s,
-                         const double* acc, const double* drho, void* posp, void* velr,
+                         const void* acc, const void* drho, void* posp, void* velr,
                          void* prev, int64_t* id, uint32_t* keys_next, sphb_ctrl_t* ctrl,
                          sphb_stream_t s);
 
@@ -336,7 +350,7 @@ typedef struct {
   int64_t* id_s;
   uint32_t *keys, *keys_sorted;
   int32_t *perm, *cell_s, *beg, *end;
-  double *acc, *drho, *visc;
+  void *acc, *drho, *visc;       /* force buffers, layout of prm->precision (above) */
 } sphb_state_t;
 
 int sphb_step(sphb_workspace_t* ws, const sphb_params_t* prm, const sphb_grid_t* grid, int64_t n,

@@ -124,6 +124,7 @@ def lib():
         "sphb_dt_terms": ([P, c_i64, c_i64, P, P, P, P, P], c_i32),
         "sphb_verlet_soa": ([P, c_i64, c_i64, c_i32, c_f64, P, P, P, P, P, P, P, P], c_i32),
         "sphb_step_launch_count": ([P, c_i64], c_i64),
+        "sphb_forces_f64": ([P, c_i64, P, P, P, P, P, P, P], c_i32),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)
@@ -141,7 +142,8 @@ EXPORTED = ("sphb_last_error", "sphb_version", "sphb_workspace_create", "sphb_wo
             "sphb_interact", "sphb_step_begin", "sphb_integrate", "sphb_step_end", "sphb_step",
             "sphb_step_launch_count", "sphb_integrate_stage", "sphb_energy", "sphb_slab_tiles",
             "sphb_slab_count", "sphb_slab_scatter", "sphb_slab_unpack", "sphb_state_from_soa",
-            "sphb_state_to_soa", "sphb_build_ranges", "sphb_dt_terms", "sphb_verlet_soa")
+            "sphb_state_to_soa", "sphb_build_ranges", "sphb_dt_terms", "sphb_verlet_soa",
+            "sphb_forces_f64")
 
 
 def check(rc: int, what: str = "") -> None:

@@ -79,7 +79,7 @@ static int check_params(const sphb_params_t* p) {
 int launch_interact(sphb_workspace* ws, const sphb_params_t& p, const sphb_grid_t& g, int64_t n,
                     int64_t nb, const float4* posp, const float4* velr, const float4* aux,
                     const int32_t* cell_sorted, const int32_t* beg, const int32_t* end,
-                    double* acc, double* drho, double* visc, sphb_ctrl_t* ctrl, cudaStream_t s) {
+                    void* acc, void* drho, void* visc, sphb_ctrl_t* ctrl, cudaStream_t s) {
   if (ws->pi_block == 256 && p.precision == SPHB_FP32)
     return pi256::launch_interact(ws, p, g, n, nb, posp, velr, aux, cell_sorted, beg, end, acc,
                                   drho, visc, ctrl, s);
@@ -339,7 +339,7 @@ int sphb_cell_ranges_from_sorted(sphb_workspace_t* ws, const sphb_grid_t* grid,
 int sphb_interact(sphb_workspace_t* ws, const sphb_params_t* prm, const sphb_grid_t* grid,
                   int64_t n, int64_t nb,
                   const void* posp, const void* velr, const void* aux, const int32_t* cell_sorted,
-                  const int32_t* beg, const int32_t* end, double* acc, double* drho, double* visc,
+                  const int32_t* beg, const int32_t* end, void* acc, void* drho, void* visc,
                   sphb_ctrl_t* ctrl, sphb_stream_t s) {
   SPHB_NONNULL(ws);
   if (int rc = check_params(prm)) return rc;
@@ -357,7 +357,7 @@ int sphb_interact(sphb_workspace_t* ws, const sphb_params_t* prm, const sphb_gri
   SPHB_NONNULL(beg);
   SPHB_NONNULL(end);
   SPHB_NONNULL(acc);
-  SPHB_NONNULL(drho);
+  if (prm->precision == SPHB_FP64) SPHB_NONNULL(drho);  /* FP32: drho travels in acc.w */
   SPHB_NONNULL(visc);
   return launch_interact(ws, *prm, *grid, n, nb, (const float4*)posp, (const float4*)velr,
                          (const float4*)aux, cell_sorted, beg, end, acc, drho, visc, ctrl,
@@ -371,7 +371,7 @@ int sphb_step_begin(sphb_ctrl_t* ctrl, sphb_stream_t s) {
 
 int sphb_integrate(sphb_workspace_t* ws, const sphb_params_t* prm, const sphb_grid_t* grid,
                    int64_t n, int64_t nb, const void* posp_s, const void* velr_s,
-                   const void* prev_s, const int64_t* id_s, const double* acc, const double* drho,
+                   const void* prev_s, const int64_t* id_s, const void* acc, const void* drho,
                    void* posp, void* velr, void* prev, int64_t* id, uint32_t* keys_next,
                    sphb_ctrl_t* ctrl, sphb_stream_t s) {
   SPHB_NONNULL(ws);
@@ -381,7 +381,8 @@ int sphb_integrate(sphb_workspace_t* ws, const sphb_params_t* prm, const sphb_gr
   if (n < 0 || nb < 0 || nb > n) return sphb_set_error(SPHB_E_INVALID, "bad n/nb");
   if (n > 0) {
     SPHB_NONNULL(posp_s); SPHB_NONNULL(velr_s); SPHB_NONNULL(prev_s); SPHB_NONNULL(id_s);
-    SPHB_NONNULL(acc); SPHB_NONNULL(drho); SPHB_NONNULL(posp); SPHB_NONNULL(velr);
+    SPHB_NONNULL(acc); if (prm->precision == SPHB_FP64) SPHB_NONNULL(drho);
+    SPHB_NONNULL(posp); SPHB_NONNULL(velr);
     SPHB_NONNULL(prev); SPHB_NONNULL(id); SPHB_NONNULL(keys_next);
   }
   return launch_integrate(ws, *prm, *grid, n, nb, (const float4*)posp_s, (const float4*)velr_s,
@@ -399,7 +400,7 @@ int sphb_step_end(sphb_ctrl_t* ctrl, const sphb_params_t* prm, sphb_step_record_
 int sphb_integrate_stage(sphb_workspace_t* ws, const sphb_params_t* prm, const sphb_grid_t* grid,
                          int64_t n, int64_t nb, int32_t stage, const void* posp_s,
                          const void* velr_s, const void* prev_s, const int64_t* id_s,
-                         const double* acc, const double* drho, void* posp, void* velr,
+                         const void* acc, const void* drho, void* posp, void* velr,
                          void* prev, int64_t* id, uint32_t* keys_next, sphb_ctrl_t* ctrl,
                          sphb_stream_t s) {
   SPHB_NONNULL(ws);
@@ -410,7 +411,8 @@ int sphb_integrate_stage(sphb_workspace_t* ws, const sphb_params_t* prm, const s
   if (n < 0 || nb < 0 || nb > n) return sphb_set_error(SPHB_E_INVALID, "bad n/nb");
   if (n > 0) {
     SPHB_NONNULL(posp_s); SPHB_NONNULL(velr_s); SPHB_NONNULL(prev_s); SPHB_NONNULL(id_s);
-    SPHB_NONNULL(acc); SPHB_NONNULL(drho); SPHB_NONNULL(posp); SPHB_NONNULL(velr);
+    SPHB_NONNULL(acc); if (prm->precision == SPHB_FP64) SPHB_NONNULL(drho);
+    SPHB_NONNULL(posp); SPHB_NONNULL(velr);
     SPHB_NONNULL(prev); SPHB_NONNULL(id); SPHB_NONNULL(keys_next);
   }
   return launch_integrate_mode(ws, *prm, *grid, n, nb, 1 + stage, (const float4*)posp_s,

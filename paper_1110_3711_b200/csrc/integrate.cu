@@ -71,7 +71,9 @@ __device__ __forceinline__ void piston_at(const sphb_params_t& p, double t, floa
 
 // MODE 0: verlet_update (sim.py:235-259), the reference.  MODE 1 / 2: symplectic predictor /
 // corrector (extension).  All fused with the next stage's assign_cells (K1) + histogram.
-template <int MODE>
+// F32: the FP32 force layout (float4 (ax, ay, az, drho) per particle in `acc`, include/
+// sphb200.h), widened exactly to f64 -- the same arithmetic as the FP64 layout's values.
+template <int MODE, bool F32>
 #ifndef SU_MINB
 #define SU_MINB 4  // 64 registers: 2x the resident warps of the default (memory-bound kernel)
 #endif
@@ -79,7 +81,7 @@ __global__ void __launch_bounds__(256, SU_MINB) k_integrate(
     sphb_params_t p, sphb_grid_t g, int cellbits, int64_t ncells, int64_t n, int64_t nb,
     const float4* __restrict__ posp_s, const float4* __restrict__ velr_s,
     const float4* __restrict__ prev_s, const int64_t* __restrict__ id_s,
-    const double* __restrict__ acc, const double* __restrict__ drho, float4* __restrict__ posp,
+    const void* __restrict__ accv, const double* __restrict__ drho, float4* __restrict__ posp,
     float4* __restrict__ velr, float4* __restrict__ prev, int64_t* __restrict__ id,
     uint32_t* __restrict__ keys_next, uint32_t* __restrict__ cnt, sphb_ctrl_t* ctrl) {
   if (!step_live(ctrl)) return;
@@ -99,7 +101,22 @@ __global__ void __launch_bounds__(256, SU_MINB) k_integrate(
     int64_t slot = -1;
     if (i < n) {
       const float4 ps = posp_s[i], vs = velr_s[i], pv = prev_s[i];
-      const double dr = drho[i];
+      double fa[3] = {0.0, 0.0, 0.0}, dr;
+      if (F32) {
+        const float4 a4 = ((const float4*)accv)[i];
+        fa[0] = a4.x;
+        fa[1] = a4.y;
+        fa[2] = a4.z;
+        dr = a4.w;
+      } else {
+        const double* acc = (const double*)accv;
+        dr = drho[i];
+        if (i >= nb) {
+          fa[0] = acc[3 * i + 0];
+          fa[1] = acc[3 * i + 1];
+          fa[2] = acc[3 * i + 2];
+        }
+      }
       float4 np, nv, nprev;
       double nrho;
       if (MODE == 0)
@@ -109,9 +126,9 @@ __global__ void __launch_bounds__(256, SU_MINB) k_integrate(
       else
         nrho = xadd((double)pv.w, xmul(dt, dr));
       if (i >= nb) {
-        const double ax = xadd(acc[3 * i + 0], p.g[0]);
-        const double ay = xadd(acc[3 * i + 1], p.g[1]);
-        const double az = xadd(acc[3 * i + 2], p.g[2]);
+        const double ax = xadd(fa[0], p.g[0]);
+        const double ay = xadd(fa[1], p.g[1]);
+        const double az = xadd(fa[2], p.g[2]);
         const double vx = (double)vs.x, vy = (double)vs.y, vz = (double)vs.z;
         if (MODE == 0) {
           np.x = __double2float_rn(xadd(xadd((double)ps.x, xmul(dt, vx)), xmul(c2, ax)));
@@ -283,7 +300,7 @@ int launch_step_begin(sphb_ctrl_t* ctrl, cudaStream_t s) {
 int launch_integrate_mode(sphb_workspace* ws, const sphb_params_t& p, const sphb_grid_t& g,
                           int64_t n, int64_t nb, int mode, const float4* posp_s,
                           const float4* velr_s, const float4* prev_s, const int64_t* id_s,
-                          const double* acc, const double* drho, float4* posp, float4* velr,
+                          const void* acc, const void* drho, float4* posp, float4* velr,
                           float4* prev, int64_t* id, uint32_t* keys_next, sphb_ctrl_t* ctrl,
                           cudaStream_t s) {
   if (p.verlet_stride < 1) return sphb_set_error(SPHB_E_INVALID, "verlet_corrector_stride must be >= 1");
@@ -294,18 +311,20 @@ int launch_integrate_mode(sphb_workspace* ws, const sphb_params_t& p, const sphb
     if (blocks > 148 * 16) blocks = 148 * 16;
     const int cb = cellbits_of(g);
     const int64_t nc = ncells_of(g);
-    if (mode == 0)
-      k_integrate<0><<<(unsigned)blocks, 256, 0, s>>>(p, g, cb, nc, n, nb, posp_s, velr_s, prev_s,
-                                                      id_s, acc, drho, posp, velr, prev, id,
-                                                      keys_next, ws->cnt, ctrl);
-    else if (mode == 1)
-      k_integrate<1><<<(unsigned)blocks, 256, 0, s>>>(p, g, cb, nc, n, nb, posp_s, velr_s, prev_s,
-                                                      id_s, acc, drho, posp, velr, prev, id,
-                                                      keys_next, ws->cnt, ctrl);
-    else
-      k_integrate<2><<<(unsigned)blocks, 256, 0, s>>>(p, g, cb, nc, n, nb, posp_s, velr_s, prev_s,
-                                                      id_s, acc, drho, posp, velr, prev, id,
-                                                      keys_next, ws->cnt, ctrl);
+    const double* dr = (const double*)drho;
+    const bool f32 = p.precision == SPHB_FP32;
+#define SPHB_K7(M, F)                                                                              \
+  k_integrate<M, F><<<(unsigned)blocks, 256, 0, s>>>(p, g, cb, nc, n, nb, posp_s, velr_s, prev_s, \
+                                                     id_s, acc, dr, posp, velr, prev, id,         \
+                                                     keys_next, ws->cnt, ctrl)
+    if (mode == 0) {
+      if (f32) SPHB_K7(0, true); else SPHB_K7(0, false);
+    } else if (mode == 1) {
+      if (f32) SPHB_K7(1, true); else SPHB_K7(1, false);
+    } else {
+      if (f32) SPHB_K7(2, true); else SPHB_K7(2, false);
+    }
+#undef SPHB_K7
     if (int rc = sphb_check_launch("k_integrate")) return rc;
   }
   if (mode == 1) {
@@ -317,7 +336,7 @@ int launch_integrate_mode(sphb_workspace* ws, const sphb_params_t& p, const sphb
 
 int launch_integrate(sphb_workspace* ws, const sphb_params_t& p, const sphb_grid_t& g, int64_t n,
                      int64_t nb, const float4* posp_s, const float4* velr_s, const float4* prev_s,
-                     const int64_t* id_s, const double* acc, const double* drho, float4* posp,
+                     const int64_t* id_s, const void* acc, const void* drho, float4* posp,
                      float4* velr, float4* prev, int64_t* id, uint32_t* keys_next,
                      sphb_ctrl_t* ctrl, cudaStream_t s) {
   return launch_integrate_mode(ws, p, g, n, nb, 0, posp_s, velr_s, prev_s, id_s, acc, drho, posp,

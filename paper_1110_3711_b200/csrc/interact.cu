@@ -90,9 +90,13 @@ struct KArgs {
   const int32_t* __restrict__ beg;
   const int32_t* __restrict__ end;
   const int4* __restrict__ blocks;  // (fluid i0, i1, boundary i0, i1) per block
+  // force outputs: FP64 = the ForceOutput layout (acc (n,3), drho (n), visc (n) f64);
+  // FP32 = acc4 (ax, ay, az, drho) float4 per particle + visc32 float (include/sphb200.h)
   double* __restrict__ acc;
   double* __restrict__ drho;
   double* __restrict__ visc;
+  float4* __restrict__ acc4;
+  float* __restrict__ visc32;
   sphb_ctrl_t* ctrl;
   // FP32 constants
   float sup2_lo, sup2_hi, tiny, h, invh, k_gc, k_tw, eta2, alpha, massf, massb, k_cs, cs_exp;
@@ -1576,18 +1580,12 @@ __global__ void __launch_bounds__(NW * 32, V8_MINB) k_interact_v8(KArgs a, K32 k
       const double ax = (double)(lo(s[0].axy) * mfac), ay = (double)(hi(s[0].axy) * mfac);
       const double az = (double)((lo(s[0].az) + hi(s[0].az)) * mfac);
       const double dr = (double)(-(lo(s[0].dr) + hi(s[0].dr)) * mfac);
-      const double vd = (double)(s[0].vd * (float)a.p.h);
-      if (isf) {
-        a.acc[3 * (int64_t)i + 0] = ax;
-        a.acc[3 * (int64_t)i + 1] = ay;
-        a.acc[3 * (int64_t)i + 2] = az;
-      } else {
-        a.acc[3 * (int64_t)i + 0] = 0.0;
-        a.acc[3 * (int64_t)i + 1] = 0.0;
-        a.acc[3 * (int64_t)i + 2] = 0.0;
-      }
-      a.drho[i] = dr;
-      a.visc[i] = vd;
+      const float vd32 = s[0].vd * (float)a.p.h;
+      const double vd = (double)vd32;
+      // FP32 layout: 20 B per particle (the values are f32 already; K7 widens them exactly)
+      a.acc4[i] = isf ? make_float4((float)ax, (float)ay, (float)az, (float)dr)
+                      : make_float4(0.f, 0.f, 0.f, (float)dr);
+      a.visc32[i] = vd32;
       if (!(isfinite(ax) && isfinite(ay) && isfinite(az) && isfinite(dr)))
         raise_div(a.ctrl, step, SPHB_DIV_NONFINITE_FORCES, 0);
       if (isf) {
@@ -1714,13 +1712,16 @@ __device__ __forceinline__ double ipow(double q, int k) {
   return r;
 }
 
+template <bool F32>
 __global__ void __launch_bounds__(256) k_wall_force(sphb_params_t p, sphb_grid_t g, int64_t n,
                                                     int64_t nb, int64_t ncells,
                                                     const float4* __restrict__ posp,
                                                     const int32_t* __restrict__ cell,
                                                     const int32_t* __restrict__ beg,
                                                     const int32_t* __restrict__ end,
-                                                    double* __restrict__ acc, sphb_ctrl_t* ctrl) {
+                                                    void* __restrict__ accv, sphb_ctrl_t* ctrl) {
+  double* acc = (double*)accv;
+  float4* acc4 = (float4*)accv;
   if (!step_live(ctrl)) return;
   (void)ncells;
   const int nx = g.dims[0], ny = g.dims[1], nz = g.dims[2], R = g.reach;
@@ -1756,11 +1757,24 @@ __global__ void __launch_bounds__(256) k_wall_force(sphb_params_t p, sphb_grid_t
       }
     }
     if (!hit) continue;
-    const double ax = xadd(acc[3 * i + 0], fx), ay = xadd(acc[3 * i + 1], fy),
-                 az = xadd(acc[3 * i + 2], fz);
-    acc[3 * i + 0] = ax;
-    acc[3 * i + 1] = ay;
-    acc[3 * i + 2] = az;
+    double ax, ay, az;
+    if (F32) {
+      float4 v = acc4[i];
+      v.x = (float)xadd((double)v.x, fx);
+      v.y = (float)xadd((double)v.y, fy);
+      v.z = (float)xadd((double)v.z, fz);
+      acc4[i] = v;
+      ax = v.x;
+      ay = v.y;
+      az = v.z;
+    } else {
+      ax = xadd(acc[3 * i + 0], fx);
+      ay = xadd(acc[3 * i + 1], fy);
+      az = xadd(acc[3 * i + 2], fz);
+      acc[3 * i + 0] = ax;
+      acc[3 * i + 1] = ay;
+      acc[3 * i + 2] = az;
+    }
     const double gx = xadd(ax, p.g[0]), gy = xadd(ay, p.g[1]), gz = xadd(az, p.g[2]);
     double fmag = __dsqrt_rn(xadd(xadd(xmul(gx, gx), xmul(gy, gy)), xmul(gz, gz)));
     fmag = fmag > 1e-30 ? fmag : 1e-30;
@@ -1790,7 +1804,7 @@ int64_t interact_launch_count(int64_t n) {
 int launch_interact(sphb_workspace* ws, const sphb_params_t& p, const sphb_grid_t& g, int64_t n,
                     int64_t nb, const float4* posp, const float4* velr, const float4* aux,
                     const int32_t* cell_sorted, const int32_t* beg, const int32_t* end,
-                    double* acc, double* drho, double* visc, sphb_ctrl_t* ctrl, cudaStream_t s) {
+                    void* acc, void* drho, void* visc, sphb_ctrl_t* ctrl, cudaStream_t s) {
   if (g.reach < 1 || g.reach > 3) return sphb_set_error(SPHB_E_INVALID, "reach must be 1..3");
   static int nsm = 0;
   if (nsm == 0) {
@@ -1810,9 +1824,11 @@ int launch_interact(sphb_workspace* ws, const sphb_params_t& p, const sphb_grid_
   a.cell = cell_sorted;
   a.beg = beg;
   a.end = end;
-  a.acc = acc;
-  a.drho = drho;
-  a.visc = visc;
+  a.acc = (double*)acc;
+  a.drho = (double*)drho;
+  a.visc = (double*)visc;
+  a.acc4 = (float4*)acc;
+  a.visc32 = (float*)visc;
   a.ctrl = ctrl;
   a.sup2_lo = (float)(p.sup2 * (1.0 - 1e-5));
   a.sup2_hi = (float)(p.sup2 * (1.0 + 1e-5));
@@ -1842,8 +1858,11 @@ int launch_interact(sphb_workspace* ws, const sphb_params_t& p, const sphb_grid_
   a.blocks = ws->blocks;
   const int rc = p.precision == SPHB_FP64 ? launch_one<double>(a, nsm, s) : launch_one<float>(a, nsm, s);
   if (rc || !(p.wall_d > 0.0) || n <= nb) return rc;
-  k_wall_force<<<(unsigned)std::min<int64_t>((n - nb + 255) / 256, 148 * 16), 256, 0, s>>>(
-      p, g, n, nb, a.ncells, posp, cell_sorted, beg, end, acc, ctrl);
+  const unsigned wb = (unsigned)std::min<int64_t>((n - nb + 255) / 256, 148 * 16);
+  if (p.precision == SPHB_FP64)
+    k_wall_force<false><<<wb, 256, 0, s>>>(p, g, n, nb, a.ncells, posp, cell_sorted, beg, end, acc, ctrl);
+  else
+    k_wall_force<true><<<wb, 256, 0, s>>>(p, g, n, nb, a.ncells, posp, cell_sorted, beg, end, acc, ctrl);
   return sphb_check_launch("k_wall_force");
 }
 

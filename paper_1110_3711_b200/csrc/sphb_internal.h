@@ -76,7 +76,7 @@ constexpr int PI_LARGE_BLOCK = 384;
   int launch_interact(sphb_workspace* ws, const sphb_params_t& p, const sphb_grid_t& g,       \
                       int64_t n, int64_t nb, const float4* posp, const float4* velr,           \
                       const float4* aux, const int32_t* cell_sorted, const int32_t* beg,       \
-                      const int32_t* end, double* acc, double* drho, double* visc,             \
+                      const int32_t* end, void* acc, void* drho, void* visc,             \
                       sphb_ctrl_t* ctrl, cudaStream_t s);                                      \
   int64_t interact_launch_count(int64_t n);                                                    \
   }
@@ -87,20 +87,20 @@ SPHB_DECLARE_PI(pi384)
 int launch_interact(sphb_workspace* ws, const sphb_params_t& p, const sphb_grid_t& g, int64_t n, int64_t nb,
                     const float4* posp, const float4* velr, const float4* aux,
                     const int32_t* cell_sorted, const int32_t* beg, const int32_t* end,
-                    double* acc, double* drho, double* visc, sphb_ctrl_t* ctrl, cudaStream_t s);
+                    void* acc, void* drho, void* visc, sphb_ctrl_t* ctrl, cudaStream_t s);
 int64_t interact_launch_count(int64_t n);
 
 // integrate.cu
 int launch_step_begin(sphb_ctrl_t* ctrl, cudaStream_t s);
 int launch_integrate(sphb_workspace* ws, const sphb_params_t& p, const sphb_grid_t& g, int64_t n,
                      int64_t nb, const float4* posp_s, const float4* velr_s, const float4* prev_s,
-                     const int64_t* id_s, const double* acc, const double* drho, float4* posp,
+                     const int64_t* id_s, const void* acc, const void* drho, float4* posp,
                      float4* velr, float4* prev, int64_t* id, uint32_t* keys_next,
                      sphb_ctrl_t* ctrl, cudaStream_t s);
 int launch_integrate_mode(sphb_workspace* ws, const sphb_params_t& p, const sphb_grid_t& g,
                           int64_t n, int64_t nb, int mode, const float4* posp_s,
                           const float4* velr_s, const float4* prev_s, const int64_t* id_s,
-                          const double* acc, const double* drho, float4* posp, float4* velr,
+                          const void* acc, const void* drho, float4* posp, float4* velr,
                           float4* prev, int64_t* id, uint32_t* keys_next, sphb_ctrl_t* ctrl,
                           cudaStream_t s);
 int launch_energy(sphb_workspace* ws, const sphb_params_t& p, int64_t n, int64_t nb,

@@ -9,6 +9,8 @@
 //                   and min over all of h / (csound + visc_dt), f64 in the reference's order
 //   k_verlet_soa    verlet_update (sim.py:235-259) on (n, 3) / (n,) f32 arrays, f64 arithmetic
 //                   in numpy's evaluation order (bit-identical)
+//   k_forces_f64    the FP32 force layout (float4 acc + drho, float visc) widened to the
+//                   ForceOutput f64 arrays (config.py:94-103)
 #include "sphb_common.cuh"
 #include "sphb_internal.h"
 
@@ -100,6 +102,21 @@ __global__ void __launch_bounds__(256) k_verlet_soa(int64_t n, int64_t nb, int c
   }
 }
 
+__global__ void __launch_bounds__(256) k_forces_f64(int64_t n, const float4* __restrict__ acc4,
+                                                    const float* __restrict__ visc32,
+                                                    double* __restrict__ acc, double* __restrict__ drho,
+                                                    double* __restrict__ visc) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const float4 a = acc4[i];
+    acc[3 * i + 0] = a.x;
+    acc[3 * i + 1] = a.y;
+    acc[3 * i + 2] = a.z;
+    drho[i] = a.w;
+    visc[i] = visc32[i];
+  }
+}
+
 unsigned grid_of(int64_t work) {
   int64_t b = (work + 255) / 256;
   if (b > 148 * 16) b = 148 * 16;
@@ -146,6 +163,26 @@ int sphb_verlet_soa(const sphb_params_t* prm, int64_t n, int64_t nb, int32_t cor
   k_verlet_soa<<<grid_of(n), 256, 0, (cudaStream_t)s>>>(n, nb, corrector, dt, *prm, pos, vel, rho,
                                                         vel_prev, rho_prev, accel, drho_dt);
   return sphb_check_launch("k_verlet_soa");
+}
+
+int sphb_forces_f64(const sphb_params_t* prm, int64_t n, const void* acc, const void* drho,
+                    const void* visc, double* acc64, double* drho64, double* visc64,
+                    sphb_stream_t s) {
+  if (!prm) return sphb_set_error(SPHB_E_INVALID, "null pointer");
+  if (n < 0) return sphb_set_error(SPHB_E_INVALID, "bad n");
+  if (n == 0) return SPHB_OK;
+  if (!acc || !visc || !acc64 || !drho64 || !visc64 || (prm->precision == SPHB_FP64 && !drho))
+    return sphb_set_error(SPHB_E_INVALID, "null pointer");
+  cudaStream_t cs = (cudaStream_t)s;
+  if (prm->precision == SPHB_FP64) {
+    cudaMemcpyAsync(acc64, acc, 24 * (size_t)n, cudaMemcpyDeviceToDevice, cs);
+    cudaMemcpyAsync(drho64, drho, 8 * (size_t)n, cudaMemcpyDeviceToDevice, cs);
+    cudaMemcpyAsync(visc64, visc, 8 * (size_t)n, cudaMemcpyDeviceToDevice, cs);
+    return sphb_check_launch("forces copy");
+  }
+  k_forces_f64<<<grid_of(n), 256, 0, cs>>>(n, (const float4*)acc, (const float*)visc, acc64,
+                                           drho64, visc64);
+  return sphb_check_launch("k_forces_f64");
 }
 
 }  // extern "C"

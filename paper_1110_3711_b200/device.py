@@ -361,6 +361,19 @@ class DeviceSim:
         idx = np.arange(first, last) % self.rec_cap
         return host[idx]
 
+    def forces(self, n: int | None = None):
+        """The last interaction's ForceOutput arrays as f64 device tensors (acc (n, 3), drho,
+        visc) in the current sorted order; FP32 layout widened by sphb_forces_f64."""
+        n = self.n if n is None else int(n)
+        dev = self.acc.device
+        acc = torch.empty((max(n, 1), 3), dtype=torch.float64, device=dev)
+        drho = torch.empty(max(n, 1), dtype=torch.float64, device=dev)
+        visc = torch.empty(max(n, 1), dtype=torch.float64, device=dev)
+        _lib.check(_lib.lib().sphb_forces_f64(_lib.ref(self.prm), n, _ptr(self.acc), _ptr(self.drho),
+                                              _ptr(self.visc), _ptr(acc), _ptr(drho), _ptr(visc),
+                                              _stream()), "sphb_forces_f64")
+        return acc[:n], drho[:n], visc[:n]
+
     def error(self):
         """None or (step, code, index, particle_id)."""
         c = self.ctrl_host()

@@ -57,6 +57,9 @@ class B200Engine:
                 acc=torch.empty((m, 3), dtype=torch.float64, device=dev),
                 drho=torch.empty(m, dtype=torch.float64, device=dev),
                 visc=torch.empty(m, dtype=torch.float64, device=dev),
+                acc64=torch.empty((m, 3), dtype=torch.float64, device=dev),
+                drho64=torch.empty(m, dtype=torch.float64, device=dev),
+                visc64=torch.empty(m, dtype=torch.float64, device=dev),
                 out=torch.empty((m, 5), dtype=torch.float64, pin_memory=True),
             )
             self._ws = Workspace(n, ncells)
@@ -121,9 +124,14 @@ class B200Engine:
         e1.record()
         out = b["out"]
         if n:
-            out[:n, :3].copy_(b["acc"][:n], non_blocking=True)
-            out[:n, 3].copy_(b["drho"][:n], non_blocking=True)
-            out[:n, 4].copy_(b["visc"][:n], non_blocking=True)
+            # the kernel's force layout (FP32: float4 + float, include/sphb200.h) widened to the
+            # ForceOutput f64 arrays (exact)
+            _lib.check(L.sphb_forces_f64(_lib.ref(prm), n, _ptr(b["acc"]), _ptr(b["drho"]),
+                                         _ptr(b["visc"]), _ptr(b["acc64"]), _ptr(b["drho64"]),
+                                         _ptr(b["visc64"]), s), "sphb_forces_f64")
+            out[:n, :3].copy_(b["acc64"][:n], non_blocking=True)
+            out[:n, 3].copy_(b["drho64"][:n], non_blocking=True)
+            out[:n, 4].copy_(b["visc64"][:n], non_blocking=True)
         c = read_ctrl(ctrl)  # synchronises
         self.last_kernel_ms = e0.elapsed_time(e1)
         o = out[:n].numpy()

@@ -215,7 +215,7 @@ def test_wave_tank_piston_follows_law():
 @pytest.mark.parametrize("frame", ["frame_small_n1.npz", "frame_c1mid_n1.npz"])
 def test_boundary_force_matches_restatement(frame):
     """accel(with) - accel(without) == oracle.wall_accel (f64 restatement); boundary rows
-    stay 0, counters and drho/visc are untouched; FP32 adds the same f64 term."""
+    stay 0, counters and drho/visc are untouched; FP32 adds the same term within 1e-5."""
     import types
     z = golden(frame)
     p0 = oracle.params_from_npz(z)
@@ -241,7 +241,10 @@ def test_boundary_force_matches_restatement(frame):
         assert np.array_equal(a.drho_dt, b.drho_dt) and np.array_equal(a.visc_dt, b.visc_dt)
         assert (a.stats.true_pairs, a.stats.force_evals) == (b.stats.true_pairs, b.stats.force_evals)
         scale = max(np.abs(ref).max(), np.abs(a.accel).max())
-        assert np.abs((b.accel - a.accel) - ref).max() <= 1e-12 * scale, precision
+        # FP64: the f64 term added exactly; FP32: accelerations are stored as f32 (the FP32
+        # force layout), so the sum is rounded -- the FP32 contract's 1e-5 bar
+        tol = 1e-12 if precision == "fp64" else 1e-5
+        assert np.abs((b.accel - a.accel) - ref).max() <= tol * scale, precision
 
 
 def test_boundary_force_keeps_fluid_off_the_floor():

@@ -509,8 +509,8 @@ def test_pi_block_matches_128(name, block):
         ra, rb = a.records(step, step + 1), b.records(step, step + 1)
         for f in ("candidate_pairs", "hits_ordered", "force_evals", "ff_force_evals"):
             assert int(ra[f][0]) == int(rb[f][0]), f
-        for x, y in ((a.acc, b.acc), (a.drho, b.drho), (a.visc, b.visc)):
-            assert oracle.rel_linf(x[:a.n].cpu().numpy(), y[:b.n].cpu().numpy()) <= FP32_TOL
+        for x, y in zip(a.forces(), b.forces()):
+            assert oracle.rel_linf(x.cpu().numpy(), y.cpu().numpy()) <= FP32_TOL
         assert abs(float(ra["dt"][0]) / float(rb["dt"][0]) - 1.0) <= 1e-6
     assert 0.0 < b.pi_lane_use() <= 1.0 and int(b.ctrl_host()["nblk"][0]) < int(a.ctrl_host()["nblk"][0])
 
