@@ -53,6 +53,8 @@ def parse():
                     help="replay the timed steps as one CUDA graph (auto: below 2M particles)")
     ap.add_argument("--pi-block", default="auto", choices=["auto", "128", "256", "384"],
                     help="targets per interaction block (auto: sim.initial_pi_block)")
+    ap.add_argument("--pi-kernel", default="gather", choices=["gather", "symmetric"],
+                    help="FP32 interaction kernel: one-sided gather or symmetric pair evaluation")
     ap.add_argument("--e2e-chunks", type=int, default=8,
                     help="row chunks of the pipelined H2D/D2H state round trip (1 = serial)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -569,6 +571,8 @@ def main():
         sim.set_pi_block(initial_pi_block(sim.n, args.n_subdiv))
     elif args.pi_block != "auto":
         sim.set_pi_block(int(args.pi_block))
+    if args.pi_kernel == "symmetric" and prec == _lib.SPHB_FP32:
+        sim.set_pi_kernel("symmetric")
     for _ in range(args.warmup):
         sim.launch_step()
     torch.cuda.synchronize()
@@ -718,7 +722,8 @@ def main():
         "scaling": "weak" if world > 1 else "weak", "vs_baseline": None, "dtype": args.precision,
         "data": "synthetic: reference dam-break lattice (Scenario/build_dam_break), hydrostatic rho",
         "config": workload_config(cfg_name, sc, system, args.n_subdiv, world),
-        "build": {"pi_block": sim.pi_block, "pi_lane_use": round(sim.pi_lane_use(), 4),
+        "build": {"pi_block": sim.pi_block, "pi_kernel": sim.pi_kernel,
+                  "pi_lane_use": round(sim.pi_lane_use(), 4),
                   "cuda_graph": use_graph},
         "interactions_per_s": true_pairs * world * args.steps / (total_ms * 1e-3),
         "pair_evals_per_s": evals * world * args.steps / (total_ms * 1e-3),

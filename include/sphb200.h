@@ -85,7 +85,11 @@ typedef struct {
                                     are that kernel's normalisation and 1/W(dp) */
   int32_t integrator;            /* SPHB_INT_VERLET (reference, sim.py:235-259) |
                                     SPHB_INT_SYMPLECTIC (two-stage position-Verlet) */
-  int32_t pad_;
+  int32_t counters;              /* SPHB_COUNTERS_GATHER: the gather traversal's StepStats
+                                    (gather.py:103-109, cellpairs asymmetric);
+                                    SPHB_COUNTERS_SYMMETRIC: run_cells_symmetric's (kernels.py:
+                                    121-175, cellpairs.py:92-99): half-stencil candidates,
+                                    force_evals = unordered pairs, ff unordered */
   int64_t piston_id0, piston_id1; /* boundary particles with id in [id0, id1) follow the
                                      piston x(t) = x0 + S/2 (1 - cos 2 pi t/T); id0 == id1: none */
   double piston_x0, piston_stroke, piston_period;
@@ -98,6 +102,8 @@ typedef struct {
 
 enum { SPHB_KERNEL_CUBIC = 0, SPHB_KERNEL_WENDLAND = 1 };
 enum { SPHB_INT_VERLET = 0, SPHB_INT_SYMPLECTIC = 1 };
+enum { SPHB_COUNTERS_GATHER = 0, SPHB_COUNTERS_SYMMETRIC = 1 };
+enum { SPHB_PI_GATHER = 0, SPHB_PI_SYMMETRIC = 1 };
 
 /* Device-resident control block (one per simulation, caller allocates 256 B). */
 typedef struct {
@@ -146,6 +152,17 @@ int sphb_workspace_set_mover_cap(sphb_workspace_t* ws, int64_t cap);
  * particle counts, e.g. after a dam collapses).
  * Results agree within the FP32 tolerance (accumulation order); FP64 always uses 128. */
 int sphb_workspace_set_pi_block(sphb_workspace_t* ws, int32_t targets);
+/* The FP32 interaction kernel (FP64 always runs the gather kernel):
+ *   SPHB_PI_GATHER     one-sided gather (each ordered pair evaluated by its target, the
+ *                      reference's GPU strategy, gather.py:1-10; K6 dt in its epilogue);
+ *   SPHB_PI_SYMMETRIC  symmetric pair evaluation (K5s): each unordered pair once over the
+ *                      forward half stencil (run_cells_symmetric, kernels.py:121-175), the
+ *                      reaction scattered to the partner (eval_scatter, kernels.py:29-68) through
+ *                      shared-memory rows flushed with vector reductions; 384-target blocks,
+ *                      cell order (order 0) only; dt after the scatter (one extra pass).
+ * Hit sets and counters are identical; forces agree within the FP32 tolerance (summation
+ * order).  Counters follow prm->counters either way. */
+int sphb_workspace_set_pi_kernel(sphb_workspace_t* ws, int32_t kernel);
 /* The last sphb_step sort's path (0 movers-only, 1 radix) and mover count (synchronising
  * read, diagnostics only). */
 int sphb_workspace_sort_info(const sphb_workspace_t* ws, int64_t* movers, int32_t* mode);

@@ -17,6 +17,8 @@ CSRC = os.path.join(HERE, "csrc")
 
 SPHB_OK, SPHB_E_INVALID, SPHB_E_CUDA, SPHB_E_CAPACITY = 0, -1, -2, -3
 SPHB_DIV_LEFT_DOMAIN, SPHB_DIV_NONFINITE_FORCES, SPHB_DIV_NONFINITE_STATE = 1, 2, 3
+SPHB_COUNTERS_GATHER, SPHB_COUNTERS_SYMMETRIC = 0, 1
+SPHB_PI_GATHER, SPHB_PI_SYMMETRIC = 0, 1
 SPHB_FP32, SPHB_FP64 = 0, 1
 SPHB_KERNEL_CUBIC, SPHB_KERNEL_WENDLAND = 0, 1
 SPHB_INT_VERLET, SPHB_INT_SYMPLECTIC = 0, 1
@@ -34,7 +36,7 @@ class ParamsDesc(ctypes.Structure):
                                      "rho0", "gamma", "mass_fluid", "mass_boundary", "tait_b")] + \
                [("g", c_f64 * 3), ("cfl", c_f64), ("dt_min", c_f64), ("dt_max", c_f64),
                 ("verlet_stride", c_i32), ("order", c_i32), ("precision", c_i32),
-                ("kernel", c_i32), ("integrator", c_i32), ("pad_", c_i32),
+                ("kernel", c_i32), ("integrator", c_i32), ("counters", c_i32),
                 ("piston_id0", c_i64), ("piston_id1", c_i64), ("piston_x0", c_f64),
                 ("piston_stroke", c_f64), ("piston_period", c_f64),
                 ("wall_d", c_f64), ("wall_r0", c_f64), ("wall_p1", c_i32), ("wall_p2", c_i32)]
@@ -96,6 +98,7 @@ def lib():
         "sphb_workspace_set_mover_cap": ([P, c_i64], c_i32),
         "sphb_workspace_sort_info": ([P, P, P], c_i32),
         "sphb_workspace_set_pi_block": ([P, c_i32], c_i32),
+        "sphb_workspace_set_pi_kernel": ([P, c_i32], c_i32),
         "sphb_ctrl_init": ([P, c_i64, c_f64, P], c_i32),
         "sphb_cell_keys": ([P, P, P, c_i64, c_i64, P, P, P, P], c_i32),
         "sphb_sort": ([P, P, P, c_i64, P, P, P, P], c_i32),
@@ -136,7 +139,7 @@ def lib():
 
 EXPORTED = ("sphb_last_error", "sphb_version", "sphb_workspace_create", "sphb_workspace_destroy",
             "sphb_workspace_reset", "sphb_workspace_bytes",
-            "sphb_workspace_set_mover_cap", "sphb_workspace_sort_info", "sphb_workspace_set_pi_block", "sphb_ctrl_init", "sphb_cell_keys",
+            "sphb_workspace_set_mover_cap", "sphb_workspace_sort_info", "sphb_workspace_set_pi_block", "sphb_workspace_set_pi_kernel", "sphb_ctrl_init", "sphb_cell_keys",
             "sphb_sort", "sphb_sort_ranges", "sphb_nl_build", "sphb_reorder", "sphb_cell_ranges",
             "sphb_cell_ranges_from_sorted", "sphb_cell_hist",
             "sphb_interact", "sphb_step_begin", "sphb_integrate", "sphb_step_end", "sphb_step",

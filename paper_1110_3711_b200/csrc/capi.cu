@@ -67,6 +67,8 @@ static int check_params(const sphb_params_t* p) {
   if (p->precision != SPHB_FP32 && p->precision != SPHB_FP64)
     return sphb_set_error(SPHB_E_INVALID, "precision must be SPHB_FP32 or SPHB_FP64");
   if (!(p->wall_d >= 0.0)) return sphb_set_error(SPHB_E_INVALID, "wall_d must be >= 0");
+  if (p->counters != SPHB_COUNTERS_GATHER && p->counters != SPHB_COUNTERS_SYMMETRIC)
+    return sphb_set_error(SPHB_E_INVALID, "counters must be SPHB_COUNTERS_GATHER or SPHB_COUNTERS_SYMMETRIC");
   if (p->wall_d > 0.0) {
     if (!(p->wall_r0 > 0.0 && p->wall_r0 <= 2.0 * p->h))
       return sphb_set_error(SPHB_E_INVALID, "wall_r0 must lie in (0, 2h]");
@@ -80,14 +82,22 @@ int launch_interact(sphb_workspace* ws, const sphb_params_t& p, const sphb_grid_
                     int64_t nb, const float4* posp, const float4* velr, const float4* aux,
                     const int32_t* cell_sorted, const int32_t* beg, const int32_t* end,
                     void* acc, void* drho, void* visc, sphb_ctrl_t* ctrl, cudaStream_t s) {
-  if (ws->pi_block == 256 && p.precision == SPHB_FP32)
-    return pi256::launch_interact(ws, p, g, n, nb, posp, velr, aux, cell_sorted, beg, end, acc,
-                                  drho, visc, ctrl, s);
-  if (ws->pi_block == PI_LARGE_BLOCK && p.precision == SPHB_FP32)
-    return pi384::launch_interact(ws, p, g, n, nb, posp, velr, aux, cell_sorted, beg, end, acc,
-                                  drho, visc, ctrl, s);
-  return pi128::launch_interact(ws, p, g, n, nb, posp, velr, aux, cell_sorted, beg, end, acc, drho,
+  int rc;
+  const bool f32 = p.precision == SPHB_FP32;
+  if (ws->pi_kernel == SPHB_PI_SYMMETRIC && f32 && p.order == 0)
+    rc = pi384s::launch_interact(ws, p, g, n, nb, posp, velr, aux, cell_sorted, beg, end, acc, drho,
+                                 visc, ctrl, s);
+  else if (ws->pi_block == 256 && f32)
+    rc = pi256::launch_interact(ws, p, g, n, nb, posp, velr, aux, cell_sorted, beg, end, acc, drho,
                                 visc, ctrl, s);
+  else if (ws->pi_block == PI_LARGE_BLOCK && f32)
+    rc = pi384::launch_interact(ws, p, g, n, nb, posp, velr, aux, cell_sorted, beg, end, acc, drho,
+                                visc, ctrl, s);
+  else
+    rc = pi128::launch_interact(ws, p, g, n, nb, posp, velr, aux, cell_sorted, beg, end, acc, drho,
+                                visc, ctrl, s);
+  if (rc || p.counters != SPHB_COUNTERS_SYMMETRIC) return rc;
+  return launch_sym_counters(ws, g, beg, end, ctrl, s);
 }
 
 int64_t interact_launch_count(int64_t n) { return pi128::interact_launch_count(n); }
@@ -128,6 +138,8 @@ int sphb_workspace_create(int64_t n_max, int64_t ncells_max, sphb_workspace_t** 
   ws->max_blocks = n1 + n1 / 64 + 16;
   if (e == cudaSuccess) e = alloc((void**)&ws->blocks, 2 * sizeof(int4) * ws->max_blocks);
   if (e == cudaSuccess) e = alloc((void**)&ws->energy_part, sizeof(double) * 5 * 592);
+  if (e == cudaSuccess) e = alloc((void**)&ws->sym_scratch, sizeof(unsigned long long));
+  if (e == cudaSuccess) e = cudaMemset(ws->sym_scratch, 0, sizeof(unsigned long long));
   {
     const int64_t words = (n1 + MV_TILE_ROWS - 1) / MV_TILE_ROWS * (MV_TILE_ROWS / 32);
     ws->mover_cap_max = n1 < MOVER_CAP_MAX ? n1 : MOVER_CAP_MAX;
@@ -158,6 +170,7 @@ int sphb_workspace_create(int64_t n_max, int64_t ncells_max, sphb_workspace_t** 
 int sphb_workspace_destroy(sphb_workspace_t* ws) {
   if (!ws) return SPHB_OK;
   cudaFree(ws->cnt);
+  cudaFree(ws->sym_scratch);
   for (int k = 0; k < 2; ++k) {
     cudaFree(ws->keys_tmp[k]);
     cudaFree(ws->vals_tmp[k]);
@@ -197,6 +210,14 @@ int sphb_workspace_set_pi_block(sphb_workspace_t* ws, int32_t targets) {
     return sphb_set_error(SPHB_E_INVALID, "interaction block must be 128, 256 or %d targets",
                           PI_LARGE_BLOCK);
   ws->pi_block = targets;
+  return SPHB_OK;
+}
+
+int sphb_workspace_set_pi_kernel(sphb_workspace_t* ws, int32_t kernel) {
+  SPHB_NONNULL(ws);
+  if (kernel != SPHB_PI_GATHER && kernel != SPHB_PI_SYMMETRIC)
+    return sphb_set_error(SPHB_E_INVALID, "interaction kernel must be SPHB_PI_GATHER or SPHB_PI_SYMMETRIC");
+  ws->pi_kernel = kernel;
   return SPHB_OK;
 }
 

@@ -957,7 +957,7 @@ struct Own32 {
 };
 
 struct Acc32 {
-  f2_t axy, az, dr, hits;
+  f2_t axy, az, dr, hits, hitsf;  // hitsf: hits on fluid candidates (symmetric build only)
   float vd;
 };
 
@@ -970,7 +970,15 @@ constexpr int V8_ROWS = V8_SCAP + 8;  // staged rows: SCAP candidates + the dumm
 constexpr int V8_REC_OFF = 32 * V8_ROWS;
 constexpr int V8_ZERO_OFF = V8_REC_OFF + 8 * V8_SCAP;
 constexpr int V8_FIFO_OFF = V8_ZERO_OFF + 64;
-constexpr int V8_SMEM = V8_FIFO_OFF + 8 * NW * V8_RING * 32;
+// symmetric build (K5s, SPHB_SYM): per staged row the reactions it receives from this block's
+// targets, float4 (ax, ay, az, drho) + u32 (visc bits), flushed to global memory per batch
+#ifndef SPHB_SYM
+#define SPHB_SYM 0
+#endif
+constexpr bool V8_SYM = SPHB_SYM != 0;
+constexpr int V8_ACC_OFF = V8_FIFO_OFF + 8 * NW * V8_RING * 32;
+constexpr int V8_VD_OFF = V8_ACC_OFF + (V8_SYM ? 16 * V8_ROWS : 0);
+constexpr int V8_SMEM = V8_VD_OFF + (V8_SYM ? 4 * V8_ROWS : 0);
 // tensor-core screen: D = |x_j|^2 - 2 x_i.x_j + (|x_i|^2 - thr) in units of (2h)^2 from FP16
 // block-centred coordinates (|x| <= 4, |x|^2 < 32): coordinate rounding moves r^2 by <= 6.8e-3
 // at the cutoff and the FP16 |x_j|^2 by <= 7.8e-3, so thr = 1.02 never drops a true hit
@@ -1005,10 +1013,34 @@ struct Geo2 {
   f2_t a1xy, a1zw, b1zw, a2xy, a2zw, b2zw, dxy1, dxy2, dz, r2, dot;
 };
 
+// Symmetric build: where a pair's reaction goes.  The staged row's accumulators (float4 +
+// u32) receive -ratio * (i-side force term), ratio * (i-side drho term) and |mu|, ratio =
+// m_i / m_j (1 with equal masses: the masses are applied once, at the flush).
+struct SymCtx {
+  uint32_t smA, acc, vd;   // shared addresses: staged A rows, reaction rows, visc rows
+  float ratio_f, ratio_b;  // m_i / m_j for a fluid / boundary candidate
+};
+
+__device__ __forceinline__ void sym_react(const SymCtx& y, uint32_t ad, float fx, float fy,
+                                          float fz, float dr, float mu) {
+  const bool jb = ad & 1u;  // boundary candidate: drho and visc only (accel stays 0)
+  const uint32_t row = ((ad & ~1u) - y.smA) >> 4;
+  const float r = jb ? y.ratio_b : y.ratio_f;
+  float* acc = reinterpret_cast<float*>(__cvta_shared_to_generic(y.acc + 16u * row));
+  if (!jb) {
+    atomicAdd(acc + 0, -r * fx);
+    atomicAdd(acc + 1, -r * fy);
+    atomicAdd(acc + 2, -r * fz);
+  }
+  atomicAdd(acc + 3, r * dr);
+  atomicMax(reinterpret_cast<unsigned*>(__cvta_shared_to_generic(y.vd + 4u * row)),
+            __float_as_uint(mu));
+}
+
 template <bool G7, bool EQM, bool WEND, int NG>
 __device__ __forceinline__ void eval_v8(const KArgs& a, const K32& c, const Own32& o,
                                         const uint32_t (&ad)[2 * NG], int xlo, int xhi,
-                                        Acc32 (&s)[NG]) {
+                                        Acc32 (&s)[NG], const SymCtx& sy) {
   constexpr uint32_t OFFB = 16u * V8_ROWS;  // A -> B rows
   Geo2 g[NG];
   // the sure-hit mask and the clamped r2 live in float registers across the (rare) exact
@@ -1019,7 +1051,8 @@ __device__ __forceinline__ void eval_v8(const KArgs& a, const K32& c, const Own3
   for (int k = 0; k < NG; ++k) {
     f2_t b1xy, b2xy;
     // non-EQM: bit 0 of a popped address flags a boundary-list candidate (its mass)
-    const uint32_t p1 = EQM ? ad[2 * k] : (ad[2 * k] & ~1u), p2 = EQM ? ad[2 * k + 1] : (ad[2 * k + 1] & ~1u);
+    const uint32_t p1 = (EQM && !V8_SYM) ? ad[2 * k] : (ad[2 * k] & ~1u),
+                   p2 = (EQM && !V8_SYM) ? ad[2 * k + 1] : (ad[2 * k + 1] & ~1u);
     lds_2x64(p1, g[k].a1xy, g[k].a1zw);
     lds_2x64(p2, g[k].a2xy, g[k].a2zw);
     lds_2x64(p1 + OFFB, b1xy, g[k].b1zw);
@@ -1134,6 +1167,18 @@ __device__ __forceinline__ void eval_v8(const KArgs& a, const K32& c, const Own3
     s[k].dr = fma2(GCN, g[k].dot, s[k].dr);
     s[k].vd = fmaxf(s[k].vd, fmaxf(fabsf(lo(MU)), fabsf(hi(MU))));
     s[k].hits = add2(s[k].hits, OK);
+    if (V8_SYM) {
+      // ff hits: fluid candidates (the target side is applied at the epilogue)
+      s[k].hitsf = add2(s[k].hitsf, mul2(OK, pk((ad[2 * k] & 1u) ? 0.0f : 1.0f,
+                                                  (ad[2 * k + 1] & 1u) ? 0.0f : 1.0f)));
+      const f2_t DR = mul2(GCN, g[k].dot);
+      if (okf[2 * k] != 0.0f)
+        sym_react(sy, ad[2 * k], lo(g[k].dxy1) * lo(FM), hi(g[k].dxy1) * lo(FM), lo(g[k].dz) * lo(FM),
+                  lo(DR), fabsf(lo(MU)));
+      if (okf[2 * k + 1] != 0.0f)
+        sym_react(sy, ad[2 * k + 1], lo(g[k].dxy2) * hi(FM), hi(g[k].dxy2) * hi(FM),
+                  hi(g[k].dz) * hi(FM), hi(DR), fabsf(hi(MU)));
+    }
   }
 }
 
@@ -1170,6 +1215,8 @@ __global__ void __launch_bounds__(NW * 32, V8_MINB) k_interact_v8(KArgs a, K32 k
   const uint32_t smR = smA + V8_REC_OFF;  // screen records: half2 (x, y), half2 (z, |x|^2)
   const uint32_t dummy = smA + 16u * SCAP;
   if (tid < 16) g_sm32[V8_ZERO_OFF / 4 + tid] = 0u;
+  if (V8_SYM)  // reaction rows start at zero; every flush re-zeroes the rows it drained
+    for (int r = tid; r < 5 * V8_ROWS; r += NW * 32) g_sm32[V8_ACC_OFF / 4 + r] = 0u;
   // tensor-core screen lane roles: g = lane / 4 (fragment row / column), t = lane % 4
   const int fg = lane >> 2, ft = lane & 3;
   // B fragment (K rows 2t, 2t+1; column g of N-tile n <-> candidate 8 (g/2) + 2n + g%2):
@@ -1221,7 +1268,11 @@ __global__ void __launch_bounds__(NW * 32, V8_MINB) k_interact_v8(KArgs a, K32 k
     const int rowkey = bm.x;
     const int cxa = bm.y, cxb = bm.z;
     const int nlist = nf ? 2 : 1;
-    const int nseg = nlist * side * side;
+    // symmetric build: the own row (forward cells only, j > i per target) and the forward rows
+    // (dz = 0, dy = 1..r; dz = 1..r, dy = -r..r): every unordered pair once, as
+    // run_cells_symmetric / forward_offsets (kernels.py:121-175, grid.py:147-156)
+    const int nrow = V8_SYM ? 1 + reach + reach * side : side * side;
+    const int nseg = nlist * nrow;
     const int gcz = rowkey / ny, gcy = rowkey - gcz * ny;
     const int bxlo = max(cxa - reach, 0), bxhi = min(cxb + reach, nx - 1);
     const double cs = a.g.cell_size;
@@ -1235,7 +1286,7 @@ __global__ void __launch_bounds__(NW * 32, V8_MINB) k_interact_v8(KArgs a, K32 k
                        xext * xext + 2.0 * yzext * yzext < 30.0;
     // the fluid targets' own row (fluid list, dy = dz = 0)
     const int rr_c = reach * side + reach;
-    const int selfseg = nf ? ((nlist == 2 && a.p.order == 1) ? rr_c : rr_c * nlist) : -1;
+    const int selfseg = (nf && !V8_SYM) ? ((nlist == 2 && a.p.order == 1) ? rr_c : rr_c * nlist) : -1;
 
     if (tid < MAXSEG) {
       int len = 0;
@@ -1249,11 +1300,17 @@ __global__ void __launch_bounds__(NW * 32, V8_MINB) k_interact_v8(KArgs a, K32 k
           li = tid % nlist;
           rr = tid / nlist;
         }
-        const int dz = rr / side - reach, dy = rr % side - reach;
+        int dz = rr / side - reach, dy = rr % side - reach, sxlo = bxlo;
+        if (V8_SYM) {
+          const int q = rr - 1 - reach;
+          dz = rr == 0 ? 0 : (q < 0 ? 0 : 1 + q / side);
+          dy = rr == 0 ? 0 : (q < 0 ? rr : q % side - reach);
+          sxlo = rr == 0 ? cxa : bxlo;
+        }
         const int zz = gcz + dz, yy = gcy + dy;
         if (zz >= 0 && zz < nz && yy >= 0 && yy < ny) {
           const int64_t rowoff = (li == 0 ? a.ncells : 0) + (int64_t)nx * (yy + (int64_t)ny * zz);
-          sg.g0 = a.beg[rowoff + bxlo];
+          sg.g0 = a.beg[rowoff + sxlo];
           sg.g1 = a.end[rowoff + bxhi];
           sg.rowoff = (int)rowoff;
           len = max(sg.g1 - sg.g0, 0);
@@ -1295,7 +1352,7 @@ __global__ void __launch_bounds__(NW * 32, V8_MINB) k_interact_v8(KArgs a, K32 k
     const bool wactive = warp * 32 < nf + nbt;
     Own32 o;
     float ocs = 0.f;
-    int xlo = 0, xhi = -1;
+    int xlo = 0, xhi = -1, cxi = INT_MAX;
     {
       float4 pi = make_float4(0.f, 0.f, 0.f, 0.f), vi = make_float4(0.f, 0.f, 0.f, 1.f),
              xi = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -1303,7 +1360,7 @@ __global__ void __launch_bounds__(NW * 32, V8_MINB) k_interact_v8(KArgs a, K32 k
         pi = a.posp[i];
         vi = a.velr[i];
         xi = a.aux[i];
-        const int cxi = a.cell[i] - rowkey * nx;
+        cxi = a.cell[i] - rowkey * nx;
         xlo = max(cxi - reach, 0);
         xhi = min(cxi + reach, nx - 1);
       }
@@ -1317,14 +1374,47 @@ __global__ void __launch_bounds__(NW * 32, V8_MINB) k_interact_v8(KArgs a, K32 k
     }
     const int wxlo = __reduce_min_sync(SPHB_FULL, valid ? xlo : INT_MAX);
     const int wxhi = __reduce_max_sync(SPHB_FULL, valid ? xhi : INT_MIN);
+    // symmetric build: own-row lower bounds (global indices) -- fluid targets take fluid
+    // candidates j > i and boundary candidates from their own cell on, boundary targets fluid
+    // candidates from the next cell on (kernels.py:144-175); the warp's own-row window starts
+    // at its lowest target cell
+    int lbF = INT_MAX, lbB = INT_MAX;
+    const int wcxlo = V8_SYM ? __reduce_min_sync(SPHB_FULL, valid ? cxi : INT_MAX) : 0;
+    SymCtx sy = {0u, 0u, 0u, 1.0f, 1.0f};
+    if (V8_SYM) {
+      if (valid) {
+        const int64_t rB = (int64_t)rowkey * nx, rF = a.ncells + rB;
+        lbF = isf ? i + 1 : a.end[rF + cxi];
+        lbB = isf ? a.beg[rB + cxi] : INT_MAX;
+      }
+      const float mi = isf ? (float)a.p.mass_fluid : (float)a.p.mass_boundary;
+      sy.smA = smA;
+      sy.acc = smA + V8_ACC_OFF;
+      sy.vd = smA + V8_VD_OFF;
+      sy.ratio_f = EQM ? 1.0f : mi / (float)a.p.mass_fluid;
+      sy.ratio_b = EQM ? 1.0f : mi / (float)a.p.mass_boundary;
+    }
     Acc32 s[V8_NG];
 #pragma unroll
     for (int k = 0; k < V8_NG; ++k) {
-      s[k].axy = s[k].az = s[k].dr = s[k].hits = bc(0.0f);
+      s[k].axy = s[k].az = s[k].dr = s[k].hits = s[k].hitsf = bc(0.0f);
       s[k].vd = 0.0f;
     }
     unsigned long long cand = 0;
-    if (valid) {  // candidate count = sum of this lane's row-range lengths (loads batched by 6)
+    if (valid && V8_SYM) {  // the gather traversal's candidate count (full stencil rows)
+      for (int dz = -reach; dz <= reach; ++dz) {
+        const int zz = gcz + dz;
+        if (zz < 0 || zz >= nz) continue;
+        for (int dy = -reach; dy <= reach; ++dy) {
+          const int yy = gcy + dy;
+          if (yy < 0 || yy >= ny) continue;
+          const int64_t rb = (int64_t)nx * (yy + (int64_t)ny * zz), rf = a.ncells + rb;
+          cand += (unsigned long long)(a.end[rf + xhi] - a.beg[rf + xlo]);
+          if (isf) cand += (unsigned long long)(a.end[rb + xhi] - a.beg[rb + xlo]);
+        }
+      }
+      if (isf) cand -= 1;
+    } else if (valid) {  // candidate count = sum of this lane's row-range lengths (loads batched by 6)
       for (int k0 = 0; k0 < nseg; k0 += 6) {
         int e[6], b[6];
 #pragma unroll
@@ -1415,7 +1505,7 @@ __global__ void __launch_bounds__(NW * 32, V8_MINB) k_interact_v8(KArgs a, K32 k
         uint32_t ad[2 * V8_NG];
 #pragma unroll
         for (int k = 0; k < 2 * V8_NG; ++k) ad[k] = pop();
-        eval_v8<G7, EQM, WEND, V8_NG>(a, k32, o, ad, xlo, xhi, s);
+        eval_v8<G7, EQM, WEND, V8_NG>(a, k32, o, ad, xlo, xhi, s, sy);
       }
       pend = pend > P * K ? pend - P * K : 0u;
       __syncwarp();
@@ -1480,11 +1570,13 @@ __global__ void __launch_bounds__(NW * 32, V8_MINB) k_interact_v8(KArgs a, K32 k
           const int len = sg.g1 - sg.g0;
           return len > 0 && sg.pos < q1 && sg.pos + len > q0;
         };
+        // the warp's lowest cell in row k (symmetric own row: its lowest target cell)
+        auto wlo = [&](int k) { return (V8_SYM && k < nlist) ? max(wcxlo, 0) : wxlo; };
         int kn = 0;
         while (kn < nseg && !live(kn)) ++kn;
         int nb0 = 0, nb1 = 0;
         if (kn < nseg) {
-          nb0 = a.beg[sSeg[kn].rowoff + wxlo];
+          nb0 = a.beg[sSeg[kn].rowoff + wlo(kn)];
           nb1 = a.end[sSeg[kn].rowoff + wxhi];
         }
         while (kn < nseg) {
@@ -1494,7 +1586,7 @@ __global__ void __launch_bounds__(NW * 32, V8_MINB) k_interact_v8(KArgs a, K32 k
           ++kn;
           while (kn < nseg && !live(kn)) ++kn;
           if (kn < nseg) {
-            nb0 = a.beg[sSeg[kn].rowoff + wxlo];
+            nb0 = a.beg[sSeg[kn].rowoff + wlo(kn)];
             nb1 = a.end[sSeg[kn].rowoff + wxhi];
           }
           const int lo_ = max(sg.pos + (wg0 - sg.g0), q0) - q0;
@@ -1505,6 +1597,12 @@ __global__ void __launch_bounds__(NW * 32, V8_MINB) k_interact_v8(KArgs a, K32 k
           const bool selfrow = k == selfseg;
           // own staged position in the self row (fluid targets), else out of range
           const int selfpos = (selfrow && isf) ? sg.pos + (i - sg.g0) - q0 : INT_MIN / 2;
+          // symmetric own row: staged position of the lane's lower bound (batch-relative)
+          int lbpos = INT_MIN / 2;
+          if (V8_SYM && k < nlist) {
+            const int lb = boundary_list ? lbB : lbF;
+            lbpos = lb == INT_MAX ? INT_MAX / 2 : sg.pos + (lb - sg.g0) - q0;
+          }
           for (int k0 = lo_; k0 < hi_; k0 += 32) {
             uint32_t hit;
             if (use16) {
@@ -1549,9 +1647,13 @@ __global__ void __launch_bounds__(NW * 32, V8_MINB) k_interact_v8(KArgs a, K32 k
               const int d = selfpos - k0;
               if ((unsigned)d < 32u) bits &= ~(1u << d);
             }
+            if (V8_SYM) {  // own row: candidates at or above the lane's lower bound only
+              const int d = lbpos - k0;
+              bits = d >= 32 ? 0u : (d > 0 ? bits & ~((1u << d) - 1u) : bits);
+            }
             if (__any_sync(SPHB_FULL, bits != 0u && cnt == (uint32_t)RINGC)) drain(false);
             if (bits) {
-              sts64u(tp, bits, smA + 16u * (uint32_t)k0 + ((!EQM && boundary_list) ? 1u : 0u));
+              sts64u(tp, bits, smA + 16u * (uint32_t)k0 + (((!EQM || V8_SYM) && boundary_list) ? 1u : 0u));
               tp = tp + 256u == rend ? ring : tp + 256u;
               ++cnt;
               pend += __popc(bits);
@@ -1561,6 +1663,32 @@ __global__ void __launch_bounds__(NW * 32, V8_MINB) k_interact_v8(KArgs a, K32 k
         drain(true);
       }
       __syncthreads();
+      if (V8_SYM) {
+        // the batch's reactions -> global memory (one REDG.F32x4 + RED.MAX per touched row, rows
+        // contiguous per stencil row: coalesced), scaled as the targets' own sums below
+        const float mfac = EQM ? (float)a.p.mass_fluid : 1.0f, hq = (float)a.p.h;
+        for (int k = 0; k < nseg; ++k) {
+          const Seg sg = sSeg[k];
+          const int lo_p = max(sg.pos, q0), hi_p = min(sg.pos + (sg.g1 - sg.g0), q1);
+          for (int p = lo_p + tid; p < hi_p; p += NW * 32) {
+            const uint32_t r = (uint32_t)(p - q0);
+            const float4 v = lds4(smA + V8_ACC_OFF + 16u * r);
+            const uint32_t m = lds32(smA + V8_VD_OFF + 4u * r);
+            if (m != 0u || v.w != 0.0f || v.x != 0.0f || v.y != 0.0f || v.z != 0.0f) {
+              const int64_t j = (int64_t)sg.g0 + (p - sg.pos);
+              asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(a.acc4 + j),
+                           "f"(v.x * mfac), "f"(v.y * mfac), "f"(v.z * mfac), "f"(-v.w * mfac)
+                           : "memory");
+              asm volatile("red.global.max.u32 [%0], %1;" ::"l"(a.visc32 + j),
+                           "r"(__float_as_uint(__uint_as_float(m) * hq)) : "memory");
+              asm volatile("st.shared.v4.u32 [%0], {%1, %1, %1, %1};" ::"r"(smA + V8_ACC_OFF + 16u * r),
+                           "r"(0u) : "memory");
+              sts32(smA + V8_VD_OFF + 4u * r, 0u);
+            }
+          }
+        }
+        __syncthreads();
+      }
     }
 
     if (valid) {
@@ -1575,13 +1703,27 @@ __global__ void __launch_bounds__(NW * 32, V8_MINB) k_interact_v8(KArgs a, K32 k
       const int hits = (int)(lo(s[0].hits) + hi(s[0].hits));
       c_cand += cand;
       c_hits += (unsigned long long)hits;
-      c_ff += isf ? hits : -hits;  // ff = F targets' hits - B targets' hits (F-B == B-F)
+      if (V8_SYM) {
+#pragma unroll
+        for (int k = 1; k < V8_NG; ++k) s[0].hitsf = add2(s[0].hitsf, s[k].hitsf);
+        c_ff += isf ? (int)(lo(s[0].hitsf) + hi(s[0].hitsf)) : 0;
+      } else {
+        c_ff += isf ? hits : -hits;  // ff = F targets' hits - B targets' hits (F-B == B-F)
+      }
       const float mfac = EQM ? (float)a.p.mass_fluid : 1.0f;
       const double ax = (double)(lo(s[0].axy) * mfac), ay = (double)(hi(s[0].axy) * mfac);
       const double az = (double)((lo(s[0].az) + hi(s[0].az)) * mfac);
       const double dr = (double)(-(lo(s[0].dr) + hi(s[0].dr)) * mfac);
       const float vd32 = s[0].vd * (float)a.p.h;
       const double vd = (double)vd32;
+      if (V8_SYM) {  // other blocks add this particle's reactions too: atomics, dt after PI
+        asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(a.acc4 + i),
+                     "f"(isf ? (float)ax : 0.f), "f"(isf ? (float)ay : 0.f), "f"(isf ? (float)az : 0.f),
+                     "f"((float)dr) : "memory");
+        asm volatile("red.global.max.u32 [%0], %1;" ::"l"(a.visc32 + i), "r"(__float_as_uint(vd32))
+                     : "memory");
+        continue;
+      }
       // FP32 layout: 20 B per particle (the values are f32 already; K7 widens them exactly)
       a.acc4[i] = isf ? make_float4((float)ax, (float)ay, (float)az, (float)dr)
                       : make_float4(0.f, 0.f, 0.f, (float)dr);
@@ -1603,6 +1745,10 @@ __global__ void __launch_bounds__(NW * 32, V8_MINB) k_interact_v8(KArgs a, K32 k
   c_cand = warp_sum_u64(c_cand);
   c_hits = warp_sum_u64(c_hits);
   unsigned long long ffu = warp_sum_u64((unsigned long long)c_ff);
+  if (V8_SYM) {  // unordered hits -> the gather traversal's ordered counts (each pair twice)
+    c_hits *= 2;
+    ffu *= 2;
+  }
   if (lane == 0) {
     if (dtf_min < INFINITY) atomic_min_pos(&a.ctrl->dtmin_f, dtf_min);
     if (dtcv_min < INFINITY) atomic_min_pos(&a.ctrl->dtmin_cv, dtcv_min);
@@ -1786,6 +1932,39 @@ __global__ void __launch_bounds__(256) k_wall_force(sphb_params_t p, sphb_grid_t
   if ((threadIdx.x & 31) == 0 && dtf_min < INFINITY) atomic_min_pos(&ctrl->dtmin_f, dtf_min);
 }
 
+// Symmetric build: the compute_dt reductions (sim.py:215-232) once every reaction has landed
+// (the gather build does this in its epilogue, K6), on the FP32 force layout: min over fluid of
+// sqrt(h / max(|a + g|, 1e-30)), min over all of h / (csound + visc_dt); non-finite forces
+// flagged as the gather epilogue does (sim.py:328-329).
+__global__ void __launch_bounds__(256) k_dt_f32(sphb_params_t p, int64_t n, int64_t nb,
+                                                const float4* __restrict__ acc4,
+                                                const float* __restrict__ visc32,
+                                                const float4* __restrict__ aux, sphb_ctrl_t* ctrl) {
+  if (!step_live(ctrl)) return;
+  double dtf = INFINITY, dtcv = INFINITY;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const float4 a = acc4[i];
+    const double vd = (double)visc32[i], cs = (double)aux[i].y;
+    if (!(isfinite(a.x) && isfinite(a.y) && isfinite(a.z) && isfinite(a.w)))
+      raise_div(ctrl, ctrl->step, SPHB_DIV_NONFINITE_FORCES, 0);
+    if (i >= nb) {
+      const double fx = xadd((double)a.x, p.g[0]), fy = xadd((double)a.y, p.g[1]),
+                   fz = xadd((double)a.z, p.g[2]);
+      double fmag = __dsqrt_rn(xadd(xadd(xmul(fx, fx), xmul(fy, fy)), xmul(fz, fz)));
+      fmag = fmag > 1e-30 ? fmag : 1e-30;
+      dtf = fmin(dtf, __dsqrt_rn(xdiv(p.h, fmag)));
+    }
+    dtcv = fmin(dtcv, xdiv(p.h, xadd(cs, vd)));
+  }
+  dtf = warp_min(dtf);
+  dtcv = warp_min(dtcv);
+  if ((threadIdx.x & 31) == 0) {
+    if (dtf < INFINITY) atomic_min_pos(&ctrl->dtmin_f, dtf);
+    if (dtcv < INFINITY) atomic_min_pos(&ctrl->dtmin_cv, dtcv);
+  }
+}
+
 }  // namespace
 
 #ifndef SPHB_PI_NS
@@ -1798,7 +1977,19 @@ namespace SPHB_PI_NS {
 
 int64_t interact_launch_count(int64_t n) {
   (void)n;
-  return 2;
+  return V8_SYM ? 3 : 2;  // k_blocks, the interaction kernel (+ k_dt_f32)
+}
+
+static int launch_wall(const sphb_params_t& p, const sphb_grid_t& g, int64_t n, int64_t nb,
+                       int64_t ncells, const float4* posp, const int32_t* cell_sorted,
+                       const int32_t* beg, const int32_t* end, void* acc, sphb_ctrl_t* ctrl,
+                       cudaStream_t s) {
+  const unsigned wb = (unsigned)std::min<int64_t>((n - nb + 255) / 256, 148 * 16);
+  if (p.precision == SPHB_FP64)
+    k_wall_force<false><<<wb, 256, 0, s>>>(p, g, n, nb, ncells, posp, cell_sorted, beg, end, acc, ctrl);
+  else
+    k_wall_force<true><<<wb, 256, 0, s>>>(p, g, n, nb, ncells, posp, cell_sorted, beg, end, acc, ctrl);
+  return sphb_check_launch("k_wall_force");
 }
 
 int launch_interact(sphb_workspace* ws, const sphb_params_t& p, const sphb_grid_t& g, int64_t n,
@@ -1856,14 +2047,17 @@ int launch_interact(sphb_workspace* ws, const sphb_params_t& p, const sphb_grid_
   // one launch for both item classes: fluid targets (F-F + F-B) and boundary targets (B-F,
   // drho + visc only) of the same cells share the staged candidates
   a.blocks = ws->blocks;
-  const int rc = p.precision == SPHB_FP64 ? launch_one<double>(a, nsm, s) : launch_one<float>(a, nsm, s);
-  if (rc || !(p.wall_d > 0.0) || n <= nb) return rc;
-  const unsigned wb = (unsigned)std::min<int64_t>((n - nb + 255) / 256, 148 * 16);
-  if (p.precision == SPHB_FP64)
-    k_wall_force<false><<<wb, 256, 0, s>>>(p, g, n, nb, a.ncells, posp, cell_sorted, beg, end, acc, ctrl);
-  else
-    k_wall_force<true><<<wb, 256, 0, s>>>(p, g, n, nb, a.ncells, posp, cell_sorted, beg, end, acc, ctrl);
-  return sphb_check_launch("k_wall_force");
+  const bool sym = V8_SYM && p.precision == SPHB_FP32;
+  if (sym) {  // every block adds into these (targets' own sums and their partners' reactions)
+    cudaMemsetAsync(acc, 0, sizeof(float4) * (size_t)n, s);
+    cudaMemsetAsync(visc, 0, sizeof(float) * (size_t)n, s);
+  }
+  int rc = p.precision == SPHB_FP64 ? launch_one<double>(a, nsm, s) : launch_one<float>(a, nsm, s);
+  if (!rc && p.wall_d > 0.0 && n > nb) rc = launch_wall(p, g, n, nb, a.ncells, posp, cell_sorted, beg, end, acc, ctrl, s);
+  if (rc || !sym) return rc;
+  k_dt_f32<<<(unsigned)std::min<int64_t>((n + 255) / 256, 148 * 16), 256, 0, s>>>(
+      p, n, nb, a.acc4, a.visc32, aux, ctrl);
+  return sphb_check_launch("k_dt_f32");
 }
 
 }  // namespace SPHB_PI_NS

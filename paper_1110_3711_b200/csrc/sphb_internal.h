@@ -40,6 +40,8 @@ struct sphb_workspace {
   int4* mv_kv = nullptr;       // 2*ncells_max per-key (SB, MB, old begin, chain head)
   int64_t mover_cap_max = 0, mover_cap = 0;
   int32_t pi_block = 128;  // targets per interaction block: 128, 256 or 384 (pi128/256/384)
+  int32_t pi_kernel = 0;   // SPHB_PI_GATHER | SPHB_PI_SYMMETRIC (pi384s)
+  unsigned long long* sym_scratch = nullptr;  // half-stencil candidate count (SPHB_COUNTERS_SYMMETRIC)
   size_t bytes = 0;
 };
 
@@ -83,12 +85,18 @@ constexpr int PI_LARGE_BLOCK = 384;
 SPHB_DECLARE_PI(pi128)
 SPHB_DECLARE_PI(pi256)
 SPHB_DECLARE_PI(pi384)
+SPHB_DECLARE_PI(pi384s)  // the symmetric build (K5s) of the 384-target blocking
 // the workspace's blocking (FP64 always pi128)
 int launch_interact(sphb_workspace* ws, const sphb_params_t& p, const sphb_grid_t& g, int64_t n, int64_t nb,
                     const float4* posp, const float4* velr, const float4* aux,
                     const int32_t* cell_sorted, const int32_t* beg, const int32_t* end,
                     void* acc, void* drho, void* visc, sphb_ctrl_t* ctrl, cudaStream_t s);
 int64_t interact_launch_count(int64_t n);
+
+// stepfn.cu: StepStats of the symmetric traversal (SPHB_COUNTERS_SYMMETRIC) from the gather-type
+// counters of either kernel
+int launch_sym_counters(sphb_workspace* ws, const sphb_grid_t& g, const int32_t* beg,
+                        const int32_t* end, sphb_ctrl_t* ctrl, cudaStream_t s);
 
 // integrate.cu
 int launch_step_begin(sphb_ctrl_t* ctrl, cudaStream_t s);

@@ -9,6 +9,10 @@
 //                   and min over all of h / (csound + visc_dt), f64 in the reference's order
 //   k_verlet_soa    verlet_update (sim.py:235-259) on (n, 3) / (n,) f32 arrays, f64 arithmetic
 //                   in numpy's evaluation order (bit-identical)
+//   k_sym_cand      StepStats of the symmetric traversal (SPHB_COUNTERS_SYMMETRIC): the
+//   k_sym_final     half-stencil candidate count of run_cells_symmetric (kernels.py:121-175)
+//                   per cell from begin/end, force_evals = unordered pairs, ff unordered
+//                   (cellpairs.py:92-99 reports the symmetric counts as they are)
 //   k_forces_f64    the FP32 force layout (float4 acc + drho, float visc) widened to the
 //                   ForceOutput f64 arrays (config.py:94-103)
 #include "sphb_common.cuh"
@@ -117,6 +121,57 @@ __global__ void __launch_bounds__(256) k_forces_f64(int64_t n, const float4* __r
   }
 }
 
+__device__ __forceinline__ bool live(const sphb_ctrl_t* c) {
+  return c->active && c->err >= ((uint64_t)(c->step + 1) << 40);
+}
+
+// per cell c: nf(nf-1)/2 + nf nb + sum over forward cells d of (nf nf_d + nf nb_d + nb nf_d)
+// (scan_block calls of run_cells_symmetric, kernels.py:144-175; forward_offsets grid.py:147-156)
+__global__ void __launch_bounds__(256) k_sym_cand(sphb_grid_t g, const int32_t* __restrict__ beg,
+                                                  const int32_t* __restrict__ end,
+                                                  unsigned long long* out, const sphb_ctrl_t* ctrl) {
+  if (!live(ctrl)) return;
+  const int nx = g.dims[0], ny = g.dims[1], nz = g.dims[2], R = g.reach;
+  const int64_t nc = (int64_t)nx * ny * nz;
+  unsigned long long acc = 0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < nc; c += stride) {
+    const long long nf = end[nc + c] - beg[nc + c], nbc = end[c] - beg[c];
+    if (nf == 0 && nbc == 0) continue;
+    const int cz = (int)(c / ((int64_t)nx * ny)), rem = (int)(c - (int64_t)cz * nx * ny);
+    const int cy = rem / nx, cx = rem - cy * nx;
+    long long t = nf * (nf - 1) / 2 + nf * nbc;
+    for (int dz = 0; dz <= R; ++dz) {
+      const int zz = cz + dz;
+      if (zz >= nz) continue;
+      for (int dy = dz > 0 ? -R : 0; dy <= R; ++dy) {
+        const int yy = cy + dy;
+        if (yy < 0 || yy >= ny) continue;
+        for (int dx = (dz > 0 || dy > 0) ? -R : 1; dx <= R; ++dx) {
+          const int xx = cx + dx;
+          if (xx < 0 || xx >= nx) continue;
+          const int64_t d = xx + (int64_t)nx * (yy + (int64_t)ny * zz);
+          const long long nfd = end[nc + d] - beg[nc + d], nbd = end[d] - beg[d];
+          t += nf * nfd + nf * nbd + nbc * nfd;
+        }
+      }
+    }
+    acc += (unsigned long long)t;
+  }
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0 && acc) atomicAdd(out, acc);
+}
+
+// gather-type counters (ordered hits, evals = ordered hits, ff ordered) -> symmetric ones
+__global__ void k_sym_final(sphb_ctrl_t* ctrl, unsigned long long* cand) {
+  if (live(ctrl)) {
+    ctrl->counters[0] = *cand;
+    ctrl->counters[2] = ctrl->counters[1] / 2;
+    ctrl->counters[3] = ctrl->counters[3] / 2;
+  }
+  *cand = 0;
+}
+
 unsigned grid_of(int64_t work) {
   int64_t b = (work + 255) / 256;
   if (b > 148 * 16) b = 148 * 16;
@@ -124,6 +179,15 @@ unsigned grid_of(int64_t work) {
 }
 
 }  // namespace
+
+int launch_sym_counters(sphb_workspace* ws, const sphb_grid_t& g, const int32_t* beg,
+                        const int32_t* end, sphb_ctrl_t* ctrl, cudaStream_t s) {
+  const int64_t nc = (int64_t)g.dims[0] * g.dims[1] * g.dims[2];
+  k_sym_cand<<<grid_of(nc), 256, 0, s>>>(g, beg, end, ws->sym_scratch, ctrl);
+  if (int rc = sphb_check_launch("k_sym_cand")) return rc;
+  k_sym_final<<<1, 1, 0, s>>>(ctrl, ws->sym_scratch);
+  return sphb_check_launch("k_sym_final");
+}
 
 extern "C" {
 

@@ -69,6 +69,10 @@ class Workspace:
         _lib.check(_lib.lib().sphb_workspace_set_pi_block(self._h, int(targets)),
                    "sphb_workspace_set_pi_block")
 
+    def set_pi_kernel(self, kernel: int):
+        _lib.check(_lib.lib().sphb_workspace_set_pi_kernel(self._h, int(kernel)),
+                   "sphb_workspace_set_pi_kernel")
+
     def sort_info(self) -> tuple[int, int]:
         """(movers, mode) of the last sphb_step sort; mode 0 movers-only, 1 radix."""
         m, mode = ctypes.c_int64(), ctypes.c_int32()
@@ -113,7 +117,8 @@ class DeviceSim:
 
     def __init__(self, system, params, reach: int, order: int = 0, precision: int = _lib.SPHB_FP32,
                  max_steps: int = -1, t_end: float = math.inf, record_capacity: int = 4096,
-                 vel_prev=None, rho_prev=None, device=None, workspace: Workspace | None = None):
+                 vel_prev=None, rho_prev=None, device=None, workspace: Workspace | None = None,
+                 counters: int = 0):
         require_cuda()
         self.device = torch.device(device or f"cuda:{torch.cuda.current_device()}")
         self.params = params
@@ -122,7 +127,8 @@ class DeviceSim:
         self.mass_fluid = float(system.mass_fluid)
         self.mass_boundary = float(system.mass_boundary)
         self.grid = grid_desc(params, reach)
-        self.prm = params_desc(params, self.mass_fluid, self.mass_boundary, order, precision)
+        self.prm = params_desc(params, self.mass_fluid, self.mass_boundary, order, precision,
+                               counters)
         _, dims = grid_dims(params)
         self.ncells = int(np.prod(dims))
         n, dev = self.n, self.device
@@ -151,6 +157,19 @@ class DeviceSim:
         self._graph = None
         self._graph_steps = 0
         self.pi_block = 128
+        self.pi_kernel = "gather"
+
+    def set_pi_kernel(self, kernel: str):
+        """FP32 interaction kernel: "gather" (one-sided, K6 dt in its epilogue) or "symmetric"
+        (each unordered pair once, reactions scattered: sphb_workspace_set_pi_kernel).  Drops a
+        captured graph."""
+        code = {"gather": _lib.SPHB_PI_GATHER, "symmetric": _lib.SPHB_PI_SYMMETRIC}[kernel]
+        self.ws.set_pi_kernel(code)
+        self.pi_kernel = kernel
+        if kernel == "symmetric":  # the symmetric build's blocking (pi384s)
+            self.ws.set_pi_block(384)
+            self.pi_block = 384
+        self._graph = None
 
     def set_pi_block(self, targets: int):
         """Targets per FP32 interaction block: 128 (4-warp CTAs, the default), 256 (8-warp CTAs)
@@ -345,6 +364,8 @@ class DeviceSim:
         sim.ctrl.copy_(torch.as_tensor(c).to(sim.device))
         if "pi_block" in z:  # the interaction blocking in use when the checkpoint was written
             sim.set_pi_block(int(z["pi_block"]))
+        if "pi_kernel" in z and str(z["pi_kernel"]) == "symmetric":
+            sim.set_pi_kernel("symmetric")
         return sim
 
     # ------------------------------------------------------------------ readback

@@ -25,14 +25,19 @@ PRECISION_CODE = {"fp32": _lib.SPHB_FP32, "fp64": _lib.SPHB_FP64}
 class B200Engine:
     """Device gather engine; holds its device buffers across calls (resized on demand)."""
 
-    def __init__(self, config: EngineConfig, pi_block="auto"):
+    def __init__(self, config: EngineConfig, pi_block="auto", pi_kernel="gather"):
         """``pi_block``: targets per FP32 interaction block (128, 256, 384) or "auto", the
         production rule of run_simulation (sim.initial_pi_block of the frame's particle count
-        and n_subdiv), so the engine path runs the same interaction build as the stepper."""
+        and n_subdiv), so the engine path runs the same interaction build as the stepper.
+        ``pi_kernel``: "gather" or "symmetric" (pair evaluation once per unordered pair, the
+        reactions scattered, 384-target blocks; cell-order variants only)."""
         self.config = config.validated()
         if pi_block not in (128, 256, 384, "auto"):
             raise ValueError("pi_block must be 128, 256, 384 or 'auto'")
+        if pi_kernel not in ("gather", "symmetric"):
+            raise ValueError("pi_kernel must be 'gather' or 'symmetric'")
         self.pi_block = pi_block
+        self.pi_kernel = pi_kernel
         self.last_pi_block = None
         self._buf = None
         self._ws = None
@@ -83,7 +88,7 @@ class B200Engine:
         _, dims = grid_dims(params)
         ncells = int(np.prod(dims))
         prm = params_desc(params, system.mass_fluid, system.mass_boundary, cfg.device_order(),
-                          PRECISION_CODE[cfg.precision])
+                          PRECISION_CODE[cfg.precision], cfg.device_counters())
         b = self._buffers(n, ncells)
         if n:
             # pack the caller's frame as K3 lays it out: posp = (pos, prrho), velr = (vel, rho),
@@ -106,7 +111,11 @@ class B200Engine:
             blk = initial_pi_block(n, params.n_subdiv)
         else:
             blk = int(self.pi_block)
+        sym = self.pi_kernel == "symmetric"
+        if sym:
+            blk = 384
         self._ws.set_pi_block(blk)
+        self._ws.set_pi_kernel(_lib.SPHB_PI_SYMMETRIC if sym else _lib.SPHB_PI_GATHER)
         self.last_pi_block = blk
         ctrl = new_ctrl(torch.device("cuda"))
         L, s = _lib.lib(), _stream()
@@ -136,7 +145,7 @@ class B200Engine:
         self.last_kernel_ms = e0.elapsed_time(e1)
         o = out[:n].numpy()
         accel = np.ascontiguousarray(o[:, :3])
-        raw = [int(v) for v in c["counters"]]
+        raw = [int(v) for v in c["counters"]]  # raw[1]: ordered hits (either counter mode)
         stats = StepStats(candidate_pairs=raw[0], true_pairs=raw[1] // 2, force_evals=raw[2],
                           ff_force_evals=raw[3], engine_tag=self.tag,
                           neighbor_bytes=NEIGHBOR_BYTES[cfg.derived_mode])
@@ -144,9 +153,9 @@ class B200Engine:
                            visc_dt=np.ascontiguousarray(o[:, 4]), stats=stats)
 
 
-def make_engine(config: EngineConfig, pi_block="auto") -> B200Engine:
+def make_engine(config: EngineConfig, pi_block="auto", pi_kernel="gather") -> B200Engine:
     """engines/__init__.py:30-34 -- every validated config runs on the B200."""
-    return B200Engine(config.validated(), pi_block=pi_block)
+    return B200Engine(config.validated(), pi_block=pi_block, pi_kernel=pi_kernel)
 
 
 def compute_forces_gather(system, derived, grid, cindex, ranges, params,

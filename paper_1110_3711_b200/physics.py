@@ -53,7 +53,7 @@ def pack_params(params, mass_fluid: float, mass_boundary: float) -> np.ndarray:
 
 
 def params_desc(params, mass_fluid: float, mass_boundary: float, order: int = 0,
-                precision: int = _lib.SPHB_FP32) -> "_lib.ParamsDesc":
+                precision: int = _lib.SPHB_FP32, counters: int = 0) -> "_lib.ParamsDesc":
     d = _lib.ParamsDesc()
     for name, v in zip(PP_NAMES, pack_params(params, mass_fluid, mass_boundary)):
         setattr(d, name, float(v))
@@ -66,6 +66,7 @@ def params_desc(params, mass_fluid: float, mass_boundary: float, order: int = 0,
     d.verlet_stride = int(params.verlet_corrector_stride)
     d.order = int(order)
     d.precision = int(precision)
+    d.counters = int(counters)  # SPHB_COUNTERS_GATHER / _SYMMETRIC (EngineConfig.device_counters)
     d.kernel = _lib.SPHB_KERNEL_WENDLAND if kernel_of(params) == "wendland" else _lib.SPHB_KERNEL_CUBIC
     d.integrator = (_lib.SPHB_INT_SYMPLECTIC if getattr(params, "integrator", "verlet") == "symplectic"
                     else _lib.SPHB_INT_VERLET)

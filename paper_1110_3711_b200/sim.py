@@ -149,6 +149,7 @@ class _Timer:
 def make_device_sim(system, params, cfg: EngineConfig, max_steps=None, t_end=None, **kw) -> DeviceSim:
     return DeviceSim(system, params, reach=cfg.device_reach(params.n_subdiv),
                      order=cfg.device_order(), precision=PRECISION_CODE[cfg.precision],
+                     counters=cfg.device_counters(),
                      max_steps=-1 if max_steps is None else int(max_steps),
                      t_end=math.inf if t_end is None else float(t_end), **kw)
 
@@ -157,7 +158,7 @@ def run_simulation(scenario_or_system, params, config: EngineConfig, max_steps: 
                    t_end: float | None = None, snapshot_every: int = 0, snapshot_sink=None,
                    stats_sink=None, *, chunk: int = 256, stage_timing: bool = True,
                    checkpoint_every: int = 0, checkpoint_path=None, resume_from=None,
-                   pi_block="auto"):
+                   pi_block="auto", pi_kernel="gather"):
     """NL -> PI -> SU loop on the B200.  Returns (system, stats_list) like sim.py:272-352;
     raises DivergenceError on the first out-of-domain particle or non-finite state.
 
@@ -171,7 +172,9 @@ def run_simulation(scenario_or_system, params, config: EngineConfig, max_steps: 
     numbers and the stop rules continue from the checkpoint's step).
 
     ``pi_block``: targets per FP32 interaction block, 128, 256, 384 or "auto" (initial_pi_block of
-    the particle count; recorded in checkpoints so resumed runs keep the same blocking)."""
+    the particle count; recorded in checkpoints so resumed runs keep the same blocking).
+    ``pi_kernel``: "gather" or "symmetric" FP32 interaction (DeviceSim.set_pi_kernel); the
+    symmetric kernel needs the cell traversal order (every config but fastcellshalf)."""
     if max_steps is None and t_end is None:
         raise ValueError("need max_steps or t_end")
     validate(params)
@@ -189,6 +192,7 @@ def run_simulation(scenario_or_system, params, config: EngineConfig, max_steps: 
     if resume_from is not None:
         sim = DeviceSim.from_checkpoint(resume_from, params, reach=cfg.device_reach(params.n_subdiv),
                                         order=cfg.device_order(), precision=PRECISION_CODE[cfg.precision],
+                                        counters=cfg.device_counters(),
                                         max_steps=-1 if max_steps is None else int(max_steps),
                                         t_end=math.inf if t_end is None else float(t_end),
                                         record_capacity=max(chunk, 1))
@@ -202,6 +206,10 @@ def run_simulation(scenario_or_system, params, config: EngineConfig, max_steps: 
     adapt = pi_block == "auto" and cfg.precision == "fp32"
     if resume_from is None and (pi_block != "auto" or adapt):
         sim.set_pi_block(initial_pi_block(sim.n, params.n_subdiv) if adapt else int(pi_block))
+    if pi_kernel not in ("gather", "symmetric"):
+        raise ValueError("pi_kernel must be 'gather' or 'symmetric'")
+    if pi_kernel == "symmetric" and cfg.precision == "fp32" and cfg.device_order() == 0:
+        sim.set_pi_kernel("symmetric")
     stats_out: list[StepStats] = []
     nbytes = NEIGHBOR_BYTES[cfg.derived_mode]
     done_steps = int(sim.ctrl_host()["step"])

@@ -230,7 +230,8 @@ def save_checkpoint(path, sim) -> None:
              mass_fluid=np.float64(sim.mass_fluid), mass_boundary=np.float64(sim.mass_boundary),
              posp=sim.posp[:n].cpu().numpy(), velr=sim.velr[:n].cpu().numpy(),
              prev=sim.prev[:n].cpu().numpy(), id=sim.id[:n].cpu().numpy(), ctrl=ctrl,
-             pi_block=np.int32(getattr(sim, "pi_block", 128)))
+             pi_block=np.int32(getattr(sim, "pi_block", 128)),
+             pi_kernel=np.array(getattr(sim, "pi_kernel", "gather")))
 
 
 def load_checkpoint(path) -> dict:

@@ -196,6 +196,66 @@ def test_interact_fp32_each_blocking_vs_reference(name, variant, block):
             out.stats.ff_force_evals] == list(z[f"{variant}_counters"])
 
 
+CELL_FRAMES = [(f, v) for f, v in FRAMES if v != "fastcellshalf"]
+
+
+@pytest.mark.parametrize("name,variant", CELL_FRAMES)
+def test_symmetric_kernel_vs_reference_gather(name, variant):
+    """The symmetric FP32 kernel (each unordered pair evaluated once, the reaction scattered to
+    the partner) reproduces the reference's gather output: counters bit-exact (the hit set is
+    the same), forces within 1e-5 (summation order only)."""
+    z = golden(name)
+    system, derived, grid, cindex, prm = frame_objects(z)
+    out = sph.make_engine(gather_cfg(variant, "fp32"), pi_kernel="symmetric").compute(
+        system, derived, grid, cindex, prm)
+    nb = system.count_boundary
+    assert np.all(out.accel[:nb] == 0.0)
+    for a, f in ((out.accel, "accel"), (out.drho_dt, "drho"), (out.visc_dt, "visc")):
+        assert oracle.rel_linf(a, z[f"{variant}_{f}"]) <= FP32_TOL, f
+    assert [out.stats.candidate_pairs, out.stats.true_pairs, out.stats.force_evals,
+            out.stats.ff_force_evals] == list(z[f"{variant}_counters"])
+
+
+SYM_FRAMES = ["small_n1", "small_n2", "mid5k_n1", "mid5k_n2", "uniform3k_n1", "c1mid_n1"]
+
+
+@pytest.mark.parametrize("name", SYM_FRAMES)
+@pytest.mark.parametrize("precision,kernel", [("fp32", "symmetric"), ("fp32", "gather"),
+                                              ("fp64", "gather")])
+def test_cellpairs_symmetric_config_vs_reference(name, precision, kernel):
+    """EngineConfig(symmetry=True) -- the reference's CellPairsEngine with run_cells_symmetric --
+    reports the symmetric traversal's StepStats (half-stencil candidates, force_evals = unordered
+    pairs, unordered ff; cellpairs.py:92-99) whichever device kernel runs; forces within 1e-5
+    (FP32) / 1e-12 (FP64: the one-sided sums differ from the symmetric ones in order only) of
+    the reference's own output (tests/golden/make_golden_sym.py)."""
+    z = golden(f"frame_{name}.npz")
+    g = golden(f"sym_{name}.npz")
+    system, derived, grid, cindex, prm = frame_objects(z)
+    cfg = sph.EngineConfig(symmetry=True, precision=precision)
+    out = sph.make_engine(cfg, pi_kernel=kernel).compute(system, derived, grid, cindex, prm)
+    assert [out.stats.candidate_pairs, out.stats.true_pairs, out.stats.force_evals,
+            out.stats.ff_force_evals] == list(g["sym1_counters"])
+    tol = FP32_TOL if precision == "fp32" else 1e-12
+    for a, f in ((out.accel, "accel"), (out.drho_dt, "drho"), (out.visc_dt, "visc")):
+        assert oracle.rel_linf(a, g[f"sym1_{f}"]) <= tol, f
+    assert out.stats.engine_tag.startswith("b200-cellpairs-on")
+
+
+@pytest.mark.parametrize("name", SYM_FRAMES)
+def test_cellpairs_asymmetric_config_vs_reference(name):
+    """EngineConfig(symmetry=False): run_cells_asymmetric's counters and (FP64) its forces bit
+    for bit -- the one-sided cell traversal accumulates in the gather kernels' order."""
+    z = golden(f"frame_{name}.npz")
+    g = golden(f"sym_{name}.npz")
+    system, derived, grid, cindex, prm = frame_objects(z)
+    out = sph.make_engine(sph.EngineConfig(symmetry=False, precision="fp64")).compute(
+        system, derived, grid, cindex, prm)
+    assert [out.stats.candidate_pairs, out.stats.true_pairs, out.stats.force_evals,
+            out.stats.ff_force_evals] == list(g["asym1_counters"])
+    assert np.array_equal(out.accel, g["asym1_accel"]) and np.array_equal(out.drho_dt, g["asym1_drho"])
+    assert np.array_equal(out.visc_dt, g["asym1_visc"])
+
+
 def test_engine_auto_blocking_is_the_run_rule():
     z = golden("frame_c1_n1.npz")
     system, derived, grid, cindex, prm = frame_objects(z)
@@ -266,8 +326,9 @@ def test_run_simulation_fp32_one_step_and_short_trajectory():
     np.testing.assert_allclose(dts, z["dt"][:10], rtol=1e-5)
 
 
-@pytest.mark.parametrize("pi_block", ["auto", 384])
-def test_drift_1000_steps_fp32_vs_reference(pi_block):
+@pytest.mark.parametrize("pi_block,pi_kernel", [("auto", "gather"), (384, "gather"),
+                                               (384, "symmetric")])
+def test_drift_1000_steps_fp32_vs_reference(pi_block, pi_kernel):
     """SURVEY.md §8(d) drift bar: E = KE + PE + IE; tolerances stated in DESIGN.md.  Run with
     the size rule's build (C1: pi256) and with the production 384-target build forced."""
     z = golden("drift_c1.npz")
@@ -283,7 +344,7 @@ def test_drift_1000_steps_fp32_vs_reference(pi_block):
 
     system, stats = sph.run_simulation(sc, prm, gather_cfg("slowcellsh", "fp32"), max_steps=1000,
                                        snapshot_every=10, snapshot_sink=Sink(), stage_timing=False,
-                                       pi_block=pi_block)
+                                       pi_block=pi_block, pi_kernel=pi_kernel)
     got = np.array(rows)
     ref = z["diag"][1:]
     assert got.shape == ref.shape and np.array_equal(got[:, 0], ref[:, 0])
@@ -492,7 +553,7 @@ def test_state_soa_round_trip():
     assert L.sphb_state_from_soa(-1, 1, *ptrs, 0, 0, 0, s) == _lib.SPHB_E_INVALID
 
 
-@pytest.mark.parametrize("block", [256, 384])
+@pytest.mark.parametrize("block", [256, 384, "symmetric"])
 @pytest.mark.parametrize("name", ["c1", "c2"])
 def test_pi_block_matches_128(name, block):
     """The 256- and 384-target blockings (pi256 / pi384: 8- / 12-warp CTAs) gives the 128-target one's counters
@@ -502,7 +563,10 @@ def test_pi_block_matches_128(name, block):
     system = sph.build_dam_break(sc, prm)
     a = D.DeviceSim(system, prm, reach=1, precision=0)
     b = D.DeviceSim(system, prm, reach=1, precision=0)
-    b.set_pi_block(block)
+    if block == "symmetric":
+        b.set_pi_kernel("symmetric")
+    else:
+        b.set_pi_block(block)
     for step in range(4):
         a.launch_step()
         b.launch_step()
@@ -601,6 +665,29 @@ def _device_counters(name, n_subdiv, precision="fp32"):
 
 
 @pytest.mark.slow
+@pytest.mark.parametrize("n_subdiv", [1, 2])
+def test_c2_symmetric_kernel_vs_oracle(c2_frames, n_subdiv):
+    """C2 through the symmetric FP32 kernel: gather counters bit-exact and forces within 1e-5 of
+    the oracle gather; and the cellpairs-symmetric config's counters equal the oracle's
+    symmetric traversal (oracle.cellpairs, bit-exact to the reference's)."""
+    system, prm, ss, der, nl, (cell, perm, cidx, ref) = c2_frames(n_subdiv)
+    variant = "slowcellsh" if n_subdiv == 1 else "slowcellshalf"
+    grid = types.SimpleNamespace(cell_of=nl["cell_of"])
+    out = sph.make_engine(gather_cfg(variant, "fp32"), pi_kernel="symmetric").compute(ss, der, grid, None, prm)
+    _check_vs_oracle(out, ref)
+    sym = oracle.cellpairs(ss.pos, ss.vel, ss.rho, ss.count_boundary, ss.mass_fluid, ss.mass_boundary,
+                           cell_dims(prm), cidx, prm, symmetric=True, threads=16)
+    outs = sph.make_engine(sph.EngineConfig(symmetry=True), pi_kernel="symmetric").compute(
+        ss, der, grid, None, prm)
+    _check_vs_oracle(outs, sym)
+
+
+def cell_dims(prm):
+    from paper_1110_3711_b200.physics import grid_dims
+    return grid_dims(prm)[1]
+
+
+@pytest.mark.slow
 @pytest.mark.parametrize("n_subdiv,block", [(1, 128), (1, 256), (1, 384), (2, 128), (2, 384)])
 def test_c2_each_blocking_vs_oracle(c2_frames, n_subdiv, block):
     """C2 (1,142,622 particles) through the engine with each FP32 build forced: counters
@@ -631,6 +718,9 @@ def test_c3_10m_production_build_vs_oracle():
     out = eng.compute(ss, der, types.SimpleNamespace(cell_of=nl["cell_of"]), None, prm)
     assert eng.last_pi_block == 384
     _check_vs_oracle(out, ref)
+    out = sph.make_engine(gather_cfg("slowcellsh", "fp32"), pi_kernel="symmetric").compute(
+        ss, der, types.SimpleNamespace(cell_of=nl["cell_of"]), None, prm)
+    _check_vs_oracle(out, ref)
 
 
 @pytest.mark.slow
@@ -654,6 +744,8 @@ def test_collapsed_c2_production_build_vs_fp64():
         eng = sph.make_engine(cfg, pi_block=block)
         out = eng.compute(ss, der, grid, None, prm)
         _check_vs_oracle(out, ref)
+    out = sph.make_engine(cfg, pi_kernel="symmetric").compute(ss, der, grid, None, prm)
+    _check_vs_oracle(out, ref)
 
 
 @pytest.mark.slow
