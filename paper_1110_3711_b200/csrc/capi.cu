@@ -137,6 +137,7 @@ int sphb_workspace_create(int64_t n_max, int64_t ncells_max, sphb_workspace_t** 
   // a block never spans two cell rows and holds >= 1 target: #blocks <= n/BT + n
   ws->max_blocks = n1 + n1 / 64 + 16;
   if (e == cudaSuccess) e = alloc((void**)&ws->blocks, 2 * sizeof(int4) * ws->max_blocks);
+  if (e == cudaSuccess) e = alloc((void**)&ws->row_off, sizeof(int32_t) * (ncells_max + 1));
   if (e == cudaSuccess) e = alloc((void**)&ws->energy_part, sizeof(double) * 5 * 592);
   if (e == cudaSuccess) e = alloc((void**)&ws->sym_scratch, sizeof(unsigned long long));
   if (e == cudaSuccess) e = cudaMemset(ws->sym_scratch, 0, sizeof(unsigned long long));
@@ -171,6 +172,7 @@ int sphb_workspace_destroy(sphb_workspace_t* ws) {
   if (!ws) return SPHB_OK;
   cudaFree(ws->cnt);
   cudaFree(ws->sym_scratch);
+  cudaFree(ws->row_off);
   for (int k = 0; k < 2; ++k) {
     cudaFree(ws->keys_tmp[k]);
     cudaFree(ws->vals_tmp[k]);

@@ -389,121 +389,120 @@ __device__ __forceinline__ bool screen(const KArgs& a, const C32&, const Own<dou
 // (fluid targets and boundary targets of the same cells share one staged candidate set).
 // Only cell columns [tx0, tx1) hold targets (the owned slab of an X-slab decomposition;
 // halo columns outside it are candidates only).  A cell with more than BT targets is split
-// into single-list blocks.
+// into single-list chunks.
 // Block record (2 x int4): (fluid i0, i1, boundary i0, i1), (row, first cell x, last cell x, 0)
-__device__ __forceinline__ void emit_block(sphb_ctrl_t* ctrl, int4* out, int4 b, int row, int xa,
-                                           int xb) {
-  const uint32_t k = atomicAdd(&ctrl->nblk[0], 1u);
-  out[2 * k] = b;
-  out[2 * k + 1] = make_int4(row, xa, xb, 0);
-}
-
-constexpr int KB_BUF = 64;  // block records buffered per row before one range reservation
-
+//
+// Two passes over the rows (COUNT: records per row; then, after an exclusive scan over the
+// rows, WRITE: records at the row's offset), so the block list is in row order (z-major, then
+// y): the persistent interaction CTAs pulling consecutive blocks work on neighbouring rows
+// whose stencil rows overlap, and the staged rows come from L2 instead of DRAM.
+template <bool COUNT>
 __global__ void __launch_bounds__(32) k_blocks(sphb_grid_t g, int64_t ncells,
                                                const int32_t* __restrict__ beg,
                                                const int32_t* __restrict__ end,
+                                               int32_t* __restrict__ row_off,
                                                int4* __restrict__ blk, sphb_ctrl_t* ctrl) {
   // one warp per cell row: the lanes stage the row's cumulative ends (both lists) in shared
-  // memory, lane 0 makes the greedy cut, and the row's records are written with ONE atomic
-  // range reservation per KB_BUF records (a per-record atomic on one counter serialises ~10^5
-  // atomics per step at the L2)
+  // memory, lane 0 makes the greedy cut
   extern __shared__ int32_t s_ends[];  // [span] fluid ends, then [span] boundary ends
-  __shared__ int4 s_rec[2 * KB_BUF];
-  __shared__ int s_nrec;
   if (!step_live(ctrl)) return;
   const int nx = g.dims[0];
   const int64_t nrows = (int64_t)g.dims[1] * g.dims[2];
-  if (g.tx1 <= g.tx0) return;
   const int span = g.tx1 - g.tx0, lane = threadIdx.x;
-  auto flush = [&]() {  // all lanes: reserve a range, copy the buffered records
-    __syncwarp();
-    const int nrec = s_nrec;
-    uint32_t base = 0;
-    if (lane == 0 && nrec) base = atomicAdd(&ctrl->nblk[0], (uint32_t)nrec);
-    base = __shfl_sync(SPHB_FULL, base, 0);
-    for (int k = lane; k < 2 * nrec; k += 32) blk[2 * (int64_t)base + k] = s_rec[k];
-    __syncwarp();
-    if (lane == 0) s_nrec = 0;
-    __syncwarp();
-  };
-  if (lane == 0) s_nrec = 0;
   for (int64_t r = blockIdx.x; r < nrows; r += gridDim.x) {
     const int64_t cb = r * nx, cf = ncells + r * nx;  // row offsets in the B / F tables
-    if (end[cf + g.tx1 - 1] <= beg[cf + g.tx0] && end[cb + g.tx1 - 1] <= beg[cb + g.tx0]) continue;
+    if (span <= 0 ||
+        (end[cf + g.tx1 - 1] <= beg[cf + g.tx0] && end[cb + g.tx1 - 1] <= beg[cb + g.tx0])) {
+      if (COUNT && lane == 0) row_off[r] = 0;
+      continue;
+    }
     for (int k = lane; k < span; k += 32) {
       s_ends[k] = end[cf + g.tx0 + k];
       s_ends[span + k] = end[cb + g.tx0 + k];
     }
     __syncwarp();
-    // lane 0 cuts; whenever its buffer fills, the warp flushes (k resumes where it stopped)
-    int k = 0;
-    int32_t f0 = beg[cf + g.tx0], b0 = beg[cb + g.tx0];  // open block
-    int32_t fcur = f0, bcur = b0;
-    int xa = -1, xl = -1;  // first / last non-empty cell of the open block
-    bool done = false;
-    while (true) {
-      if (lane == 0) {
-        bool direct = false;  // (shadowed per cell below)
-        auto emit_to = [&](bool dir, int4 b, int x0, int x1) {
-          if (dir) {
-            emit_block(ctrl, blk, b, (int)r, x0, x1);
-            return;
-          }
-          const int n = s_nrec;
-          s_rec[2 * n] = b;
-          s_rec[2 * n + 1] = make_int4((int)r, x0, x1, 0);
-          s_nrec = n + 1;
-        };
-        (void)direct;
-        for (; k < span; ++k) {
-          const int x = g.tx0 + k;
-          const int32_t fe = s_ends[k], be = s_ends[span + k];
-          if (fe == fcur && be == bcur) continue;  // empty cell
-          // records this cell can emit (close + oversized chunks); stop and flush when the
-          // buffer cannot take them, unless it is empty (then records go out directly)
-          const int need = 1 + (fe - f0 + BT - 1) / BT + (be - b0 + BT - 1) / BT;
-          if (s_nrec + need > KB_BUF && s_nrec > 0) break;
-          const bool direct = need > KB_BUF;
-          if ((fe - f0) + (be - b0) > BT && (fcur > f0 || bcur > b0)) {  // close before this cell
-            emit_to(direct, make_int4(f0, fcur, b0, bcur), xa, xl);
-            f0 = fcur;
-            b0 = bcur;
-            xa = -1;
-          }
-          if ((fe - f0) + (be - b0) > BT) {  // one oversized cell: single-list chunks of <= BT
-            for (int32_t p = f0; p < fe; p += BT)
-              emit_to(direct, make_int4(p, min(p + BT, fe), be, be), x, x);
-            for (int32_t p = b0; p < be; p += BT)
-              emit_to(direct, make_int4(fe, fe, p, min(p + BT, be)), x, x);
-            f0 = fe;
-            b0 = be;
-          } else {
-            if (xa < 0) xa = x;
-            xl = x;
-          }
-          fcur = fe;
-          bcur = be;
+    if (lane == 0) {
+      int nrec = 0;
+      int4* out = COUNT ? nullptr : blk + 2 * (int64_t)row_off[r];
+      auto emit = [&](int4 b, int x0, int x1) {
+        if (!COUNT) {
+          out[2 * nrec] = b;
+          out[2 * nrec + 1] = make_int4((int)r, x0, x1, 0);
         }
-        if (k >= span) {
-          if (fcur > f0 || bcur > b0) {
-            if (s_nrec == KB_BUF) {  // no room for the final record: write it directly
-              emit_block(ctrl, blk, make_int4(f0, fcur, b0, bcur), (int)r, xa, xl);
-            } else {
-              emit_to(false, make_int4(f0, fcur, b0, bcur), xa, xl);
-            }
-          }
-          done = true;
+        ++nrec;
+      };
+      int32_t f0 = beg[cf + g.tx0], b0 = beg[cb + g.tx0];  // open block
+      int32_t fcur = f0, bcur = b0;
+      int xa = -1, xl = -1;  // first / last non-empty cell of the open block
+      for (int k = 0; k < span; ++k) {
+        const int x = g.tx0 + k;
+        const int32_t fe = s_ends[k], be = s_ends[span + k];
+        if (fe == fcur && be == bcur) continue;  // empty cell
+        if ((fe - f0) + (be - b0) > BT && (fcur > f0 || bcur > b0)) {  // close before this cell
+          emit(make_int4(f0, fcur, b0, bcur), xa, xl);
+          f0 = fcur;
+          b0 = bcur;
+          xa = -1;
         }
+        if ((fe - f0) + (be - b0) > BT) {  // one oversized cell: single-list chunks of <= BT
+          for (int32_t p = f0; p < fe; p += BT) emit(make_int4(p, min(p + BT, fe), be, be), x, x);
+          for (int32_t p = b0; p < be; p += BT) emit(make_int4(fe, fe, p, min(p + BT, be)), x, x);
+          f0 = fe;
+          b0 = be;
+        } else {
+          if (xa < 0) xa = x;
+          xl = x;
+        }
+        fcur = fe;
+        bcur = be;
       }
-      done = __shfl_sync(SPHB_FULL, done, 0);
-      if (done) break;
-      flush();
+      if (fcur > f0 || bcur > b0) emit(make_int4(f0, fcur, b0, bcur), xa, xl);
+      if (COUNT) row_off[r] = nrec;
     }
-    __syncwarp();  // lane 0's record-count writes are visible to the warp (racecheck)
-    if (s_nrec >= KB_BUF / 2) flush();
+    __syncwarp();
   }
-  flush();
+}
+
+// exclusive scan of the per-row record counts (one CTA: rows ~10^4); the total is the launch's
+// block count (ctrl->nblk[0], read by the interaction CTAs)
+constexpr int KB_SCAN = 1024;
+__global__ void __launch_bounds__(KB_SCAN) k_blocks_scan(int32_t* row_off, int64_t nrows,
+                                                         sphb_ctrl_t* ctrl) {
+  if (!step_live(ctrl)) return;
+  __shared__ int32_t s_w[KB_SCAN / 32];
+  __shared__ int32_t s_carry;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) s_carry = 0;
+  __syncthreads();
+  for (int64_t base = 0; base < nrows; base += KB_SCAN) {
+    const int64_t r = base + tid;
+    const int32_t v = r < nrows ? row_off[r] : 0;
+    int32_t x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int32_t y = __shfl_up_sync(SPHB_FULL, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) s_w[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+      int32_t w = s_w[lane];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int32_t y = __shfl_up_sync(SPHB_FULL, w, o);
+        if (lane >= o) w += y;
+      }
+      s_w[lane] = w;  // inclusive per-warp totals
+    }
+    __syncthreads();
+    const int32_t carry = s_carry;
+    const int32_t excl = carry + (warp ? s_w[warp - 1] : 0) + x - v;
+    if (r < nrows) row_off[r] = excl;
+    __syncthreads();
+    if (tid == KB_SCAN - 1) s_carry = carry + s_w[KB_SCAN / 32 - 1];
+    __syncthreads();
+  }
+  if (tid == 0) ctrl->nblk[0] = (uint32_t)s_carry;
 }
 
 // ------------------------------------------------------------------ the interaction kernel
@@ -1467,7 +1466,14 @@ __global__ void __launch_bounds__(NW * 32, V8_MINB) k_interact_v8(KArgs a, K32 k
     // Entries are (mask, row address) pairs, 8 B, RINGC per lane; hp / tp are the lane's read
     // and write entry addresses (stride 256 B: 32 lanes), cnt the entries queued.  An
     // exhausted FIFO points cb one row past the dummy: the empty pop (bfind = -1) lands on it.
-    uint32_t hp = ring, tp = ring, cnt = 0, pend = 0, cur = 0u, cb = dummy + 16u;
+    // Symmetric build: masks are queued rotated left by the lane index, so lanes holding the
+    // same word (neighbouring targets share most candidates) pop different candidates in the
+    // same iteration -- their reactions then hit different shared-memory rows (no CAS
+    // contention).  rot = 0 in the gather builds (pop order = staged order).
+    const uint32_t rot = V8_SYM ? (uint32_t)lane : 0u;
+    // an empty pop (bfind = -1) must land on the dummy row: b = 31 - rot rotated, -1 plain
+    const uint32_t dummy_cb = V8_SYM ? dummy - 16u * (31u - rot) : dummy + 16u;
+    uint32_t hp = ring, tp = ring, cnt = 0, pend = 0, cur = 0u, cb = dummy_cb;
     // the head entry is held in registers (nx_mask, nx_cb): a refill is a register move plus
     // the load of the following entry, which has several pops to land
     uint32_t nx_mask = 0u, nx_cb = 0u;
@@ -1482,10 +1488,12 @@ __global__ void __launch_bounds__(NW * 32, V8_MINB) k_interact_v8(KArgs a, K32 k
         nx_mask = e.x;
         nx_cb = e.y;
       }
-      cb = (need & !have) ? dummy + 16u : cb;
+      cb = (need & !have) ? dummy_cb : cb;
       const int tb = flo32(cur);
       cur = clear_bit(cur, tb);
-      return cb + 16u * (uint32_t)tb;  // bit b <-> candidate k0 + b; empty (-1) -> the dummy
+      // bit b <-> candidate k0 + b (rotated: b = tb - rot); empty (tb = -1) -> the dummy
+      if (V8_SYM) return cb + 16u * (((uint32_t)tb - rot) & 31u);
+      return cb + 16u * (uint32_t)tb;
     };
     auto drain = [&](bool full) {
       __syncwarp();
@@ -1653,7 +1661,8 @@ __global__ void __launch_bounds__(NW * 32, V8_MINB) k_interact_v8(KArgs a, K32 k
             }
             if (__any_sync(SPHB_FULL, bits != 0u && cnt == (uint32_t)RINGC)) drain(false);
             if (bits) {
-              sts64u(tp, bits, smA + 16u * (uint32_t)k0 + (((!EQM || V8_SYM) && boundary_list) ? 1u : 0u));
+              const uint32_t qb = V8_SYM ? __funnelshift_l(bits, bits, rot) : bits;
+              sts64u(tp, qb, smA + 16u * (uint32_t)k0 + (((!EQM || V8_SYM) && boundary_list) ? 1u : 0u));
               tp = tp + 256u == rend ? ring : tp + 256u;
               ++cnt;
               pend += __popc(bits);
@@ -1977,7 +1986,7 @@ namespace SPHB_PI_NS {
 
 int64_t interact_launch_count(int64_t n) {
   (void)n;
-  return V8_SYM ? 3 : 2;  // k_blocks, the interaction kernel (+ k_dt_f32)
+  return V8_SYM ? 5 : 4;  // k_blocks (count, scan, write), the interaction kernel (+ k_dt_f32)
 }
 
 static int launch_wall(const sphb_params_t& p, const sphb_grid_t& g, int64_t n, int64_t nb,
@@ -2042,7 +2051,11 @@ int launch_interact(sphb_workspace* ws, const sphb_params_t& p, const sphb_grid_
   if (gb < 1) gb = 1;
   const size_t sm_blocks = sizeof(int32_t) * 2 * (size_t)(g.tx1 - g.tx0);
   if (sm_blocks > 48 * 1024) return sphb_set_error(SPHB_E_INVALID, "more than 6144 cell columns per slab");
-  k_blocks<<<gb, 32, sm_blocks, s>>>(g, a.ncells, beg, end, ws->blocks, ctrl);
+  k_blocks<true><<<gb, 32, sm_blocks, s>>>(g, a.ncells, beg, end, ws->row_off, ws->blocks, ctrl);
+  if (int rc = sphb_check_launch("k_blocks count")) return rc;
+  k_blocks_scan<<<1, KB_SCAN, 0, s>>>(ws->row_off, nrows, ctrl);
+  if (int rc = sphb_check_launch("k_blocks_scan")) return rc;
+  k_blocks<false><<<gb, 32, sm_blocks, s>>>(g, a.ncells, beg, end, ws->row_off, ws->blocks, ctrl);
   if (int rc = sphb_check_launch("k_blocks")) return rc;
   // one launch for both item classes: fluid targets (F-F + F-B) and boundary targets (B-F,
   // drho + visc only) of the same cells share the staged candidates

@@ -26,6 +26,7 @@ struct sphb_workspace {
   uint32_t* scan_partials = nullptr;
   int4* blocks = nullptr;  // interaction target blocks (fluid i0,i1, boundary i0,i1)
   int64_t max_blocks = 0;
+  int32_t* row_off = nullptr;  // per cell row: block records (k_blocks count pass), then offsets
   int64_t max_sort_tiles = 0, max_scan_tiles = 0;
   double* energy_part = nullptr;  // 592 x 5 partial sums of sphb_energy
   // movers-only sort (nl.cu, k_mv_*): state words, per-32-row mover bitmap and prefix, tile
