@@ -81,10 +81,12 @@ def peaks():
     return hbm, hbm_src, fp32, fp32_src
 
 
-def traffic_for(cfg_name):
-    """DRAM bytes per launch of the fluid k_interact from the committed ncu capture."""
+def traffic_for(cfg_name, n_subdiv, pi_block, pi_kernel):
+    """DRAM bytes (read + write) per launch of the interaction kernel from a committed ncu
+    capture of exactly this workload and build (profiles/ncu_traffic.json), else None."""
     try:
-        t = json.load(open(os.path.join(ROOT, "profiles", "r01_ncu_traffic.json")))[cfg_name]
+        key = f"{cfg_name}/n{n_subdiv}/pi{pi_block}/{pi_kernel}"
+        t = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))[key]
         return float(t["dram_bytes_read"] + t["dram_bytes_write"]), t["source"]
     except Exception:
         return None, None
@@ -626,7 +628,7 @@ def main():
     flops = FLOP_PER_CAND * cand + FLOP_PER_EVAL * evals
     achieved = flops / (pi_mean * 1e-3) / 1e12
     nl_su_ms = float(np.mean(nl_ms) + np.mean(su_ms))
-    traffic, traffic_src = traffic_for(cfg_name)
+    traffic, traffic_src = traffic_for(cfg_name, args.n_subdiv, sim.pi_block, sim.pi_kernel)
     nlsu_gbs = BYTES_NL_SU * system.n / (nl_su_ms * 1e-3) / 1e9
 
     # ---- e2e: the same step through the C ABI with HOST buffers (H2D state in, D2H state out)
