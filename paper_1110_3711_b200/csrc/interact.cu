@@ -131,6 +131,7 @@ struct Seg {
   int g0, g1;   // global particle range of the block's union for this stencil row
   int pos;      // start in the concatenated candidate sequence
   int rowoff;   // offset of the row's first cell in beg/end (list offset included)
+  int dyz;      // row offset from the block's origin row: (dy + 16) | (dz + 16) << 8
 };
 
 __device__ __forceinline__ bool step_live(const sphb_ctrl_t* c) {
@@ -396,19 +397,96 @@ __device__ __forceinline__ bool screen(const KArgs& a, const C32&, const Own<dou
 // rows, WRITE: records at the row's offset), so the block list is in row order (z-major, then
 // y): the persistent interaction CTAs pulling consecutive blocks work on neighbouring rows
 // whose stencil rows overlap, and the staged rows come from L2 instead of DRAM.
+//
+// Bricks (h/2 cells, reach 2, cell order): the unit is a pair of rows in y times a pair in z,
+// cut along x into blocks of whole cell columns (4 cells) holding <= BT targets.  A brick
+// stages the union of its rows' stencils, (2r + 2)^2 rows instead of (2r + 1)^2 per row, so
+// per target ~12 staged candidates at rest (2 x 2 rows x 12 cells of 8 particles over
+// 6 x 6 rows x 16 cells) where 1-row blocks need ~31.  Record: (0, 0, 0, 0),
+// (row of (y0, z0), first cell x, last cell x, 1).  A column with more than BT targets falls
+// back to 1-row single-list chunks.
 template <bool COUNT>
 __global__ void __launch_bounds__(32) k_blocks(sphb_grid_t g, int64_t ncells,
                                                const int32_t* __restrict__ beg,
                                                const int32_t* __restrict__ end,
                                                int32_t* __restrict__ row_off,
-                                               int4* __restrict__ blk, sphb_ctrl_t* ctrl) {
+                                               int4* __restrict__ blk, sphb_ctrl_t* ctrl,
+                                               int brick) {
   // one warp per cell row: the lanes stage the row's cumulative ends (both lists) in shared
   // memory, lane 0 makes the greedy cut
   extern __shared__ int32_t s_ends[];  // [span] fluid ends, then [span] boundary ends
   if (!step_live(ctrl)) return;
-  const int nx = g.dims[0];
-  const int64_t nrows = (int64_t)g.dims[1] * g.dims[2];
+  const int nx = g.dims[0], ny = g.dims[1], nz = g.dims[2];
+  const int nyb = brick ? (ny + 1) / 2 : ny, nzb = brick ? (nz + 1) / 2 : nz;
+  const int64_t nrows = (int64_t)nyb * nzb;
   const int span = g.tx1 - g.tx0, lane = threadIdx.x;
+  if (brick) {
+    for (int64_t r = blockIdx.x; r < nrows; r += gridDim.x) {
+      const int y0 = 2 * (int)(r % nyb), z0 = 2 * (int)(r / nyb);
+      int tot_all = 0;
+      for (int k = lane; k < span; k += 32) {  // targets of the brick's cell column x
+        const int x = g.tx0 + k;
+        int c = 0;
+        for (int sub = 0; sub < 4; ++sub) {
+          const int yy = y0 + (sub & 1), zz = z0 + (sub >> 1);
+          if (yy >= ny || zz >= nz) continue;
+          const int64_t rb = (int64_t)nx * (yy + (int64_t)ny * zz) + x, rf = ncells + rb;
+          c += (end[rf] - beg[rf]) + (end[rb] - beg[rb]);
+        }
+        s_ends[k] = c;
+        tot_all += c;
+      }
+      tot_all = __reduce_add_sync(SPHB_FULL, tot_all);
+      __syncwarp();
+      if (tot_all == 0) {
+        if (COUNT && lane == 0) row_off[r] = 0;
+        continue;
+      }
+      if (lane == 0) {
+        int nrec = 0;
+        int4* out = COUNT ? nullptr : blk + 2 * (int64_t)row_off[r];
+        auto emit = [&](int4 b, int4 m) {
+          if (!COUNT) {
+            out[2 * nrec] = b;
+            out[2 * nrec + 1] = m;
+          }
+          ++nrec;
+        };
+        const int key0 = y0 + ny * z0;
+        int tot = 0, xa = -1, xl = -1;
+        for (int k = 0; k < span; ++k) {
+          const int x = g.tx0 + k, c = s_ends[k];
+          if (c == 0) continue;
+          if (tot + c > BT && tot > 0) {
+            emit(make_int4(0, 0, 0, 0), make_int4(key0, xa, xl, 1));
+            tot = 0;
+            xa = -1;
+          }
+          if (c > BT) {  // oversized column: 1-row single-list chunks
+            for (int sub = 0; sub < 4; ++sub) {
+              const int yy = y0 + (sub & 1), zz = z0 + (sub >> 1);
+              if (yy >= ny || zz >= nz) continue;
+              const int key = yy + ny * zz;
+              const int64_t rb = (int64_t)nx * key + x, rf = ncells + rb;
+              const int32_t fb = beg[rf], fe = end[rf], bb0 = beg[rb], be = end[rb];
+              for (int32_t p = fb; p < fe; p += BT)
+                emit(make_int4(p, min(p + BT, fe), be, be), make_int4(key, x, x, 0));
+              for (int32_t p = bb0; p < be; p += BT)
+                emit(make_int4(fe, fe, p, min(p + BT, be)), make_int4(key, x, x, 0));
+            }
+            continue;
+          }
+          if (xa < 0) xa = x;
+          xl = x;
+          tot += c;
+        }
+        if (tot > 0) emit(make_int4(0, 0, 0, 0), make_int4(key0, xa, xl, 1));
+        if (COUNT) row_off[r] = nrec;
+      }
+      __syncwarp();
+    }
+    return;
+  }
   for (int64_t r = blockIdx.x; r < nrows; r += gridDim.x) {
     const int64_t cb = r * nx, cf = ncells + r * nx;  // row offsets in the B / F tables
     if (span <= 0 ||
@@ -1263,33 +1341,50 @@ __global__ void __launch_bounds__(NW * 32, V8_MINB) k_interact_v8(KArgs a, K32 k
     const uint32_t blk = (uint32_t)s_blk;
     if (blk >= nblocks) break;
     const int4 bb = s_bb[0], bm = s_bb[1];
-    const int f0 = bb.x, nf = bb.y - bb.x, b0 = bb.z, nbt = bb.w - bb.z;
+    // brick block (h/2 cells, reach >= 2: bm.w = 1): rows (y0 + sy, z0 + sz), sy, sz in {0, 1},
+    // over cells [cxa, cxb]; its targets are the four rows' fluid ranges, then their boundary
+    // ranges (derived from beg / end below).  Row block (bm.w = 0): one row, ranges in bb.
+    const bool brick = bm.w != 0;
+    const int bsd = brick ? 2 : 1;  // rows per side of the block
     const int rowkey = bm.x;
     const int cxa = bm.y, cxb = bm.z;
-    const int nlist = nf ? 2 : 1;
+    const int nlist = (brick || bb.y > bb.x) ? 2 : 1;
     // symmetric build: the own row (forward cells only, j > i per target) and the forward rows
     // (dz = 0, dy = 1..r; dz = 1..r, dy = -r..r): every unordered pair once, as
     // run_cells_symmetric / forward_offsets (kernels.py:121-175, grid.py:147-156)
-    const int nrow = V8_SYM ? 1 + reach + reach * side : side * side;
+    const int bside = side + bsd - 1;  // staged rows per side: 2r + 1 (row) / 2r + 2 (brick)
+    const int nrow = V8_SYM ? 1 + reach + reach * side : bside * bside;
     const int nseg = nlist * nrow;
     const int gcz = rowkey / ny, gcy = rowkey - gcz * ny;
     const int bxlo = max(cxa - reach, 0), bxhi = min(cxb + reach, nx - 1);
     const double cs = a.g.cell_size;
     const float h16_s = (float)(0.5 * a.p.invh);
     const float h16_xc = (float)(a.g.origin[0] + 0.5 * (bxlo + bxhi + 1) * cs);
-    const float h16_yc = (float)(a.g.origin[1] + (gcy + 0.5) * cs);
-    const float h16_zc = (float)(a.g.origin[2] + (gcz + 0.5) * cs);
+    const float h16_yc = (float)(a.g.origin[1] + (gcy + 0.5 * bsd) * cs);
+    const float h16_zc = (float)(a.g.origin[2] + (gcz + 0.5 * bsd) * cs);
     const double xext = 0.5 * (bxhi - bxlo + 1) * cs * (0.5 * a.p.invh);
-    const double yzext = (reach + 0.5) * cs * (0.5 * a.p.invh);
+    const double yzext = (reach + 0.5 * bsd) * cs * (0.5 * a.p.invh);
     const bool use16 = xext <= H16_MAXABS && yzext <= H16_MAXABS &&
                        xext * xext + 2.0 * yzext * yzext < 30.0;
     // the fluid targets' own row (fluid list, dy = dz = 0)
     const int rr_c = reach * side + reach;
-    const int selfseg = (nf && !V8_SYM) ? ((nlist == 2 && a.p.order == 1) ? rr_c : rr_c * nlist) : -1;
+    const int selfseg = (bb.y > bb.x && !V8_SYM) ? ((nlist == 2 && a.p.order == 1) ? rr_c : rr_c * nlist) : -1;
 
+    __shared__ int s_tlo[8], s_tlen[8];  // brick targets: F rows 0..3, then B rows 0..3
+    if (brick && tid < 8) {
+      const int li = tid >> 2, sub = tid & 3, yy = gcy + (sub & 1), zz = gcz + (sub >> 1);
+      int lo = 0, len = 0;
+      if (yy < ny && zz < nz) {
+        const int64_t ro = (li == 0 ? a.ncells : 0) + (int64_t)nx * (yy + (int64_t)ny * zz);
+        lo = a.beg[ro + cxa];
+        len = max(a.end[ro + cxb] - lo, 0);
+      }
+      s_tlo[tid] = lo;
+      s_tlen[tid] = len;
+    }
     if (tid < MAXSEG) {
       int len = 0;
-      Seg sg = {0, 0, 0, 0};
+      Seg sg = {0, 0, 0, 0, 0};
       if (tid < nseg) {
         int li, rr;
         if (nlist == 2 && a.p.order == 1) {
@@ -1299,7 +1394,7 @@ __global__ void __launch_bounds__(NW * 32, V8_MINB) k_interact_v8(KArgs a, K32 k
           li = tid % nlist;
           rr = tid / nlist;
         }
-        int dz = rr / side - reach, dy = rr % side - reach, sxlo = bxlo;
+        int dz = rr / bside - reach, dy = rr % bside - reach, sxlo = bxlo;
         if (V8_SYM) {
           const int q = rr - 1 - reach;
           dz = rr == 0 ? 0 : (q < 0 ? 0 : 1 + q / side);
@@ -1312,6 +1407,7 @@ __global__ void __launch_bounds__(NW * 32, V8_MINB) k_interact_v8(KArgs a, K32 k
           sg.g0 = a.beg[rowoff + sxlo];
           sg.g1 = a.end[rowoff + bxhi];
           sg.rowoff = (int)rowoff;
+          sg.dyz = (dy + 16) | ((dz + 16) << 8);
           len = max(sg.g1 - sg.g0, 0);
           if (len == 0) sg.g1 = sg.g0;
         }
@@ -1345,10 +1441,36 @@ __global__ void __launch_bounds__(NW * 32, V8_MINB) k_interact_v8(KArgs a, K32 k
     const int total = s_nseg_tot;
 
     const int t = warp * 32 + lane;
+    int nf = bb.y - bb.x, nbt = bb.w - bb.z, i, rsy = 0, rsz = 0;
+    if (brick) {  // lane t -> (sub-range, offset): fluid ranges first, then boundary ranges
+      int pre = 0, kk = 0, lo = s_tlo[0];
+      nf = s_tlen[0] + s_tlen[1] + s_tlen[2] + s_tlen[3];
+      nbt = s_tlen[4] + s_tlen[5] + s_tlen[6] + s_tlen[7];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int len = s_tlen[k];
+        if (t >= pre && t < pre + len) {
+          kk = k;
+          lo = s_tlo[k] + (t - pre);
+        }
+        pre += len;
+      }
+      i = lo;
+      rsy = kk & 1;
+      rsz = (kk >> 1) & 1;
+    } else {
+      i = t < nf ? bb.x + t : bb.z + (t - nf);
+    }
     const bool isf = t < nf;
-    const int i = isf ? f0 + t : b0 + (t - nf);
     const bool valid = t < nf + nbt;
     const bool wactive = warp * 32 < nf + nbt;
+    // the lane's stencil rows among the staged ones (a brick stages the union of its rows')
+    auto in_rows = [&](int dyz) {
+      return abs((dyz & 255) - 16 - rsy) <= reach && abs((dyz >> 8) - 16 - rsz) <= reach;
+    };
+    // the fluid target's own row among the segments (brick: per lane)
+    const int selfseg_l =
+        !brick ? selfseg : ((rsz + reach) * bside + (rsy + reach)) * nlist;
     Own32 o;
     float ocs = 0.f;
     int xlo = 0, xhi = -1, cxi = INT_MAX;
@@ -1359,7 +1481,7 @@ __global__ void __launch_bounds__(NW * 32, V8_MINB) k_interact_v8(KArgs a, K32 k
         pi = a.posp[i];
         vi = a.velr[i];
         xi = a.aux[i];
-        cxi = a.cell[i] - rowkey * nx;
+        cxi = a.cell[i] - (rowkey + rsy + ny * rsz) * nx;
         xlo = max(cxi - reach, 0);
         xhi = min(cxi + reach, nx - 1);
       }
@@ -1422,7 +1544,7 @@ __global__ void __launch_bounds__(NW * 32, V8_MINB) k_interact_v8(KArgs a, K32 k
           const int k = k0 + u;
           if (k < nseg) {
             const Seg sg = sSeg[k];
-            if (sg.g1 > sg.g0 && (isf || sg.rowoff >= a.ncells)) {
+            if (sg.g1 > sg.g0 && (isf || sg.rowoff >= a.ncells) && in_rows(sg.dyz)) {
               e[u] = a.end[sg.rowoff + xhi];
               b[u] = a.beg[sg.rowoff + xlo];
             }
@@ -1601,8 +1723,10 @@ __global__ void __launch_bounds__(NW * 32, V8_MINB) k_interact_v8(KArgs a, K32 k
           const int hi_ = min(sg.pos + (wg1 - sg.g0), q1) - q0;
           if (hi_ <= lo_) continue;
           const bool boundary_list = sg.rowoff < a.ncells;
-          const uint32_t lanemask = (valid && (isf || !boundary_list)) ? 0xffffffffu : 0u;
-          const bool selfrow = k == selfseg;
+          const bool inr = in_rows(sg.dyz);
+          if (brick && !__any_sync(SPHB_FULL, valid && inr)) continue;
+          const uint32_t lanemask = (valid && inr && (isf || !boundary_list)) ? 0xffffffffu : 0u;
+          const bool selfrow = k == selfseg_l;
           // own staged position in the self row (fluid targets), else out of range
           const int selfpos = (selfrow && isf) ? sg.pos + (i - sg.g0) - q0 : INT_MIN / 2;
           // symmetric own row: staged position of the lane's lower bound (batch-relative)
@@ -2051,11 +2175,14 @@ int launch_interact(sphb_workspace* ws, const sphb_params_t& p, const sphb_grid_
   if (gb < 1) gb = 1;
   const size_t sm_blocks = sizeof(int32_t) * 2 * (size_t)(g.tx1 - g.tx0);
   if (sm_blocks > 48 * 1024) return sphb_set_error(SPHB_E_INVALID, "more than 6144 cell columns per slab");
-  k_blocks<true><<<gb, 32, sm_blocks, s>>>(g, a.ncells, beg, end, ws->row_off, ws->blocks, ctrl);
+  // bricks for h/2 cells (reach 2) in the FP32 gather kernel's cell order
+  const int brick = (g.reach == 2 && p.order == 0 && p.precision == SPHB_FP32 && !V8_SYM) ? 1 : 0;
+  const int64_t nunits = brick ? (int64_t)((g.dims[1] + 1) / 2) * ((g.dims[2] + 1) / 2) : nrows;
+  k_blocks<true><<<gb, 32, sm_blocks, s>>>(g, a.ncells, beg, end, ws->row_off, ws->blocks, ctrl, brick);
   if (int rc = sphb_check_launch("k_blocks count")) return rc;
-  k_blocks_scan<<<1, KB_SCAN, 0, s>>>(ws->row_off, nrows, ctrl);
+  k_blocks_scan<<<1, KB_SCAN, 0, s>>>(ws->row_off, nunits, ctrl);
   if (int rc = sphb_check_launch("k_blocks_scan")) return rc;
-  k_blocks<false><<<gb, 32, sm_blocks, s>>>(g, a.ncells, beg, end, ws->row_off, ws->blocks, ctrl);
+  k_blocks<false><<<gb, 32, sm_blocks, s>>>(g, a.ncells, beg, end, ws->row_off, ws->blocks, ctrl, brick);
   if (int rc = sphb_check_launch("k_blocks")) return rc;
   // one launch for both item classes: fluid targets (F-F + F-B) and boundary targets (B-F,
   // drho + visc only) of the same cells share the staged candidates
