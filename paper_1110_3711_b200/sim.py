@@ -52,12 +52,11 @@ PI_LARGE_MIN_TARGETS = 4 * 148 * 384
 
 
 def initial_pi_block(n_targets: int, n_subdiv: int = 1) -> int:
-    """The "auto" blocking for ``n_targets`` interaction targets.  With h/2 cells (n_subdiv 2:
-    8 particles per cell, a 5x5 stencil of rows) a large block stages ~2x its capacity in
-    several batches: 128 targets win there (C3 n_subdiv 2, ms/step: 27.5 with 128, 34.5 with
-    256, 36.6 with 384)."""
-    if int(n_subdiv) != 1:
-        return 128
+    """The "auto" blocking for ``n_targets`` interaction targets: 384 from 4 such blocks per SM,
+    256 below.  With h/2 cells (n_subdiv 2: 8 particles per cell, a 5x5 stencil of rows) the
+    FP32 kernel cuts 2x2-row bricks, which stage ~12 candidates per target like the 384-target
+    row blocks at n_subdiv 1 (C3 n_subdiv 2, ms/step: 19.6 with 384-target bricks, 22.2 with
+    256, 34.3 with 128; 26.2 with the earlier 128-target row blocks)."""
     return 384 if n_targets >= PI_LARGE_MIN_TARGETS else 256
 
 
