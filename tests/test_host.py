@@ -160,4 +160,4 @@ def test_auto_interaction_blocking_policy():
     assert S.initial_pi_block(10_200_478) == 384        # C3
     assert S.initial_pi_block(S.PI_LARGE_MIN_TARGETS) == 384
     assert S.initial_pi_block(S.PI_LARGE_MIN_TARGETS - 1) == 256
-    assert S.initial_pi_block(10_200_478, n_subdiv=2) == 128  # h/2 cells: multi-batch staging
+    assert S.initial_pi_block(10_200_478, n_subdiv=2) == 384  # h/2 cells: 2x2-row bricks
