@@ -57,6 +57,11 @@ def parse():
                     help="FP32 interaction kernel: one-sided gather or symmetric pair evaluation")
     ap.add_argument("--e2e-chunks", type=int, default=8,
                     help="row chunks of the pipelined H2D/D2H state round trip (1 = serial)")
+    ap.add_argument("--collapsed-step", type=int, default=6000,
+                    help="N=1: also time the step after advancing the run to this step (the "
+                         "column has collapsed: cells hold uneven counts); 0 = skip")
+    ap.add_argument("--fp64-steps", type=int, default=5,
+                    help="N=1: also time this many FP64 steps (bit-exact to the reference); 0 = skip")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget-s", type=float, default=20.0)
     ap.add_argument("--slab-path", action="store_true",
@@ -613,6 +618,8 @@ def main():
     err = sim.error()
     if err is not None:
         raise RuntimeError(f"divergence during bench: {err}")
+    build_info = {"pi_block": sim.pi_block, "pi_kernel": sim.pi_kernel,
+                  "pi_lane_use": round(sim.pi_lane_use(), 4), "cuda_graph": use_graph}
     recs = sim.records(first, first + args.steps)
     nl_ms = [e[0].elapsed_time(e[1]) for e in ev]
     pi_ms = [e[1].elapsed_time(e[2]) for e in ev]
@@ -628,7 +635,8 @@ def main():
     flops = FLOP_PER_CAND * cand + FLOP_PER_EVAL * evals
     achieved = flops / (pi_mean * 1e-3) / 1e12
     nl_su_ms = float(np.mean(nl_ms) + np.mean(su_ms))
-    traffic, traffic_src = traffic_for(cfg_name, args.n_subdiv, sim.pi_block, sim.pi_kernel)
+    traffic, traffic_src = traffic_for(cfg_name, args.n_subdiv, build_info["pi_block"],
+                                       build_info["pi_kernel"])
     nlsu_gbs = BYTES_NL_SU * system.n / (nl_su_ms * 1e-3) / 1e9
 
     # ---- e2e: the same step through the C ABI with HOST buffers (H2D state in, D2H state out)
@@ -718,15 +726,77 @@ def main():
         e2e_value = n_all * args.e2e_steps / (e2e_ms * 1e-3)
 
     launches = sim.launches_per_step() * args.steps
+
+    def timed_steps(dsim, k, use_graph_k):
+        """k steps of ``dsim`` timed with CUDA events (graph replay when asked); mean stage
+        times from an eager pass of the same length right before when replaying."""
+        evs = [[Ev() for _ in range(4)] for _ in range(k)]
+        for j in range(k):
+            dsim.launch_step(events=evs[j])
+        torch.cuda.synchronize()
+        stage = {"nl": float(np.mean([e[0].elapsed_time(e[1]) for e in evs])),
+                 "pi": float(np.mean([e[1].elapsed_time(e[2]) for e in evs])),
+                 "su": float(np.mean([e[2].elapsed_time(e[3]) for e in evs]))}
+        f0 = int(dsim.ctrl_host()["step"])
+        if use_graph_k:
+            dsim.capture(k)
+        a0, a1 = Ev(), Ev()
+        torch.cuda.synchronize()
+        a0.record()
+        if use_graph_k:
+            dsim.run_graph()
+        else:
+            for _ in range(k):
+                dsim.launch_step()
+        a1.record()
+        torch.cuda.synchronize()
+        recs_k = dsim.records(f0, f0 + k)
+        return a0.elapsed_time(a1) / k, stage, recs_k
+
+    # ---- the collapsed state: the same run advanced to --collapsed-step (cells hold 30-100
+    # particles instead of the lattice's 64), then timed again
+    collapsed = None
+    if world == 1 and args.collapsed_step > 0:
+        now = int(sim.ctrl_host()["step"])
+        chunk = 500
+        while now < args.collapsed_step:
+            for _ in range(min(chunk, args.collapsed_step - now)):
+                sim.launch_step()
+            torch.cuda.synchronize()
+            now = int(sim.ctrl_host()["step"])
+            if sim.error() is not None:
+                raise RuntimeError(f"divergence while advancing: {sim.error()}")
+        ms_c, stage_c, recs_c = timed_steps(sim, args.steps, False)
+        e_c = float(np.mean(recs_c["force_evals"].astype(np.float64)))
+        c_c = float(np.mean(recs_c["candidate_pairs"].astype(np.float64)))
+        collapsed = {"step": now, "value": system.n / (ms_c * 1e-3), "unit": UNIT, "ms_per_step": ms_c,
+                     "stage_ms": stage_c, "pi_lane_use": round(sim.pi_lane_use(), 4),
+                     "t_sim_s": float(sim.ctrl_host()["t_sim"]),
+                     "interactions_per_s": e_c / 2 / (ms_c * 1e-3),
+                     "pi_fp32_frac": (FLOP_PER_CAND * c_c + FLOP_PER_EVAL * e_c) / (stage_c["pi"] * 1e-3) / 1e12 / fp32,
+                     "steps": args.steps}
+    # ---- FP64: the instantiation that is bit-identical to the reference (its arithmetic)
+    fp64 = None
+    if world == 1 and args.fp64_steps > 0 and prec == _lib.SPHB_FP32:
+        del sim  # room for the second system
+        torch.cuda.empty_cache()
+        sim64 = DeviceSim(system, prm, reach=args.n_subdiv, precision=_lib.SPHB_FP64,
+                          record_capacity=max(64, 3 * args.fp64_steps + 8))
+        for _ in range(2):
+            sim64.launch_step()
+        ms64, stage64, _ = timed_steps(sim64, args.fp64_steps, False)
+        fp64 = {"value": system.n / (ms64 * 1e-3), "unit": UNIT, "ms_per_step": ms64,
+                "stage_ms": stage64, "steps": args.fp64_steps,
+                "note": "FP64 kernels: forces, dt and trajectories bit-identical to the reference"}
+        del sim64
+        torch.cuda.empty_cache()
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
         "scaling": "weak" if world > 1 else "weak", "vs_baseline": None, "dtype": args.precision,
         "data": "synthetic: reference dam-break lattice (Scenario/build_dam_break), hydrostatic rho",
         "config": workload_config(cfg_name, sc, system, args.n_subdiv, world),
-        "build": {"pi_block": sim.pi_block, "pi_kernel": sim.pi_kernel,
-                  "pi_lane_use": round(sim.pi_lane_use(), 4),
-                  "cuda_graph": use_graph},
+        "build": build_info,
         "interactions_per_s": true_pairs * world * args.steps / (total_ms * 1e-3),
         "pair_evals_per_s": evals * world * args.steps / (total_ms * 1e-3),
         "stage_ms": {"nl": float(np.mean(nl_ms)), "pi": pi_mean, "su": float(np.mean(su_ms))},
@@ -755,6 +825,10 @@ def main():
                                "sphb_state_from_soa -> sphb_* step -> sphb_state_to_soa -> D2H, "
                                f"round trip pipelined in {args.e2e_chunks} row chunks over "
                                "full-duplex PCIe (H2D of step k+1 chunk c after D2H of step k chunk c)"}
+    if collapsed is not None:
+        line["collapsed"] = collapsed
+    if fp64 is not None:
+        line["fp64"] = fp64
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         if system.n <= FULL_NL_SU_MAX:  # ~3 whole reference steps (C3: ~15-20 s of CPU work)
             cb = cpu_steps(system, prm, args.n_subdiv, 1, 2)

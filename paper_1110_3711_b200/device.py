@@ -321,7 +321,12 @@ class DeviceSim:
         self._graph.replay()
 
     def launches_per_step(self) -> int:
-        return int(_lib.lib().sphb_step_launch_count(_lib.ref(self.grid), self.n))
+        k = int(_lib.lib().sphb_step_launch_count(_lib.ref(self.grid), self.n))
+        if self.pi_kernel == "symmetric" and int(self.prm.precision) == _lib.SPHB_FP32:
+            k += 1  # k_dt_f32 after the scatter
+        if int(self.prm.counters) == _lib.SPHB_COUNTERS_SYMMETRIC:
+            k += 2  # k_sym_cand, k_sym_final
+        return k
 
     # ------------------------------------------------------------------ diagnostics
     def energy(self) -> dict:
