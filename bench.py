@@ -24,11 +24,13 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
-# rank 0's stdout carries exactly one JSON line: NCCL's own messages go to stderr
-# (the image's NCCL_DEBUG=VERSION prints a version banner on stdout; an explicit INFO/WARN/TRACE
-# setting is respected)
+# rank 0's stdout carries exactly one JSON line: NCCL's own messages go to stderr.  The
+# image's NCCL_DEBUG=VERSION prints a banner on stdout; instead NCCL logs at INFO for the INIT
+# subsystem only (communicator set-up: nRanks, NVLS / P2P transport, channels), to stderr, so the
+# rank count and transport of a multi-GPU run can be checked.  An explicit setting is respected.
 if os.environ.get("NCCL_DEBUG", "VERSION").upper() == "VERSION":
-    os.environ["NCCL_DEBUG"] = "WARN"
+    os.environ["NCCL_DEBUG"] = "INFO"
+    os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
 os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
 
 METRIC = "particle-steps/sec and interactions/sec at 1/2/4/8 B200 vs host-CPU ref; % HBM roofline"
@@ -51,7 +53,7 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=20)
     ap.add_argument("--graph", default="auto", choices=["auto", "on", "off"],
                     help="replay the timed steps as one CUDA graph (auto: below 2M particles)")
-    ap.add_argument("--pi-block", default="auto", choices=["auto", "128", "256", "384"],
+    ap.add_argument("--pi-block", default="auto", choices=["auto", "128", "256", "384", "512"],
                     help="targets per interaction block (auto: sim.initial_pi_block)")
     ap.add_argument("--pi-kernel", default="gather", choices=["gather", "symmetric"],
                     help="FP32 interaction kernel: one-sided gather or symmetric pair evaluation")

@@ -90,6 +90,9 @@ int launch_interact(sphb_workspace* ws, const sphb_params_t& p, const sphb_grid_
   else if (ws->pi_block == 256 && f32)
     rc = pi256::launch_interact(ws, p, g, n, nb, posp, velr, aux, cell_sorted, beg, end, acc, drho,
                                 visc, ctrl, s);
+  else if (ws->pi_block == 512 && f32)
+    rc = pi512::launch_interact(ws, p, g, n, nb, posp, velr, aux, cell_sorted, beg, end, acc, drho,
+                                visc, ctrl, s);
   else if (ws->pi_block == PI_LARGE_BLOCK && f32)
     rc = pi384::launch_interact(ws, p, g, n, nb, posp, velr, aux, cell_sorted, beg, end, acc, drho,
                                 visc, ctrl, s);
@@ -208,8 +211,8 @@ int sphb_workspace_set_mover_cap(sphb_workspace_t* ws, int64_t cap) {
 
 int sphb_workspace_set_pi_block(sphb_workspace_t* ws, int32_t targets) {
   SPHB_NONNULL(ws);
-  if (targets != 128 && targets != 256 && targets != PI_LARGE_BLOCK)
-    return sphb_set_error(SPHB_E_INVALID, "interaction block must be 128, 256 or %d targets",
+  if (targets != 128 && targets != 256 && targets != PI_LARGE_BLOCK && targets != 512)
+    return sphb_set_error(SPHB_E_INVALID, "interaction block must be 128, 256, %d or 512 targets",
                           PI_LARGE_BLOCK);
   ws->pi_block = targets;
   return SPHB_OK;

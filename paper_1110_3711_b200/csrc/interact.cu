@@ -2176,7 +2176,8 @@ int launch_interact(sphb_workspace* ws, const sphb_params_t& p, const sphb_grid_
   const size_t sm_blocks = sizeof(int32_t) * 2 * (size_t)(g.tx1 - g.tx0);
   if (sm_blocks > 48 * 1024) return sphb_set_error(SPHB_E_INVALID, "more than 6144 cell columns per slab");
   // bricks for h/2 cells (reach 2) in the FP32 gather kernel's cell order
-  const int brick = (g.reach == 2 && p.order == 0 && p.precision == SPHB_FP32 && !V8_SYM) ? 1 : 0;
+  // (the 512-target build cuts bricks at every reach: 2 x 2 rows x 2 lattice cells at n = 1)
+  const int brick = ((g.reach == 2 || BT == 512) && p.order == 0 && p.precision == SPHB_FP32 && !V8_SYM) ? 1 : 0;
   const int64_t nunits = brick ? (int64_t)((g.dims[1] + 1) / 2) * ((g.dims[2] + 1) / 2) : nrows;
   k_blocks<true><<<gb, 32, sm_blocks, s>>>(g, a.ncells, beg, end, ws->row_off, ws->blocks, ctrl, brick);
   if (int rc = sphb_check_launch("k_blocks count")) return rc;

@@ -86,7 +86,8 @@ constexpr int PI_LARGE_BLOCK = 384;
 SPHB_DECLARE_PI(pi128)
 SPHB_DECLARE_PI(pi256)
 SPHB_DECLARE_PI(pi384)
-SPHB_DECLARE_PI(pi384s)  // the symmetric build (K5s) of the 384-target blocking
+SPHB_DECLARE_PI(pi384s)
+SPHB_DECLARE_PI(pi512)   // 16-warp CTAs on 2 x 2-row bricks  // the symmetric build (K5s) of the 384-target blocking
 // the workspace's blocking (FP64 always pi128)
 int launch_interact(sphb_workspace* ws, const sphb_params_t& p, const sphb_grid_t& g, int64_t n, int64_t nb,
                     const float4* posp, const float4* velr, const float4* aux,

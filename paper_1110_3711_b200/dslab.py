@@ -467,8 +467,9 @@ class DeviceSlabSim:
             self.rebalance()
         for r in self.ranks:
             r.nl_pi()
+        # the step's dt is global (min over ranks) and needed now; the counters stay per rank in
+        # each rank's record ring and are summed over ranks only when read (records())
         self.comm.allreduce([r.dt_words() for r in self.ranks], "min")
-        self.comm.allreduce([r.counter_words() for r in self.ranks], "sum")
         for r in self.ranks:
             r.su_and_count()
         self._exchange()
@@ -480,8 +481,16 @@ class DeviceSlabSim:
 
     # -------------------------------------------------------------- readback
     def records(self, first, last):
+        """StepStats records [first, last): dt (the same on every rank) and the counters summed
+        over the ranks (one all-reduce per read instead of one per step)."""
+        words = _lib.REC_DTYPE.itemsize // 8
+        cnt = [r.rec.view(torch.int64).reshape(-1, words)[:, 1:].clone() for r in self.ranks]
+        self.comm.allreduce(cnt, "sum")
         r = self.ranks[0]
-        host = r.rec.cpu().numpy().view(_lib.REC_DTYPE)
+        host = r.rec.cpu().numpy().view(_lib.REC_DTYPE).copy()
+        summed = cnt[0].cpu().numpy().view(np.uint64)
+        for k, f in enumerate(("candidate_pairs", "hits_ordered", "force_evals", "ff_force_evals")):
+            host[f] = summed[:, k]
         return host[np.arange(first, last) % r.rec_cap]
 
     def ctrl_host(self):

@@ -26,14 +26,14 @@ class B200Engine:
     """Device gather engine; holds its device buffers across calls (resized on demand)."""
 
     def __init__(self, config: EngineConfig, pi_block="auto", pi_kernel="gather"):
-        """``pi_block``: targets per FP32 interaction block (128, 256, 384) or "auto", the
+        """``pi_block``: targets per FP32 interaction block (128, 256, 384, 512) or "auto", the
         production rule of run_simulation (sim.initial_pi_block of the frame's particle count
         and n_subdiv), so the engine path runs the same interaction build as the stepper.
         ``pi_kernel``: "gather" or "symmetric" (pair evaluation once per unordered pair, the
         reactions scattered, 384-target blocks; cell-order variants only)."""
         self.config = config.validated()
-        if pi_block not in (128, 256, 384, "auto"):
-            raise ValueError("pi_block must be 128, 256, 384 or 'auto'")
+        if pi_block not in (128, 256, 384, 512, "auto"):
+            raise ValueError("pi_block must be 128, 256, 384, 512 or 'auto'")
         if pi_kernel not in ("gather", "symmetric"):
             raise ValueError("pi_kernel must be 'gather' or 'symmetric'")
         self.pi_block = pi_block

@@ -170,7 +170,7 @@ def run_simulation(scenario_or_system, params, config: EngineConfig, max_steps: 
     bit-identically from such a checkpoint (``scenario_or_system`` may then be None; step
     numbers and the stop rules continue from the checkpoint's step).
 
-    ``pi_block``: targets per FP32 interaction block, 128, 256, 384 or "auto" (initial_pi_block of
+    ``pi_block``: targets per FP32 interaction block, 128, 256, 384, 512 or "auto" (initial_pi_block of
     the particle count; recorded in checkpoints so resumed runs keep the same blocking).
     ``pi_kernel``: "gather" or "symmetric" FP32 interaction (DeviceSim.set_pi_kernel); the
     symmetric kernel needs the cell traversal order (every config but fastcellshalf)."""
@@ -200,8 +200,8 @@ def run_simulation(scenario_or_system, params, config: EngineConfig, max_steps: 
         system = build_dam_break(scenario_or_system, params) if isinstance(scenario_or_system, Scenario) \
             else scenario_or_system
         sim = make_device_sim(system, params, cfg, max_steps, t_end, record_capacity=max(chunk, 1))
-    if pi_block not in (128, 256, 384, "auto"):
-        raise ValueError("pi_block must be 128, 256, 384 or 'auto'")
+    if pi_block not in (128, 256, 384, 512, "auto"):
+        raise ValueError("pi_block must be 128, 256, 384, 512 or 'auto'")
     adapt = pi_block == "auto" and cfg.precision == "fp32"
     if resume_from is None and (pi_block != "auto" or adapt):
         sim.set_pi_block(initial_pi_block(sim.n, params.n_subdiv) if adapt else int(pi_block))

@@ -176,7 +176,7 @@ def test_interact_fp32_within_tolerance(name, variant):
     out.stats.validate()
 
 
-@pytest.mark.parametrize("block", [128, 256, 384])
+@pytest.mark.parametrize("block", [128, 256, 384, 512])
 @pytest.mark.parametrize("name,variant", FRAMES)
 def test_interact_fp32_each_blocking_vs_reference(name, variant, block):
     """Every FP32 interaction build (pi128 / pi256 / pi384: 4-, 8-, 12-warp CTAs), selected
