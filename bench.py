@@ -55,8 +55,10 @@ def parse():
                     help="replay the timed steps as one CUDA graph (auto: below 2M particles)")
     ap.add_argument("--pi-block", default="auto", choices=["auto", "128", "256", "384", "512"],
                     help="targets per interaction block (auto: sim.initial_pi_block)")
-    ap.add_argument("--pi-kernel", default="gather", choices=["gather", "symmetric"],
-                    help="FP32 interaction kernel: one-sided gather or symmetric pair evaluation")
+    ap.add_argument("--pi-kernel", default="tuned", choices=["tuned", "gather", "symmetric", "paired"],
+                    help="FP32 interaction kernel: tuned (the faster of gather / paired, timed in the "
+                         "warm-up like run_simulation(pi_kernel='tuned')), one-sided gather, "
+                         "symmetric pair evaluation, or the gather with two targets per lane (paired)")
     ap.add_argument("--e2e-chunks", type=int, default=8,
                     help="row chunks of the pipelined H2D/D2H state round trip (1 = serial)")
     ap.add_argument("--collapsed-step", type=int, default=6000,
@@ -580,9 +582,15 @@ def main():
         sim.set_pi_block(initial_pi_block(sim.n, args.n_subdiv))
     elif args.pi_block != "auto":
         sim.set_pi_block(int(args.pi_block))
-    if args.pi_kernel == "symmetric" and prec == _lib.SPHB_FP32:
-        sim.set_pi_kernel("symmetric")
-    for _ in range(args.warmup):
+    tuned = args.pi_kernel == "tuned" and prec == _lib.SPHB_FP32 and args.pi_block == "auto"
+    cands = sim.pi_candidates(args.n_subdiv) if tuned else []
+    if args.pi_kernel not in ("gather", "tuned") and prec == _lib.SPHB_FP32:
+        sim.set_pi_kernel(args.pi_kernel)
+    warm = args.warmup
+    if tuned and warm >= len(cands):  # the first warm-up steps time each candidate build once
+        sim.tune_pi(cands)
+        warm -= len(cands)
+    for _ in range(warm):
         sim.launch_step()
     torch.cuda.synchronize()
     first = int(sim.ctrl_host()["step"])
@@ -621,7 +629,8 @@ def main():
     if err is not None:
         raise RuntimeError(f"divergence during bench: {err}")
     build_info = {"pi_block": sim.pi_block, "pi_kernel": sim.pi_kernel,
-                  "pi_lane_use": round(sim.pi_lane_use(), 4), "cuda_graph": use_graph}
+                  "pi_lane_use": round(sim.pi_lane_use(), 4), "cuda_graph": use_graph,
+                  "pi_policy": "tuned" if tuned else args.pi_kernel, "pi_tuning_ms": sim.tuning}
     recs = sim.records(first, first + args.steps)
     nl_ms = [e[0].elapsed_time(e[1]) for e in ev]
     pi_ms = [e[1].elapsed_time(e[2]) for e in ev]
@@ -768,11 +777,14 @@ def main():
             now = int(sim.ctrl_host()["step"])
             if sim.error() is not None:
                 raise RuntimeError(f"divergence while advancing: {sim.error()}")
+        if tuned:  # the measured selection again, in this state
+            sim.tune_pi(cands)
         ms_c, stage_c, recs_c = timed_steps(sim, args.steps, False)
         e_c = float(np.mean(recs_c["force_evals"].astype(np.float64)))
         c_c = float(np.mean(recs_c["candidate_pairs"].astype(np.float64)))
         collapsed = {"step": now, "value": system.n / (ms_c * 1e-3), "unit": UNIT, "ms_per_step": ms_c,
                      "stage_ms": stage_c, "pi_lane_use": round(sim.pi_lane_use(), 4),
+                     "pi_kernel": sim.pi_kernel, "pi_block": sim.pi_block, "pi_tuning_ms": sim.tuning,
                      "t_sim_s": float(sim.ctrl_host()["t_sim"]),
                      "interactions_per_s": e_c / 2 / (ms_c * 1e-3),
                      "pi_fp32_frac": (FLOP_PER_CAND * c_c + FLOP_PER_EVAL * e_c) / (stage_c["pi"] * 1e-3) / 1e12 / fp32,

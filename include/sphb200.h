@@ -103,7 +103,7 @@ typedef struct {
 enum { SPHB_KERNEL_CUBIC = 0, SPHB_KERNEL_WENDLAND = 1 };
 enum { SPHB_INT_VERLET = 0, SPHB_INT_SYMPLECTIC = 1 };
 enum { SPHB_COUNTERS_GATHER = 0, SPHB_COUNTERS_SYMMETRIC = 1 };
-enum { SPHB_PI_GATHER = 0, SPHB_PI_SYMMETRIC = 1 };
+enum { SPHB_PI_GATHER = 0, SPHB_PI_SYMMETRIC = 1, SPHB_PI_PAIRED = 2 };
 
 /* Device-resident control block (one per simulation, caller allocates 256 B). */
 typedef struct {
@@ -159,7 +159,10 @@ int sphb_workspace_set_pi_block(sphb_workspace_t* ws, int32_t targets);
  *                      forward half stencil (run_cells_symmetric, kernels.py:121-175), the
  *                      reaction scattered to the partner (eval_scatter, kernels.py:29-68) through
  *                      shared-memory rows flushed with vector reductions; 384-target blocks,
- *                      cell order (order 0) only; dt after the scatter (one extra pass).
+ *                      cell order (order 0) only; dt after the scatter (one extra pass);
+ *   SPHB_PI_PAIRED     the gather with two targets per lane (k_interact_v12): 8-warp CTAs on
+ *                      512-target bricks, one FIFO of the two targets' union of maybes, pair
+ *                      math packed across the two targets; gather semantics and K6 epilogue.
  * Hit sets and counters are identical; forces agree within the FP32 tolerance (summation
  * order).  Counters follow prm->counters either way. */
 int sphb_workspace_set_pi_kernel(sphb_workspace_t* ws, int32_t kernel);

@@ -18,7 +18,7 @@ CSRC = os.path.join(HERE, "csrc")
 SPHB_OK, SPHB_E_INVALID, SPHB_E_CUDA, SPHB_E_CAPACITY = 0, -1, -2, -3
 SPHB_DIV_LEFT_DOMAIN, SPHB_DIV_NONFINITE_FORCES, SPHB_DIV_NONFINITE_STATE = 1, 2, 3
 SPHB_COUNTERS_GATHER, SPHB_COUNTERS_SYMMETRIC = 0, 1
-SPHB_PI_GATHER, SPHB_PI_SYMMETRIC = 0, 1
+SPHB_PI_GATHER, SPHB_PI_SYMMETRIC, SPHB_PI_PAIRED = 0, 1, 2
 SPHB_FP32, SPHB_FP64 = 0, 1
 SPHB_KERNEL_CUBIC, SPHB_KERNEL_WENDLAND = 0, 1
 SPHB_INT_VERLET, SPHB_INT_SYMPLECTIC = 0, 1

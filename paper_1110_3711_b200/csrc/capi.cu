@@ -84,7 +84,10 @@ int launch_interact(sphb_workspace* ws, const sphb_params_t& p, const sphb_grid_
                     void* acc, void* drho, void* visc, sphb_ctrl_t* ctrl, cudaStream_t s) {
   int rc;
   const bool f32 = p.precision == SPHB_FP32;
-  if (ws->pi_kernel == SPHB_PI_SYMMETRIC && f32 && p.order == 0)
+  if (ws->pi_kernel == SPHB_PI_PAIRED && f32)
+    rc = pi512p::launch_interact(ws, p, g, n, nb, posp, velr, aux, cell_sorted, beg, end, acc, drho,
+                                 visc, ctrl, s);
+  else if (ws->pi_kernel == SPHB_PI_SYMMETRIC && f32 && p.order == 0)
     rc = pi384s::launch_interact(ws, p, g, n, nb, posp, velr, aux, cell_sorted, beg, end, acc, drho,
                                  visc, ctrl, s);
   else if (ws->pi_block == 256 && f32)
@@ -220,8 +223,9 @@ int sphb_workspace_set_pi_block(sphb_workspace_t* ws, int32_t targets) {
 
 int sphb_workspace_set_pi_kernel(sphb_workspace_t* ws, int32_t kernel) {
   SPHB_NONNULL(ws);
-  if (kernel != SPHB_PI_GATHER && kernel != SPHB_PI_SYMMETRIC)
-    return sphb_set_error(SPHB_E_INVALID, "interaction kernel must be SPHB_PI_GATHER or SPHB_PI_SYMMETRIC");
+  if (kernel != SPHB_PI_GATHER && kernel != SPHB_PI_SYMMETRIC && kernel != SPHB_PI_PAIRED)
+    return sphb_set_error(SPHB_E_INVALID,
+                          "interaction kernel must be SPHB_PI_GATHER, SPHB_PI_SYMMETRIC or SPHB_PI_PAIRED");
   ws->pi_kernel = kernel;
   return SPHB_OK;
 }

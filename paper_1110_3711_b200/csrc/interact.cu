@@ -46,7 +46,10 @@ namespace {
 #define SPHB_NW 4
 #endif
 constexpr int NW = SPHB_NW;      // warps per CTA (pi128: 4, two CTAs per SM; pi384: 12, one)
-constexpr int BT = NW * 32;      // targets per block
+#ifndef SPHB_PAIR
+#define SPHB_PAIR 0              // 1: two targets per lane (k_interact_v12, interact_pair.cuh)
+#endif
+constexpr int BT = NW * 32 * (SPHB_PAIR ? 2 : 1);  // targets per block
 #ifndef SPHB_H16
 #define SPHB_H16 1
 #endif
@@ -405,6 +408,12 @@ __device__ __forceinline__ bool screen(const KArgs& a, const C32&, const Own<dou
 // 6 x 6 rows x 16 cells) where 1-row blocks need ~31.  Record: (0, 0, 0, 0),
 // (row of (y0, z0), first cell x, last cell x, 1).  A column with more than BT targets falls
 // back to 1-row single-list chunks.
+// Paired build (two targets per lane): a lane's two targets must come from the same list, so
+// the fluid targets of a block take an even number of slots (padded) -- a block fits when
+// pad2(fluid) + boundary <= BT.
+__device__ __forceinline__ int block_slots(int nf, int ntot) {
+  return SPHB_PAIR ? ntot + (nf & 1) : ntot;
+}
 template <bool COUNT>
 __global__ void __launch_bounds__(32) k_blocks(sphb_grid_t g, int64_t ncells,
                                                const int32_t* __restrict__ beg,
@@ -426,14 +435,16 @@ __global__ void __launch_bounds__(32) k_blocks(sphb_grid_t g, int64_t ncells,
       int tot_all = 0;
       for (int k = lane; k < span; k += 32) {  // targets of the brick's cell column x
         const int x = g.tx0 + k;
-        int c = 0;
+        int c = 0, cf = 0;
         for (int sub = 0; sub < 4; ++sub) {
           const int yy = y0 + (sub & 1), zz = z0 + (sub >> 1);
           if (yy >= ny || zz >= nz) continue;
           const int64_t rb = (int64_t)nx * (yy + (int64_t)ny * zz) + x, rf = ncells + rb;
+          cf += end[rf] - beg[rf];
           c += (end[rf] - beg[rf]) + (end[rb] - beg[rb]);
         }
         s_ends[k] = c;
+        s_ends[span + k] = cf;  // fluid part (the paired build's slot padding)
         tot_all += c;
       }
       tot_all = __reduce_add_sync(SPHB_FULL, tot_all);
@@ -453,16 +464,16 @@ __global__ void __launch_bounds__(32) k_blocks(sphb_grid_t g, int64_t ncells,
           ++nrec;
         };
         const int key0 = y0 + ny * z0;
-        int tot = 0, xa = -1, xl = -1;
+        int tot = 0, totf = 0, xa = -1, xl = -1;
         for (int k = 0; k < span; ++k) {
-          const int x = g.tx0 + k, c = s_ends[k];
+          const int x = g.tx0 + k, c = s_ends[k], cf = s_ends[span + k];
           if (c == 0) continue;
-          if (tot + c > BT && tot > 0) {
+          if (block_slots(totf + cf, tot + c) > BT && tot > 0) {
             emit(make_int4(0, 0, 0, 0), make_int4(key0, xa, xl, 1));
-            tot = 0;
+            tot = totf = 0;
             xa = -1;
           }
-          if (c > BT) {  // oversized column: 1-row single-list chunks
+          if (block_slots(cf, c) > BT) {  // oversized column: 1-row single-list chunks
             for (int sub = 0; sub < 4; ++sub) {
               const int yy = y0 + (sub & 1), zz = z0 + (sub >> 1);
               if (yy >= ny || zz >= nz) continue;
@@ -479,6 +490,7 @@ __global__ void __launch_bounds__(32) k_blocks(sphb_grid_t g, int64_t ncells,
           if (xa < 0) xa = x;
           xl = x;
           tot += c;
+          totf += cf;
         }
         if (tot > 0) emit(make_int4(0, 0, 0, 0), make_int4(key0, xa, xl, 1));
         if (COUNT) row_off[r] = nrec;
@@ -516,13 +528,13 @@ __global__ void __launch_bounds__(32) k_blocks(sphb_grid_t g, int64_t ncells,
         const int x = g.tx0 + k;
         const int32_t fe = s_ends[k], be = s_ends[span + k];
         if (fe == fcur && be == bcur) continue;  // empty cell
-        if ((fe - f0) + (be - b0) > BT && (fcur > f0 || bcur > b0)) {  // close before this cell
+        if (block_slots(fe - f0, (fe - f0) + (be - b0)) > BT && (fcur > f0 || bcur > b0)) {  // close before this cell
           emit(make_int4(f0, fcur, b0, bcur), xa, xl);
           f0 = fcur;
           b0 = bcur;
           xa = -1;
         }
-        if ((fe - f0) + (be - b0) > BT) {  // one oversized cell: single-list chunks of <= BT
+        if (block_slots(fe - f0, (fe - f0) + (be - b0)) > BT) {  // one oversized cell: single-list chunks of <= BT
           for (int32_t p = f0; p < fe; p += BT) emit(make_int4(p, min(p + BT, fe), be, be), x, x);
           for (int32_t p = b0; p < be; p += BT) emit(make_int4(fe, fe, p, min(p + BT, be)), x, x);
           f0 = fe;
@@ -1894,6 +1906,8 @@ __global__ void __launch_bounds__(NW * 32, V8_MINB) k_interact_v8(KArgs a, K32 k
   }
 }
 
+#include "interact_pair.cuh"
+
 template <typename R>
 constexpr size_t smem_bytes() {
   return sizeof(float4) * Cfg<R>::NARR * Cfg<R>::SCAP + (Cfg<R>::H16 ? 6 * Cfg<R>::SCAP : 0) +
@@ -1934,8 +1948,30 @@ int launch_v8(const KArgs& a, const K32& k, int nsm, cudaStream_t s) {
   return sphb_check_launch("k_interact_v8");
 }
 
+#if SPHB_PAIR
+template <bool G7, bool EQM, bool WEND>
+int launch_v12(const KArgs& a, const K32& k, int nsm, cudaStream_t s) {
+  static bool init = false;
+  const size_t bytes = V8_SMEM;
+  if (!init) {
+    cudaError_t e = cudaFuncSetAttribute(k_interact_v12<G7, EQM, WEND>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (e != cudaSuccess)
+      return sphb_set_error(SPHB_E_CUDA, "smem attribute: %s", cudaGetErrorString(e));
+    init = true;
+  }
+  k_interact_v12<G7, EQM, WEND><<<nsm, NW * 32, bytes, s>>>(a, k);
+  return sphb_check_launch("k_interact_v12");
+}
+#endif
+
 template <bool WEND>
 int launch_v8_kernel(const KArgs& a, const K32& k, bool eqm, int nsm, cudaStream_t s) {
+#if SPHB_PAIR
+  if (a.gamma7)
+    return eqm ? launch_v12<true, true, WEND>(a, k, nsm, s) : launch_v12<true, false, WEND>(a, k, nsm, s);
+  return eqm ? launch_v12<false, true, WEND>(a, k, nsm, s) : launch_v12<false, false, WEND>(a, k, nsm, s);
+#endif
   if (a.gamma7)
     return eqm ? launch_v8<true, true, WEND>(a, k, nsm, s) : launch_v8<true, false, WEND>(a, k, nsm, s);
   return eqm ? launch_v8<false, true, WEND>(a, k, nsm, s) : launch_v8<false, false, WEND>(a, k, nsm, s);
@@ -2177,7 +2213,7 @@ int launch_interact(sphb_workspace* ws, const sphb_params_t& p, const sphb_grid_
   if (sm_blocks > 48 * 1024) return sphb_set_error(SPHB_E_INVALID, "more than 6144 cell columns per slab");
   // bricks for h/2 cells (reach 2) in the FP32 gather kernel's cell order
   // (the 512-target build cuts bricks at every reach: 2 x 2 rows x 2 lattice cells at n = 1)
-  const int brick = ((g.reach == 2 || BT == 512) && p.order == 0 && p.precision == SPHB_FP32 && !V8_SYM) ? 1 : 0;
+  const int brick = ((g.reach == 2 || BT == 512 || SPHB_PAIR) && p.order == 0 && p.precision == SPHB_FP32 && !V8_SYM) ? 1 : 0;
   const int64_t nunits = brick ? (int64_t)((g.dims[1] + 1) / 2) * ((g.dims[2] + 1) / 2) : nrows;
   k_blocks<true><<<gb, 32, sm_blocks, s>>>(g, a.ncells, beg, end, ws->row_off, ws->blocks, ctrl, brick);
   if (int rc = sphb_check_launch("k_blocks count")) return rc;

@@ -41,7 +41,7 @@ struct sphb_workspace {
   int4* mv_kv = nullptr;       // 2*ncells_max per-key (SB, MB, old begin, chain head)
   int64_t mover_cap_max = 0, mover_cap = 0;
   int32_t pi_block = 128;  // targets per interaction block: 128, 256 or 384 (pi128/256/384)
-  int32_t pi_kernel = 0;   // SPHB_PI_GATHER | SPHB_PI_SYMMETRIC (pi384s)
+  int32_t pi_kernel = 0;   // SPHB_PI_GATHER | SPHB_PI_SYMMETRIC (pi384s) | SPHB_PI_PAIRED (pi512p)
   unsigned long long* sym_scratch = nullptr;  // half-stencil candidate count (SPHB_COUNTERS_SYMMETRIC)
   size_t bytes = 0;
 };
@@ -87,7 +87,8 @@ SPHB_DECLARE_PI(pi128)
 SPHB_DECLARE_PI(pi256)
 SPHB_DECLARE_PI(pi384)
 SPHB_DECLARE_PI(pi384s)
-SPHB_DECLARE_PI(pi512)   // 16-warp CTAs on 2 x 2-row bricks  // the symmetric build (K5s) of the 384-target blocking
+SPHB_DECLARE_PI(pi512)   // 16-warp CTAs on 2 x 2-row bricks
+SPHB_DECLARE_PI(pi512p)  // 8-warp CTAs, two targets per lane, 512-target bricks (SPHB_PI_PAIRED)
 // the workspace's blocking (FP64 always pi128)
 int launch_interact(sphb_workspace* ws, const sphb_params_t& p, const sphb_grid_t& g, int64_t n, int64_t nb,
                     const float4* posp, const float4* velr, const float4* aux,

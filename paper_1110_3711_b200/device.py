@@ -158,18 +158,61 @@ class DeviceSim:
         self._graph_steps = 0
         self.pi_block = 128
         self.pi_kernel = "gather"
+        self.tuning = None  # the last tune_pi result
 
     def set_pi_kernel(self, kernel: str):
         """FP32 interaction kernel: "gather" (one-sided, K6 dt in its epilogue) or "symmetric"
         (each unordered pair once, reactions scattered: sphb_workspace_set_pi_kernel).  Drops a
         captured graph."""
-        code = {"gather": _lib.SPHB_PI_GATHER, "symmetric": _lib.SPHB_PI_SYMMETRIC}[kernel]
+        code = {"gather": _lib.SPHB_PI_GATHER, "symmetric": _lib.SPHB_PI_SYMMETRIC,
+                "paired": _lib.SPHB_PI_PAIRED}[kernel]
         self.ws.set_pi_kernel(code)
         self.pi_kernel = kernel
         if kernel == "symmetric":  # the symmetric build's blocking (pi384s)
             self.ws.set_pi_block(384)
             self.pi_block = 384
+        elif kernel == "paired":  # two targets per lane: 512-target bricks (pi512p)
+            self.ws.set_pi_block(512)
+            self.pi_block = 512
         self._graph = None
+
+    def select_pi(self, kernel: str, block: int):
+        """One FP32 interaction build: ``kernel`` ("gather", "symmetric", "paired") with the
+        gather kernel's ``block`` (the other two carry their own blocking)."""
+        self.set_pi_kernel(kernel)
+        if kernel == "gather":
+            self.set_pi_block(block)
+
+    def pi_candidates(self, n_subdiv: int = 1) -> list[tuple[str, int]]:
+        """The builds the "tuned" policy times against each other: the gather kernel with the
+        size rule's blocking (sim.initial_pi_block) and the paired kernel (two targets per lane,
+        512-target bricks).  At rest the paired build is the faster one; once cells fill unevenly
+        (a collapsed column) its bricks leave more lanes idle and the row blocks win."""
+        from .sim import initial_pi_block
+        return [("gather", initial_pi_block(self.n, n_subdiv)), ("paired", 512)]
+
+    def tune_pi(self, candidates, events=None) -> dict:
+        """Run one ordinary step with each candidate build (the state advances as usual), time
+        each step's PI stage with CUDA events and keep the fastest build.  ``events``: the
+        per-step event lists to record into (launch_step's layout), else fresh ones.  Returns
+        {"kernel/block": PI ms}."""
+        evs = events if events is not None else [
+            [torch.cuda.Event(enable_timing=True) for _ in range(self.n_stage_events())]
+            for _ in candidates]
+        for (kern, blk), ev in zip(candidates, evs):
+            self.select_pi(kern, blk)
+            self.launch_step(events=ev)
+        torch.cuda.synchronize()
+        return self.tune_choose(candidates, evs)
+
+    def tune_choose(self, candidates, events) -> dict:
+        """The selection half of tune_pi, for steps already launched with ``events`` (one per
+        candidate, in order) and completed."""
+        ms = [DeviceSim.stage_seconds(ev)[1] * 1e3 for ev in events]
+        best = int(np.argmin(ms))
+        self.select_pi(*candidates[best])
+        self.tuning = {f"{k}/{b}": round(t, 4) for (k, b), t in zip(candidates, ms)}
+        return self.tuning
 
     def set_pi_block(self, targets: int):
         """Targets per FP32 interaction block: 128 (4-warp CTAs, the default), 256 (8-warp CTAs)
@@ -369,8 +412,8 @@ class DeviceSim:
         sim.ctrl.copy_(torch.as_tensor(c).to(sim.device))
         if "pi_block" in z:  # the interaction blocking in use when the checkpoint was written
             sim.set_pi_block(int(z["pi_block"]))
-        if "pi_kernel" in z and str(z["pi_kernel"]) == "symmetric":
-            sim.set_pi_kernel("symmetric")
+        if "pi_kernel" in z and str(z["pi_kernel"]) in ("symmetric", "paired"):
+            sim.set_pi_kernel(str(z["pi_kernel"]))
         return sim
 
     # ------------------------------------------------------------------ readback

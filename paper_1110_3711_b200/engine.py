@@ -29,13 +29,14 @@ class B200Engine:
         """``pi_block``: targets per FP32 interaction block (128, 256, 384, 512) or "auto", the
         production rule of run_simulation (sim.initial_pi_block of the frame's particle count
         and n_subdiv), so the engine path runs the same interaction build as the stepper.
-        ``pi_kernel``: "gather" or "symmetric" (pair evaluation once per unordered pair, the
-        reactions scattered, 384-target blocks; cell-order variants only)."""
+        ``pi_kernel``: "gather", "symmetric" (pair evaluation once per unordered pair, the
+        reactions scattered, 384-target blocks; cell-order variants only) or "paired" (the
+        gather with two targets per lane on 512-target bricks)."""
         self.config = config.validated()
         if pi_block not in (128, 256, 384, 512, "auto"):
             raise ValueError("pi_block must be 128, 256, 384, 512 or 'auto'")
-        if pi_kernel not in ("gather", "symmetric"):
-            raise ValueError("pi_kernel must be 'gather' or 'symmetric'")
+        if pi_kernel not in ("gather", "symmetric", "paired"):
+            raise ValueError("pi_kernel must be 'gather', 'symmetric' or 'paired'")
         self.pi_block = pi_block
         self.pi_kernel = pi_kernel
         self.last_pi_block = None
@@ -111,11 +112,12 @@ class B200Engine:
             blk = initial_pi_block(n, params.n_subdiv)
         else:
             blk = int(self.pi_block)
-        sym = self.pi_kernel == "symmetric"
-        if sym:
-            blk = 384
+        kern = {"gather": _lib.SPHB_PI_GATHER, "symmetric": _lib.SPHB_PI_SYMMETRIC,
+                "paired": _lib.SPHB_PI_PAIRED}[self.pi_kernel]
+        if self.pi_kernel != "gather":  # the builds' own blockings (pi384s / pi512p)
+            blk = 384 if self.pi_kernel == "symmetric" else 512
         self._ws.set_pi_block(blk)
-        self._ws.set_pi_kernel(_lib.SPHB_PI_SYMMETRIC if sym else _lib.SPHB_PI_GATHER)
+        self._ws.set_pi_kernel(kern)
         self.last_pi_block = blk
         ctrl = new_ctrl(torch.device("cuda"))
         L, s = _lib.lib(), _stream()

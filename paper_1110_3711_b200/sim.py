@@ -157,7 +157,7 @@ def run_simulation(scenario_or_system, params, config: EngineConfig, max_steps: 
                    t_end: float | None = None, snapshot_every: int = 0, snapshot_sink=None,
                    stats_sink=None, *, chunk: int = 256, stage_timing: bool = True,
                    checkpoint_every: int = 0, checkpoint_path=None, resume_from=None,
-                   pi_block="auto", pi_kernel="gather"):
+                   pi_block="auto", pi_kernel="gather", retune_every: int = 500):
     """NL -> PI -> SU loop on the B200.  Returns (system, stats_list) like sim.py:272-352;
     raises DivergenceError on the first out-of-domain particle or non-finite state.
 
@@ -172,8 +172,14 @@ def run_simulation(scenario_or_system, params, config: EngineConfig, max_steps: 
 
     ``pi_block``: targets per FP32 interaction block, 128, 256, 384, 512 or "auto" (initial_pi_block of
     the particle count; recorded in checkpoints so resumed runs keep the same blocking).
-    ``pi_kernel``: "gather" or "symmetric" FP32 interaction (DeviceSim.set_pi_kernel); the
-    symmetric kernel needs the cell traversal order (every config but fastcellshalf)."""
+    ``pi_kernel``: "gather", "symmetric" or "paired" FP32 interaction (DeviceSim.set_pi_kernel);
+    the symmetric kernel needs the cell traversal order (every config but fastcellshalf).
+    "tuned": measured selection -- every ``retune_every`` steps the next steps run once with
+    each of DeviceSim.pi_candidates (the gather kernel on the size rule's blocking, the paired
+    kernel), their PI stages are timed with CUDA events and the fastest build runs until the
+    next tuning point (the tuning steps are ordinary steps of the run).  The choice follows
+    the timing, so FP32 results are reproducible to the FP32 tolerance, not bit for bit; the
+    other settings are deterministic."""
     if max_steps is None and t_end is None:
         raise ValueError("need max_steps or t_end")
     validate(params)
@@ -205,21 +211,35 @@ def run_simulation(scenario_or_system, params, config: EngineConfig, max_steps: 
     adapt = pi_block == "auto" and cfg.precision == "fp32"
     if resume_from is None and (pi_block != "auto" or adapt):
         sim.set_pi_block(initial_pi_block(sim.n, params.n_subdiv) if adapt else int(pi_block))
-    if pi_kernel not in ("gather", "symmetric"):
-        raise ValueError("pi_kernel must be 'gather' or 'symmetric'")
+    if pi_kernel not in ("gather", "symmetric", "paired", "tuned"):
+        raise ValueError("pi_kernel must be 'gather', 'symmetric', 'paired' or 'tuned'")
     if pi_kernel == "symmetric" and cfg.precision == "fp32" and cfg.device_order() == 0:
         sim.set_pi_kernel("symmetric")
+    if pi_kernel == "paired" and cfg.precision == "fp32":
+        sim.set_pi_kernel("paired")
+    tuned = pi_kernel == "tuned" and cfg.precision == "fp32"
+    cands = sim.pi_candidates(params.n_subdiv) if tuned else []
+    last_tune = None
     stats_out: list[StepStats] = []
     nbytes = NEIGHBOR_BYTES[cfg.derived_mode]
     done_steps = int(sim.ctrl_host()["step"])
     while True:
         # chunks end on multiples of ``chunk`` (snapshot / checkpoint steps), also after a
-        # resume from a step that is not one
+        # resume from a step that is not one; a tuning chunk is one step per candidate build
         this = chunk - done_steps % chunk
-        timer = _Timer(this, sim.n_stage_events()) if stage_timing else None
+        tune_now = tuned and (last_tune is None or done_steps - last_tune >= int(retune_every)) \
+            and this >= len(cands)  # (else at the next chunk)
+        if tune_now:
+            this = len(cands)
+        timer = _Timer(this, sim.n_stage_events()) if (stage_timing or tune_now) else None
         for k in range(this):
+            if tune_now:
+                sim.select_pi(*cands[k])
             sim.launch_step(events=timer.ev[k] if timer else None)
         c = sim.ctrl_host()  # synchronises
+        if tune_now:
+            sim.tune_choose(cands, timer.ev)
+            last_tune = done_steps
         now = int(c["step"])
         recs = sim.records(done_steps, now)
         for k, r in enumerate(recs):
@@ -228,7 +248,7 @@ def run_simulation(scenario_or_system, params, config: EngineConfig, max_steps: 
                            true_pairs=int(r["hits_ordered"]) // 2,
                            force_evals=int(r["force_evals"]), ff_force_evals=int(r["ff_force_evals"]),
                            engine_tag=cfg.tag, neighbor_bytes=nbytes)
-            if timer is not None:
+            if stage_timing:
                 st.stage_nl_s, st.stage_pi_s, st.stage_su_s, st.wall_seconds = \
                     DeviceSim.stage_seconds(timer.ev[k])
             step_no = done_steps + k + 1

@@ -26,10 +26,10 @@ torch.cuda.synchronize()
 mine = sim.gather_host()
 parts = [None] * dist.get_world_size()
 dist.gather_object(mine, parts if dist.get_rank() == 0 else None, dst=0)
+recs = sim.records(0, steps)  # collective: the counters are summed over the ranks here
 if dist.get_rank() == 0:
     pos, vel, rho, ids, fl = (np.concatenate([p[k] for p in parts]) for k in range(5))
     o = np.argsort(ids)
-    recs = sim.records(0, steps)
     np.savez(out, pos=pos[o], vel=vel[o], rho=rho[o], id=ids[o], fl=fl[o], dt=recs["dt"],
              cand=recs["candidate_pairs"], hits=recs["hits_ordered"], evals=recs["force_evals"],
              ff=recs["ff_force_evals"], bounds=np.array(sim.bounds))

@@ -196,6 +196,24 @@ def test_interact_fp32_each_blocking_vs_reference(name, variant, block):
             out.stats.ff_force_evals] == list(z[f"{variant}_counters"])
 
 
+@pytest.mark.parametrize("name,variant", FRAMES)
+def test_paired_kernel_vs_reference(name, variant):
+    """The FP32 gather with two targets per lane (k_interact_v12, 512-target bricks; row blocks
+    for the ranges order) against the reference's own gather output on every golden frame
+    (n1 / n2, all three variants): forces within 1e-5, counters bit-exact."""
+    z = golden(name)
+    system, derived, grid, cindex, prm = frame_objects(z)
+    eng = sph.make_engine(gather_cfg(variant, "fp32"), pi_kernel="paired")
+    out = eng.compute(system, derived, grid, cindex, prm, ranges=object())
+    assert eng.last_pi_block == 512
+    nb = system.count_boundary
+    assert np.all(out.accel[:nb] == 0.0)
+    for a, f in ((out.accel, "accel"), (out.drho_dt, "drho"), (out.visc_dt, "visc")):
+        assert oracle.rel_linf(a, z[f"{variant}_{f}"]) <= FP32_TOL, f
+    assert [out.stats.candidate_pairs, out.stats.true_pairs, out.stats.force_evals,
+            out.stats.ff_force_evals] == list(z[f"{variant}_counters"])
+
+
 CELL_FRAMES = [(f, v) for f, v in FRAMES if v != "fastcellshalf"]
 
 
@@ -327,7 +345,7 @@ def test_run_simulation_fp32_one_step_and_short_trajectory():
 
 
 @pytest.mark.parametrize("pi_block,pi_kernel", [("auto", "gather"), (384, "gather"),
-                                               (384, "symmetric")])
+                                               (384, "symmetric"), ("auto", "paired")])
 def test_drift_1000_steps_fp32_vs_reference(pi_block, pi_kernel):
     """SURVEY.md §8(d) drift bar: E = KE + PE + IE; tolerances stated in DESIGN.md.  Run with
     the size rule's build (C1: pi256) and with the production 384-target build forced."""
@@ -553,7 +571,7 @@ def test_state_soa_round_trip():
     assert L.sphb_state_from_soa(-1, 1, *ptrs, 0, 0, 0, s) == _lib.SPHB_E_INVALID
 
 
-@pytest.mark.parametrize("block", [256, 384, "symmetric"])
+@pytest.mark.parametrize("block", [256, 384, "symmetric", "paired"])
 @pytest.mark.parametrize("name", ["c1", "c2"])
 def test_pi_block_matches_128(name, block):
     """The 256- and 384-target blockings (pi256 / pi384: 8- / 12-warp CTAs) gives the 128-target one's counters
@@ -563,16 +581,17 @@ def test_pi_block_matches_128(name, block):
     system = sph.build_dam_break(sc, prm)
     a = D.DeviceSim(system, prm, reach=1, precision=0)
     b = D.DeviceSim(system, prm, reach=1, precision=0)
-    if block == "symmetric":
-        b.set_pi_kernel("symmetric")
+    if block in ("symmetric", "paired"):
+        b.set_pi_kernel(block)
     else:
         b.set_pi_block(block)
     for step in range(4):
         a.launch_step()
         b.launch_step()
         ra, rb = a.records(step, step + 1), b.records(step, step + 1)
-        if block == "symmetric" and step > 0:
-            # the scattered reactions sum in another order: after one step positions differ in
+        if block in ("symmetric", "paired") and step > 0:
+            # the reactions (symmetric) / the pair sums (paired) add in another order: after one
+            # step positions differ in
             # the last bit, the lattice's pairs sitting exactly at r = 2h may flip and the two
             # runs are no longer the same state (same-frame parity: the C2 / C3 / collapsed
             # oracle tests and the golden frames)
@@ -585,6 +604,32 @@ def test_pi_block_matches_128(name, block):
             assert oracle.rel_linf(x.cpu().numpy(), y.cpu().numpy()) <= FP32_TOL
         assert abs(float(ra["dt"][0]) / float(rb["dt"][0]) - 1.0) <= 1e-6
     assert 0.0 < b.pi_lane_use() <= 1.0 and int(b.ctrl_host()["nblk"][0]) < int(a.ctrl_host()["nblk"][0])
+
+
+def test_run_simulation_tuned_policy():
+    """pi_kernel="tuned": tuning chunks run one step per candidate build (gather on the size
+    rule's blocking, paired), the faster build runs on; the run equals the gather run within
+    the FP32 tolerance (the first step's counters exactly: same state) and tunes at the start
+    and every ``retune_every`` steps."""
+    sc = sph.named_scenario("c2")
+    prm = sph.make_params(sc)
+    cfg = gather_cfg("slowcellsh", "fp32")
+    sa, sta = sph.run_simulation(sc, prm, cfg, max_steps=24, chunk=8, pi_kernel="gather")
+    sb, stb = sph.run_simulation(sc, prm, cfg, max_steps=24, chunk=8, pi_kernel="tuned",
+                                 retune_every=8)
+    assert len(stb) == 24 and [s.step for s in stb] == list(range(24))
+    assert (sta[0].candidate_pairs, sta[0].true_pairs, sta[0].force_evals) == \
+        (stb[0].candidate_pairs, stb[0].true_pairs, stb[0].force_evals)
+    for a, b in zip(sta, stb):
+        assert abs(a.true_pairs - b.true_pairs) <= 1e-5 * a.true_pairs
+        assert abs(a.dt / b.dt - 1.0) <= 1e-4
+    oa, ob = np.argsort(sa.id), np.argsort(sb.id)
+    for f in ("pos", "vel", "rho"):
+        assert oracle.rel_linf(getattr(sb, f)[ob], getattr(sa, f)[oa]) <= 1e-4, f
+    sim = D.DeviceSim(sph.build_dam_break(sc, prm), prm, reach=1, precision=0)
+    t = sim.tune_pi(sim.pi_candidates(1))
+    assert set(t) == {"gather/384", "paired/512"} and all(v > 0 for v in t.values())
+    assert (sim.pi_kernel, sim.pi_block) in (("gather", 384), ("paired", 512))
 
 
 def test_run_simulation_auto_blocking_follows_the_size_rule():
@@ -696,7 +741,8 @@ def cell_dims(prm):
 
 
 @pytest.mark.slow
-@pytest.mark.parametrize("n_subdiv,block", [(1, 128), (1, 256), (1, 384), (2, 128), (2, 384)])
+@pytest.mark.parametrize("n_subdiv,block", [(1, 128), (1, 256), (1, 384), (1, "paired"), (2, 128),
+                                            (2, 384), (2, "paired")])
 def test_c2_each_blocking_vs_oracle(c2_frames, n_subdiv, block):
     """C2 (1,142,622 particles) through the engine with each FP32 build forced: counters
     bit-exact and forces within 1e-5 of the oracle gather (bit-exact to the reference).  At
@@ -705,9 +751,10 @@ def test_c2_each_blocking_vs_oracle(c2_frames, n_subdiv, block):
     system, prm, ss, der, nl, (cell, perm, cidx, ref) = c2_frames(n_subdiv)
     assert np.array_equal(nl["sort_perm"], perm)
     variant = "slowcellsh" if n_subdiv == 1 else "slowcellshalf"
-    eng = sph.make_engine(gather_cfg(variant, "fp32"), pi_block=block)
+    eng = sph.make_engine(gather_cfg(variant, "fp32"), pi_block=512 if block == "paired" else block,
+                          pi_kernel="paired" if block == "paired" else "gather")
     out = eng.compute(ss, der, types.SimpleNamespace(cell_of=nl["cell_of"]), None, prm)
-    assert eng.last_pi_block == block
+    assert eng.last_pi_block == (512 if block == "paired" else block)
     _check_vs_oracle(out, ref)
 
 
@@ -726,9 +773,10 @@ def test_c3_10m_production_build_vs_oracle():
     out = eng.compute(ss, der, types.SimpleNamespace(cell_of=nl["cell_of"]), None, prm)
     assert eng.last_pi_block == 384
     _check_vs_oracle(out, ref)
-    out = sph.make_engine(gather_cfg("slowcellsh", "fp32"), pi_kernel="symmetric").compute(
-        ss, der, types.SimpleNamespace(cell_of=nl["cell_of"]), None, prm)
-    _check_vs_oracle(out, ref)
+    for kern in ("symmetric", "paired"):
+        out = sph.make_engine(gather_cfg("slowcellsh", "fp32"), pi_kernel=kern).compute(
+            ss, der, types.SimpleNamespace(cell_of=nl["cell_of"]), None, prm)
+        _check_vs_oracle(out, ref)
 
 
 @pytest.mark.slow
@@ -752,8 +800,9 @@ def test_collapsed_c2_production_build_vs_fp64():
         eng = sph.make_engine(cfg, pi_block=block)
         out = eng.compute(ss, der, grid, None, prm)
         _check_vs_oracle(out, ref)
-    out = sph.make_engine(cfg, pi_kernel="symmetric").compute(ss, der, grid, None, prm)
-    _check_vs_oracle(out, ref)
+    for kern in ("symmetric", "paired"):
+        out = sph.make_engine(cfg, pi_kernel=kern).compute(ss, der, grid, None, prm)
+        _check_vs_oracle(out, ref)
 
 
 @pytest.mark.slow
