@@ -52,6 +52,8 @@ enum {
   SPHB_DIV_LEFT_DOMAIN = 1,
   SPHB_DIV_NONFINITE_FORCES = 2,
   SPHB_DIV_NONFINITE_STATE = 3,
+  SPHB_DIV_SLAB_MARGIN = 4, /* X slabs only: a particle moved more than one cell column in one
+                               step, beyond the edge bands the neighbours exchange */
 };
 
 enum { SPHB_FP32 = 0, SPHB_FP64 = 1 };
@@ -356,6 +358,38 @@ int sphb_slab_scatter(const sphb_grid_t* grid, int64_t n, int64_t nb, const uint
  * step needs no K1, only sphb_cell_hist on those keys. */
 int sphb_slab_unpack(const void* buf, int64_t r0, int64_t cnt, int64_t dst, void* nposp,
                      void* nvelr, void* nprev, int64_t* nid, uint32_t* nkeys, sphb_stream_t s);
+
+/* ---- X-slab edge bands: the per-step exchange with rows kept in place (dslab.DeviceSlabSim).
+ * A slab grid (tx0 > 0 or tx1 < dims[0]) sorts with one extra bin after the two lists, so its
+ * begin/end tables hold 2 ncells + 1 entries: rows that left the slab and last step's halo
+ * copies get the dead key from sphb_integrate and sort to the tail; the live rows are the
+ * first end[2 ncells - 1].  Per step, after NL: sphb_band_count sizes the edge bands (the
+ * `width` = reach + 1 edge columns on each side with a neighbour, `sides` bit 0 left, bit 1
+ * right) and writes info[8] = {live rows, boundary rows, band rows left, band rows right,
+ * error word, active, step, 0} (device; the host reads it while the interaction runs).
+ * After the edge targets' interaction, sphb_band_pack writes each band row's sorted state and
+ * forces (SPHB_BAND_ROW_BYTES each) into the side's send buffer; they travel while the
+ * interior targets run.  The receiver's sphb_band_integrate applies the step's update with
+ * sphb_integrate's arithmetic and dt to a received buffer, appends the rows at [dst, dst +
+ * cnt) and classifies them by their new column: inside the slab -> owned (migrants), within
+ * reach columns outside -> halo copies (id' = -1 - id), else dead.  sphb_slab_tail then sets
+ * the dead bin's end to the next step's row count.  scratch holds
+ * sphb_band_scratch_words(grid) int32 (device). */
+#define SPHB_BAND_ROW_BYTES 96
+int64_t sphb_band_scratch_words(const sphb_grid_t* grid);
+int sphb_band_count(const sphb_grid_t* grid, int32_t width, int32_t sides, const int32_t* beg,
+                    const int32_t* end, int32_t* scratch, int64_t* info, const sphb_ctrl_t* ctrl,
+                    sphb_stream_t s);
+int sphb_band_pack(const sphb_params_t* prm, const sphb_grid_t* grid, int32_t width,
+                   int32_t sides, const int32_t* beg, const int32_t* end, const int32_t* scratch,
+                   const void* posp_s, const void* velr_s, const void* prev_s,
+                   const int64_t* id_s, const void* acc, const void* drho, void* send_l,
+                   void* send_r, sphb_stream_t s);
+int sphb_band_integrate(sphb_workspace_t* ws, const sphb_params_t* prm, const sphb_grid_t* grid,
+                        const void* buf, int64_t cnt, int64_t dst, void* posp, void* velr,
+                        void* prev, int64_t* id, uint32_t* keys_next, uint32_t* keys_sorted,
+                        sphb_ctrl_t* ctrl, sphb_stream_t s);
+int sphb_slab_tail(const sphb_grid_t* grid, int32_t* end, int64_t n_next, sphb_stream_t s);
 
 /* Closes the step: dt/counters into rec[step % rec_capacity], t_sim += dt, step += 1. */
 int sphb_step_end(sphb_ctrl_t* ctrl, const sphb_params_t* prm, sphb_step_record_t* rec,

@@ -123,14 +123,14 @@ int sphb_workspace_create(int64_t n_max, int64_t ncells_max, sphb_workspace_t** 
   ws->ncells_max = ncells_max;
   const int64_t n1 = n_max > 0 ? n_max : 1;
   ws->max_sort_tiles = (n1 + SORT_TILE - 1) / SORT_TILE;
-  ws->max_scan_tiles = (2 * ncells_max + SCAN_TILE - 1) / SCAN_TILE;
+  ws->max_scan_tiles = (2 * ncells_max + 1 + SCAN_TILE - 1) / SCAN_TILE;  // + an X slab's dead bin
   size_t bytes = 0;
   auto alloc = [&](void** p, size_t b) -> cudaError_t {
     bytes += b;
     return cudaMalloc(p, b);
   };
   cudaError_t e = cudaSuccess;
-  if (e == cudaSuccess) e = alloc((void**)&ws->cnt, sizeof(uint32_t) * 2 * ncells_max);
+  if (e == cudaSuccess) e = alloc((void**)&ws->cnt, sizeof(uint32_t) * (2 * ncells_max + 1));
   for (int k = 0; k < 2 && e == cudaSuccess; ++k) {
     e = alloc((void**)&ws->keys_tmp[k], sizeof(uint32_t) * n1);
     if (e == cudaSuccess) e = alloc((void**)&ws->vals_tmp[k], sizeof(int32_t) * n1);
@@ -152,18 +152,18 @@ int sphb_workspace_create(int64_t n_max, int64_t ncells_max, sphb_workspace_t** 
     ws->mover_cap_max = n1 < MOVER_CAP_MAX ? n1 : MOVER_CAP_MAX;
     ws->mover_cap = ws->mover_cap_max;
     const size_t mc = (size_t)ws->mover_cap_max;
-    if (e == cudaSuccess) e = alloc((void**)&ws->mv_state, sizeof(uint32_t) * 4);
+    if (e == cudaSuccess) e = alloc((void**)&ws->mv_state, sizeof(uint32_t) * 8);
     if (e == cudaSuccess) e = alloc((void**)&ws->mv_bits, sizeof(uint32_t) * words);
     if (e == cudaSuccess) e = alloc((void**)&ws->mv_wpre, sizeof(uint32_t) * words);
     if (e == cudaSuccess) e = alloc((void**)&ws->mv_tile, sizeof(uint32_t) * (words / 32 + 1));
     if (e == cudaSuccess) e = alloc((void**)&ws->mv_pos, sizeof(int32_t) * mc);
     if (e == cudaSuccess) e = alloc((void**)&ws->mv_next, sizeof(int32_t) * mc);
-    if (e == cudaSuccess) e = alloc((void**)&ws->mv_head, sizeof(int32_t) * 2 * ncells_max);
-    if (e == cudaSuccess) e = alloc((void**)&ws->mv_kv, sizeof(int4) * 2 * ncells_max);
-    if (e == cudaSuccess) e = cudaMemset(ws->mv_state, 0, sizeof(uint32_t) * 4);
-    if (e == cudaSuccess) e = cudaMemset(ws->mv_head, 0xff, sizeof(int32_t) * 2 * ncells_max);
+    if (e == cudaSuccess) e = alloc((void**)&ws->mv_head, sizeof(int32_t) * (2 * ncells_max + 1));
+    if (e == cudaSuccess) e = alloc((void**)&ws->mv_kv, sizeof(int4) * (2 * ncells_max + 1));
+    if (e == cudaSuccess) e = cudaMemset(ws->mv_state, 0, sizeof(uint32_t) * 8);
+    if (e == cudaSuccess) e = cudaMemset(ws->mv_head, 0xff, sizeof(int32_t) * (2 * ncells_max + 1));
   }
-  if (e == cudaSuccess) e = cudaMemset(ws->cnt, 0, sizeof(uint32_t) * 2 * ncells_max);
+  if (e == cudaSuccess) e = cudaMemset(ws->cnt, 0, sizeof(uint32_t) * (2 * ncells_max + 1));
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
   ws->bytes = bytes;
   if (e != cudaSuccess) {
@@ -197,9 +197,9 @@ int sphb_workspace_destroy(sphb_workspace_t* ws) {
 
 int sphb_workspace_reset(sphb_workspace_t* ws, sphb_stream_t s) {
   SPHB_NONNULL(ws);
-  SPHB_CUDA(cudaMemsetAsync(ws->cnt, 0, sizeof(uint32_t) * 2 * ws->ncells_max, (cudaStream_t)s));
-  SPHB_CUDA(cudaMemsetAsync(ws->mv_state, 0, sizeof(uint32_t) * 4, (cudaStream_t)s));
-  SPHB_CUDA(cudaMemsetAsync(ws->mv_head, 0xff, sizeof(int32_t) * 2 * ws->ncells_max, (cudaStream_t)s));
+  SPHB_CUDA(cudaMemsetAsync(ws->cnt, 0, sizeof(uint32_t) * (2 * ws->ncells_max + 1), (cudaStream_t)s));
+  SPHB_CUDA(cudaMemsetAsync(ws->mv_state, 0, sizeof(uint32_t) * 8, (cudaStream_t)s));
+  SPHB_CUDA(cudaMemsetAsync(ws->mv_head, 0xff, sizeof(int32_t) * (2 * ws->ncells_max + 1), (cudaStream_t)s));
   return SPHB_OK;
 }
 
@@ -564,6 +564,71 @@ int sphb_slab_unpack(const void* buf, int64_t r0, int64_t cnt, int64_t dst, void
   }
   return launch_slab_unpack(buf, r0, cnt, dst, (float4*)nposp, (float4*)nvelr, (float4*)nprev, nid,
                             nkeys, (cudaStream_t)s);
+}
+
+int64_t sphb_band_scratch_words(const sphb_grid_t* grid) {
+  if (!grid || check_grid(grid)) return 0;
+  return band_scratch_words(*grid);
+}
+
+static int check_band(const sphb_grid_t* grid, int32_t width, int32_t sides) {
+  if (int rc = check_grid(grid)) return rc;
+  if (width < 1) return sphb_set_error(SPHB_E_INVALID, "band width must be >= 1");
+  if (sides < 0 || sides > 3) return sphb_set_error(SPHB_E_INVALID, "sides must be a 2-bit mask");
+  return SPHB_OK;
+}
+
+int sphb_band_count(const sphb_grid_t* grid, int32_t width, int32_t sides, const int32_t* beg,
+                    const int32_t* end, int32_t* scratch, int64_t* info, const sphb_ctrl_t* ctrl,
+                    sphb_stream_t s) {
+  if (int rc = check_band(grid, width, sides)) return rc;
+  SPHB_NONNULL(beg); SPHB_NONNULL(end); SPHB_NONNULL(scratch); SPHB_NONNULL(info);
+  SPHB_NONNULL(ctrl);
+  return launch_band_count(*grid, width, sides, beg, end, scratch, info, ctrl, (cudaStream_t)s);
+}
+
+int sphb_band_pack(const sphb_params_t* prm, const sphb_grid_t* grid, int32_t width,
+                   int32_t sides, const int32_t* beg, const int32_t* end, const int32_t* scratch,
+                   const void* posp_s, const void* velr_s, const void* prev_s,
+                   const int64_t* id_s, const void* acc, const void* drho, void* send_l,
+                   void* send_r, sphb_stream_t s) {
+  if (int rc = check_params(prm)) return rc;
+  if (int rc = check_band(grid, width, sides)) return rc;
+  SPHB_NONNULL(beg); SPHB_NONNULL(end); SPHB_NONNULL(scratch);
+  SPHB_NONNULL(posp_s); SPHB_NONNULL(velr_s); SPHB_NONNULL(prev_s); SPHB_NONNULL(id_s);
+  SPHB_NONNULL(acc);
+  if (prm->precision == SPHB_FP64) SPHB_NONNULL(drho);
+  if (sides & 1) SPHB_NONNULL(send_l);
+  if (sides & 2) SPHB_NONNULL(send_r);
+  return launch_band_pack(*prm, *grid, width, sides, beg, end, scratch, (const float4*)posp_s,
+                          (const float4*)velr_s, (const float4*)prev_s, id_s, acc, drho, send_l,
+                          send_r, (cudaStream_t)s);
+}
+
+int sphb_band_integrate(sphb_workspace_t* ws, const sphb_params_t* prm, const sphb_grid_t* grid,
+                        const void* buf, int64_t cnt, int64_t dst, void* posp, void* velr,
+                        void* prev, int64_t* id, uint32_t* keys_next, uint32_t* keys_sorted,
+                        sphb_ctrl_t* ctrl, sphb_stream_t s) {
+  SPHB_NONNULL(ws);
+  if (int rc = check_params(prm)) return rc;
+  if (int rc = check_grid(grid)) return rc;
+  SPHB_NONNULL(ctrl);
+  if (cnt < 0 || dst < 0) return sphb_set_error(SPHB_E_INVALID, "bad cnt/dst");
+  if (dst + cnt > ws->n_max) return sphb_set_error(SPHB_E_CAPACITY, "band rows exceed the workspace");
+  if (prm->integrator != SPHB_INT_VERLET)
+    return sphb_set_error(SPHB_E_INVALID, "X-slab bands integrate with the Verlet scheme only");
+  if (cnt == 0) return SPHB_OK;
+  SPHB_NONNULL(buf); SPHB_NONNULL(posp); SPHB_NONNULL(velr); SPHB_NONNULL(prev);
+  SPHB_NONNULL(id); SPHB_NONNULL(keys_next); SPHB_NONNULL(keys_sorted);
+  return launch_band_integrate(ws, *prm, *grid, buf, cnt, dst, (float4*)posp, (float4*)velr,
+                               (float4*)prev, id, keys_next, keys_sorted, ctrl, (cudaStream_t)s);
+}
+
+int sphb_slab_tail(const sphb_grid_t* grid, int32_t* end, int64_t n_next, sphb_stream_t s) {
+  if (int rc = check_grid(grid)) return rc;
+  SPHB_NONNULL(end);
+  if (n_next < 0 || n_next >= (int64_t(1) << 31)) return sphb_set_error(SPHB_E_INVALID, "bad n_next");
+  return launch_slab_tail(*grid, end, n_next, (cudaStream_t)s);
 }
 
 int sphb_state_from_soa(int64_t r0, int64_t cnt, const float* pos, const float* vel,

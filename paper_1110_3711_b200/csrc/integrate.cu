@@ -11,22 +11,13 @@
 // order, so the update is bit-identical to the reference for identical forces.
 #include "sphb_common.cuh"
 #include "sphb_internal.h"
+#include "su_row.cuh"
 
 using namespace sphb;
 
 namespace {
 
-__device__ __forceinline__ bool step_live(const sphb_ctrl_t* c) {
-  return c->active && c->err >= ((uint64_t)(c->step + 1) << 40);
-}
-
-__device__ __forceinline__ double step_dt(const sphb_ctrl_t* c, const sphb_params_t& p) {
-  const double dt_f = __longlong_as_double((long long)c->dtmin_f);
-  const double dt_cv = __longlong_as_double((long long)c->dtmin_cv);
-  double dt = xmul(p.cfl, fmin(dt_f, dt_cv));
-  dt = fmax(dt, p.dt_min);
-  return fmin(dt, p.dt_max);
-}
+__device__ __forceinline__ bool step_live(const sphb_ctrl_t* c) { return su_step_live(c); }
 
 __global__ void k_ctrl_init(sphb_ctrl_t* c, int64_t max_steps, double t_end) {
   c->step = 0;
@@ -60,20 +51,11 @@ __global__ void k_step_begin(sphb_ctrl_t* c) {
   c->nblk[0] = c->nblk[1] = 0;
 }
 
-// Piston law of the wave tank (extension): x(t) = x0 + S/2 (1 - cos wt),
-// v(t) = S/2 w sin wt, w = 2 pi / T, for boundary ids in [piston_id0, piston_id1).
-__device__ __forceinline__ void piston_at(const sphb_params_t& p, double t, float& x, float& vx) {
-  const double w = xdiv(2.0 * 3.141592653589793, p.piston_period);
-  const double hs = xmul(0.5, p.piston_stroke);
-  x = __double2float_rn(xadd(p.piston_x0, xmul(hs, xsub(1.0, cos(xmul(w, t))))));
-  vx = __double2float_rn(xmul(xmul(hs, w), sin(xmul(w, t))));
-}
-
 // MODE 0: verlet_update (sim.py:235-259), the reference.  MODE 1 / 2: symplectic predictor /
 // corrector (extension).  All fused with the next stage's assign_cells (K1) + histogram.
 // F32: the FP32 force layout (float4 (ax, ay, az, drho) per particle in `acc`, include/
 // sphb200.h), widened exactly to f64 -- the same arithmetic as the FP64 layout's values.
-template <int MODE, bool F32>
+template <int MODE, bool F32, bool SLAB>
 #ifndef SU_MINB
 #define SU_MINB 4  // 64 registers: 2x the resident warps of the default (memory-bound kernel)
 #endif
@@ -86,110 +68,68 @@ __global__ void __launch_bounds__(256, SU_MINB) k_integrate(
     uint32_t* __restrict__ keys_next, uint32_t* __restrict__ cnt, sphb_ctrl_t* ctrl) {
   if (!step_live(ctrl)) return;
   const int64_t step = ctrl->step;
-  const double dt = MODE == 2 ? ctrl->dt_stage : step_dt(ctrl, p);
-  const bool corrector = (step % p.verlet_stride) == 0;
-  const double c2 = xmul(xmul(0.5, dt), dt);
-  const double dt2 = xmul(2.0, dt);
-  const double hdt = xmul(0.5, dt);
-  const bool piston = p.piston_id1 > p.piston_id0;
-  // time the updated state belongs to (the piston law is evaluated there)
-  const double t_new = MODE == 1 ? xadd(ctrl->t_sim, hdt) : xadd(ctrl->t_sim, dt);
+  const SuStep st = su_step<MODE>(p, ctrl);
+  // X slab (dslab): last step's halo copies and rows that left the slab get the dead key (they
+  // sort to the tail and drop out); a row moving more than one column in one step would escape
+  // the neighbours' edge bands (slab.cu), which is flagged
+  constexpr bool slab = MODE == 0 && SLAB;  // the single-domain build carries none of it
+  const uint32_t dead = dead_key(cellbits);
   const int lane = threadIdx.x & 31;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n; base += stride) {
     const int64_t i = base + threadIdx.x;
     int64_t slot = -1;
     if (i < n) {
-      const float4 ps = posp_s[i], vs = velr_s[i], pv = prev_s[i];
-      double fa[3] = {0.0, 0.0, 0.0}, dr;
-      if (F32) {
-        const float4 a4 = ((const float4*)accv)[i];
-        fa[0] = a4.x;
-        fa[1] = a4.y;
-        fa[2] = a4.z;
-        dr = a4.w;
+      const int64_t pid = id_s[i];
+      if (slab && pid < 0) {  // a halo copy (its owner integrates the particle)
+        id[i] = pid;
+        keys_next[i] = dead;
+        slot = 2 * ncells;
       } else {
-        const double* acc = (const double*)accv;
-        dr = drho[i];
-        if (i >= nb) {
-          fa[0] = acc[3 * i + 0];
-          fa[1] = acc[3 * i + 1];
-          fa[2] = acc[3 * i + 2];
-        }
-      }
-      float4 np, nv, nprev;
-      double nrho;
-      if (MODE == 0)
-        nrho = corrector ? xadd((double)vs.w, xmul(dt, dr)) : xadd((double)pv.w, xmul(dt2, dr));
-      else if (MODE == 1)
-        nrho = xadd((double)vs.w, xmul(hdt, dr));
-      else
-        nrho = xadd((double)pv.w, xmul(dt, dr));
-      if (i >= nb) {
-        const double ax = xadd(fa[0], p.g[0]);
-        const double ay = xadd(fa[1], p.g[1]);
-        const double az = xadd(fa[2], p.g[2]);
-        const double vx = (double)vs.x, vy = (double)vs.y, vz = (double)vs.z;
-        if (MODE == 0) {
-          np.x = __double2float_rn(xadd(xadd((double)ps.x, xmul(dt, vx)), xmul(c2, ax)));
-          np.y = __double2float_rn(xadd(xadd((double)ps.y, xmul(dt, vy)), xmul(c2, ay)));
-          np.z = __double2float_rn(xadd(xadd((double)ps.z, xmul(dt, vz)), xmul(c2, az)));
-          if (corrector) {
-            nv.x = __double2float_rn(xadd(vx, xmul(dt, ax)));
-            nv.y = __double2float_rn(xadd(vy, xmul(dt, ay)));
-            nv.z = __double2float_rn(xadd(vz, xmul(dt, az)));
-          } else {
-            nv.x = __double2float_rn(xadd((double)pv.x, xmul(dt2, ax)));
-            nv.y = __double2float_rn(xadd((double)pv.y, xmul(dt2, ay)));
-            nv.z = __double2float_rn(xadd((double)pv.z, xmul(dt2, az)));
+        const float4 ps = posp_s[i], vs = velr_s[i], pv = prev_s[i];
+        double fa[3] = {0.0, 0.0, 0.0}, dr;
+        if (F32) {
+          const float4 a4 = ((const float4*)accv)[i];
+          fa[0] = a4.x;
+          fa[1] = a4.y;
+          fa[2] = a4.z;
+          dr = a4.w;
+        } else {
+          const double* acc = (const double*)accv;
+          dr = drho[i];
+          if (i >= nb) {
+            fa[0] = acc[3 * i + 0];
+            fa[1] = acc[3 * i + 1];
+            fa[2] = acc[3 * i + 2];
           }
-        } else if (MODE == 1) {  // r* = r + dt/2 v, v* = v + dt/2 (a + g)
-          np.x = __double2float_rn(xadd((double)ps.x, xmul(hdt, vx)));
-          np.y = __double2float_rn(xadd((double)ps.y, xmul(hdt, vy)));
-          np.z = __double2float_rn(xadd((double)ps.z, xmul(hdt, vz)));
-          nv.x = __double2float_rn(xadd(vx, xmul(hdt, ax)));
-          nv.y = __double2float_rn(xadd(vy, xmul(hdt, ay)));
-          nv.z = __double2float_rn(xadd(vz, xmul(hdt, az)));
-        } else {  // v' = v + dt (a* + g), r' = r* + dt/2 v'
-          const double ux = xadd((double)pv.x, xmul(dt, ax));
-          const double uy = xadd((double)pv.y, xmul(dt, ay));
-          const double uz = xadd((double)pv.z, xmul(dt, az));
-          nv.x = __double2float_rn(ux);
-          nv.y = __double2float_rn(uy);
-          nv.z = __double2float_rn(uz);
-          np.x = __double2float_rn(xadd((double)ps.x, xmul(hdt, (double)nv.x)));
-          np.y = __double2float_rn(xadd((double)ps.y, xmul(hdt, (double)nv.y)));
-          np.z = __double2float_rn(xadd((double)ps.z, xmul(hdt, (double)nv.z)));
         }
-      } else {
-        np.x = ps.x; np.y = ps.y; np.z = ps.z;  // boundary frozen (sim.py:256-258)
-        nv.x = vs.x; nv.y = vs.y; nv.z = vs.z;
-        if (piston) {
-          const int64_t pid = id_s[i];
-          if (pid >= p.piston_id0 && pid < p.piston_id1) piston_at(p, t_new, np.x, nv.x);
+        float4 np, nv, nprev;
+        su_row<MODE>(p, st, i >= nb, pid, ps, vs, pv, fa, dr, np, nv, nprev);
+        posp[i] = np;
+        velr[i] = nv;
+        prev[i] = nprev;
+        id[i] = pid;
+        if (!(isfinite(nv.x) && isfinite(nv.y) && isfinite(nv.z) && isfinite(nv.w)))
+          raise_div(ctrl, step, SPHB_DIV_NONFINITE_STATE, 0);
+        // next step's assign_cells (K1), fused
+        const int32_t c = cell_of(np.x, np.y, np.z, g);
+        if (c < 0) {
+          raise_div(ctrl, MODE == 1 ? step : step + 1, SPHB_DIV_LEFT_DOMAIN, (uint64_t)i);
+          keys_next[i] = 0xffffffffu;
+        } else {
+          const uint32_t list = i >= nb ? 1u : 0u;
+          keys_next[i] = (list << cellbits) | (uint32_t)c;
+          slot = (int64_t)list * ncells + c;
+          if (slab) {
+            const int col = c % g.dims[0], ocol = column_of(ps.x, g);
+            if (col - ocol > 1 || ocol - col > 1)
+              raise_div(ctrl, step + 1, SPHB_DIV_SLAB_MARGIN, (uint64_t)i);
+            if (col < g.tx0 || col >= g.tx1) {  // migrated: the neighbour integrated it too
+              keys_next[i] = dead;
+              slot = 2 * ncells;
+            }
+          }
         }
-      }
-      np.w = 0.f;  // press is recomputed by the next step's reorder (K3)
-      nv.w = __double2float_rn(nrho);
-      if (MODE == 2)
-        nprev = nv;
-      else
-        nprev = vs;  // history <- current (sim.py:254-255); symplectic: (v, rho) at t
-      posp[i] = np;
-      velr[i] = nv;
-      prev[i] = nprev;
-      id[i] = id_s[i];
-      if (!(isfinite(nv.x) && isfinite(nv.y) && isfinite(nv.z) && isfinite(nv.w)))
-        raise_div(ctrl, step, SPHB_DIV_NONFINITE_STATE, 0);
-      // next step's assign_cells (K1), fused
-      const int32_t c = cell_of(np.x, np.y, np.z, g);
-      if (c < 0) {
-        raise_div(ctrl, MODE == 1 ? step : step + 1, SPHB_DIV_LEFT_DOMAIN, (uint64_t)i);
-        keys_next[i] = 0xffffffffu;
-      } else {
-        const uint32_t list = i >= nb ? 1u : 0u;
-        keys_next[i] = (list << cellbits) | (uint32_t)c;
-        slot = (int64_t)list * ncells + c;
       }
     }
     const uint32_t peers = __match_any_sync(SPHB_FULL, (unsigned long long)slot);
@@ -313,16 +253,21 @@ int launch_integrate_mode(sphb_workspace* ws, const sphb_params_t& p, const sphb
     const int64_t nc = ncells_of(g);
     const double* dr = (const double*)drho;
     const bool f32 = p.precision == SPHB_FP32;
-#define SPHB_K7(M, F)                                                                              \
-  k_integrate<M, F><<<(unsigned)blocks, 256, 0, s>>>(p, g, cb, nc, n, nb, posp_s, velr_s, prev_s, \
-                                                     id_s, acc, dr, posp, velr, prev, id,         \
-                                                     keys_next, ws->cnt, ctrl)
+#define SPHB_K7(M, F, S)                                                                        \
+  k_integrate<M, F, S><<<(unsigned)blocks, 256, 0, s>>>(p, g, cb, nc, n, nb, posp_s, velr_s,    \
+                                                        prev_s, id_s, acc, dr, posp, velr, prev, \
+                                                        id, keys_next, ws->cnt, ctrl)
+    const bool slab = slab_grid(g);  // an X slab's dead-key rules (verlet only)
     if (mode == 0) {
-      if (f32) SPHB_K7(0, true); else SPHB_K7(0, false);
+      if (slab) {
+        if (f32) SPHB_K7(0, true, true); else SPHB_K7(0, false, true);
+      } else {
+        if (f32) SPHB_K7(0, true, false); else SPHB_K7(0, false, false);
+      }
     } else if (mode == 1) {
-      if (f32) SPHB_K7(1, true); else SPHB_K7(1, false);
+      if (f32) SPHB_K7(1, true, false); else SPHB_K7(1, false, false);
     } else {
-      if (f32) SPHB_K7(2, true); else SPHB_K7(2, false);
+      if (f32) SPHB_K7(2, true, false); else SPHB_K7(2, false, false);
     }
 #undef SPHB_K7
     if (int rc = sphb_check_launch("k_integrate")) return rc;

@@ -592,7 +592,10 @@ __global__ void __launch_bounds__(KB_SCAN) k_blocks_scan(int32_t* row_off, int64
     if (tid == KB_SCAN - 1) s_carry = carry + s_w[KB_SCAN / 32 - 1];
     __syncthreads();
   }
-  if (tid == 0) ctrl->nblk[0] = (uint32_t)s_carry;
+  if (tid == 0) {
+    ctrl->nblk[0] = (uint32_t)s_carry;
+    ctrl->tile_next[0] = 0u;  // this launch's block queue (several launches per step: X slabs)
+  }
 }
 
 // ------------------------------------------------------------------ the interaction kernel

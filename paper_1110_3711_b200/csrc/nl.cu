@@ -62,12 +62,12 @@ __global__ void __launch_bounds__(256) k_cell_keys(sphb_grid_t g, const float4* 
 
 // per-list per-cell histogram of known sort keys (key = list << cellbits | cell)
 __global__ void __launch_bounds__(256) k_hist_keys(const uint32_t* __restrict__ keys, int64_t n,
-                                                   int cellbits, int64_t ncells,
+                                                   int cellbits, int64_t ncells, bool slab,
                                                    uint32_t* __restrict__ cnt,
                                                    const sphb_ctrl_t* ctrl) {
   if (ctrl && !step_live(ctrl)) return;
   const int lane = threadIdx.x & 31;
-  const uint32_t cm = (1u << cellbits) - 1u;
+  const uint32_t cm = (1u << cellbits) - 1u, dead = dead_key(cellbits);
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n; base += stride) {
     const int64_t i = base + threadIdx.x;
@@ -75,6 +75,7 @@ __global__ void __launch_bounds__(256) k_hist_keys(const uint32_t* __restrict__ 
     if (i < n) {
       const uint32_t k = keys[i];
       if ((k >> cellbits) <= 1u && (k & cm) < (uint32_t)ncells) slot = (k >> cellbits) * ncells + (k & cm);
+      else if (slab && k == dead) slot = 2 * ncells;  // X slab: the dead bin
     }
     const uint32_t peers = __match_any_sync(SPHB_FULL, (unsigned long long)slot);
     if (slot >= 0 && lane == __ffs(peers) - 1) atomicAdd(&cnt[slot], (uint32_t)__popc(peers));
@@ -398,12 +399,13 @@ __global__ void __launch_bounds__(SCAN_BLOCK) k_scan_apply(uint32_t* __restrict_
 //   k_mv_scatter  perm / keys_sorted
 // The radix passes run instead (mode 1) unless the previous order is established (set by a
 // sort, cleared by K1 and the standalone sphb_sort), consistent, and movers <= cap.
-// state words: [0] order established, [1] inconsistency seen, [2] mode (0 movers, 1 radix), [3] m
+// state words: [0] order established, [1] inconsistency seen, [2] mode (0 movers, 1 radix), [3] m,
+// [4] the dead-bin placement counter (X slabs)
 constexpr int MV_BLOCK = 256, MV_ITEMS = 16, MV_TILE = MV_BLOCK * MV_ITEMS;  // 128 words per tile
 static_assert(MV_TILE == MV_TILE_ROWS, "workspace sizing");
 
 __device__ __forceinline__ uint32_t mv_index(uint32_t key, int cellbits, uint32_t ncells) {
-  return (key >> cellbits) * ncells + (key & ((1u << cellbits) - 1u));
+  return key_bin(key, cellbits, ncells);  // X slabs: the dead key -> the dead bin (2 ncells)
 }
 
 // Each thread checks 4 consecutive rows per round (one 16-B load of keys and of keys_sorted
@@ -416,7 +418,8 @@ __global__ void __launch_bounds__(MV_BLOCK) k_mv_flag(const uint32_t* __restrict
                                                       const int32_t* __restrict__ oend,
                                                       uint32_t* __restrict__ bits,
                                                       uint32_t* __restrict__ tile_cnt, bool vec,
-                                                      uint32_t* state, const sphb_ctrl_t* ctrl) {
+                                                      bool slab, uint32_t* state,
+                                                      const sphb_ctrl_t* ctrl) {
   if (!step_live(ctrl) || state[0] == 0u) return;
   __shared__ uint32_t s_cnt;
   if (threadIdx.x == 0) s_cnt = 0;
@@ -424,7 +427,10 @@ __global__ void __launch_bounds__(MV_BLOCK) k_mv_flag(const uint32_t* __restrict
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t t0 = (int64_t)blockIdx.x * MV_TILE;
   const uint32_t cm = (1u << cellbits) - 1u;
-  auto bad_key = [&](uint32_t k) { return (k >> cellbits) > 1u || (k & cm) >= ncells; };
+  const uint32_t dead = dead_key(cellbits);
+  auto bad_key = [&](uint32_t k) {
+    return k == dead ? !slab : ((k >> cellbits) > 1u || (k & cm) >= ncells);
+  };
   bool bad = false;
   uint32_t c = 0;
   constexpr int RROWS = 4 * MV_BLOCK;  // rows per round
@@ -460,7 +466,7 @@ __global__ void __launch_bounds__(MV_BLOCK) k_mv_flag(const uint32_t* __restrict
         continue;
       }
       const uint32_t left = j ? kp[j - 1] : kl, right = j < 3 ? kp[j + 1] : kr;
-      const uint32_t x = (kp[j] >> cellbits) * ncells + (kp[j] & cm);
+      const uint32_t x = key_bin(kp[j], cellbits, ncells);
       if (e == 0 || left != kp[j]) bad |= (e > 0 && left > kp[j]) || obeg[x] != (int32_t)e;
       if (e + 1 == n || right != kp[j]) bad |= oend[x] != (int32_t)(e + 1);
     }
@@ -498,6 +504,7 @@ __global__ void __launch_bounds__(1024) k_mv_scan(uint32_t* __restrict__ tile_cn
   }
   if (threadIdx.x == 0) {
     state[2] = (ordered && (int64_t)running <= cap) ? 0u : 1u;
+    state[4] = 0u;  // dead-bin placement counter of k_mv_scatter
     state[3] = ordered ? running : 0u;
     state[1] = 0u;
     state[0] = 1u;  // this step's sort (either path) establishes the order for the next one
@@ -550,7 +557,9 @@ __global__ void __launch_bounds__(MV_BLOCK) k_mv_compact(
       const uint32_t k = keys[i];
       const uint32_t x = mv_index(k, cellbits, ncells);
       mv_pos[j] = (int32_t)i;
-      mv_next[j] = atomicExch(&mv_head[x], j);
+      // an X slab's dead bin is placed by a counter (k_mv_scatter), not by chains: its rows
+      // are dropped, their order is irrelevant, and the bin can take many movers per step
+      mv_next[j] = x == 2u * ncells ? -1 : atomicExch(&mv_head[x], j);
       // a key absent from the previous order must have an empty old range (the run check of
       // k_mv_flag covers the keys present); otherwise fall back to the radix passes
       const int32_t ob = obeg[x];
@@ -566,7 +575,7 @@ __global__ void __launch_bounds__(256) k_mv_scatter(
     const uint32_t* __restrict__ bits, const uint32_t* __restrict__ wpre,
     const int4* __restrict__ kv, const int32_t* __restrict__ nbeg,
     const int32_t* __restrict__ mv_pos, const int32_t* __restrict__ mv_next,
-    const uint32_t* state, uint32_t* __restrict__ keys_sorted, int32_t* __restrict__ perm,
+    uint32_t* state, uint32_t* __restrict__ keys_sorted, int32_t* __restrict__ perm,
     const sphb_ctrl_t* ctrl) {
   if (!step_live(ctrl) || state[2] != 0u) return;
   const int lane = threadIdx.x & 31;
@@ -593,11 +602,14 @@ __global__ void __launch_bounds__(256) k_mv_scatter(
       const int64_t i = (cw << 7) + 32 * u + lane;
       if (i >= n) break;
       int64_t pos;
-      if (!((w[u] >> lane) & 1u))
+      if (x[u] == 2u * ncells)  // an X slab's dead rows (stayers and movers): any order
+        pos = nbeg[x[u]] + (int64_t)atomicAdd(&state[4], 1u);
+      else if (!((w[u] >> lane) & 1u))
         pos = (int64_t)c[u].x + i - (int64_t)(wp[u] + __popc(w[u] & ((1u << lane) - 1u)));
       else
         pos = i < c[u].z ? nbeg[x[u]] : c[u].y;
-      for (int32_t m = c[u].w; m >= 0; m = mv_next[m]) pos += mv_pos[m] < i;
+      if (x[u] != 2u * ncells)
+        for (int32_t m = c[u].w; m >= 0; m = mv_next[m]) pos += mv_pos[m] < i;
       perm[pos] = (int32_t)i;
       keys_sorted[pos] = k[u];
     }
@@ -640,7 +652,7 @@ int launch_cell_hist(sphb_workspace* ws, const sphb_grid_t& g, const uint32_t* k
   const int64_t nc = ncells_of(g);
   if (n > ws->n_max || nc > ws->ncells_max) return sphb_set_error(SPHB_E_CAPACITY, "n/ncells exceed workspace");
   if (n == 0) return SPHB_OK;
-  k_hist_keys<<<grid_for(n, 256), 256, 0, s>>>(keys, n, cellbits_of(g), nc, ws->cnt, ctrl);
+  k_hist_keys<<<grid_for(n, 256), 256, 0, s>>>(keys, n, cellbits_of(g), nc, slab_grid(g), ws->cnt, ctrl);
   return sphb_check_launch("k_hist_keys");
 }
 
@@ -693,7 +705,7 @@ int launch_sort_and_ranges(sphb_workspace* ws, const sphb_grid_t& g, const uint3
                            int32_t* end, const sphb_ctrl_t* ctrl, cudaStream_t s) {
   if (n > ws->n_max) return sphb_set_error(SPHB_E_CAPACITY, "n exceeds workspace");
   const int64_t nc = ncells_of(g);
-  const int64_t len = 2 * nc;
+  const int64_t len = nbins_of(g);  // both lists (+ an X slab's dead bin)
   const int64_t nscan = (len + SCAN_TILE - 1) / SCAN_TILE;
   if (nscan > ws->max_scan_tiles) return sphb_set_error(SPHB_E_CAPACITY, "ncells exceeds workspace");
   if (n == 0) return launch_cell_ranges(ws, g, beg, end, ctrl, s);
@@ -702,7 +714,7 @@ int launch_sort_and_ranges(sphb_workspace* ws, const sphb_grid_t& g, const uint3
   uint32_t* st = ws->mv_state;
   const bool vec = ((reinterpret_cast<uintptr_t>(keys) | reinterpret_cast<uintptr_t>(keys_sorted)) & 15u) == 0;
   k_mv_flag<<<(unsigned)tiles, MV_BLOCK, 0, s>>>(keys, keys_sorted, n, cb, (uint32_t)nc, beg, end,
-                                                 ws->mv_bits, ws->mv_tile, vec, st, ctrl);
+                                                 ws->mv_bits, ws->mv_tile, vec, slab_grid(g), st, ctrl);
   k_mv_scan<<<1, 1024, 0, s>>>(ws->mv_tile, tiles, ws->mover_cap, st, ctrl);
   k_mv_compact<<<(unsigned)tiles, MV_BLOCK, 0, s>>>(keys, cb, (uint32_t)nc, ws->mv_bits, ws->mv_tile,
                                                     ws->mv_wpre, ws->mv_pos,
@@ -737,7 +749,7 @@ int launch_reorder(const sphb_params_t& p, const sphb_grid_t& g, int64_t n, cons
 
 int launch_cell_ranges(sphb_workspace* ws, const sphb_grid_t& g, int32_t* beg, int32_t* end,
                        const sphb_ctrl_t* ctrl, cudaStream_t s) {
-  const int64_t len = 2 * ncells_of(g);
+  const int64_t len = nbins_of(g);
   const int64_t ntiles = (len + SCAN_TILE - 1) / SCAN_TILE;
   if (ntiles > ws->max_scan_tiles) return sphb_set_error(SPHB_E_CAPACITY, "ncells exceeds workspace");
   k_scan_reduce<<<(unsigned)ntiles, SCAN_BLOCK, 0, s>>>(ws->cnt, len, ws->scan_partials, ctrl);

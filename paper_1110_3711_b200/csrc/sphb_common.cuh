@@ -66,11 +66,32 @@ __host__ __device__ __forceinline__ int64_t ncells_of(const sphb_grid_t& g) {
   return (int64_t)g.dims[0] * g.dims[1] * g.dims[2];
 }
 
+// bits of the cell field of a sort key (list << cellbits | cell): 2^b > ncells, so the all-ones
+// cell field of list 1 is never a real cell (the X-slab dead key below)
 __host__ __device__ __forceinline__ int cellbits_of(const sphb_grid_t& g) {
   int64_t nc = ncells_of(g);
   int b = 1;
-  while ((int64_t(1) << b) < nc) ++b;
+  while ((int64_t(1) << b) <= nc) ++b;
   return b;
+}
+
+// ---------------------------------------------------------------- X-slab grids (dslab)
+// A grid whose interaction targets are a proper sub-range of columns is one rank's X slab.
+// Its sort has one extra bin after the two lists: rows that left the slab during the last
+// update and last step's halo copies carry the dead key, sort to the tail and drop out of
+// the next step (n_live = begin of the dead bin).  Single-domain grids have no dead bin.
+__host__ __device__ __forceinline__ bool slab_grid(const sphb_grid_t& g) {
+  return g.tx0 > 0 || g.tx1 < g.dims[0];
+}
+__host__ __device__ __forceinline__ uint32_t dead_key(int cellbits) { return (2u << cellbits) - 1u; }
+// per-key bins of the histogram / begin-end tables: both lists (+ the dead bin of a slab)
+__host__ __device__ __forceinline__ int64_t nbins_of(const sphb_grid_t& g) {
+  return 2 * ncells_of(g) + (slab_grid(g) ? 1 : 0);
+}
+// histogram / table index of a sort key; the dead key -> 2 ncells
+__host__ __device__ __forceinline__ uint32_t key_bin(uint32_t key, int cellbits, uint32_t ncells) {
+  return key == dead_key(cellbits) ? 2u * ncells
+                                   : (key >> cellbits) * ncells + (key & ((1u << cellbits) - 1u));
 }
 
 // ---------------------------------------------------------------- errors / ctrl

@@ -18,7 +18,7 @@ constexpr int64_t MOVER_CAP_MAX = 1 << 20;  // movers per step the movers-only s
 
 struct sphb_workspace {
   int64_t n_max = 0, ncells_max = 0;
-  uint32_t* cnt = nullptr;          // 2*ncells_max per-list histogram, kept zero between steps
+  uint32_t* cnt = nullptr;          // 2*ncells_max (+1: a slab's dead bin) per-key histogram, kept zero between steps
   uint32_t* keys_tmp[2] = {nullptr, nullptr};
   int32_t* vals_tmp[2] = {nullptr, nullptr};
   uint32_t* radix_hist = nullptr;   // RADIX * max tiles
@@ -37,8 +37,8 @@ struct sphb_workspace {
   uint32_t* mv_tile = nullptr;
   int32_t* mv_pos = nullptr;
   int32_t* mv_next = nullptr;
-  int32_t* mv_head = nullptr;  // 2*ncells_max, -1 between steps
-  int4* mv_kv = nullptr;       // 2*ncells_max per-key (SB, MB, old begin, chain head)
+  int32_t* mv_head = nullptr;  // 2*ncells_max + 1, -1 between steps
+  int4* mv_kv = nullptr;       // 2*ncells_max + 1 per-key (SB, MB, old begin, chain head)
   int64_t mover_cap_max = 0, mover_cap = 0;
   int32_t pi_block = 128;  // targets per interaction block: 128, 256 or 384 (pi128/256/384)
   int32_t pi_kernel = 0;   // SPHB_PI_GATHER | SPHB_PI_SYMMETRIC (pi384s) | SPHB_PI_PAIRED (pi512p)
@@ -130,6 +130,20 @@ int launch_slab_scatter(const sphb_grid_t& g, int64_t n, int64_t nb, const uint3
 int launch_slab_unpack(const void* buf, int64_t r0, int64_t cnt, int64_t dst, float4* nposp,
                        float4* nvelr, float4* nprev, int64_t* nid, uint32_t* nkeys,
                        cudaStream_t s);
+int64_t band_scratch_words(const sphb_grid_t& g);
+int launch_band_count(const sphb_grid_t& g, int width, int sides, const int32_t* beg,
+                      const int32_t* end, int32_t* scratch, int64_t* info,
+                      const sphb_ctrl_t* ctrl, cudaStream_t s);
+int launch_band_pack(const sphb_params_t& p, const sphb_grid_t& g, int width, int sides,
+                     const int32_t* beg, const int32_t* end, const int32_t* scratch,
+                     const float4* posp_s, const float4* velr_s, const float4* prev_s,
+                     const int64_t* id_s, const void* acc, const void* drho, void* send_l,
+                     void* send_r, cudaStream_t s);
+int launch_band_integrate(sphb_workspace* ws, const sphb_params_t& p, const sphb_grid_t& g,
+                          const void* buf, int64_t cnt, int64_t dst, float4* posp, float4* velr,
+                          float4* prev, int64_t* id, uint32_t* keys_next, uint32_t* keys_sorted,
+                          sphb_ctrl_t* ctrl, cudaStream_t s);
+int launch_slab_tail(const sphb_grid_t& g, int32_t* end, int64_t n_next, cudaStream_t s);
 int launch_cell_hist(sphb_workspace* ws, const sphb_grid_t& g, const uint32_t* keys, int64_t n,
                      const sphb_ctrl_t* ctrl, cudaStream_t s);
 int launch_step_end(sphb_ctrl_t* ctrl, const sphb_params_t& p, sphb_step_record_t* rec, int64_t cap,

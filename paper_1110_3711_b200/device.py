@@ -26,7 +26,7 @@ def _ptr(t) -> int:
 def cellbits_of(ncells: int) -> int:
     """Sort-key cell bits (sphb_common.cuh cellbits_of)."""
     b = 1
-    while (1 << b) < ncells:
+    while (1 << b) <= ncells:
         b += 1
     return b
 

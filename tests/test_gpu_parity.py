@@ -855,12 +855,12 @@ def test_c3_10m_counters_match_reference_measurement(n_subdiv, cand):
 def test_device_virtual_slabs_match_single_domain(nslabs, precision):
     """k virtual slabs on one GPU (LoopbackComm; the same exchange code as the NCCL path)
     against the single-domain device run: step 0 identical, 20 steps close (id-aligned)."""
-    from paper_1110_3711_b200 import slab
+    import slab_torch_reference as tslab
     sc = sph.Scenario(dp=0.006)
     prm = sph.make_params(sc)
     system = sph.build_dam_break(sc, prm)
     steps = 20
-    sim = slab.device_slab_simulation(system, prm, nslabs, precision=precision)
+    sim = tslab.device_slab_simulation(system, prm, nslabs, precision=precision)
     sim.run(steps)
     cfg = gather_cfg("slowcellsh", "fp64" if precision == 1 else "fp32")
     ref, stats = sph.run_simulation(sph.build_dam_break(sc, prm), prm, cfg, max_steps=steps,

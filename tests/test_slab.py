@@ -16,6 +16,7 @@ import oracle
 from slab_oracle_engine import OracleLocalEngine
 from paper_1110_3711_b200 import Scenario, build_dam_break, make_params
 from paper_1110_3711_b200 import slab
+import slab_torch_reference as tslab
 
 
 def test_rebalance_known_answers():
@@ -74,9 +75,9 @@ def test_virtual_slabs_match_single_domain(nslabs):
     cs, dims = oracle.grid_dims(prm)
     col = oracle.assign_cells(system.pos, prm)[0] % dims[0]
     bounds = slab.balanced_bounds(np.bincount(col, minlength=int(dims[0])), nslabs, 1)
-    comm = slab.LoopbackComm(nslabs)
-    ranks = slab.split_system(system, bounds, prm, lambda k: torch.device("cpu"))
-    sim = slab.SlabSimulation(ranks, prm, comm, 1, lambda r: OracleLocalEngine(
+    comm = tslab.LoopbackComm(nslabs)
+    ranks = tslab.split_system(system, bounds, prm, lambda k: torch.device("cpu"))
+    sim = tslab.SlabSimulation(ranks, prm, comm, 1, lambda r: OracleLocalEngine(
         prm, system.mass_fluid, system.mass_boundary, 1))
     steps = 12
     sim.run(steps)
@@ -99,9 +100,9 @@ def _gloo_worker(rank, world, port, steps, result_path):
     cs, dims = oracle.grid_dims(prm)
     col = oracle.assign_cells(system.pos, prm)[0] % dims[0]
     bounds = slab.balanced_bounds(np.bincount(col, minlength=int(dims[0])), world, 1)
-    comm = slab.DistComm()
-    ranks = slab.split_system(system, bounds, prm, lambda k: torch.device("cpu"))
-    sim = slab.SlabSimulation([ranks[rank]], prm, comm, 1, lambda r: OracleLocalEngine(
+    comm = tslab.DistComm()
+    ranks = tslab.split_system(system, bounds, prm, lambda k: torch.device("cpu"))
+    sim = tslab.SlabSimulation([ranks[rank]], prm, comm, 1, lambda r: OracleLocalEngine(
         prm, system.mass_fluid, system.mass_boundary, 1))
     sim.run(steps)
     host = sim.gather_host()
@@ -162,3 +163,14 @@ def test_device_slab_layout_host_logic():
     # edge ranks have no outside neighbours
     lay0 = dslab.rank_layout(tab, 0, 3)
     assert lay0["recv_rows"][0] == 0 and lay0["unpack"][0] == [(0, 0, d) for _, _, d in lay0["unpack"][0]]
+
+
+def test_band_recv_rows_from_neighbours():
+    """dslab.band_recv_rows: a rank receives its left neighbour's right band and its right
+    neighbour's left band; the end ranks have one neighbour."""
+    from paper_1110_3711_b200 import dslab
+    tab = np.array([[0, 7, -1], [5, 9, -1], [4, 0, -1]], np.int64)  # (to left, to right, err)
+    assert dslab.band_recv_rows(tab, 0, 3) == (0, 5)
+    assert dslab.band_recv_rows(tab, 1, 3) == (7, 4)
+    assert dslab.band_recv_rows(tab, 2, 3) == (9, 0)
+    assert dslab.band_recv_rows(tab[:1], 0, 1) == (0, 0)

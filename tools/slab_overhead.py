@@ -1,5 +1,5 @@
 """Per-step overhead of the X-slab machinery on one GPU: the same system stepped by DeviceSim
-(single domain), by the torch SlabSimulation and by the device-resident DeviceSlabSim with k
+(single domain), by the torch SlabSimulation (tests/, --legacy) and by the device-resident DeviceSlabSim with k
 virtual slabs (loopback comms)."""
 import sys
 import time
@@ -8,7 +8,7 @@ import torch
 
 sys.path.insert(0, ".")
 import paper_1110_3711_b200 as sph  # noqa: E402
-from paper_1110_3711_b200 import dslab, slab  # noqa: E402
+from paper_1110_3711_b200 import dslab  # noqa: E402
 from paper_1110_3711_b200.device import DeviceSim  # noqa: E402
 
 name = sys.argv[1] if len(sys.argv) > 1 else "c3"
@@ -40,7 +40,9 @@ for k in (1, 2, 4):
     print(f"DeviceSlabSim slabs={k} (loopback, one GPU): {ms:.2f} ms/step, vs single +{ms - single:.2f} ms")
     del d
     torch.cuda.empty_cache()
-if legacy:
-    s = slab.device_slab_simulation(system, prm, 1)
+if legacy:  # the torch restatement (test infrastructure)
+    sys.path.insert(0, "tests")
+    import slab_torch_reference as tslab  # noqa: E402
+    s = tslab.device_slab_simulation(system, prm, 1)
     ms = timed(s.step)
     print(f"torch SlabSimulation slabs=1: {ms:.2f} ms/step, vs single +{ms - single:.2f} ms")
