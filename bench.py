@@ -401,9 +401,10 @@ def run_reference(args, cfg_name):
 
 # ---------------------------------------------------------------- multi-GPU (X slabs)
 def run_slabs(args, cfg_name, sc, system, prm, prec, world, rank, local):
-    """One X-slab per GPU (dslab.DeviceSlabSim): device classify/scatter of migrants and halo
-    rows, NCCL send/recv of exact byte counts, owned-target interaction, device all-reduces of
-    the dt minima and counters; one host synchronisation per step (the totals all-gather)."""
+    """One X-slab per GPU (dslab.DeviceSlabSim): rows stay in place; the edge-band targets are
+    interacted first and their rows + forces travel to the neighbours (NCCL send/recv on a comm
+    stream) while the interior targets run; the receivers integrate them into migrants and next
+    halos; device all-reduce of the dt minima; counters summed when read."""
     import torch
     import torch.distributed as dist
     from paper_1110_3711_b200 import _lib, dslab
@@ -416,12 +417,19 @@ def run_slabs(args, cfg_name, sc, system, prm, prec, world, rank, local):
         sim.step()
     torch.cuda.synchronize()
     pi_blocks = [128]
+    tuning = None
     first = args.warmup
     if args.pi_block == "auto" and prec == _lib.SPHB_FP32:  # as the single-GPU path
-        from paper_1110_3711_b200.sim import PI_LARGE_MIN_TARGETS
+        from paper_1110_3711_b200.sim import PI_LARGE_MIN_TARGETS, initial_pi_block
         pi_blocks = sim.choose_pi_block(PI_LARGE_MIN_TARGETS if args.n_subdiv == 1 else None)
-        sim.step()
-        first += 1
+        if args.pi_kernel == "tuned":  # per rank: the gather blocking vs the paired build
+            cands = [("gather", initial_pi_block(sim.n_owned_max, args.n_subdiv)), ("paired", 512)]
+            tuning = sim.tune_pi(cands)
+            first += len(cands)
+            pi_blocks = [r.pi_block for r in sim.ranks]
+        else:
+            sim.step()
+            first += 1
         torch.cuda.synchronize()
     dist.barrier()
     clocks = Clocks(local)
@@ -515,9 +523,14 @@ def run_slabs(args, cfg_name, sc, system, prm, prec, world, rank, local):
         "data": "synthetic: reference dam-break lattice (Scenario/build_dam_break), hydrostatic rho",
         "config": workload_config(cfg_name, sc, system, args.n_subdiv, world),
         "build": {"slab_bounds": [int(v) for v in sim.bounds], "pi_block_rank0": int(pi_blocks[0]),
+                  "pi_kernel_rank0": {_lib.SPHB_PI_PAIRED: "paired"}.get(me.pi_kernel, "gather"),
+                  "pi_tuning_ms_rank0": tuning[0] if tuning else None,
                   "max_owned_per_gpu": int(owned.item()),
-                  "exchange": "device-resident: NCCL send/recv of migrants + halo rows, device "
-                              "all-reduce of dt and counters"},
+                  "exchange": "edge bands (reach + 1 columns per neighbour) interacted first, "
+                              "packed with their forces and sent over NCCL send/recv on a "
+                              "high-priority comm stream while the interior targets run; the "
+                              "receiver integrates them (migrants + next halo); device all-reduce "
+                              "of dt; one host read per step hidden behind the edge interaction"},
         "interactions_per_s": true_pairs * args.steps / (total_ms * 1e-3),
         "pair_evals_per_s": evals * args.steps / (total_ms * 1e-3),
         "gpu_launches": args.steps * sim.launches_per_step(),

@@ -778,6 +778,28 @@ class DeviceSlabSim:
             r.ws.set_pi_kernel(code)
             r.ws.set_pi_block(blk)
 
+    def tune_pi(self, candidates) -> list[dict]:
+        """DeviceSim.tune_pi per rank: one ordinary step with each candidate build ((kernel,
+        block) pairs; the state advances as usual), the fastest interaction phase per local
+        rank kept (ranks may differ: a slab at rest and one holding the collapsing column).
+        Returns each local rank's {"kernel/block": PI ms}."""
+        times = []
+        for kern, blk in candidates:
+            self.select_pi(kern, blk)
+            self.step()
+            torch.cuda.synchronize()
+            times.append([r.pi_events[-1][0].elapsed_time(r.pi_events[-1][1]) for r in self.ranks])
+        out = []
+        for k, r in enumerate(self.ranks):
+            ms = [t[k] for t in times]
+            kern, blk = candidates[int(np.argmin(ms))]
+            code = {"gather": _lib.SPHB_PI_GATHER, "paired": _lib.SPHB_PI_PAIRED}[kern]
+            r.pi_kernel, r.pi_block = code, (512 if kern == "paired" else blk)
+            r.ws.set_pi_kernel(r.pi_kernel)
+            r.ws.set_pi_block(r.pi_block)
+            out.append({f"{c[0]}/{c[1]}": round(t, 4) for c, t in zip(candidates, ms)})
+        return out
+
     def launches_per_step(self) -> int:
         """This library's kernel launches per step on rank 0 (NL, band count, interaction
         launches, pack, K7, band updates, tail, step begin / end)."""

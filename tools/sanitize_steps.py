@@ -17,11 +17,14 @@ sc = sph.Scenario(dp=0.02)
 prm = sph.make_params(sc, boundary_force=sph.BoundaryForce(d=5.0 * 9.81 * sc.fill_height, r0=sc.dp))
 system = sph.build_dam_break(sc, prm)
 for precision, block, integ in ((0, 128, "verlet"), (0, 256, "verlet"), (0, 384, "verlet"), (1, 128, "verlet"),
-                                (0, 128, "symplectic")):
+                                (0, 128, "symplectic"), (0, "paired", "verlet"), (0, "symmetric", "verlet")):
     p = sph.make_params(sc, integrator=integ,
                         boundary_force=sph.BoundaryForce(d=5.0 * 9.81 * sc.fill_height, r0=sc.dp))
     sim = DeviceSim(system, p, reach=1, precision=precision)
-    sim.set_pi_block(block)
+    if isinstance(block, str):
+        sim.set_pi_kernel(block)
+    else:
+        sim.set_pi_block(block)
     for _ in range(4):
         sim.launch_step()
     sim.energy()
@@ -40,11 +43,16 @@ for precision, block, integ in ((0, 128, "verlet"), (0, 256, "verlet"), (0, 384,
 # the X-slab exchange kernels (slab.cu) through two virtual ranks on this GPU
 from paper_1110_3711_b200 import dslab  # noqa: E402
 
-ds = dslab.DeviceSlabSim(system, prm, dslab.DevLoopbackComm(2), precision=0)
+# (the slab stepper has no wall-force extension), edge bands + dead-bin sort, then a re-settle
+ds = dslab.DeviceSlabSim(system, sph.make_params(sc), dslab.DevLoopbackComm(2), precision=0)
 for _ in range(4):
     ds.step()
+ds.rebalance(times=[1.0, 3.0])
+for _ in range(2):
+    ds.step()
+ds.check()
 torch.cuda.synchronize()
-print("ok slabs", flush=True)
+print("ok slabs", ds.bounds, flush=True)
 
 # the module-level step functions (stepfn.cu, grid.py)
 import types  # noqa: E402
