@@ -137,6 +137,41 @@ struct Seg {
   int dyz;      // row offset from the block's origin row: (dy + 16) | (dz + 16) << 8
 };
 
+// Staging of a batch [q0, q1) of the block's candidate sequence, issued by the 32 lanes of one
+// warp in parallel (h/2 cells: 2 x 36 stencil rows per brick, so one thread issuing every copy
+// serialised the batch start): one TMA bulk copy per (stencil row, array) into the A (posp:
+// x, y, z, prrho) and B (velr) rows, completion counted in bytes on the mbarrier.
+__device__ __forceinline__ void stage_batch(const float4* posp, const float4* velr,
+                                            const Seg* sSeg, int nseg, int q0, int q1,
+                                            uint32_t smA, uint32_t offB, uint32_t mbar, int lane) {
+  uint32_t bytes = 0;
+  for (int k = lane; k < nseg; k += 32) {
+    const Seg sg = sSeg[k];
+    const int lo_p = max(sg.pos, q0), hi_p = min(sg.pos + (sg.g1 - sg.g0), q1);
+    if (hi_p > lo_p) bytes += 32u * (uint32_t)(hi_p - lo_p);
+  }
+  bytes = __reduce_add_sync(SPHB_FULL, bytes);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  if (lane == 0)
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mbar), "r"(bytes)
+                 : "memory");
+  __syncwarp();
+  for (int k = lane; k < nseg; k += 32) {
+    const Seg sg = sSeg[k];
+    const int lo_p = max(sg.pos, q0), hi_p = min(sg.pos + (sg.g1 - sg.g0), q1);
+    if (hi_p <= lo_p) continue;
+    const int j0 = sg.g0 + (lo_p - sg.pos);
+    const uint32_t nbytes = 16u * (uint32_t)(hi_p - lo_p);
+    const uint32_t dA = smA + 16u * (uint32_t)(lo_p - q0), dB = dA + offB;
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+        ::"r"(dA), "l"(posp + j0), "r"(nbytes), "r"(mbar) : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+        ::"r"(dB), "l"(velr + j0), "r"(nbytes), "r"(mbar) : "memory");
+  }
+}
+
 __device__ __forceinline__ bool step_live(const sphb_ctrl_t* c) {
   return c->active && c->err >= ((uint64_t)(c->step + 1) << 40);
 }
@@ -1656,36 +1691,46 @@ __global__ void __launch_bounds__(NW * 32, V8_MINB) k_interact_v8(KArgs a, K32 k
       __syncwarp();
     };
 
+    // The warp's part of every staged row: cells [wxlo, wxhi] (symmetric own row: from its
+    // lowest target cell), as staged positions [wpos0, wpos1) -- computed once per block, the
+    // lanes' global loads in parallel (lane l: rows l, l + 32, ...) -- and which rows some lane
+    // of the warp needs (a brick's lanes sit in up to four rows: the warp's set wrows)
+    int wpos0[MAXSEG / 32], wpos1[MAXSEG / 32];
+    uint32_t wlive = 0;
+    {
+      const uint32_t mine = valid ? 1u << (rsy + 2 * rsz) : 0u;
+      const uint32_t wrows_all = __reduce_or_sync(SPHB_FULL, mine);
+      const uint32_t wrows_f = __reduce_or_sync(SPHB_FULL, isf ? mine : 0u);
+#pragma unroll
+      for (int g = 0; g < MAXSEG / 32; ++g) {
+        const int k = g * 32 + lane;
+        wpos0[g] = wpos1[g] = 0;
+        if (wactive && k < nseg) {
+          const Seg sg = sSeg[k];
+          if (sg.g1 > sg.g0) {
+            const int lo = (V8_SYM && k < nlist) ? max(wcxlo, 0) : wxlo;
+            const int w0 = a.beg[sg.rowoff + lo], w1 = a.end[sg.rowoff + wxhi];
+            wpos0[g] = sg.pos + (w0 - sg.g0);
+            wpos1[g] = sg.pos + (w1 - sg.g0);
+            // boundary-list rows serve the fluid targets only
+            const uint32_t wr = sg.rowoff < a.ncells ? wrows_f : wrows_all;
+            const int dy = (sg.dyz & 255) - 16, dz = (sg.dyz >> 8) - 16;
+            bool need = false;
+#pragma unroll
+            for (int r4 = 0; r4 < 4; ++r4)
+              need |= ((wr >> r4) & 1u) && abs(dy - (r4 & 1)) <= reach && abs(dz - (r4 >> 1)) <= reach;
+            if (w1 > w0 && need) wlive |= 1u << g;
+          }
+        }
+      }
+    }
+
     for (int q0 = 0; q0 < total; q0 += SCAP) {
       const int q1 = min(q0 + SCAP, total);
       // ---- stage rows [q0, q1): one TMA bulk copy per (stencil row, array) -- the sorted
       // posp rows are (x, y, z, prrho), velr rows (vx, vy, vz, rho) -- then the 8-B screen
       // records from shared memory
-      if (tid == 0) {
-        uint32_t bytes = 0;
-        for (int k = 0; k < nseg; ++k) {
-          const Seg sg = sSeg[k];
-          const int lo_p = max(sg.pos, q0), hi_p = min(sg.pos + (sg.g1 - sg.g0), q1);
-          if (hi_p > lo_p) bytes += 32u * (uint32_t)(hi_p - lo_p);
-        }
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mbar), "r"(bytes)
-                     : "memory");
-        for (int k = 0; k < nseg; ++k) {
-          const Seg sg = sSeg[k];
-          const int lo_p = max(sg.pos, q0), hi_p = min(sg.pos + (sg.g1 - sg.g0), q1);
-          if (hi_p <= lo_p) continue;
-          const int j0 = sg.g0 + (lo_p - sg.pos);
-          const uint32_t nbytes = 16u * (uint32_t)(hi_p - lo_p);
-          const uint32_t dA = smA + 16u * (uint32_t)(lo_p - q0), dB = dA + 16u * V8_ROWS;
-          asm volatile(
-              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-              ::"r"(dA), "l"(a.posp + j0), "r"(nbytes), "r"(mbar) : "memory");
-          asm volatile(
-              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-              ::"r"(dB), "l"(a.velr + j0), "r"(nbytes), "r"(mbar) : "memory");
-        }
-      }
+      if (warp == 0) stage_batch(a.posp, a.velr, sSeg, nseg, q0, q1, smA, 16u * V8_ROWS, mbar, lane);
       {  // wait for the bytes (phase parity flips per batch)
         uint32_t done = 0;
         while (!done)
@@ -1708,38 +1753,20 @@ __global__ void __launch_bounds__(NW * 32, V8_MINB) k_interact_v8(KArgs a, K32 k
       }
       __syncthreads();
       if (wactive) {
-        // the warp's part of row k: cells [wxlo, wxhi]; the next row's bounds are loaded while
-        // this row is screened
-        auto live = [&](int k) {
-          const Seg sg = sSeg[k];
-          const int len = sg.g1 - sg.g0;
-          return len > 0 && sg.pos < q1 && sg.pos + len > q0;
-        };
-        // the warp's lowest cell in row k (symmetric own row: its lowest target cell)
-        auto wlo = [&](int k) { return (V8_SYM && k < nlist) ? max(wcxlo, 0) : wxlo; };
-        int kn = 0;
-        while (kn < nseg && !live(kn)) ++kn;
-        int nb0 = 0, nb1 = 0;
-        if (kn < nseg) {
-          nb0 = a.beg[sSeg[kn].rowoff + wlo(kn)];
-          nb1 = a.end[sSeg[kn].rowoff + wxhi];
-        }
-        while (kn < nseg) {
-          const int k = kn;
-          const Seg sg = sSeg[k];
-          const int wg0 = nb0, wg1 = nb1;
-          ++kn;
-          while (kn < nseg && !live(kn)) ++kn;
-          if (kn < nseg) {
-            nb0 = a.beg[sSeg[kn].rowoff + wlo(kn)];
-            nb1 = a.end[sSeg[kn].rowoff + wxhi];
-          }
-          const int lo_ = max(sg.pos + (wg0 - sg.g0), q0) - q0;
-          const int hi_ = min(sg.pos + (wg1 - sg.g0), q1) - q0;
+        // the warp's windows (precomputed per block, wpos0/wpos1) of the live rows, in row order
+#pragma unroll
+        for (int g = 0; g < MAXSEG / 32; ++g) {
+          uint32_t mlive = __ballot_sync(SPHB_FULL, (wlive >> g) & 1u);
+          while (mlive) {
+          const int l = __ffs(mlive) - 1;
+          mlive &= mlive - 1u;
+          const int k = g * 32 + l;
+          const int lo_ = max(__shfl_sync(SPHB_FULL, wpos0[g], l), q0) - q0;
+          const int hi_ = min(__shfl_sync(SPHB_FULL, wpos1[g], l), q1) - q0;
           if (hi_ <= lo_) continue;
+          const Seg sg = sSeg[k];
           const bool boundary_list = sg.rowoff < a.ncells;
           const bool inr = in_rows(sg.dyz);
-          if (brick && !__any_sync(SPHB_FULL, valid && inr)) continue;
           const uint32_t lanemask = (valid && inr && (isf || !boundary_list)) ? 0xffffffffu : 0u;
           const bool selfrow = k == selfseg_l;
           // own staged position in the self row (fluid targets), else out of range
@@ -1806,6 +1833,7 @@ __global__ void __launch_bounds__(NW * 32, V8_MINB) k_interact_v8(KArgs a, K32 k
               ++cnt;
               pend += __popc(bits);
             }
+          }
           }
         }
         drain(true);

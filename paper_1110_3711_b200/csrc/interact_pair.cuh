@@ -587,33 +587,47 @@ __global__ void __launch_bounds__(NW * 32, 1) k_interact_v12(KArgs a, K32 k32) {
       __syncwarp();
     };
 
-    for (int q0 = 0; q0 < total; q0 += SCAP) {
-      const int q1 = min(q0 + SCAP, total);
-      if (tid == 0) {
-        uint32_t bytes = 0;
-        for (int k = 0; k < nseg; ++k) {
+    // The warp's part of every staged row (cells [wxlo, wxhi]) as staged positions [wpos0,
+    // wpos1), computed once per block by the lanes in parallel (lane l: rows l, l + 32, ...), and
+    // whether a target of the warp uses the row (its rows: wrows_all; boundary-list rows only
+    // the fluid targets': wrows_f)
+    int wpos0[MAXSEG / 32], wpos1[MAXSEG / 32];
+    uint32_t wlive = 0;
+    {
+      uint32_t mine_all = 0, mine_f = 0;
+#pragma unroll
+      for (int t = 0; t < 2; ++t) {
+        const uint32_t b = valid[t] ? 1u << (rsy[t] + 2 * rsz[t]) : 0u;
+        mine_all |= b;
+        mine_f |= isf[t] ? b : 0u;
+      }
+      const uint32_t wrows_all = __reduce_or_sync(SPHB_FULL, mine_all);
+      const uint32_t wrows_f = __reduce_or_sync(SPHB_FULL, mine_f);
+#pragma unroll
+      for (int g = 0; g < MAXSEG / 32; ++g) {
+        const int k = g * 32 + lane;
+        wpos0[g] = wpos1[g] = 0;
+        if (wactive && k < nseg) {
           const Seg sg = sSeg[k];
-          const int lo_p = max(sg.pos, q0), hi_p = min(sg.pos + (sg.g1 - sg.g0), q1);
-          if (hi_p > lo_p) bytes += 32u * (uint32_t)(hi_p - lo_p);
-        }
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mbar), "r"(bytes)
-                     : "memory");
-        for (int k = 0; k < nseg; ++k) {
-          const Seg sg = sSeg[k];
-          const int lo_p = max(sg.pos, q0), hi_p = min(sg.pos + (sg.g1 - sg.g0), q1);
-          if (hi_p <= lo_p) continue;
-          const int j0 = sg.g0 + (lo_p - sg.pos);
-          const uint32_t nbytes = 16u * (uint32_t)(hi_p - lo_p);
-          const uint32_t dA = smA + 16u * (uint32_t)(lo_p - q0), dB = dA + 16u * V8_ROWS;
-          asm volatile(
-              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-              ::"r"(dA), "l"(a.posp + j0), "r"(nbytes), "r"(mbar) : "memory");
-          asm volatile(
-              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-              ::"r"(dB), "l"(a.velr + j0), "r"(nbytes), "r"(mbar) : "memory");
+          if (sg.g1 > sg.g0) {
+            const int w0 = a.beg[sg.rowoff + wxlo], w1 = a.end[sg.rowoff + wxhi];
+            wpos0[g] = sg.pos + (w0 - sg.g0);
+            wpos1[g] = sg.pos + (w1 - sg.g0);
+            const uint32_t wr = sg.rowoff < a.ncells ? wrows_f : wrows_all;
+            const int dy = (sg.dyz & 255) - 16, dz = (sg.dyz >> 8) - 16;
+            bool need = false;
+#pragma unroll
+            for (int r4 = 0; r4 < 4; ++r4)
+              need |= ((wr >> r4) & 1u) && abs(dy - (r4 & 1)) <= reach && abs(dz - (r4 >> 1)) <= reach;
+            if (w1 > w0 && need) wlive |= 1u << g;
+          }
         }
       }
+    }
+
+    for (int q0 = 0; q0 < total; q0 += SCAP) {
+      const int q1 = min(q0 + SCAP, total);
+      if (warp == 0) stage_batch(a.posp, a.velr, sSeg, nseg, q0, q1, smA, 16u * V8_ROWS, mbar, lane);
       {
         uint32_t done = 0;
         while (!done)
@@ -646,37 +660,23 @@ __global__ void __launch_bounds__(NW * 32, 1) k_interact_v12(KArgs a, K32 k32) {
       }
       __syncthreads();
       if (wactive) {
-        auto live = [&](int k) {
-          const Seg sg = sSeg[k];
-          const int len = sg.g1 - sg.g0;
-          return len > 0 && sg.pos < q1 && sg.pos + len > q0;
-        };
-        int kn = 0;
-        while (kn < nseg && !live(kn)) ++kn;
-        int nb0 = 0, nb1 = 0;
-        if (kn < nseg) {
-          nb0 = a.beg[sSeg[kn].rowoff + wxlo];
-          nb1 = a.end[sSeg[kn].rowoff + wxhi];
-        }
-        while (kn < nseg) {
-          const int k = kn;
-          const Seg sg = sSeg[k];
-          const int wg0 = nb0, wg1 = nb1;
-          ++kn;
-          while (kn < nseg && !live(kn)) ++kn;
-          if (kn < nseg) {
-            nb0 = a.beg[sSeg[kn].rowoff + wxlo];
-            nb1 = a.end[sSeg[kn].rowoff + wxhi];
-          }
-          const int lo_ = max(sg.pos + (wg0 - sg.g0), q0) - q0;
-          const int hi_ = min(sg.pos + (wg1 - sg.g0), q1) - q0;
+        // the warp's windows (precomputed per block, wpos0/wpos1) of the live rows, in row order
+#pragma unroll
+        for (int g = 0; g < MAXSEG / 32; ++g) {
+          uint32_t mlive = __ballot_sync(SPHB_FULL, (wlive >> g) & 1u);
+          while (mlive) {
+          const int l = __ffs(mlive) - 1;
+          mlive &= mlive - 1u;
+          const int k = g * 32 + l;
+          const int lo_ = max(__shfl_sync(SPHB_FULL, wpos0[g], l), q0) - q0;
+          const int hi_ = min(__shfl_sync(SPHB_FULL, wpos1[g], l), q1) - q0;
           if (hi_ <= lo_) continue;
+          const Seg sg = sSeg[k];
           const bool boundary_list = sg.rowoff < a.ncells;
           bool use[2];
 #pragma unroll
           for (int t = 0; t < 2; ++t)
             use[t] = valid[t] && in_rows(sg.dyz, t) && (isf[t] || !boundary_list);
-          if (!__any_sync(SPHB_FULL, use[0] || use[1])) continue;
           // C per M-tile row for this staged row: targets that skip it never screen in
           float fcv[4][2];
           {
@@ -740,6 +740,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_interact_v12(KArgs a, K32 k32) {
               ++cnt;
               pend += __popc(bits);
             }
+          }
           }
         }
         drain(true);
