@@ -172,6 +172,12 @@ __device__ __forceinline__ void stage_batch(const float4* posp, const float4* ve
   }
 }
 
+__device__ __forceinline__ double ipow(double q, int k) {
+  double r = 1.0;
+  for (int e = 0; e < k; ++e) r = xmul(r, q);
+  return r;
+}
+
 __device__ __forceinline__ bool step_live(const sphb_ctrl_t* c) {
   return c->active && c->err >= ((uint64_t)(c->step + 1) << 40);
 }
@@ -242,6 +248,62 @@ template <typename R>
 struct Accum {
   R ax, ay, az, dr, vd;
 };
+
+// ------------------------------------------------------------------ fused boundary repulsion
+// Extension (off by default): the Lennard-Jones wall force of one fluid
+// target, a += D ((r0/r)^p1 - (r0/r)^p2) r_ij / r^2 over boundary particles closer than r0
+// (<= 2h: all in the stencil), evaluated in the FP32 interaction kernels' epilogue of each
+// staging batch from the staged boundary rows -- in the order of the separate k_wall_force pass
+// (stencil rows z-major, then y, then candidate index), f64, so the result is the same bits.
+// Returns whether any boundary particle was within r0.
+__device__ __forceinline__ bool wall_batch(const KArgs& a, const Seg* sSeg, int nseg, int q0,
+                                           int q1, uint32_t smA, float ox, float oy, float oz,
+                                           int xlo, int xhi, int rsy, int rsz, double& fx,
+                                           double& fy, double& fz) {
+  const double r02 = xmul(a.p.wall_r0, a.p.wall_r0);
+  const int reach = a.g.reach;
+  bool hit = false;
+  for (int k = 0; k < nseg; ++k) {
+    const Seg sg = sSeg[k];
+    if (sg.rowoff >= a.ncells || sg.g1 <= sg.g0) continue;  // boundary-list rows
+    const int dy = (sg.dyz & 255) - 16, dz = (sg.dyz >> 8) - 16;
+    if (abs(dy - rsy) > reach || abs(dz - rsz) > reach) continue;  // not this target's stencil
+    const int j0 = a.beg[sg.rowoff + xlo], j1 = a.end[sg.rowoff + xhi];
+    const int p0 = max(sg.pos + (j0 - sg.g0), q0), p1 = min(sg.pos + (j1 - sg.g0), q1);
+    for (int p = p0; p < p1; ++p) {
+      const float4 A = lds4(smA + 16u * (uint32_t)(p - q0));
+      const double dx = xsub((double)ox, (double)A.x);
+      const double dy2 = xsub((double)oy, (double)A.y);
+      const double dz2 = xsub((double)oz, (double)A.z);
+      const double r2 = xadd(xadd(xmul(dx, dx), xmul(dy2, dy2)), xmul(dz2, dz2));
+      if (!(r2 > 0.0 && r2 < r02)) continue;
+      const double q = xdiv(a.p.wall_r0, __dsqrt_rn(r2));
+      const double f = xdiv(xmul(a.p.wall_d, xsub(ipow(q, a.p.wall_p1), ipow(q, a.p.wall_p2))), r2);
+      fx = xadd(fx, xmul(f, dx));
+      fy = xadd(fy, xmul(f, dy2));
+      fz = xadd(fz, xmul(f, dz2));
+      hit = true;
+    }
+  }
+  return hit;
+}
+
+// the wall term joins the FP32 acceleration as the separate pass adds it (f64 sum, rounded),
+// and the target's force dt term with it joins the minimum (the SPH-only one is already in)
+__device__ __forceinline__ void wall_finish(const KArgs& a, int64_t i, int64_t step, float ax,
+                                            float ay, float az, float dr, double fx, double fy,
+                                            double fz, double& dtf_min) {
+  const float wx = (float)xadd((double)ax, fx), wy = (float)xadd((double)ay, fy),
+              wz = (float)xadd((double)az, fz);
+  a.acc4[i] = make_float4(wx, wy, wz, dr);
+  const double gx = xadd((double)wx, a.p.g[0]), gy = xadd((double)wy, a.p.g[1]),
+               gz = xadd((double)wz, a.p.g[2]);
+  double fmag = __dsqrt_rn(xadd(xadd(xmul(gx, gx), xmul(gy, gy)), xmul(gz, gz)));
+  fmag = fmag > 1e-30 ? fmag : 1e-30;
+  dtf_min = fmin(dtf_min, __dsqrt_rn(xdiv(a.p.h, fmag)));
+  if (!(isfinite(wx) && isfinite(wy) && isfinite(wz)))
+    raise_div(a.ctrl, step, SPHB_DIV_NONFINITE_FORCES, 0);
+}
 
 // ------------------------------------------------------------------ pair math
 // FP32 (physics.py:183-220 restated for FP32 CUDA cores).  Branch-free cubic spline:
@@ -1309,7 +1371,7 @@ __device__ __forceinline__ void eval_v8(const KArgs& a, const K32& c, const Own3
   }
 }
 
-template <bool G7, bool EQM, bool WEND>
+template <bool G7, bool EQM, bool WEND, bool WALL>
 #ifndef V8_MINB
 #define V8_MINB 2  // CTAs per SM: shared memory (V8_SMEM) and registers allow 2
 #endif
@@ -1725,6 +1787,11 @@ __global__ void __launch_bounds__(NW * 32, V8_MINB) k_interact_v8(KArgs a, K32 k
       }
     }
 
+    // fused wall force (extension; the FP32 gather builds): f64 sums over the batches
+    constexpr bool wall = WALL && !V8_SYM;  // (its own instantiation: none of it otherwise)
+    double wfx = 0.0, wfy = 0.0, wfz = 0.0;
+    bool whit = false;
+
     for (int q0 = 0; q0 < total; q0 += SCAP) {
       const int q1 = min(q0 + SCAP, total);
       // ---- stage rows [q0, q1): one TMA bulk copy per (stencil row, array) -- the sorted
@@ -1837,6 +1904,8 @@ __global__ void __launch_bounds__(NW * 32, V8_MINB) k_interact_v8(KArgs a, K32 k
           }
         }
         drain(true);
+        if constexpr (wall) if (valid && isf)
+          whit |= wall_batch(a, sSeg, nseg, q0, q1, smA, o.x, o.y, o.z, xlo, xhi, rsy, rsz, wfx, wfy, wfz);
       }
       __syncthreads();
       if (V8_SYM) {
@@ -1912,6 +1981,8 @@ __global__ void __launch_bounds__(NW * 32, V8_MINB) k_interact_v8(KArgs a, K32 k
         fmag = fmag > 1e-30 ? fmag : 1e-30;
         dtf_min = fmin(dtf_min, __dsqrt_rn(xdiv(a.p.h, fmag)));
       }
+      if (whit)
+        wall_finish(a, i, step, (float)ax, (float)ay, (float)az, (float)dr, wfx, wfy, wfz, dtf_min);
       dtcv_min = fmin(dtcv_min, xdiv(a.p.h, xadd((double)ocs, vd)));
     }
   }
@@ -1962,50 +2033,57 @@ int launch_kernel(const KArgs& a, int nsm, cudaStream_t s) {
   return sphb_check_launch("k_interact");
 }
 
-template <bool G7, bool EQM, bool WEND>
+template <bool G7, bool EQM, bool WEND, bool WALL>
 int launch_v8(const KArgs& a, const K32& k, int nsm, cudaStream_t s) {
   static int grid = 0;
   const size_t bytes = V8_SMEM;
   if (grid == 0) {
-    cudaError_t e = cudaFuncSetAttribute(k_interact_v8<G7, EQM, WEND>,
+    cudaError_t e = cudaFuncSetAttribute(k_interact_v8<G7, EQM, WEND, WALL>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
     if (e != cudaSuccess)
       return sphb_set_error(SPHB_E_CUDA, "smem attribute: %s", cudaGetErrorString(e));
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_interact_v8<G7, EQM, WEND>, NW * 32, bytes);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_interact_v8<G7, EQM, WEND, WALL>, NW * 32, bytes);
     grid = nsm * (per_sm > 0 ? per_sm : 1);
   }
-  k_interact_v8<G7, EQM, WEND><<<grid, NW * 32, bytes, s>>>(a, k);
+  k_interact_v8<G7, EQM, WEND, WALL><<<grid, NW * 32, bytes, s>>>(a, k);
   return sphb_check_launch("k_interact_v8");
 }
 
 #if SPHB_PAIR
-template <bool G7, bool EQM, bool WEND>
+template <bool G7, bool EQM, bool WEND, bool WALL>
 int launch_v12(const KArgs& a, const K32& k, int nsm, cudaStream_t s) {
   static bool init = false;
   const size_t bytes = V8_SMEM;
   if (!init) {
-    cudaError_t e = cudaFuncSetAttribute(k_interact_v12<G7, EQM, WEND>,
+    cudaError_t e = cudaFuncSetAttribute(k_interact_v12<G7, EQM, WEND, WALL>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
     if (e != cudaSuccess)
       return sphb_set_error(SPHB_E_CUDA, "smem attribute: %s", cudaGetErrorString(e));
     init = true;
   }
-  k_interact_v12<G7, EQM, WEND><<<nsm, NW * 32, bytes, s>>>(a, k);
+  k_interact_v12<G7, EQM, WEND, WALL><<<nsm, NW * 32, bytes, s>>>(a, k);
   return sphb_check_launch("k_interact_v12");
 }
 #endif
 
 template <bool WEND>
 int launch_v8_kernel(const KArgs& a, const K32& k, bool eqm, int nsm, cudaStream_t s) {
+  // the fused wall force (extension) has its own instantiations, gamma = 7 only (the other
+  // EOS exponents take the separate k_wall_force pass, launch_interact)
+  const bool wall = a.p.wall_d > 0.0 && a.gamma7;
 #if SPHB_PAIR
+  if (wall)
+    return eqm ? launch_v12<true, true, WEND, true>(a, k, nsm, s) : launch_v12<true, false, WEND, true>(a, k, nsm, s);
   if (a.gamma7)
-    return eqm ? launch_v12<true, true, WEND>(a, k, nsm, s) : launch_v12<true, false, WEND>(a, k, nsm, s);
-  return eqm ? launch_v12<false, true, WEND>(a, k, nsm, s) : launch_v12<false, false, WEND>(a, k, nsm, s);
+    return eqm ? launch_v12<true, true, WEND, false>(a, k, nsm, s) : launch_v12<true, false, WEND, false>(a, k, nsm, s);
+  return eqm ? launch_v12<false, true, WEND, false>(a, k, nsm, s) : launch_v12<false, false, WEND, false>(a, k, nsm, s);
 #endif
+  if (wall)
+    return eqm ? launch_v8<true, true, WEND, true>(a, k, nsm, s) : launch_v8<true, false, WEND, true>(a, k, nsm, s);
   if (a.gamma7)
-    return eqm ? launch_v8<true, true, WEND>(a, k, nsm, s) : launch_v8<true, false, WEND>(a, k, nsm, s);
-  return eqm ? launch_v8<false, true, WEND>(a, k, nsm, s) : launch_v8<false, false, WEND>(a, k, nsm, s);
+    return eqm ? launch_v8<true, true, WEND, false>(a, k, nsm, s) : launch_v8<true, false, WEND, false>(a, k, nsm, s);
+  return eqm ? launch_v8<false, true, WEND, false>(a, k, nsm, s) : launch_v8<false, false, WEND, false>(a, k, nsm, s);
 }
 
 template <typename R>
@@ -2052,12 +2130,6 @@ int launch_one(const KArgs& a, int nsm, cudaStream_t s) {
 // interaction stencil holds them all):  a_i += D ((r0/r)^p1 - (r0/r)^p2) r_ij / r^2.  f64,
 // added to the PI accelerations; the fluid dt term sqrt(h / |a + g|) of every target it
 // touches joins the minimum (the SPH-only term is already in it: dt stays conservative).
-__device__ __forceinline__ double ipow(double q, int k) {
-  double r = 1.0;
-  for (int e = 0; e < k; ++e) r = xmul(r, q);
-  return r;
-}
-
 template <bool F32>
 __global__ void __launch_bounds__(256) k_wall_force(sphb_params_t p, sphb_grid_t g, int64_t n,
                                                     int64_t nb, int64_t ncells,
@@ -2261,7 +2333,10 @@ int launch_interact(sphb_workspace* ws, const sphb_params_t& p, const sphb_grid_
     cudaMemsetAsync(visc, 0, sizeof(float) * (size_t)n, s);
   }
   int rc = p.precision == SPHB_FP64 ? launch_one<double>(a, nsm, s) : launch_one<float>(a, nsm, s);
-  if (!rc && p.wall_d > 0.0 && n > nb) rc = launch_wall(p, g, n, nb, a.ncells, posp, cell_sorted, beg, end, acc, ctrl, s);
+  // the wall force is fused into the FP32 gather kernels' epilogue (gamma = 7); the FP64 and
+  // symmetric kernels take the separate pass
+  if (!rc && p.wall_d > 0.0 && n > nb && (p.precision == SPHB_FP64 || sym || p.gamma != 7.0))
+    rc = launch_wall(p, g, n, nb, a.ncells, posp, cell_sorted, beg, end, acc, ctrl, s);
   if (rc || !sym) return rc;
   k_dt_f32<<<(unsigned)std::min<int64_t>((n + 255) / 256, 148 * 16), 256, 0, s>>>(
       p, n, nb, a.acc4, a.visc32, aux, ctrl);

@@ -163,7 +163,7 @@ __device__ __forceinline__ void eval_v12(const KArgs& a, const K32& c, const Own
   }
 }
 
-template <bool G7, bool EQM, bool WEND>
+template <bool G7, bool EQM, bool WEND, bool WALL>
 __global__ void __launch_bounds__(NW * 32, 1) k_interact_v12(KArgs a, K32 k32) {
   if (!step_live(a.ctrl)) return;
   constexpr int SCAP = Cfg<float>::SCAP;
@@ -625,6 +625,11 @@ __global__ void __launch_bounds__(NW * 32, 1) k_interact_v12(KArgs a, K32 k32) {
       }
     }
 
+    // fused wall force (extension): f64 sums per target over the batches
+    constexpr bool wall = WALL;  // (its own instantiation: none of it otherwise)
+    double wf[2][3] = {{0.0, 0.0, 0.0}, {0.0, 0.0, 0.0}};
+    bool whit[2] = {false, false};
+
     for (int q0 = 0; q0 < total; q0 += SCAP) {
       const int q1 = min(q0 + SCAP, total);
       if (warp == 0) stage_batch(a.posp, a.velr, sSeg, nseg, q0, q1, smA, 16u * V8_ROWS, mbar, lane);
@@ -744,6 +749,13 @@ __global__ void __launch_bounds__(NW * 32, 1) k_interact_v12(KArgs a, K32 k32) {
           }
         }
         drain(true);
+        if constexpr (wall) {
+#pragma unroll
+          for (int t = 0; t < 2; ++t)
+            if (valid[t] && isf[t])
+              whit[t] |= wall_batch(a, sSeg, nseg, q0, q1, smA, ox2[t], oy2[t], oz2[t], xlo[t], xhi[t],
+                                    rsy[t], rsz[t], wf[t][0], wf[t][1], wf[t][2]);
+        }
       }
       __syncthreads();
     }
@@ -784,6 +796,9 @@ __global__ void __launch_bounds__(NW * 32, 1) k_interact_v12(KArgs a, K32 k32) {
         fmag = fmag > 1e-30 ? fmag : 1e-30;
         dtf_min = fmin(dtf_min, __dsqrt_rn(xdiv(a.p.h, fmag)));
       }
+      if (whit[t])
+        wall_finish(a, i, step, (float)ax, (float)ay, (float)az, (float)dr, wf[t][0], wf[t][1],
+                    wf[t][2], dtf_min);
       dtcv_min = fmin(dtcv_min, xdiv(a.p.h, xadd((double)ocs[t], vd)));
     }
   }
