@@ -828,7 +828,9 @@ def main():
         "pair_evals_per_s": evals * world * args.steps / (total_ms * 1e-3),
         "stage_ms": {"nl": float(np.mean(nl_ms)), "pi": pi_mean, "su": float(np.mean(su_ms))},
         "counters_per_step": {"candidates": cand, "force_evals": evals, "true_pairs": true_pairs},
-        "roofline": {"bound": "fp32", "kernel": "k_interact_v8 (one launch: fluid + boundary targets)",
+        "roofline": {"bound": "fp32", "kernel": ("k_interact_v12 (paired)" if sim.pi_kernel == "paired" else
+                                                     "k_interact_v8 (" + str(sim.pi_kernel) + ")") +
+                     " -- one launch: fluid + boundary targets",
                      "achieved": achieved, "peak": fp32, "unit": "TFLOP/s",
                      "frac": achieved / fp32, "traffic": traffic,
                      "traffic_note": ("dram read+write bytes of one launch, " + traffic_src)
