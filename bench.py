@@ -409,7 +409,7 @@ def run_slabs(args, cfg_name, sc, system, prm, prec, world, rank, local):
     import torch.distributed as dist
     from paper_1110_3711_b200 import _lib, dslab
 
-    sim = dslab.DeviceSlabSim(system, prm, dslab.DevDistComm(), precision=prec,
+    sim = dslab.DeviceSlabSim(system, prm, dslab.make_dist_comm(), precision=prec,
                               rebalance_every=args.rebalance_every)
     me = sim.ranks[0]
     Ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
@@ -526,11 +526,17 @@ def run_slabs(args, cfg_name, sc, system, prm, prec, world, rank, local):
                   "pi_kernel_rank0": {_lib.SPHB_PI_PAIRED: "paired"}.get(me.pi_kernel, "gather"),
                   "pi_tuning_ms_rank0": tuning[0] if tuning else None,
                   "max_owned_per_gpu": int(owned.item()),
-                  "exchange": "edge bands (reach + 1 columns per neighbour) interacted first, "
-                              "packed with their forces and sent over NCCL send/recv on a "
-                              "high-priority comm stream while the interior targets run; the "
-                              "receiver integrates them (migrants + next halo); device all-reduce "
-                              "of dt; one host read per step hidden behind the edge interaction"},
+                  "exchange": ("edge bands (reach + 1 columns per neighbour) interacted first; "
+                               + ("one kernel packs them with their forces straight into the "
+                                  "neighbours' memory (CUDA IPC, NVLink P2P stores) and flags them, "
+                                  "on a comm stream next to the interior targets"
+                                  if getattr(sim.comm, "transport", "") == "peer" else
+                                  "packed with their forces and sent over NCCL send/recv on a "
+                                  "high-priority comm stream while the interior targets run")
+                               + "; the receiver integrates them (migrants + next halo); device "
+                                 "all-reduce of dt; one host read per step hidden behind the edge "
+                                 "interaction"),
+                  "band_transport": getattr(sim.comm, "transport", "nccl"),
         "interactions_per_s": true_pairs * args.steps / (total_ms * 1e-3),
         "pair_evals_per_s": evals * args.steps / (total_ms * 1e-3),
         "gpu_launches": args.steps * sim.launches_per_step(),
@@ -549,6 +555,8 @@ def run_slabs(args, cfg_name, sc, system, prm, prec, world, rank, local):
                                "decomposed step"}
     if rank == 0:
         print(json.dumps(line), flush=True)
+    if hasattr(sim.comm, "close"):
+        sim.comm.close()
     dist.destroy_process_group()
 
 

@@ -54,6 +54,8 @@ enum {
   SPHB_DIV_NONFINITE_STATE = 3,
   SPHB_DIV_SLAB_MARGIN = 4, /* X slabs only: a particle moved more than one cell column in one
                                step, beyond the edge bands the neighbours exchange */
+  SPHB_DIV_EXCHANGE_TIMEOUT = 5, /* X slabs, peer-memory transport: a neighbour's band did not
+                                    arrive within the wait limit */
 };
 
 enum { SPHB_FP32 = 0, SPHB_FP64 = 1 };
@@ -390,6 +392,22 @@ int sphb_band_integrate(sphb_workspace_t* ws, const sphb_params_t* prm, const sp
                         void* prev, int64_t* id, uint32_t* keys_next, uint32_t* keys_sorted,
                         sphb_ctrl_t* ctrl, sphb_stream_t s);
 int sphb_slab_tail(const sphb_grid_t* grid, int32_t* end, int64_t n_next, sphb_stream_t s);
+/* Peer-memory transport of the edge bands (NVLink P2P stores; one kernel packs AND sends):
+ * sphb_band_put is sphb_band_pack writing each side's rows straight into the neighbour's
+ * receive buffer (peer_l / peer_r: device pointers of the neighbours' memory, CUDA IPC), then --
+ * every block's stores fenced at system scope, the last block elected through `done` (a
+ * device uint32, zero between launches) -- stores `tag` into the neighbours' flag words
+ * (peer_flag_l / _r, release, system scope).  sphb_band_wait makes the stream wait until this
+ * rank's own flag words (flag_l / flag_r, NULL = no neighbour) reach `tag` (acquire, system
+ * scope); after ~10 s it records SPHB_DIV_EXCHANGE_TIMEOUT in ctrl and returns. */
+int sphb_band_put(const sphb_params_t* prm, const sphb_grid_t* grid, int32_t width, int32_t sides,
+                  const int32_t* beg, const int32_t* end, const int32_t* scratch,
+                  const void* posp_s, const void* velr_s, const void* prev_s, const int64_t* id_s,
+                  const void* acc, const void* drho, void* peer_l, void* peer_r,
+                  uint64_t* peer_flag_l, uint64_t* peer_flag_r, uint64_t tag, uint32_t* done,
+                  sphb_stream_t s);
+int sphb_band_wait(const uint64_t* flag_l, const uint64_t* flag_r, uint64_t tag, sphb_ctrl_t* ctrl,
+                   sphb_stream_t s);
 
 /* Closes the step: dt/counters into rec[step % rec_capacity], t_sim += dt, step += 1. */
 int sphb_step_end(sphb_ctrl_t* ctrl, const sphb_params_t* prm, sphb_step_record_t* rec,

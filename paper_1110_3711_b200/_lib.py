@@ -18,6 +18,7 @@ CSRC = os.path.join(HERE, "csrc")
 SPHB_OK, SPHB_E_INVALID, SPHB_E_CUDA, SPHB_E_CAPACITY = 0, -1, -2, -3
 SPHB_DIV_LEFT_DOMAIN, SPHB_DIV_NONFINITE_FORCES, SPHB_DIV_NONFINITE_STATE = 1, 2, 3
 SPHB_DIV_SLAB_MARGIN = 4  # X slabs: a particle moved more than one cell column in one step
+SPHB_DIV_EXCHANGE_TIMEOUT = 5  # X slabs, peer-memory transport: a band never arrived
 SPHB_COUNTERS_GATHER, SPHB_COUNTERS_SYMMETRIC = 0, 1
 SPHB_PI_GATHER, SPHB_PI_SYMMETRIC, SPHB_PI_PAIRED = 0, 1, 2
 SPHB_FP32, SPHB_FP64 = 0, 1
@@ -125,6 +126,9 @@ def lib():
         "sphb_band_pack": ([P, P, c_i32, c_i32, P, P, P, P, P, P, P, P, P, P, P, P], c_i32),
         "sphb_band_integrate": ([P, P, P, P, c_i64, c_i64, P, P, P, P, P, P, P, P], c_i32),
         "sphb_slab_tail": ([P, P, c_i64, P], c_i32),
+        "sphb_band_put": ([P, P, c_i32, c_i32, P, P, P, P, P, P, P, P, P, P, P, P, P,
+                           ctypes.c_uint64, P, P], c_i32),
+        "sphb_band_wait": ([P, P, ctypes.c_uint64, P, P], c_i32),
         "sphb_cell_hist": ([P, P, P, c_i64, P, P], c_i32),
         "sphb_step": ([P, P, P, c_i64, c_i64, P, P, P, c_i64, P], c_i32),
         "sphb_state_from_soa": ([c_i64, c_i64, P, P, P, P, P, P, P, P, P], c_i32),
@@ -152,6 +156,7 @@ EXPORTED = ("sphb_last_error", "sphb_version", "sphb_workspace_create", "sphb_wo
             "sphb_step_launch_count", "sphb_integrate_stage", "sphb_energy", "sphb_slab_tiles",
             "sphb_slab_count", "sphb_slab_scatter", "sphb_slab_unpack", "sphb_band_scratch_words",
             "sphb_band_count", "sphb_band_pack", "sphb_band_integrate", "sphb_slab_tail",
+            "sphb_band_put", "sphb_band_wait",
             "sphb_state_from_soa",
             "sphb_state_to_soa", "sphb_build_ranges", "sphb_dt_terms", "sphb_verlet_soa",
             "sphb_forces_f64")

@@ -624,6 +624,32 @@ int sphb_band_integrate(sphb_workspace_t* ws, const sphb_params_t* prm, const sp
                                (float4*)prev, id, keys_next, keys_sorted, ctrl, (cudaStream_t)s);
 }
 
+int sphb_band_put(const sphb_params_t* prm, const sphb_grid_t* grid, int32_t width, int32_t sides,
+                  const int32_t* beg, const int32_t* end, const int32_t* scratch,
+                  const void* posp_s, const void* velr_s, const void* prev_s, const int64_t* id_s,
+                  const void* acc, const void* drho, void* peer_l, void* peer_r,
+                  uint64_t* peer_flag_l, uint64_t* peer_flag_r, uint64_t tag, uint32_t* done,
+                  sphb_stream_t s) {
+  if (int rc = check_params(prm)) return rc;
+  if (int rc = check_band(grid, width, sides)) return rc;
+  SPHB_NONNULL(beg); SPHB_NONNULL(end); SPHB_NONNULL(scratch); SPHB_NONNULL(done);
+  SPHB_NONNULL(posp_s); SPHB_NONNULL(velr_s); SPHB_NONNULL(prev_s); SPHB_NONNULL(id_s);
+  SPHB_NONNULL(acc);
+  if (prm->precision == SPHB_FP64) SPHB_NONNULL(drho);
+  if (sides & 1) { SPHB_NONNULL(peer_l); SPHB_NONNULL(peer_flag_l); }
+  if (sides & 2) { SPHB_NONNULL(peer_r); SPHB_NONNULL(peer_flag_r); }
+  return launch_band_put(*prm, *grid, width, sides, beg, end, scratch, (const float4*)posp_s,
+                         (const float4*)velr_s, (const float4*)prev_s, id_s, acc, drho, peer_l,
+                         peer_r, (sides & 1) ? peer_flag_l : nullptr, (sides & 2) ? peer_flag_r : nullptr,
+                         tag, done, (cudaStream_t)s);
+}
+
+int sphb_band_wait(const uint64_t* flag_l, const uint64_t* flag_r, uint64_t tag, sphb_ctrl_t* ctrl,
+                   sphb_stream_t s) {
+  SPHB_NONNULL(ctrl);
+  return launch_band_wait(flag_l, flag_r, tag, ctrl, (cudaStream_t)s);
+}
+
 int sphb_slab_tail(const sphb_grid_t* grid, int32_t* end, int64_t n_next, sphb_stream_t s) {
   if (int rc = check_grid(grid)) return rc;
   SPHB_NONNULL(end);

@@ -308,14 +308,18 @@ __global__ void __launch_bounds__(1024) k_band_info(BandGeom b, const int32_t* _
   }
 }
 
-// one warp per segment: rows [sb, se) -> the side's send buffer at the segment's offset
+// one warp per segment: rows [sb, se) -> the side's send buffer at the segment's offset.  The
+// peer-memory transport passes the neighbours' receive buffers (NVLink stores) and their flag
+// words: every block fences its stores at system scope, the last one (elected on `done`)
+// releases `tag` into the flags.
 __global__ void __launch_bounds__(256) k_band_pack(
     BandGeom b, const int32_t* __restrict__ beg, const int32_t* __restrict__ end,
     const int32_t* __restrict__ scratch, const float4* __restrict__ posp_s,
     const float4* __restrict__ velr_s, const float4* __restrict__ prev_s,
     const int64_t* __restrict__ id_s, const void* __restrict__ accv,
     const double* __restrict__ drho, bool f32, BandRow* __restrict__ send_l,
-    BandRow* __restrict__ send_r) {
+    BandRow* __restrict__ send_r, unsigned long long* flag_l, unsigned long long* flag_r,
+    unsigned long long tag, uint32_t* done) {
   const int lane = threadIdx.x & 31;
   const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
   for (int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); w < 2 * b.nseg;
@@ -353,6 +357,34 @@ __global__ void __launch_bounds__(256) k_band_pack(
       q.pad = 0;
       out[k] = q;
     }
+  }
+  if (done) {  // peer-memory transport: signal the neighbours once every block's rows are out
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0 && atomicAdd(done, 1u) == gridDim.x - 1) {
+      *done = 0u;
+      __threadfence_system();
+      if (flag_l) asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(flag_l), "l"(tag) : "memory");
+      if (flag_r) asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(flag_r), "l"(tag) : "memory");
+    }
+  }
+}
+
+// the receiving side: wait for this rank's flag words (written by the neighbours' k_band_pack)
+__global__ void k_band_wait(const unsigned long long* flag_l, const unsigned long long* flag_r,
+                            unsigned long long tag, sphb_ctrl_t* ctrl) {
+  const unsigned long long* f = threadIdx.x == 0 ? flag_l : flag_r;
+  if (threadIdx.x > 1 || !f) return;
+  const long long t0 = clock64();
+  for (;;) {
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(f) : "memory");
+    if (v >= tag) return;
+    if (clock64() - t0 > 20000000000ll) {  // ~10 s at 2 GHz: the neighbour is gone
+      raise_div(ctrl, ctrl->step, SPHB_DIV_EXCHANGE_TIMEOUT, 0);
+      return;
+    }
+    __nanosleep(200);
   }
 }
 
@@ -479,8 +511,37 @@ int launch_band_pack(const sphb_params_t& p, const sphb_grid_t& g, int width, in
   if (blocks > 148 * 8) blocks = 148 * 8;
   k_band_pack<<<(unsigned)blocks, 256, 0, s>>>(b, beg, end, scratch, posp_s, velr_s, prev_s, id_s,
                                                acc, (const double*)drho, p.precision == SPHB_FP32,
-                                               (BandRow*)send_l, (BandRow*)send_r);
+                                               (BandRow*)send_l, (BandRow*)send_r, nullptr, nullptr,
+                                               0ull, nullptr);
   return sphb_check_launch("k_band_pack");
+}
+
+int launch_band_put(const sphb_params_t& p, const sphb_grid_t& g, int width, int sides,
+                    const int32_t* beg, const int32_t* end, const int32_t* scratch,
+                    const float4* posp_s, const float4* velr_s, const float4* prev_s,
+                    const int64_t* id_s, const void* acc, const void* drho, void* peer_l,
+                    void* peer_r, uint64_t* flag_l, uint64_t* flag_r, uint64_t tag, uint32_t* done,
+                    cudaStream_t s) {
+  const BandGeom b = band_geom(g, width, sides);
+  if (!sides) return SPHB_OK;
+  // a few CTAs: the put runs on a comm stream next to the interior interaction, whose
+  // persistent CTAs take the other SMs; 32 x 8 warps keep enough NVLink stores in flight
+  int64_t blocks = (2 * b.nseg + 7) / 8;
+  if (blocks > 32) blocks = 32;
+  k_band_pack<<<(unsigned)blocks, 256, 0, s>>>(b, beg, end, scratch, posp_s, velr_s, prev_s, id_s,
+                                               acc, (const double*)drho, p.precision == SPHB_FP32,
+                                               (BandRow*)peer_l, (BandRow*)peer_r,
+                                               (unsigned long long*)flag_l, (unsigned long long*)flag_r,
+                                               (unsigned long long)tag, done);
+  return sphb_check_launch("k_band_pack (peer)");
+}
+
+int launch_band_wait(const uint64_t* flag_l, const uint64_t* flag_r, uint64_t tag, sphb_ctrl_t* ctrl,
+                     cudaStream_t s) {
+  if (!flag_l && !flag_r) return SPHB_OK;
+  k_band_wait<<<1, 32, 0, s>>>((const unsigned long long*)flag_l, (const unsigned long long*)flag_r,
+                                (unsigned long long)tag, ctrl);
+  return sphb_check_launch("k_band_wait");
 }
 
 int launch_band_integrate(sphb_workspace* ws, const sphb_params_t& p, const sphb_grid_t& g,

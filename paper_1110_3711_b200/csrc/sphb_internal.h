@@ -144,6 +144,14 @@ int launch_band_integrate(sphb_workspace* ws, const sphb_params_t& p, const sphb
                           float4* prev, int64_t* id, uint32_t* keys_next, uint32_t* keys_sorted,
                           sphb_ctrl_t* ctrl, cudaStream_t s);
 int launch_slab_tail(const sphb_grid_t& g, int32_t* end, int64_t n_next, cudaStream_t s);
+int launch_band_put(const sphb_params_t& p, const sphb_grid_t& g, int width, int sides,
+                    const int32_t* beg, const int32_t* end, const int32_t* scratch,
+                    const float4* posp_s, const float4* velr_s, const float4* prev_s,
+                    const int64_t* id_s, const void* acc, const void* drho, void* peer_l,
+                    void* peer_r, uint64_t* flag_l, uint64_t* flag_r, uint64_t tag, uint32_t* done,
+                    cudaStream_t s);
+int launch_band_wait(const uint64_t* flag_l, const uint64_t* flag_r, uint64_t tag, sphb_ctrl_t* ctrl,
+                     cudaStream_t s);
 int launch_cell_hist(sphb_workspace* ws, const sphb_grid_t& g, const uint32_t* keys, int64_t n,
                      const sphb_ctrl_t* ctrl, cudaStream_t s);
 int launch_step_end(sphb_ctrl_t* ctrl, const sphb_params_t& p, sphb_step_record_t* rec, int64_t cap,

@@ -201,6 +201,79 @@ class DevDistComm:
         return [done]
 
 
+class DevPeerComm(DevDistComm):
+    """DevDistComm whose edge bands travel by peer-memory stores instead of NCCL: each rank's
+    band kernel (sphb_band_put) writes its rows straight into the neighbours' receive buffers
+    -- CUDA IPC mappings of the neighbours' device memory, NVLink P2P stores on a multi-GPU
+    box -- and releases a step tag into their flag words; a receiver's stream waits for its
+    flags (sphb_band_wait) before integrating.  Pack and send are one kernel, on a
+    high-priority comm stream with 32 CTAs, next to the interior interaction.  Receive buffers
+    are double-buffered by the tag's parity (a sender cannot run two steps ahead: it needs the
+    receiver's band of the step in between).  The control plane (band sizes, dt all-reduce,
+    re-layouts) stays on torch.distributed.  Several processes may share one GPU (the CPU-side
+    control then runs over gloo): IPC handles of one device open in another process."""
+
+    transport = "peer"
+
+    def __init__(self, cap_rows: int = 1 << 16):
+        super().__init__()
+        self.dev = torch.device("cuda", torch.cuda.current_device())
+        self.pstream = torch.cuda.Stream(priority=-1)
+        self.done = torch.zeros(1, dtype=torch.int32, device=self.dev)
+        self.flags = torch.zeros(2, dtype=torch.int64, device=self.dev)  # from left, from right
+        self.tag = 0
+        self.cap = 0
+        self.put_ev = torch.cuda.Event()
+        self._share(int(cap_rows))
+
+    def _share(self, cap):
+        """(Re)allocate the receive buffers and map the neighbours' (collective)."""
+        from torch.multiprocessing.reductions import rebuild_cuda_tensor, reduce_tensor
+        torch.cuda.synchronize()
+        self.cap = cap
+        self.recv = [torch.zeros((2, cap, BAND_WORDS), dtype=torch.float32, device=self.dev)
+                     for _ in range(2)]
+        mine = [reduce_tensor(t)[1] for t in (self.recv[0], self.recv[1], self.flags)]
+        allh = [None] * self.nranks
+        self.dist.all_gather_object(allh, mine, group=self.cpu_group)
+        r, n = self.rank, self.nranks
+        self.peer, self.peer_flag = [None, None], [None, None]
+        err = None
+        try:
+            if r > 0:  # my left band lands in the left neighbour's "from right" buffer and flag
+                self.peer[0] = rebuild_cuda_tensor(*allh[r - 1][1])
+                self.peer_flag[0] = rebuild_cuda_tensor(*allh[r - 1][2])[1:2]
+            if r < n - 1:
+                self.peer[1] = rebuild_cuda_tensor(*allh[r + 1][0])
+                self.peer_flag[1] = rebuild_cuda_tensor(*allh[r + 1][2])[0:1]
+        except Exception as e:  # noqa: BLE001 -- raised after the collective below
+            err = e
+        self.dist.barrier(group=self.cpu_group)
+        if err is not None:
+            raise err
+
+    def ensure_capacity(self, max_rows: int):
+        """Every rank calls this with the same number (the all-gathered band sizes)."""
+        if max_rows > self.cap:
+            self._share(int(max_rows * 1.3) + 1024)
+
+    def close(self):
+        """Drop the neighbours' mappings before the producers exit (collective)."""
+        torch.cuda.synchronize()
+        self.peer, self.peer_flag = [None, None], [None, None]
+        self.dist.barrier(group=self.cpu_group)
+
+    def next_tag(self) -> int:
+        self.tag += 1
+        return self.tag
+
+    def recv_view(self, side: int, tag: int):
+        return self.recv[side][tag & 1]
+
+    def peer_view(self, side: int, tag: int):
+        return self.peer[side][tag & 1] if self.peer[side] is not None else None
+
+
 # ------------------------------------------------------------------ one rank
 class _Arrays:
     def __init__(self, cap, dev):
@@ -411,6 +484,24 @@ class DevRank:
                                         _ptr(sl), _ptr(sr), s), "sphb_band_pack")
         self.pack_ev.record()
 
+    def phase_put(self, comm, tag):
+        """Peer transport: pack the bands straight into the neighbours' buffers (one kernel on
+        the comm stream, after the edge interaction) and flag them."""
+        L, sa = _lib.lib(), self.s
+        comp = torch.cuda.current_stream()
+        ev = torch.cuda.Event()
+        ev.record(comp)
+        ps = comm.pstream
+        ps.wait_event(ev)
+        pl, pr = comm.peer_view(0, tag), comm.peer_view(1, tag)
+        fl, fr = comm.peer_flag
+        _lib.check(L.sphb_band_put(_lib.ref(self.prm), _lib.ref(self.grid), self.width, self.sides,
+                                   _ptr(self.beg), _ptr(self.end), _ptr(self.scratch), _ptr(sa.posp),
+                                   _ptr(sa.velr), _ptr(sa.prev), _ptr(sa.id), _ptr(sa.acc),
+                                   _ptr(sa.drho), _ptr(pl), _ptr(pr), _ptr(fl), _ptr(fr), tag,
+                                   _ptr(comm.done), ps.cuda_stream), "sphb_band_put")
+        comm.put_ev.record(ps)
+
     def phase_interior(self):
         if self.sides:
             self._interact(self.inner_grids)
@@ -420,11 +511,22 @@ class DevRank:
     def dt_words(self):
         return self.ctrl.view(torch.int64)[5:7]
 
-    def phase_update(self, recv_rows, recv_event):
-        """K7 on the live rows, the received bands integrated and appended, step end."""
+    def phase_update(self, recv_rows, recv_event, peer=None):
+        """K7 on the live rows, the received bands integrated and appended, step end.
+        ``peer``: (comm, tag) of the peer-memory transport (wait for the flags, read its
+        buffers), else the bands are in self.recv."""
+        comp = torch.cuda.current_stream()
         if recv_event is not None:
-            torch.cuda.current_stream().wait_event(recv_event)
+            comp.wait_event(recv_event)
         L, s, ws = _lib.lib(), _stream(), self.ws.handle
+        bufs = self.recv
+        if peer is not None:
+            comm, tag = peer
+            comp.wait_event(comm.put_ev)  # the sorted arrays are read by our own put
+            fl = comm.flags[0:1] if self.sides & 1 else None
+            fr = comm.flags[1:2] if self.sides & 2 else None
+            _lib.check(L.sphb_band_wait(_ptr(fl), _ptr(fr), tag, _ptr(self.ctrl), s), "sphb_band_wait")
+            bufs = [comm.recv_view(0, tag), comm.recv_view(1, tag)]
         g, p, a, sa = _lib.ref(self.grid), _lib.ref(self.prm), self.a, self.s
         old = self._retired[0] if self._retired else None  # sorted arrays of a regrown rank
         src = old if old is not None else sa
@@ -436,7 +538,7 @@ class DevRank:
         for side in (0, 1):
             cnt = int(recv_rows[side])
             if cnt:
-                _lib.check(L.sphb_band_integrate(ws, p, g, _ptr(self.recv[side]), cnt, dst,
+                _lib.check(L.sphb_band_integrate(ws, p, g, _ptr(bufs[side]), cnt, dst,
                                                  _ptr(a.posp), _ptr(a.velr), _ptr(a.prev),
                                                  _ptr(a.id), _ptr(a.key), _ptr(self.keys_sorted),
                                                  _ptr(self.ctrl), s), "sphb_band_integrate")
@@ -687,25 +789,36 @@ class DeviceSlabSim:
         tab = self.comm.host_allgather(mine)
         self._raise_errors(tab[:, 2])
         items, recv_rows = [], []
+        peer = getattr(self.comm, "transport", None) == "peer" and n > 1
+        tag = None
+        if peer:  # every rank sees the same table: the same capacity decision
+            self.comm.ensure_capacity(int(tab[:, :2].max()))
+            tag = self.comm.next_tag()
         for r in ranks:
             rows = band_recv_rows(tab, r.rank, n)
             recv_rows.append(rows)
             n_next = r.n_live + rows[0] + rows[1]
             if n_next > r.cap:
                 r._grow_mid_step(n_next)
+            if peer:
+                r.phase_put(self.comm, tag)
+                continue
             r.phase_pack()
             rl = r._buf(r.recv, 0, rows[0], BAND_WORDS)
             rr = r._buf(r.recv, 1, rows[1], BAND_WORDS)
             items.append(dict(send_l=(r.send[0], r.band_rows[0]), send_r=(r.send[1], r.band_rows[1]),
                               recv_l=(rl, rows[0]), recv_r=(rr, rows[1])))
-        done = self.comm.band_sendrecv(items, [r.pack_ev for r in ranks]) if n > 1 else [None] * len(ranks)
+        if peer:
+            done = [None] * len(ranks)
+        else:
+            done = self.comm.band_sendrecv(items, [r.pack_ev for r in ranks]) if n > 1 else [None] * len(ranks)
         for r in ranks:
             r.phase_interior()
         # the step's dt is global (min over ranks); the counters stay per rank in each rank's
         # record ring and are summed over ranks only when read (records())
         self.comm.allreduce([r.dt_words() for r in ranks], "min")
         for r, rows, ev in zip(ranks, recv_rows, done):
-            r.phase_update(rows, ev)
+            r.phase_update(rows, ev, (self.comm, tag) if peer else None)
         self.step_index += 1
 
     def run(self, steps):
@@ -817,4 +930,27 @@ def estimate_steps_per_sync() -> int:
     return 1
 
 
-__all__ = ["DeviceSlabSim", "DevLoopbackComm", "DevDistComm", "rank_layout", "band_recv_rows"]
+def make_dist_comm(transport: str | None = None):
+    """The production communicator: edge bands by peer-memory stores (DevPeerComm) unless
+    ``transport`` (or $SPHB_SLAB_TRANSPORT) is "nccl"; falls back to NCCL send/recv when the
+    peer mappings cannot be set up on every rank (decided collectively)."""
+    import os
+    import torch.distributed as dist
+    want = transport or os.environ.get("SPHB_SLAB_TRANSPORT", "peer")
+    if want == "peer" and dist.get_world_size() > 1:
+        ok, err = True, None
+        try:
+            comm = DevPeerComm()
+        except Exception as e:  # noqa: BLE001 -- IPC / P2P unavailable on this box
+            ok, err, comm = False, e, None
+        flags = [None] * dist.get_world_size()
+        dist.all_gather_object(flags, ok)
+        if all(flags):
+            return comm
+        print(f"[dslab] peer-memory band transport unavailable ({err}); using NCCL send/recv",
+              flush=True)
+    return DevDistComm()
+
+
+__all__ = ["DeviceSlabSim", "DevLoopbackComm", "DevDistComm", "DevPeerComm", "make_dist_comm",
+           "rank_layout", "band_recv_rows"]

@@ -915,7 +915,8 @@ def test_device_resident_slabs_match_single_domain(nslabs, precision):
     assert int(fl.sum()) == system.count_fluid
 
 
-def test_device_slabs_two_processes(tmp_path):
+@pytest.mark.parametrize("transport", ["copy", "peer"])
+def test_device_slabs_two_processes(tmp_path, transport):
     """DeviceSlabSim with DevDistComm across two real processes (torchrun, gloo: they share
     this box's GPU; NCCL only changes the transport): every step's dt and counters equal the
     single-domain FP64 run's, the id set is conserved and the 20-step state matches."""
@@ -932,7 +933,7 @@ def test_device_slabs_two_processes(tmp_path):
     proc = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
                            "--nproc-per-node", "2", "--master-addr", "127.0.0.1", "--master-port",
                            str(port), os.path.join(root, "tests", "slab_mp_worker.py"), str(out),
-                           str(steps)], capture_output=True, text=True, timeout=600, cwd=root)
+                           str(steps), transport], capture_output=True, text=True, timeout=600, cwd=root)
     assert proc.returncode == 0, proc.stderr[-3000:]
     z = np.load(out)
     sc = sph.Scenario(dp=0.006)
