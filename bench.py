@@ -536,11 +536,11 @@ def run_slabs(args, cfg_name, sc, system, prm, prec, world, rank, local):
                                + "; the receiver integrates them (migrants + next halo); device "
                                  "all-reduce of dt; one host read per step hidden behind the edge "
                                  "interaction"),
-                  "band_transport": getattr(sim.comm, "transport", "nccl"),
+                  "band_transport": getattr(sim.comm, "transport", "nccl")},
         "interactions_per_s": true_pairs * args.steps / (total_ms * 1e-3),
         "pair_evals_per_s": evals * args.steps / (total_ms * 1e-3),
         "gpu_launches": args.steps * sim.launches_per_step(),
-        "roofline": {"bound": "fp32", "kernel": "k_interact_v8 (per GPU, owned targets)",
+        "roofline": {"bound": "fp32", "kernel": "the interaction kernel (per GPU, owned targets)",
                      "achieved": achieved, "peak": fp32, "unit": "TFLOP/s", "frac": achieved / fp32,
                      "traffic": None,
                      "work": f"{FLOP_PER_CAND}*candidates + {FLOP_PER_EVAL}*evals per step / GPUs",
