@@ -35,6 +35,8 @@
 
 #include <climits>
 
+#include <cstdlib>
+
 #include "sphb_common.cuh"
 #include "sphb_internal.h"
 
@@ -305,6 +307,43 @@ __device__ __forceinline__ void wall_finish(const KArgs& a, int64_t i, int64_t s
     raise_div(a.ctrl, step, SPHB_DIV_NONFINITE_FORCES, 0);
 }
 
+// ------------------------------------------------------------------ candidate counts
+// A target's candidate count is the sum of its stencil rows' range lengths (the reference's
+// loop count, kernels.py:355-371).  The lanes of one cell share it, so each distinct (x range,
+// row offset in a brick, list) of the warp is summed once by all 32 lanes in parallel over the
+// staged rows (lane l: rows l, l + 32, ...) and taken by the lanes that have it -- at h/2
+// cells a warp holds ~4 cells x 8 targets over 2 x 36 staged rows.
+__device__ __forceinline__ unsigned long long cand_count(const KArgs& a, const Seg* sSeg, int nseg,
+                                                         bool valid, bool isf, int xlo, int xhi,
+                                                         int rsy, int rsz, int lane) {
+  const int reach = a.g.reach;
+  const uint32_t klo = (uint32_t)xlo | ((uint32_t)xhi << 16);
+  const uint32_t khi = (uint32_t)rsy | ((uint32_t)rsz << 1) | (isf ? 4u : 0u);
+  uint32_t todo = __ballot_sync(SPHB_FULL, valid);
+  unsigned long long mine = 0;
+  while (todo) {
+    const int l = __ffs(todo) - 1;
+    const uint32_t plo = __shfl_sync(SPHB_FULL, klo, l), phi = __shfl_sync(SPHB_FULL, khi, l);
+    const int pxlo = (int)(plo & 0xffffu), pxhi = (int)(plo >> 16);
+    const int psy = (int)(phi & 1u), psz = (int)((phi >> 1) & 1u);
+    const bool pf = (phi & 4u) != 0u;
+    int part = 0;
+    for (int k = lane; k < nseg; k += 32) {
+      const Seg sg = sSeg[k];
+      if (sg.g1 <= sg.g0 || (!pf && sg.rowoff < a.ncells)) continue;  // boundary targets: fluid rows
+      const int dy = (sg.dyz & 255) - 16, dz = (sg.dyz >> 8) - 16;
+      if (abs(dy - psy) > reach || abs(dz - psz) > reach) continue;
+      part += a.end[sg.rowoff + pxhi] - a.beg[sg.rowoff + pxlo];
+    }
+    part = (int)__reduce_add_sync(SPHB_FULL, (uint32_t)part);
+    const bool same = valid && klo == plo && khi == phi;
+    if (same) mine = (unsigned long long)part;
+    todo &= ~__ballot_sync(SPHB_FULL, same);
+  }
+  if (valid && isf) mine -= 1;  // the reference skips j == i before counting (kernels.py:369-371)
+  return mine;
+}
+
 // ------------------------------------------------------------------ pair math
 // FP32 (physics.py:183-220 restated for FP32 CUDA cores).  Branch-free cubic spline:
 // W ~ t^3/4 - u^3, dW/dq ~ -3/4 t^2 + 3 u^2 with t = 2 - q, u = max(1 - q, 0).
@@ -517,7 +556,7 @@ __global__ void __launch_bounds__(32) k_blocks(sphb_grid_t g, int64_t ncells,
                                                const int32_t* __restrict__ end,
                                                int32_t* __restrict__ row_off,
                                                int4* __restrict__ blk, sphb_ctrl_t* ctrl,
-                                               int brick) {
+                                               int brick, int maxc) {
   // one warp per cell row: the lanes stage the row's cumulative ends (both lists) in shared
   // memory, lane 0 makes the greedy cut
   extern __shared__ int32_t s_ends[];  // [span] fluid ends, then [span] boundary ends
@@ -565,7 +604,10 @@ __global__ void __launch_bounds__(32) k_blocks(sphb_grid_t g, int64_t ncells,
         for (int k = 0; k < span; ++k) {
           const int x = g.tx0 + k, c = s_ends[k], cf = s_ends[span + k];
           if (c == 0) continue;
-          if (block_slots(totf + cf, tot + c) > BT && tot > 0) {
+          // close before x when the targets would not fit, or when the block's columns would
+          // exceed maxc (the FP16 tensor-core screen's coordinate range, else the kernel falls
+          // back to the CUDA-core screen)
+          if ((block_slots(totf + cf, tot + c) > BT || (xa >= 0 && x - xa + 1 > maxc)) && tot > 0) {
             emit(make_int4(0, 0, 0, 0), make_int4(key0, xa, xl, 1));
             tot = totf = 0;
             xa = -1;
@@ -625,7 +667,8 @@ __global__ void __launch_bounds__(32) k_blocks(sphb_grid_t g, int64_t ncells,
         const int x = g.tx0 + k;
         const int32_t fe = s_ends[k], be = s_ends[span + k];
         if (fe == fcur && be == bcur) continue;  // empty cell
-        if (block_slots(fe - f0, (fe - f0) + (be - b0)) > BT && (fcur > f0 || bcur > b0)) {  // close before this cell
+        if ((block_slots(fe - f0, (fe - f0) + (be - b0)) > BT || (xa >= 0 && x - xa + 1 > maxc)) &&
+            (fcur > f0 || bcur > b0)) {  // close before this cell
           emit(make_int4(f0, fcur, b0, bcur), xa, xl);
           f0 = fcur;
           b0 = bcur;
@@ -1647,25 +1690,8 @@ __global__ void __launch_bounds__(NW * 32, V8_MINB) k_interact_v8(KArgs a, K32 k
         }
       }
       if (isf) cand -= 1;
-    } else if (valid) {  // candidate count = sum of this lane's row-range lengths (loads batched by 6)
-      for (int k0 = 0; k0 < nseg; k0 += 6) {
-        int e[6], b[6];
-#pragma unroll
-        for (int u = 0; u < 6; ++u) {
-          e[u] = b[u] = 0;
-          const int k = k0 + u;
-          if (k < nseg) {
-            const Seg sg = sSeg[k];
-            if (sg.g1 > sg.g0 && (isf || sg.rowoff >= a.ncells) && in_rows(sg.dyz)) {
-              e[u] = a.end[sg.rowoff + xhi];
-              b[u] = a.beg[sg.rowoff + xlo];
-            }
-          }
-        }
-#pragma unroll
-        for (int u = 0; u < 6; ++u) cand += (unsigned long long)(e[u] - b[u]);
-      }
-      if (isf) cand -= 1;
+    } else if (!V8_SYM) {
+      cand = cand_count(a, sSeg, nseg, valid, isf, xlo, xhi, rsy, rsz, lane);
     }
 
     // A / C fragments of the tensor-core screen: target row r = 16 m + g (+ 8) holds
@@ -2318,11 +2344,20 @@ int launch_interact(sphb_workspace* ws, const sphb_params_t& p, const sphb_grid_
   // (the 512-target build cuts bricks at every reach: 2 x 2 rows x 2 lattice cells at n = 1)
   const int brick = ((g.reach == 2 || BT == 512 || SPHB_PAIR) && p.order == 0 && p.precision == SPHB_FP32 && !V8_SYM) ? 1 : 0;
   const int64_t nunits = brick ? (int64_t)((g.dims[1] + 1) / 2) * ((g.dims[2] + 1) / 2) : nrows;
-  k_blocks<true><<<gb, 32, sm_blocks, s>>>(g, a.ncells, beg, end, ws->row_off, ws->blocks, ctrl, brick);
+  // block x extent: columns [cxa - r, cxb + r] must stay within the FP16 screen's +-4 (2h)
+  // around the block centre (use16 in the kernels), span <= 16 / (cell_size / h) columns
+  int maxc = INT_MAX;
+  if (p.precision == SPHB_FP32) {
+    const int span = (int)floor(16.0 / (g.cell_size * p.invh) + 1e-9);
+    maxc = span - 2 * g.reach > 1 ? span - 2 * g.reach : 1;
+  }
+  static const char* maxc_env = getenv("SPHB_BLOCK_MAXC");  // A/B experiments only
+  if (maxc_env && atoi(maxc_env) > 0) maxc = atoi(maxc_env);
+  k_blocks<true><<<gb, 32, sm_blocks, s>>>(g, a.ncells, beg, end, ws->row_off, ws->blocks, ctrl, brick, maxc);
   if (int rc = sphb_check_launch("k_blocks count")) return rc;
   k_blocks_scan<<<1, KB_SCAN, 0, s>>>(ws->row_off, nunits, ctrl);
   if (int rc = sphb_check_launch("k_blocks_scan")) return rc;
-  k_blocks<false><<<gb, 32, sm_blocks, s>>>(g, a.ncells, beg, end, ws->row_off, ws->blocks, ctrl, brick);
+  k_blocks<false><<<gb, 32, sm_blocks, s>>>(g, a.ncells, beg, end, ws->row_off, ws->blocks, ctrl, brick, maxc);
   if (int rc = sphb_check_launch("k_blocks")) return rc;
   // one launch for both item classes: fluid targets (F-F + F-B) and boundary targets (B-F,
   // drho + visc only) of the same cells share the staged candidates

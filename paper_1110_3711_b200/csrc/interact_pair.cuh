@@ -489,30 +489,12 @@ __global__ void __launch_bounds__(NW * 32, 1) k_interact_v12(KArgs a, K32 k32) {
       s[k].ax = s[k].ay = s[k].az = s[k].dr = s[k].hits = bc(0.0f);
       s[k].vd0 = s[k].vd1 = 0.0f;
     }
-    // candidate counts: the sum of each target's stencil-row range lengths (loads batched by 6)
-    unsigned long long cand[2] = {0, 0};
+    // candidate counts: the sum of each target's stencil-row range lengths, per distinct
+    // (x range, row, list) of the warp (cand_count)
+    unsigned long long cand[2];
 #pragma unroll
-    for (int t = 0; t < 2; ++t) {
-      if (!valid[t]) continue;
-      for (int k0 = 0; k0 < nseg; k0 += 6) {
-        int e[6], b[6];
-#pragma unroll
-        for (int u = 0; u < 6; ++u) {
-          e[u] = b[u] = 0;
-          const int k = k0 + u;
-          if (k < nseg) {
-            const Seg sg = sSeg[k];
-            if (sg.g1 > sg.g0 && (isf[t] || sg.rowoff >= a.ncells) && in_rows(sg.dyz, t)) {
-              e[u] = a.end[sg.rowoff + xhi[t]];
-              b[u] = a.beg[sg.rowoff + xlo[t]];
-            }
-          }
-        }
-#pragma unroll
-        for (int u = 0; u < 6; ++u) cand[t] += (unsigned long long)(e[u] - b[u]);
-      }
-      if (isf[t]) cand[t] -= 1;
-    }
+    for (int t = 0; t < 2; ++t)
+      cand[t] = cand_count(a, sSeg, nseg, valid[t], isf[t], xlo[t], xhi[t], rsy[t], rsz[t], lane);
 
     // A fragments of the screen: M-tile m holds target slot m / 2 of lanes 16 (m % 2) + row
     // (rows g, g + 8 of the tile); C = |x|^2 - thr, or NOHIT for a target the row must skip
