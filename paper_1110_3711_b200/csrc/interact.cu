@@ -1594,6 +1594,10 @@ __global__ void __launch_bounds__(NW * 32, V8_MINB) k_interact_v8(KArgs a, K32 k
     }
     __syncthreads();
     const int total = s_nseg_tot;
+    // the first staging batch goes out now: its bulk copies land while the lanes set up their
+    // targets, windows and candidate counts (global loads)
+    if (warp == 0 && total > 0)  // (no batch, no mbarrier phase: an empty block stages nothing)
+      stage_batch(a.posp, a.velr, sSeg, nseg, 0, min(SCAP, total), smA, 16u * V8_ROWS, mbar, lane);
 
     const int t = warp * 32 + lane;
     int nf = bb.y - bb.x, nbt = bb.w - bb.z, i, rsy = 0, rsz = 0;
@@ -1823,7 +1827,7 @@ __global__ void __launch_bounds__(NW * 32, V8_MINB) k_interact_v8(KArgs a, K32 k
       // ---- stage rows [q0, q1): one TMA bulk copy per (stencil row, array) -- the sorted
       // posp rows are (x, y, z, prrho), velr rows (vx, vy, vz, rho) -- then the 8-B screen
       // records from shared memory
-      if (warp == 0) stage_batch(a.posp, a.velr, sSeg, nseg, q0, q1, smA, 16u * V8_ROWS, mbar, lane);
+      if (warp == 0 && q0 > 0) stage_batch(a.posp, a.velr, sSeg, nseg, q0, q1, smA, 16u * V8_ROWS, mbar, lane);
       {  // wait for the bytes (phase parity flips per batch)
         uint32_t done = 0;
         while (!done)

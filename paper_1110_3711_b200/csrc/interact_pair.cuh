@@ -317,6 +317,9 @@ __global__ void __launch_bounds__(NW * 32, 1) k_interact_v12(KArgs a, K32 k32) {
     }
     __syncthreads();
     const int total = s_nseg_tot;
+    // the first staging batch goes out now: its bulk copies land during the targets' setup
+    if (warp == 0 && total > 0)  // (no batch, no mbarrier phase: an empty block stages nothing)
+      stage_batch(a.posp, a.velr, sSeg, nseg, 0, min(SCAP, total), smA, 16u * V8_ROWS, mbar, lane);
 
     // ---- the lane's two targets: block slots 64 w + 2 lane + t
     // slots: fluid targets [0, nf), boundary targets from the even slot nfp = pad2(nf) on, so
@@ -614,7 +617,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_interact_v12(KArgs a, K32 k32) {
 
     for (int q0 = 0; q0 < total; q0 += SCAP) {
       const int q1 = min(q0 + SCAP, total);
-      if (warp == 0) stage_batch(a.posp, a.velr, sSeg, nseg, q0, q1, smA, 16u * V8_ROWS, mbar, lane);
+      if (warp == 0 && q0 > 0) stage_batch(a.posp, a.velr, sSeg, nseg, q0, q1, smA, 16u * V8_ROWS, mbar, lane);
       {
         uint32_t done = 0;
         while (!done)
