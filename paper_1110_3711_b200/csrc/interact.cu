@@ -1486,13 +1486,15 @@ __global__ void __launch_bounds__(NW * 32, V8_MINB) k_interact_v8(KArgs a, K32 k
       s_blk = (int)nxt;
       s_bb[0] = nxt_b;
       s_bb[1] = nxt_m;
+    }
+    __syncthreads();
+    if (tid == 0) {  // the next record: its atomic and loads overlap this block (not the barrier)
       nxt = atomicAdd(&a.ctrl->tile_next[0], 1u);
       if (nxt < nblocks) {
         nxt_b = a.blocks[2 * nxt];
         nxt_m = a.blocks[2 * nxt + 1];
       }
     }
-    __syncthreads();
     const uint32_t blk = (uint32_t)s_blk;
     if (blk >= nblocks) break;
     const int4 bb = s_bb[0], bm = s_bb[1];
