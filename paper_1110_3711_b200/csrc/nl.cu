@@ -154,7 +154,8 @@ __global__ void __launch_bounds__(SORT_BLOCK) k_radix_hist(const uint32_t* __res
   }
 }
 
-__global__ void __launch_bounds__(1024) k_radix_rowscan(uint32_t* __restrict__ hist, int64_t ntiles,
+constexpr int RS_BLOCK = 256;  // k_radix_rowscan threads (a skipped pass dispatches 256 x 256 threads)
+__global__ void __launch_bounds__(RS_BLOCK) k_radix_rowscan(uint32_t* __restrict__ hist, int64_t ntiles,
                                                         uint32_t* __restrict__ digit_total,
                                                         const sphb_ctrl_t* ctrl,
                                                         const uint32_t* skip) {
@@ -162,11 +163,11 @@ __global__ void __launch_bounds__(1024) k_radix_rowscan(uint32_t* __restrict__ h
   __shared__ uint32_t s_warp[32];
   uint32_t* row = hist + (int64_t)blockIdx.x * ntiles;
   uint32_t running = 0;
-  for (int64_t base = 0; base < ntiles; base += 1024) {
+  for (int64_t base = 0; base < ntiles; base += RS_BLOCK) {
     int64_t k = base + threadIdx.x;
     uint32_t v = k < ntiles ? row[k] : 0;
     uint32_t total;
-    uint32_t ex = block_exclusive_scan<1024>(v, &total, s_warp);
+    uint32_t ex = block_exclusive_scan<RS_BLOCK>(v, &total, s_warp);
     if (k < ntiles) row[k] = running + ex;
     running += total;
   }
@@ -678,9 +679,10 @@ static void radix_passes(sphb_workspace* ws, const sphb_grid_t& g, const uint32_
     uint32_t* kout = last ? (keys_sorted ? keys_sorted : ws->keys_tmp[pass & 1]) : ws->keys_tmp[pass & 1];
     int32_t* vout = last ? perm : ws->vals_tmp[pass & 1];
     const int shift = pass * RADIX_BITS;
-    const unsigned grid = (unsigned)(ntiles < 148 * 8 ? ntiles : 148 * 8);
+    // persistent over tiles; 2 CTAs per SM keep a skipped pass (the movers-only sort ran) cheap
+    const unsigned grid = (unsigned)(ntiles < 148 * 2 ? ntiles : 148 * 2);
     k_radix_hist<<<grid, SORT_BLOCK, 0, s>>>(kin, n, shift, ws->radix_hist, ntiles, ctrl, skip);
-    k_radix_rowscan<<<RADIX, 1024, 0, s>>>(ws->radix_hist, ntiles, ws->digit_total, ctrl, skip);
+    k_radix_rowscan<<<RADIX, RS_BLOCK, 0, s>>>(ws->radix_hist, ntiles, ws->digit_total, ctrl, skip);
     k_radix_scatter<<<grid, SORT_BLOCK, 0, s>>>(kin, vin, n, shift, ws->radix_hist,
                                                             ws->digit_total, ntiles, kout, vout,
                                                             ctrl, skip);
