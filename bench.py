@@ -836,8 +836,8 @@ def main():
         "pair_evals_per_s": evals * world * args.steps / (total_ms * 1e-3),
         "stage_ms": {"nl": float(np.mean(nl_ms)), "pi": pi_mean, "su": float(np.mean(su_ms))},
         "counters_per_step": {"candidates": cand, "force_evals": evals, "true_pairs": true_pairs},
-        "roofline": {"bound": "fp32", "kernel": ("k_interact_v12 (paired)" if sim.pi_kernel == "paired" else
-                                                     "k_interact_v8 (" + str(sim.pi_kernel) + ")") +
+        "roofline": {"bound": "fp32", "kernel": ("k_interact_v12 (paired)" if build_info["pi_kernel"] == "paired" else
+                                                     "k_interact_v8 (" + str(build_info["pi_kernel"]) + ")") +
                      " -- one launch: fluid + boundary targets",
                      "achieved": achieved, "peak": fp32, "unit": "TFLOP/s",
                      "frac": achieved / fp32, "traffic": traffic,

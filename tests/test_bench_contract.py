@@ -5,6 +5,8 @@ import os
 import subprocess
 import sys
 
+import pytest
+
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
@@ -42,3 +44,25 @@ def test_bench_cli_parses_the_driver_flags():
     for flag in ("--gpus", "--steps", "--warmup", "--impl", "--config", "--e2e-steps",
                  "--pi-block", "--graph"):
         assert flag in out.stdout, flag
+
+
+def test_bench_py_compiles():
+    """bench.py parses (the driver runs it as a script; --help above imports only argparse)."""
+    import ast
+    with open(os.path.join(ROOT, "bench.py")) as fh:
+        ast.parse(fh.read())
+
+
+@pytest.mark.gpu
+def test_bench_default_legs_on_c1():
+    """The whole default bench (tuning, timed steps, e2e, collapsed and FP64 legs, CPU baseline)
+    end to end on the small C1 dam break, so a broken leg fails here, not at round end."""
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--config", "c1",
+                          "--steps", "5", "--warmup", "3", "--e2e-steps", "3",
+                          "--collapsed-step", "50", "--fp64-steps", "2", "--cpu-budget-s", "2"],
+                         capture_output=True, text=True, cwd=ROOT, timeout=900)
+    assert out.returncode == 0, out.stderr[-3000:]
+    d = json.loads(out.stdout.strip().splitlines()[-1])
+    for k in ("metric", "value", "e2e", "roofline", "cpu_baseline", "collapsed", "fp64", "gpu_launches"):
+        assert k in d, k
+    assert d["value"] > 0 and d["e2e"]["value"] > 0 and d["collapsed"]["value"] > 0
