@@ -301,6 +301,8 @@ class _Sorted:
 class DevRank:
     """A slab's arrays, engine scratch and step phases on one device."""
 
+    CAP_FACTOR, CAP_SLACK = 1.25, 4096  # row capacity headroom (tests set it tight: regrowth)
+
     def __init__(self, rank, nranks, bounds, params, prm, reach, dev, n_hint):
         self.rank, self.nranks = rank, nranks
         self.params, self.prm, self.reach, self.dev = params, prm, int(reach), dev
@@ -366,7 +368,7 @@ class DevRank:
         """Capacity of every per-row array (between steps: nothing to keep but the rows)."""
         if n <= self.cap:
             return
-        cap = int(n * 1.25) + 4096
+        cap = int(n * self.CAP_FACTOR) + self.CAP_SLACK
         old = getattr(self, "a", None)
         self.a, self.b = _Arrays(cap, self.dev), _Arrays(cap, self.dev)
         if old is not None and self.n:
@@ -374,8 +376,11 @@ class DevRank:
                 getattr(self.a, f)[: self.n].copy_(getattr(old, f)[: self.n])
         self.s = _Sorted(cap, self.dev)
         self.keys_sorted = torch.zeros(cap, dtype=torch.int32, device=self.dev)
+        old_tiles = getattr(self, "tiles", None)
         self.tiles = torch.zeros(NCAT * int(_lib.lib().sphb_slab_tiles(cap)) + NCAT,
                                  dtype=torch.int32, device=self.dev)
+        if old_tiles is not None:  # a re-layout grows between its count and its scatter
+            self.tiles[: old_tiles.shape[0]].copy_(old_tiles)
         self._new_ws(cap)
         self.cap = cap
 
@@ -391,7 +396,7 @@ class DevRank:
         be running): K7 still reads this step's sorted arrays and writes the new primary arrays,
         the next sort needs the previous order (keys_sorted) and a workspace of the new size
         whose histogram K7 fills.  The old buffers are kept until the next step."""
-        cap = int(n_next * 1.25) + 4096
+        cap = int(n_next * self.CAP_FACTOR) + self.CAP_SLACK
         self._retired = [self.s, self.ws, self.a, self.b]
         self.a, self.b = _Arrays(cap, self.dev), _Arrays(cap, self.dev)
         ks = torch.zeros(cap, dtype=torch.int32, device=self.dev)

@@ -951,6 +951,32 @@ def test_device_slabs_two_processes(tmp_path, transport):
         assert oracle.rel_linf(z[f], getattr(ref, f)[b]) <= 1e-9, f
 
 
+def test_device_slabs_regrow_mid_step(monkeypatch):
+    """Row capacities with no headroom: arrivals outgrow a rank's arrays in the middle of a step
+    (DevRank._grow_mid_step: new primary arrays and workspace while this step's sorted arrays
+    are still being read) -- the FP64 run still matches the single domain at every step."""
+    from paper_1110_3711_b200 import dslab
+    monkeypatch.setattr(dslab.DevRank, "CAP_FACTOR", 1.0)
+    monkeypatch.setattr(dslab.DevRank, "CAP_SLACK", 0)
+    sc = sph.Scenario(dp=0.006)
+    prm = sph.make_params(sc)
+    steps = 12
+    sim = dslab.DeviceSlabSim(sph.build_dam_break(sc, prm), prm, dslab.DevLoopbackComm(3), precision=1)
+    caps0 = [r.cap for r in sim.ranks]
+    sim.run(steps)
+    assert any(r.cap > c for r, c in zip(sim.ranks, caps0))  # a rank did regrow
+    ref, stats = sph.run_simulation(sph.build_dam_break(sc, prm), prm, gather_cfg("slowcellsh", "fp64"),
+                                    max_steps=steps, stage_timing=False)
+    recs = sim.records(0, steps)
+    assert np.array_equal(recs["dt"], np.array([s.dt for s in stats]))
+    assert np.array_equal(recs["hits_ordered"].astype(np.int64) // 2,
+                          np.array([s.true_pairs for s in stats], np.int64))
+    pos, vel, rho, ids, fl = sim.gather_host()
+    assert np.array_equal(ids, np.sort(ref.id))
+    b = np.argsort(ref.id)
+    assert oracle.rel_linf(pos, ref.pos[b]) <= 1e-9 and oracle.rel_linf(rho, ref.rho[b]) <= 1e-9
+
+
 def test_device_slabs_rebalance_keeps_results():
     """Time-balanced slab bounds (DeviceSlabSim.rebalance): forced uneven times move the
     bounds by several columns (multi-hop settle), a measured rebalance runs every 6 steps; ids
