@@ -96,10 +96,11 @@ __device__ __forceinline__ void eval_v12(const KArgs& a, const K32& c, const Own
       for (int kk = 1; kk < NG; ++kk) adk = (b >> 1) == kk ? ad[kk] : adk;
       const bool t1 = b & 1;
       bool acc = false;
-      if (cm) {  // (the target's coordinates re-read: the packed pair stays packed)
+      if (cm) {  // the target's coordinates: a half of the packed registers
         const float4 A = lds4(adk & ~1u);
-        const float4 P = a.posp[t1 ? ti[1] : ti[0]];
-        acc = cold_accept(a, P.x, P.y, P.z, A, t1 ? xlo[1] : xlo[0], t1 ? xhi[1] : xhi[0]);
+        const float px = t1 ? hi(o.x) : lo(o.x), py = t1 ? hi(o.y) : lo(o.y),
+                    pz = t1 ? hi(o.z) : lo(o.z);
+        acc = cold_accept(a, px, py, pz, A, t1 ? xlo[1] : xlo[0], t1 ? xhi[1] : xhi[0]);
         cm &= cm - 1u;
       }
 #pragma unroll
