@@ -606,8 +606,10 @@ __global__ void __launch_bounds__(32) k_blocks(sphb_grid_t g, int64_t ncells,
           if (c == 0) continue;
           // close before x when the targets would not fit, or when the block's columns would
           // exceed maxc (the FP16 tensor-core screen's coordinate range, else the kernel falls
-          // back to the CUDA-core screen)
-          if ((block_slots(totf + cf, tot + c) > BT || (xa >= 0 && x - xa + 1 > maxc)) && tot > 0) {
+          // back to the CUDA-core screen) and the block is at least a quarter full (sparse rows,
+          // e.g. a small system's mostly empty tank: fuller blocks on the fallback screen win)
+          if ((block_slots(totf + cf, tot + c) > BT || (xa >= 0 && x - xa + 1 > maxc && 4 * tot >= BT)) &&
+              tot > 0) {
             emit(make_int4(0, 0, 0, 0), make_int4(key0, xa, xl, 1));
             tot = totf = 0;
             xa = -1;
@@ -667,7 +669,8 @@ __global__ void __launch_bounds__(32) k_blocks(sphb_grid_t g, int64_t ncells,
         const int x = g.tx0 + k;
         const int32_t fe = s_ends[k], be = s_ends[span + k];
         if (fe == fcur && be == bcur) continue;  // empty cell
-        if ((block_slots(fe - f0, (fe - f0) + (be - b0)) > BT || (xa >= 0 && x - xa + 1 > maxc)) &&
+        if ((block_slots(fe - f0, (fe - f0) + (be - b0)) > BT ||
+             (xa >= 0 && x - xa + 1 > maxc && 4 * ((fcur - f0) + (bcur - b0)) >= BT)) &&
             (fcur > f0 || bcur > b0)) {  // close before this cell
           emit(make_int4(f0, fcur, b0, bcur), xa, xl);
           f0 = fcur;
