@@ -215,7 +215,9 @@ int sphb_nl_build(sphb_workspace_t* ws, const sphb_grid_t* grid, const void* pos
 /* K3 -- reorder gathers (grid.py:111-114) fused with compute_derived (physics.py:96-110):
  * *_out[i] = *_in[perm[i]] for posp, velr, prev, id; posp_out.w = prrho; aux_out = (press,
  * csound, tensil, list mass);
- * cell_out[i] = cell of the sorted key.  prev_in/prev_out/id may be NULL.
+ * cell_out[i] = cell of the sorted key.  prev_in/prev_out/id may be NULL; aux_out may be NULL
+ * when the interaction that follows is an FP32 gather / paired build (they recompute a
+ * target's row with this kernel's arithmetic: sphb_step skips the aux pass then).
  * The derived values are the reference's (f64 pow, f32-rounded, bit-identical) for
  * prm->precision == SPHB_FP64; SPHB_FP32 with gamma = 7 evaluates (rho/rho0)^7 and ^3 by
  * multiplication (press / csound within 1 f32 ulp; the FP32 force tolerance is 1e-5). */
@@ -255,7 +257,8 @@ int sphb_cell_ranges_from_sorted(sphb_workspace_t* ws, const sphb_grid_t* grid,
 /* K5/K5b/K6 -- GatherEngine.compute (engines/gather.py:42-110): fused fluid pass
  * (gather_fluid_cells / _ranges, kernels.py:326-497) and boundary pass (gather_boundary_*,
  * kernels.py:500-596), plus the compute_dt reductions (sim.py:215-232) in the epilogue.
- * Raw counters and the two dt minima accumulate into ctrl. */
+ * Raw counters and the two dt minima accumulate into ctrl.  aux may be NULL for the FP32
+ * gather / paired builds (not for SPHB_FP64 or the symmetric build). */
 int sphb_interact(sphb_workspace_t* ws, const sphb_params_t* prm, const sphb_grid_t* grid,
                   int64_t n, int64_t nb,
                   const void* posp, const void* velr, const void* aux, const int32_t* cell_sorted,

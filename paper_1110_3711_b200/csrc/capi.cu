@@ -303,7 +303,6 @@ int sphb_reorder(const sphb_params_t* prm, const sphb_grid_t* grid, int64_t n,
     SPHB_NONNULL(velr_in);
     SPHB_NONNULL(posp_out);
     SPHB_NONNULL(velr_out);
-    SPHB_NONNULL(aux_out);
   }
   return launch_reorder(*prm, *grid, n, perm, keys_sorted, (const float4*)posp_in,
                         (const float4*)velr_in, (const float4*)prev_in, id_in, (float4*)posp_out,
@@ -382,7 +381,9 @@ int sphb_interact(sphb_workspace_t* ws, const sphb_params_t* prm, const sphb_gri
   if (n == 0) return SPHB_OK;
   SPHB_NONNULL(posp);
   SPHB_NONNULL(velr);
-  SPHB_NONNULL(aux);
+  // aux (derived rows) may be NULL for the FP32 gather / paired builds: they recompute a
+  // target's own values; the FP64 kernel and the symmetric build read them
+  if (prm->precision == SPHB_FP64 || ws->pi_kernel == SPHB_PI_SYMMETRIC) SPHB_NONNULL(aux);
   SPHB_NONNULL(cell_sorted);
   SPHB_NONNULL(beg);
   SPHB_NONNULL(end);
@@ -471,6 +472,9 @@ static int stage_pass(sphb_workspace_t* ws, const sphb_params_t* prm, const sphb
                       int64_t n, int64_t nb, const sphb_state_t* st, sphb_ctrl_t* ctrl, int mode,
                       cudaStream_t cs) {
   int rc;
+  // the FP32 gather / paired kernels need no aux rows (16 B per particle less to write)
+  float4* aux = (prm->precision == SPHB_FP32 && ws->pi_kernel != SPHB_PI_SYMMETRIC)
+                    ? nullptr : (float4*)st->aux;
   {
     NvtxRange r("sphb NL");  // stage ranges (the reference's perf_counter stages, sim.py:306-348)
     if ((rc = launch_sort_and_ranges(ws, *grid, st->keys, n, st->keys_sorted, st->perm, st->beg,
@@ -479,13 +483,13 @@ static int stage_pass(sphb_workspace_t* ws, const sphb_params_t* prm, const sphb
     if ((rc = launch_reorder(*prm, *grid, n, st->perm, st->keys_sorted, (const float4*)st->posp,
                              (const float4*)st->velr, (const float4*)st->prev, st->id,
                              (float4*)st->posp_s, (float4*)st->velr_s, (float4*)st->prev_s, st->id_s,
-                             (float4*)st->aux, st->cell_s, ctrl, cs)))
+                             aux, st->cell_s, ctrl, cs)))
       return rc;
   }
   {
     NvtxRange r("sphb PI");
     if ((rc = launch_interact(ws, *prm, *grid, n, nb, (const float4*)st->posp_s,
-                              (const float4*)st->velr_s, (const float4*)st->aux, st->cell_s, st->beg,
+                              (const float4*)st->velr_s, aux, st->cell_s, st->beg,
                               st->end, st->acc, st->drho, st->visc, ctrl, cs)))
       return rc;
   }

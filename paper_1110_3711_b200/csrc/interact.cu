@@ -106,6 +106,7 @@ struct KArgs {
   // FP32 constants
   float sup2_lo, sup2_hi, tiny, h, invh, k_gc, k_tw, eta2, alpha, massf, massb, k_cs, cs_exp;
   int gamma7;
+  double inv_rho0;  // 1 / rho0 (host): a target's csound without a division
 };
 
 // FP32 constants of the pair loop, pinned in registers (an opaque move stops the compiler
@@ -1644,7 +1645,12 @@ __global__ void __launch_bounds__(NW * 32, V8_MINB) k_interact_v8(KArgs a, K32 k
       if (valid) {
         pi = a.posp[i];
         vi = a.velr[i];
-        xi = a.aux[i];
+        if (a.aux) {
+          xi = a.aux[i];
+        } else {  // no aux rows this step: the target's own csound / tensil
+          const float2 ct = target_cs_tensil<G7>((double)vi.w, pi.w, a.inv_rho0, a.p);
+          xi = make_float4(0.f, ct.x, ct.y, 0.f);
+        }
         cxi = a.cell[i] - (rowkey + rsy + ny * rsz) * nx;
         xlo = max(cxi - reach, 0);
         xhi = min(cxi + reach, nx - 1);
@@ -2340,6 +2346,7 @@ int launch_interact(sphb_workspace* ws, const sphb_params_t& p, const sphb_grid_
   a.massf = (float)p.mass_fluid;
   a.massb = (float)p.mass_boundary;
   a.gamma7 = p.gamma == 7.0;
+  a.inv_rho0 = 1.0 / p.rho0;
   a.cs_exp = (float)((p.gamma - 1.0) * 0.5);
   a.k_cs = a.gamma7 ? (float)(cbrt(p.c0) / p.rho0)
                     : (float)(p.c0 * pow(p.rho0, -(p.gamma - 1.0) * 0.5));

@@ -466,7 +466,12 @@ __global__ void __launch_bounds__(NW * 32, 1) k_interact_v12(KArgs a, K32 k32) {
         if (valid[t]) {
           pi[t] = a.posp[ti[t]];
           vi[t] = a.velr[ti[t]];
-          xi[t] = a.aux[ti[t]];
+          if (a.aux) {
+            xi[t] = a.aux[ti[t]];
+          } else {  // no aux rows this step: the target's own csound / tensil
+            const float2 ct = target_cs_tensil<G7>((double)vi[t].w, pi[t].w, a.inv_rho0, a.p);
+            xi[t] = make_float4(0.f, ct.x, ct.y, 0.f);
+          }
           const int cxi = a.cell[ti[t]] - (rowkey + rsy[t] + ny * rsz[t]) * nx;
           xlo[t] = max(cxi - reach, 0);
           xhi[t] = min(cxi + reach, nx - 1);

@@ -250,7 +250,6 @@ __global__ void __launch_bounds__(256, NL_MINB) k_reorder(
     int32_t* __restrict__ cell_out, const sphb_ctrl_t* ctrl) {
   if (!step_live(ctrl)) return;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  const double inv_rho0 = 1.0 / p.rho0;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
     const int32_t o = perm ? perm[i] : (int32_t)i;
     const uint32_t ks = keys_sorted ? keys_sorted[i] : 0u;
@@ -261,27 +260,16 @@ __global__ void __launch_bounds__(256, NL_MINB) k_reorder(
     long long id = 0;
     if (has_prev) pv = prev_in[o];
     if (has_id) id = id_in[o];
-    const double rho = (double)vr.w;
-    float press;
-    Derived d;
-    if (FAST) {
-      const double x = rho * inv_rho0, x3 = x * x * x;
-      press = __double2float_rn(p.tait_b * (x3 * x3 * x - 1.0));
-      const double inv_rho2 = 1.0 / (rho * rho);
-      d.prrho = __double2float_rn((double)press * inv_rho2);
-      d.csound = __double2float_rn(p.c0 * x3);
-      d.tensil = __double2float_rn((press > 0.0f ? 0.01 : -0.2) * (double)press * inv_rho2);
-    } else {
-      press = eos_press(rho, p.tait_b, p.rho0, p.gamma);
-      d = derive((double)press, rho, p.c0, p.rho0, p.gamma);
-    }
+    const Deriv4 d = derived_of<FAST>((double)vr.w, p);
     // posp.w = prrho: the interaction stages (x, y, z, prrho) rows with one bulk copy
     pp.w = d.prrho;
     posp_out[i] = pp;
     velr_out[i] = vr;
     const bool boundary = keys_sorted ? ((ks >> cellbits) & 1u) == 0u : false;
-    aux_out[i] = make_float4(press, d.csound, d.tensil,
-                             (float)(boundary ? p.mass_boundary : p.mass_fluid));
+    // aux may be absent: the FP32 gather / paired interaction recomputes a target's row
+    if (aux_out)
+      aux_out[i] = make_float4(d.press, d.csound, d.tensil,
+                               (float)(boundary ? p.mass_boundary : p.mass_fluid));
     if (has_prev) prev_out[i] = pv;
     if (has_id) id_out[i] = id;
     if (cell_out && keys_sorted) cell_out[i] = (int32_t)(ks & cellmask);

@@ -42,6 +42,47 @@ __device__ __forceinline__ Derived derive(double press, double rho, double c0, d
   return d;
 }
 
+// The step's derived quantities of one particle from its density (physics.py:119-134).
+// FAST (FP32 precision, gamma = 7): x^7 and x^3 by multiplication, every operation explicitly
+// rounded, so K3 and the FP32 interaction kernels (which recompute a target's values instead of
+// reading the aux row) get the same bits; else the exact f64 pow path (bit-identical to the
+// reference, FP64 precision and the public compute_derived).
+struct Deriv4 {
+  float press, prrho, csound, tensil;
+};
+template <bool FAST>
+__device__ __forceinline__ Deriv4 derived_of(double rho, const sphb_params_t& p) {
+  Deriv4 r;
+  if (FAST) {
+    const double x = xmul(rho, xdiv(1.0, p.rho0)), x3 = xmul(xmul(x, x), x);
+    r.press = __double2float_rn(xmul(p.tait_b, xsub(xmul(xmul(x3, x3), x), 1.0)));
+    const double inv_rho2 = xdiv(1.0, xmul(rho, rho));
+    r.prrho = __double2float_rn(xmul((double)r.press, inv_rho2));
+    r.csound = __double2float_rn(xmul(p.c0, x3));
+    r.tensil = __double2float_rn(xmul(xmul(r.press > 0.0f ? 0.01 : -0.2, (double)r.press), inv_rho2));
+  } else {
+    r.press = eos_press(rho, p.tait_b, p.rho0, p.gamma);
+    const Derived d = derive((double)r.press, rho, p.c0, p.rho0, p.gamma);
+    r.prrho = d.prrho;
+    r.csound = d.csound;
+    r.tensil = d.tensil;
+  }
+  return r;
+}
+
+// A target's (csound, tensil) in the FP32 interaction kernels when no aux rows were written:
+// csound with K3's arithmetic (inv_rho0 = 1 / rho0 from the host: no division here), tensil
+// from the staged prrho (within 1 f32 ulp of K3's; it only scales the tensile correction)
+template <bool G7>
+__device__ __forceinline__ float2 target_cs_tensil(double rho, float prrho, double inv_rho0,
+                                                   const sphb_params_t& p) {
+  const double x = xmul(rho, inv_rho0);
+  const double cs = G7 ? xmul(p.c0, xmul(xmul(x, x), x))
+                       : xmul(p.c0, pow(x, xmul(xsub(p.gamma, 1.0), 0.5)));
+  const float ten = __double2float_rn(xmul(prrho > 0.0f ? 0.01 : -0.2, (double)prrho));
+  return make_float2(__double2float_rn(cs), ten);
+}
+
 // ---------------------------------------------------------------- cells (grid.py:77-93)
 // Returns the linear cell (x fastest) or -1 when outside [origin, domain_max] (NaN -> -1).
 __device__ __forceinline__ int32_t cell_of(float x, float y, float z, const sphb_grid_t& g) {

@@ -149,16 +149,20 @@ class DeviceSim:
         self.ws.reset()
         self.upload(system, vel_prev, rho_prev)
         self.ctrl = new_ctrl(dev, max_steps, t_end)
-        self._state = _lib.StateDesc(*[_ptr(t) for t in (
-            self.posp, self.velr, self.prev, self.id, self.posp_s, self.velr_s, self.prev_s,
-            self.aux, self.id_s, self.keys, self.keys_sorted, self.perm, self.cell_s, self.beg,
-            self.end, self.acc, self.drho, self.visc)])
+        self._make_state()
         self.first_keys()
         self._graph = None
         self._graph_steps = 0
         self.pi_block = 128
         self.pi_kernel = "gather"
         self.tuning = None  # the last tune_pi result
+
+    def _make_state(self):
+        """The sphb_step descriptor of the current buffers (rebuilt when the id buffers swap)."""
+        self._state = _lib.StateDesc(*[_ptr(t) for t in (
+            self.posp, self.velr, self.prev, self.id, self.posp_s, self.velr_s, self.prev_s,
+            self.aux, self.id_s, self.keys, self.keys_sorted, self.perm, self.cell_s, self.beg,
+            self.end, self.acc, self.drho, self.visc)])
 
     def set_pi_kernel(self, kernel: str):
         """FP32 interaction kernel: "gather" (one-sided, K6 dt in its epilogue) or "symmetric"
@@ -287,6 +291,9 @@ class DeviceSim:
         ev[0] after NL, ev[1] after PI, ev[2] after the update."""
         L, s, ws = _lib.lib(), _stream(), self.ws.handle
         g, p, n, nb = _lib.ref(self.grid), _lib.ref(self.prm), self.n, self.nb
+        # the FP32 gather / paired kernels recompute a target's derived row: no aux pass
+        aux = self.aux if (int(self.prm.precision) == _lib.SPHB_FP64 or self.pi_kernel == "symmetric") \
+            else None
         nvtx = torch.cuda.nvtx
         nvtx.range_push("sphb NL")
         _lib.check(L.sphb_sort_ranges(ws, g, _ptr(self.keys), n, _ptr(self.keys_sorted),
@@ -295,13 +302,13 @@ class DeviceSim:
         _lib.check(L.sphb_reorder(p, g, n, _ptr(self.perm), _ptr(self.keys_sorted), _ptr(self.posp),
                                   _ptr(self.velr), _ptr(self.prev), _ptr(self.id), _ptr(self.posp_s),
                                   _ptr(self.velr_s), _ptr(self.prev_s), _ptr(self.id_s),
-                                  _ptr(self.aux), _ptr(self.cell_s), _ptr(self.ctrl), s),
+                                  _ptr(aux), _ptr(self.cell_s), _ptr(self.ctrl), s),
                    "sphb_reorder")
         ev[0].record()
         nvtx.range_pop()
         nvtx.range_push("sphb PI")
         _lib.check(L.sphb_interact(ws, p, g, n, nb, _ptr(self.posp_s), _ptr(self.velr_s),
-                                   _ptr(self.aux), _ptr(self.cell_s), _ptr(self.beg),
+                                   _ptr(aux), _ptr(self.cell_s), _ptr(self.beg),
                                    _ptr(self.end), _ptr(self.acc), _ptr(self.drho),
                                    _ptr(self.visc), _ptr(self.ctrl), s), "sphb_interact")
         ev[1].record()

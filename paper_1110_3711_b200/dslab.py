@@ -429,12 +429,17 @@ class DevRank:
         self.n, self.nb = n, int(nb)
 
     # -------------------------------------------------------------- step phases
+    def _aux(self):
+        """The derived rows: only the FP64 kernel reads them (the FP32 gather / paired builds
+        recompute a target's own values)."""
+        return self.s.aux if int(self.prm.precision) == _lib.SPHB_FP64 else None
+
     def _interact(self, grids):
         L, s, ws, sa = _lib.lib(), _stream(), self.ws.handle, self.s
         p = _lib.ref(self.prm)
         for g in grids:
             _lib.check(L.sphb_interact(ws, p, _lib.ref(g), self.n, 0, _ptr(sa.posp), _ptr(sa.velr),
-                                       _ptr(sa.aux), _ptr(sa.cell), _ptr(self.beg), _ptr(self.end),
+                                       _ptr(self._aux()), _ptr(sa.cell), _ptr(self.beg), _ptr(self.end),
                                        _ptr(sa.acc), _ptr(sa.drho), _ptr(sa.visc), _ptr(self.ctrl),
                                        s), "sphb_interact")
 
@@ -455,7 +460,7 @@ class DevRank:
                    "sphb_sort_ranges")
         _lib.check(L.sphb_reorder(p, g, n, _ptr(sa.perm), _ptr(self.keys_sorted), _ptr(a.posp),
                                   _ptr(a.velr), _ptr(a.prev), _ptr(a.id), _ptr(sa.posp),
-                                  _ptr(sa.velr), _ptr(sa.prev), _ptr(sa.id), _ptr(sa.aux),
+                                  _ptr(sa.velr), _ptr(sa.prev), _ptr(sa.id), _ptr(self._aux()),
                                   _ptr(sa.cell), _ptr(self.ctrl), s), "sphb_reorder")
         _lib.check(L.sphb_band_count(g, self.width, self.sides, _ptr(self.beg), _ptr(self.end),
                                      _ptr(self.scratch), _ptr(self.info), _ptr(self.ctrl), s),
