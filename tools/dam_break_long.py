@@ -1,7 +1,10 @@
 """C3 dam break over a long run on one GPU: how the step cost evolves as the column collapses
 (cells fill unevenly, more rows change cell per step), with the energy diagnostics.
 
-  python tools/dam_break_long.py [c3] [out.json] [steps] [every] [128|384|auto]
+  python tools/dam_break_long.py [c3] [out.json] [steps] [every] [128|384|auto|tuned]
+
+("tuned": run_simulation(pi_kernel="tuned")'s policy -- at every window start one step of each
+of DeviceSim.pi_candidates, the faster build runs the window.)
 
 Per window of ``every`` steps: mean ms/step and NL / PI / SU stage means (CUDA events), the
 movers-only sort's mover count and path on the window's last step, t_sim, KE/PE/IE.
@@ -27,15 +30,18 @@ sc = sph.named_scenario(name)
 prm = sph.make_params(sc)
 system = sph.build_dam_break(sc, prm)
 sim = DeviceSim(system, prm, reach=1, record_capacity=steps + 8)
-if blocking == "auto":
+if blocking in ("auto", "tuned"):
     sim.set_pi_block(sph.sim.initial_pi_block(sim.n, prm.n_subdiv))
-if blocking != "auto":
+else:
     sim.set_pi_block(int(blocking))
 n = sim.n
 rows = []
 e0 = sim.energy()
 done = 0
 while done < steps:
+    if blocking == "tuned" and steps - done > every:
+        sim.tune_pi(sim.pi_candidates(prm.n_subdiv))  # (ordinary steps of the run)
+        done += 2
     k = min(every, steps - done)
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(sim.n_stage_events())] for _ in range(k)]
     for i in range(k):
@@ -51,7 +57,7 @@ while done < steps:
     e = sim.energy()
     nblk = int(c["nblk"][0])
     lane = sim.pi_lane_use(c)
-    block_now = sim.pi_block
+    block_now = f"{sim.pi_kernel}/{sim.pi_block}"
     rows.append(dict(step=done, t_sim=float(c["t_sim"]), ms_per_step=float(st[:, 3].mean()),
                      pi_block=block_now, pi_blocks=nblk, lane_use=lane,
                      nl_ms=float(st[:, 0].mean()), pi_ms=float(st[:, 1].mean()),
