@@ -91,9 +91,15 @@ __device__ __forceinline__ void eval_v12(const KArgs& a, const K32& c, const Own
     }
     do {
       const int b = __ffs(cm) - 1;  // slot 2 k + t: candidate k, target t
+      // the popped address of candidate b / 2 by explicit selects (an indexed pick made ptxas
+      // keep the pops in local memory: three stores per drain iteration)
       uint32_t adk = ad[0];
 #pragma unroll
-      for (int kk = 1; kk < NG; ++kk) adk = (b >> 1) == kk ? ad[kk] : adk;
+      for (int kk = 1; kk < NG; ++kk) {
+        const uint32_t hit = (uint32_t)((b >> 1) == kk);
+        asm("{ .reg .pred q; setp.ne.u32 q, %2, 0; selp.b32 %0, %1, %0, q; }"
+            : "+r"(adk) : "r"(ad[kk]), "r"(hit));
+      }
       const bool t1 = b & 1;
       bool acc = false;
       if (cm) {  // the target's coordinates: a half of the packed registers
