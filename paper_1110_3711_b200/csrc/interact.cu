@@ -1326,9 +1326,14 @@ __device__ __forceinline__ void eval_v8(const KArgs& a, const K32& c, const Own3
     // (in_cold == !is_sure && r2 < sup2_hi: r2 in [sup2_lo, sup2_hi) or r2 <= tiny)
     do {
       const int k = __ffs(cm) - 1;
+      // the popped address by explicit selects (an indexed pick keeps the pops in local memory)
       uint32_t adk = ad[0];
 #pragma unroll
-      for (int kk = 1; kk < 2 * NG; ++kk) adk = k == kk ? ad[kk] : adk;
+      for (int kk = 1; kk < 2 * NG; ++kk) {
+        const uint32_t hit = (uint32_t)(k == kk);
+        asm("{ .reg .pred q; setp.ne.u32 q, %2, 0; selp.b32 %0, %1, %0, q; }"
+            : "+r"(adk) : "r"(ad[kk]), "r"(hit));
+      }
       bool acc = false;
       if (cm) {
         const float4 A = lds4(adk & ~1u);
