@@ -608,9 +608,12 @@ def main():
     if args.pi_kernel not in ("gather", "tuned") and prec == _lib.SPHB_FP32:
         sim.set_pi_kernel(args.pi_kernel)
     warm = args.warmup
-    if tuned and warm >= len(cands):  # the first warm-up steps time each candidate build once
+    warm_run = 0
+    if tuned and warm >= len(cands):  # the first warm-up steps time the candidate builds
         sim.tune_pi(cands)
-        warm -= len(cands)
+        warm -= sim.tuning_steps  # (a first tuning runs each build twice: >= W warm-up steps)
+        warm_run = sim.tuning_steps
+    warm_run += max(warm, 0)
     for _ in range(warm):
         sim.launch_step()
     torch.cuda.synchronize()
@@ -649,7 +652,7 @@ def main():
     err = sim.error()
     if err is not None:
         raise RuntimeError(f"divergence during bench: {err}")
-    build_info = {"pi_block": sim.pi_block, "pi_kernel": sim.pi_kernel,
+    build_info = {"warmup_steps_run": warm_run, "pi_block": sim.pi_block, "pi_kernel": sim.pi_kernel,
                   "pi_lane_use": round(sim.pi_lane_use(), 4), "cuda_graph": use_graph,
                   "pi_policy": "tuned" if tuned else args.pi_kernel, "pi_tuning_ms": sim.tuning}
     recs = sim.records(first, first + args.steps)

@@ -195,11 +195,19 @@ class DeviceSim:
         from .sim import initial_pi_block
         return [("gather", initial_pi_block(self.n, n_subdiv)), ("paired", 512)]
 
-    def tune_pi(self, candidates, events=None) -> dict:
-        """Run one ordinary step with each candidate build (the state advances as usual), time
-        each step's PI stage with CUDA events and keep the fastest build.  ``events``: the
-        per-step event lists to record into (launch_step's layout), else fresh ones.  Returns
-        {"kernel/block": PI ms}."""
+    def tune_pi(self, candidates, events=None, repeats: int | None = None) -> dict:
+        """Run ordinary steps with each candidate build (the state advances as usual), time
+        each step's PI stage with CUDA events and keep the fastest build.  The first tuning of
+        a simulation runs every candidate twice and decides on the second round: a kernel's
+        first launch in a process carries its one-time module load (lazy loading), which must
+        not decide the choice.  ``events``: the per-step event lists of the deciding round
+        (launch_step's layout), else fresh ones.  Returns {"kernel/block": PI ms};
+        ``self.tuning_steps`` is the number of steps it ran."""
+        reps = (2 if self.tuning is None else 1) if repeats is None else int(repeats)
+        for _ in range(reps - 1):  # untimed warm round
+            for kern, blk in candidates:
+                self.select_pi(kern, blk)
+                self.launch_step()
         evs = events if events is not None else [
             [torch.cuda.Event(enable_timing=True) for _ in range(self.n_stage_events())]
             for _ in candidates]
@@ -207,6 +215,7 @@ class DeviceSim:
             self.select_pi(kern, blk)
             self.launch_step(events=ev)
         torch.cuda.synchronize()
+        self.tuning_steps = reps * len(candidates)
         return self.tune_choose(candidates, evs)
 
     def tune_choose(self, candidates, events) -> dict:

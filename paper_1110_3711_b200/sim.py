@@ -228,17 +228,19 @@ def run_simulation(scenario_or_system, params, config: EngineConfig, max_steps: 
         # resume from a step that is not one; a tuning chunk is one step per candidate build
         this = chunk - done_steps % chunk
         tune_now = tuned and (last_tune is None or done_steps - last_tune >= int(retune_every)) \
-            and this >= len(cands)  # (else at the next chunk)
+            and this >= 2 * len(cands)  # (else at the next chunk)
         if tune_now:
-            this = len(cands)
+            # the first tuning runs each build twice and decides on the second round (a
+            # kernel's first launch carries its one-time module load)
+            this = len(cands) * (2 if last_tune is None else 1)
         timer = _Timer(this, sim.n_stage_events()) if (stage_timing or tune_now) else None
         for k in range(this):
             if tune_now:
-                sim.select_pi(*cands[k])
+                sim.select_pi(*cands[k % len(cands)])
             sim.launch_step(events=timer.ev[k] if timer else None)
         c = sim.ctrl_host()  # synchronises
         if tune_now:
-            sim.tune_choose(cands, timer.ev)
+            sim.tune_choose(cands, timer.ev[-len(cands):])
             last_tune = done_steps
         now = int(c["step"])
         recs = sim.records(done_steps, now)
