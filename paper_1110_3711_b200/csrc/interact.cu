@@ -1324,6 +1324,7 @@ __device__ __forceinline__ void eval_v8(const KArgs& a, const K32& c, const Own3
       cm |= (in_cold(hi(g[k].r2), c) ? 1u : 0u) << (2 * k + 1);
     }
     // (in_cold == !is_sure && r2 < sup2_hi: r2 in [sup2_lo, sup2_hi) or r2 <= tiny)
+    uint32_t accm = 0;  // accepted cold slots
     do {
       const int k = __ffs(cm) - 1;
       // the popped address by explicit selects (an indexed pick keeps the pops in local memory)
@@ -1340,18 +1341,19 @@ __device__ __forceinline__ void eval_v8(const KArgs& a, const K32& c, const Own3
         acc = cold_accept(a, o.x, o.y, o.z, A, xlo, xhi);
         cm &= cm - 1u;
       }
-#pragma unroll
-      for (int kk = 0; kk < NG; ++kk) {
-        if (acc && k == 2 * kk) {
-          okf[2 * kk] = 1.0f;
-          r2m[2 * kk] = lo(g[kk].r2);
-        }
-        if (acc && k == 2 * kk + 1) {
-          okf[2 * kk + 1] = 1.0f;
-          r2m[2 * kk + 1] = hi(g[kk].r2);
-        }
-      }
+      accm |= acc ? 1u << k : 0u;
     } while (__any_sync(SPHB_FULL, cm != 0u));
+#pragma unroll
+    for (int kk = 0; kk < NG; ++kk) {  // once after the rounds, not once per round
+      if ((accm >> (2 * kk)) & 1u) {
+        okf[2 * kk] = 1.0f;
+        r2m[2 * kk] = lo(g[kk].r2);
+      }
+      if ((accm >> (2 * kk + 1)) & 1u) {
+        okf[2 * kk + 1] = 1.0f;
+        r2m[2 * kk + 1] = hi(g[kk].r2);
+      }
+    }
   }
 #pragma unroll
   for (int k = 0; k < NG; ++k) {

@@ -89,6 +89,7 @@ __device__ __forceinline__ void eval_v12(const KArgs& a, const K32& c, const Own
       cm |= ((in_cold(lo(R2[k]), c) && ad[k] != own0) ? 1u : 0u) << (2 * k);
       cm |= ((in_cold(hi(R2[k]), c) && ad[k] != own1) ? 1u : 0u) << (2 * k + 1);
     }
+    uint32_t accm = 0;  // accepted cold slots
     do {
       const int b = __ffs(cm) - 1;  // slot 2 k + t: candidate k, target t
       // the popped address of candidate b / 2 by explicit selects (an indexed pick made ptxas
@@ -109,14 +110,15 @@ __device__ __forceinline__ void eval_v12(const KArgs& a, const K32& c, const Own
         acc = cold_accept(a, px, py, pz, A, t1 ? xlo[1] : xlo[0], t1 ? xhi[1] : xhi[0]);
         cm &= cm - 1u;
       }
-#pragma unroll
-      for (int kk = 0; kk < 2 * NG; ++kk) {
-        if (acc && b == kk) {
-          okf[kk] = 1.0f;
-          r2m[kk] = (kk & 1) ? hi(R2[kk >> 1]) : lo(R2[kk >> 1]);
-        }
-      }
+      accm |= acc ? 1u << b : 0u;
     } while (__any_sync(SPHB_FULL, cm != 0u));
+#pragma unroll
+    for (int kk = 0; kk < 2 * NG; ++kk) {  // once after the rounds, not once per round
+      if ((accm >> kk) & 1u) {
+        okf[kk] = 1.0f;
+        r2m[kk] = (kk & 1) ? hi(R2[kk >> 1]) : lo(R2[kk >> 1]);
+      }
+    }
   }
 #pragma unroll
   for (int k = 0; k < NG; ++k) {
