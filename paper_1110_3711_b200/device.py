@@ -189,11 +189,15 @@ class DeviceSim:
 
     def pi_candidates(self, n_subdiv: int = 1) -> list[tuple[str, int]]:
         """The builds the "tuned" policy times against each other: the gather kernel with the
-        size rule's blocking (sim.initial_pi_block) and the paired kernel (two targets per lane,
-        512-target bricks).  At rest the paired build is the faster one; once cells fill unevenly
+        size rule's blocking (sim.initial_pi_block; small systems also 384), and the paired kernel
+        (two targets per lane, 512-target bricks).  At rest the paired build is the faster one; once cells fill unevenly
         (a collapsed column) its bricks leave more lanes idle and the row blocks win."""
         from .sim import initial_pi_block
-        return [("gather", initial_pi_block(self.n, n_subdiv)), ("paired", 512)]
+        first = initial_pi_block(self.n, n_subdiv)
+        # small systems (a few blocks per SM: per-block latency, not lane use, decides) also
+        # try the 384-target blocks (C1: 0.10 vs 0.12 ms PI with 256)
+        extra = [("gather", 384)] if first != 384 else []
+        return [("gather", first)] + extra + [("paired", 512)]
 
     def tune_pi(self, candidates, events=None, repeats: int | None = None) -> dict:
         """Run ordinary steps with each candidate build (the state advances as usual), time
