@@ -715,7 +715,7 @@ def main():
         s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
         ev_in = [torch.cuda.Event() for _ in bounds]
         ev_out = [torch.cuda.Event() for _ in bounds]
-        ev_packed = torch.cuda.Event()
+        ev_packed = [torch.cuda.Event() for _ in bounds]
 
         def h2d_chunk(c):
             lo, hi = bounds[c]
@@ -736,11 +736,12 @@ def main():
                 from_soa(lo, hi)
             sim.first_keys_resync()
             sim.launch_step()
-            to_soa(0, n)
-            ev_packed.record(comp)
-            s_out.wait_event(ev_packed)
+            for c, (lo, hi) in enumerate(bounds):  # each chunk leaves as soon as it is converted
+                to_soa(lo, hi)
+                ev_packed[c].record(comp)
             with torch.cuda.stream(s_out):
                 for c, (lo, hi) in enumerate(bounds):
+                    s_out.wait_event(ev_packed[c])
                     for hbuf, dbuf in pairs:
                         hbuf[lo:hi].copy_(dbuf[lo:hi], non_blocking=True)
                     ev_out[c].record(s_out)
