@@ -308,43 +308,6 @@ __device__ __forceinline__ void wall_finish(const KArgs& a, int64_t i, int64_t s
     raise_div(a.ctrl, step, SPHB_DIV_NONFINITE_FORCES, 0);
 }
 
-// ------------------------------------------------------------------ candidate counts
-// A target's candidate count is the sum of its stencil rows' range lengths (the reference's
-// loop count, kernels.py:355-371).  The lanes of one cell share it, so each distinct (x range,
-// row offset in a brick, list) of the warp is summed once by all 32 lanes in parallel over the
-// staged rows (lane l: rows l, l + 32, ...) and taken by the lanes that have it -- at h/2
-// cells a warp holds ~4 cells x 8 targets over 2 x 36 staged rows.
-__device__ __forceinline__ unsigned long long cand_count(const KArgs& a, const Seg* sSeg, int nseg,
-                                                         bool valid, bool isf, int xlo, int xhi,
-                                                         int rsy, int rsz, int lane) {
-  const int reach = a.g.reach;
-  const uint32_t klo = (uint32_t)xlo | ((uint32_t)xhi << 16);
-  const uint32_t khi = (uint32_t)rsy | ((uint32_t)rsz << 1) | (isf ? 4u : 0u);
-  uint32_t todo = __ballot_sync(SPHB_FULL, valid);
-  unsigned long long mine = 0;
-  while (todo) {
-    const int l = __ffs(todo) - 1;
-    const uint32_t plo = __shfl_sync(SPHB_FULL, klo, l), phi = __shfl_sync(SPHB_FULL, khi, l);
-    const int pxlo = (int)(plo & 0xffffu), pxhi = (int)(plo >> 16);
-    const int psy = (int)(phi & 1u), psz = (int)((phi >> 1) & 1u);
-    const bool pf = (phi & 4u) != 0u;
-    int part = 0;
-    for (int k = lane; k < nseg; k += 32) {
-      const Seg sg = sSeg[k];
-      if (sg.g1 <= sg.g0 || (!pf && sg.rowoff < a.ncells)) continue;  // boundary targets: fluid rows
-      const int dy = (sg.dyz & 255) - 16, dz = (sg.dyz >> 8) - 16;
-      if (abs(dy - psy) > reach || abs(dz - psz) > reach) continue;
-      part += a.end[sg.rowoff + pxhi] - a.beg[sg.rowoff + pxlo];
-    }
-    part = (int)__reduce_add_sync(SPHB_FULL, (uint32_t)part);
-    const bool same = valid && klo == plo && khi == phi;
-    if (same) mine = (unsigned long long)part;
-    todo &= ~__ballot_sync(SPHB_FULL, same);
-  }
-  if (valid && isf) mine -= 1;  // the reference skips j == i before counting (kernels.py:369-371)
-  return mine;
-}
-
 // ------------------------------------------------------------------ pair math
 // FP32 (physics.py:183-220 restated for FP32 CUDA cores).  Branch-free cubic spline:
 // W ~ t^3/4 - u^3, dW/dq ~ -3/4 t^2 + 3 u^2 with t = 2 - q, u = max(1 - q, 0).
@@ -739,6 +702,53 @@ __global__ void __launch_bounds__(KB_SCAN) k_blocks_scan(int32_t* row_off, int64
   if (tid == 0) {
     ctrl->nblk[0] = (uint32_t)s_carry;
     ctrl->tile_next[0] = 0u;  // this launch's block queue (several launches per step: X slabs)
+  }
+}
+
+// ------------------------------------------------------------------ candidate counter
+// candidate_pairs of the gather traversal (kernels.py:355-371, counted before the distance
+// test) depends on the cell tables alone: a fluid target of cell c visits every particle of
+// both lists in its stencil rows' x ranges [max(x - r, 0), min(x + r, nx - 1)] except itself, a
+// boundary target the fluid ones, so  cand = sum_c nf_c (F_c + B_c - 1) + nb_c F_c.  One thread
+// per target cell of the window (x fastest: coalesced table loads, empty cells leave after two
+// loads); the FP32 gather kernels then carry no per-target counting (its global loads sat on
+// every block's setup path).
+constexpr int KC_THREADS = 256;
+__global__ void __launch_bounds__(KC_THREADS) k_cand_cells(sphb_grid_t g, int64_t ncells,
+                                                          const int32_t* __restrict__ beg,
+                                                          const int32_t* __restrict__ end,
+                                                          sphb_ctrl_t* ctrl) {
+  if (!step_live(ctrl)) return;
+  const int nx = g.dims[0], ny = g.dims[1], nz = g.dims[2], R = g.reach;
+  const int span = g.tx1 - g.tx0;
+  const int64_t total = (int64_t)span * ny * nz;
+  unsigned long long acc = 0;
+  for (int64_t t = (int64_t)blockIdx.x * KC_THREADS + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * KC_THREADS) {
+    const int64_t row = t / span;
+    const int x = g.tx0 + (int)(t - row * span);
+    const int64_t cb = (int64_t)nx * row + x, cf = ncells + cb;
+    const int nb = end[cb] - beg[cb], nf = end[cf] - beg[cf];
+    if (nb <= 0 && nf <= 0) continue;
+    const int y = (int)(row % ny), z = (int)(row / ny);
+    const int xlo = max(x - R, 0), xhi = min(x + R, nx - 1);
+    long long F = 0, B = 0;
+    for (int zz = max(z - R, 0); zz <= min(z + R, nz - 1); ++zz)
+      for (int yy = max(y - R, 0); yy <= min(y + R, ny - 1); ++yy) {
+        const int64_t rb = (int64_t)nx * (yy + (int64_t)ny * zz), rf = ncells + rb;
+        F += end[rf + xhi] - beg[rf + xlo];
+        B += end[rb + xhi] - beg[rb + xlo];
+      }
+    acc += (unsigned long long)((long long)max(nf, 0) * (F + B - 1) + (long long)max(nb, 0) * F);
+  }
+  __shared__ unsigned long long s_acc[KC_THREADS / 32];
+  acc = warp_sum_u64(acc);
+  if ((threadIdx.x & 31) == 0) s_acc[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    acc = threadIdx.x < KC_THREADS / 32 ? s_acc[threadIdx.x] : 0ull;
+    acc = warp_sum_u64(acc);
+    if (threadIdx.x == 0 && acc) atomicAdd((unsigned long long*)&ctrl->counters[0], acc);
   }
 }
 
@@ -1712,9 +1722,7 @@ __global__ void __launch_bounds__(NW * 32, V8_MINB) k_interact_v8(KArgs a, K32 k
         }
       }
       if (isf) cand -= 1;
-    } else if (!V8_SYM) {
-      cand = cand_count(a, sSeg, nseg, valid, isf, xlo, xhi, rsy, rsz, lane);
-    }
+    }  // (gather builds: counted from the cell tables, k_cand_cells)
 
     // A / C fragments of the tensor-core screen: target row r = 16 m + g (+ 8) holds
     // K = (-2x, -2y, -2z, 1, 0, 0, 0, 0) and C = |x|^2 - thr of its FP16 block-centred position
@@ -2297,7 +2305,9 @@ namespace SPHB_PI_NS {
 
 int64_t interact_launch_count(int64_t n) {
   (void)n;
-  return V8_SYM ? 5 : 4;  // k_blocks (count, scan, write), the interaction kernel (+ k_dt_f32)
+  // k_blocks (count, scan, write), the interaction kernel; the FP32 gather builds add
+  // k_cand_cells, the symmetric one k_dt_f32 (counted by the callers: device.py, dslab.py)
+  return 4;
 }
 
 static int launch_wall(const sphb_params_t& p, const sphb_grid_t& g, int64_t n, int64_t nb,
@@ -2386,6 +2396,12 @@ int launch_interact(sphb_workspace* ws, const sphb_params_t& p, const sphb_grid_
   // drho + visc only) of the same cells share the staged candidates
   a.blocks = ws->blocks;
   const bool sym = V8_SYM && p.precision == SPHB_FP32;
+  if (p.precision == SPHB_FP32 && !sym) {  // the FP32 gather kernels' candidate counter
+    const int64_t ncand = (int64_t)(g.tx1 - g.tx0) * g.dims[1] * g.dims[2];
+    const unsigned kc = (unsigned)std::max<int64_t>(1, std::min<int64_t>((ncand + KC_THREADS - 1) / KC_THREADS, 148 * 8));
+    k_cand_cells<<<kc, KC_THREADS, 0, s>>>(g, a.ncells, beg, end, ctrl);
+    if (int rc = sphb_check_launch("k_cand_cells")) return rc;
+  }
   if (sym) {  // every block adds into these (targets' own sums and their partners' reactions)
     cudaMemsetAsync(acc, 0, sizeof(float4) * (size_t)n, s);
     cudaMemsetAsync(visc, 0, sizeof(float) * (size_t)n, s);

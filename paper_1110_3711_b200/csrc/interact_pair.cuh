@@ -211,7 +211,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_interact_v12(KArgs a, K32 k32) {
   const uint32_t ring = pin_u32(smem_addr(g_sm32 + MASK0) + 8u * (warp * RINGC * 32 + lane));
   const uint32_t rend = ring + 256u * RINGC;
 
-  unsigned long long c_cand = 0, c_hits = 0;
+  unsigned long long c_hits = 0;
   long long c_ff = 0;
   double dtf_min = INFINITY, dtcv_min = INFINITY;
 
@@ -508,13 +508,6 @@ __global__ void __launch_bounds__(NW * 32, 1) k_interact_v12(KArgs a, K32 k32) {
       s[k].ax = s[k].ay = s[k].az = s[k].dr = s[k].hits = bc(0.0f);
       s[k].vd0 = s[k].vd1 = 0.0f;
     }
-    // candidate counts: the sum of each target's stencil-row range lengths, per distinct
-    // (x range, row, list) of the warp (cand_count)
-    unsigned long long cand[2];
-#pragma unroll
-    for (int t = 0; t < 2; ++t)
-      cand[t] = cand_count(a, sSeg, nseg, valid[t], isf[t], xlo[t], xhi[t], rsy[t], rsz[t], lane);
-
     // A fragments of the screen: M-tile m holds target slot m / 2 of lanes 16 (m % 2) + row
     // (rows g, g + 8 of the tile); C = |x|^2 - thr, or NOHIT for a target the row must skip
     uint32_t fa[4][2];
@@ -776,7 +769,6 @@ __global__ void __launch_bounds__(NW * 32, 1) k_interact_v12(KArgs a, K32 k32) {
     for (int t = 0; t < 2; ++t) {
       if (!valid[t]) continue;
       const int hits = (int)(t ? hi(s[0].hits) : lo(s[0].hits));
-      c_cand += cand[t];
       c_hits += (unsigned long long)hits;
       c_ff += isf[t] ? hits : -hits;  // ff = F targets' hits - B targets' hits (F-B == B-F)
       const double ax = (double)((t ? hi(s[0].ax) : lo(s[0].ax)) * mfac);
@@ -806,13 +798,11 @@ __global__ void __launch_bounds__(NW * 32, 1) k_interact_v12(KArgs a, K32 k32) {
 
   dtf_min = warp_min(dtf_min);
   dtcv_min = warp_min(dtcv_min);
-  c_cand = warp_sum_u64(c_cand);
   c_hits = warp_sum_u64(c_hits);
   const unsigned long long ffu = warp_sum_u64((unsigned long long)c_ff);
   if (lane == 0) {
     if (dtf_min < INFINITY) atomic_min_pos(&a.ctrl->dtmin_f, dtf_min);
     if (dtcv_min < INFINITY) atomic_min_pos(&a.ctrl->dtmin_cv, dtcv_min);
-    if (c_cand) atomicAdd((unsigned long long*)&a.ctrl->counters[0], c_cand);
     if (c_hits) {
       atomicAdd((unsigned long long*)&a.ctrl->counters[1], c_hits);
       atomicAdd((unsigned long long*)&a.ctrl->counters[2], c_hits);

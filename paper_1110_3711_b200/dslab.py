@@ -929,9 +929,10 @@ class DeviceSlabSim:
         r = self.ranks[0]
         base = int(_lib.lib().sphb_step_launch_count(_lib.ref(r.grid), r.n))
         npi = len(r.edge_grids) + len(r.inner_grids)
-        # + band count (2); each further interaction launch: k_blocks x 3 + the kernel;
-        # pack, two band updates and the tail on a rank with neighbours
-        return base + 2 + 4 * (npi - 1) + (4 if r.sides else 0)
+        # + band count (2); every interaction launch: k_blocks x 3, k_cand_cells and the kernel
+        # (the first one's four in base); pack, two band updates and the tail on a rank with
+        # neighbours
+        return base + 2 + npi + 4 * (npi - 1) + (4 if r.sides else 0)
 
 
 def estimate_steps_per_sync() -> int:
