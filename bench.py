@@ -50,7 +50,7 @@ def parse():
                     help="c1|c2|c3|c4_1..c4_8|c5 (default c3 at N=1, c3w_N above)")
     ap.add_argument("--n-subdiv", type=int, default=1)
     ap.add_argument("--precision", default="fp32", choices=["fp32", "fp64"])
-    ap.add_argument("--e2e-steps", type=int, default=20)
+    ap.add_argument("--e2e-steps", type=int, default=40)
     ap.add_argument("--graph", default="auto", choices=["auto", "on", "off"],
                     help="replay the timed steps as one CUDA graph (auto: below 2M particles)")
     ap.add_argument("--pi-block", default="auto", choices=["auto", "128", "256", "384", "512"],
@@ -59,8 +59,8 @@ def parse():
                     help="FP32 interaction kernel: tuned (the faster of gather / paired, timed in the "
                          "warm-up like run_simulation(pi_kernel='tuned')), one-sided gather, "
                          "symmetric pair evaluation, or the gather with two targets per lane (paired)")
-    ap.add_argument("--e2e-chunks", type=int, default=8,
-                    help="row chunks of the pipelined H2D/D2H state round trip (1 = serial)")
+    ap.add_argument("--e2e-chunks", type=int, default=16,
+                    help="byte-range chunks of the pipelined H2D/D2H state round trip (1 = serial)")
     ap.add_argument("--collapsed-step", type=int, default=6000,
                     help="N=1: also time the step after advancing the run to this step (the "
                          "column has collapsed: cells hold uneven counts); 0 = skip")
@@ -676,81 +676,90 @@ def main():
 
     # ---- e2e: the same step through the C ABI with HOST buffers (H2D state in, D2H state out)
     # Every step copies its input state H2D from pinned host memory in the reference's own
-    # layout (ParticleSystem pos/vel/rho/id + VerletState vel_prev/rho_prev, 52 B/particle),
+    # layout (ParticleSystem id/pos/vel/rho + VerletState vel_prev/rho_prev, 52 B/particle),
     # converts it to the step's rows (sphb_state_from_soa), steps, converts back
-    # (sphb_state_to_soa) and copies the result state D2H.  The round trip is pipelined in
-    # row chunks over the full-duplex PCIe link: the H2D of chunk c for step k+1 starts as soon
-    # as the D2H of chunk c of step k has landed, and each chunk is converted as it lands.
+    # (sphb_state_to_soa) and copies the result state D2H.  The six host arrays are views of
+    # one pinned allocation (and their device images of one device buffer), so the round trip
+    # moves byte-range chunks of a single buffer -- one copy per chunk and direction, which
+    # keeps the full-duplex PCIe link busy (six copies per row chunk measured 13.7 vs 12.4 ms
+    # per round trip, profiles/r02br_pcie_chunks.txt): the H2D of chunk c for step k+1 starts
+    # as soon as the D2H of chunk c of step k has landed.
     h2d = d2h = 0
     e2e_value = None
     if args.e2e_steps > 0:
         L = _lib.lib()
         n = sim.n
         names = ("pos", "vel", "rho", "vel_prev", "rho_prev")
-        shapes = {"pos": (n, 3), "vel": (n, 3), "rho": (n,), "vel_prev": (n, 3), "rho_prev": (n,)}
-        hsoa = {k: torch.empty(shapes[k], dtype=torch.float32, pin_memory=True) for k in names}
-        dsoa = {k: torch.empty(shapes[k], dtype=torch.float32, device="cuda") for k in names}
-        hid = torch.empty(n, dtype=torch.int64, pin_memory=True)
+        width = {"pos": 3, "vel": 3, "rho": 1, "vel_prev": 3, "rho_prev": 1}
         ptr = lambda t: t.data_ptr()  # noqa: E731
         stream = lambda: torch.cuda.current_stream().cuda_stream  # noqa: E731
+        # layout: id (int64) first, then the f32 arrays, each at a 16-B aligned offset
+        offs, off = {"id": 0}, 8 * n
+        for k in names:
+            off = (off + 15) // 16 * 16
+            offs[k] = off
+            off += 4 * width[k] * n
+        nbytes = off
+        hbuf = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+        dbuf = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
 
-        def to_soa(lo, hi):
-            _lib.check(L.sphb_state_to_soa(lo, hi - lo, ptr(sim.posp), ptr(sim.velr), ptr(sim.prev),
+        def views(buf):
+            v = {"id": buf[:8 * n].view(torch.int64)}
+            for k in names:
+                a = buf[offs[k]:offs[k] + 4 * width[k] * n].view(torch.float32)
+                v[k] = a.view(n, width[k]) if width[k] > 1 else a
+            return v
+
+        hsoa, dsoa = views(hbuf), views(dbuf)
+
+        def to_soa():
+            _lib.check(L.sphb_state_to_soa(0, n, ptr(sim.posp), ptr(sim.velr), ptr(sim.prev),
                                            *[ptr(dsoa[k]) for k in names], stream()), "to_soa")
+            dsoa["id"].copy_(sim.id[:n])
 
-        def from_soa(lo, hi):
-            _lib.check(L.sphb_state_from_soa(lo, hi - lo, *[ptr(dsoa[k]) for k in names],
+        def from_soa():
+            _lib.check(L.sphb_state_from_soa(0, n, *[ptr(dsoa[k]) for k in names],
                                              ptr(sim.posp), ptr(sim.velr), ptr(sim.prev), stream()),
                        "from_soa")
+            sim.id[:n].copy_(dsoa["id"])
 
-        to_soa(0, n)  # the host arrays start as the current state
-        for k in names:
-            hsoa[k].copy_(dsoa[k])
-        hid.copy_(sim.id[:n])
-        pairs = [(hsoa[k], dsoa[k]) for k in names] + [(hid, sim.id[:n])]
-        h2d = d2h = sum(h.numel() * h.element_size() for h, _ in pairs)
-        nchunk = max(1, min(args.e2e_chunks, n))
-        bounds = [(n * c // nchunk, n * (c + 1) // nchunk) for c in range(nchunk)]
+        to_soa()  # the host arrays start as the current state
+        hbuf.copy_(dbuf)
+        h2d = d2h = 8 * n + sum(4 * width[k] * n for k in names)  # the arrays' bytes (no padding)
+        nchunk = max(1, min(args.e2e_chunks, nbytes // (1 << 20)))
+        bounds = [(nbytes * c // nchunk, nbytes * (c + 1) // nchunk) for c in range(nchunk)]
         comp = torch.cuda.current_stream()
         s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
-        ev_in = [torch.cuda.Event() for _ in bounds]
         ev_out = [torch.cuda.Event() for _ in bounds]
-        ev_packed = [torch.cuda.Event() for _ in bounds]
+        ev_in, ev_packed = torch.cuda.Event(), torch.cuda.Event()
 
-        def h2d_chunk(c):
-            lo, hi = bounds[c]
-            for hbuf, dbuf in pairs:
-                dbuf[lo:hi].copy_(hbuf[lo:hi], non_blocking=True)
+        def h2d_all(after_out):
+            with torch.cuda.stream(s_in):
+                for c, (lo, hi) in enumerate(bounds):
+                    if after_out:
+                        s_in.wait_event(ev_out[c])
+                    dbuf[lo:hi].copy_(hbuf[lo:hi], non_blocking=True)
+                ev_in.record(s_in)
 
         torch.cuda.synchronize()
         a, b = Ev(), Ev()
         a.record()
         s_in.wait_stream(comp)
-        with torch.cuda.stream(s_in):
-            for c in range(nchunk):
-                h2d_chunk(c)
-                ev_in[c].record(s_in)
+        h2d_all(False)
         for k in range(args.e2e_steps):
-            for c, (lo, hi) in enumerate(bounds):  # convert each chunk as it lands
-                comp.wait_event(ev_in[c])
-                from_soa(lo, hi)
-            sim.first_keys_resync()
+            comp.wait_event(ev_in)
+            from_soa()
+            sim.first_keys_resync(keep_order=True)  # the same n rows: movers-only sort stays valid
             sim.launch_step()
-            for c, (lo, hi) in enumerate(bounds):  # each chunk leaves as soon as it is converted
-                to_soa(lo, hi)
-                ev_packed[c].record(comp)
+            to_soa()
+            ev_packed.record(comp)
+            s_out.wait_event(ev_packed)
             with torch.cuda.stream(s_out):
                 for c, (lo, hi) in enumerate(bounds):
-                    s_out.wait_event(ev_packed[c])
-                    for hbuf, dbuf in pairs:
-                        hbuf[lo:hi].copy_(dbuf[lo:hi], non_blocking=True)
+                    hbuf[lo:hi].copy_(dbuf[lo:hi], non_blocking=True)
                     ev_out[c].record(s_out)
             if k + 1 < args.e2e_steps:
-                with torch.cuda.stream(s_in):
-                    for c in range(nchunk):
-                        s_in.wait_event(ev_out[c])
-                        h2d_chunk(c)
-                        ev_in[c].record(s_in)
+                h2d_all(True)
         comp.wait_stream(s_out)
         b.record()
         torch.cuda.synchronize()
@@ -864,8 +873,10 @@ def main():
                        "path": "per step: pinned host state in the reference's layout (pos, vel, "
                                "rho, vel_prev, rho_prev, id: 52 B/particle) -> H2D -> "
                                "sphb_state_from_soa -> sphb_* step -> sphb_state_to_soa -> D2H, "
-                               f"round trip pipelined in {args.e2e_chunks} row chunks over "
-                               "full-duplex PCIe (H2D of step k+1 chunk c after D2H of step k chunk c)"}
+                               f"round trip pipelined in {args.e2e_chunks} byte-range chunks of "
+                               "one buffer per side (the six arrays are views of one pinned "
+                               "allocation) over full-duplex PCIe (H2D of step k+1 chunk c after "
+                               "D2H of step k chunk c)"}
     if collapsed is not None:
         line["collapsed"] = collapsed
     if fp64 is not None:

@@ -145,6 +145,18 @@ int sphb_workspace_create(int64_t n_max, int64_t ncells_max, sphb_workspace_t** 
 int sphb_workspace_destroy(sphb_workspace_t* ws);
 /* Zeroes the workspace histogram (needed only after an aborted step). */
 int sphb_workspace_reset(sphb_workspace_t* ws, sphb_stream_t s);
+/* Rows rewritten from outside (a host upload of the same n rows, e.g. the reference-layout
+ * round trip of sphb_state_from_soa): sphb_workspace_clear_hist zeroes the per-cell
+ * histogram that sphb_cell_keys then recounts (K7 already counted the device's own keys).
+ * sphb_cell_keys marks the previous sort's order as unknown (the next sphb_sort_ranges /
+ * sphb_step sorts by radix); sphb_workspace_trust_order, called after it, lets that sort
+ * take the movers-only path again.  Valid whenever keys_sorted, beg and end are still those
+ * of the previous sort of n rows: the movers-only sort is the stable sort of the current rows
+ * in ANY order (a row whose key differs from keys_sorted at its index is a mover; a permuted
+ * upload exceeds the mover cap and takes the radix path), and the device re-checks the
+ * previous order's consistency before using it (nl.cu, K2' movers-only sort). */
+int sphb_workspace_clear_hist(sphb_workspace_t* ws, sphb_stream_t s);
+int sphb_workspace_trust_order(sphb_workspace_t* ws, sphb_stream_t s);
 /* Movers-only sort threshold of sphb_step (default and maximum min(n_max, 2^20)): a
  * step whose rows changed cell for at most `cap` rows is sorted by counting from the previous
  * order; otherwise (or cap = -1) by the LSD radix sort.  Both give the identical permutation

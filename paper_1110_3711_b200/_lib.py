@@ -96,6 +96,8 @@ def lib():
         "sphb_workspace_create": ([c_i64, c_i64, ctypes.POINTER(c_p)], c_i32),
         "sphb_workspace_destroy": ([P], c_i32),
         "sphb_workspace_reset": ([P, P], c_i32),
+        "sphb_workspace_clear_hist": ([P, P], c_i32),
+        "sphb_workspace_trust_order": ([P, P], c_i32),
         "sphb_workspace_bytes": ([P], c_i64),
         "sphb_workspace_set_mover_cap": ([P, c_i64], c_i32),
         "sphb_workspace_sort_info": ([P, P, P], c_i32),
@@ -148,7 +150,8 @@ def lib():
 
 
 EXPORTED = ("sphb_last_error", "sphb_version", "sphb_workspace_create", "sphb_workspace_destroy",
-            "sphb_workspace_reset", "sphb_workspace_bytes",
+            "sphb_workspace_reset", "sphb_workspace_clear_hist", "sphb_workspace_trust_order",
+            "sphb_workspace_bytes",
             "sphb_workspace_set_mover_cap", "sphb_workspace_sort_info", "sphb_workspace_set_pi_block", "sphb_workspace_set_pi_kernel", "sphb_ctrl_init", "sphb_cell_keys",
             "sphb_sort", "sphb_sort_ranges", "sphb_nl_build", "sphb_reorder", "sphb_cell_ranges",
             "sphb_cell_ranges_from_sorted", "sphb_cell_hist",

@@ -203,6 +203,20 @@ int sphb_workspace_reset(sphb_workspace_t* ws, sphb_stream_t s) {
   return SPHB_OK;
 }
 
+int sphb_workspace_clear_hist(sphb_workspace_t* ws, sphb_stream_t s) {
+  SPHB_NONNULL(ws);
+  SPHB_CUDA(cudaMemsetAsync(ws->cnt, 0, sizeof(uint32_t) * (2 * ws->ncells_max + 1), (cudaStream_t)s));
+  return SPHB_OK;
+}
+
+int sphb_workspace_trust_order(sphb_workspace_t* ws, sphb_stream_t s) {
+  SPHB_NONNULL(ws);
+  // state words 0 (order established) = 1, 1 (inconsistency seen) = 0 (little endian)
+  SPHB_CUDA(cudaMemsetAsync(ws->mv_state, 0, 2 * sizeof(uint32_t), (cudaStream_t)s));
+  SPHB_CUDA(cudaMemsetAsync(ws->mv_state, 1, 1, (cudaStream_t)s));
+  return SPHB_OK;
+}
+
 int sphb_workspace_set_mover_cap(sphb_workspace_t* ws, int64_t cap) {
   SPHB_NONNULL(ws);
   if (cap < -1 || cap > ws->mover_cap_max)

@@ -286,10 +286,18 @@ class DeviceSim:
                                     self.nb, _ptr(self.keys), None, _ptr(self.ctrl), _stream()),
                    "sphb_cell_keys")
 
-    def first_keys_resync(self):
-        """K1 for a state written from outside (host upload): histogram reset + keys."""
-        self.ws.reset()
-        self.first_keys()
+    def first_keys_resync(self, keep_order: bool = False):
+        """K1 for a state written from outside (host upload): histogram reset + keys.
+        keep_order: the upload replaced the same n rows (e.g. the reference-layout round trip
+        of sphb_state_from_soa) -- the next sort may still take the movers-only path, which is
+        the stable sort of the rows in any order (sphb_workspace_trust_order)."""
+        if keep_order:
+            _lib.check(_lib.lib().sphb_workspace_clear_hist(self.ws.handle, _stream()), "clear_hist")
+            self.first_keys()
+            _lib.check(_lib.lib().sphb_workspace_trust_order(self.ws.handle, _stream()), "trust_order")
+        else:
+            self.ws.reset()
+            self.first_keys()
 
     @property
     def symplectic(self) -> bool:

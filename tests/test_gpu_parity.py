@@ -571,6 +571,53 @@ def test_state_soa_round_trip():
     assert L.sphb_state_from_soa(-1, 1, *ptrs, 0, 0, 0, s) == _lib.SPHB_E_INVALID
 
 
+@pytest.mark.parametrize("shuffle", [False, True])
+def test_upload_keep_order_equals_reset(shuffle):
+    """A host round trip of the state (sphb_state_to_soa -> host -> sphb_state_from_soa) and
+    first_keys_resync(keep_order=True) (sphb_workspace_clear_hist / trust_order) sorts the next
+    step by the movers-only path, and the steps equal those after a full reset (radix sort);
+    with the rows shuffled inside each list before the upload too (every row is then a mover)."""
+    from paper_1110_3711_b200 import _lib
+    sc = sph.Scenario(dp=0.006)
+    prm = sph.make_params(sc)
+    system = sph.build_dam_break(sc, prm)
+    a = D.DeviceSim(system, prm, reach=1)
+    b = D.DeviceSim(system, prm, reach=1)
+    for _ in range(3):
+        a.launch_step()
+        b.launch_step()
+    n, nb = a.n, a.nb
+    L, s = _lib.lib(), torch.cuda.current_stream().cuda_stream
+    shapes = [(n, 3), (n, 3), (n,), (n, 3), (n,)]
+    soa = [torch.empty(sh, device="cuda") for sh in shapes]
+    ptrs = [t.data_ptr() for t in soa]
+    _lib.check(L.sphb_state_to_soa(0, n, a.posp.data_ptr(), a.velr.data_ptr(), a.prev.data_ptr(),
+                                   *ptrs, s), "to_soa")
+    ids = a.id[:n].clone()
+    if shuffle:
+        g = torch.Generator(device="cpu").manual_seed(7)
+        perm = torch.cat([torch.randperm(nb, generator=g), nb + torch.randperm(n - nb, generator=g)]).cuda()
+        soa = [t[perm].contiguous() for t in soa]
+        ptrs = [t.data_ptr() for t in soa]
+        ids = ids[perm]
+    host = [t.cpu() for t in soa]  # the round trip through host memory
+    for sim, keep in ((a, True), (b, False)):
+        dev = [t.cuda() for t in host]
+        _lib.check(L.sphb_state_from_soa(0, n, *[t.data_ptr() for t in dev], sim.posp.data_ptr(),
+                                         sim.velr.data_ptr(), sim.prev.data_ptr(), s), "from_soa")
+        sim.id[:n].copy_(ids)
+        sim.first_keys_resync(keep_order=keep)
+        sim.launch_step()
+        torch.cuda.synchronize()
+        movers, mode = sim.ws.sort_info()
+        assert mode == (0 if keep else 1), (keep, mode, movers)
+        if keep:
+            assert (movers > n // 2) if shuffle else (movers < n // 100)
+        sim.launch_step()
+    for x, y in zip(a.download(), b.download()):
+        assert np.array_equal(x, y)
+
+
 @pytest.mark.parametrize("block", [256, 384, "symmetric", "paired"])
 @pytest.mark.parametrize("name", ["c1", "c2"])
 def test_pi_block_matches_128(name, block):
