@@ -446,8 +446,9 @@ def run_slabs(args, cfg_name, sc, system, prm, prec, world, rank, local):
     total_ms = float(tt.item())
     # e2e: the same decomposed step with each rank's resident rows round-tripped through pinned
     # host buffers every step, in the reference's state layout (pos, vel, rho, vel_prev,
-    # rho_prev, id: 52 B/row; sphb_state_to_soa / sphb_state_from_soa) and pipelined in row
-    # chunks over the full-duplex PCIe link (as the single-GPU path)
+    # rho_prev, id: 52 B/row; sphb_state_to_soa / sphb_state_from_soa) and pipelined in
+    # byte-range chunks of one buffer per side over the full-duplex PCIe link (as the
+    # single-GPU path)
     h2d = d2h = 0
     e2e_value = None
     if args.e2e_steps > 0:
@@ -455,48 +456,61 @@ def run_slabs(args, cfg_name, sc, system, prm, prec, world, rank, local):
         cap = int(me.n * 1.5) + 1024
         names = ("pos", "vel", "rho", "vel_prev", "rho_prev")
         width = {"pos": 3, "vel": 3, "rho": 1, "vel_prev": 3, "rho_prev": 1}
-        mk = lambda w, **kw: torch.empty((cap, w) if w > 1 else (cap,), dtype=torch.float32, **kw)  # noqa: E731
-        hsoa = {k: mk(width[k], pin_memory=True) for k in names}
-        dsoa = {k: mk(width[k], device="cuda") for k in names}
-        hid = torch.empty(cap, dtype=torch.int64, pin_memory=True)
+        # the six arrays of this step's n rows as views of one buffer per side (id first, the
+        # f32 arrays at 16-B aligned offsets): byte-range chunks, one copy each way per chunk
+        hbuf = torch.empty(56 * cap + 128, dtype=torch.uint8, pin_memory=True)
+        dbuf = torch.empty(56 * cap + 128, dtype=torch.uint8, device="cuda")
+
+        def layout(n):
+            offs, off = {"id": 0}, 8 * n
+            for k in names:
+                off = (off + 15) // 16 * 16
+                offs[k] = off
+                off += 4 * width[k] * n
+            return offs, off
+
+        def views(buf, n, offs):
+            v = {"id": buf[:8 * n].view(torch.int64)}
+            for k in names:
+                x = buf[offs[k]:offs[k] + 4 * width[k] * n].view(torch.float32)
+                v[k] = x.view(n, width[k]) if width[k] > 1 else x
+            return v
+
         nchunk = max(1, args.e2e_chunks)
         s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
-        ev_in = [torch.cuda.Event() for _ in range(nchunk)]
         ev_out = [torch.cuda.Event() for _ in range(nchunk)]
-        ev_packed = torch.cuda.Event()
+        ev_in, ev_packed = torch.cuda.Event(), torch.cuda.Event()
         torch.cuda.synchronize()
         a, b = Ev(), Ev()
         a.record()
-        nbytes = 0
         for _ in range(args.e2e_steps):
             comp = torch.cuda.current_stream()
             n = me.n
             if n > cap:
                 raise RuntimeError("e2e staging too small for this rank's rows")
+            offs, nb_ = layout(n)
+            dsoa = views(dbuf, n, offs)
             _lib.check(L.sphb_state_to_soa(0, n, me.a.posp.data_ptr(), me.a.velr.data_ptr(),
                                            me.a.prev.data_ptr(), *[dsoa[k].data_ptr() for k in names],
                                            comp.cuda_stream), "to_soa")
+            dsoa["id"].copy_(me.a.id[:n])
             ev_packed.record(comp)
-            bounds = [(n * c // nchunk, n * (c + 1) // nchunk) for c in range(nchunk)]
-            pairs = [(hsoa[k], dsoa[k]) for k in names] + [(hid, me.a.id)]
+            bounds = [(nb_ * c // nchunk, nb_ * (c + 1) // nchunk) for c in range(nchunk)]
             s_out.wait_event(ev_packed)
             for c, (lo, hi) in enumerate(bounds):
                 with torch.cuda.stream(s_out):
-                    for hbuf, dbuf in pairs:
-                        hbuf[lo:hi].copy_(dbuf[lo:hi], non_blocking=True)
+                    hbuf[lo:hi].copy_(dbuf[lo:hi], non_blocking=True)
                     ev_out[c].record(s_out)
                 with torch.cuda.stream(s_in):
                     s_in.wait_event(ev_out[c])
-                    for hbuf, dbuf in pairs:
-                        dbuf[lo:hi].copy_(hbuf[lo:hi], non_blocking=True)
-                    ev_in[c].record(s_in)
-            for c, (lo, hi) in enumerate(bounds):
-                comp.wait_event(ev_in[c])
-                _lib.check(L.sphb_state_from_soa(lo, hi - lo, *[dsoa[k].data_ptr() for k in names],
-                                                 me.a.posp.data_ptr(), me.a.velr.data_ptr(),
-                                                 me.a.prev.data_ptr(), comp.cuda_stream), "from_soa")
-            nbytes = n * 52
-            h2d = d2h = nbytes
+                    dbuf[lo:hi].copy_(hbuf[lo:hi], non_blocking=True)
+            ev_in.record(s_in)
+            comp.wait_event(ev_in)
+            _lib.check(L.sphb_state_from_soa(0, n, *[dsoa[k].data_ptr() for k in names],
+                                             me.a.posp.data_ptr(), me.a.velr.data_ptr(),
+                                             me.a.prev.data_ptr(), comp.cuda_stream), "from_soa")
+            me.a.id[:n].copy_(dsoa["id"])
+            h2d = d2h = n * 52
             sim.step()
         b.record()
         torch.cuda.synchronize()
