@@ -60,6 +60,9 @@ constexpr int BT = NW * 32 * (SPHB_PAIR ? 2 : 1);  // targets per block
 #endif
 constexpr int RING = SPHB_H16 ? 32 : 48;  // per-lane FIFO entries (non-empty 32-candidate words)
 constexpr int MAXSEG = 128;      // stencil row segments per block (2 lists x (2r+1)^2, r <= 3)
+#ifndef HYBRID_T
+#define HYBRID_T 32  // n = 1, 384-target build: quads below this mean cell count become bricks
+#endif
 
 template <typename R>
 struct Cfg;
@@ -514,6 +517,64 @@ __device__ __forceinline__ bool screen(const KArgs& a, const C32&, const Own<dou
 __device__ __forceinline__ int block_slots(int nf, int ntot) {
   return SPHB_PAIR ? ntot + (nf & 1) : ntot;
 }
+// Row blocks of one cell row r (records written at out when !COUNT); the record count, on
+// every lane.  s_ends: [span] fluid ends, then [span] boundary ends of the row.
+template <bool COUNT>
+__device__ int row_records(const sphb_grid_t& g, int64_t ncells, const int32_t* __restrict__ beg,
+                           const int32_t* __restrict__ end, int64_t r, int4* out, int maxc,
+                           int32_t* s_ends, int lane) {
+  const int nx = g.dims[0], span = g.tx1 - g.tx0;
+  const int64_t cb = r * nx, cf = ncells + r * nx;  // row offsets in the B / F tables
+  if (span <= 0 ||
+      (end[cf + g.tx1 - 1] <= beg[cf + g.tx0] && end[cb + g.tx1 - 1] <= beg[cb + g.tx0]))
+    return 0;
+  for (int k = lane; k < span; k += 32) {
+    s_ends[k] = end[cf + g.tx0 + k];
+    s_ends[span + k] = end[cb + g.tx0 + k];
+  }
+  __syncwarp();
+  int nrec = 0;
+  if (lane == 0) {
+    auto emit = [&](int4 b, int x0, int x1) {
+      if (!COUNT) {
+        out[2 * nrec] = b;
+        out[2 * nrec + 1] = make_int4((int)r, x0, x1, 0);
+      }
+      ++nrec;
+    };
+    int32_t f0 = beg[cf + g.tx0], b0 = beg[cb + g.tx0];  // open block
+    int32_t fcur = f0, bcur = b0;
+    int xa = -1, xl = -1;  // first / last non-empty cell of the open block
+    for (int k = 0; k < span; ++k) {
+      const int x = g.tx0 + k;
+      const int32_t fe = s_ends[k], be = s_ends[span + k];
+      if (fe == fcur && be == bcur) continue;  // empty cell
+      if ((block_slots(fe - f0, (fe - f0) + (be - b0)) > BT ||
+           (xa >= 0 && x - xa + 1 > maxc && 4 * ((fcur - f0) + (bcur - b0)) >= BT)) &&
+          (fcur > f0 || bcur > b0)) {  // close before this cell
+        emit(make_int4(f0, fcur, b0, bcur), xa, xl);
+        f0 = fcur;
+        b0 = bcur;
+        xa = -1;
+      }
+      if (block_slots(fe - f0, (fe - f0) + (be - b0)) > BT) {  // one oversized cell: single-list chunks of <= BT
+        for (int32_t p = f0; p < fe; p += BT) emit(make_int4(p, min(p + BT, fe), be, be), x, x);
+        for (int32_t p = b0; p < be; p += BT) emit(make_int4(fe, fe, p, min(p + BT, be)), x, x);
+        f0 = fe;
+        b0 = be;
+      } else {
+        if (xa < 0) xa = x;
+        xl = x;
+      }
+      fcur = fe;
+      bcur = be;
+    }
+    if (fcur > f0 || bcur > b0) emit(make_int4(f0, fcur, b0, bcur), xa, xl);
+  }
+  __syncwarp();
+  return __shfl_sync(SPHB_FULL, nrec, 0);
+}
+
 template <bool COUNT>
 __global__ void __launch_bounds__(32) k_blocks(sphb_grid_t g, int64_t ncells,
                                                const int32_t* __restrict__ beg,
@@ -533,6 +594,7 @@ __global__ void __launch_bounds__(32) k_blocks(sphb_grid_t g, int64_t ncells,
     for (int64_t r = blockIdx.x; r < nrows; r += gridDim.x) {
       const int y0 = 2 * (int)(r % nyb), z0 = 2 * (int)(r / nyb);
       int tot_all = 0;
+      int ne = 0;  // non-empty cells of the four rows (hybrid blocking)
       for (int k = lane; k < span; k += 32) {  // targets of the brick's cell column x
         const int x = g.tx0 + k;
         int c = 0, cf = 0;
@@ -540,17 +602,35 @@ __global__ void __launch_bounds__(32) k_blocks(sphb_grid_t g, int64_t ncells,
           const int yy = y0 + (sub & 1), zz = z0 + (sub >> 1);
           if (yy >= ny || zz >= nz) continue;
           const int64_t rb = (int64_t)nx * (yy + (int64_t)ny * zz) + x, rf = ncells + rb;
-          cf += end[rf] - beg[rf];
-          c += (end[rf] - beg[rf]) + (end[rb] - beg[rb]);
+          const int nfc = end[rf] - beg[rf], call = nfc + (end[rb] - beg[rb]);
+          cf += nfc;
+          c += call;
+          ne += call > 0 ? 1 : 0;
         }
         s_ends[k] = c;
         s_ends[span + k] = cf;  // fluid part (the paired build's slot padding)
         tot_all += c;
       }
       tot_all = __reduce_add_sync(SPHB_FULL, tot_all);
+      ne = __reduce_add_sync(SPHB_FULL, ne);
       __syncwarp();
       if (tot_all == 0) {
         if (COUNT && lane == 0) row_off[r] = 0;
+        continue;
+      }
+      if (brick > 1 && tot_all >= brick * ne) {
+        // hybrid blocking (n = 1 gather builds): a quad whose cells hold >= `brick` targets on
+        // average is cut into row blocks, row by row (dense rows fill 1-row blocks; bricks pay
+        // for sparse ones, where the column cap leaves 1-row blocks mostly empty)
+        int nrec = 0;
+        for (int sub = 0; sub < 4; ++sub) {
+          const int yy = y0 + (sub & 1), zz = z0 + (sub >> 1);
+          if (yy >= ny || zz >= nz) continue;
+          nrec += row_records<COUNT>(g, ncells, beg, end, (int64_t)yy + (int64_t)ny * zz,
+                                     COUNT ? nullptr : blk + 2 * ((int64_t)row_off[r] + nrec), maxc,
+                                     s_ends, lane);
+        }
+        if (COUNT && lane == 0) row_off[r] = nrec;
         continue;
       }
       if (lane == 0) {
@@ -605,58 +685,10 @@ __global__ void __launch_bounds__(32) k_blocks(sphb_grid_t g, int64_t ncells,
     return;
   }
   for (int64_t r = blockIdx.x; r < nrows; r += gridDim.x) {
-    const int64_t cb = r * nx, cf = ncells + r * nx;  // row offsets in the B / F tables
-    if (span <= 0 ||
-        (end[cf + g.tx1 - 1] <= beg[cf + g.tx0] && end[cb + g.tx1 - 1] <= beg[cb + g.tx0])) {
-      if (COUNT && lane == 0) row_off[r] = 0;
-      continue;
-    }
-    for (int k = lane; k < span; k += 32) {
-      s_ends[k] = end[cf + g.tx0 + k];
-      s_ends[span + k] = end[cb + g.tx0 + k];
-    }
-    __syncwarp();
-    if (lane == 0) {
-      int nrec = 0;
-      int4* out = COUNT ? nullptr : blk + 2 * (int64_t)row_off[r];
-      auto emit = [&](int4 b, int x0, int x1) {
-        if (!COUNT) {
-          out[2 * nrec] = b;
-          out[2 * nrec + 1] = make_int4((int)r, x0, x1, 0);
-        }
-        ++nrec;
-      };
-      int32_t f0 = beg[cf + g.tx0], b0 = beg[cb + g.tx0];  // open block
-      int32_t fcur = f0, bcur = b0;
-      int xa = -1, xl = -1;  // first / last non-empty cell of the open block
-      for (int k = 0; k < span; ++k) {
-        const int x = g.tx0 + k;
-        const int32_t fe = s_ends[k], be = s_ends[span + k];
-        if (fe == fcur && be == bcur) continue;  // empty cell
-        if ((block_slots(fe - f0, (fe - f0) + (be - b0)) > BT ||
-             (xa >= 0 && x - xa + 1 > maxc && 4 * ((fcur - f0) + (bcur - b0)) >= BT)) &&
-            (fcur > f0 || bcur > b0)) {  // close before this cell
-          emit(make_int4(f0, fcur, b0, bcur), xa, xl);
-          f0 = fcur;
-          b0 = bcur;
-          xa = -1;
-        }
-        if (block_slots(fe - f0, (fe - f0) + (be - b0)) > BT) {  // one oversized cell: single-list chunks of <= BT
-          for (int32_t p = f0; p < fe; p += BT) emit(make_int4(p, min(p + BT, fe), be, be), x, x);
-          for (int32_t p = b0; p < be; p += BT) emit(make_int4(fe, fe, p, min(p + BT, be)), x, x);
-          f0 = fe;
-          b0 = be;
-        } else {
-          if (xa < 0) xa = x;
-          xl = x;
-        }
-        fcur = fe;
-        bcur = be;
-      }
-      if (fcur > f0 || bcur > b0) emit(make_int4(f0, fcur, b0, bcur), xa, xl);
-      if (COUNT) row_off[r] = nrec;
-    }
-    __syncwarp();
+    const int nrec = row_records<COUNT>(g, ncells, beg, end, r,
+                                        COUNT ? nullptr : blk + 2 * (int64_t)row_off[r], maxc,
+                                        s_ends, lane);
+    if (COUNT && lane == 0) row_off[r] = nrec;
   }
 }
 
@@ -2375,7 +2407,16 @@ int launch_interact(sphb_workspace* ws, const sphb_params_t& p, const sphb_grid_
   if (sm_blocks > 48 * 1024) return sphb_set_error(SPHB_E_INVALID, "more than 6144 cell columns per slab");
   // bricks for h/2 cells (reach 2) in the FP32 gather kernel's cell order
   // (the 512-target build cuts bricks at every reach: 2 x 2 rows x 2 lattice cells at n = 1)
-  const int brick = ((g.reach == 2 || BT == 512 || SPHB_PAIR) && p.order == 0 && p.precision == SPHB_FP32 && !V8_SYM) ? 1 : 0;
+  // hybrid at n = 1 (the row-block gather builds): 2 x 2-row quads whose cells hold fewer than
+  // HYBRID_T targets on average become bricks, the others row blocks (k_blocks)
+  const bool brickable = p.order == 0 && p.precision == SPHB_FP32 && !V8_SYM;
+  static const char* hyb_env = getenv("SPHB_HYBRID_T");  // A/B experiments only (0 = rows)
+  // (measured, profiles/r02bu_hybrid_blocking_ab.txt: 384-target blocks collapsed 16.01 ->
+  // 15.79 ms at T = 32, at rest neutral; the 256-target build loses at rest, so rows only)
+  const int hyb_t = hyb_env ? atoi(hyb_env) : (BT == PI_LARGE_BLOCK ? HYBRID_T : 0);
+  const int brick = !brickable ? 0
+                    : (g.reach == 2 || BT == 512 || SPHB_PAIR) ? 1
+                    : (hyb_t > 1 ? hyb_t : 0);
   const int64_t nunits = brick ? (int64_t)((g.dims[1] + 1) / 2) * ((g.dims[2] + 1) / 2) : nrows;
   // block x extent: columns [cxa - r, cxb + r] must stay within the FP16 screen's +-4 (2h)
   // around the block centre (use16 in the kernels), span <= 16 / (cell_size / h) columns
