@@ -1,6 +1,7 @@
 """A few steps of a small dam break through every kernel family, for compute-sanitizer:
-FP32 (pi128, pi256 and pi384 interaction builds, movers-only + radix sorts, symplectic, wall force,
-energy, SoA state conversion) and FP64.
+FP32 (pi128, pi256 and pi384 interaction builds -- the last with the hybrid brick / row
+blocking --, the candidate counter, movers-only + radix sorts, the upload resync, symplectic,
+wall force, energy, SoA state conversion) and FP64.
 
   compute-sanitizer --tool memcheck|racecheck|synccheck|initcheck python tools/sanitize_steps.py
 """
@@ -36,6 +37,8 @@ for precision, block, integ in ((0, 128, "verlet"), (0, 256, "verlet"), (0, 384,
                                    *[t.data_ptr() for t in soa], s), "to_soa")
     _lib.check(L.sphb_state_from_soa(0, n, *[t.data_ptr() for t in soa], sim.posp.data_ptr(),
                                      sim.velr.data_ptr(), sim.prev.data_ptr(), s), "from_soa")
+    sim.first_keys_resync(keep_order=True)  # the upload path (clear_hist / trust_order)
+    sim.launch_step()
     torch.cuda.synchronize()
     assert sim.error() is None, sim.error()
     print("ok", precision, block, integ, sim.ws.sort_info(), flush=True)
