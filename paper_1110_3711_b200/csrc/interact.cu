@@ -511,6 +511,10 @@ __device__ __forceinline__ bool screen(const KArgs& a, const C32&, const Own<dou
 // 6 x 6 rows x 16 cells) where 1-row blocks need ~31.  Record: (0, 0, 0, 0),
 // (row of (y0, z0), first cell x, last cell x, 1).  A column with more than BT targets falls
 // back to 1-row single-list chunks.
+// Hybrid (brick = T > 1: the 384-target build at n = 1): the unit is the quad, but a quad
+// whose non-empty cells hold >= T targets on average is cut into row blocks, row by row --
+// the FP16 screen's column cap (6 lattice cells) leaves sparse 1-row blocks mostly empty,
+// while dense rows fill them and stage fewer rows per target than a brick.
 // Paired build (two targets per lane): a lane's two targets must come from the same list, so
 // the fluid targets of a block take an even number of slots (padded) -- a block fits when
 // pad2(fluid) + boundary <= BT.
