@@ -266,6 +266,15 @@ int sphb_cell_ranges_from_sorted(sphb_workspace_t* ws, const sphb_grid_t* grid,
  *              particle; drho is unused (may be NULL).  20 B per particle written by PI and
  *              16 B read by K7; sphb_forces_f64 widens it (exactly) to the FP64 layout. */
 
+/* The block list of the next sphb_interact (the interaction's work decomposition: k_blocks and
+ * the FP32 gather builds' candidate counter) built from the cell ranges on the workspace's own
+ * high-priority stream, forked from s -- call it after the ranges (sphb_sort_ranges) and
+ * before K3 (sphb_reorder), so it runs while K3 moves the rows.  The next sphb_interact with
+ * the same beg / end, grid window and build waits for it instead of building it (sphb_step
+ * does this internally).  Optional: without it sphb_interact builds the list itself. */
+int sphb_interact_plan(sphb_workspace_t* ws, const sphb_params_t* prm, const sphb_grid_t* grid,
+                       const int32_t* beg, const int32_t* end, sphb_ctrl_t* ctrl, sphb_stream_t s);
+
 /* K5/K5b/K6 -- GatherEngine.compute (engines/gather.py:42-110): fused fluid pass
  * (gather_fluid_cells / _ranges, kernels.py:326-497) and boundary pass (gather_boundary_*,
  * kernels.py:500-596), plus the compute_dt reductions (sim.py:215-232) in the epilogue.

@@ -97,6 +97,7 @@ def lib():
         "sphb_workspace_destroy": ([P], c_i32),
         "sphb_workspace_reset": ([P, P], c_i32),
         "sphb_workspace_clear_hist": ([P, P], c_i32),
+        "sphb_interact_plan": ([P, P, P, P, P, P, P], c_i32),
         "sphb_workspace_trust_order": ([P, P], c_i32),
         "sphb_workspace_bytes": ([P], c_i64),
         "sphb_workspace_set_mover_cap": ([P, c_i64], c_i32),
@@ -155,7 +156,7 @@ EXPORTED = ("sphb_last_error", "sphb_version", "sphb_workspace_create", "sphb_wo
             "sphb_workspace_set_mover_cap", "sphb_workspace_sort_info", "sphb_workspace_set_pi_block", "sphb_workspace_set_pi_kernel", "sphb_ctrl_init", "sphb_cell_keys",
             "sphb_sort", "sphb_sort_ranges", "sphb_nl_build", "sphb_reorder", "sphb_cell_ranges",
             "sphb_cell_ranges_from_sorted", "sphb_cell_hist",
-            "sphb_interact", "sphb_step_begin", "sphb_integrate", "sphb_step_end", "sphb_step",
+            "sphb_interact", "sphb_interact_plan", "sphb_step_begin", "sphb_integrate", "sphb_step_end", "sphb_step",
             "sphb_step_launch_count", "sphb_integrate_stage", "sphb_energy", "sphb_slab_tiles",
             "sphb_slab_count", "sphb_slab_scatter", "sphb_slab_unpack", "sphb_band_scratch_words",
             "sphb_band_count", "sphb_band_pack", "sphb_band_integrate", "sphb_slab_tail",

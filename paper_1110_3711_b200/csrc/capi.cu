@@ -106,6 +106,43 @@ int launch_interact(sphb_workspace* ws, const sphb_params_t& p, const sphb_grid_
   return launch_sym_counters(ws, g, beg, end, ctrl, s);
 }
 
+static int plan_dispatch(sphb_workspace* ws, const sphb_params_t& p, const sphb_grid_t& g,
+                         const int32_t* beg, const int32_t* end, sphb_ctrl_t* ctrl, cudaStream_t s) {
+  const bool f32 = p.precision == SPHB_FP32;  // the same build choice as launch_interact
+  if (ws->pi_kernel == SPHB_PI_PAIRED && f32) return pi512p::plan_interact(ws, p, g, beg, end, ctrl, s);
+  if (ws->pi_kernel == SPHB_PI_SYMMETRIC && f32 && p.order == 0)
+    return pi384s::plan_interact(ws, p, g, beg, end, ctrl, s);
+  if (ws->pi_block == 256 && f32) return pi256::plan_interact(ws, p, g, beg, end, ctrl, s);
+  if (ws->pi_block == 512 && f32) return pi512::plan_interact(ws, p, g, beg, end, ctrl, s);
+  if (ws->pi_block == PI_LARGE_BLOCK && f32) return pi384::plan_interact(ws, p, g, beg, end, ctrl, s);
+  return pi128::plan_interact(ws, p, g, beg, end, ctrl, s);
+}
+
+int plan_interact_async(sphb_workspace* ws, const sphb_params_t& p, const sphb_grid_t& g,
+                        const int32_t* beg, const int32_t* end, sphb_ctrl_t* ctrl, cudaStream_t s) {
+  ws->plan.valid = false;
+  if (cudaError_t e = cudaEventRecord(ws->ev_fork, s))
+    return sphb_set_error(SPHB_E_CUDA, "plan fork: %s", cudaGetErrorString(e));
+  if (cudaError_t e = cudaStreamWaitEvent(ws->side, ws->ev_fork, 0))
+    return sphb_set_error(SPHB_E_CUDA, "plan fork: %s", cudaGetErrorString(e));
+  if (int rc = plan_dispatch(ws, p, g, beg, end, ctrl, ws->side)) return rc;
+  if (cudaError_t e = cudaEventRecord(ws->ev_plan, ws->side))
+    return sphb_set_error(SPHB_E_CUDA, "plan join: %s", cudaGetErrorString(e));
+  sphb_workspace::Plan& pl = ws->plan;
+  pl.beg = beg;
+  pl.end = end;
+  for (int k = 0; k < 3; ++k) pl.dims[k] = g.dims[k];
+  pl.tx0 = g.tx0;
+  pl.tx1 = g.tx1;
+  pl.reach = g.reach;
+  pl.precision = p.precision;
+  pl.order = p.order;
+  pl.pi_block = ws->pi_block;
+  pl.pi_kernel = ws->pi_kernel;
+  pl.valid = true;
+  return SPHB_OK;
+}
+
 int64_t interact_launch_count(int64_t n) { return pi128::interact_launch_count(n); }
 
 extern "C" {
@@ -164,6 +201,13 @@ int sphb_workspace_create(int64_t n_max, int64_t ncells_max, sphb_workspace_t** 
     if (e == cudaSuccess) e = cudaMemset(ws->mv_head, 0xff, sizeof(int32_t) * (2 * ncells_max + 1));
   }
   if (e == cudaSuccess) e = cudaMemset(ws->cnt, 0, sizeof(uint32_t) * (2 * ncells_max + 1));
+  if (e == cudaSuccess) {  // the interaction plan's side stream (highest priority) and events
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    e = cudaStreamCreateWithPriority(&ws->side, cudaStreamNonBlocking, hi);
+  }
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ws->ev_fork, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ws->ev_plan, cudaEventDisableTiming);
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
   ws->bytes = bytes;
   if (e != cudaSuccess) {
@@ -188,6 +232,9 @@ int sphb_workspace_destroy(sphb_workspace_t* ws) {
   cudaFree(ws->scan_partials);
   cudaFree(ws->blocks);
   cudaFree(ws->energy_part);
+  if (ws->side) cudaStreamDestroy(ws->side);
+  if (ws->ev_fork) cudaEventDestroy(ws->ev_fork);
+  if (ws->ev_plan) cudaEventDestroy(ws->ev_plan);
   for (void* p : {(void*)ws->mv_state, (void*)ws->mv_bits, (void*)ws->mv_wpre, (void*)ws->mv_tile,
                   (void*)ws->mv_pos, (void*)ws->mv_next, (void*)ws->mv_head, (void*)ws->mv_kv})
     cudaFree(p);
@@ -379,6 +426,17 @@ int sphb_cell_ranges_from_sorted(sphb_workspace_t* ws, const sphb_grid_t* grid,
   return launch_cell_ranges(ws, *grid, beg, end, nullptr, (cudaStream_t)s);
 }
 
+int sphb_interact_plan(sphb_workspace_t* ws, const sphb_params_t* prm, const sphb_grid_t* grid,
+                       const int32_t* beg, const int32_t* end, sphb_ctrl_t* ctrl, sphb_stream_t s) {
+  SPHB_NONNULL(ws);
+  if (int rc = check_params(prm)) return rc;
+  SPHB_NONNULL(ctrl);
+  if (int rc = check_grid(grid)) return rc;
+  SPHB_NONNULL(beg);
+  SPHB_NONNULL(end);
+  return plan_interact_async(ws, *prm, *grid, beg, end, ctrl, (cudaStream_t)s);
+}
+
 int sphb_interact(sphb_workspace_t* ws, const sphb_params_t* prm, const sphb_grid_t* grid,
                   int64_t n, int64_t nb,
                   const void* posp, const void* velr, const void* aux, const int32_t* cell_sorted,
@@ -494,6 +552,8 @@ static int stage_pass(sphb_workspace_t* ws, const sphb_params_t* prm, const sphb
     if ((rc = launch_sort_and_ranges(ws, *grid, st->keys, n, st->keys_sorted, st->perm, st->beg,
                                      st->end, ctrl, cs)))
       return rc;
+    // the interaction's block list on the side stream, concurrently with K3
+    if ((rc = plan_interact_async(ws, *prm, *grid, st->beg, st->end, ctrl, cs))) return rc;
     if ((rc = launch_reorder(*prm, *grid, n, st->perm, st->keys_sorted, (const float4*)st->posp,
                              (const float4*)st->velr, (const float4*)st->prev, st->id,
                              (float4*)st->posp_s, (float4*)st->velr_s, (float4*)st->prev_s, st->id_s,

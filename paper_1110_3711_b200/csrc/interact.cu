@@ -2358,11 +2358,77 @@ static int launch_wall(const sphb_params_t& p, const sphb_grid_t& g, int64_t n, 
   return sphb_check_launch("k_wall_force");
 }
 
+// The interaction's block list: k_blocks (count, scan, write) and the FP32 gather builds'
+// candidate counter, on stream s (sphb_step / sphb_interact_plan run it on the workspace's
+// side stream, concurrently with K3).
+int plan_interact(sphb_workspace* ws, const sphb_params_t& p, const sphb_grid_t& g,
+                  const int32_t* beg, const int32_t* end, sphb_ctrl_t* ctrl, cudaStream_t s) {
+  if (g.reach < 1 || g.reach > 3) return sphb_set_error(SPHB_E_INVALID, "reach must be 1..3");
+  const int64_t ncells = ncells_of(g);
+  const int64_t nrows = (int64_t)g.dims[1] * g.dims[2];
+  // one warp per cell row (rows ~10^4): every SM busy, the row's ends staged in shared memory
+  int gb = (int)(nrows < 148 * 32 ? nrows : 148 * 32);
+  if (gb < 1) gb = 1;
+  const size_t sm_blocks = sizeof(int32_t) * 2 * (size_t)(g.tx1 - g.tx0);
+  if (sm_blocks > 48 * 1024) return sphb_set_error(SPHB_E_INVALID, "more than 6144 cell columns per slab");
+  // bricks for h/2 cells (reach 2) in the FP32 gather kernel's cell order
+  // (the 512-target build cuts bricks at every reach: 2 x 2 rows x 2 lattice cells at n = 1)
+  // hybrid at n = 1 (the row-block gather builds): 2 x 2-row quads whose cells hold fewer than
+  // HYBRID_T targets on average become bricks, the others row blocks (k_blocks)
+  const bool brickable = p.order == 0 && p.precision == SPHB_FP32 && !V8_SYM;
+  static const char* hyb_env = getenv("SPHB_HYBRID_T");  // A/B experiments only (0 = rows)
+  // (measured, profiles/r02bu_hybrid_blocking_ab.txt: 384-target blocks collapsed 16.01 ->
+  // 15.79 ms at T = 32, at rest neutral; the 256-target build loses at rest, so rows only)
+  const int hyb_t = hyb_env ? atoi(hyb_env) : (BT == PI_LARGE_BLOCK ? HYBRID_T : 0);
+  const int brick = !brickable ? 0
+                    : (g.reach == 2 || BT == 512 || SPHB_PAIR) ? 1
+                    : (hyb_t > 1 ? hyb_t : 0);
+  const int64_t nunits = brick ? (int64_t)((g.dims[1] + 1) / 2) * ((g.dims[2] + 1) / 2) : nrows;
+  // block x extent: columns [cxa - r, cxb + r] must stay within the FP16 screen's +-4 (2h)
+  // around the block centre (use16 in the kernels), span <= 16 / (cell_size / h) columns
+  int maxc = INT_MAX;
+  if (p.precision == SPHB_FP32) {
+    const int span = (int)floor(16.0 / (g.cell_size * p.invh) + 1e-9);
+    maxc = span - 2 * g.reach > 1 ? span - 2 * g.reach : 1;
+  }
+  static const char* maxc_env = getenv("SPHB_BLOCK_MAXC");  // A/B experiments only
+  if (maxc_env && atoi(maxc_env) > 0) maxc = atoi(maxc_env);
+  k_blocks<true><<<gb, 32, sm_blocks, s>>>(g, ncells, beg, end, ws->row_off, ws->blocks, ctrl, brick, maxc);
+  if (int rc = sphb_check_launch("k_blocks count")) return rc;
+  k_blocks_scan<<<1, KB_SCAN, 0, s>>>(ws->row_off, nunits, ctrl);
+  if (int rc = sphb_check_launch("k_blocks_scan")) return rc;
+  k_blocks<false><<<gb, 32, sm_blocks, s>>>(g, ncells, beg, end, ws->row_off, ws->blocks, ctrl, brick, maxc);
+  if (int rc = sphb_check_launch("k_blocks")) return rc;
+  if (p.precision == SPHB_FP32 && !V8_SYM) {  // the FP32 gather kernels' candidate counter
+    const int64_t ncand = (int64_t)(g.tx1 - g.tx0) * g.dims[1] * g.dims[2];
+    const unsigned kc = (unsigned)std::max<int64_t>(1, std::min<int64_t>((ncand + KC_THREADS - 1) / KC_THREADS, 148 * 8));
+    k_cand_cells<<<kc, KC_THREADS, 0, s>>>(g, ncells, beg, end, ctrl);
+    if (int rc = sphb_check_launch("k_cand_cells")) return rc;
+  }
+  return SPHB_OK;
+}
+
 int launch_interact(sphb_workspace* ws, const sphb_params_t& p, const sphb_grid_t& g, int64_t n,
                     int64_t nb, const float4* posp, const float4* velr, const float4* aux,
                     const int32_t* cell_sorted, const int32_t* beg, const int32_t* end,
                     void* acc, void* drho, void* visc, sphb_ctrl_t* ctrl, cudaStream_t s) {
   if (g.reach < 1 || g.reach > 3) return sphb_set_error(SPHB_E_INVALID, "reach must be 1..3");
+  // the block list: built on the side stream during K3 when this call's tables, window and
+  // build match the pending plan, else here
+  // (a pending plan that does not match is still waited for: it writes the same buffers)
+  const sphb_workspace::Plan& pl = ws->plan;
+  const bool pending = pl.valid;
+  const bool match = pending && pl.beg == beg && pl.end == end && pl.dims[0] == g.dims[0] &&
+                     pl.dims[1] == g.dims[1] && pl.dims[2] == g.dims[2] && pl.tx0 == g.tx0 &&
+                     pl.tx1 == g.tx1 && pl.reach == g.reach && pl.precision == p.precision &&
+                     pl.order == p.order && pl.pi_block == ws->pi_block &&
+                     pl.pi_kernel == ws->pi_kernel;
+  ws->plan.valid = false;
+  if (pending)
+    if (cudaError_t e = cudaStreamWaitEvent(s, ws->ev_plan, 0))
+      return sphb_set_error(SPHB_E_CUDA, "plan wait: %s", cudaGetErrorString(e));
+  if (!match)
+    if (int rc = plan_interact(ws, p, g, beg, end, ctrl, s)) return rc;
   static int nsm = 0;
   if (nsm == 0) {
     int dev = 0;
@@ -2403,50 +2469,10 @@ int launch_interact(sphb_workspace* ws, const sphb_params_t& p, const sphb_grid_
   a.cs_exp = (float)((p.gamma - 1.0) * 0.5);
   a.k_cs = a.gamma7 ? (float)(cbrt(p.c0) / p.rho0)
                     : (float)(p.c0 * pow(p.rho0, -(p.gamma - 1.0) * 0.5));
-  const int64_t nrows = (int64_t)g.dims[1] * g.dims[2];
-  // one warp per cell row (rows ~10^4): every SM busy, the row's ends staged in shared memory
-  int gb = (int)(nrows < 148 * 32 ? nrows : 148 * 32);
-  if (gb < 1) gb = 1;
-  const size_t sm_blocks = sizeof(int32_t) * 2 * (size_t)(g.tx1 - g.tx0);
-  if (sm_blocks > 48 * 1024) return sphb_set_error(SPHB_E_INVALID, "more than 6144 cell columns per slab");
-  // bricks for h/2 cells (reach 2) in the FP32 gather kernel's cell order
-  // (the 512-target build cuts bricks at every reach: 2 x 2 rows x 2 lattice cells at n = 1)
-  // hybrid at n = 1 (the row-block gather builds): 2 x 2-row quads whose cells hold fewer than
-  // HYBRID_T targets on average become bricks, the others row blocks (k_blocks)
-  const bool brickable = p.order == 0 && p.precision == SPHB_FP32 && !V8_SYM;
-  static const char* hyb_env = getenv("SPHB_HYBRID_T");  // A/B experiments only (0 = rows)
-  // (measured, profiles/r02bu_hybrid_blocking_ab.txt: 384-target blocks collapsed 16.01 ->
-  // 15.79 ms at T = 32, at rest neutral; the 256-target build loses at rest, so rows only)
-  const int hyb_t = hyb_env ? atoi(hyb_env) : (BT == PI_LARGE_BLOCK ? HYBRID_T : 0);
-  const int brick = !brickable ? 0
-                    : (g.reach == 2 || BT == 512 || SPHB_PAIR) ? 1
-                    : (hyb_t > 1 ? hyb_t : 0);
-  const int64_t nunits = brick ? (int64_t)((g.dims[1] + 1) / 2) * ((g.dims[2] + 1) / 2) : nrows;
-  // block x extent: columns [cxa - r, cxb + r] must stay within the FP16 screen's +-4 (2h)
-  // around the block centre (use16 in the kernels), span <= 16 / (cell_size / h) columns
-  int maxc = INT_MAX;
-  if (p.precision == SPHB_FP32) {
-    const int span = (int)floor(16.0 / (g.cell_size * p.invh) + 1e-9);
-    maxc = span - 2 * g.reach > 1 ? span - 2 * g.reach : 1;
-  }
-  static const char* maxc_env = getenv("SPHB_BLOCK_MAXC");  // A/B experiments only
-  if (maxc_env && atoi(maxc_env) > 0) maxc = atoi(maxc_env);
-  k_blocks<true><<<gb, 32, sm_blocks, s>>>(g, a.ncells, beg, end, ws->row_off, ws->blocks, ctrl, brick, maxc);
-  if (int rc = sphb_check_launch("k_blocks count")) return rc;
-  k_blocks_scan<<<1, KB_SCAN, 0, s>>>(ws->row_off, nunits, ctrl);
-  if (int rc = sphb_check_launch("k_blocks_scan")) return rc;
-  k_blocks<false><<<gb, 32, sm_blocks, s>>>(g, a.ncells, beg, end, ws->row_off, ws->blocks, ctrl, brick, maxc);
-  if (int rc = sphb_check_launch("k_blocks")) return rc;
   // one launch for both item classes: fluid targets (F-F + F-B) and boundary targets (B-F,
   // drho + visc only) of the same cells share the staged candidates
   a.blocks = ws->blocks;
   const bool sym = V8_SYM && p.precision == SPHB_FP32;
-  if (p.precision == SPHB_FP32 && !sym) {  // the FP32 gather kernels' candidate counter
-    const int64_t ncand = (int64_t)(g.tx1 - g.tx0) * g.dims[1] * g.dims[2];
-    const unsigned kc = (unsigned)std::max<int64_t>(1, std::min<int64_t>((ncand + KC_THREADS - 1) / KC_THREADS, 148 * 8));
-    k_cand_cells<<<kc, KC_THREADS, 0, s>>>(g, a.ncells, beg, end, ctrl);
-    if (int rc = sphb_check_launch("k_cand_cells")) return rc;
-  }
   if (sym) {  // every block adds into these (targets' own sums and their partners' reactions)
     cudaMemsetAsync(acc, 0, sizeof(float4) * (size_t)n, s);
     cudaMemsetAsync(visc, 0, sizeof(float) * (size_t)n, s);

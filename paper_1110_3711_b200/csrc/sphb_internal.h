@@ -44,6 +44,18 @@ struct sphb_workspace {
   int32_t pi_kernel = 0;   // SPHB_PI_GATHER | SPHB_PI_SYMMETRIC (pi384s) | SPHB_PI_PAIRED (pi512p)
   unsigned long long* sym_scratch = nullptr;  // half-stencil candidate count (SPHB_COUNTERS_SYMMETRIC)
   size_t bytes = 0;
+  // the interaction's block list built on a side stream while K3 reorders (sphb_interact_plan,
+  // sphb_step): the next sphb_interact with the same tables and window waits on ev_plan
+  // instead of building it again
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_plan = nullptr;
+  struct Plan {
+    bool valid = false;
+    const int32_t* beg = nullptr;
+    const int32_t* end = nullptr;
+    int32_t dims[3] = {0, 0, 0}, tx0 = 0, tx1 = 0, reach = 0, precision = 0, order = 0;
+    int32_t pi_block = 0, pi_kernel = 0;
+  } plan;
 };
 
 // nl.cu
@@ -76,6 +88,8 @@ int64_t nl_launch_count(const sphb_grid_t& g, int64_t n);
 constexpr int PI_LARGE_BLOCK = 384;
 #define SPHB_DECLARE_PI(NS)                                                                     \
   namespace NS {                                                                                \
+  int plan_interact(sphb_workspace* ws, const sphb_params_t& p, const sphb_grid_t& g,         \
+                    const int32_t* beg, const int32_t* end, sphb_ctrl_t* ctrl, cudaStream_t s); \
   int launch_interact(sphb_workspace* ws, const sphb_params_t& p, const sphb_grid_t& g,       \
                       int64_t n, int64_t nb, const float4* posp, const float4* velr,           \
                       const float4* aux, const int32_t* cell_sorted, const int32_t* beg,       \
@@ -96,6 +110,10 @@ int launch_interact(sphb_workspace* ws, const sphb_params_t& p, const sphb_grid_
                     void* acc, void* drho, void* visc, sphb_ctrl_t* ctrl, cudaStream_t s);
 int64_t interact_launch_count(int64_t n);
 
+// the block list of the next interaction (k_blocks, its scan, k_cand_cells) on the workspace's
+// side stream, forked from s after the cell ranges (capi.cu)
+int plan_interact_async(sphb_workspace* ws, const sphb_params_t& p, const sphb_grid_t& g,
+                        const int32_t* beg, const int32_t* end, sphb_ctrl_t* ctrl, cudaStream_t s);
 // stepfn.cu: StepStats of the symmetric traversal (SPHB_COUNTERS_SYMMETRIC) from the gather-type
 // counters of either kernel
 int launch_sym_counters(sphb_workspace* ws, const sphb_grid_t& g, const int32_t* beg,

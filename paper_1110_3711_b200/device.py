@@ -320,6 +320,9 @@ class DeviceSim:
         _lib.check(L.sphb_sort_ranges(ws, g, _ptr(self.keys), n, _ptr(self.keys_sorted),
                                       _ptr(self.perm), _ptr(self.beg), _ptr(self.end),
                                       _ptr(self.ctrl), s), "sphb_sort_ranges")
+        # the interaction's block list on the workspace's side stream while K3 runs
+        _lib.check(L.sphb_interact_plan(ws, p, g, _ptr(self.beg), _ptr(self.end), _ptr(self.ctrl), s),
+                   "sphb_interact_plan")
         _lib.check(L.sphb_reorder(p, g, n, _ptr(self.perm), _ptr(self.keys_sorted), _ptr(self.posp),
                                   _ptr(self.velr), _ptr(self.prev), _ptr(self.id), _ptr(self.posp_s),
                                   _ptr(self.velr_s), _ptr(self.prev_s), _ptr(self.id_s),
