@@ -877,7 +877,7 @@ def main():
                                "frac": nlsu_gbs / hbm, "traffic": None,
                                "work": f"{BYTES_NL_SU} B/particle-step over NL+SU stages",
                                "note": "the NL stage also hosts the interaction's block planning "
-                                       "(k_blocks, k_cand_cells) on a side stream, concurrent "
+                                       "(k_blocks with the candidate counter) on a side stream, concurrent "
                                        "with K3 (sphb_interact_plan)",
                                "peak_source": hbm_src},
         "roofline_composite": composite_roofline(system.n, cand, evals, hbm, fp32, ms_step),

@@ -106,6 +106,7 @@ int launch_interact(sphb_workspace* ws, const sphb_params_t& p, const sphb_grid_
   return launch_sym_counters(ws, g, beg, end, ctrl, s);
 }
 
+constexpr int64_t PLAN_ASYNC_MIN_ROWS = 1 << 19;
 static int plan_dispatch(sphb_workspace* ws, const sphb_params_t& p, const sphb_grid_t& g,
                          const int32_t* beg, const int32_t* end, sphb_ctrl_t* ctrl, cudaStream_t s) {
   const bool f32 = p.precision == SPHB_FP32;  // the same build choice as launch_interact
@@ -121,6 +122,9 @@ static int plan_dispatch(sphb_workspace* ws, const sphb_params_t& p, const sphb_
 int plan_interact_async(sphb_workspace* ws, const sphb_params_t& p, const sphb_grid_t& g,
                         const int32_t* beg, const int32_t* end, sphb_ctrl_t* ctrl, cudaStream_t s) {
   ws->plan.valid = false;
+  // small systems (launch-bound, CUDA graphs): K3 takes a few microseconds, the side branch
+  // would only add its fork / join -- sphb_interact builds the list in line
+  if (ws->n_max < PLAN_ASYNC_MIN_ROWS) return SPHB_OK;
   if (cudaError_t e = cudaEventRecord(ws->ev_fork, s))
     return sphb_set_error(SPHB_E_CUDA, "plan fork: %s", cudaGetErrorString(e));
   if (cudaError_t e = cudaStreamWaitEvent(ws->side, ws->ev_fork, 0))

@@ -521,21 +521,86 @@ __device__ __forceinline__ bool screen(const KArgs& a, const C32&, const Own<dou
 __device__ __forceinline__ int block_slots(int nf, int ntot) {
   return SPHB_PAIR ? ntot + (nf & 1) : ntot;
 }
+// candidate_pairs of the gather traversal (kernels.py:355-371, counted before the distance
+// test) depends on the cell tables alone: a fluid target of cell c visits every particle of
+// both lists in its stencil rows' x ranges [max(x - r, 0), min(x + r, nx - 1)] except itself, a
+// boundary target the fluid ones, so  cand = sum_c nf_c (F_c + B_c - 1) + nb_c F_c.  k_blocks'
+// count pass sums it per cell (its lanes walk the cells anyway); the FP32 gather kernels then
+// carry no per-target counting (its global loads sat on every block's setup path).
+__device__ __forceinline__ unsigned long long cell_cand(const sphb_grid_t& g, int64_t ncells,
+                                                        const int32_t* __restrict__ beg,
+                                                        const int32_t* __restrict__ end, int x,
+                                                        int y, int z, int nf, int nb) {
+  if (nf <= 0 && nb <= 0) return 0ull;
+  const int nx = g.dims[0], ny = g.dims[1], nz = g.dims[2], R = g.reach;
+  const int xlo = max(x - R, 0), xhi = min(x + R, nx - 1);
+  long long F = 0, B = 0;
+  for (int zz = max(z - R, 0); zz <= min(z + R, nz - 1); ++zz)
+    for (int yy = max(y - R, 0); yy <= min(y + R, ny - 1); ++yy) {
+      const int64_t rb = (int64_t)nx * (yy + (int64_t)ny * zz), rf = ncells + rb;
+      F += end[rf + xhi] - beg[rf + xlo];
+      B += end[rb + xhi] - beg[rb + xlo];
+    }
+  return (unsigned long long)((long long)max(nf, 0) * (F + B - 1) + (long long)max(nb, 0) * F);
+}
+__device__ __forceinline__ void add_cand(sphb_ctrl_t* ctrl, unsigned long long c) {
+  c = warp_sum_u64(c);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd((unsigned long long*)&ctrl->counters[0], c);
+}
+
+// Reach >= 2 (h/2 cells: 25 stencil rows per cell) the count pass's lanes would walk too many
+// rows each: one thread per target cell of the window instead (x fastest: coalesced table
+// loads, empty cells leave after two loads), on the same side stream.
+constexpr int KC_THREADS = 256;
+__global__ void __launch_bounds__(KC_THREADS) k_cand_cells(sphb_grid_t g, int64_t ncells,
+                                                          const int32_t* __restrict__ beg,
+                                                          const int32_t* __restrict__ end,
+                                                          sphb_ctrl_t* ctrl) {
+  if (!step_live(ctrl)) return;
+  const int ny = g.dims[1], nx = g.dims[0];
+  const int span = g.tx1 - g.tx0;
+  const int64_t total = (int64_t)span * ny * g.dims[2];
+  unsigned long long acc = 0;
+  for (int64_t t = (int64_t)blockIdx.x * KC_THREADS + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * KC_THREADS) {
+    const int64_t row = t / span;
+    const int x = g.tx0 + (int)(t - row * span);
+    const int64_t cb = (int64_t)nx * row + x, cf = ncells + cb;
+    acc += cell_cand(g, ncells, beg, end, x, (int)(row % ny), (int)(row / ny), end[cf] - beg[cf],
+                     end[cb] - beg[cb]);
+  }
+  __shared__ unsigned long long s_acc[KC_THREADS / 32];
+  acc = warp_sum_u64(acc);
+  if ((threadIdx.x & 31) == 0) s_acc[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    acc = threadIdx.x < KC_THREADS / 32 ? s_acc[threadIdx.x] : 0ull;
+    acc = warp_sum_u64(acc);
+    if (threadIdx.x == 0 && acc) atomicAdd((unsigned long long*)&ctrl->counters[0], acc);
+  }
+}
+
 // Row blocks of one cell row r (records written at out when !COUNT); the record count, on
 // every lane.  s_ends: [span] fluid ends, then [span] boundary ends of the row.
 template <bool COUNT>
 __device__ int row_records(const sphb_grid_t& g, int64_t ncells, const int32_t* __restrict__ beg,
                            const int32_t* __restrict__ end, int64_t r, int4* out, int maxc,
-                           int32_t* s_ends, int lane) {
+                           int32_t* s_ends, int lane, sphb_ctrl_t* cand_ctrl) {
   const int nx = g.dims[0], span = g.tx1 - g.tx0;
   const int64_t cb = r * nx, cf = ncells + r * nx;  // row offsets in the B / F tables
   if (span <= 0 ||
       (end[cf + g.tx1 - 1] <= beg[cf + g.tx0] && end[cb + g.tx1 - 1] <= beg[cb + g.tx0]))
     return 0;
+  unsigned long long cand = 0;
   for (int k = lane; k < span; k += 32) {
-    s_ends[k] = end[cf + g.tx0 + k];
-    s_ends[span + k] = end[cb + g.tx0 + k];
+    const int32_t fe = end[cf + g.tx0 + k], be = end[cb + g.tx0 + k];
+    s_ends[k] = fe;
+    s_ends[span + k] = be;
+    if (COUNT && cand_ctrl)
+      cand += cell_cand(g, ncells, beg, end, g.tx0 + k, (int)(r % g.dims[1]), (int)(r / g.dims[1]),
+                        fe - beg[cf + g.tx0 + k], be - beg[cb + g.tx0 + k]);
   }
+  if (COUNT && cand_ctrl) add_cand(cand_ctrl, cand);
   __syncwarp();
   int nrec = 0;
   if (lane == 0) {
@@ -585,7 +650,9 @@ __global__ void __launch_bounds__(32) k_blocks(sphb_grid_t g, int64_t ncells,
                                                const int32_t* __restrict__ end,
                                                int32_t* __restrict__ row_off,
                                                int4* __restrict__ blk, sphb_ctrl_t* ctrl,
-                                               int brick, int maxc) {
+                                               int brick, int maxc, bool count_cand) {
+  // count pass of the FP32 gather builds: also the candidate counter (cell_cand)
+  sphb_ctrl_t* const cand_ctrl = (COUNT && count_cand) ? ctrl : nullptr;
   // one warp per cell row: the lanes stage the row's cumulative ends (both lists) in shared
   // memory, lane 0 makes the greedy cut
   extern __shared__ int32_t s_ends[];  // [span] fluid ends, then [span] boundary ends
@@ -599,6 +666,7 @@ __global__ void __launch_bounds__(32) k_blocks(sphb_grid_t g, int64_t ncells,
       const int y0 = 2 * (int)(r % nyb), z0 = 2 * (int)(r / nyb);
       int tot_all = 0;
       int ne = 0;  // non-empty cells of the four rows (hybrid blocking)
+      unsigned long long cand = 0;
       for (int k = lane; k < span; k += 32) {  // targets of the brick's cell column x
         const int x = g.tx0 + k;
         int c = 0, cf = 0;
@@ -606,10 +674,11 @@ __global__ void __launch_bounds__(32) k_blocks(sphb_grid_t g, int64_t ncells,
           const int yy = y0 + (sub & 1), zz = z0 + (sub >> 1);
           if (yy >= ny || zz >= nz) continue;
           const int64_t rb = (int64_t)nx * (yy + (int64_t)ny * zz) + x, rf = ncells + rb;
-          const int nfc = end[rf] - beg[rf], call = nfc + (end[rb] - beg[rb]);
+          const int nfc = end[rf] - beg[rf], nbc = end[rb] - beg[rb], call = nfc + nbc;
           cf += nfc;
           c += call;
           ne += call > 0 ? 1 : 0;
+          if (cand_ctrl) cand += cell_cand(g, ncells, beg, end, x, yy, zz, nfc, nbc);
         }
         s_ends[k] = c;
         s_ends[span + k] = cf;  // fluid part (the paired build's slot padding)
@@ -617,6 +686,7 @@ __global__ void __launch_bounds__(32) k_blocks(sphb_grid_t g, int64_t ncells,
       }
       tot_all = __reduce_add_sync(SPHB_FULL, tot_all);
       ne = __reduce_add_sync(SPHB_FULL, ne);
+      if (cand_ctrl) add_cand(cand_ctrl, cand);
       __syncwarp();
       if (tot_all == 0) {
         if (COUNT && lane == 0) row_off[r] = 0;
@@ -632,7 +702,7 @@ __global__ void __launch_bounds__(32) k_blocks(sphb_grid_t g, int64_t ncells,
           if (yy >= ny || zz >= nz) continue;
           nrec += row_records<COUNT>(g, ncells, beg, end, (int64_t)yy + (int64_t)ny * zz,
                                      COUNT ? nullptr : blk + 2 * ((int64_t)row_off[r] + nrec), maxc,
-                                     s_ends, lane);
+                                     s_ends, lane, nullptr);
         }
         if (COUNT && lane == 0) row_off[r] = nrec;
         continue;
@@ -691,7 +761,7 @@ __global__ void __launch_bounds__(32) k_blocks(sphb_grid_t g, int64_t ncells,
   for (int64_t r = blockIdx.x; r < nrows; r += gridDim.x) {
     const int nrec = row_records<COUNT>(g, ncells, beg, end, r,
                                         COUNT ? nullptr : blk + 2 * (int64_t)row_off[r], maxc,
-                                        s_ends, lane);
+                                        s_ends, lane, cand_ctrl);
     if (COUNT && lane == 0) row_off[r] = nrec;
   }
 }
@@ -738,53 +808,6 @@ __global__ void __launch_bounds__(KB_SCAN) k_blocks_scan(int32_t* row_off, int64
   if (tid == 0) {
     ctrl->nblk[0] = (uint32_t)s_carry;
     ctrl->tile_next[0] = 0u;  // this launch's block queue (several launches per step: X slabs)
-  }
-}
-
-// ------------------------------------------------------------------ candidate counter
-// candidate_pairs of the gather traversal (kernels.py:355-371, counted before the distance
-// test) depends on the cell tables alone: a fluid target of cell c visits every particle of
-// both lists in its stencil rows' x ranges [max(x - r, 0), min(x + r, nx - 1)] except itself, a
-// boundary target the fluid ones, so  cand = sum_c nf_c (F_c + B_c - 1) + nb_c F_c.  One thread
-// per target cell of the window (x fastest: coalesced table loads, empty cells leave after two
-// loads); the FP32 gather kernels then carry no per-target counting (its global loads sat on
-// every block's setup path).
-constexpr int KC_THREADS = 256;
-__global__ void __launch_bounds__(KC_THREADS) k_cand_cells(sphb_grid_t g, int64_t ncells,
-                                                          const int32_t* __restrict__ beg,
-                                                          const int32_t* __restrict__ end,
-                                                          sphb_ctrl_t* ctrl) {
-  if (!step_live(ctrl)) return;
-  const int nx = g.dims[0], ny = g.dims[1], nz = g.dims[2], R = g.reach;
-  const int span = g.tx1 - g.tx0;
-  const int64_t total = (int64_t)span * ny * nz;
-  unsigned long long acc = 0;
-  for (int64_t t = (int64_t)blockIdx.x * KC_THREADS + threadIdx.x; t < total;
-       t += (int64_t)gridDim.x * KC_THREADS) {
-    const int64_t row = t / span;
-    const int x = g.tx0 + (int)(t - row * span);
-    const int64_t cb = (int64_t)nx * row + x, cf = ncells + cb;
-    const int nb = end[cb] - beg[cb], nf = end[cf] - beg[cf];
-    if (nb <= 0 && nf <= 0) continue;
-    const int y = (int)(row % ny), z = (int)(row / ny);
-    const int xlo = max(x - R, 0), xhi = min(x + R, nx - 1);
-    long long F = 0, B = 0;
-    for (int zz = max(z - R, 0); zz <= min(z + R, nz - 1); ++zz)
-      for (int yy = max(y - R, 0); yy <= min(y + R, ny - 1); ++yy) {
-        const int64_t rb = (int64_t)nx * (yy + (int64_t)ny * zz), rf = ncells + rb;
-        F += end[rf + xhi] - beg[rf + xlo];
-        B += end[rb + xhi] - beg[rb + xlo];
-      }
-    acc += (unsigned long long)((long long)max(nf, 0) * (F + B - 1) + (long long)max(nb, 0) * F);
-  }
-  __shared__ unsigned long long s_acc[KC_THREADS / 32];
-  acc = warp_sum_u64(acc);
-  if ((threadIdx.x & 31) == 0) s_acc[threadIdx.x >> 5] = acc;
-  __syncthreads();
-  if (threadIdx.x < 32) {
-    acc = threadIdx.x < KC_THREADS / 32 ? s_acc[threadIdx.x] : 0ull;
-    acc = warp_sum_u64(acc);
-    if (threadIdx.x == 0 && acc) atomicAdd((unsigned long long*)&ctrl->counters[0], acc);
   }
 }
 
@@ -1758,7 +1781,7 @@ __global__ void __launch_bounds__(NW * 32, V8_MINB) k_interact_v8(KArgs a, K32 k
         }
       }
       if (isf) cand -= 1;
-    }  // (gather builds: counted from the cell tables, k_cand_cells)
+    }  // (gather builds: counted from the cell tables, k_blocks' count pass)
 
     // A / C fragments of the tensor-core screen: target row r = 16 m + g (+ 8) holds
     // K = (-2x, -2y, -2z, 1, 0, 0, 0, 0) and C = |x|^2 - thr of its FP16 block-centred position
@@ -2341,8 +2364,8 @@ namespace SPHB_PI_NS {
 
 int64_t interact_launch_count(int64_t n) {
   (void)n;
-  // k_blocks (count, scan, write), the interaction kernel; the FP32 gather builds add
-  // k_cand_cells, the symmetric one k_dt_f32 (counted by the callers: device.py, dslab.py)
+  // k_blocks (count, scan, write), the interaction kernel (the symmetric build adds k_dt_f32,
+  // the gather builds at reach >= 2 k_cand_cells: counted by the callers, device.py)
   return 4;
 }
 
@@ -2358,8 +2381,8 @@ static int launch_wall(const sphb_params_t& p, const sphb_grid_t& g, int64_t n, 
   return sphb_check_launch("k_wall_force");
 }
 
-// The interaction's block list: k_blocks (count, scan, write) and the FP32 gather builds'
-// candidate counter, on stream s (sphb_step / sphb_interact_plan run it on the workspace's
+// The interaction's block list: k_blocks (count -- with the FP32 gather builds' candidate
+// counter --, scan, write), on stream s (sphb_step / sphb_interact_plan run it on the workspace's
 // side stream, concurrently with K3).
 int plan_interact(sphb_workspace* ws, const sphb_params_t& p, const sphb_grid_t& g,
                   const int32_t* beg, const int32_t* end, sphb_ctrl_t* ctrl, cudaStream_t s) {
@@ -2379,7 +2402,10 @@ int plan_interact(sphb_workspace* ws, const sphb_params_t& p, const sphb_grid_t&
   static const char* hyb_env = getenv("SPHB_HYBRID_T");  // A/B experiments only (0 = rows)
   // (measured, profiles/r02bu_hybrid_blocking_ab.txt: 384-target blocks collapsed 16.01 ->
   // 15.79 ms at T = 32, at rest neutral; the 256-target build loses at rest, so rows only)
-  const int hyb_t = hyb_env ? atoi(hyb_env) : (BT == PI_LARGE_BLOCK ? HYBRID_T : 0);
+  // Small systems (fewer than ~8 blocks per SM) keep row blocks: fuller bricks mean fewer
+  // blocks than SMs there (C1: gather 384 PI 0.103 -> 0.117 ms with bricks)
+  const int hyb_t = hyb_env ? atoi(hyb_env)
+                            : ((BT == PI_LARGE_BLOCK && ws->n_max >= (int64_t)148 * 8 * BT) ? HYBRID_T : 0);
   const int brick = !brickable ? 0
                     : (g.reach == 2 || BT == 512 || SPHB_PAIR) ? 1
                     : (hyb_t > 1 ? hyb_t : 0);
@@ -2393,13 +2419,17 @@ int plan_interact(sphb_workspace* ws, const sphb_params_t& p, const sphb_grid_t&
   }
   static const char* maxc_env = getenv("SPHB_BLOCK_MAXC");  // A/B experiments only
   if (maxc_env && atoi(maxc_env) > 0) maxc = atoi(maxc_env);
-  k_blocks<true><<<gb, 32, sm_blocks, s>>>(g, ncells, beg, end, ws->row_off, ws->blocks, ctrl, brick, maxc);
+  // the FP32 gather builds' candidate counter rides on the count pass (reach 1), or takes its
+  // own kernel (reach >= 2)
+  const bool cand = p.precision == SPHB_FP32 && !V8_SYM;
+  const bool count_cand = cand && g.reach == 1;
+  k_blocks<true><<<gb, 32, sm_blocks, s>>>(g, ncells, beg, end, ws->row_off, ws->blocks, ctrl, brick, maxc, count_cand);
   if (int rc = sphb_check_launch("k_blocks count")) return rc;
   k_blocks_scan<<<1, KB_SCAN, 0, s>>>(ws->row_off, nunits, ctrl);
   if (int rc = sphb_check_launch("k_blocks_scan")) return rc;
-  k_blocks<false><<<gb, 32, sm_blocks, s>>>(g, ncells, beg, end, ws->row_off, ws->blocks, ctrl, brick, maxc);
+  k_blocks<false><<<gb, 32, sm_blocks, s>>>(g, ncells, beg, end, ws->row_off, ws->blocks, ctrl, brick, maxc, false);
   if (int rc = sphb_check_launch("k_blocks")) return rc;
-  if (p.precision == SPHB_FP32 && !V8_SYM) {  // the FP32 gather kernels' candidate counter
+  if (cand && !count_cand) {
     const int64_t ncand = (int64_t)(g.tx1 - g.tx0) * g.dims[1] * g.dims[2];
     const unsigned kc = (unsigned)std::max<int64_t>(1, std::min<int64_t>((ncand + KC_THREADS - 1) / KC_THREADS, 148 * 8));
     k_cand_cells<<<kc, KC_THREADS, 0, s>>>(g, ncells, beg, end, ctrl);

@@ -110,7 +110,7 @@ int launch_interact(sphb_workspace* ws, const sphb_params_t& p, const sphb_grid_
                     void* acc, void* drho, void* visc, sphb_ctrl_t* ctrl, cudaStream_t s);
 int64_t interact_launch_count(int64_t n);
 
-// the block list of the next interaction (k_blocks, its scan, k_cand_cells) on the workspace's
+// the block list of the next interaction (k_blocks with the candidate counter, its scan; k_cand_cells at reach 2) on the workspace's
 // side stream, forked from s after the cell ranges (capi.cu)
 int plan_interact_async(sphb_workspace* ws, const sphb_params_t& p, const sphb_grid_t& g,
                         const int32_t* beg, const int32_t* end, sphb_ctrl_t* ctrl, cudaStream_t s);

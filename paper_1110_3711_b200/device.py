@@ -397,7 +397,10 @@ class DeviceSim:
     def launches_per_step(self) -> int:
         k = int(_lib.lib().sphb_step_launch_count(_lib.ref(self.grid), self.n))
         if int(self.prm.precision) == _lib.SPHB_FP32:
-            k += 1  # symmetric: k_dt_f32 after the scatter; gather builds: k_cand_cells
+            if self.pi_kernel == "symmetric":
+                k += 1  # k_dt_f32 after the scatter
+            elif int(self.grid.reach) >= 2:
+                k += 1  # k_cand_cells (reach 1: the counter rides on k_blocks)
         if int(self.prm.counters) == _lib.SPHB_COUNTERS_SYMMETRIC:
             k += 2  # k_sym_cand, k_sym_final
         return k

@@ -929,10 +929,11 @@ class DeviceSlabSim:
         r = self.ranks[0]
         base = int(_lib.lib().sphb_step_launch_count(_lib.ref(r.grid), r.n))
         npi = len(r.edge_grids) + len(r.inner_grids)
-        # + band count (2); every interaction launch: k_blocks x 3, k_cand_cells and the kernel
-        # (the first one's four in base); pack, two band updates and the tail on a rank with
-        # neighbours
-        return base + 2 + npi + 4 * (npi - 1) + (4 if r.sides else 0)
+        # + band count (2); each further interaction launch: k_blocks x 3 + the kernel (+
+        # k_cand_cells per launch at reach >= 2); pack, two band updates and the tail on a rank
+        # with neighbours
+        cand = npi if int(r.grid.reach) >= 2 else 0
+        return base + 2 + cand + 4 * (npi - 1) + (4 if r.sides else 0)
 
 
 def estimate_steps_per_sync() -> int:
