@@ -271,7 +271,9 @@ int sphb_cell_ranges_from_sorted(sphb_workspace_t* ws, const sphb_grid_t* grid,
  * high-priority stream, forked from s -- call it after the ranges (sphb_sort_ranges) and
  * before K3 (sphb_reorder), so it runs while K3 moves the rows.  The next sphb_interact with
  * the same beg / end, grid window and build waits for it instead of building it (sphb_step
- * does this internally).  Optional: without it sphb_interact builds the list itself. */
+ * does this internally).  Optional: without it sphb_interact builds the list itself.  A plan
+ * belongs to the step's own sphb_interact (call them in pairs); sphb_workspace_reset drops a
+ * pending one. */
 int sphb_interact_plan(sphb_workspace_t* ws, const sphb_params_t* prm, const sphb_grid_t* grid,
                        const int32_t* beg, const int32_t* end, sphb_ctrl_t* ctrl, sphb_stream_t s);
 

@@ -110,13 +110,13 @@ constexpr int64_t PLAN_ASYNC_MIN_ROWS = 1 << 19;
 static int plan_dispatch(sphb_workspace* ws, const sphb_params_t& p, const sphb_grid_t& g,
                          const int32_t* beg, const int32_t* end, sphb_ctrl_t* ctrl, cudaStream_t s) {
   const bool f32 = p.precision == SPHB_FP32;  // the same build choice as launch_interact
-  if (ws->pi_kernel == SPHB_PI_PAIRED && f32) return pi512p::plan_interact(ws, p, g, beg, end, ctrl, s);
+  if (ws->pi_kernel == SPHB_PI_PAIRED && f32) return pi512p::plan_interact(ws, p, g, beg, end, ctrl, s, ws->cand_acc);
   if (ws->pi_kernel == SPHB_PI_SYMMETRIC && f32 && p.order == 0)
-    return pi384s::plan_interact(ws, p, g, beg, end, ctrl, s);
-  if (ws->pi_block == 256 && f32) return pi256::plan_interact(ws, p, g, beg, end, ctrl, s);
-  if (ws->pi_block == 512 && f32) return pi512::plan_interact(ws, p, g, beg, end, ctrl, s);
-  if (ws->pi_block == PI_LARGE_BLOCK && f32) return pi384::plan_interact(ws, p, g, beg, end, ctrl, s);
-  return pi128::plan_interact(ws, p, g, beg, end, ctrl, s);
+    return pi384s::plan_interact(ws, p, g, beg, end, ctrl, s, ws->cand_acc);
+  if (ws->pi_block == 256 && f32) return pi256::plan_interact(ws, p, g, beg, end, ctrl, s, ws->cand_acc);
+  if (ws->pi_block == 512 && f32) return pi512::plan_interact(ws, p, g, beg, end, ctrl, s, ws->cand_acc);
+  if (ws->pi_block == PI_LARGE_BLOCK && f32) return pi384::plan_interact(ws, p, g, beg, end, ctrl, s, ws->cand_acc);
+  return pi128::plan_interact(ws, p, g, beg, end, ctrl, s, ws->cand_acc);
 }
 
 int plan_interact_async(sphb_workspace* ws, const sphb_params_t& p, const sphb_grid_t& g,
@@ -188,6 +188,8 @@ int sphb_workspace_create(int64_t n_max, int64_t ncells_max, sphb_workspace_t** 
   if (e == cudaSuccess) e = alloc((void**)&ws->energy_part, sizeof(double) * 5 * 592);
   if (e == cudaSuccess) e = alloc((void**)&ws->sym_scratch, sizeof(unsigned long long));
   if (e == cudaSuccess) e = cudaMemset(ws->sym_scratch, 0, sizeof(unsigned long long));
+  if (e == cudaSuccess) e = alloc((void**)&ws->cand_acc, sizeof(unsigned long long));
+  if (e == cudaSuccess) e = cudaMemset(ws->cand_acc, 0, sizeof(unsigned long long));
   {
     const int64_t words = (n1 + MV_TILE_ROWS - 1) / MV_TILE_ROWS * (MV_TILE_ROWS / 32);
     ws->mover_cap_max = n1 < MOVER_CAP_MAX ? n1 : MOVER_CAP_MAX;
@@ -226,6 +228,7 @@ int sphb_workspace_destroy(sphb_workspace_t* ws) {
   if (!ws) return SPHB_OK;
   cudaFree(ws->cnt);
   cudaFree(ws->sym_scratch);
+  cudaFree(ws->cand_acc);
   cudaFree(ws->row_off);
   for (int k = 0; k < 2; ++k) {
     cudaFree(ws->keys_tmp[k]);
@@ -248,6 +251,9 @@ int sphb_workspace_destroy(sphb_workspace_t* ws) {
 
 int sphb_workspace_reset(sphb_workspace_t* ws, sphb_stream_t s) {
   SPHB_NONNULL(ws);
+  ws->plan.valid = false;  // a pending interaction plan is dropped, with its candidate count
+  if (ws->side) SPHB_CUDA(cudaStreamSynchronize(ws->side));
+  SPHB_CUDA(cudaMemsetAsync(ws->cand_acc, 0, sizeof(unsigned long long), (cudaStream_t)s));
   SPHB_CUDA(cudaMemsetAsync(ws->cnt, 0, sizeof(uint32_t) * (2 * ws->ncells_max + 1), (cudaStream_t)s));
   SPHB_CUDA(cudaMemsetAsync(ws->mv_state, 0, sizeof(uint32_t) * 8, (cudaStream_t)s));
   SPHB_CUDA(cudaMemsetAsync(ws->mv_head, 0xff, sizeof(int32_t) * (2 * ws->ncells_max + 1), (cudaStream_t)s));
@@ -767,7 +773,7 @@ int sphb_state_to_soa(int64_t r0, int64_t cnt, const void* posp, const void* vel
 int64_t sphb_step_launch_count(const sphb_grid_t* grid, int64_t n) {
   if (!grid) return 0;
   return 1 /*begin*/ + nl_launch_count(*grid, n) + interact_launch_count(n) + 1 /*integrate*/ +
-         1 /*end*/;  // (a symplectic step runs the middle three twice, plus k_stage_mid)
+         1 /*end*/ + (n >= PLAN_ASYNC_MIN_ROWS ? 1 : 0) /*k_cand_take after a side-stream plan*/;  // (a symplectic step runs the middle three twice, plus k_stage_mid)
 }
 
 }  // extern "C"

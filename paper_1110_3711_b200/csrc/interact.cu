@@ -543,9 +543,9 @@ __device__ __forceinline__ unsigned long long cell_cand(const sphb_grid_t& g, in
     }
   return (unsigned long long)((long long)max(nf, 0) * (F + B - 1) + (long long)max(nb, 0) * F);
 }
-__device__ __forceinline__ void add_cand(sphb_ctrl_t* ctrl, unsigned long long c) {
+__device__ __forceinline__ void add_cand(unsigned long long* acc, unsigned long long c) {
   c = warp_sum_u64(c);
-  if ((threadIdx.x & 31) == 0 && c) atomicAdd((unsigned long long*)&ctrl->counters[0], c);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(acc, c);
 }
 
 // Reach >= 2 (h/2 cells: 25 stencil rows per cell) the count pass's lanes would walk too many
@@ -555,7 +555,8 @@ constexpr int KC_THREADS = 256;
 __global__ void __launch_bounds__(KC_THREADS) k_cand_cells(sphb_grid_t g, int64_t ncells,
                                                           const int32_t* __restrict__ beg,
                                                           const int32_t* __restrict__ end,
-                                                          sphb_ctrl_t* ctrl) {
+                                                          const sphb_ctrl_t* ctrl,
+                                                          unsigned long long* cand_acc) {
   if (!step_live(ctrl)) return;
   const int ny = g.dims[1], nx = g.dims[0];
   const int span = g.tx1 - g.tx0;
@@ -576,8 +577,15 @@ __global__ void __launch_bounds__(KC_THREADS) k_cand_cells(sphb_grid_t g, int64_
   if (threadIdx.x < 32) {
     acc = threadIdx.x < KC_THREADS / 32 ? s_acc[threadIdx.x] : 0ull;
     acc = warp_sum_u64(acc);
-    if (threadIdx.x == 0 && acc) atomicAdd((unsigned long long*)&ctrl->counters[0], acc);
+    if (threadIdx.x == 0 && acc) atomicAdd(cand_acc, acc);
   }
+}
+
+// the side-stream plan's candidate count into the step counters (one thread)
+__global__ void k_cand_take(unsigned long long* cand_acc, sphb_ctrl_t* ctrl) {
+  const unsigned long long c = *cand_acc;
+  *cand_acc = 0ull;
+  if (c) atomicAdd((unsigned long long*)&ctrl->counters[0], c);
 }
 
 // Row blocks of one cell row r (records written at out when !COUNT); the record count, on
@@ -585,7 +593,7 @@ __global__ void __launch_bounds__(KC_THREADS) k_cand_cells(sphb_grid_t g, int64_
 template <bool COUNT>
 __device__ int row_records(const sphb_grid_t& g, int64_t ncells, const int32_t* __restrict__ beg,
                            const int32_t* __restrict__ end, int64_t r, int4* out, int maxc,
-                           int32_t* s_ends, int lane, sphb_ctrl_t* cand_ctrl) {
+                           int32_t* s_ends, int lane, unsigned long long* cand_ctrl) {
   const int nx = g.dims[0], span = g.tx1 - g.tx0;
   const int64_t cb = r * nx, cf = ncells + r * nx;  // row offsets in the B / F tables
   if (span <= 0 ||
@@ -650,9 +658,11 @@ __global__ void __launch_bounds__(32) k_blocks(sphb_grid_t g, int64_t ncells,
                                                const int32_t* __restrict__ end,
                                                int32_t* __restrict__ row_off,
                                                int4* __restrict__ blk, sphb_ctrl_t* ctrl,
-                                               int brick, int maxc, bool count_cand) {
-  // count pass of the FP32 gather builds: also the candidate counter (cell_cand)
-  sphb_ctrl_t* const cand_ctrl = (COUNT && count_cand) ? ctrl : nullptr;
+                                               int brick, int maxc,
+                                               unsigned long long* cand_acc) {
+  // count pass of the FP32 gather builds (reach 1): also the candidate counter (cell_cand),
+  // into the plan's accumulator (the interaction kernel moves it into the step counters)
+  unsigned long long* const cand_ctrl = COUNT ? cand_acc : nullptr;
   // one warp per cell row: the lanes stage the row's cumulative ends (both lists) in shared
   // memory, lane 0 makes the greedy cut
   extern __shared__ int32_t s_ends[];  // [span] fluid ends, then [span] boundary ends
@@ -2385,7 +2395,8 @@ static int launch_wall(const sphb_params_t& p, const sphb_grid_t& g, int64_t n, 
 // counter --, scan, write), on stream s (sphb_step / sphb_interact_plan run it on the workspace's
 // side stream, concurrently with K3).
 int plan_interact(sphb_workspace* ws, const sphb_params_t& p, const sphb_grid_t& g,
-                  const int32_t* beg, const int32_t* end, sphb_ctrl_t* ctrl, cudaStream_t s) {
+                  const int32_t* beg, const int32_t* end, sphb_ctrl_t* ctrl, cudaStream_t s,
+                  unsigned long long* cand_acc) {
   if (g.reach < 1 || g.reach > 3) return sphb_set_error(SPHB_E_INVALID, "reach must be 1..3");
   const int64_t ncells = ncells_of(g);
   const int64_t nrows = (int64_t)g.dims[1] * g.dims[2];
@@ -2423,16 +2434,18 @@ int plan_interact(sphb_workspace* ws, const sphb_params_t& p, const sphb_grid_t&
   // own kernel (reach >= 2)
   const bool cand = p.precision == SPHB_FP32 && !V8_SYM;
   const bool count_cand = cand && g.reach == 1;
-  k_blocks<true><<<gb, 32, sm_blocks, s>>>(g, ncells, beg, end, ws->row_off, ws->blocks, ctrl, brick, maxc, count_cand);
+  k_blocks<true><<<gb, 32, sm_blocks, s>>>(g, ncells, beg, end, ws->row_off, ws->blocks, ctrl, brick,
+                                           maxc, count_cand ? cand_acc : nullptr);
   if (int rc = sphb_check_launch("k_blocks count")) return rc;
   k_blocks_scan<<<1, KB_SCAN, 0, s>>>(ws->row_off, nunits, ctrl);
   if (int rc = sphb_check_launch("k_blocks_scan")) return rc;
-  k_blocks<false><<<gb, 32, sm_blocks, s>>>(g, ncells, beg, end, ws->row_off, ws->blocks, ctrl, brick, maxc, false);
+  k_blocks<false><<<gb, 32, sm_blocks, s>>>(g, ncells, beg, end, ws->row_off, ws->blocks, ctrl, brick,
+                                            maxc, nullptr);
   if (int rc = sphb_check_launch("k_blocks")) return rc;
   if (cand && !count_cand) {
     const int64_t ncand = (int64_t)(g.tx1 - g.tx0) * g.dims[1] * g.dims[2];
     const unsigned kc = (unsigned)std::max<int64_t>(1, std::min<int64_t>((ncand + KC_THREADS - 1) / KC_THREADS, 148 * 8));
-    k_cand_cells<<<kc, KC_THREADS, 0, s>>>(g, ncells, beg, end, ctrl);
+    k_cand_cells<<<kc, KC_THREADS, 0, s>>>(g, ncells, beg, end, ctrl, cand_acc);
     if (int rc = sphb_check_launch("k_cand_cells")) return rc;
   }
   return SPHB_OK;
@@ -2457,8 +2470,18 @@ int launch_interact(sphb_workspace* ws, const sphb_params_t& p, const sphb_grid_
   if (pending)
     if (cudaError_t e = cudaStreamWaitEvent(s, ws->ev_plan, 0))
       return sphb_set_error(SPHB_E_CUDA, "plan wait: %s", cudaGetErrorString(e));
-  if (!match)
-    if (int rc = plan_interact(ws, p, g, beg, end, ctrl, s)) return rc;
+  if (match) {  // the side-stream plan counted candidates into the workspace: take them
+    k_cand_take<<<1, 1, 0, s>>>(ws->cand_acc, ctrl);
+    if (int rc = sphb_check_launch("k_cand_take")) return rc;
+  } else {
+    if (pending)  // the discarded plan's candidate count
+      if (cudaError_t e = cudaMemsetAsync(ws->cand_acc, 0, sizeof(unsigned long long), s))
+        return sphb_set_error(SPHB_E_CUDA, "plan reset: %s", cudaGetErrorString(e));
+    // in line: straight into the step counters
+    if (int rc = plan_interact(ws, p, g, beg, end, ctrl, s,
+                               (unsigned long long*)&ctrl->counters[0]))
+      return rc;
+  }
   static int nsm = 0;
   if (nsm == 0) {
     int dev = 0;

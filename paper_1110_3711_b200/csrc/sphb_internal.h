@@ -47,6 +47,7 @@ struct sphb_workspace {
   // the interaction's block list built on a side stream while K3 reorders (sphb_interact_plan,
   // sphb_step): the next sphb_interact with the same tables and window waits on ev_plan
   // instead of building it again
+  unsigned long long* cand_acc = nullptr;  // the plan's candidate count until the kernel takes it
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_plan = nullptr;
   struct Plan {
@@ -89,7 +90,8 @@ constexpr int PI_LARGE_BLOCK = 384;
 #define SPHB_DECLARE_PI(NS)                                                                     \
   namespace NS {                                                                                \
   int plan_interact(sphb_workspace* ws, const sphb_params_t& p, const sphb_grid_t& g,         \
-                    const int32_t* beg, const int32_t* end, sphb_ctrl_t* ctrl, cudaStream_t s); \
+                    const int32_t* beg, const int32_t* end, sphb_ctrl_t* ctrl, cudaStream_t s,  \
+                    unsigned long long* cand_acc);                                            \
   int launch_interact(sphb_workspace* ws, const sphb_params_t& p, const sphb_grid_t& g,       \
                       int64_t n, int64_t nb, const float4* posp, const float4* velr,           \
                       const float4* aux, const int32_t* cell_sorted, const int32_t* beg,       \

@@ -933,7 +933,9 @@ class DeviceSlabSim:
         # k_cand_cells per launch at reach >= 2); pack, two band updates and the tail on a rank
         # with neighbours
         cand = npi if int(r.grid.reach) >= 2 else 0
-        return base + 2 + cand + 4 * (npi - 1) + (4 if r.sides else 0)
+        # (the slab stepper plans in line: no k_cand_take, which base counts from 2^19 rows)
+        take = 1 if r.n >= 1 << 19 else 0
+        return base - take + 2 + cand + 4 * (npi - 1) + (4 if r.sides else 0)
 
 
 def estimate_steps_per_sync() -> int:

@@ -571,6 +571,44 @@ def test_state_soa_round_trip():
     assert L.sphb_state_from_soa(-1, 1, *ptrs, 0, 0, 0, s) == _lib.SPHB_E_INVALID
 
 
+@pytest.mark.parametrize("variant", ["match", "mismatch"])
+def test_interact_plan_side_stream_equals_inline(monkeypatch, variant):
+    """The interaction's block list built on the workspace's side stream during K3
+    (sphb_interact_plan, taken by the next sphb_interact) gives the same steps as the list built
+    in line; a plan that does not match the call (the build changed in between) is waited for
+    and rebuilt."""
+    from paper_1110_3711_b200 import _lib
+    sc = sph.named_scenario("c2")  # >= 2^19 rows: the side-stream plan is active
+    prm = sph.make_params(sc)
+    system = sph.build_dam_break(sc, prm)
+    L = _lib.lib()
+    real = L.sphb_interact_plan
+    blk = 384 if variant == "match" else 256
+    out = []
+    for plan in (True, False):
+        sim = D.DeviceSim(system, prm, reach=1, record_capacity=16)
+        sim.set_pi_block(blk)
+        if not plan:
+            monkeypatch.setattr(L, "sphb_interact_plan", lambda *args: 0)
+        elif variant == "mismatch":  # planned for 384, then the 256-target build runs
+            def planned_other(*args, sim=sim):
+                sim.set_pi_block(384)
+                rc = real(*args)
+                sim.set_pi_block(256)
+                return rc
+            monkeypatch.setattr(L, "sphb_interact_plan", planned_other)
+        for _ in range(3):
+            sim.launch_step([torch.cuda.Event(enable_timing=True) for _ in range(4)])
+        torch.cuda.synchronize()
+        monkeypatch.setattr(L, "sphb_interact_plan", real)
+        recs = sim.records(0, 3)
+        out.append((sim.download(), recs["candidate_pairs"], recs["hits_ordered"]))
+    (a_state, a_cand, a_hits), (b_state, b_cand, b_hits) = out
+    assert np.array_equal(a_cand, b_cand) and np.array_equal(a_hits, b_hits)
+    for x, y in zip(a_state, b_state):
+        assert np.array_equal(x, y)
+
+
 @pytest.mark.parametrize("shuffle", [False, True])
 def test_upload_keep_order_equals_reset(shuffle):
     """A host round trip of the state (sphb_state_to_soa -> host -> sphb_state_from_soa) and
