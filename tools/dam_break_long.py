@@ -1,7 +1,7 @@
 """C3 dam break over a long run on one GPU: how the step cost evolves as the column collapses
 (cells fill unevenly, more rows change cell per step), with the energy diagnostics.
 
-  python tools/dam_break_long.py [c3] [out.json] [steps] [every] [128|384|auto|tuned]
+  python tools/dam_break_long.py [c3] [out.json] [steps] [every] [128|384|auto|tuned] [n_subdiv]
 
 ("tuned": run_simulation(pi_kernel="tuned")'s policy -- at every window start one step of each
 of DeviceSim.pi_candidates, the faster build runs the window.)
@@ -25,11 +25,12 @@ out = sys.argv[2] if len(sys.argv) > 2 else None
 steps = int(sys.argv[3]) if len(sys.argv) > 3 else 10000
 every = int(sys.argv[4]) if len(sys.argv) > 4 else 500
 blocking = sys.argv[5] if len(sys.argv) > 5 else "auto"
+n_subdiv = int(sys.argv[6]) if len(sys.argv) > 6 else 1
 t0 = time.time()
 sc = sph.named_scenario(name)
-prm = sph.make_params(sc)
+prm = sph.make_params(sc, n_subdiv=n_subdiv)
 system = sph.build_dam_break(sc, prm)
-sim = DeviceSim(system, prm, reach=1, record_capacity=steps + 8)
+sim = DeviceSim(system, prm, reach=n_subdiv, record_capacity=steps + 8)
 if blocking in ("auto", "tuned"):
     sim.set_pi_block(sph.sim.initial_pi_block(sim.n, prm.n_subdiv))
 else:
