@@ -964,6 +964,29 @@ def test_device_virtual_slabs_match_single_domain(nslabs, precision):
     assert oracle.rel_linf(rho[a], ref.rho[b]) <= tol
 
 
+def test_device_slabs_c2_fp32_counters_match_single_domain():
+    """C2 (1.14M particles) on three virtual X slabs in FP32: the ranks' windows are large
+    enough for the 384-target build's hybrid brick / row blocking and the count-pass
+    candidate counter, over edge and interior grids -- the first step's counters (candidates
+    from the cell tables, exact hits) and dt equal the single-domain step's."""
+    from paper_1110_3711_b200 import dslab
+    sc = sph.named_scenario("c2")
+    prm = sph.make_params(sc)
+    system = sph.build_dam_break(sc, prm)
+    sim = dslab.DeviceSlabSim(system, prm, dslab.DevLoopbackComm(3), precision=0)
+    sim.run(2)
+    got = sim.records(0, 2)
+    one = D.DeviceSim(system, prm, reach=1, record_capacity=8)
+    one.set_pi_block(384)
+    for _ in range(2):
+        one.launch_step()
+    torch.cuda.synchronize()
+    want = one.records(0, 2)
+    for k in ("candidate_pairs", "hits_ordered", "force_evals", "ff_force_evals"):
+        assert int(got[k][0]) == int(want[k][0]), k
+    assert got["dt"][0] == want["dt"][0]
+
+
 @pytest.mark.parametrize("nslabs,precision", [(1, 1), (2, 1), (3, 0), (4, 1)])
 def test_device_resident_slabs_match_single_domain(nslabs, precision):
     """The production multi-GPU stepper (dslab.DeviceSlabSim: device classify/scatter/unpack,
