@@ -191,7 +191,7 @@ def workload_config(cfg_name, sc, system, n_subdiv, world):
     n = system.n
     if world > 1:
         wl = f"{cfg_name}: {scenario_kind(sc)}, {n:,} particles over {world} GPUs (~{n // world:,} per GPU)"
-        par = f"{world} X-slabs (NCCL send/recv of migrants + halo rows)"
+        par = f"{world} X-slabs (edge bands with their forces written into the neighbours' memory -- CUDA IPC peer stores, NCCL send/recv fallback -- while the interior interacts)"
     else:
         wl = (f"{cfg_name}: {scenario_kind(sc)}, {n:,} particles per GPU "
               f"({system.count_fluid:,} fluid + {system.count_boundary:,} boundary)")
